@@ -1,0 +1,846 @@
+/* TEST INFRASTRUCTURE ONLY — see hsaw_oracle.h. Plain-C restatement of the reference hot path.
+ * Compiled with -ffp-contract=off so every FP64 operation rounds exactly as the reference's
+ * (g++ -O2 on x86-64: SSE2 doubles, no fused multiply-add). */
+#include "hsaw_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_INVALID_NODE 0xFFFFFFFFu /* kInvalidNode, proj/include/hsaw/types.hpp:12 */
+
+/* ------------------------------------------------------------------------------------------
+ * prng — proj/include/hsaw/prng.hpp
+ * ---------------------------------------------------------------------------------------- */
+
+/* splitmix_next, prng.hpp:29-38 */
+void orc_splitmix_next(uint64_t state, uint64_t* out_state, uint64_t* out_output) {
+    uint64_t z = state + 0x9E3779B97F4A7C15ULL;
+    uint64_t o = z;
+    o ^= o >> 30;
+    o *= 0xBF58476D1CE4E5B9ULL;
+    o ^= o >> 27;
+    o *= 0x94D049BB133111EBULL;
+    o ^= o >> 31;
+    *out_state = z;
+    *out_output = o;
+}
+
+/* prg_next (xorshift64*), prng.hpp:41-48 */
+uint64_t orc_prg_next(uint64_t* state) {
+    uint64_t x = *state;
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    *state = x;
+    return x * 0x2545F4914F6CDD1DULL;
+}
+
+/* u01, prng.hpp:51-53 */
+double orc_u01(uint64_t output) { return (double)(output >> 11) * 0x1.0p-53; }
+
+/* pick_uniform_node, prng.hpp:57-61 */
+uint32_t orc_pick_uniform_node(uint64_t* state, uint32_t n) {
+    double r = orc_u01(orc_prg_next(state));
+    uint32_t v = (uint32_t)(r * (double)n);
+    return v < n ? v : n - 1;
+}
+
+/* seed_from_worker, prng.hpp:65-72 */
+uint64_t orc_seed_from_worker(uint64_t worker_id) {
+    uint64_t st = worker_id;
+    for (;;) {
+        uint64_t ns, out;
+        orc_splitmix_next(st, &ns, &out);
+        if (out != 0) return out;
+        st = ns;
+    }
+}
+
+/* ------------------------------------------------------------------------------------------
+ * live-edge pick — proj/include/hsaw/graph.hpp:61-80
+ * ---------------------------------------------------------------------------------------- */
+
+static uint32_t ceil_log2_u64(uint64_t d) { /* d >= 1 */
+    return d <= 1 ? 0u : (uint32_t)(64 - __builtin_clzll(d - 1));
+}
+
+/* Algorithmic bytes of one pick (stated in DESIGN.md):
+ * d = 0: offsets pair (16); r >= total: + total read (24); success: + ceil(log2 d) probes of 8 B
+ * + in_src (4). The p_of read (8) is added by the caller when resolve() runs. */
+static uint64_t pick_bytes(uint64_t d, int success) {
+    if (d == 0) return 16;
+    if (!success) return 24;
+    return 28 + 8ull * ceil_log2_u64(d);
+}
+
+int orc_pick_live_in_edge(uint64_t* state, const orc_graph* g, uint32_t v, uint32_t* src,
+                          uint32_t* edge) {
+    double r = orc_u01(orc_prg_next(state)); /* exactly one draw, graph.hpp:63 */
+    uint64_t lo = g->in_offsets[v];
+    uint64_t hi = g->in_offsets[v + 1];
+    if (lo == hi || r >= g->in_cum[hi - 1]) return 0; /* graph.hpp:66 */
+    if (hi - lo <= 16) {                               /* graph.hpp:67-70 */
+        while (g->in_cum[lo] <= r) ++lo;
+    } else { /* first cumulative entry > r, graph.hpp:72-78 */
+        while (lo < hi) {
+            uint64_t mid = lo + (hi - lo) / 2;
+            if (g->in_cum[mid] > r)
+                hi = mid;
+            else
+                lo = mid + 1;
+        }
+    }
+    *src = g->in_src[lo];
+    *edge = (uint32_t)lo;
+    return 1;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * one walk attempt — proj/src/sampler.cpp:16-204
+ * ---------------------------------------------------------------------------------------- */
+
+typedef struct { /* WalkCursor, sampler.cpp:16-62 */
+    uint64_t s;
+    uint32_t node;
+    uint32_t edges;
+} cursor;
+
+/* WalkCursor::start with an empty domain, sampler.cpp:21-37 */
+static int cursor_start(cursor* c, const orc_graph* g, uint64_t* draws) {
+    c->node = orc_pick_uniform_node(&c->s, g->n);
+    ++*draws;
+    if (g->p_of[c->node] > 0.0) {
+        double r = orc_u01(orc_prg_next(&c->s));
+        ++*draws;
+        if (r <= g->p_of[c->node]) return 1; /* length-0 hit */
+    }
+    return 0;
+}
+
+/* WalkCursor::advance_edge, sampler.cpp:41-49. 0 stepped, 1 no edge, 2 length cap */
+static int cursor_advance(cursor* c, const orc_graph* g, uint32_t* u, uint32_t* e, uint64_t len_cap,
+                          uint64_t* draws, uint64_t* steps, uint64_t* bytes) {
+    if (c->edges >= len_cap) return 2;
+    uint64_t d = g->in_offsets[c->node + 1] - g->in_offsets[c->node];
+    int ok = orc_pick_live_in_edge(&c->s, g, c->node, u, e);
+    ++*draws;
+    ++*steps;
+    *bytes += pick_bytes(d, ok);
+    return ok ? 0 : 1;
+}
+
+/* WalkCursor::resolve, sampler.cpp:53-61 */
+static int cursor_resolve(cursor* c, const orc_graph* g, uint32_t u, uint64_t* draws,
+                          uint64_t* bytes) {
+    ++c->edges;
+    *bytes += 8; /* p_of[u] */
+    if (g->p_of[u] > 0.0) {
+        double r = orc_u01(orc_prg_next(&c->s));
+        ++*draws;
+        if (r <= g->p_of[u]) return 1;
+    }
+    c->node = u;
+    return 0;
+}
+
+typedef struct { /* WindowFilter, sampler.cpp:65-86 */
+    uint32_t ring[8];
+    uint32_t size, pos;
+} window_t;
+
+static void win_push(window_t* w, uint32_t u) {
+    if (w->size == 0) return;
+    w->ring[w->pos] = u;
+    w->pos = (w->pos + 1) % w->size;
+}
+static void win_reset(window_t* w, uint32_t width, uint32_t v0) {
+    w->size = width > 8 ? 8 : width;
+    for (uint32_t i = 0; i < w->size; ++i) w->ring[i] = ORC_INVALID_NODE;
+    w->pos = 0;
+    win_push(w, v0);
+}
+static int win_contains(const window_t* w, uint32_t u) {
+    for (uint32_t i = 0; i < w->size; ++i)
+        if (w->ring[i] == u) return 1;
+    return 0;
+}
+
+typedef struct { /* BrentState, sampler.cpp:90-109 */
+    uint32_t anchor, power, lam;
+} brent_t;
+
+static int brent_check(brent_t* b, uint32_t u) {
+    if (u == b->anchor) return 1;
+    if (++b->lam == b->power) {
+        b->anchor = u;
+        b->power <<= 1;
+        b->lam = 0;
+    }
+    return 0;
+}
+
+orc_attempt_result orc_attempt(const orc_graph* g, uint64_t* state, int heuristic, uint32_t window,
+                               uint64_t len_cap) {
+    orc_attempt_result res;
+    memset(&res, 0, sizeof res);
+    uint64_t snapshot = *state; /* sampler.cpp:155 */
+    cursor hare = {*state, ORC_INVALID_NODE, 0};
+    res.alg_bytes += 8; /* start-node p_of */
+    if (cursor_start(&hare, g, &res.draws)) { /* sampler.cpp:157-164 */
+        res.accepted = 1;
+        res.len = 0;
+        *state = hare.s;
+        return res;
+    }
+    window_t win;
+    win_reset(&win, window, hare.node); /* sampler.cpp:166-167 */
+    brent_t brent = {hare.node, 1, 0};  /* sampler.cpp:168-169, 95-99 */
+    /* FloydState, sampler.cpp:113-138: second cursor replaying the stream from the snapshot */
+    cursor tortoise = {snapshot, ORC_INVALID_NODE, 0};
+    uint64_t hare_pos = 0, scratch = 0;
+    if (heuristic == 1) (void)cursor_start(&tortoise, g, &scratch);
+
+    for (;;) { /* sampler.cpp:174-201 */
+        uint32_t u = ORC_INVALID_NODE, e = 0;
+        if (cursor_advance(&hare, g, &u, &e, len_cap, &res.draws, &res.steps, &res.alg_bytes) != 0)
+            break; /* no edge or length cap */
+        int cyc = win_contains(&win, u);
+        if (!cyc && heuristic == 0) cyc = brent_check(&brent, u);
+        if (!cyc && heuristic == 1) {
+            ++hare_pos;
+            if (hare_pos % 2 == 0) {
+                uint32_t tu = ORC_INVALID_NODE, te = 0;
+                (void)cursor_advance(&tortoise, g, &tu, &te, len_cap, &scratch, &scratch, &scratch);
+                (void)cursor_resolve(&tortoise, g, tu, &scratch, &scratch);
+                cyc = tortoise.node == u;
+            }
+        }
+        if (cyc) {
+            res.cycle_flagged = 1;
+            break;
+        }
+        if (cursor_resolve(&hare, g, u, &res.draws, &res.alg_bytes)) {
+            res.accepted = 1;
+            res.len = hare.edges;
+            break;
+        }
+        win_push(&win, u);
+    }
+    *state = hare.s; /* sampler.cpp:202 */
+    return res;
+}
+
+/* thread_sample, sampler.cpp:267-290 */
+uint32_t orc_thread_sample(const orc_graph* g, uint64_t worker_id, uint32_t l, const orc_cfg* cfg,
+                           uint64_t* seeds, uint32_t* lens, uint64_t* stats4) {
+    uint64_t s = orc_seed_from_worker(worker_id);
+    for (int i = 0; i < 8; ++i) (void)orc_prg_next(&s); /* burn-in */
+    uint32_t count = 0;
+    for (uint32_t i = 0; i < l; ++i) {
+        uint64_t snapshot = s;
+        orc_attempt_result r = orc_attempt(g, &s, cfg->heuristic, cfg->window, g->n);
+        if (stats4) {
+            stats4[0] += 1;
+            stats4[1] += r.draws;
+            stats4[2] += r.steps;
+            stats4[3] += r.alg_bytes;
+        }
+        if (r.accepted) {
+            seeds[count] = snapshot;
+            lens[count] = r.len;
+            ++count;
+        }
+    }
+    return count;
+}
+
+/* DecodeContext::decode_restricted with an empty domain, sampler.cpp:299-338 */
+int orc_decode(const orc_graph* g, uint64_t seed, uint32_t len, uint32_t* mark, uint32_t epoch,
+               uint32_t* nodes, uint32_t* edges) {
+    if (seed == 0) return -2;
+    cursor c = {seed, ORC_INVALID_NODE, 0};
+    uint64_t scratch = 0;
+    int start_hit = cursor_start(&c, g, &scratch);
+    uint32_t nn = 0;
+    nodes[nn++] = c.node;
+    if (start_hit) return len != 0 ? -2 : 1;
+    if (len == 0) return -2;
+    mark[c.node] = epoch;
+    for (;;) {
+        uint32_t u = ORC_INVALID_NODE, e = 0;
+        if (cursor_advance(&c, g, &u, &e, g->n, &scratch, &scratch, &scratch) != 0) return -2;
+        if (mark[u] == epoch) return 0; /* missed cycle */
+        int hit = cursor_resolve(&c, g, u, &scratch, &scratch);
+        nodes[nn++] = u;
+        edges[nn - 2] = e;
+        if (hit) return c.edges != len ? -2 : 1;
+        if (c.edges >= len) return -2;
+        mark[u] = epoch;
+    }
+}
+
+/* ------------------------------------------------------------------------------------------
+ * stream / pool — proj/src/sampler.cpp:383-501
+ * Batches are worker ids seed+0, seed+1, ...; samples are kept in (batch, seq) order and the pool
+ * is cut at the first whole-batch prefix reaching the target (:472-493). The reference's round
+ * sizing (:406-421) is "only a speed knob", so the restatement simply walks batch by batch.
+ * ---------------------------------------------------------------------------------------- */
+
+struct orc_pool {
+    uint64_t nsamples, attempts, total_edges;
+    uint64_t cap_samples, cap_items;
+    uint64_t* edge_off; /* nsamples+1 */
+    uint32_t* nodes;    /* total_edges + nsamples */
+    uint32_t* edges;    /* total_edges */
+    uint64_t* tag_worker;
+    uint32_t* tag_seq;
+    /* full stream bookkeeping for orc_interdict */
+    uint64_t nbatches, cap_batches;
+    uint64_t* accepted_after_batch;
+};
+
+static void pool_reserve(orc_pool* p, uint64_t more_samples, uint64_t more_items) {
+    if (p->nsamples + more_samples + 1 > p->cap_samples) {
+        uint64_t c = p->cap_samples ? p->cap_samples : 1024;
+        while (c < p->nsamples + more_samples + 1) c *= 2;
+        p->edge_off = realloc(p->edge_off, c * 8);
+        p->tag_worker = realloc(p->tag_worker, c * 8);
+        p->tag_seq = realloc(p->tag_seq, c * 4);
+        p->cap_samples = c;
+    }
+    uint64_t need = p->total_edges + p->nsamples + more_items + more_samples;
+    if (need > p->cap_items) {
+        uint64_t c = p->cap_items ? p->cap_items : 4096;
+        while (c < need) c *= 2;
+        p->nodes = realloc(p->nodes, c * 4);
+        p->edges = realloc(p->edges, c * 4);
+        p->cap_items = c;
+    }
+}
+
+typedef struct {
+    const orc_graph* g;
+    orc_cfg cfg;
+    uint64_t seed;
+    uint32_t* mark;
+    uint32_t epoch;
+    uint64_t* enc_seed;
+    uint32_t* enc_len;
+    uint32_t* tmp_nodes;
+    uint32_t* tmp_edges;
+    uint64_t tmp_cap;
+    orc_pool* pool;
+} stream_t;
+
+static int stream_init(stream_t* st, const orc_graph* g, uint64_t seed, const orc_cfg* cfg) {
+    memset(st, 0, sizeof *st);
+    st->g = g;
+    st->cfg = *cfg;
+    st->seed = seed;
+    st->mark = calloc(g->n ? g->n : 1, 4);
+    st->enc_seed = malloc(8ull * (cfg->batch_size ? cfg->batch_size : 1));
+    st->enc_len = malloc(4ull * (cfg->batch_size ? cfg->batch_size : 1));
+    st->pool = calloc(1, sizeof(orc_pool));
+    return 0;
+}
+
+static void stream_free(stream_t* st, int keep_pool) {
+    free(st->mark);
+    free(st->enc_seed);
+    free(st->enc_len);
+    free(st->tmp_nodes);
+    free(st->tmp_edges);
+    if (!keep_pool) orc_pool_free(st->pool);
+}
+
+/* one batch = thread_sample + immediate decode, sampler.cpp:430-439, merged :452-460 */
+static int stream_one_batch(stream_t* st) {
+    orc_pool* p = st->pool;
+    uint64_t wid = st->seed + p->nbatches;
+    uint32_t cnt = orc_thread_sample(st->g, wid, st->cfg.batch_size, &st->cfg, st->enc_seed,
+                                     st->enc_len, NULL);
+    for (uint32_t i = 0; i < cnt; ++i) {
+        uint64_t need = (uint64_t)st->enc_len[i] + 1;
+        if (need > st->tmp_cap) {
+            st->tmp_cap = need * 2;
+            st->tmp_nodes = realloc(st->tmp_nodes, st->tmp_cap * 4);
+            st->tmp_edges = realloc(st->tmp_edges, st->tmp_cap * 4);
+        }
+        if (++st->epoch == 0) { /* sampler.cpp:301-304 */
+            memset(st->mark, 0, 4ull * st->g->n);
+            st->epoch = 1;
+        }
+        int rc = orc_decode(st->g, st->enc_seed[i], st->enc_len[i], st->mark, st->epoch,
+                            st->tmp_nodes, st->tmp_edges);
+        if (rc < 0) return 2;
+        if (rc == 0) continue; /* dropped by the exact recheck */
+        uint32_t len = st->enc_len[i];
+        pool_reserve(p, 1, len);
+        uint64_t eo = p->total_edges, w = p->nsamples;
+        p->edge_off[w] = eo;
+        memcpy(p->nodes + eo + w, st->tmp_nodes, 4ull * (len + 1));
+        memcpy(p->edges + eo, st->tmp_edges, 4ull * len);
+        p->tag_worker[w] = wid;
+        p->tag_seq[w] = i; /* seq assigned before decode drops, sampler.cpp:283-284 */
+        p->total_edges += len;
+        p->nsamples += 1;
+        p->edge_off[p->nsamples] = p->total_edges;
+    }
+    if (p->nbatches + 1 > p->cap_batches) {
+        p->cap_batches = p->cap_batches ? p->cap_batches * 2 : 1024;
+        p->accepted_after_batch = realloc(p->accepted_after_batch, p->cap_batches * 8);
+    }
+    p->accepted_after_batch[p->nbatches++] = p->nsamples;
+    return 0;
+}
+
+/* SampleStream::ensure, sampler.cpp:388-463: grows until min_accepted samples exist; the attempt
+ * budget allows floor(max_attempts / batch_size) batches in total, then SamplingError (:396-404). */
+static int stream_ensure(stream_t* st, uint64_t min_accepted) {
+    orc_pool* p = st->pool;
+    pool_reserve(p, 0, 0);
+    if (p->nsamples == 0) p->edge_off[0] = 0;
+    while (p->nsamples < min_accepted) {
+        uint64_t attempts_so_far = p->nbatches * st->cfg.batch_size;
+        uint64_t budget_left =
+            st->cfg.max_attempts > attempts_so_far ? st->cfg.max_attempts - attempts_so_far : 0;
+        if (st->cfg.batch_size == 0 || budget_left / st->cfg.batch_size == 0) return 3;
+        int rc = stream_one_batch(st);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+/* counters_for, sampler.cpp:472-482 */
+static int stream_counters(const stream_t* st, uint64_t min_accepted, uint64_t* attempts,
+                           uint64_t* accepted) {
+    const orc_pool* p = st->pool;
+    if (min_accepted == 0) {
+        *attempts = 0;
+        *accepted = 0;
+        return 0;
+    }
+    for (uint64_t b = 0; b < p->nbatches; ++b) { /* lower_bound over the cumulative counts */
+        if (p->accepted_after_batch[b] >= min_accepted) {
+            *attempts = (b + 1) * st->cfg.batch_size;
+            *accepted = p->accepted_after_batch[b];
+            return 0;
+        }
+    }
+    return 4;
+}
+
+/* stream_samples = ensure + to_pool, sampler.cpp:484-501 */
+int orc_stream_samples(const orc_graph* g, uint64_t target, uint64_t seed, const orc_cfg* cfg,
+                       orc_pool** out) {
+    stream_t st;
+    stream_init(&st, g, seed, cfg);
+    int rc = stream_ensure(&st, target);
+    if (rc) {
+        stream_free(&st, 0);
+        return rc;
+    }
+    uint64_t attempts = 0, accepted = 0;
+    stream_counters(&st, target, &attempts, &accepted);
+    orc_pool* p = st.pool;
+    /* to_pool keeps all samples of the minimal whole-batch prefix; ensure() here never runs past
+     * that prefix, so accepted == nsamples. */
+    p->attempts = attempts;
+    p->nsamples = accepted;
+    p->total_edges = p->edge_off[accepted];
+    stream_free(&st, 1);
+    *out = p;
+    return 0;
+}
+
+void orc_pool_stats(const orc_pool* p, uint64_t* nsamples, uint64_t* attempts,
+                    uint64_t* total_edges) {
+    *nsamples = p->nsamples;
+    *attempts = p->attempts;
+    *total_edges = p->total_edges;
+}
+
+void orc_pool_copy(const orc_pool* p, uint64_t* edge_off, uint32_t* nodes, uint32_t* edges,
+                   uint64_t* tag_worker, uint32_t* tag_seq) {
+    memcpy(edge_off, p->edge_off, 8 * (p->nsamples + 1));
+    memcpy(nodes, p->nodes, 4 * (p->total_edges + p->nsamples));
+    memcpy(edges, p->edges, 4 * p->total_edges);
+    if (tag_worker) memcpy(tag_worker, p->tag_worker, 8 * p->nsamples);
+    if (tag_seq) memcpy(tag_seq, p->tag_seq, 4 * p->nsamples);
+}
+
+void orc_pool_free(orc_pool* p) {
+    if (!p) return;
+    free(p->edge_off);
+    free(p->nodes);
+    free(p->edges);
+    free(p->tag_worker);
+    free(p->tag_seq);
+    free(p->accepted_after_batch);
+    free(p);
+}
+
+/* ------------------------------------------------------------------------------------------
+ * coverage index + greedy — proj/src/coverage.cpp:13-166
+ * ---------------------------------------------------------------------------------------- */
+
+typedef struct {
+    uint32_t limit;
+    uint64_t nsets;
+    uint8_t* is_cand;    /* limit */
+    uint32_t* cands;     /* ascending candidate ids, coverage.cpp:55-57 */
+    uint64_t ncands;
+    uint64_t* by_off;    /* limit+1: item -> sample ids (CSR form of by_item_) */
+    uint32_t* by_sample; /* in insertion (sample id) order, like push_back at :33 */
+} cov_index;
+
+static void cov_free(cov_index* ix) {
+    free(ix->is_cand);
+    free(ix->cands);
+    free(ix->by_off);
+    free(ix->by_sample);
+}
+
+/* CoverageIndex raw item-set constructor, coverage.cpp:60-74 (candidate_mask :13-27).
+ * status 2 when a candidate id is out of range (:18-20). */
+static int cov_build(cov_index* ix, uint32_t limit, uint64_t nsets, const uint64_t* set_off,
+                     const uint32_t* items, const uint32_t* cand_ids, uint64_t ncand) {
+    memset(ix, 0, sizeof *ix);
+    ix->limit = limit;
+    ix->nsets = nsets;
+    ix->is_cand = calloc(limit ? limit : 1, 1);
+    if (cand_ids) {
+        for (uint64_t i = 0; i < ncand; ++i) {
+            if (cand_ids[i] >= limit) {
+                cov_free(ix);
+                return 2;
+            }
+            ix->is_cand[cand_ids[i]] = 1;
+        }
+    } else {
+        memset(ix->is_cand, 1, limit);
+    }
+    ix->by_off = calloc((uint64_t)limit + 2, 8);
+    for (uint64_t s = 0; s < nsets; ++s)
+        for (uint64_t j = set_off[s]; j < set_off[s + 1]; ++j)
+            if (items[j] < limit && ix->is_cand[items[j]]) ix->by_off[items[j] + 1]++;
+    for (uint64_t i = 0; i < limit; ++i) ix->by_off[i + 1] += ix->by_off[i];
+    ix->by_sample = malloc(4 * (ix->by_off[limit] ? ix->by_off[limit] : 1));
+    uint64_t* fill = malloc(8 * ((uint64_t)limit + 1));
+    memcpy(fill, ix->by_off, 8 * ((uint64_t)limit + 1));
+    for (uint64_t s = 0; s < nsets; ++s)
+        for (uint64_t j = set_off[s]; j < set_off[s + 1]; ++j)
+            if (items[j] < limit && ix->is_cand[items[j]])
+                ix->by_sample[fill[items[j]]++] = (uint32_t)s;
+    free(fill);
+    ix->cands = malloc(4 * ((uint64_t)limit ? limit : 1));
+    for (uint32_t i = 0; i < limit; ++i)
+        if (ix->is_cand[i]) ix->cands[ix->ncands++] = i;
+    return 0;
+}
+
+/* coverage_of, coverage.cpp:76-89 */
+static uint64_t cov_coverage_of(const cov_index* ix, const uint32_t* q, uint64_t nq) {
+    uint8_t* covered = calloc(ix->nsets ? ix->nsets : 1, 1);
+    uint64_t count = 0;
+    for (uint64_t i = 0; i < nq; ++i) {
+        uint32_t item = q[i];
+        if (item >= ix->limit) continue;
+        for (uint64_t j = ix->by_off[item]; j < ix->by_off[item + 1]; ++j) {
+            uint32_t sid = ix->by_sample[j];
+            if (!covered[sid]) {
+                covered[sid] = 1;
+                ++count;
+            }
+        }
+    }
+    free(covered);
+    return count;
+}
+
+/* greedy_max_cover_naive, coverage.cpp:140-166 */
+static void greedy_naive(const cov_index* ix, uint32_t k, uint32_t* solution, uint64_t* coverage) {
+    uint8_t* covered = calloc(ix->nsets ? ix->nsets : 1, 1);
+    uint8_t* selected = calloc((uint64_t)ix->limit + 1, 1);
+    uint64_t cov = 0;
+    for (uint32_t iter = 0; iter < k; ++iter) {
+        uint64_t best_gain = 0;
+        uint32_t best_item = ORC_INVALID_NODE;
+        for (uint64_t c = 0; c < ix->ncands; ++c) {
+            uint32_t item = ix->cands[c];
+            if (selected[item]) continue;
+            uint64_t gain = 0;
+            for (uint64_t j = ix->by_off[item]; j < ix->by_off[item + 1]; ++j)
+                if (!covered[ix->by_sample[j]]) ++gain;
+            if (best_item == ORC_INVALID_NODE || gain > best_gain) { /* first max wins, :155 */
+                best_gain = gain;
+                best_item = item;
+            }
+        }
+        solution[iter] = best_item;
+        selected[best_item] = 1;
+        cov += best_gain;
+        for (uint64_t j = ix->by_off[best_item]; j < ix->by_off[best_item + 1]; ++j)
+            covered[ix->by_sample[j]] = 1;
+    }
+    *coverage = cov;
+    free(covered);
+    free(selected);
+}
+
+/* greedy_max_cover (CELF), coverage.cpp:91-138: max-heap on (gain desc, item asc) with stamps */
+typedef struct {
+    uint64_t gain;
+    uint32_t item, stamp;
+} heap_entry;
+
+static int entry_worse(const heap_entry* a, const heap_entry* b) { /* Worse, :101-106 */
+    if (a->gain != b->gain) return a->gain < b->gain;
+    return a->item > b->item;
+}
+static void heap_push(heap_entry* h, uint64_t* n, heap_entry e) {
+    uint64_t i = (*n)++;
+    h[i] = e;
+    while (i > 0) {
+        uint64_t p = (i - 1) / 2;
+        if (!entry_worse(&h[p], &h[i])) break;
+        heap_entry t = h[p];
+        h[p] = h[i];
+        h[i] = t;
+        i = p;
+    }
+}
+static heap_entry heap_pop(heap_entry* h, uint64_t* n) {
+    heap_entry top = h[0];
+    h[0] = h[--(*n)];
+    uint64_t i = 0;
+    for (;;) {
+        uint64_t l = 2 * i + 1, r = l + 1, best = i;
+        if (l < *n && entry_worse(&h[best], &h[l])) best = l;
+        if (r < *n && entry_worse(&h[best], &h[r])) best = r;
+        if (best == i) break;
+        heap_entry t = h[best];
+        h[best] = h[i];
+        h[i] = t;
+        i = best;
+    }
+    return top;
+}
+
+static void greedy_lazy(const cov_index* ix, uint32_t k, uint32_t* solution, uint64_t* coverage) {
+    heap_entry* heap = malloc(sizeof(heap_entry) * (ix->ncands + (uint64_t)k + 1));
+    uint64_t hn = 0;
+    for (uint64_t c = 0; c < ix->ncands; ++c) {
+        uint32_t item = ix->cands[c];
+        heap_entry e = {ix->by_off[item + 1] - ix->by_off[item], item, 0};
+        heap_push(heap, &hn, e);
+    }
+    uint8_t* covered = calloc(ix->nsets ? ix->nsets : 1, 1);
+    uint8_t* selected = calloc((uint64_t)ix->limit + 1, 1);
+    uint64_t cov = 0;
+    for (uint32_t iter = 0; iter < k; ++iter) {
+        for (;;) {
+            heap_entry top = heap_pop(heap, &hn);
+            if (selected[top.item]) continue;
+            if (top.stamp != iter) {
+                uint64_t gain = 0;
+                for (uint64_t j = ix->by_off[top.item]; j < ix->by_off[top.item + 1]; ++j)
+                    if (!covered[ix->by_sample[j]]) ++gain;
+                heap_entry e = {gain, top.item, iter};
+                heap_push(heap, &hn, e);
+                continue;
+            }
+            solution[iter] = top.item;
+            selected[top.item] = 1;
+            cov += top.gain;
+            for (uint64_t j = ix->by_off[top.item]; j < ix->by_off[top.item + 1]; ++j)
+                covered[ix->by_sample[j]] = 1;
+            break;
+        }
+    }
+    *coverage = cov;
+    free(heap);
+    free(covered);
+    free(selected);
+}
+
+int orc_greedy(uint32_t limit, uint64_t nsets, const uint64_t* set_off, const uint32_t* items,
+               const uint32_t* cand_ids, uint64_t ncand, uint32_t k, int lazy, uint32_t* solution,
+               uint64_t* coverage) {
+    cov_index ix;
+    int rc = cov_build(&ix, limit, nsets, set_off, items, cand_ids, ncand);
+    if (rc) return rc;
+    if (k > ix.ncands) { /* coverage.cpp:93-94 / :142-143 */
+        cov_free(&ix);
+        return 1;
+    }
+    if (lazy)
+        greedy_lazy(&ix, k, solution, coverage);
+    else
+        greedy_naive(&ix, k, solution, coverage);
+    cov_free(&ix);
+    return 0;
+}
+
+int orc_coverage_of(uint32_t limit, uint64_t nsets, const uint64_t* set_off, const uint32_t* items,
+                    const uint32_t* cand_ids, uint64_t ncand, const uint32_t* query,
+                    uint64_t nquery, uint64_t* coverage) {
+    cov_index ix;
+    int rc = cov_build(&ix, limit, nsets, set_off, items, cand_ids, ncand);
+    if (rc) return rc;
+    *coverage = cov_coverage_of(&ix, query, nquery);
+    cov_free(&ix);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * schedule + check — proj/src/coverage.cpp:168-231
+ * ---------------------------------------------------------------------------------------- */
+
+/* ln_choose, coverage.cpp:168-173 */
+double orc_ln_choose(uint64_t M, uint64_t k) {
+    double s = 0.0;
+    for (uint64_t i = 1; i <= k; ++i) s += log((double)(M - k + i) / (double)i);
+    return s;
+}
+
+/* compute_schedule_m, coverage.cpp:179-204; lambda_samples :175-177 */
+int orc_schedule_m(uint64_t M, uint32_t k, double epsilon, double delta, orc_schedule* s) {
+    if (!(epsilon > 0.0) || epsilon >= 1.0) return 1;
+    if (!(delta > 0.0) || delta >= 1.0) return 1;
+    if (k < 1 || k > M) return 1;
+    s->epsilon = epsilon;
+    s->delta = delta;
+    s->k = k;
+    double c = (2.0 - 1.0 / exp(1.0)) * (2.0 - 1.0 / exp(1.0));
+    double a = 2.0 + 2.0 * epsilon / 3.0;
+    double eps2 = epsilon * epsilon;
+    s->n_max = c * a * (double)M * (log(6.0 / delta) + orc_ln_choose(M, k)) / ((double)k * eps2);
+    double lambda0 = a * log(3.0 / delta) / eps2;
+    double t = ceil(log2(2.0 * s->n_max / lambda0));
+    s->t_max = t < 1.0 ? 1 : (uint32_t)t;
+    s->lambda = a * log(3.0 * s->t_max / delta) / eps2;
+    s->lambda1 = 1.0 + (1.0 + epsilon) * a * log(3.0 * s->t_max / delta) / eps2;
+    s->lambda_samples = (uint64_t)ceil(s->lambda);
+    return 0;
+}
+
+/* check_solution, coverage.cpp:212-231 (coverage counts supplied by the caller) */
+int orc_check(double cov_r, double cov_rp, double n_rp, const orc_schedule* sched, uint32_t t,
+              double* eps_t_out) {
+    if (cov_rp < sched->lambda1) {
+        *eps_t_out = INFINITY;
+        return 0;
+    }
+    double eps = sched->epsilon;
+    double pow2 = ldexp(1.0, (int)t - 1);
+    double one_me = 1.0 - 1.0 / exp(1.0);
+    double eps1 = cov_r / cov_rp - 1.0;
+    double eps2 = eps * sqrt(n_rp * (1.0 + eps) / (pow2 * cov_rp));
+    double eps3 =
+        eps * sqrt(n_rp * (1.0 + eps) * (one_me - eps) / ((1.0 + eps / 3.0) * pow2 * cov_rp));
+    double eps_t = (eps1 + eps2 + eps1 * eps2) * (one_me - eps) + one_me * eps3;
+    *eps_t_out = eps_t;
+    return eps_t <= eps;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * interdiction — proj/src/interdiction.cpp:12-87
+ * ---------------------------------------------------------------------------------------- */
+
+/* item sets of samples [off, off+cnt): edge ids (kind 0, coverage.cpp:50) or all nodes incl.
+ * start and hit (kind 1, coverage.cpp:52), as CSR over a fresh copy. */
+static void slice_sets(const orc_pool* p, int kind, uint64_t off, uint64_t cnt, uint64_t** set_off,
+                       uint32_t** items) {
+    uint64_t* so = malloc(8 * (cnt + 1));
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < cnt; ++i) {
+        uint64_t w = off + i, len = p->edge_off[w + 1] - p->edge_off[w];
+        so[i] = total;
+        total += kind == 0 ? len : len + 1;
+    }
+    so[cnt] = total;
+    uint32_t* it = malloc(4 * (total ? total : 1));
+    for (uint64_t i = 0; i < cnt; ++i) {
+        uint64_t w = off + i, len = p->edge_off[w + 1] - p->edge_off[w];
+        if (kind == 0)
+            memcpy(it + so[i], p->edges + p->edge_off[w], 4 * len);
+        else
+            memcpy(it + so[i], p->nodes + p->edge_off[w] + w, 4 * (len + 1));
+    }
+    *set_off = so;
+    *items = it;
+}
+
+int orc_interdict(const orc_graph* g, int kind, const uint32_t* cand_ids, uint64_t ncand,
+                  uint32_t k, double eps, double delta, uint64_t seed, const orc_cfg* cfg,
+                  orc_result* out, uint32_t* solution) {
+    uint32_t limit = kind == 0 ? g->m : g->n;
+    /* CandidateSet::validate, proj/src/graph.cpp:432-443; k range, interdiction.cpp:17-18 */
+    uint64_t csize = cand_ids ? ncand : limit;
+    if (csize == 0) return 2;
+    if (cand_ids) {
+        uint8_t* seen = calloc(limit ? limit : 1, 1);
+        for (uint64_t i = 0; i < ncand; ++i) {
+            if (cand_ids[i] >= limit || seen[cand_ids[i]]) {
+                free(seen);
+                return 2;
+            }
+            seen[cand_ids[i]] = 1;
+        }
+        free(seen);
+    }
+    if (k < 1 || k > csize) return 1;
+    orc_schedule sched;
+    int rc = orc_schedule_m(limit, k, eps, delta, &sched); /* compute_schedule, :206-210 */
+    if (rc) return rc;
+    uint64_t lam = sched.lambda_samples;
+
+    stream_t st;
+    stream_init(&st, g, seed, cfg);
+    uint64_t size = 0, coverage = 0;
+    uint32_t t = 0;
+    int pass = 0;
+    for (;;) { /* interdiction.cpp:36-47 */
+        ++t;
+        size = lam << (t - 1);
+        rc = stream_ensure(&st, 2 * size);
+        if (rc) {
+            stream_free(&st, 0);
+            return rc;
+        }
+        uint64_t *off_r, *off_rp;
+        uint32_t *it_r, *it_rp;
+        slice_sets(st.pool, kind, 0, size, &off_r, &it_r);
+        slice_sets(st.pool, kind, size, size, &off_rp, &it_rp);
+        rc = orc_greedy(limit, size, off_r, it_r, cand_ids, ncand, k, 1, solution, &coverage);
+        uint64_t cov_r = 0, cov_rp = 0;
+        if (!rc) rc = orc_coverage_of(limit, size, off_r, it_r, cand_ids, ncand, solution, k, &cov_r);
+        if (!rc)
+            rc = orc_coverage_of(limit, size, off_rp, it_rp, cand_ids, ncand, solution, k, &cov_rp);
+        free(off_r);
+        free(it_r);
+        free(off_rp);
+        free(it_rp);
+        if (rc) {
+            stream_free(&st, 0);
+            return rc;
+        }
+        double eps_t;
+        pass = orc_check((double)cov_r, (double)cov_rp, (double)size, &sched, t, &eps_t);
+        if (pass || (double)size >= sched.n_max) break;
+    }
+    uint64_t attempts = 0, accepted = 0;
+    stream_counters(&st, 2 * size, &attempts, &accepted); /* interdiction.cpp:54-55 */
+    out->k = k;
+    out->iterations = t;
+    out->coverage = coverage;
+    out->samples_used = 2 * size;
+    out->attempts = attempts;
+    out->passed_check = pass;
+    double influence = (double)g->n * (double)accepted / (double)attempts; /* :57-59 */
+    out->est_suspension = influence * (double)coverage / (double)size;     /* :60-61 */
+    stream_free(&st, 0);
+    return 0;
+}

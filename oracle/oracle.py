@@ -1,0 +1,646 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes bindings for the two CPU checkers.
+
+* ``Port``  -> oracle/_build/libhsaw_oracle.so, the plain-C restatement (hsaw_oracle.c)
+* ``Ref``   -> oracle/_ref/libhsaw_ref.so, the unmodified reference behind ref_shim.cpp
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs import
+this module. The product package (paper_1702_05854_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_SO = os.path.join(HERE, "_build", "libhsaw_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libhsaw_ref.so")
+
+u64p = C.POINTER(C.c_uint64)
+u32p = C.POINTER(C.c_uint32)
+f64p = C.POINTER(C.c_double)
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def build(force: bool = False) -> None:
+    """Compile the C restatement (always possible) and the reference shim (only where
+    /root/reference exists). Building the checker is not using it."""
+    if force or not os.path.exists(PORT_SO) or os.path.getmtime(PORT_SO) < max(
+        os.path.getmtime(os.path.join(HERE, f)) for f in ("hsaw_oracle.c", "hsaw_oracle.h")
+    ):
+        subprocess.check_call(["make", "-s", "-C", HERE, "oracle"])
+    if os.path.isdir("/root/reference/proj/src") and (
+        force
+        or not os.path.exists(REF_SO)
+        or os.path.getmtime(REF_SO) < os.path.getmtime(os.path.join(HERE, "ref_shim.cpp"))
+    ):
+        subprocess.check_call(["make", "-s", "-C", HERE, "ref"])
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)
+
+
+@dataclass
+class Csr:
+    """ProbGraph + SuspectSet as flat arrays (proj/include/hsaw/graph.hpp:19-51,84-94)."""
+
+    n: int
+    m: int
+    in_offsets: np.ndarray  # u64[n+1]
+    in_src: np.ndarray  # u32[m]
+    in_cum: np.ndarray  # f64[m]
+    p_of: np.ndarray  # f64[n]
+
+    def __post_init__(self):
+        self.in_offsets = np.ascontiguousarray(self.in_offsets, dtype=np.uint64)
+        self.in_src = np.ascontiguousarray(self.in_src, dtype=np.uint32)
+        self.in_cum = np.ascontiguousarray(self.in_cum, dtype=np.float64)
+        self.p_of = np.ascontiguousarray(self.p_of, dtype=np.float64)
+        assert self.in_offsets.shape == (self.n + 1,)
+        assert self.in_src.shape == (self.m,) and self.in_cum.shape == (self.m,)
+        assert self.p_of.shape == (self.n,)
+
+
+@dataclass
+class PoolData:
+    attempts: int
+    edge_off: np.ndarray  # u64[ns+1]
+    nodes: np.ndarray  # u32[total_edges+ns]; walk w: nodes[edge_off[w]+w : edge_off[w+1]+w+1]
+    edges: np.ndarray  # u32[total_edges];    walk w: edges[edge_off[w] : edge_off[w+1]]
+    tag_worker: np.ndarray
+    tag_seq: np.ndarray
+
+    @property
+    def nsamples(self) -> int:
+        return len(self.edge_off) - 1
+
+    def walk_nodes(self, w: int) -> np.ndarray:
+        return self.nodes[int(self.edge_off[w]) + w : int(self.edge_off[w + 1]) + w + 1]
+
+    def walk_edges(self, w: int) -> np.ndarray:
+        return self.edges[int(self.edge_off[w]) : int(self.edge_off[w + 1])]
+
+    def item_sets(self, kind: int, off: int = 0, cnt: int | None = None):
+        """CSR item sets of walks [off, off+cnt): edges (kind 0) or nodes (kind 1)."""
+        cnt = self.nsamples - off if cnt is None else cnt
+        eo = self.edge_off[off : off + cnt + 1].astype(np.int64)
+        if kind == 0:
+            so = (eo - eo[0]).astype(np.uint64)
+            return so, self.edges[eo[0] : eo[-1]].copy()
+        idx = np.arange(cnt + 1, dtype=np.int64)
+        so = (eo - eo[0] + idx).astype(np.uint64)
+        return so, self.nodes[eo[0] + off : eo[-1] + off + cnt].copy()
+
+
+class _OrcGraph(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("m", C.c_uint32), ("in_offsets", u64p), ("in_src", u32p),
+                ("in_cum", f64p), ("p_of", f64p)]
+
+
+class _OrcCfg(C.Structure):
+    _fields_ = [("heuristic", C.c_int), ("window", C.c_uint32), ("batch_size", C.c_uint32),
+                ("max_attempts", C.c_uint64)]
+
+
+class _OrcSchedule(C.Structure):
+    _fields_ = [("epsilon", C.c_double), ("delta", C.c_double), ("lambda_", C.c_double),
+                ("lambda1", C.c_double), ("n_max", C.c_double), ("k", C.c_uint32),
+                ("t_max", C.c_uint32), ("lambda_samples", C.c_uint64)]
+
+
+class _OrcResult(C.Structure):
+    _fields_ = [("k", C.c_uint32), ("iterations", C.c_uint32), ("coverage", C.c_uint64),
+                ("samples_used", C.c_uint64), ("attempts", C.c_uint64),
+                ("est_suspension", C.c_double), ("passed_check", C.c_int)]
+
+
+class _RefResult(C.Structure):
+    _fields_ = [("k", C.c_uint32), ("iterations", C.c_uint32), ("coverage", C.c_uint64),
+                ("samples_used", C.c_uint64), ("attempts", C.c_uint64),
+                ("est_suspension", C.c_double), ("wall_time_s", C.c_double),
+                ("passed_check", C.c_int)]
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        super().__init__(f"status {status}: {msg}")
+        self.status = status
+
+
+def _sets(set_off, items):
+    set_off = np.ascontiguousarray(set_off, dtype=np.uint64)
+    items = np.ascontiguousarray(items, dtype=np.uint32)
+    if items.size == 0:
+        items = np.zeros(1, dtype=np.uint32)
+    return set_off, items
+
+
+def _cand(cand):
+    if cand is None:
+        return None, 0, 0
+    a = np.ascontiguousarray(cand, dtype=np.uint32)
+    if a.size == 0:
+        return np.zeros(1, dtype=np.uint32), 0, 1
+    return a, a.size, 1
+
+
+class Port:
+    """Plain-C restatement (kind = 'port')."""
+
+    kind = "port"
+
+    def __init__(self):
+        build()
+        L = self.L = C.CDLL(PORT_SO)
+        L.orc_prg_next.restype = C.c_uint64
+        L.orc_u01.restype = C.c_double
+        L.orc_u01.argtypes = [C.c_uint64]
+        L.orc_seed_from_worker.restype = C.c_uint64
+        L.orc_seed_from_worker.argtypes = [C.c_uint64]
+        L.orc_pick_uniform_node.restype = C.c_uint32
+        L.orc_splitmix_next.argtypes = [C.c_uint64, u64p, u64p]
+        L.orc_thread_sample.restype = C.c_uint32
+        L.orc_thread_sample.argtypes = [C.POINTER(_OrcGraph), C.c_uint64, C.c_uint32,
+                                        C.POINTER(_OrcCfg), u64p, u32p, u64p]
+        L.orc_decode.argtypes = [C.POINTER(_OrcGraph), C.c_uint64, C.c_uint32, u32p, C.c_uint32,
+                                 u32p, u32p]
+        L.orc_stream_samples.argtypes = [C.POINTER(_OrcGraph), C.c_uint64, C.c_uint64,
+                                         C.POINTER(_OrcCfg), C.POINTER(C.c_void_p)]
+        L.orc_pool_stats.argtypes = [C.c_void_p, u64p, u64p, u64p]
+        L.orc_pool_copy.argtypes = [C.c_void_p, u64p, u32p, u32p, u64p, u32p]
+        L.orc_pool_free.argtypes = [C.c_void_p]
+        L.orc_greedy.argtypes = [C.c_uint32, C.c_uint64, u64p, u32p, u32p, C.c_uint64, C.c_uint32,
+                                 C.c_int, u32p, u64p]
+        L.orc_coverage_of.argtypes = [C.c_uint32, C.c_uint64, u64p, u32p, u32p, C.c_uint64, u32p,
+                                      C.c_uint64, u64p]
+        L.orc_ln_choose.restype = C.c_double
+        L.orc_ln_choose.argtypes = [C.c_uint64, C.c_uint64]
+        L.orc_schedule_m.argtypes = [C.c_uint64, C.c_uint32, C.c_double, C.c_double,
+                                     C.POINTER(_OrcSchedule)]
+        L.orc_check.argtypes = [C.c_double, C.c_double, C.c_double, C.POINTER(_OrcSchedule),
+                                C.c_uint32, f64p]
+        L.orc_interdict.argtypes = [C.POINTER(_OrcGraph), C.c_int, u32p, C.c_uint64, C.c_uint32,
+                                    C.c_double, C.c_double, C.c_uint64, C.POINTER(_OrcCfg),
+                                    C.POINTER(_OrcResult), u32p]
+
+    # -- prng
+    def splitmix_next(self, state):
+        a, b = C.c_uint64(), C.c_uint64()
+        self.L.orc_splitmix_next(state, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def prg_next(self, state):
+        s = C.c_uint64(state)
+        out = self.L.orc_prg_next(C.byref(s))
+        return s.value, out
+
+    def u01(self, out):
+        return self.L.orc_u01(out)
+
+    def seed_from_worker(self, w):
+        return self.L.orc_seed_from_worker(w)
+
+    def pick_uniform_node(self, state, n):
+        s = C.c_uint64(state)
+        v = self.L.orc_pick_uniform_node(C.byref(s), C.c_uint32(n))
+        return s.value, v
+
+    # -- helpers
+    @staticmethod
+    def _g(csr: Csr):
+        return _OrcGraph(csr.n, csr.m, _p(csr.in_offsets, u64p), _p(csr.in_src, u32p),
+                         _p(csr.in_cum, f64p), _p(csr.p_of, f64p))
+
+    @staticmethod
+    def _cfg(heuristic=0, window=2, batch_size=10, max_attempts=100_000_000):
+        return _OrcCfg(heuristic, window, batch_size, max_attempts)
+
+    # -- sampler
+    def thread_sample(self, csr, worker_id, l, heuristic=0, window=2, want_stats=False):
+        g, cfg = self._g(csr), self._cfg(heuristic, window)
+        seeds = np.zeros(max(l, 1), dtype=np.uint64)
+        lens = np.zeros(max(l, 1), dtype=np.uint32)
+        stats = np.zeros(4, dtype=np.uint64)
+        cnt = self.L.orc_thread_sample(C.byref(g), worker_id, l, C.byref(cfg), _p(seeds, u64p),
+                                       _p(lens, u32p), _p(stats, u64p))
+        if want_stats:
+            return seeds[:cnt].copy(), lens[:cnt].copy(), stats
+        return seeds[:cnt].copy(), lens[:cnt].copy()
+
+    def decode(self, csr, seed, length):
+        g = self._g(csr)
+        mark = np.zeros(max(csr.n, 1), dtype=np.uint32)
+        nodes = np.zeros(length + 2, dtype=np.uint32)
+        edges = np.zeros(length + 1, dtype=np.uint32)
+        rc = self.L.orc_decode(C.byref(g), seed, length, _p(mark, u32p), 1, _p(nodes, u32p),
+                               _p(edges, u32p))
+        if rc < 0:
+            raise OracleError(-rc, "decode")
+        if rc == 0:
+            return None
+        return nodes[: length + 1].copy(), edges[:length].copy()
+
+    def stream_samples(self, csr, target, seed=0, workers=1, heuristic=0, window=2, batch_size=10,
+                       max_attempts=100_000_000) -> PoolData:
+        g, cfg = self._g(csr), self._cfg(heuristic, window, batch_size, max_attempts)
+        h = C.c_void_p()
+        rc = self.L.orc_stream_samples(C.byref(g), target, seed, C.byref(cfg), C.byref(h))
+        if rc:
+            raise OracleError(rc, "stream_samples")
+        try:
+            return _copy_pool(self.L.orc_pool_stats, self.L.orc_pool_copy, h)
+        finally:
+            self.L.orc_pool_free(h)
+
+    # -- coverage
+    def greedy(self, limit, set_off, items, k, cand=None, lazy=True, kind=0):
+        set_off, items = _sets(set_off, items)
+        ca, nc, _ = _cand(cand)
+        sol = np.zeros(max(k, 1), dtype=np.uint32)
+        cov = C.c_uint64()
+        rc = self.L.orc_greedy(limit, len(set_off) - 1, _p(set_off, u64p), _p(items, u32p),
+                               _p(ca, u32p), nc, k, int(lazy), _p(sol, u32p), C.byref(cov))
+        if rc:
+            raise OracleError(rc, "greedy")
+        return sol[:k].copy(), cov.value
+
+    def coverage_of(self, limit, set_off, items, query, cand=None, kind=0):
+        set_off, items = _sets(set_off, items)
+        ca, nc, _ = _cand(cand)
+        q = np.ascontiguousarray(query, dtype=np.uint32)
+        cov = C.c_uint64()
+        rc = self.L.orc_coverage_of(limit, len(set_off) - 1, _p(set_off, u64p), _p(items, u32p),
+                                    _p(ca, u32p), nc, _p(q, u32p), q.size, C.byref(cov))
+        if rc:
+            raise OracleError(rc, "coverage_of")
+        return cov.value
+
+    def ln_choose(self, M, k):
+        return self.L.orc_ln_choose(M, k)
+
+    def schedule(self, M, k, eps, delta):
+        s = _OrcSchedule()
+        rc = self.L.orc_schedule_m(M, k, eps, delta, C.byref(s))
+        if rc:
+            raise OracleError(rc, "schedule")
+        return dict(n_max=s.n_max, lambda_=s.lambda_, lambda1=s.lambda1, t_max=s.t_max,
+                    lambda_samples=s.lambda_samples)
+
+    def check(self, cov_r, cov_rp, n_rp, M, k, eps, delta, t):
+        s = _OrcSchedule()
+        rc = self.L.orc_schedule_m(M, k, eps, delta, C.byref(s))
+        if rc:
+            raise OracleError(rc, "schedule")
+        e = C.c_double()
+        ok = self.L.orc_check(float(cov_r), float(cov_rp), float(n_rp), C.byref(s), t, C.byref(e))
+        return bool(ok), e.value
+
+    def interdict(self, csr, kind, k, eps, delta, seed=0, cand=None, workers=1, batch_size=10,
+                  max_attempts=100_000_000):
+        g, cfg = self._g(csr), self._cfg(0, 2, batch_size, max_attempts)
+        ca, nc, has = _cand(cand)
+        res = _OrcResult()
+        sol = np.zeros(max(k, 1), dtype=np.uint32)
+        rc = self.L.orc_interdict(C.byref(g), kind, _p(ca, u32p) if has else None, nc, k, eps,
+                                  delta, seed, C.byref(cfg), C.byref(res), _p(sol, u32p))
+        if rc:
+            raise OracleError(rc, "interdict")
+        return dict(kind="edge" if kind == 0 else "node", k=res.k, epsilon=eps, delta=delta,
+                    solution=[int(x) for x in sol[:k]], est_suspension=res.est_suspension,
+                    coverage=res.coverage, samples_used=res.samples_used, attempts=res.attempts,
+                    iterations=res.iterations, passed_check=bool(res.passed_check))
+
+
+def _copy_pool(stats_fn, copy_fn, h) -> PoolData:
+    ns, at, te = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    stats_fn(h, C.byref(ns), C.byref(at), C.byref(te))
+    ns, at, te = ns.value, at.value, te.value
+    eo = np.zeros(ns + 1, dtype=np.uint64)
+    nodes = np.zeros(max(te + ns, 1), dtype=np.uint32)
+    edges = np.zeros(max(te, 1), dtype=np.uint32)
+    tw = np.zeros(max(ns, 1), dtype=np.uint64)
+    ts = np.zeros(max(ns, 1), dtype=np.uint32)
+    copy_fn(h, _p(eo, u64p), _p(nodes, u32p), _p(edges, u32p), _p(tw, u64p), _p(ts, u32p))
+    return PoolData(at, eo, nodes[: te + ns], edges[:te], tw[:ns], ts[:ns])
+
+
+class Ref:
+    """The unmodified reference library through ref_shim.cpp (kind = 'reference')."""
+
+    kind = "reference"
+
+    def __init__(self):
+        build()
+        if not have_ref():
+            raise FileNotFoundError(REF_SO)
+        L = self.L = C.CDLL(REF_SO)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_prg_next.restype = C.c_uint64
+        L.ref_u01.restype = C.c_double
+        L.ref_u01.argtypes = [C.c_uint64]
+        L.ref_seed_from_worker.restype = C.c_uint64
+        L.ref_seed_from_worker.argtypes = [C.c_uint64]
+        L.ref_pick_uniform_node.restype = C.c_uint32
+        L.ref_splitmix_next.argtypes = [C.c_uint64, u64p, u64p]
+        L.ref_graph_from_csr.restype = C.c_void_p
+        L.ref_graph_from_csr.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p]
+        L.ref_graph_build.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, f64p, C.c_int,
+                                      C.c_uint64, C.POINTER(C.c_void_p)]
+        L.ref_graph_load_edge_list.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int,
+                                               C.c_char_p, C.POINTER(C.c_void_p)]
+        L.ref_graph_synth.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.ref_graph_save_cache.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_graph_load_cache.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        L.ref_graph_save_edge_list.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_graph_validate.argtypes = [C.c_void_p]
+        L.ref_graph_dims.argtypes = [C.c_void_p, u32p, u32p]
+        L.ref_graph_copy.argtypes = [C.c_void_p, u64p, u32p, f64p, f64p, u32p]
+        L.ref_graph_free.argtypes = [C.c_void_p]
+        L.ref_suspects_from_p.argtypes = [C.c_void_p, f64p, C.POINTER(C.c_void_p)]
+        L.ref_suspects_random.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64,
+                                          C.POINTER(C.c_void_p)]
+        L.ref_suspects_load.argtypes = [C.c_char_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.ref_suspects_copy_p.argtypes = [C.c_void_p, f64p]
+        L.ref_suspects_size.restype = C.c_uint64
+        L.ref_suspects_size.argtypes = [C.c_void_p]
+        L.ref_suspects_free.argtypes = [C.c_void_p]
+        L.ref_thread_sample.restype = C.c_int64
+        L.ref_thread_sample.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_int,
+                                        C.c_uint32, u64p, u32p]
+        L.ref_decode.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, u32p, u32p]
+        L.ref_stream_samples.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64,
+                                         C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, C.c_uint64,
+                                         C.POINTER(C.c_void_p)]
+        L.ref_pool_stats.argtypes = [C.c_void_p, u64p, u64p, u64p]
+        L.ref_pool_copy.argtypes = [C.c_void_p, u64p, u32p, u32p, u64p, u32p]
+        L.ref_pool_free.argtypes = [C.c_void_p]
+        L.ref_greedy.argtypes = [C.c_int, C.c_uint32, C.c_uint64, u64p, u32p, u32p, C.c_uint64,
+                                 C.c_int, C.c_uint32, C.c_int, u32p, u64p]
+        L.ref_coverage_of.argtypes = [C.c_int, C.c_uint32, C.c_uint64, u64p, u32p, u32p,
+                                      C.c_uint64, C.c_int, u32p, C.c_uint64, u64p]
+        L.ref_schedule.argtypes = [C.c_uint64, C.c_uint32, C.c_double, C.c_double, f64p, u32p]
+        L.ref_ln_choose.restype = C.c_double
+        L.ref_ln_choose.argtypes = [C.c_uint64, C.c_uint64]
+        L.ref_check_solution.argtypes = [C.c_int, C.c_uint32, C.c_uint64, u64p, u32p, C.c_uint64,
+                                         u64p, u32p, u32p, C.c_uint64, C.c_int, u32p, C.c_uint64,
+                                         C.c_uint64, C.c_uint32, C.c_double, C.c_double,
+                                         C.c_uint32, C.POINTER(C.c_int), f64p]
+        L.ref_interdict.argtypes = [C.c_void_p, C.c_void_p, C.c_int, u32p, C.c_uint64, C.c_int,
+                                    C.c_uint32, C.c_double, C.c_double, C.c_uint32, C.c_uint64,
+                                    C.c_uint32, C.c_uint64, C.POINTER(_RefResult), u32p,
+                                    C.c_char_p, C.c_uint64]
+
+    def _chk(self, rc, what):
+        if rc:
+            raise OracleError(rc, f"{what}: {self.L.ref_last_error().decode()}")
+
+    # -- prng
+    def splitmix_next(self, state):
+        a, b = C.c_uint64(), C.c_uint64()
+        self.L.ref_splitmix_next(state, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def prg_next(self, state):
+        s = C.c_uint64(state)
+        out = self.L.ref_prg_next(C.byref(s))
+        return s.value, out
+
+    def u01(self, out):
+        return self.L.ref_u01(out)
+
+    def seed_from_worker(self, w):
+        return self.L.ref_seed_from_worker(w)
+
+    def pick_uniform_node(self, state, n):
+        s = C.c_uint64(state)
+        v = self.L.ref_pick_uniform_node(C.byref(s), C.c_uint32(n))
+        return s.value, v
+
+    # -- graph handles -> Csr
+    def _to_csr(self, gh, p_of=None) -> Csr:
+        n, m = C.c_uint32(), C.c_uint32()
+        self.L.ref_graph_dims(gh, C.byref(n), C.byref(m))
+        n, m = n.value, m.value
+        off = np.zeros(n + 1, dtype=np.uint64)
+        src = np.zeros(max(m, 1), dtype=np.uint32)
+        cum = np.zeros(max(m, 1), dtype=np.float64)
+        self.L.ref_graph_copy(gh, _p(off, u64p), _p(src, u32p), _p(cum, f64p), None, None)
+        return Csr(n, m, off, src[:m], cum[:m], np.zeros(n) if p_of is None else p_of)
+
+    def graph_extra(self, gh):
+        """(weight f64[m], edge_dst u32[m]) of a graph handle."""
+        n, m = C.c_uint32(), C.c_uint32()
+        self.L.ref_graph_dims(gh, C.byref(n), C.byref(m))
+        w = np.zeros(max(m.value, 1), dtype=np.float64)
+        d = np.zeros(max(m.value, 1), dtype=np.uint32)
+        self.L.ref_graph_copy(gh, None, None, None, _p(w, f64p), _p(d, u32p))
+        return w[: m.value], d[: m.value]
+
+    def build_graph(self, n, u, v, w=None, mode=1, seed=0):
+        u = np.ascontiguousarray(u, dtype=np.uint32)
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        wa = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+        h = C.c_void_p()
+        self._chk(self.L.ref_graph_build(n, u.size, _p(u, u32p), _p(v, u32p), _p(wa, f64p), mode,
+                                         seed, C.byref(h)), "build_graph")
+        return h
+
+    def load_edge_list(self, path, mode=1, seed=0, symmetrize=False, mapping_out=None):
+        h = C.c_void_p()
+        self._chk(self.L.ref_graph_load_edge_list(
+            path.encode(), mode, seed, int(symmetrize),
+            mapping_out.encode() if mapping_out else None, C.byref(h)), "load_edge_list")
+        return h
+
+    def synth_graph(self, n, density, seed):
+        h = C.c_void_p()
+        self._chk(self.L.ref_graph_synth(n, density, seed, C.byref(h)), "synth_graph")
+        return h
+
+    def graph_from_csr(self, csr: Csr):
+        return C.c_void_p(self.L.ref_graph_from_csr(csr.n, csr.m, _p(csr.in_offsets, u64p),
+                                                    _p(csr.in_src, u32p), _p(csr.in_cum, f64p)))
+
+    def save_cache(self, gh, path):
+        self._chk(self.L.ref_graph_save_cache(gh, path.encode()), "save_cache")
+
+    def load_cache(self, path):
+        h = C.c_void_p()
+        self._chk(self.L.ref_graph_load_cache(path.encode(), C.byref(h)), "load_cache")
+        return h
+
+    def save_edge_list(self, gh, path):
+        self._chk(self.L.ref_graph_save_edge_list(gh, path.encode()), "save_edge_list")
+
+    def validate(self, gh):
+        self._chk(self.L.ref_graph_validate(gh), "validate")
+
+    def graph_free(self, gh):
+        self.L.ref_graph_free(gh)
+
+    def random_suspects(self, gh, count, seed) -> np.ndarray:
+        h = C.c_void_p()
+        self._chk(self.L.ref_suspects_random(gh, count, seed, C.byref(h)), "random_suspects")
+        return self._p_of(gh, h)
+
+    def load_suspects(self, path, gh) -> np.ndarray:
+        h = C.c_void_p()
+        self._chk(self.L.ref_suspects_load(path.encode(), gh, C.byref(h)), "load_suspects")
+        return self._p_of(gh, h)
+
+    def _p_of(self, gh, vh):
+        n, m = C.c_uint32(), C.c_uint32()
+        self.L.ref_graph_dims(gh, C.byref(n), C.byref(m))
+        p = np.zeros(max(n.value, 1), dtype=np.float64)
+        self.L.ref_suspects_copy_p(vh, _p(p, f64p))
+        self.L.ref_suspects_free(vh)
+        return p[: n.value]
+
+    class _Handles:
+        def __init__(self, ref, csr):
+            self.ref = ref
+            self.g = ref.graph_from_csr(csr)
+            self.vi = C.c_void_p()
+            ref._chk(ref.L.ref_suspects_from_p(self.g, _p(csr.p_of, f64p), C.byref(self.vi)),
+                     "suspects")
+
+        def __enter__(self):
+            return self
+
+        def __exit__(self, *a):
+            self.ref.L.ref_suspects_free(self.vi)
+            self.ref.L.ref_graph_free(self.g)
+
+    def handles(self, csr: Csr):
+        return Ref._Handles(self, csr)
+
+    # -- sampler (same signatures as Port)
+    def thread_sample(self, csr, worker_id, l, heuristic=0, window=2, hd=None):
+        seeds = np.zeros(max(l, 1), dtype=np.uint64)
+        lens = np.zeros(max(l, 1), dtype=np.uint32)
+
+        def run(h):
+            cnt = self.L.ref_thread_sample(h.g, h.vi, worker_id, l, heuristic, window,
+                                           _p(seeds, u64p), _p(lens, u32p))
+            if cnt < 0:
+                raise OracleError(-cnt, "thread_sample")
+            return seeds[:cnt].copy(), lens[:cnt].copy()
+
+        if hd is not None:
+            return run(hd)
+        with self.handles(csr) as h:
+            return run(h)
+
+    def decode(self, csr, seed, length, hd=None):
+        nodes = np.zeros(length + 2, dtype=np.uint32)
+        edges = np.zeros(length + 1, dtype=np.uint32)
+
+        def run(h):
+            rc = self.L.ref_decode(h.g, h.vi, seed, length, _p(nodes, u32p), _p(edges, u32p))
+            if rc < 0:
+                raise OracleError(-rc, "decode: " + self.L.ref_last_error().decode())
+            return None if rc == 0 else (nodes[: length + 1].copy(), edges[:length].copy())
+
+        if hd is not None:
+            return run(hd)
+        with self.handles(csr) as h:
+            return run(h)
+
+    def stream_samples(self, csr, target, seed=0, workers=1, heuristic=0, window=2, batch_size=10,
+                       max_attempts=100_000_000, hd=None, copy=True):
+        def run(h):
+            ph = C.c_void_p()
+            self._chk(self.L.ref_stream_samples(h.g, h.vi, workers, target, seed, heuristic,
+                                                window, batch_size, max_attempts, C.byref(ph)),
+                      "stream_samples")
+            try:
+                if copy:
+                    return _copy_pool(self.L.ref_pool_stats, self.L.ref_pool_copy, ph)
+                ns, at, te = C.c_uint64(), C.c_uint64(), C.c_uint64()
+                self.L.ref_pool_stats(ph, C.byref(ns), C.byref(at), C.byref(te))
+                return ns.value, at.value, te.value
+            finally:
+                self.L.ref_pool_free(ph)
+
+        if hd is not None:
+            return run(hd)
+        with self.handles(csr) as h:
+            return run(h)
+
+    # -- coverage
+    def greedy(self, limit, set_off, items, k, cand=None, lazy=True, kind=0):
+        set_off, items = _sets(set_off, items)
+        ca, nc, has = _cand(cand)
+        sol = np.zeros(max(k, 1), dtype=np.uint32)
+        cov = C.c_uint64()
+        self._chk(self.L.ref_greedy(kind, limit, len(set_off) - 1, _p(set_off, u64p),
+                                    _p(items, u32p), _p(ca, u32p), nc, has, k, int(not lazy),
+                                    _p(sol, u32p), C.byref(cov)), "greedy")
+        return sol[:k].copy(), cov.value
+
+    def coverage_of(self, limit, set_off, items, query, cand=None, kind=0):
+        set_off, items = _sets(set_off, items)
+        ca, nc, has = _cand(cand)
+        q = np.ascontiguousarray(query, dtype=np.uint32)
+        cov = C.c_uint64()
+        self._chk(self.L.ref_coverage_of(kind, limit, len(set_off) - 1, _p(set_off, u64p),
+                                         _p(items, u32p), _p(ca, u32p), nc, has, _p(q, u32p),
+                                         q.size, C.byref(cov)), "coverage_of")
+        return cov.value
+
+    def ln_choose(self, M, k):
+        return self.L.ref_ln_choose(M, k)
+
+    def schedule(self, M, k, eps, delta):
+        out = np.zeros(4, dtype=np.float64)
+        t = C.c_uint32()
+        self._chk(self.L.ref_schedule(M, k, eps, delta, _p(out, f64p), C.byref(t)), "schedule")
+        return dict(n_max=out[0], lambda_=out[1], lambda1=out[2], t_max=t.value,
+                    lambda_samples=int(out[3]))
+
+    def check_solution(self, limit, sets_r, sets_rp, solution, M, k, eps, delta, t, cand=None,
+                       kind=0):
+        so_r, it_r = _sets(*sets_r)
+        so_p, it_p = _sets(*sets_rp)
+        ca, nc, has = _cand(cand)
+        sol = np.ascontiguousarray(solution, dtype=np.uint32)
+        ok, e = C.c_int(), C.c_double()
+        self._chk(self.L.ref_check_solution(kind, limit, len(so_r) - 1, _p(so_r, u64p),
+                                            _p(it_r, u32p), len(so_p) - 1, _p(so_p, u64p),
+                                            _p(it_p, u32p), _p(ca, u32p), nc, has, _p(sol, u32p),
+                                            sol.size, M, k, eps, delta, t, C.byref(ok),
+                                            C.byref(e)), "check_solution")
+        return bool(ok.value), e.value
+
+    def interdict(self, csr, kind, k, eps, delta, seed=0, cand=None, workers=1, batch_size=10,
+                  max_attempts=100_000_000, hd=None, want_json=False):
+        ca, nc, has = _cand(cand)
+        res = _RefResult()
+        sol = np.zeros(max(k, 1), dtype=np.uint32)
+        buf = C.create_string_buffer(1 << 16)
+
+        def run(h):
+            self._chk(self.L.ref_interdict(h.g, h.vi, kind, _p(ca, u32p), nc, has, k, eps, delta,
+                                           workers, seed, batch_size, max_attempts, C.byref(res),
+                                           _p(sol, u32p), buf, len(buf)), "interdict")
+
+        if hd is not None:
+            run(hd)
+        else:
+            with self.handles(csr) as h:
+                run(h)
+        out = dict(kind="edge" if kind == 0 else "node", k=res.k, epsilon=eps, delta=delta,
+                   solution=[int(x) for x in sol[:k]], est_suspension=res.est_suspension,
+                   coverage=res.coverage, samples_used=res.samples_used, attempts=res.attempts,
+                   iterations=res.iterations, passed_check=bool(res.passed_check))
+        if want_json:
+            out["json"] = buf.value.decode()
+            out["wall_time_s"] = res.wall_time_s
+        return out
