@@ -1,0 +1,181 @@
+/*
+ * hsaw_gpu.h — C-ABI of the B200-native HSAW sampling + greedy max-cover path.
+ *
+ * This is the drop-in boundary for the eSIA/nSIA hot path of arXiv 1702.05854 as implemented by
+ * the reference library in /root/reference/proj. The reference has no FFI layer of its own: the
+ * path sits behind plain C++ functions in namespace `hsaw`. Every entry point below names the
+ * reference interface (file:line, relative to /root/reference/) whose work it takes over; the C++
+ * host layer in paper_1702_05854_b200/host/ re-exposes the reference's own signatures on top of
+ * these calls (see INTEGRATION.md for the binding a maintainer would add).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; host arrays are borrowed for the duration of a call;
+ *     outputs are written to caller-allocated host buffers unless a parameter says "device".
+ *   - every function returns an hsaw_status; hsaw_gpu_last_error() gives the message.
+ *   - handles are single-owner and not thread-safe (like SampleStream/DecodeContext,
+ *     proj/include/hsaw/sampler.hpp:85-163).
+ *   - there is NO CPU fallback: without a CUDA device every call fails with HSAW_ECUDA.
+ *   - ids are uint32 (NodeId/EdgeId, proj/include/hsaw/types.hpp:9-10), so m < 2^32.
+ */
+#ifndef HSAW_GPU_H
+#define HSAW_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. 1..3 mirror the exception -> exit-code mapping of proj/src/cli.cpp:520-538 so the
+ * host layer can rethrow the matching exception type. */
+typedef enum hsaw_status {
+    HSAW_OK = 0,
+    HSAW_EINVAL = 1,  /* std::invalid_argument */
+    HSAW_EDATA = 2,   /* hsaw::DataError (proj/include/hsaw/types.hpp:21) */
+    HSAW_EBUDGET = 3, /* hsaw::SamplingError (types.hpp:26): attempt budget exhausted */
+    HSAW_ERANGE = 4,  /* std::out_of_range: prefix/counters beyond what is materialised */
+    HSAW_ECUDA = 5    /* CUDA runtime failure / no device */
+} hsaw_status;
+
+typedef struct hsaw_gpu_ctx hsaw_gpu_ctx;         /* one device + the uploaded graph */
+typedef struct hsaw_gpu_stream hsaw_gpu_stream;   /* SampleStream, device resident */
+typedef struct hsaw_gpu_walkset hsaw_gpu_walkset; /* fixed item sets (CoverageIndex input) */
+
+/* SamplerConfig, proj/include/hsaw/sampler.hpp:48-55. */
+typedef struct hsaw_sampler_cfg {
+    int32_t heuristic;     /* 0 Brent (default), 1 Floyd (not on device: HSAW_EINVAL), 2 None */
+    uint32_t window;       /* exact short-cycle window, 0..8 (default 2) */
+    uint32_t batch_size;   /* attempts chained per batch / worker id (default 10) */
+    uint64_t max_attempts; /* stream budget (default 100000000) */
+} hsaw_sampler_cfg;
+
+/* ItemKind, proj/include/hsaw/types.hpp:14. */
+enum { HSAW_KIND_EDGE = 0, HSAW_KIND_NODE = 1 };
+
+/* ---- context ------------------------------------------------------------------------------- */
+
+/* Binds a CUDA device. cuda_stream: a cudaStream_t the caller owns (e.g. a torch stream) or NULL
+ * to let the context create its own; all kernels of this context are launched on it. */
+int hsaw_gpu_ctx_create(int device, void* cuda_stream, hsaw_gpu_ctx** out);
+void hsaw_gpu_ctx_destroy(hsaw_gpu_ctx* ctx);
+const char* hsaw_gpu_last_error(const hsaw_gpu_ctx* ctx);
+/* The cudaStream_t kernels run on (for CUDA-event timing by the caller). */
+void* hsaw_gpu_ctx_cuda_stream(const hsaw_gpu_ctx* ctx);
+int hsaw_gpu_ctx_sync(hsaw_gpu_ctx* ctx);
+
+/* Replaces the host-resident ProbGraph + SuspectSet the reference sampler reads
+ * (proj/include/hsaw/graph.hpp:19-51 in_offsets/in_src/in_cum, :84-94 p_of). The arrays are the
+ * reference's own: in_offsets u64[n+1], in_src u32[m], in_cum f64[m] (per-row sequential FP64
+ * cumulative sums, proj/src/graph.cpp:158-192 — uploaded, never recomputed), p_of f64[n].
+ * They are re-laid out on the device into 32-byte node records and 16-byte edge records holding
+ * exact integer thresholds. HSAW_EDATA if a row's cumulative array decreases. */
+int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* in_offsets,
+                          const uint32_t* in_src, const double* in_cum, const double* p_of);
+/* Same, but p_of replaced later without re-uploading the CSR (new SuspectSet on the same graph). */
+int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of);
+/* Bytes of device memory held by the uploaded graph. */
+uint64_t hsaw_gpu_graph_bytes(const hsaw_gpu_ctx* ctx);
+
+/* ---- sampler: encode / decode (kernels K1, K2) ---------------------------------------------- */
+
+/* thread_sample for a range of batches (proj/src/sampler.cpp:267-290; worker ids
+ * first_worker_id + b, b in [0, nbatches)): out_count[b] accepted attempts of batch b, their
+ * (seed, len) in out_seed/out_len[b * batch_size + seq]. Bit-exact with the reference stream.
+ * stats (nullable) u64[8]: {attempts, draws, steps(picks), alg_bytes, accepted, 0, 0, 0}. */
+int hsaw_gpu_encode_batches(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg* cfg,
+                            uint64_t first_worker_id, uint64_t nbatches, uint64_t* out_seed,
+                            uint32_t* out_len, uint32_t* out_count, uint64_t* stats);
+
+/* DecodeContext::decode for an array of encoded walks (proj/src/sampler.cpp:295-338).
+ * edge_off u64[nwalks+1] must be the exclusive prefix sum of lens. Walk w gets nodes
+ * [edge_off[w]+w, edge_off[w+1]+w+1) and edges [edge_off[w], edge_off[w+1]).
+ * out_status[w]: 1 decoded, 0 dropped (revisit found by the exact recheck), 2 replay mismatch
+ * (the reference throws DataError, sampler.cpp:306-335). */
+int hsaw_gpu_decode_walks(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* seeds,
+                          const uint32_t* lens, const uint64_t* edge_off, uint32_t* out_nodes,
+                          uint32_t* out_edges, uint8_t* out_status);
+
+/* ---- sample stream (proj/src/sampler.cpp:383-501) ------------------------------------------- */
+
+/* SampleStream ctor. Batch b of the stream uses worker id seed + b (sampler.cpp:430). */
+int hsaw_gpu_stream_create(hsaw_gpu_ctx* ctx, uint64_t seed, const hsaw_sampler_cfg* cfg,
+                           hsaw_gpu_stream** out);
+void hsaw_gpu_stream_destroy(hsaw_gpu_stream* s);
+
+/* SampleStream::ensure (sampler.cpp:388-463): grow until >= min_accepted decoded samples exist.
+ * HSAW_EBUDGET once floor(max_attempts / batch_size) batches did not suffice. */
+int hsaw_gpu_stream_ensure(hsaw_gpu_stream* s, uint64_t min_accepted);
+
+/* Multi-GPU building block: sample exactly the global batches [first_batch, first_batch +
+ * nbatches) and append their decoded walks to this (rank-local) stream. Ranges must be issued in
+ * increasing order. accepted_in_range: decoded walks they produced. */
+int hsaw_gpu_stream_sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches,
+                                 uint64_t* accepted_in_range);
+
+/* accepted = decoded walks held, batches = batches run, total_edges = sum of their lengths. */
+int hsaw_gpu_stream_size(const hsaw_gpu_stream* s, uint64_t* accepted, uint64_t* batches,
+                         uint64_t* total_edges);
+
+/* SampleStream::counters_for (sampler.cpp:472-482): attempts/accepted of the minimal whole-batch
+ * prefix reaching min_accepted. HSAW_ERANGE if not materialised. */
+int hsaw_gpu_stream_counters(const hsaw_gpu_stream* s, uint64_t min_accepted, uint64_t* attempts,
+                             uint64_t* accepted);
+
+/* Rank-local variant for sharded streams: within the ranges this stream ran, the number of
+ * batches (counted from its first local batch) needed to hold min_local decoded walks and the
+ * decoded count at that batch. */
+int hsaw_gpu_stream_local_cut(const hsaw_gpu_stream* s, uint64_t min_local, uint64_t* nbatches,
+                              uint64_t* accepted);
+
+/* SampleStream::prefix / to_pool (sampler.cpp:465-493) copied to the host: walks
+ * [off, off + cnt). edge_off u64[cnt+1] (rebased to 0), nodes u32[E + cnt], edges u32[E] with
+ * E = total edges of the slice (hsaw_gpu_stream_slice_edges). tags nullable. */
+int hsaw_gpu_stream_slice_edges(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
+                                uint64_t* total_edges);
+int hsaw_gpu_stream_export(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
+                           uint64_t* edge_off, uint32_t* nodes, uint32_t* edges,
+                           uint64_t* tag_worker, uint32_t* tag_seq);
+
+/* Sampler work counters accumulated over the stream's life (u64[8], as in encode_batches; [5] =
+ * decode picks, [6] = walks dropped by the exact recheck). */
+int hsaw_gpu_stream_stats(const hsaw_gpu_stream* s, uint64_t* stats);
+
+/* ---- fixed walk sets (fixed-walk-set parity mode) ------------------------------------------- */
+
+/* Raw item sets, as the CoverageIndex item-set constructor takes them
+ * (proj/src/coverage.cpp:60-74): set i = items[set_off[i] .. set_off[i+1]). limit = id space
+ * (g.m for edges, g.n for nodes). */
+int hsaw_gpu_walkset_import(hsaw_gpu_ctx* ctx, uint32_t limit, uint64_t nsets,
+                            const uint64_t* set_off, const uint32_t* items,
+                            hsaw_gpu_walkset** out);
+void hsaw_gpu_walkset_destroy(hsaw_gpu_walkset* w);
+
+/* ---- greedy max-cover + coverage (kernels K3-K6) -------------------------------------------- */
+
+/* CoverageIndex(kind, samples[off, off+cnt), cand) + greedy_max_cover(idx, k)
+ * (proj/src/coverage.cpp:37-58, 91-138). Exactly one of stream / walkset is non-NULL; kind picks
+ * edge ids or all nodes of the stream's walks (coverage.cpp:49-53) and is ignored for walksets.
+ * cand_ids NULL = CandidateSet::all. solution u32[k] in selection order (ties and zero-gain
+ * slots -> smallest id, coverage.cpp:101-106,155); coverage = sum of marginal gains.
+ * HSAW_EINVAL if k exceeds the candidate count, HSAW_EDATA for a candidate id >= limit. */
+int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
+                    const hsaw_gpu_walkset* walkset, int kind, uint64_t off, uint64_t cnt,
+                    const uint32_t* cand_ids, uint64_t ncand, uint32_t k, uint32_t* solution,
+                    uint64_t* coverage);
+
+/* CoverageIndex::coverage_of (proj/src/coverage.cpp:76-89) on walks [off, off+cnt): number of
+ * distinct walks containing at least one of the candidate items in `items`. */
+int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
+                         const hsaw_gpu_walkset* walkset, int kind, uint64_t off, uint64_t cnt,
+                         const uint32_t* cand_ids, uint64_t ncand, const uint32_t* items,
+                         uint64_t nitems, uint64_t* coverage);
+
+/* ---- instrumentation ------------------------------------------------------------------------ */
+
+/* Number of kernel launches this context has issued since creation (bench.py "gpu_launches"). */
+uint64_t hsaw_gpu_launch_count(const hsaw_gpu_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSAW_GPU_H */

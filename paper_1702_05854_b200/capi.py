@@ -1,0 +1,362 @@
+"""ctypes binding of include/hsaw_gpu.h (plumbing for tests/ and bench.py — not the product).
+
+The product is the shared library; this module only marshals numpy arrays into its C-ABI. There is
+no fallback of any kind: a missing library or a missing CUDA device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _build
+
+u64p = C.POINTER(C.c_uint64)
+u32p = C.POINTER(C.c_uint32)
+u8p = C.POINTER(C.c_uint8)
+f64p = C.POINTER(C.c_double)
+
+HSAW_OK, HSAW_EINVAL, HSAW_EDATA, HSAW_EBUDGET, HSAW_ERANGE, HSAW_ECUDA = range(6)
+KIND_EDGE, KIND_NODE = 0, 1
+
+STAT_NAMES = ("attempts", "draws", "steps", "alg_bytes", "accepted", "decode_steps", "dropped",
+              "spare")
+
+
+class HsawError(RuntimeError):
+    """Mirrors the reference's exception -> exit-code mapping (proj/src/cli.cpp:520-538)."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"hsaw_gpu status {status}: {msg}")
+        self.status = status
+        self.msg = msg
+
+
+class SamplerCfg(C.Structure):
+    """hsaw_sampler_cfg == SamplerConfig (proj/include/hsaw/sampler.hpp:48-55)."""
+
+    _fields_ = [("heuristic", C.c_int32), ("window", C.c_uint32), ("batch_size", C.c_uint32),
+                ("max_attempts", C.c_uint64)]
+
+    def __init__(self, heuristic=0, window=2, batch_size=10, max_attempts=100_000_000):
+        super().__init__(heuristic, window, batch_size, max_attempts)
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    """Loads libhsaw_gpu.so from the package tree (never from site-packages, never rebuilt here)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(_build.GPU_SO):
+        raise ImportError(
+            f"{_build.GPU_SO} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(nvcc, sm_100a). There is no CPU fallback for this path.")
+    L = C.CDLL(_build.GPU_SO)
+    vp = C.c_void_p
+    L.hsaw_gpu_ctx_create.argtypes = [C.c_int, vp, C.POINTER(vp)]
+    L.hsaw_gpu_ctx_destroy.argtypes = [vp]
+    L.hsaw_gpu_ctx_destroy.restype = None
+    L.hsaw_gpu_last_error.argtypes = [vp]
+    L.hsaw_gpu_last_error.restype = C.c_char_p
+    L.hsaw_gpu_ctx_cuda_stream.argtypes = [vp]
+    L.hsaw_gpu_ctx_cuda_stream.restype = vp
+    L.hsaw_gpu_ctx_sync.argtypes = [vp]
+    L.hsaw_gpu_graph_upload.argtypes = [vp, C.c_uint32, C.c_uint32, u64p, u32p, f64p, f64p]
+    L.hsaw_gpu_suspects_upload.argtypes = [vp, f64p]
+    L.hsaw_gpu_graph_bytes.argtypes = [vp]
+    L.hsaw_gpu_graph_bytes.restype = C.c_uint64
+    L.hsaw_gpu_launch_count.argtypes = [vp]
+    L.hsaw_gpu_launch_count.restype = C.c_uint64
+    L.hsaw_gpu_encode_batches.argtypes = [vp, C.POINTER(SamplerCfg), C.c_uint64, C.c_uint64, u64p,
+                                          u32p, u32p, u64p]
+    L.hsaw_gpu_decode_walks.argtypes = [vp, C.c_uint64, u64p, u32p, u64p, u32p, u32p, u8p]
+    L.hsaw_gpu_stream_create.argtypes = [vp, C.c_uint64, C.POINTER(SamplerCfg), C.POINTER(vp)]
+    L.hsaw_gpu_stream_destroy.argtypes = [vp]
+    L.hsaw_gpu_stream_destroy.restype = None
+    L.hsaw_gpu_stream_ensure.argtypes = [vp, C.c_uint64]
+    L.hsaw_gpu_stream_sample_range.argtypes = [vp, C.c_uint64, C.c_uint64, u64p]
+    L.hsaw_gpu_stream_size.argtypes = [vp, u64p, u64p, u64p]
+    L.hsaw_gpu_stream_counters.argtypes = [vp, C.c_uint64, u64p, u64p]
+    L.hsaw_gpu_stream_local_cut.argtypes = [vp, C.c_uint64, u64p, u64p]
+    L.hsaw_gpu_stream_slice_edges.argtypes = [vp, C.c_uint64, C.c_uint64, u64p]
+    L.hsaw_gpu_stream_export.argtypes = [vp, C.c_uint64, C.c_uint64, u64p, u32p, u32p, u64p, u32p]
+    L.hsaw_gpu_stream_stats.argtypes = [vp, u64p]
+    L.hsaw_gpu_walkset_import.argtypes = [vp, C.c_uint32, C.c_uint64, u64p, u32p, C.POINTER(vp)]
+    L.hsaw_gpu_walkset_destroy.argtypes = [vp]
+    L.hsaw_gpu_walkset_destroy.restype = None
+    L.hsaw_gpu_greedy.argtypes = [vp, vp, vp, C.c_int, C.c_uint64, C.c_uint64, u32p, C.c_uint64,
+                                  C.c_uint32, u32p, u64p]
+    L.hsaw_gpu_coverage_of.argtypes = [vp, vp, vp, C.c_int, C.c_uint64, C.c_uint64, u32p,
+                                       C.c_uint64, u32p, C.c_uint64, u64p]
+    _LIB = L
+    return L
+
+
+# Every symbol include/hsaw_gpu.h declares (checked by the CPU test-suite against the built .so).
+EXPORTS = (
+    "hsaw_gpu_ctx_create", "hsaw_gpu_ctx_destroy", "hsaw_gpu_last_error",
+    "hsaw_gpu_ctx_cuda_stream", "hsaw_gpu_ctx_sync", "hsaw_gpu_graph_upload",
+    "hsaw_gpu_suspects_upload", "hsaw_gpu_graph_bytes", "hsaw_gpu_encode_batches",
+    "hsaw_gpu_decode_walks", "hsaw_gpu_stream_create", "hsaw_gpu_stream_destroy",
+    "hsaw_gpu_stream_ensure", "hsaw_gpu_stream_sample_range", "hsaw_gpu_stream_size",
+    "hsaw_gpu_stream_counters", "hsaw_gpu_stream_local_cut", "hsaw_gpu_stream_slice_edges",
+    "hsaw_gpu_stream_export", "hsaw_gpu_stream_stats", "hsaw_gpu_walkset_import",
+    "hsaw_gpu_walkset_destroy", "hsaw_gpu_greedy", "hsaw_gpu_coverage_of",
+    "hsaw_gpu_launch_count",
+)
+
+
+@dataclass
+class Pool:
+    """Host copy of a stream slice, same layout as the oracle's PoolData."""
+
+    attempts: int
+    edge_off: np.ndarray
+    nodes: np.ndarray
+    edges: np.ndarray
+    tag_worker: np.ndarray
+    tag_seq: np.ndarray
+
+    @property
+    def nsamples(self) -> int:
+        return len(self.edge_off) - 1
+
+    def walk_nodes(self, w):
+        return self.nodes[int(self.edge_off[w]) + w: int(self.edge_off[w + 1]) + w + 1]
+
+    def walk_edges(self, w):
+        return self.edges[int(self.edge_off[w]): int(self.edge_off[w + 1])]
+
+
+class Context:
+    """hsaw_gpu_ctx: one device + the uploaded graph."""
+
+    def __init__(self, device: int = 0, cuda_stream: int | None = None):
+        self.L = lib()
+        self.h = C.c_void_p()
+        rc = self.L.hsaw_gpu_ctx_create(device, C.c_void_p(cuda_stream) if cuda_stream else None,
+                                        C.byref(self.h))
+        if rc != HSAW_OK:
+            raise HsawError(rc, "hsaw_gpu_ctx_create failed: no usable CUDA device "
+                                "(this path has no CPU fallback)")
+        self.n = self.m = 0
+
+    def close(self):
+        if self.h:
+            self.L.hsaw_gpu_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _chk(self, rc):
+        if rc != HSAW_OK:
+            raise HsawError(rc, self.L.hsaw_gpu_last_error(self.h).decode())
+
+    def sync(self):
+        self._chk(self.L.hsaw_gpu_ctx_sync(self.h))
+
+    @property
+    def cuda_stream(self) -> int:
+        return int(self.L.hsaw_gpu_ctx_cuda_stream(self.h) or 0)
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.hsaw_gpu_launch_count(self.h))
+
+    @property
+    def graph_bytes(self) -> int:
+        return int(self.L.hsaw_gpu_graph_bytes(self.h))
+
+    def upload_graph(self, n, m, in_offsets, in_src, in_cum, p_of):
+        in_offsets = np.ascontiguousarray(in_offsets, dtype=np.uint64)
+        in_src = np.ascontiguousarray(in_src, dtype=np.uint32)
+        in_cum = np.ascontiguousarray(in_cum, dtype=np.float64)
+        p_of = np.ascontiguousarray(p_of, dtype=np.float64)
+        assert in_offsets.shape == (n + 1,) and in_src.shape == (m,) and in_cum.shape == (m,)
+        assert p_of.shape == (n,)
+        self._chk(self.L.hsaw_gpu_graph_upload(self.h, n, m, _p(in_offsets, u64p),
+                                               _p(in_src, u32p), _p(in_cum, f64p), _p(p_of, f64p)))
+        self.n, self.m = n, m
+
+    def upload_suspects(self, p_of):
+        p_of = np.ascontiguousarray(p_of, dtype=np.float64)
+        assert p_of.shape == (self.n,)
+        self._chk(self.L.hsaw_gpu_suspects_upload(self.h, _p(p_of, f64p)))
+
+    # ---- K1 / K2 parity entry points
+    def encode_batches(self, first_worker, nbatches, cfg: SamplerCfg | None = None):
+        cfg = cfg or SamplerCfg()
+        l = cfg.batch_size
+        seeds = np.zeros(max(nbatches * l, 1), dtype=np.uint64)
+        lens = np.zeros(max(nbatches * l, 1), dtype=np.uint32)
+        counts = np.zeros(max(nbatches, 1), dtype=np.uint32)
+        stats = np.zeros(8, dtype=np.uint64)
+        self._chk(self.L.hsaw_gpu_encode_batches(self.h, C.byref(cfg), first_worker, nbatches,
+                                                 _p(seeds, u64p), _p(lens, u32p), _p(counts, u32p),
+                                                 _p(stats, u64p)))
+        return (seeds[: nbatches * l].reshape(nbatches, l), lens[: nbatches * l].reshape(nbatches, l),
+                counts[:nbatches], dict(zip(STAT_NAMES, (int(x) for x in stats))))
+
+    def decode_walks(self, seeds, lens):
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        lens = np.ascontiguousarray(lens, dtype=np.uint32)
+        nw = seeds.size
+        eo = np.zeros(nw + 1, dtype=np.uint64)
+        np.cumsum(lens, out=eo[1:])
+        total = int(eo[-1])
+        nodes = np.zeros(max(total + nw, 1), dtype=np.uint32)
+        edges = np.zeros(max(total, 1), dtype=np.uint32)
+        status = np.zeros(max(nw, 1), dtype=np.uint8)
+        self._chk(self.L.hsaw_gpu_decode_walks(self.h, nw, _p(seeds, u64p), _p(lens, u32p),
+                                               _p(eo, u64p), _p(nodes, u32p), _p(edges, u32p),
+                                               _p(status, u8p)))
+        return eo, nodes[: total + nw], edges[:total], status[:nw]
+
+    def stream(self, seed=0, cfg: SamplerCfg | None = None) -> "Stream":
+        return Stream(self, seed, cfg or SamplerCfg())
+
+    def walkset(self, limit, set_off, items) -> "WalkSet":
+        return WalkSet(self, limit, set_off, items)
+
+    # ---- greedy / coverage
+    def greedy(self, k, *, stream=None, walkset=None, kind=KIND_EDGE, off=0, cnt=None, cand=None):
+        src = stream if stream is not None else walkset
+        cnt = src.count - off if cnt is None else cnt
+        ca = None if cand is None else np.ascontiguousarray(cand, dtype=np.uint32)
+        if ca is not None and ca.size == 0:
+            ca_ptr, nc = C.cast(C.c_void_p(1), u32p), 0  # explicit empty candidate set
+        else:
+            ca_ptr, nc = _p(ca, u32p), 0 if ca is None else ca.size
+        sol = np.zeros(max(k, 1), dtype=np.uint32)
+        cov = C.c_uint64()
+        self._chk(self.L.hsaw_gpu_greedy(self.h, stream.h if stream is not None else None,
+                                         walkset.h if walkset is not None else None, kind, off,
+                                         cnt, ca_ptr, nc, k, _p(sol, u32p), C.byref(cov)))
+        return sol[:k].copy(), cov.value
+
+    def coverage_of(self, items, *, stream=None, walkset=None, kind=KIND_EDGE, off=0, cnt=None,
+                    cand=None):
+        src = stream if stream is not None else walkset
+        cnt = src.count - off if cnt is None else cnt
+        ca = None if cand is None else np.ascontiguousarray(cand, dtype=np.uint32)
+        it = np.ascontiguousarray(items, dtype=np.uint32)
+        cov = C.c_uint64()
+        self._chk(self.L.hsaw_gpu_coverage_of(self.h, stream.h if stream is not None else None,
+                                              walkset.h if walkset is not None else None, kind,
+                                              off, cnt, _p(ca, u32p), 0 if ca is None else ca.size,
+                                              _p(it, u32p) if it.size else None, it.size,
+                                              C.byref(cov)))
+        return cov.value
+
+
+class Stream:
+    """hsaw_gpu_stream == SampleStream (proj/include/hsaw/sampler.hpp:133-163)."""
+
+    def __init__(self, ctx: Context, seed: int, cfg: SamplerCfg):
+        self.ctx, self.L, self.cfg, self.seed = ctx, ctx.L, cfg, seed
+        self.h = C.c_void_p()
+        ctx._chk(self.L.hsaw_gpu_stream_create(ctx.h, seed, C.byref(cfg), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            self.L.hsaw_gpu_stream_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def ensure(self, min_accepted):
+        self.ctx._chk(self.L.hsaw_gpu_stream_ensure(self.h, min_accepted))
+
+    def sample_range(self, first_batch, nbatches) -> int:
+        acc = C.c_uint64()
+        self.ctx._chk(self.L.hsaw_gpu_stream_sample_range(self.h, first_batch, nbatches,
+                                                          C.byref(acc)))
+        return acc.value
+
+    def size(self):
+        a, b, e = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.ctx._chk(self.L.hsaw_gpu_stream_size(self.h, C.byref(a), C.byref(b), C.byref(e)))
+        return a.value, b.value, e.value
+
+    @property
+    def count(self) -> int:
+        return self.size()[0]
+
+    def counters_for(self, min_accepted):
+        at, ac = C.c_uint64(), C.c_uint64()
+        self.ctx._chk(self.L.hsaw_gpu_stream_counters(self.h, min_accepted, C.byref(at),
+                                                      C.byref(ac)))
+        return at.value, ac.value
+
+    def local_cut(self, min_local):
+        nb, ac = C.c_uint64(), C.c_uint64()
+        self.ctx._chk(self.L.hsaw_gpu_stream_local_cut(self.h, min_local, C.byref(nb),
+                                                       C.byref(ac)))
+        return nb.value, ac.value
+
+    def stats(self) -> dict:
+        st = np.zeros(8, dtype=np.uint64)
+        self.ctx._chk(self.L.hsaw_gpu_stream_stats(self.h, _p(st, u64p)))
+        return dict(zip(STAT_NAMES, (int(x) for x in st)))
+
+    def export(self, off=0, cnt=None, attempts=0) -> Pool:
+        cnt = self.count - off if cnt is None else cnt
+        te = C.c_uint64()
+        self.ctx._chk(self.L.hsaw_gpu_stream_slice_edges(self.h, off, cnt, C.byref(te)))
+        te = te.value
+        eo = np.zeros(cnt + 1, dtype=np.uint64)
+        nodes = np.zeros(max(te + cnt, 1), dtype=np.uint32)
+        edges = np.zeros(max(te, 1), dtype=np.uint32)
+        tw = np.zeros(max(cnt, 1), dtype=np.uint64)
+        ts = np.zeros(max(cnt, 1), dtype=np.uint32)
+        self.ctx._chk(self.L.hsaw_gpu_stream_export(self.h, off, cnt, _p(eo, u64p),
+                                                    _p(nodes, u32p), _p(edges, u32p),
+                                                    _p(tw, u64p), _p(ts, u32p)))
+        return Pool(attempts, eo, nodes[: te + cnt], edges[:te], tw[:cnt], ts[:cnt])
+
+    def to_pool(self, min_accepted) -> Pool:
+        """SampleStream::to_pool (proj/src/sampler.cpp:484-493)."""
+        attempts, accepted = self.counters_for(min_accepted)
+        return self.export(0, accepted, attempts)
+
+
+class WalkSet:
+    """hsaw_gpu_walkset: raw item sets for the fixed-walk-set parity mode."""
+
+    def __init__(self, ctx: Context, limit, set_off, items):
+        self.ctx, self.L = ctx, ctx.L
+        set_off = np.ascontiguousarray(set_off, dtype=np.uint64)
+        items = np.ascontiguousarray(items, dtype=np.uint32)
+        self.count = set_off.size - 1
+        self.h = C.c_void_p()
+        ctx._chk(self.L.hsaw_gpu_walkset_import(ctx.h, limit, self.count, _p(set_off, u64p),
+                                                _p(items, u32p) if items.size else None,
+                                                C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            self.L.hsaw_gpu_walkset_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,167 @@
+// Shared host/device plumbing for libhsaw_gpu: error handling, device vectors, the context object
+// and the device-side graph layout. Product code — never includes anything from oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/hsaw_gpu.h"
+
+namespace hsawgpu {
+
+constexpr uint32_t kInvalidNode = 0xFFFFFFFFu;  // proj/include/hsaw/types.hpp:12
+constexpr unsigned kFullMask = 0xFFFFFFFFu;
+
+// ---- device-side graph layout ---------------------------------------------------
+// One 32-byte sector per node: everything a walk needs on arrival at the node (acceptance
+// threshold) and for the next live-edge pick (row start, degree, total-weight threshold, guess
+// scale). Thresholds are exact integer images of the reference's doubles: with k = draw >> 11,
+// u01 = k * 2^-53 (proj/include/hsaw/prng.hpp:51-53), so
+//   r >= c   <=>  k >= ceil(c * 2^53)          ("no edge", graph.hpp:66; "cum > r", :67-78)
+//   r <= p   <=>  k <  floor(p * 2^53) + 1      (acceptance, proj/src/sampler.cpp:34,57)
+struct __align__(32) NodeRec {
+    uint32_t lo;       // first in-edge slot (edge id of the row start); m < 2^32
+    uint32_t deg;      // in-degree
+    uint64_t tot_thr;  // ceil(in_cum[hi-1] * 2^53); 0 for an empty row
+    uint64_t acc_thr;  // 0 = not a suspect; else floor(p_of * 2^53) + 1
+    uint64_t scale;    // round(deg / total * 2^31): interpolation guess = (k * scale) >> 84
+};
+static_assert(sizeof(NodeRec) == 32, "node record must be one 32-byte sector");
+
+// One 16-byte record per in-edge, in CSR (edge id) order.
+struct __align__(16) EdgeRec {
+    uint64_t thr;      // ceil(in_cum[e] * 2^53): slot e is picked iff thr[e-1] <= k < thr[e]
+    uint32_t src;      // in_src[e]
+    uint32_t prev_hi;  // thr[e-1] >> 21 (0 for the first slot of a row): one-load verification
+};
+static_assert(sizeof(EdgeRec) == 16, "edge record must be 16 bytes");
+
+struct DeviceGraph {
+    uint32_t n = 0, m = 0;
+    NodeRec* nodes = nullptr;
+    EdgeRec* edges = nullptr;
+};
+
+// ---- errors ------------------------------------------------------------------------------------
+struct Error {
+    int status;
+    std::string msg;
+};
+
+#define HSAW_CUDA_CHECK(expr)                                                                  \
+    do {                                                                                       \
+        cudaError_t _e = (expr);                                                               \
+        if (_e != cudaSuccess)                                                                 \
+            throw ::hsawgpu::Error{HSAW_ECUDA, std::string(#expr) + ": " +                     \
+                                                   cudaGetErrorString(_e)};                    \
+    } while (0)
+
+[[noreturn]] inline void fail(int status, const std::string& msg) { throw Error{status, msg}; }
+
+// ---- device vector with amortised growth -------------------------------------------------------
+template <class T>
+struct DevVec {
+    T* p = nullptr;
+    uint64_t size = 0, cap = 0;
+
+    DevVec() = default;
+    DevVec(const DevVec&) = delete;
+    DevVec& operator=(const DevVec&) = delete;
+    ~DevVec() { release(); }
+
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        size = cap = 0;
+    }
+    // Grows capacity (x1.5 steps) preserving the first `size` elements.
+    void reserve(uint64_t want, cudaStream_t st) {
+        if (want <= cap) return;
+        uint64_t ncap = cap + cap / 2;
+        if (ncap < want) ncap = want;
+        if (ncap < 1024) ncap = 1024;
+        T* np = nullptr;
+        HSAW_CUDA_CHECK(cudaMalloc(&np, ncap * sizeof(T)));
+        if (p && size) {
+            cudaError_t e = cudaMemcpyAsync(np, p, size * sizeof(T), cudaMemcpyDeviceToDevice, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) {
+                cudaFree(np);
+                HSAW_CUDA_CHECK(e);
+            }
+        }
+        if (p) cudaFree(p);
+        p = np;
+        cap = ncap;
+    }
+    // Scratch use: capacity only, contents undefined.
+    void ensure_scratch(uint64_t want) {
+        if (want <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        uint64_t ncap = want + want / 4;
+        HSAW_CUDA_CHECK(cudaMalloc(&p, ncap * sizeof(T)));
+        cap = ncap;
+    }
+};
+
+}  // namespace hsawgpu
+
+// ---- the context (opaque to C callers) ---------------------------------------------------------
+struct hsaw_gpu_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    hsawgpu::DeviceGraph g;
+    uint64_t graph_bytes = 0;
+    uint64_t launches = 0;
+    std::string last_error;
+    // reusable scratch
+    hsawgpu::DevVec<unsigned char> cub_tmp;
+    hsawgpu::DevVec<uint32_t> chk_list, chk_counters;  // distinctness-check scratch
+    // greedy / coverage scratch (greedy.cu), reused across the doubling iterations
+    hsawgpu::DevVec<uint32_t> g_cand_bits, g_cnt, g_fill, g_inv, g_covered, g_solution, g_query_bits;
+    hsawgpu::DevVec<uint64_t> g_pos, g_partial, g_gains;
+    uint64_t* d_scalars = nullptr;  // 64 u64 of device scratch for counters / cursors
+    uint64_t* h_scalars = nullptr;  // pinned mirror
+};
+
+namespace hsawgpu {
+
+// Runs `f`, mapping exceptions to status codes and recording the message on the context.
+template <class F>
+int guarded(hsaw_gpu_ctx* ctx, F&& f) {
+    try {
+        if (ctx) HSAW_CUDA_CHECK(cudaSetDevice(ctx->device));
+        f();
+        return HSAW_OK;
+    } catch (const Error& e) {
+        if (ctx) ctx->last_error = e.msg;
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        if (ctx) ctx->last_error = "host allocation failed";
+        return HSAW_ECUDA;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->last_error = e.what();
+        return HSAW_ECUDA;
+    }
+}
+
+inline void check_launch(hsaw_gpu_ctx* ctx, const char* what) {
+    ++ctx->launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(HSAW_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// exclusive prefix sums (CUB) on the context stream; out may have a wider type than in
+void exclusive_sum_u32_to_u64(hsaw_gpu_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t count);
+void exclusive_sum_u32(hsaw_gpu_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t count);
+void exclusive_sum_u8_to_u32(hsaw_gpu_ctx* ctx, const uint8_t* in, uint32_t* out, uint64_t count);
+
+}  // namespace hsawgpu

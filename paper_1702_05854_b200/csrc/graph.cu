@@ -1,0 +1,292 @@
+// Context lifetime and graph upload: the reference's CSR arrays are copied to the device once and
+// re-laid out by two kernels into the node/edge records the walk kernels read.
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+
+using namespace hsawgpu;
+
+namespace {
+
+// ceil(c * 2^53) as an exact integer, saturated to 2^53 (any threshold >= 2^53 never excludes a
+// 53-bit draw). c * 2^53 is exact (power-of-two scaling); the conversion rounds toward +inf.
+__device__ __forceinline__ uint64_t ge_threshold(double c) {
+    if (!(c > 0.0)) return 0;  // also NaN
+    if (c >= 1.0) return 1ull << 53;
+    return __double2ull_ru(c * 0x1.0p53);
+}
+
+// floor(p * 2^53) + 1 for suspects (r <= p  <=>  k < floor(p*2^53)+1), 0 for non-suspects
+// (is_suspect is p > 0, proj/include/hsaw/graph.hpp:91).
+__device__ __forceinline__ uint64_t accept_threshold(double p) {
+    if (!(p > 0.0)) return 0;
+    if (p >= 1.0) return (1ull << 53) + 1;
+    return __double2ull_rd(p * 0x1.0p53) + 1;
+}
+
+__global__ void build_node_records(uint32_t n, const uint64_t* __restrict__ off,
+                                   const double* __restrict__ cum, const double* __restrict__ p_of,
+                                   NodeRec* __restrict__ out) {
+    uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    uint64_t lo = off[v], hi = off[v + 1];
+    NodeRec r;
+    r.lo = (uint32_t)lo;
+    r.deg = (uint32_t)(hi - lo);
+    r.tot_thr = 0;
+    r.scale = 0;
+    if (hi > lo) {
+        double total = cum[hi - 1];
+        r.tot_thr = ge_threshold(total);
+        double sc = total > 0.0 ? (double)r.deg / total * 2147483648.0 : 0.0;
+        r.scale = sc >= 1.8e19 ? ~0ull : (uint64_t)(sc + 0.5);
+    }
+    r.acc_thr = accept_threshold(p_of[v]);
+    out[v] = r;
+}
+
+__global__ void update_accept_thresholds(uint32_t n, const double* __restrict__ p_of,
+                                         NodeRec* __restrict__ out) {
+    uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    out[v].acc_thr = accept_threshold(p_of[v]);
+}
+
+// One thread per edge slot; row membership via edge_row (filled by mark_rows + scan would cost a
+// pass, so rows are walked by one warp each instead: lanes stride the row).
+__global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
+                                   const uint32_t* __restrict__ src, const double* __restrict__ cum,
+                                   EdgeRec* __restrict__ out, uint32_t* __restrict__ bad_row) {
+    uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t v = warp; v < n; v += nwarps) {
+        uint64_t lo = off[v], hi = off[v + 1];
+        for (uint64_t e = lo + lane; e < hi; e += 32) {
+            double c = cum[e];
+            EdgeRec r;
+            r.thr = ge_threshold(c);
+            r.src = src[e];
+            uint64_t prev = 0;
+            if (e > lo) {
+                double cp = cum[e - 1];
+                prev = ge_threshold(cp);
+                if (!(c >= cp)) atomicMin(bad_row, v);  // decreasing or NaN cumulative weights
+            }
+            uint64_t ph = prev >> 21;
+            r.prev_hi = ph > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ph;
+            out[e] = r;
+        }
+    }
+}
+
+void free_graph(hsaw_gpu_ctx* ctx) {
+    if (ctx->g.nodes) cudaFree(ctx->g.nodes);
+    if (ctx->g.edges) cudaFree(ctx->g.edges);
+    ctx->g = DeviceGraph{};
+    ctx->graph_bytes = 0;
+}
+
+}  // namespace
+
+namespace hsawgpu {
+
+template <class InIt, class OutT>
+static void exclusive_sum_impl(hsaw_gpu_ctx* ctx, InIt in, OutT* out, uint64_t count) {
+    if (count == 0) return;
+    size_t bytes = 0;
+    HSAW_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, count, ctx->stream));
+    ctx->cub_tmp.ensure_scratch(bytes ? bytes : 1);
+    HSAW_CUDA_CHECK(
+        cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, bytes, in, out, count, ctx->stream));
+    ++ctx->launches;
+}
+
+struct WidenU32 {
+    const uint32_t* p;
+    using value_type = uint64_t;
+    using difference_type = int64_t;
+    using pointer = const uint64_t*;
+    using reference = uint64_t;
+    using iterator_category = std::random_access_iterator_tag;
+    __host__ __device__ uint64_t operator[](int64_t i) const { return p[i]; }
+    __host__ __device__ uint64_t operator*() const { return *p; }
+    __host__ __device__ WidenU32 operator+(int64_t i) const { return WidenU32{p + i}; }
+};
+struct WidenU8 {
+    const uint8_t* p;
+    using value_type = uint32_t;
+    using difference_type = int64_t;
+    using pointer = const uint32_t*;
+    using reference = uint32_t;
+    using iterator_category = std::random_access_iterator_tag;
+    __host__ __device__ uint32_t operator[](int64_t i) const { return p[i]; }
+    __host__ __device__ uint32_t operator*() const { return *p; }
+    __host__ __device__ WidenU8 operator+(int64_t i) const { return WidenU8{p + i}; }
+};
+
+void exclusive_sum_u32_to_u64(hsaw_gpu_ctx* ctx, const uint32_t* in, uint64_t* out,
+                              uint64_t count) {
+    exclusive_sum_impl(ctx, WidenU32{in}, out, count);
+}
+void exclusive_sum_u32(hsaw_gpu_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t count) {
+    exclusive_sum_impl(ctx, in, out, count);
+}
+void exclusive_sum_u8_to_u32(hsaw_gpu_ctx* ctx, const uint8_t* in, uint32_t* out, uint64_t count) {
+    exclusive_sum_impl(ctx, WidenU8{in}, out, count);
+}
+
+}  // namespace hsawgpu
+
+extern "C" {
+
+int hsaw_gpu_ctx_create(int device, void* cuda_stream, hsaw_gpu_ctx** out) {
+    if (!out) return HSAW_EINVAL;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+        cudaGetLastError();
+        return HSAW_ECUDA;  // no CPU fallback: the path needs a CUDA device
+    }
+    auto* ctx = new hsaw_gpu_ctx;
+    ctx->device = device;
+    int rc = guarded(ctx, [&] {
+        cudaDeviceProp prop{};
+        HSAW_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        ctx->sm_count = prop.multiProcessorCount;
+        if (cuda_stream) {
+            ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+        } else {
+            HSAW_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            ctx->own_stream = true;
+        }
+        HSAW_CUDA_CHECK(cudaMalloc(&ctx->d_scalars, 64 * sizeof(uint64_t)));
+        HSAW_CUDA_CHECK(cudaMallocHost(&ctx->h_scalars, 64 * sizeof(uint64_t)));
+    });
+    if (rc != HSAW_OK) {
+        hsaw_gpu_ctx_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return HSAW_OK;
+}
+
+void hsaw_gpu_ctx_destroy(hsaw_gpu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    free_graph(ctx);
+    if (ctx->d_scalars) cudaFree(ctx->d_scalars);
+    if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
+    ctx->cub_tmp.release();
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* hsaw_gpu_last_error(const hsaw_gpu_ctx* ctx) {
+    return ctx ? ctx->last_error.c_str() : "no context (CUDA device unavailable?)";
+}
+
+void* hsaw_gpu_ctx_cuda_stream(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int hsaw_gpu_ctx_sync(hsaw_gpu_ctx* ctx) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] { HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+uint64_t hsaw_gpu_graph_bytes(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->graph_bytes : 0; }
+uint64_t hsaw_gpu_launch_count(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* in_offsets,
+                          const uint32_t* in_src, const double* in_cum, const double* p_of) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (n == 0) fail(HSAW_EDATA, "graph: no nodes");
+        if (!in_offsets || !p_of || (m && (!in_src || !in_cum)))
+            fail(HSAW_EINVAL, "graph_upload: null array");
+        if (in_offsets[0] != 0 || in_offsets[n] != m)
+            fail(HSAW_EDATA, "graph: offsets do not cover edge range");
+        for (uint32_t v = 0; v < n; ++v)
+            if (in_offsets[v + 1] < in_offsets[v]) fail(HSAW_EDATA, "graph: offsets not monotone");
+        for (uint32_t e = 0; e < m; ++e)
+            if (in_src[e] >= n) fail(HSAW_EDATA, "graph: source id out of range");
+        free_graph(ctx);
+        cudaStream_t st = ctx->stream;
+        uint64_t* d_off = nullptr;
+        uint32_t* d_src = nullptr;
+        double *d_cum = nullptr, *d_p = nullptr;
+        uint32_t* d_bad = nullptr;
+        auto cleanup = [&] {
+            cudaFree(d_off);
+            cudaFree(d_src);
+            cudaFree(d_cum);
+            cudaFree(d_p);
+            cudaFree(d_bad);
+        };
+        try {
+            HSAW_CUDA_CHECK(cudaMalloc(&ctx->g.nodes, (uint64_t)n * sizeof(NodeRec)));
+            HSAW_CUDA_CHECK(
+                cudaMalloc(&ctx->g.edges, (uint64_t)(m ? m : 1) * sizeof(EdgeRec)));
+            HSAW_CUDA_CHECK(cudaMalloc(&d_off, ((uint64_t)n + 1) * 8));
+            HSAW_CUDA_CHECK(cudaMalloc(&d_src, (uint64_t)(m ? m : 1) * 4));
+            HSAW_CUDA_CHECK(cudaMalloc(&d_cum, (uint64_t)(m ? m : 1) * 8));
+            HSAW_CUDA_CHECK(cudaMalloc(&d_p, (uint64_t)n * 8));
+            HSAW_CUDA_CHECK(cudaMalloc(&d_bad, 4));
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(d_off, in_offsets, ((uint64_t)n + 1) * 8,
+                                            cudaMemcpyHostToDevice, st));
+            if (m) {
+                HSAW_CUDA_CHECK(
+                    cudaMemcpyAsync(d_src, in_src, (uint64_t)m * 4, cudaMemcpyHostToDevice, st));
+                HSAW_CUDA_CHECK(
+                    cudaMemcpyAsync(d_cum, in_cum, (uint64_t)m * 8, cudaMemcpyHostToDevice, st));
+            }
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_bad, 0xFF, 4, st));
+            build_node_records<<<(n + 255) / 256, 256, 0, st>>>(n, d_off, d_cum, d_p, ctx->g.nodes);
+            check_launch(ctx, "build_node_records");
+            if (m) {
+                int blocks = ctx->sm_count * 8;
+                build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, ctx->g.edges,
+                                                           d_bad);
+                check_launch(ctx, "build_edge_records");
+            }
+            uint32_t bad = 0;
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+            if (bad != 0xFFFFFFFFu)
+                fail(HSAW_EDATA, "graph: cumulative weights not increasing at node " +
+                                     std::to_string(bad));
+        } catch (...) {
+            cleanup();
+            free_graph(ctx);
+            throw;
+        }
+        cleanup();
+        ctx->g.n = n;
+        ctx->g.m = m;
+        ctx->graph_bytes = (uint64_t)n * sizeof(NodeRec) + (uint64_t)m * sizeof(EdgeRec);
+    });
+}
+
+int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (!ctx->g.nodes) fail(HSAW_EINVAL, "suspects_upload: no graph uploaded");
+        if (!p_of) fail(HSAW_EINVAL, "suspects_upload: null array");
+        uint32_t n = ctx->g.n;
+        double* d_p = nullptr;
+        HSAW_CUDA_CHECK(cudaMalloc(&d_p, (uint64_t)n * 8));
+        cudaError_t e =
+            cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, ctx->stream);
+        if (e == cudaSuccess) {
+            update_accept_thresholds<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, d_p,
+                                                                               ctx->g.nodes);
+            ++ctx->launches;
+            e = cudaStreamSynchronize(ctx->stream);
+        }
+        cudaFree(d_p);
+        HSAW_CUDA_CHECK(e);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,492 @@
+// Greedy max-cover on device-resident walks (kernels K3-K6):
+//   K3  item_histogram     marginal-gain counts = occurrences of each candidate item in R_t
+//   K3b scatter_inverted   item -> walks inverted index (counting sort: histogram, scan, scatter)
+//   K4  argmax_partial     per-block max of (count desc, id asc) keys
+//   K5  cover_winner       final argmax + mark the winner's walks covered + decrement the counts
+//                          of every other item in those walks
+//   K6  count_covered      CoverageIndex::coverage_of
+// Semantics follow proj/src/coverage.cpp:91-166: each round selects the candidate with the largest
+// number of still-uncovered walks containing it, ties to the smallest id; rounds whose best gain
+// is zero are padded with the smallest unselected candidate ids (host side).
+#include <algorithm>
+
+#include "common.cuh"
+#include "stream.cuh"
+
+using namespace hsawgpu;
+
+struct hsaw_gpu_walkset {
+    hsaw_gpu_ctx* ctx = nullptr;
+    uint32_t limit = 0;
+    uint64_t nsets = 0, nitems = 0;
+    DevVec<uint64_t> off;
+    DevVec<uint32_t> items;
+};
+
+namespace {
+
+// Walks [w0, w0 + cnt) of either source. Walk w occupies items[off[w] + add*w, off[w+1] + add*(w+1)).
+struct WalkView {
+    const uint64_t* off;
+    const uint32_t* items;
+    uint64_t w0, cnt;
+    uint32_t add;  // 1 for the node arrays of a stream (len + 1 nodes per walk), else 0
+    uint32_t limit;
+};
+
+__device__ __forceinline__ bool is_cand(const uint32_t* __restrict__ cand_bits, uint32_t item) {
+    return cand_bits == nullptr || ((cand_bits[item >> 5] >> (item & 31)) & 1u);
+}
+
+__global__ void set_bits(const uint32_t* __restrict__ ids, uint64_t n, uint32_t* __restrict__ bits) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicOr(&bits[ids[i] >> 5], 1u << (ids[i] & 31));
+}
+
+__global__ void clear_bits(const uint32_t* __restrict__ ids, uint64_t n,
+                           uint32_t* __restrict__ bits) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) bits[ids[i] >> 5] = 0;
+}
+
+// K3: flat, coalesced pass over the item range of the walks.
+__global__ void item_histogram(WalkView v, uint64_t p0, uint64_t p1,
+                               const uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ cnt) {
+    uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = p0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < p1; p += stride) {
+        uint32_t item = v.items[p];
+        if (item < v.limit && is_cand(cand_bits, item)) atomicAdd(&cnt[item], 1u);
+    }
+}
+
+// K3b: one warp per walk; slot order inside an item's list is irrelevant (set semantics).
+__global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ cand_bits,
+                                 const uint64_t* __restrict__ pos, uint32_t* __restrict__ fill,
+                                 uint32_t* __restrict__ inv) {
+    uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = warp; i < v.cnt; i += nwarps) {
+        uint64_t w = v.w0 + i;
+        uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
+        for (uint64_t p = b + lane; p < e; p += 32) {
+            uint32_t item = v.items[p];
+            if (item < v.limit && is_cand(cand_bits, item)) {
+                uint32_t slot = atomicAdd(&fill[item], 1u);
+                inv[pos[item] + slot] = (uint32_t)i;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t block_max_u64(uint64_t v, uint64_t* smem) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t other = __shfl_xor_sync(kFullMask, v, o);
+        v = other > v ? other : v;
+    }
+    uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) smem[wid] = v;
+    __syncthreads();
+    uint32_t nw = blockDim.x >> 5;
+    v = threadIdx.x < nw ? smem[threadIdx.x] : 0;
+    if (wid == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t other = __shfl_xor_sync(kFullMask, v, o);
+            v = other > v ? other : v;
+        }
+        if (lane == 0) smem[0] = v;
+    }
+    __syncthreads();
+    v = smem[0];
+    __syncthreads();
+    return v;
+}
+
+// K4: key = count << 32 | ~id, so the max key is (largest count, smallest id); count 0 -> key 0.
+__global__ void __launch_bounds__(256) argmax_partial(const uint32_t* __restrict__ cnt,
+                                                      uint32_t limit,
+                                                      uint64_t* __restrict__ partial) {
+    __shared__ uint64_t smem[32];
+    uint64_t best = 0;
+    uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+    const uint32_t limit4 = limit & ~3u;
+    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < limit4;
+         i += stride) {
+        uint4 c = *reinterpret_cast<const uint4*>(cnt + i);
+        uint32_t id = (uint32_t)i;
+        uint64_t k0 = c.x ? ((uint64_t)c.x << 32) | (0xFFFFFFFFu - id) : 0;
+        uint64_t k1 = c.y ? ((uint64_t)c.y << 32) | (0xFFFFFFFFu - (id + 1)) : 0;
+        uint64_t k2 = c.z ? ((uint64_t)c.z << 32) | (0xFFFFFFFFu - (id + 2)) : 0;
+        uint64_t k3 = c.w ? ((uint64_t)c.w << 32) | (0xFFFFFFFFu - (id + 3)) : 0;
+        k0 = k1 > k0 ? k1 : k0;
+        k2 = k3 > k2 ? k3 : k2;
+        k0 = k2 > k0 ? k2 : k0;
+        best = k0 > best ? k0 : best;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (limit - limit4)) {
+        uint32_t id = limit4 + threadIdx.x;
+        uint32_t c = cnt[id];
+        uint64_t k = c ? ((uint64_t)c << 32) | (0xFFFFFFFFu - id) : 0;
+        best = k > best ? k : best;
+    }
+    best = block_max_u64(best, smem);
+    if (threadIdx.x == 0) partial[blockIdx.x] = best;
+}
+
+// K5: every block re-reduces the partial maxima (identical result), then the blocks share the
+// winner's inverted list: one warp per listed walk, claimed through an atomicOr on the covered
+// bitmap, decrementing the counts of the walk's candidate items.
+__global__ void __launch_bounds__(256) cover_winner(WalkView v, const uint64_t* __restrict__ partial,
+                                                    uint32_t npartial,
+                                                    const uint32_t* __restrict__ cand_bits,
+                                                    const uint64_t* __restrict__ pos,
+                                                    const uint32_t* __restrict__ inv,
+                                                    uint32_t* __restrict__ cnt,
+                                                    uint32_t* __restrict__ covered,
+                                                    uint32_t round, uint32_t* __restrict__ solution,
+                                                    uint64_t* __restrict__ gains) {
+    __shared__ uint64_t smem[32];
+    uint64_t best = 0;
+    for (uint32_t i = threadIdx.x; i < npartial; i += blockDim.x) {
+        uint64_t k = partial[i];
+        best = k > best ? k : best;
+    }
+    best = block_max_u64(best, smem);
+    uint32_t gain = (uint32_t)(best >> 32);
+    uint32_t item = 0xFFFFFFFFu - (uint32_t)best;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        solution[round] = gain ? item : 0xFFFFFFFFu;
+        gains[round] = gain;
+    }
+    if (gain == 0) return;
+    uint64_t lb = pos[item], le = pos[item + 1];
+    uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = lb + warp; i < le; i += nwarps) {
+        uint32_t lw = inv[i];
+        uint32_t old = 0;
+        if (lane == 0) old = atomicOr(&covered[lw >> 5], 1u << (lw & 31));
+        old = __shfl_sync(kFullMask, old, 0);
+        if (old & (1u << (lw & 31))) continue;  // already covered (earlier round or duplicate item)
+        uint64_t w = v.w0 + lw;
+        uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
+        for (uint64_t p = b + lane; p < e; p += 32) {
+            uint32_t it = v.items[p];
+            if (it < v.limit && is_cand(cand_bits, it)) atomicSub(&cnt[it], 1u);
+        }
+    }
+}
+
+// K6: one warp per walk; a walk counts once if any of its items is in the query bitmap.
+__global__ void __launch_bounds__(256) count_covered(WalkView v,
+                                                     const uint32_t* __restrict__ query_bits,
+                                                     unsigned long long* __restrict__ out) {
+    uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t mine = 0;
+    for (uint64_t i = warp; i < v.cnt; i += nwarps) {
+        uint64_t w = v.w0 + i;
+        uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
+        bool hit = false;
+        for (uint64_t p = b + lane; p < e && !hit; p += 32) {
+            uint32_t it = v.items[p];
+            hit = it < v.limit && ((query_bits[it >> 5] >> (it & 31)) & 1u);
+        }
+        if (__any_sync(kFullMask, hit) && lane == 0) ++mine;
+    }
+    if (lane == 0 && mine) atomicAdd(out, (unsigned long long)mine);
+}
+
+WalkView make_view(const hsaw_gpu_stream* s, const hsaw_gpu_walkset* ws, int kind, uint64_t off,
+                   uint64_t cnt) {
+    if ((s != nullptr) == (ws != nullptr))
+        fail(HSAW_EINVAL, "exactly one of stream / walkset must be given");
+    WalkView v{};
+    if (s) {
+        if (kind != HSAW_KIND_EDGE && kind != HSAW_KIND_NODE) fail(HSAW_EINVAL, "unknown item kind");
+        if (off + cnt > s->accepted)
+            fail(HSAW_ERANGE, "sample stream prefix not materialized");
+        v.off = s->edge_off.p;
+        v.items = kind == HSAW_KIND_EDGE ? s->edges.p : s->nodes.p;
+        v.add = kind == HSAW_KIND_EDGE ? 0u : 1u;
+        v.limit = kind == HSAW_KIND_EDGE ? s->ctx->g.m : s->ctx->g.n;
+    } else {
+        if (off + cnt > ws->nsets) fail(HSAW_ERANGE, "walk set range out of bounds");
+        v.off = ws->off.p;
+        v.items = ws->items.p;
+        v.add = 0;
+        v.limit = ws->limit;
+    }
+    v.w0 = off;
+    v.cnt = cnt;
+    return v;
+}
+
+// first/last item position of the view (two 8-byte reads)
+void view_span(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t* p0, uint64_t* p1) {
+    uint64_t a = 0, b = 0;
+    HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], v.off + v.w0, 8, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[1], v.off + v.w0 + v.cnt, 8,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    a = ctx->h_scalars[0];
+    b = ctx->h_scalars[1];
+    *p0 = a + (uint64_t)v.add * v.w0;
+    *p1 = b + (uint64_t)v.add * (v.w0 + v.cnt);
+}
+
+// Sorted, de-duplicated candidate ids (host) + device bitmap. Returns the candidate count.
+uint64_t prepare_candidates(hsaw_gpu_ctx* ctx, uint32_t limit, const uint32_t* cand_ids,
+                            uint64_t ncand, std::vector<uint32_t>& sorted,
+                            DevVec<uint32_t>& bits) {
+    if (!cand_ids) return limit;  // CandidateSet::all
+    sorted.assign(cand_ids, cand_ids + ncand);
+    for (uint32_t id : sorted)
+        if (id >= limit)  // candidate_mask, proj/src/coverage.cpp:18-20
+            fail(HSAW_EDATA, "candidate id out of range: " + std::to_string(id));
+    std::sort(sorted.begin(), sorted.end());
+    sorted.erase(std::unique(sorted.begin(), sorted.end()), sorted.end());
+    uint64_t words = ((uint64_t)limit + 31) / 32 + 1;
+    bits.ensure_scratch(words);
+    HSAW_CUDA_CHECK(cudaMemsetAsync(bits.p, 0, words * 4, ctx->stream));
+    if (!sorted.empty()) {
+        DevVec<uint32_t> d_ids;
+        d_ids.ensure_scratch(sorted.size());
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(d_ids.p, sorted.data(), sorted.size() * 4,
+                                        cudaMemcpyHostToDevice, ctx->stream));
+        set_bits<<<(unsigned)((sorted.size() + 255) / 256), 256, 0, ctx->stream>>>(
+            d_ids.p, sorted.size(), bits.p);
+        check_launch(ctx, "set_bits");
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    }
+    return sorted.size();
+}
+
+}  // namespace
+
+extern "C" {
+
+int hsaw_gpu_walkset_import(hsaw_gpu_ctx* ctx, uint32_t limit, uint64_t nsets,
+                            const uint64_t* set_off, const uint32_t* items,
+                            hsaw_gpu_walkset** out) {
+    if (!ctx || !out) return HSAW_EINVAL;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        if (!set_off) fail(HSAW_EINVAL, "walkset_import: null offsets");
+        if (nsets > 0xFFFFFFFFull) fail(HSAW_EINVAL, "walkset_import: more than 2^32 sets");
+        if (set_off[0] != 0) fail(HSAW_EINVAL, "walkset_import: offsets must start at 0");
+        for (uint64_t i = 0; i < nsets; ++i)
+            if (set_off[i + 1] < set_off[i]) fail(HSAW_EINVAL, "walkset_import: offsets decrease");
+        uint64_t nitems = set_off[nsets];
+        if (nitems && !items) fail(HSAW_EINVAL, "walkset_import: null items");
+        auto* w = new hsaw_gpu_walkset;
+        w->ctx = ctx;
+        w->limit = limit;
+        w->nsets = nsets;
+        w->nitems = nitems;
+        try {
+            w->off.ensure_scratch(nsets + 1);
+            w->items.ensure_scratch(nitems + 1);
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(w->off.p, set_off, (nsets + 1) * 8,
+                                            cudaMemcpyHostToDevice, ctx->stream));
+            if (nitems)
+                HSAW_CUDA_CHECK(cudaMemcpyAsync(w->items.p, items, nitems * 4,
+                                                cudaMemcpyHostToDevice, ctx->stream));
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            delete w;
+            throw;
+        }
+        *out = w;
+    });
+}
+
+void hsaw_gpu_walkset_destroy(hsaw_gpu_walkset* w) {
+    if (!w) return;
+    cudaSetDevice(w->ctx->device);
+    delete w;
+}
+
+int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
+                    const hsaw_gpu_walkset* walkset, int kind, uint64_t off, uint64_t cnt,
+                    const uint32_t* cand_ids, uint64_t ncand, uint32_t k, uint32_t* solution,
+                    uint64_t* coverage) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (!solution || !coverage) fail(HSAW_EINVAL, "greedy: null output");
+        WalkView v = make_view(stream, walkset, kind, off, cnt);
+        if (cnt > 0xFFFFFFFFull) fail(HSAW_EINVAL, "greedy: more than 2^32 walks");  // coverage.hpp:41
+        cudaStream_t st = ctx->stream;
+        const uint32_t limit = v.limit;
+        std::vector<uint32_t> cand_sorted;
+        DevVec<uint32_t>& cand_bits = ctx->g_cand_bits;
+        uint64_t ncands = prepare_candidates(ctx, limit, cand_ids, ncand, cand_sorted, cand_bits);
+        const uint32_t* d_cand = cand_ids ? cand_bits.p : nullptr;
+        if (k > ncands)  // proj/src/coverage.cpp:93-94
+            fail(HSAW_EINVAL, "budget k exceeds candidate count");
+        *coverage = 0;
+        if (k == 0) return;
+
+        // ---- K3: marginal-gain counts
+        DevVec<uint32_t>& d_cnt = ctx->g_cnt;
+        DevVec<uint32_t>& d_fill = ctx->g_fill;
+        DevVec<uint64_t>& d_pos = ctx->g_pos;
+        d_cnt.ensure_scratch((uint64_t)limit + 4);
+        d_fill.ensure_scratch((uint64_t)limit + 4);
+        d_pos.ensure_scratch((uint64_t)limit + 2);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
+        uint64_t p0 = 0, p1 = 0;
+        if (cnt) view_span(ctx, v, &p0, &p1);
+        const int wide = ctx->sm_count * 8;
+        if (p1 > p0) {
+            int hb = (int)std::min<uint64_t>((p1 - p0 + 255) / 256, (uint64_t)wide);
+            item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt.p);
+            check_launch(ctx, "item_histogram");
+        }
+        // ---- K3b: inverted index by counting sort
+        exclusive_sum_u32_to_u64(ctx, d_cnt.p, d_pos.p, (uint64_t)limit + 1);
+        uint64_t occurrences = 0;
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], d_pos.p + limit, 8,
+                                        cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        occurrences = ctx->h_scalars[0];
+        DevVec<uint32_t>& d_inv = ctx->g_inv;
+        d_inv.ensure_scratch(occurrences + 1);
+        if (occurrences) {
+            int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
+            scatter_inverted<<<sb, 256, 0, st>>>(v, d_cand, d_pos.p, d_fill.p, d_inv.p);
+            check_launch(ctx, "scatter_inverted");
+        }
+        // ---- rounds
+        DevVec<uint32_t>& d_cov = ctx->g_covered;
+        uint64_t cov_words = (cnt + 31) / 32 + 1;
+        d_cov.ensure_scratch(cov_words);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
+        const uint32_t npartial =
+            (uint32_t)std::min<uint64_t>(((uint64_t)limit / 4 + 255) / 256 + 1, (uint64_t)wide);
+        DevVec<uint64_t>& d_partial = ctx->g_partial;
+        d_partial.ensure_scratch(npartial);
+        DevVec<uint32_t>& d_sol = ctx->g_solution;
+        DevVec<uint64_t>& d_gain = ctx->g_gains;
+        d_sol.ensure_scratch(k);
+        d_gain.ensure_scratch(k);
+        std::vector<uint32_t> h_sol(k, 0xFFFFFFFFu);
+        std::vector<uint64_t> h_gain(k, 0);
+        const int cover_blocks = ctx->sm_count * 2;
+        uint32_t done = 0;
+        bool exhausted = occurrences == 0;
+        while (done < k && !exhausted) {
+            uint32_t group = std::min<uint32_t>(k - done, 64);
+            for (uint32_t r = done; r < done + group; ++r) {
+                argmax_partial<<<npartial, 256, 0, st>>>(d_cnt.p, limit, d_partial.p);
+                check_launch(ctx, "argmax_partial");
+                cover_winner<<<cover_blocks, 256, 0, st>>>(v, d_partial.p, npartial, d_cand,
+                                                           d_pos.p, d_inv.p, d_cnt.p, d_cov.p, r,
+                                                           d_sol.p, d_gain.p);
+                check_launch(ctx, "cover_winner");
+            }
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(h_sol.data() + done, d_sol.p + done, group * 4ull,
+                                            cudaMemcpyDeviceToHost, st));
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(h_gain.data() + done, d_gain.p + done, group * 8ull,
+                                            cudaMemcpyDeviceToHost, st));
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+            for (uint32_t r = done; r < done + group; ++r) {
+                if (h_gain[r] == 0) {
+                    exhausted = true;
+                    done = r;
+                    break;
+                }
+            }
+            if (!exhausted) done += group;
+        }
+        // ---- zero-gain padding: smallest unselected candidates in ascending order
+        // (proj/src/coverage.cpp:101-106,155; pinned by tests/test_coverage.cpp:58-64)
+        uint64_t cov = 0;
+        for (uint32_t r = 0; r < done; ++r) {
+            solution[r] = h_sol[r];
+            cov += h_gain[r];
+        }
+        if (done < k) {
+            std::vector<uint32_t> chosen(solution, solution + done);
+            std::sort(chosen.begin(), chosen.end());
+            uint64_t ci = 0;  // index into the ascending candidate sequence
+            size_t sj = 0;
+            for (uint32_t r = done; r < k; ++r) {
+                for (;;) {
+                    uint32_t c = cand_ids ? cand_sorted[ci] : (uint32_t)ci;
+                    while (sj < chosen.size() && chosen[sj] < c) ++sj;
+                    if (sj < chosen.size() && chosen[sj] == c) {
+                        ++ci;
+                        continue;
+                    }
+                    solution[r] = c;
+                    ++ci;
+                    break;
+                }
+            }
+        }
+        *coverage = cov;
+    });
+}
+
+int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
+                         const hsaw_gpu_walkset* walkset, int kind, uint64_t off, uint64_t cnt,
+                         const uint32_t* cand_ids, uint64_t ncand, const uint32_t* items,
+                         uint64_t nitems, uint64_t* coverage) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (!coverage) fail(HSAW_EINVAL, "coverage_of: null output");
+        if (nitems && !items) fail(HSAW_EINVAL, "coverage_of: null items");
+        WalkView v = make_view(stream, walkset, kind, off, cnt);
+        *coverage = 0;
+        if (cnt == 0 || nitems == 0) return;
+        cudaStream_t st = ctx->stream;
+        // only candidate items are indexed (CoverageIndex::insert, proj/src/coverage.cpp:31-35)
+        std::vector<uint32_t> q;
+        q.reserve(nitems);
+        std::vector<uint32_t> cand_sorted;
+        if (cand_ids) {
+            cand_sorted.assign(cand_ids, cand_ids + ncand);
+            std::sort(cand_sorted.begin(), cand_sorted.end());
+        }
+        for (uint64_t i = 0; i < nitems; ++i) {
+            uint32_t it = items[i];
+            if (it >= v.limit) continue;
+            if (cand_ids && !std::binary_search(cand_sorted.begin(), cand_sorted.end(), it)) continue;
+            q.push_back(it);
+        }
+        if (q.empty()) return;
+        DevVec<uint32_t>& bits = ctx->g_query_bits;
+        uint64_t words = ((uint64_t)v.limit + 31) / 32 + 1;
+        if (bits.cap < words) {
+            bits.ensure_scratch(words);
+            HSAW_CUDA_CHECK(cudaMemsetAsync(bits.p, 0, bits.cap * 4, st));  // kept all-zero between calls
+        }
+        DevVec<uint32_t>& d_q = ctx->g_solution;
+        d_q.ensure_scratch(q.size());
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(d_q.p, q.data(), q.size() * 4, cudaMemcpyHostToDevice, st));
+        unsigned qb = (unsigned)((q.size() + 255) / 256);
+        set_bits<<<qb, 256, 0, st>>>(d_q.p, q.size(), bits.p);
+        check_launch(ctx, "set_bits");
+        unsigned long long* d_out = reinterpret_cast<unsigned long long*>(ctx->d_scalars + 8);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_out, 0, 8, st));
+        int blocks = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)ctx->sm_count * 8);
+        count_covered<<<blocks, 256, 0, st>>>(v, bits.p, d_out);
+        check_launch(ctx, "count_covered");
+        clear_bits<<<qb, 256, 0, st>>>(d_q.p, q.size(), bits.p);
+        check_launch(ctx, "clear_bits");
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(&ctx->h_scalars[0], d_out, 8, cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        *coverage = ctx->h_scalars[0];
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,683 @@
+// Sampler kernels for sm_100a:
+//   K1  encode_kernel         thread_sample for a range of batches (proj/src/sampler.cpp:267-290)
+//   K2  decode_kernel         DecodeContext::decode replay (proj/src/sampler.cpp:295-338)
+//   K2b distinct_kernel(s)    the exact visited-set verdict of decode, on the materialised nodes
+//
+// Execution model: one lane owns one batch (K1) or one walk (K2) at a time — the
+// xorshift64* chain inside a batch is strictly sequential — and the warp runs ONE flattened loop
+// whose body is "one draw + at most one edge-record load + one node-record load" for every lane,
+// whatever phase of its walk the lane is in. Lanes that finish refill from a global cursor with a
+// warp-aggregated atomicAdd, so a warp never waits for its longest attempt.
+#include "sampler.cuh"
+#include "walk.cuh"
+
+namespace hsawgpu {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct EncodeParams {
+    const NodeRec* nodes;
+    const EdgeRec* edges;
+    uint32_t n;
+    uint32_t l;       // attempts per batch
+    uint32_t window;  // runtime width for the generic kernel
+    uint64_t first_worker;
+    uint64_t nbatches;
+    uint64_t* out_seed;
+    uint32_t* out_len;
+    uint32_t* out_count;
+    uint64_t* stats;   // u64[8]
+    uint64_t* cursor;  // next batch index of this launch
+};
+
+// WindowFilter (proj/src/sampler.cpp:65-86) as a shift register of the last W pushed nodes: the
+// ring buffer's content is exactly that set, and contains() only asks for membership.
+template <int W>
+struct Window {
+    uint32_t r[W > 0 ? W : 1];
+    __device__ __forceinline__ void reset(uint32_t, uint32_t v0) {
+#pragma unroll
+        for (int i = 0; i < W; ++i) r[i] = kInvalidNode;
+        push(v0);
+    }
+    __device__ __forceinline__ bool contains(uint32_t u) const {
+        bool c = false;
+#pragma unroll
+        for (int i = 0; i < W; ++i) c |= r[i] == u;
+        return c;
+    }
+    __device__ __forceinline__ void push(uint32_t u) {
+        if (W == 0) return;
+#pragma unroll
+        for (int i = W - 1; i > 0; --i) r[i] = r[i - 1];
+        r[0] = u;
+    }
+};
+
+// Runtime width 0..8 (any SamplerConfig::window, clamped to 8 as sampler.cpp:71 does).
+template <>
+struct Window<-1> {
+    uint32_t r[8];
+    uint32_t size;
+    __device__ __forceinline__ void reset(uint32_t w, uint32_t v0) {
+        size = w > 8 ? 8 : w;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = kInvalidNode;
+        push(v0);
+    }
+    __device__ __forceinline__ bool contains(uint32_t u) const {
+        bool c = false;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c |= (i < (int)size) && r[i] == u;
+        return c;
+    }
+    __device__ __forceinline__ void push(uint32_t u) {
+        if (size == 0) return;
+#pragma unroll
+        for (int i = 7; i > 0; --i)
+            if (i < (int)size) r[i] = r[i - 1];
+        r[0] = u;
+    }
+};
+
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+    return v;
+}
+
+// Warp-aggregated claim of work items from a global cursor. Returns true and sets `mine` for
+// lanes that wanted and got an item; sets `drained` (warp-uniform) once the cursor passed total.
+__device__ __forceinline__ bool claim(uint64_t* cursor, uint64_t total, bool want, uint32_t lane,
+                                      uint64_t& mine, bool& drained) {
+    unsigned need = __ballot_sync(kFullMask, want);
+    if (!need) return false;
+    int leader = __ffs(need) - 1;
+    uint64_t base = 0;
+    if ((int)lane == leader)
+        base = atomicAdd(reinterpret_cast<unsigned long long*>(cursor),
+                         (unsigned long long)__popc(need));
+    base = __shfl_sync(kFullMask, base, leader);
+    if (base + __popc(need) >= total) drained = true;
+    if (!want) return false;
+    mine = base + __popc(need & ((1u << lane) - 1));
+    return mine < total;
+}
+
+// ---- K1 ----------------------------------------------------------------------------------------
+// HEUR: 0 Brent, 2 None (CycleHeuristic, proj/include/hsaw/sampler.hpp:46). WIN: window width or
+// -1 for the runtime-width variant.
+template <int HEUR, int WIN>
+__global__ void __launch_bounds__(kThreads) encode_kernel(EncodeParams p) {
+    const uint32_t lane = threadIdx.x & 31;
+    const NodeRec* __restrict__ nodes = p.nodes;
+    const EdgeRec* __restrict__ edges = p.edges;
+
+    uint64_t s = 0, snapshot = 0, bidx = 0;
+    uint32_t lo = 0, deg = 0;
+    uint64_t tot = 0, scale = 0;
+    uint32_t nedges = 0, att = 0, cnt = 0;
+    bool have = false, fresh = true, drained = false;
+    Window<WIN> win;
+    uint32_t b_anchor = kInvalidNode, b_power = 1, b_lam = 0;
+    uint64_t st_draws = 0, st_steps = 0, st_bytes = 0, st_att = 0, st_acc = 0;
+
+    for (;;) {
+        if (!drained) {
+            uint64_t mine = 0;
+            if (claim(p.cursor, p.nbatches, !have, lane, mine, drained)) {
+                bidx = mine;
+                s = seed_from_worker(p.first_worker + mine);  // sampler.cpp:272
+#pragma unroll
+                for (int i = 0; i < 8; ++i) (void)prg_next(s);  // burn-in, sampler.cpp:273
+                att = 0;
+                cnt = 0;
+                fresh = true;
+                have = true;
+            }
+        }
+        if (!__any_sync(kFullMask, have)) break;
+        if (!have) continue;
+
+        // ---- one step of this lane's current attempt (run_walk_attempt, sampler.cpp:147-204)
+        uint32_t u = 0;
+        bool walking;
+        if (fresh) {
+            snapshot = s;  // Seed_h, sampler.cpp:155,277
+            uint64_t k = draw53(s);
+            u = start_node(k, p.n);  // sampler.cpp:24
+            nedges = 0;
+            walking = true;
+            st_draws += 1;
+            st_att += 1;
+        } else {
+            walking = false;
+            if (nedges < p.n) {  // len_cap = g.n, sampler.cpp:43,281
+                uint64_t k = draw53(s);
+                st_draws += 1;
+                st_steps += 1;
+                bool live = deg != 0 && k < tot;  // graph.hpp:66
+                st_bytes += pick_alg_bytes(deg, live);
+                if (live) {
+                    (void)pick_slot(edges, lo, deg, scale, k, u);
+                    bool cyc = win.contains(u);  // sampler.cpp:180
+                    if (HEUR == 0 && !cyc) {     // BrentState::check, sampler.cpp:100-108
+                        if (u == b_anchor) {
+                            cyc = true;
+                        } else if (++b_lam == b_power) {
+                            b_anchor = u;
+                            b_power <<= 1;
+                            b_lam = 0;
+                        }
+                    }
+                    if (!cyc) {
+                        ++nedges;  // resolve(), sampler.cpp:54
+                        walking = true;
+                    }
+                }
+            }
+        }
+
+        bool attempt_done = true;
+        if (walking) {
+            NodeRec rec = load_node(nodes, u);
+            st_bytes += 8;  // p_of[u]
+            bool accepted = false;
+            if (rec.acc_thr != 0) {  // is_suspect, sampler.cpp:32,55
+                uint64_t k2 = draw53(s);
+                st_draws += 1;
+                accepted = k2 < rec.acc_thr;  // r <= p_of[u], sampler.cpp:34,57
+            }
+            if (accepted) {
+                uint64_t slot = bidx * p.l + cnt;  // seq = index among accepted, sampler.cpp:283
+                p.out_seed[slot] = snapshot;
+                p.out_len[slot] = nedges;
+                ++cnt;
+                st_acc += 1;
+            } else {
+                lo = rec.lo;
+                deg = rec.deg;
+                tot = rec.tot_thr;
+                scale = rec.scale;
+                if (fresh) {
+                    win.reset(p.window, u);  // sampler.cpp:166-169
+                    b_anchor = u;
+                    b_power = 1;
+                    b_lam = 0;
+                } else {
+                    win.push(u);  // sampler.cpp:200
+                }
+                attempt_done = false;
+                if (deg == 0) {
+                    // The next pick is certain to fail after exactly one draw (empty row), unless
+                    // the length cap stops it before drawing: settle it now, saving an iteration.
+                    if (nedges < p.n) {
+                        (void)prg_next(s);
+                        st_draws += 1;
+                        st_steps += 1;
+                        st_bytes += 16;
+                    }
+                    attempt_done = true;
+                }
+            }
+        }
+        if (attempt_done) {
+            fresh = true;
+            if (++att == p.l) {
+                p.out_count[bidx] = cnt;
+                have = false;
+            }
+        } else {
+            fresh = false;
+        }
+    }
+
+    st_draws = warp_sum(st_draws);
+    st_steps = warp_sum(st_steps);
+    st_bytes = warp_sum(st_bytes);
+    st_att = warp_sum(st_att);
+    st_acc = warp_sum(st_acc);
+    if (lane == 0 && p.stats) {
+        auto* st = reinterpret_cast<unsigned long long*>(p.stats);
+        atomicAdd(st + ST_ATTEMPTS, (unsigned long long)st_att);
+        atomicAdd(st + ST_DRAWS, (unsigned long long)st_draws);
+        atomicAdd(st + ST_STEPS, (unsigned long long)st_steps);
+        atomicAdd(st + ST_BYTES, (unsigned long long)st_bytes);
+        atomicAdd(st + ST_ACCEPTED, (unsigned long long)st_acc);
+    }
+}
+
+// ---- K2 ----------------------------------------------------------------------------------------
+struct DecodeParams {
+    const NodeRec* nodes;
+    const EdgeRec* edges;
+    uint32_t n;
+    uint64_t nwalks;
+    const uint64_t* seed;
+    const uint32_t* len;
+    const uint64_t* edge_off;
+    uint32_t* out_nodes;
+    uint32_t* out_edges;
+    uint8_t* status;
+    uint32_t* nnodes;  // nullable: nodes written per walk (only needed for foreign encodings)
+    uint64_t* stats;
+    uint64_t* cursor;
+};
+
+__global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
+    const uint32_t lane = threadIdx.x & 31;
+    const NodeRec* __restrict__ nodes = p.nodes;
+    const EdgeRec* __restrict__ edges = p.edges;
+
+    uint64_t s = 0, w = 0, base = 0;
+    uint32_t lo = 0, deg = 0, len = 0, nedges = 0;
+    uint64_t tot = 0, scale = 0;
+    bool have = false, fresh = true, drained = false;
+    uint64_t st_steps = 0;
+
+    for (;;) {
+        if (!drained) {
+            uint64_t mine = 0;
+            if (claim(p.cursor, p.nwalks, !have, lane, mine, drained)) {
+                w = mine;
+                s = p.seed[w];
+                len = p.len[w];
+                base = p.edge_off[w];
+                fresh = true;
+                have = true;
+            }
+        }
+        if (!__any_sync(kFullMask, have)) break;
+        if (!have) continue;
+
+        uint32_t verdict = 0;  // 0 keep walking, 1 decoded, 2 mismatch
+        uint32_t u = 0;
+        bool arrived = false;
+        if (fresh) {
+            if (s == 0) {
+                verdict = 2;  // "decode: zero seed state", sampler.cpp:306
+                nedges = 0;
+                if (p.nnodes) p.nnodes[w] = 0;
+            } else {
+                uint64_t k = draw53(s);
+                u = start_node(k, p.n);
+                nedges = 0;
+                p.out_nodes[base + w] = u;
+                arrived = true;
+            }
+        } else {
+            // advance_edge with len_cap = n (sampler.cpp:322-324): any stop here is a mismatch
+            if (nedges >= p.n) {
+                verdict = 2;
+            } else {
+                uint64_t k = draw53(s);
+                st_steps += 1;
+                if (deg == 0 || k >= tot) {
+                    verdict = 2;
+                } else {
+                    uint32_t slot = pick_slot(edges, lo, deg, scale, k, u);
+                    p.out_edges[base + nedges] = lo + slot;
+                    ++nedges;
+                    p.out_nodes[base + w + nedges] = u;
+                    arrived = true;
+                }
+            }
+        }
+        if (arrived) {
+            NodeRec rec = load_node(nodes, u);
+            bool hit = false;
+            if (rec.acc_thr != 0) hit = draw53(s) < rec.acc_thr;
+            if (hit) {
+                verdict = nedges == len ? 1 : 2;  // sampler.cpp:311-314, 329-332
+            } else if (nedges >= len) {
+                verdict = 2;  // sampler.cpp:316-317, 334-335
+            } else {
+                lo = rec.lo;
+                deg = rec.deg;
+                tot = rec.tot_thr;
+                scale = rec.scale;
+                fresh = false;
+            }
+        }
+        if (verdict != 0) {
+            p.status[w] = (uint8_t)verdict;
+            if (p.nnodes && !(fresh && s == 0)) p.nnodes[w] = nedges + 1;
+            have = false;
+        }
+    }
+    st_steps = warp_sum(st_steps);
+    if (lane == 0 && p.stats)
+        atomicAdd(reinterpret_cast<unsigned long long*>(p.stats) + ST_DECODE_STEPS,
+                  (unsigned long long)st_steps);
+}
+
+// ---- K2b ---------------------------------------------------------------------------------------
+// Verdict to reproduce (sampler.cpp:318-337): the walk is dropped iff its replayed nodes are not
+// pairwise distinct. One warp per walk; <= 32 nodes: one __match_any_sync; <= kSmemNodes: an
+// open-addressing hash set in shared memory; longer walks are queued for distinct_long_kernel.
+constexpr int kCheckWarps = 4;
+constexpr uint32_t kTableSize = 4096;              // u32 slots per warp
+constexpr uint32_t kSmemNodes = kTableSize / 2;    // load factor <= 0.5
+
+struct CheckParams {
+    uint64_t nwalks;
+    const uint64_t* edge_off;
+    const uint32_t* nodes;
+    const uint32_t* nnodes;  // nullable: default len + 1
+    uint8_t* status;
+    uint32_t* long_list;   // (walk id, node count) pairs needing the long path
+    uint32_t* long_count;  // [0] long walks queued, [1] walks dropped (status 1 -> 0)
+    uint32_t long_cap;
+};
+
+__device__ __forceinline__ uint32_t node_hash(uint32_t v, uint32_t bits) {
+    return (v * 2654435761u) >> (32 - bits);
+}
+
+__global__ void __launch_bounds__(kCheckWarps * 32) distinct_kernel(CheckParams p) {
+    extern __shared__ uint32_t tables[];  // kCheckWarps x kTableSize
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t wib = threadIdx.x >> 5;
+    uint32_t* tab = tables + wib * kTableSize;
+    uint64_t warp = (uint64_t)blockIdx.x * kCheckWarps + wib;
+    uint64_t nwarps = (uint64_t)gridDim.x * kCheckWarps;
+    uint32_t dropped = 0;
+    for (uint64_t w = warp; w < p.nwalks; w += nwarps) {
+        uint8_t st = p.status[w];
+        if (st == 0) continue;
+        uint64_t base = p.edge_off[w] + w;
+        uint32_t nn = p.nnodes ? p.nnodes[w] : (uint32_t)(p.edge_off[w + 1] - p.edge_off[w]) + 1;
+        bool dup = false;
+        if (nn <= 1) {
+            // a single node cannot repeat
+        } else if (nn <= 32) {
+            uint32_t v = lane < nn ? p.nodes[base + lane] : 0;
+            unsigned valid = nn == 32 ? kFullMask : ((1u << nn) - 1);
+            unsigned same = __match_any_sync(kFullMask, v) & valid & ~(1u << lane);
+            dup = __any_sync(kFullMask, lane < nn && same != 0);
+        } else if (nn <= kSmemNodes) {
+            uint32_t bits = 32 - __clz(2 * nn - 1);  // table of >= 2*nn slots
+            uint32_t size = 1u << bits;
+            for (uint32_t i = lane; i < size; i += 32) tab[i] = kInvalidNode;
+            __syncwarp();
+            bool mydup = false;
+            for (uint32_t i = lane; i < nn; i += 32) {
+                uint32_t v = p.nodes[base + i];
+                uint32_t h = node_hash(v, bits);
+                for (;;) {
+                    uint32_t old = atomicCAS(&tab[h], kInvalidNode, v);
+                    if (old == kInvalidNode) break;
+                    if (old == v) {
+                        mydup = true;
+                        break;
+                    }
+                    h = (h + 1) & (size - 1);
+                }
+            }
+            dup = __any_sync(kFullMask, mydup);
+            __syncwarp();
+        } else {
+            if (lane == 0) {
+                uint32_t at = atomicAdd(p.long_count, 1u);
+                if (at < p.long_cap) {
+                    p.long_list[2 * at] = (uint32_t)w;
+                    p.long_list[2 * at + 1] = nn;
+                }
+            }
+            continue;
+        }
+        if (dup) {
+            if (lane == 0) p.status[w] = 0;
+            if (st == 1) ++dropped;
+        }
+    }
+    if (lane == 0 && dropped) atomicAdd(p.long_count + 1, dropped);
+}
+
+// Long walks (> kSmemNodes nodes): one block per walk, hash set in global scratch.
+__global__ void __launch_bounds__(256) distinct_long_kernel(CheckParams p, uint32_t nlong,
+                                                            const uint64_t* table_off,
+                                                            uint32_t* tables) {
+    uint32_t i = blockIdx.x;
+    if (i >= nlong) return;
+    uint32_t w = p.long_list[2 * i];
+    uint64_t base = p.edge_off[w] + w;
+    uint32_t nn = p.long_list[2 * i + 1];
+    uint32_t* tab = tables + table_off[i];
+    uint64_t size = table_off[i + 1] - table_off[i];  // power of two >= 2*nn
+    uint32_t bits = 63 - __clzll((long long)size);
+    for (uint64_t j = threadIdx.x; j < size; j += blockDim.x) tab[j] = kInvalidNode;
+    __syncthreads();
+    bool mydup = false;
+    for (uint32_t j = threadIdx.x; j < nn; j += blockDim.x) {
+        uint32_t v = p.nodes[base + j];
+        uint64_t h = node_hash(v, bits);
+        for (;;) {
+            uint32_t old = atomicCAS(&tab[h], kInvalidNode, v);
+            if (old == kInvalidNode) break;
+            if (old == v) {
+                mydup = true;
+                break;
+            }
+            h = (h + 1) & (size - 1);
+        }
+    }
+    if (__syncthreads_or(mydup) && threadIdx.x == 0) {
+        if (p.status[w] == 1) atomicAdd(p.long_count + 1, 1u);
+        p.status[w] = 0;
+    }
+}
+
+template <class K>
+int persistent_blocks(hsaw_gpu_ctx* ctx, K kernel, uint64_t items) {
+    int per_sm = 0;
+    HSAW_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
+    if (per_sm < 1) per_sm = 1;
+    uint64_t want = (items + kThreads - 1) / kThreads;
+    uint64_t full = (uint64_t)ctx->sm_count * per_sm;  // one resident wave: 148 x blocks/SM
+    return (int)(want < full ? (want ? want : 1) : full);
+}
+
+}  // namespace
+
+void validate_cfg(const hsaw_sampler_cfg& cfg) {
+    if (cfg.heuristic == 1)
+        fail(HSAW_EINVAL,
+             "sampler: the Floyd heuristic is not available on the device path (use Brent or None)");
+    if (cfg.heuristic != 0 && cfg.heuristic != 2) fail(HSAW_EINVAL, "sampler: unknown heuristic");
+    if (cfg.batch_size == 0) fail(HSAW_EINVAL, "sampler: batch_size must be positive");
+}
+
+void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t first_worker,
+                   uint64_t nbatches, uint64_t* d_seed, uint32_t* d_len, uint32_t* d_count,
+                   uint64_t* d_stats, uint64_t* d_cursor) {
+    if (nbatches == 0) return;
+    EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, cfg.batch_size, cfg.window,
+                   first_worker, nbatches, d_seed, d_len, d_count, d_stats, d_cursor};
+    HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
+    auto go = [&](auto kernel) {
+        int blocks = persistent_blocks(ctx, kernel, nbatches);
+        kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+        check_launch(ctx, "encode_kernel");
+    };
+    bool brent = cfg.heuristic == 0;
+    if (cfg.window == 2)
+        brent ? go(encode_kernel<0, 2>) : go(encode_kernel<2, 2>);
+    else if (cfg.window == 0)
+        brent ? go(encode_kernel<0, 0>) : go(encode_kernel<2, 0>);
+    else
+        brent ? go(encode_kernel<0, -1>) : go(encode_kernel<2, -1>);
+}
+
+static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
+                               const uint32_t* d_len, const uint64_t* d_edge_off,
+                               uint32_t* d_nodes, uint32_t* d_edges, uint8_t* d_status,
+                               uint32_t* d_nnodes, uint64_t* d_stats, uint64_t* d_cursor) {
+    if (nwalks == 0) return;
+    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, nwalks,   d_seed,  d_len,   d_edge_off,
+                   d_nodes,      d_edges,      d_status, d_nnodes, d_stats, d_cursor};
+    HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
+    int blocks = persistent_blocks(ctx, decode_kernel, nwalks);
+    decode_kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+    check_launch(ctx, "decode_kernel");
+}
+
+void launch_decode(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
+                   const uint32_t* d_len, const uint64_t* d_edge_off, uint32_t* d_nodes,
+                   uint32_t* d_edges, uint8_t* d_status, uint64_t* d_stats, uint64_t* d_cursor) {
+    launch_decode_impl(ctx, nwalks, d_seed, d_len, d_edge_off, d_nodes, d_edges, d_status,
+                       nullptr, d_stats, d_cursor);
+}
+
+// Shared by the stream path (nnodes == nullptr) and decode_walks (foreign encodings).
+static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
+                                    const uint64_t* d_edge_off, const uint32_t* d_nodes,
+                                    const uint32_t* d_nnodes, uint8_t* d_status) {
+    if (nwalks == 0) return 0;
+    if (nwalks > 0xFFFFFFFFull) fail(HSAW_EINVAL, "distinct check: more than 2^32 walks per call");
+    const uint32_t long_cap = 1u << 16;
+    ctx->chk_list.ensure_scratch(2ull * long_cap);
+    ctx->chk_counters.ensure_scratch(2);
+    uint32_t* counters = ctx->chk_counters.p;
+    HSAW_CUDA_CHECK(cudaMemsetAsync(counters, 0, 8, ctx->stream));
+    CheckParams p{nwalks, d_edge_off, d_nodes, d_nnodes, d_status, ctx->chk_list.p, counters,
+                  long_cap};
+    const int smem = kCheckWarps * kTableSize * 4;
+    static bool attr_set = false;
+    if (!attr_set) {
+        HSAW_CUDA_CHECK(cudaFuncSetAttribute(distinct_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_set = true;
+    }
+    uint64_t want = (nwalks + kCheckWarps - 1) / kCheckWarps;
+    uint64_t full = (uint64_t)ctx->sm_count * 3;  // 64 KB of tables per block: 3 blocks / SM
+    int blocks = (int)(want < full ? want : full);
+    distinct_kernel<<<blocks, kCheckWarps * 32, smem, ctx->stream>>>(p);
+    check_launch(ctx, "distinct_kernel");
+    uint32_t* h = reinterpret_cast<uint32_t*>(ctx->h_scalars + 32);
+    HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    uint32_t nlong = h[0];
+    if (nlong > long_cap) fail(HSAW_ECUDA, "distinct check: too many long walks in one round");
+    if (nlong) {
+        // rare path: size one global hash table per long walk, run one block per walk
+        std::vector<uint32_t> pairs(2ull * nlong);
+        HSAW_CUDA_CHECK(cudaMemcpy(pairs.data(), ctx->chk_list.p, 8ull * nlong,
+                                   cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> toff(nlong + 1, 0);
+        for (uint32_t i = 0; i < nlong; ++i) {
+            uint64_t nn = pairs[2 * i + 1];
+            uint64_t size = 1;
+            while (size < 2 * nn) size <<= 1;
+            toff[i + 1] = toff[i] + size;
+        }
+        DevVec<uint32_t> tables;
+        DevVec<uint64_t> d_toff;
+        tables.ensure_scratch(toff[nlong]);
+        d_toff.ensure_scratch(nlong + 1);
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(d_toff.p, toff.data(), 8ull * (nlong + 1),
+                                        cudaMemcpyHostToDevice, ctx->stream));
+        distinct_long_kernel<<<nlong, 256, 0, ctx->stream>>>(p, nlong, d_toff.p, tables.p);
+        check_launch(ctx, "distinct_long_kernel");
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    }
+    return h[1];
+}
+
+uint32_t launch_distinct_check(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_edge_off,
+                               const uint32_t* d_nodes, uint8_t* d_status) {
+    return distinct_check_impl(ctx, nwalks, d_edge_off, d_nodes, nullptr, d_status);
+}
+
+}  // namespace hsawgpu
+
+using namespace hsawgpu;
+
+extern "C" {
+
+int hsaw_gpu_encode_batches(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg* cfg,
+                            uint64_t first_worker_id, uint64_t nbatches, uint64_t* out_seed,
+                            uint32_t* out_len, uint32_t* out_count, uint64_t* stats) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (!cfg || !out_seed || !out_len || !out_count) fail(HSAW_EINVAL, "encode: null argument");
+        if (!ctx->g.nodes) fail(HSAW_EINVAL, "encode: no graph uploaded");
+        validate_cfg(*cfg);
+        if (nbatches == 0) return;
+        uint64_t slots = nbatches * cfg->batch_size;
+        DevVec<uint64_t> d_seed, d_stats;
+        DevVec<uint32_t> d_len, d_count;
+        d_seed.ensure_scratch(slots);
+        d_len.ensure_scratch(slots);
+        d_count.ensure_scratch(nbatches);
+        d_stats.ensure_scratch(9);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_stats.p, 0, 72, ctx->stream));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_seed.p, 0, slots * 8, ctx->stream));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_len.p, 0, slots * 4, ctx->stream));
+        launch_encode(ctx, *cfg, first_worker_id, nbatches, d_seed.p, d_len.p, d_count.p,
+                      d_stats.p, d_stats.p + 8);
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(out_seed, d_seed.p, slots * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(out_len, d_len.p, slots * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(out_count, d_count.p, nbatches * 4, cudaMemcpyDeviceToHost,
+                                        ctx->stream));
+        if (stats)
+            HSAW_CUDA_CHECK(
+                cudaMemcpyAsync(stats, d_stats.p, 64, cudaMemcpyDeviceToHost, ctx->stream));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int hsaw_gpu_decode_walks(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* seeds,
+                          const uint32_t* lens, const uint64_t* edge_off, uint32_t* out_nodes,
+                          uint32_t* out_edges, uint8_t* out_status) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (!ctx->g.nodes) fail(HSAW_EINVAL, "decode: no graph uploaded");
+        if (nwalks == 0) return;
+        if (!seeds || !lens || !edge_off || !out_nodes || !out_edges || !out_status)
+            fail(HSAW_EINVAL, "decode: null argument");
+        uint64_t total = 0;
+        for (uint64_t w = 0; w < nwalks; ++w) {
+            if (edge_off[w] != total) fail(HSAW_EINVAL, "decode: edge_off is not the prefix sum of lens");
+            total += lens[w];
+        }
+        if (edge_off[nwalks] != total) fail(HSAW_EINVAL, "decode: edge_off is not the prefix sum of lens");
+        DevVec<uint64_t> d_seed, d_off, d_scal;
+        DevVec<uint32_t> d_len, d_nodes, d_edges, d_nn;
+        DevVec<uint8_t> d_status;
+        d_seed.ensure_scratch(nwalks);
+        d_len.ensure_scratch(nwalks);
+        d_off.ensure_scratch(nwalks + 1);
+        d_nodes.ensure_scratch(total + nwalks);
+        d_edges.ensure_scratch(total + 1);
+        d_nn.ensure_scratch(nwalks);
+        d_status.ensure_scratch(nwalks);
+        d_scal.ensure_scratch(9);
+        cudaStream_t st = ctx->stream;
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(d_seed.p, seeds, nwalks * 8, cudaMemcpyHostToDevice, st));
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(d_len.p, lens, nwalks * 4, cudaMemcpyHostToDevice, st));
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(d_off.p, edge_off, (nwalks + 1) * 8, cudaMemcpyHostToDevice, st));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_scal.p, 0, 72, st));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_nodes.p, 0xFF, (total + nwalks) * 4, st));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_edges.p, 0xFF, (total + 1) * 4, st));
+        launch_decode_impl(ctx, nwalks, d_seed.p, d_len.p, d_off.p, d_nodes.p, d_edges.p,
+                           d_status.p, d_nn.p, d_scal.p, d_scal.p + 8);
+        (void)distinct_check_impl(ctx, nwalks, d_off.p, d_nodes.p, d_nn.p, d_status.p);
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(out_nodes, d_nodes.p, (total + nwalks) * 4,
+                                        cudaMemcpyDeviceToHost, st));
+        if (total)
+            HSAW_CUDA_CHECK(
+                cudaMemcpyAsync(out_edges, d_edges.p, total * 4, cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(out_status, d_status.p, nwalks, cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+}  // extern "C"

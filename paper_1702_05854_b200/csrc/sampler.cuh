@@ -1,0 +1,32 @@
+// Launch wrappers of the sampler kernels (sampler.cu), used by the C-ABI entry points in
+// sampler.cu itself and by the sample stream (stream.cu). All pointers are device pointers.
+#pragma once
+
+#include "common.cuh"
+
+namespace hsawgpu {
+
+// index into the u64[8] stats block (hsaw_gpu.h: hsaw_gpu_encode_batches)
+enum { ST_ATTEMPTS = 0, ST_DRAWS = 1, ST_STEPS = 2, ST_BYTES = 3, ST_ACCEPTED = 4,
+       ST_DECODE_STEPS = 5, ST_DROPPED = 6, ST_SPARE = 7 };
+
+void validate_cfg(const hsaw_sampler_cfg& cfg);
+
+// K1: batches [first_worker, first_worker + nbatches) -> per-batch count + (seed, len) slots.
+// d_stats: u64[8] accumulated (never reset here). d_cursor: one zeroed u64 of scratch.
+void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t first_worker,
+                   uint64_t nbatches, uint64_t* d_seed, uint32_t* d_len, uint32_t* d_count,
+                   uint64_t* d_stats, uint64_t* d_cursor);
+
+// K2: replay nwalks encoded walks into nodes/edges at edge_off (exclusive sum of lens).
+// d_status[w]: 1 replayed, 2 mismatch. d_cursor: one zeroed u64 of scratch.
+void launch_decode(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
+                   const uint32_t* d_len, const uint64_t* d_edge_off, uint32_t* d_nodes,
+                   uint32_t* d_edges, uint8_t* d_status, uint64_t* d_stats, uint64_t* d_cursor);
+
+// K2b: exact self-avoidance recheck; sets d_status[w] = 0 for walks (status 1) whose node list
+// is not pairwise distinct. Synchronises the stream; returns the number of walks dropped.
+uint32_t launch_distinct_check(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_edge_off,
+                           const uint32_t* d_nodes, uint8_t* d_status);
+
+}  // namespace hsawgpu

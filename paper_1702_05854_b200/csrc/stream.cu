@@ -1,0 +1,441 @@
+// Sample stream: orchestration of K1 (encode) -> gather -> K2 (decode) -> K2b (exact recheck) ->
+// deterministic compaction into the dense walk pool. Order contract (proj/src/sampler.cpp:452-460):
+// walks are appended in (batch, seq) order — positions come from prefix sums, never from atomics —
+// so prefixes of the pool are pure functions of (graph, suspects, seed) exactly as in the reference.
+#include "stream.cuh"
+
+#include "sampler.cuh"
+
+using namespace hsawgpu;
+
+namespace {
+
+constexpr uint64_t kMaxChunkBatches = 1ull << 22;  // bounds per-chunk scratch (slots = 10x this)
+
+// (batch, seq) slots -> dense encoded list in batch-major order. One thread per slot.
+__global__ void gather_encoded(uint64_t nbatches, uint32_t l, uint64_t first_global_batch,
+                               const uint32_t* __restrict__ count,
+                               const uint32_t* __restrict__ first,
+                               const uint64_t* __restrict__ slot_seed,
+                               const uint32_t* __restrict__ slot_len, uint64_t* __restrict__ enc_seed,
+                               uint32_t* __restrict__ enc_len, uint64_t* __restrict__ enc_batch,
+                               uint32_t* __restrict__ enc_seq) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nbatches * l) return;
+    uint64_t b = i / l;
+    uint32_t j = (uint32_t)(i - b * l);
+    if (j >= count[b]) return;
+    uint32_t dst = first[b] + j;
+    enc_seed[dst] = slot_seed[i];
+    enc_len[dst] = slot_len[i];
+    enc_batch[dst] = first_global_batch + b;
+    enc_seq[dst] = j;
+}
+
+// status -> (valid flag, valid length) for the two compaction scans; flags a replay mismatch.
+__global__ void mark_valid(uint64_t nwalks, const uint8_t* __restrict__ status,
+                           const uint32_t* __restrict__ enc_len, uint32_t* __restrict__ vflag,
+                           uint32_t* __restrict__ vlen, uint32_t* __restrict__ mismatch) {
+    uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w > nwalks) return;
+    if (w == nwalks) {  // scan sentinels
+        vflag[w] = 0;
+        vlen[w] = 0;
+        return;
+    }
+    uint8_t st = status[w];
+    if (st == 2) atomicExch(mismatch, 1u);
+    vflag[w] = st == 1;
+    vlen[w] = st == 1 ? enc_len[w] : 0;
+}
+
+// One warp per decoded walk: copy it to its final place in the pool.
+__global__ void compact_walks(uint64_t nwalks, const uint32_t* __restrict__ vflag,
+                              const uint32_t* __restrict__ vidx, const uint64_t* __restrict__ voff,
+                              const uint64_t* __restrict__ tmp_off,
+                              const uint32_t* __restrict__ tmp_nodes,
+                              const uint32_t* __restrict__ tmp_edges,
+                              const uint32_t* __restrict__ enc_len,
+                              const uint64_t* __restrict__ enc_batch,
+                              const uint32_t* __restrict__ enc_seq, uint64_t base_walk,
+                              uint64_t base_edge, uint64_t* __restrict__ edge_off,
+                              uint32_t* __restrict__ nodes, uint32_t* __restrict__ edges,
+                              uint64_t* __restrict__ tag_batch, uint32_t* __restrict__ tag_seq) {
+    uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w = warp; w < nwalks; w += nwarps) {
+        if (!vflag[w]) continue;
+        uint64_t dw = base_walk + vidx[w];
+        uint64_t de = base_edge + voff[w];
+        uint32_t len = enc_len[w];
+        uint64_t se = tmp_off[w];
+        if (lane == 0) {
+            edge_off[dw] = de;
+            tag_batch[dw] = enc_batch[w];
+            tag_seq[dw] = enc_seq[w];
+        }
+        for (uint32_t i = lane; i <= len; i += 32) nodes[de + dw + i] = tmp_nodes[se + w + i];
+        for (uint32_t i = lane; i < len; i += 32) edges[de + i] = tmp_edges[se + i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        edge_off[base_walk + vidx[nwalks]] = base_edge + voff[nwalks];
+}
+
+// accepted_after_batch (sampler.cpp:459) for the batches of this chunk.
+__global__ void batch_cumulative(uint64_t nbatches, const uint32_t* __restrict__ first,
+                                 const uint32_t* __restrict__ vidx, uint64_t base_walk,
+                                 uint64_t* __restrict__ out) {
+    uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nbatches) return;
+    out[b] = base_walk + vidx[first[b + 1]];
+}
+
+// first index with a[i] >= key, or n
+__global__ void lower_bound_u64(const uint64_t* __restrict__ a, uint64_t n, uint64_t key,
+                                uint64_t* __restrict__ out) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        if (a[mid] >= key)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    out[0] = lo;
+    out[1] = lo < n ? a[lo] : 0;
+}
+
+inline int blocks_for(uint64_t items, int threads) {
+    uint64_t b = (items + threads - 1) / threads;
+    return (int)(b ? b : 1);
+}
+
+uint64_t read_u64(hsaw_gpu_ctx* ctx, const uint64_t* d) {
+    HSAW_CUDA_CHECK(
+        cudaMemcpyAsync(ctx->h_scalars, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    return ctx->h_scalars[0];
+}
+uint32_t read_u32(hsaw_gpu_ctx* ctx, const uint32_t* d) {
+    HSAW_CUDA_CHECK(
+        cudaMemcpyAsync(ctx->h_scalars, d, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    return *reinterpret_cast<uint32_t*>(ctx->h_scalars);
+}
+
+// Samples global batches [first_batch, first_batch + nb) (nb <= kMaxChunkBatches) and appends.
+void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
+    hsaw_gpu_ctx* ctx = s->ctx;
+    cudaStream_t st = ctx->stream;
+    const uint32_t l = s->cfg.batch_size;
+    const uint64_t slots = nb * l;
+    if (slots > 0xFFFFFFF0ull) fail(HSAW_EINVAL, "stream: chunk too large for 32-bit walk ids");
+
+    // ---- K1
+    s->slot_seed.ensure_scratch(slots + 1);
+    s->slot_len.ensure_scratch(slots + 1);
+    s->count.ensure_scratch(nb + 1);
+    s->first.ensure_scratch(nb + 1);
+    HSAW_CUDA_CHECK(cudaMemsetAsync(s->count.p + nb, 0, 4, st));
+    launch_encode(ctx, s->cfg, s->seed + first_batch, nb, s->slot_seed.p, s->slot_len.p,
+                  s->count.p, s->stats.p, s->stats.p + 8);
+    exclusive_sum_u32(ctx, s->count.p, s->first.p, nb + 1);
+    const uint64_t E = read_u32(ctx, s->first.p + nb);  // encoded (heuristically accepted) walks
+
+    uint64_t A = 0, VT = 0;
+    s->vidx.ensure_scratch(E + 1);
+    if (E > 0) {
+        // ---- dense (batch, seq) order
+        s->enc_seed.ensure_scratch(E);
+        s->enc_len.ensure_scratch(E + 1);
+        s->enc_batch.ensure_scratch(E);
+        s->enc_seq.ensure_scratch(E);
+        s->tmp_off.ensure_scratch(E + 1);
+        gather_encoded<<<blocks_for(slots, 256), 256, 0, st>>>(
+            nb, l, first_batch, s->count.p, s->first.p, s->slot_seed.p, s->slot_len.p,
+            s->enc_seed.p, s->enc_len.p, s->enc_batch.p, s->enc_seq.p);
+        check_launch(ctx, "gather_encoded");
+        HSAW_CUDA_CHECK(cudaMemsetAsync(s->enc_len.p + E, 0, 4, st));
+        exclusive_sum_u32_to_u64(ctx, s->enc_len.p, s->tmp_off.p, E + 1);
+        const uint64_t T = read_u64(ctx, s->tmp_off.p + E);  // edges of all encoded walks
+
+        // ---- K2 + K2b
+        s->tmp_nodes.ensure_scratch(T + E);
+        s->tmp_edges.ensure_scratch(T + 1);
+        s->status.ensure_scratch(E);
+        launch_decode(ctx, E, s->enc_seed.p, s->enc_len.p, s->tmp_off.p, s->tmp_nodes.p,
+                      s->tmp_edges.p, s->status.p, s->stats.p, s->stats.p + 8);
+        s->dropped += launch_distinct_check(ctx, E, s->tmp_off.p, s->tmp_nodes.p, s->status.p);
+
+        // ---- compaction offsets. The slot arrays are dead after the gather and hold
+        // slots + 1 >= E + 1 entries, so they double as the valid-flag / valid-length scan inputs.
+        uint32_t* vflag = s->slot_len.p;
+        uint32_t* vlen = reinterpret_cast<uint32_t*>(s->slot_seed.p);
+        s->voff.ensure_scratch(E + 1);
+        uint32_t* mismatch = reinterpret_cast<uint32_t*>(s->stats.p + 9);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(mismatch, 0, 4, st));
+        mark_valid<<<blocks_for(E + 1, 256), 256, 0, st>>>(E, s->status.p, s->enc_len.p, vflag,
+                                                           vlen, mismatch);
+        check_launch(ctx, "mark_valid");
+        exclusive_sum_u32(ctx, vflag, s->vidx.p, E + 1);
+        exclusive_sum_u32_to_u64(ctx, vlen, s->voff.p, E + 1);
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(ctx->h_scalars + 1, s->voff.p + E, 8, cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(ctx->h_scalars + 2, mismatch, 4, cudaMemcpyDeviceToHost, st));
+        A = read_u32(ctx, s->vidx.p + E);
+        VT = ctx->h_scalars[1];
+        if (*reinterpret_cast<uint32_t*>(ctx->h_scalars + 2) != 0)
+            fail(HSAW_EDATA, "decode: replay disagreed with generation (internal error)");
+
+        // ---- append to the pool
+        s->edge_off.reserve(s->accepted + A + 1, st);
+        s->nodes.reserve(s->total_edges + VT + s->accepted + A, st);
+        s->edges.reserve(s->total_edges + VT + 1, st);
+        s->tag_batch.reserve(s->accepted + A + 1, st);
+        s->tag_seq.reserve(s->accepted + A + 1, st);
+        int cblocks = (int)std::min<uint64_t>((E + 7) / 8, (uint64_t)ctx->sm_count * 16);
+        compact_walks<<<cblocks, 256, 0, st>>>(
+            E, vflag, s->vidx.p, s->voff.p, s->tmp_off.p, s->tmp_nodes.p, s->tmp_edges.p,
+            s->enc_len.p, s->enc_batch.p, s->enc_seq.p, s->accepted, s->total_edges,
+            s->edge_off.p, s->nodes.p, s->edges.p, s->tag_batch.p, s->tag_seq.p);
+        check_launch(ctx, "compact_walks");
+    } else {
+        HSAW_CUDA_CHECK(cudaMemsetAsync(s->vidx.p, 0, 4, st));
+        s->edge_off.reserve(s->accepted + 1, st);
+        uint64_t te = s->total_edges;
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(s->edge_off.p + s->accepted, &te, 8, cudaMemcpyHostToDevice, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+
+    // ---- per-batch cumulative counts
+    s->accepted_after_batch.size = s->local_batches;
+    s->accepted_after_batch.reserve(s->local_batches + nb, st);
+    if (E > 0) {
+        batch_cumulative<<<blocks_for(nb, 256), 256, 0, st>>>(
+            nb, s->first.p, s->vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches);
+        check_launch(ctx, "batch_cumulative");
+    } else {
+        std::vector<uint64_t> flat(nb, s->accepted);
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(s->accepted_after_batch.p + s->local_batches, flat.data(),
+                                        nb * 8, cudaMemcpyHostToDevice, st));
+    }
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+
+    s->accepted += A;
+    s->total_edges += VT;
+    s->local_batches += nb;
+    s->edge_off.size = s->accepted + 1;
+    s->nodes.size = s->total_edges + s->accepted;
+    s->edges.size = s->total_edges;
+    s->tag_batch.size = s->accepted;
+    s->tag_seq.size = s->accepted;
+    s->accepted_after_batch.size = s->local_batches;
+}
+
+void sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches) {
+    if (first_batch < s->last_batch_end)
+        fail(HSAW_EINVAL, "stream: batch ranges must be issued in increasing order");
+    uint64_t done = 0;
+    while (done < nbatches) {
+        uint64_t nb = std::min(nbatches - done, kMaxChunkBatches);
+        sample_chunk(s, first_batch + done, nb);
+        done += nb;
+        s->last_batch_end = first_batch + done;
+    }
+    s->last_batch_end = first_batch + nbatches;
+}
+
+void local_cut(const hsaw_gpu_stream* s, uint64_t min_count, uint64_t* idx, uint64_t* value) {
+    hsaw_gpu_ctx* ctx = s->ctx;
+    uint64_t* d_out = ctx->d_scalars;
+    lower_bound_u64<<<1, 1, 0, ctx->stream>>>(s->accepted_after_batch.p, s->local_batches,
+                                              min_count, d_out);
+    check_launch(ctx, "lower_bound_u64");
+    HSAW_CUDA_CHECK(
+        cudaMemcpyAsync(ctx->h_scalars, d_out, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    *idx = ctx->h_scalars[0];
+    *value = ctx->h_scalars[1];
+}
+
+}  // namespace
+
+extern "C" {
+
+int hsaw_gpu_stream_create(hsaw_gpu_ctx* ctx, uint64_t seed, const hsaw_sampler_cfg* cfg,
+                           hsaw_gpu_stream** out) {
+    if (!ctx || !out) return HSAW_EINVAL;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        if (!cfg) fail(HSAW_EINVAL, "stream_create: null config");
+        if (!ctx->g.nodes) fail(HSAW_EINVAL, "stream_create: no graph uploaded");
+        validate_cfg(*cfg);
+        auto* s = new hsaw_gpu_stream;
+        s->ctx = ctx;
+        s->seed = seed;
+        s->cfg = *cfg;
+        try {
+            s->stats.ensure_scratch(16);
+            HSAW_CUDA_CHECK(cudaMemsetAsync(s->stats.p, 0, 16 * 8, ctx->stream));
+            s->edge_off.reserve(1024, ctx->stream);
+            HSAW_CUDA_CHECK(cudaMemsetAsync(s->edge_off.p, 0, 8, ctx->stream));
+            s->edge_off.size = 1;
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+void hsaw_gpu_stream_destroy(hsaw_gpu_stream* s) {
+    if (!s) return;
+    cudaSetDevice(s->ctx->device);
+    cudaStreamSynchronize(s->ctx->stream);
+    delete s;
+}
+
+int hsaw_gpu_stream_ensure(hsaw_gpu_stream* s, uint64_t min_accepted) {
+    if (!s) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        const uint64_t bs = s->cfg.batch_size;
+        while (s->accepted < min_accepted) {
+            // budget rule of sampler.cpp:396-404: floor(max_attempts / batch_size) batches overall
+            uint64_t attempts_so_far = s->next_batch * bs;
+            uint64_t budget_left =
+                s->cfg.max_attempts > attempts_so_far ? s->cfg.max_attempts - attempts_so_far : 0;
+            uint64_t max_batches = budget_left / bs;
+            if (max_batches == 0)
+                fail(HSAW_EBUDGET,
+                     "attempt budget exhausted while sampling walks; suspects may be unreachable");
+            // round size: only a speed knob (sampler.cpp:406-421) — pools are cut at whole-batch
+            // prefixes by accepted count, so over-materialising never changes a result
+            uint64_t need = min_accepted - s->accepted;
+            uint64_t batches;
+            if (s->accepted == 0) {
+                batches = s->grow;
+                s->grow = std::min<uint64_t>(s->grow * 8, 1ull << 22);
+            } else {
+                double rate = (double)s->accepted / (double)attempts_so_far;
+                double est = (double)need / (rate * (double)bs);
+                batches = (uint64_t)(est * 1.1) + 64;
+            }
+            batches = std::max<uint64_t>(std::min(batches, max_batches), 1);
+            sample_range(s, s->next_batch, batches);
+            s->next_batch += batches;
+        }
+    });
+}
+
+int hsaw_gpu_stream_sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches,
+                                 uint64_t* accepted_in_range) {
+    if (!s) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        uint64_t before = s->accepted;
+        sample_range(s, first_batch, nbatches);
+        if (first_batch + nbatches > s->next_batch) s->next_batch = first_batch + nbatches;
+        if (accepted_in_range) *accepted_in_range = s->accepted - before;
+    });
+}
+
+int hsaw_gpu_stream_size(const hsaw_gpu_stream* s, uint64_t* accepted, uint64_t* batches,
+                         uint64_t* total_edges) {
+    if (!s) return HSAW_EINVAL;
+    if (accepted) *accepted = s->accepted;
+    if (batches) *batches = s->local_batches;
+    if (total_edges) *total_edges = s->total_edges;
+    return HSAW_OK;
+}
+
+int hsaw_gpu_stream_counters(const hsaw_gpu_stream* s, uint64_t min_accepted, uint64_t* attempts,
+                             uint64_t* accepted) {
+    if (!s || !attempts || !accepted) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        if (min_accepted == 0) {  // sampler.cpp:474
+            *attempts = 0;
+            *accepted = 0;
+            return;
+        }
+        uint64_t idx = 0, val = 0;
+        local_cut(s, min_accepted, &idx, &val);
+        if (idx >= s->local_batches)
+            fail(HSAW_ERANGE, "sample stream target not materialized");  // sampler.cpp:477-478
+        *attempts = (idx + 1) * s->cfg.batch_size;
+        *accepted = val;
+    });
+}
+
+int hsaw_gpu_stream_local_cut(const hsaw_gpu_stream* s, uint64_t min_local, uint64_t* nbatches,
+                              uint64_t* accepted) {
+    if (!s || !nbatches || !accepted) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        if (min_local == 0) {
+            *nbatches = 0;
+            *accepted = 0;
+            return;
+        }
+        uint64_t idx = 0, val = 0;
+        local_cut(s, min_local, &idx, &val);
+        if (idx >= s->local_batches) fail(HSAW_ERANGE, "local cut beyond materialised batches");
+        *nbatches = idx + 1;
+        *accepted = val;
+    });
+}
+
+int hsaw_gpu_stream_slice_edges(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
+                                uint64_t* total_edges) {
+    if (!s || !total_edges) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        if (off + cnt > s->accepted)
+            fail(HSAW_ERANGE, "sample stream prefix not materialized");  // sampler.cpp:467-468
+        uint64_t eo[2] = {0, 0};
+        HSAW_CUDA_CHECK(cudaMemcpy(&eo[0], s->edge_off.p + off, 8, cudaMemcpyDeviceToHost));
+        HSAW_CUDA_CHECK(cudaMemcpy(&eo[1], s->edge_off.p + off + cnt, 8, cudaMemcpyDeviceToHost));
+        *total_edges = eo[1] - eo[0];
+    });
+}
+
+int hsaw_gpu_stream_export(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
+                           uint64_t* edge_off, uint32_t* nodes, uint32_t* edges,
+                           uint64_t* tag_worker, uint32_t* tag_seq) {
+    if (!s || !edge_off) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        if (off + cnt > s->accepted)
+            fail(HSAW_ERANGE, "sample stream prefix not materialized");
+        cudaStream_t st = s->ctx->stream;
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(edge_off, s->edge_off.p + off, (cnt + 1) * 8,
+                                        cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        uint64_t e0 = edge_off[0], e1 = edge_off[cnt];
+        if (nodes && (e1 - e0 + cnt))
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(nodes, s->nodes.p + e0 + off, (e1 - e0 + cnt) * 4,
+                                            cudaMemcpyDeviceToHost, st));
+        if (edges && e1 > e0)
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(edges, s->edges.p + e0, (e1 - e0) * 4,
+                                            cudaMemcpyDeviceToHost, st));
+        if (tag_worker && cnt)
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(tag_worker, s->tag_batch.p + off, cnt * 8,
+                                            cudaMemcpyDeviceToHost, st));
+        if (tag_seq && cnt)
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(tag_seq, s->tag_seq.p + off, cnt * 4,
+                                            cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (uint64_t i = 0; i <= cnt; ++i) edge_off[i] -= e0;
+        if (tag_worker)
+            for (uint64_t i = 0; i < cnt; ++i) tag_worker[i] += s->seed;  // worker id = seed + batch
+    });
+}
+
+int hsaw_gpu_stream_stats(const hsaw_gpu_stream* s, uint64_t* stats) {
+    if (!s || !stats) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        HSAW_CUDA_CHECK(cudaMemcpy(stats, s->stats.p, 64, cudaMemcpyDeviceToHost));
+        stats[hsawgpu::ST_DROPPED] = s->dropped;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// Device-resident SampleStream (proj/src/sampler.cpp:383-501): decoded walks in deterministic
+// (batch, seq) order in one dense pool, plus the per-batch cumulative accepted counts that
+// counters_for needs.
+#pragma once
+
+#include "common.cuh"
+
+struct hsaw_gpu_stream {
+    hsaw_gpu_ctx* ctx = nullptr;
+    uint64_t seed = 0;
+    hsaw_sampler_cfg cfg{};
+
+    // pool: walk w has edges [edge_off[w], edge_off[w+1]) and nodes
+    // [edge_off[w] + w, edge_off[w+1] + w + 1)  (len + 1 nodes per walk, no padding)
+    hsawgpu::DevVec<uint64_t> edge_off;  // accepted + 1
+    hsawgpu::DevVec<uint32_t> nodes;     // total_edges + accepted
+    hsawgpu::DevVec<uint32_t> edges;     // total_edges
+    hsawgpu::DevVec<uint64_t> tag_batch; // global batch index of each walk (worker id = seed + it)
+    hsawgpu::DevVec<uint32_t> tag_seq;   // seq within the batch, assigned before decode drops
+    uint64_t accepted = 0, total_edges = 0;
+
+    // cumulative decoded count after each batch this stream ran, in the order it ran them
+    hsawgpu::DevVec<uint64_t> accepted_after_batch;
+    uint64_t local_batches = 0;
+    uint64_t next_batch = 0;   // next global batch for ensure()
+    uint64_t last_batch_end = 0;  // ranges must be increasing
+    uint64_t grow = 4096;      // first-round size while nothing has been accepted yet
+
+    hsawgpu::DevVec<uint64_t> stats;  // u64[8] + cursor scratch
+    uint64_t dropped = 0;             // walks removed by the exact recheck
+
+    // per-chunk scratch (reused)
+    hsawgpu::DevVec<uint64_t> slot_seed, enc_seed, tmp_off, voff;
+    hsawgpu::DevVec<uint32_t> slot_len, count, first, enc_len, enc_seq, tmp_nodes, tmp_edges, vidx;
+    hsawgpu::DevVec<uint64_t> enc_batch;
+    hsawgpu::DevVec<uint8_t> status;
+};

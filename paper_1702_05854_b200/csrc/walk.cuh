@@ -1,0 +1,126 @@
+// Device-side primitives of one HSAW walk step: the xorshift64* stream, the start-node draw, the
+// node-record load and the live in-edge pick with one-load verification. Shared by the encode
+// kernel (K1) and the decode kernel (K2) so that generation and replay cannot disagree.
+#pragma once
+
+#include "common.cuh"
+
+namespace hsawgpu {
+
+// xorshift64* step, proj/include/hsaw/prng.hpp:41-48. Returns the scrambled output.
+__device__ __forceinline__ uint64_t prg_next(uint64_t& s) {
+    uint64_t x = s;
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    s = x;
+    return x * 0x2545F4914F6CDD1DULL;
+}
+
+// One draw as the 53-bit integer k with u01 = k * 2^-53 (prng.hpp:51-53).
+__device__ __forceinline__ uint64_t draw53(uint64_t& s) { return prg_next(s) >> 11; }
+
+// splitmix step + zero skip, prng.hpp:29-38,65-72.
+__device__ __forceinline__ uint64_t seed_from_worker(uint64_t worker_id) {
+    uint64_t st = worker_id;
+    for (;;) {
+        uint64_t z = st + 0x9E3779B97F4A7C15ULL;
+        uint64_t o = z;
+        o ^= o >> 30;
+        o *= 0xBF58476D1CE4E5B9ULL;
+        o ^= o >> 27;
+        o *= 0x94D049BB133111EBULL;
+        o ^= o >> 31;
+        if (o != 0) return o;
+        st = z;
+    }
+}
+
+// pick_uniform_node, prng.hpp:57-61: floor(fl(u01 * (double)n)) clamped to n-1. The product is a
+// single IEEE round-to-nearest FP64 multiply on both sides (no FMA contraction possible).
+__device__ __forceinline__ uint32_t start_node(uint64_t k, uint32_t n) {
+    double r = __dmul_rn(__ull2double_rn(k), 0x1.0p-53);  // exact: k < 2^53
+    uint32_t v = __double2uint_rz(__dmul_rn(r, __uint2double_rn(n)));
+    return v < n ? v : n - 1;
+}
+
+// 256-bit read-only load of one node record (LDG.E.256 on sm_100a): one sector, one request.
+__device__ __forceinline__ NodeRec load_node(const NodeRec* __restrict__ nodes, uint32_t v) {
+    uint64_t a, b, c, d;
+    asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(nodes + v));
+    NodeRec r;
+    r.lo = (uint32_t)a;
+    r.deg = (uint32_t)(a >> 32);
+    r.tot_thr = b;
+    r.acc_thr = c;
+    r.scale = d;
+    return r;
+}
+
+__device__ __forceinline__ EdgeRec load_edge(const EdgeRec* __restrict__ edges, uint64_t e) {
+    uint64_t a, b;
+    asm volatile("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(edges + e));
+    EdgeRec r;
+    r.thr = a;
+    r.src = (uint32_t)b;
+    r.prev_hi = (uint32_t)(b >> 32);
+    return r;
+}
+
+__device__ __forceinline__ uint32_t ceil_log2(uint32_t d) {  // d >= 1
+    return d <= 1 ? 0u : 32u - __clz(d - 1);
+}
+
+// pick_live_in_edge (proj/include/hsaw/graph.hpp:61-80) for a draw k that already passed the
+// "no edge" test (deg > 0 and k < tot_thr). Returns the slot index within the row: the first i
+// with k < thr[lo+i] — identical to both the linear scan (:67-70) and the binary search (:72-78)
+// of the reference because rows are non-decreasing. Fast path: one record load at the
+// interpolation guess, verified against thr[g] and the packed top bits of thr[g-1]; anything the
+// single load cannot prove falls back to a binary search over the row.
+__device__ __forceinline__ uint32_t pick_slot(const EdgeRec* __restrict__ edges, uint32_t lo,
+                                              uint32_t deg, uint64_t scale, uint64_t k,
+                                              uint32_t& src_out) {
+    uint64_t gq = __umul64hi(k << 11, scale) >> 31;
+    uint32_t g = gq >= deg ? deg - 1 : (uint32_t)gq;
+    EdgeRec rec = load_edge(edges, (uint64_t)lo + g);
+    bool below = k < rec.thr;
+    bool above_prev = g == 0 || (uint32_t)(k >> 21) > rec.prev_hi;
+    if (below && above_prev) {
+        src_out = rec.src;
+        return g;
+    }
+    // slow path: exact first index with k < thr, restricted to the side the probe ruled in
+    // invariant: answer in [a, b] and k < thr[b] is known (thr[deg-1] == tot_thr > k)
+    uint32_t a, b;
+    if (below) {
+        a = 0;
+        b = g;
+    } else {
+        a = g + 1;
+        b = deg - 1;
+        if (a > b) a = b;  // unreachable for k < tot_thr; keeps the final load inside the row
+    }
+    while (a < b) {
+        uint32_t mid = a + (b - a) / 2;
+        EdgeRec pr = load_edge(edges, (uint64_t)lo + mid);
+        if (k < pr.thr)
+            b = mid;
+        else
+            a = mid + 1;
+    }
+    rec = load_edge(edges, (uint64_t)lo + a);
+    src_out = rec.src;
+    return a;
+}
+
+// Algorithmic bytes of one pick in the reference layout:
+// empty row 16; r >= total 24; success 28 + 8*ceil(log2 d). p_of (8) is added when resolve runs.
+__device__ __forceinline__ uint32_t pick_alg_bytes(uint32_t deg, bool success) {
+    if (deg == 0) return 16;
+    if (!success) return 24;
+    return 28 + 8 * ceil_log2(deg);
+}
+
+}  // namespace hsawgpu
