@@ -175,6 +175,23 @@ int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
 /* Number of kernel launches this context has issued since creation (bench.py "gpu_launches"). */
 uint64_t hsaw_gpu_launch_count(const hsaw_gpu_ctx* ctx);
 
+/* Device time per stage, measured with CUDA events recorded on the context stream directly around
+ * the stage's kernels (so it is the kernels' own duration, not the host call's). */
+enum {
+    HSAW_STAGE_ENCODE = 0,   /* K1 encode_kernel */
+    HSAW_STAGE_DECODE = 1,   /* K2 decode_kernel */
+    HSAW_STAGE_DISTINCT = 2, /* K2b exact self-avoidance recheck */
+    HSAW_STAGE_COMPACT = 3,  /* gather + scans + deterministic compaction */
+    HSAW_STAGE_INDEX = 4,    /* K3 histogram + inverted index */
+    HSAW_STAGE_ROUNDS = 5,   /* K4/K5 greedy rounds */
+    HSAW_STAGE_COVERAGE = 6, /* K6 coverage_of */
+    HSAW_STAGE_UPLOAD = 7,   /* graph transform kernels */
+    HSAW_STAGE_COUNT = 8
+};
+/* ms[HSAW_STAGE_COUNT] accumulated milliseconds, count[HSAW_STAGE_COUNT] timed regions (both
+ * nullable); reset != 0 zeroes the accumulators afterwards. Synchronises the stream. */
+int hsaw_gpu_stage_times(hsaw_gpu_ctx* ctx, double* ms, uint64_t* count, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,7 @@ f64p = C.POINTER(C.c_double)
 HSAW_OK, HSAW_EINVAL, HSAW_EDATA, HSAW_EBUDGET, HSAW_ERANGE, HSAW_ECUDA = range(6)
 KIND_EDGE, KIND_NODE = 0, 1
 
+STAGE_NAMES = ("encode", "decode", "distinct", "compact", "index", "rounds", "coverage", "upload")
 STAT_NAMES = ("attempts", "draws", "steps", "alg_bytes", "accepted", "decode_steps", "dropped",
               "spare")
 
@@ -76,6 +77,7 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_graph_bytes.restype = C.c_uint64
     L.hsaw_gpu_launch_count.argtypes = [vp]
     L.hsaw_gpu_launch_count.restype = C.c_uint64
+    L.hsaw_gpu_stage_times.argtypes = [vp, f64p, u64p, C.c_int]
     L.hsaw_gpu_encode_batches.argtypes = [vp, C.POINTER(SamplerCfg), C.c_uint64, C.c_uint64, u64p,
                                           u32p, u32p, u64p]
     L.hsaw_gpu_decode_walks.argtypes = [vp, C.c_uint64, u64p, u32p, u64p, u32p, u32p, u8p]
@@ -111,7 +113,7 @@ EXPORTS = (
     "hsaw_gpu_stream_counters", "hsaw_gpu_stream_local_cut", "hsaw_gpu_stream_slice_edges",
     "hsaw_gpu_stream_export", "hsaw_gpu_stream_stats", "hsaw_gpu_walkset_import",
     "hsaw_gpu_walkset_destroy", "hsaw_gpu_greedy", "hsaw_gpu_coverage_of",
-    "hsaw_gpu_launch_count",
+    "hsaw_gpu_launch_count", "hsaw_gpu_stage_times",
 )
 
 
@@ -175,6 +177,13 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self.L.hsaw_gpu_launch_count(self.h))
+
+    def stage_times(self, reset: bool = False) -> dict:
+        """{stage: (ms, timed regions)} measured with CUDA events around the kernels."""
+        ms = np.zeros(8, dtype=np.float64)
+        cnt = np.zeros(8, dtype=np.uint64)
+        self._chk(self.L.hsaw_gpu_stage_times(self.h, _p(ms, f64p), _p(cnt, u64p), int(reset)))
+        return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(STAGE_NAMES)}
 
     @property
     def graph_bytes(self) -> int:

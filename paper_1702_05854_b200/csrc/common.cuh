@@ -130,6 +130,15 @@ struct hsaw_gpu_ctx {
     hsawgpu::DevVec<uint64_t> g_pos, g_partial, g_gains;
     uint64_t* d_scalars = nullptr;  // 64 u64 of device scratch for counters / cursors
     uint64_t* h_scalars = nullptr;  // pinned mirror
+    // per-stage device time, measured with CUDA events on `stream` around the kernels themselves
+    struct Pending {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<cudaEvent_t> free_events;
+    std::vector<Pending> pending;
+    double stage_ms[HSAW_STAGE_COUNT] = {};
+    uint64_t stage_launches[HSAW_STAGE_COUNT] = {};
 };
 
 namespace hsawgpu {
@@ -157,6 +166,45 @@ inline void check_launch(hsaw_gpu_ctx* ctx, const char* what) {
     ++ctx->launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(HSAW_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- stage timing: tic/toc bracket kernels with events; collect() after a stream sync ----------
+struct StageScope {
+    hsaw_gpu_ctx* ctx;
+    int stage;
+    cudaEvent_t a = nullptr, b = nullptr;
+    static cudaEvent_t get(hsaw_gpu_ctx* c) {
+        if (!c->free_events.empty()) {
+            cudaEvent_t e = c->free_events.back();
+            c->free_events.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        HSAW_CUDA_CHECK(cudaEventCreate(&e));
+        return e;
+    }
+    StageScope(hsaw_gpu_ctx* c, int s) : ctx(c), stage(s) {
+        a = get(c);
+        b = get(c);
+        cudaEventRecord(a, c->stream);
+    }
+    ~StageScope() {
+        cudaEventRecord(b, ctx->stream);
+        ctx->pending.push_back({stage, a, b});
+        ++ctx->stage_launches[stage];
+    }
+};
+
+// Folds finished event pairs into ctx->stage_ms. Call after the stream has been synchronised.
+inline void collect_timings(hsaw_gpu_ctx* ctx) {
+    for (auto& p : ctx->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) ctx->stage_ms[p.stage] += ms;
+        ctx->free_events.push_back(p.a);
+        ctx->free_events.push_back(p.b);
+    }
+    ctx->pending.clear();
+    cudaGetLastError();
 }
 
 // exclusive prefix sums (CUB) on the context stream; out may have a wider type than in

@@ -175,6 +175,8 @@ void hsaw_gpu_ctx_destroy(hsaw_gpu_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    collect_timings(ctx);
+    for (cudaEvent_t e : ctx->free_events) cudaEventDestroy(e);
     free_graph(ctx);
     if (ctx->d_scalars) cudaFree(ctx->d_scalars);
     if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
@@ -196,6 +198,22 @@ int hsaw_gpu_ctx_sync(hsaw_gpu_ctx* ctx) {
 
 uint64_t hsaw_gpu_graph_bytes(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->graph_bytes : 0; }
 uint64_t hsaw_gpu_launch_count(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int hsaw_gpu_stage_times(hsaw_gpu_ctx* ctx, double* ms, uint64_t* count, int reset) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        collect_timings(ctx);
+        for (int i = 0; i < HSAW_STAGE_COUNT; ++i) {
+            if (ms) ms[i] = ctx->stage_ms[i];
+            if (count) count[i] = ctx->stage_launches[i];
+            if (reset) {
+                ctx->stage_ms[i] = 0;
+                ctx->stage_launches[i] = 0;
+            }
+        }
+    });
+}
 
 int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* in_offsets,
                           const uint32_t* in_src, const double* in_cum, const double* p_of) {
@@ -242,13 +260,17 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             }
             HSAW_CUDA_CHECK(cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_bad, 0xFF, 4, st));
-            build_node_records<<<(n + 255) / 256, 256, 0, st>>>(n, d_off, d_cum, d_p, ctx->g.nodes);
-            check_launch(ctx, "build_node_records");
-            if (m) {
-                int blocks = ctx->sm_count * 8;
-                build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, ctx->g.edges,
-                                                           d_bad);
-                check_launch(ctx, "build_edge_records");
+            {
+                StageScope timer(ctx, HSAW_STAGE_UPLOAD);
+                build_node_records<<<(n + 255) / 256, 256, 0, st>>>(n, d_off, d_cum, d_p,
+                                                                    ctx->g.nodes);
+                check_launch(ctx, "build_node_records");
+                if (m) {
+                    int blocks = ctx->sm_count * 8;
+                    build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum,
+                                                               ctx->g.edges, d_bad);
+                    check_launch(ctx, "build_edge_records");
+                }
             }
             uint32_t bad = 0;
             HSAW_CUDA_CHECK(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));

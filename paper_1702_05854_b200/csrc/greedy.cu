@@ -344,13 +344,16 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         uint64_t p0 = 0, p1 = 0;
         if (cnt) view_span(ctx, v, &p0, &p1);
         const int wide = ctx->sm_count * 8;
-        if (p1 > p0) {
-            int hb = (int)std::min<uint64_t>((p1 - p0 + 255) / 256, (uint64_t)wide);
-            item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt.p);
-            check_launch(ctx, "item_histogram");
+        {
+            StageScope timer(ctx, HSAW_STAGE_INDEX);
+            if (p1 > p0) {
+                int hb = (int)std::min<uint64_t>((p1 - p0 + 255) / 256, (uint64_t)wide);
+                item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt.p);
+                check_launch(ctx, "item_histogram");
+            }
+            // ---- K3b: inverted index by counting sort
+            exclusive_sum_u32_to_u64(ctx, d_cnt.p, d_pos.p, (uint64_t)limit + 1);
         }
-        // ---- K3b: inverted index by counting sort
-        exclusive_sum_u32_to_u64(ctx, d_cnt.p, d_pos.p, (uint64_t)limit + 1);
         uint64_t occurrences = 0;
         HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], d_pos.p + limit, 8,
                                         cudaMemcpyDeviceToHost, st));
@@ -359,6 +362,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         DevVec<uint32_t>& d_inv = ctx->g_inv;
         d_inv.ensure_scratch(occurrences + 1);
         if (occurrences) {
+            StageScope timer(ctx, HSAW_STAGE_INDEX);
             int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
             scatter_inverted<<<sb, 256, 0, st>>>(v, d_cand, d_pos.p, d_fill.p, d_inv.p);
             check_launch(ctx, "scatter_inverted");
@@ -383,13 +387,16 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         bool exhausted = occurrences == 0;
         while (done < k && !exhausted) {
             uint32_t group = std::min<uint32_t>(k - done, 64);
-            for (uint32_t r = done; r < done + group; ++r) {
-                argmax_partial<<<npartial, 256, 0, st>>>(d_cnt.p, limit, d_partial.p);
-                check_launch(ctx, "argmax_partial");
-                cover_winner<<<cover_blocks, 256, 0, st>>>(v, d_partial.p, npartial, d_cand,
-                                                           d_pos.p, d_inv.p, d_cnt.p, d_cov.p, r,
-                                                           d_sol.p, d_gain.p);
-                check_launch(ctx, "cover_winner");
+            {
+                StageScope timer(ctx, HSAW_STAGE_ROUNDS);
+                for (uint32_t r = done; r < done + group; ++r) {
+                    argmax_partial<<<npartial, 256, 0, st>>>(d_cnt.p, limit, d_partial.p);
+                    check_launch(ctx, "argmax_partial");
+                    cover_winner<<<cover_blocks, 256, 0, st>>>(v, d_partial.p, npartial, d_cand,
+                                                               d_pos.p, d_inv.p, d_cnt.p, d_cov.p,
+                                                               r, d_sol.p, d_gain.p);
+                    check_launch(ctx, "cover_winner");
+                }
             }
             HSAW_CUDA_CHECK(cudaMemcpyAsync(h_sol.data() + done, d_sol.p + done, group * 4ull,
                                             cudaMemcpyDeviceToHost, st));
@@ -405,6 +412,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             }
             if (!exhausted) done += group;
         }
+        collect_timings(ctx);
         // ---- zero-gain padding: smallest unselected candidates in ascending order
         // (proj/src/coverage.cpp:101-106,155; pinned by tests/test_coverage.cpp:58-64)
         uint64_t cov = 0;
@@ -477,14 +485,18 @@ int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         check_launch(ctx, "set_bits");
         unsigned long long* d_out = reinterpret_cast<unsigned long long*>(ctx->d_scalars + 8);
         HSAW_CUDA_CHECK(cudaMemsetAsync(d_out, 0, 8, st));
-        int blocks = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)ctx->sm_count * 8);
-        count_covered<<<blocks, 256, 0, st>>>(v, bits.p, d_out);
-        check_launch(ctx, "count_covered");
-        clear_bits<<<qb, 256, 0, st>>>(d_q.p, q.size(), bits.p);
-        check_launch(ctx, "clear_bits");
+        {
+            StageScope timer(ctx, HSAW_STAGE_COVERAGE);
+            int blocks = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)ctx->sm_count * 8);
+            count_covered<<<blocks, 256, 0, st>>>(v, bits.p, d_out);
+            check_launch(ctx, "count_covered");
+            clear_bits<<<qb, 256, 0, st>>>(d_q.p, q.size(), bits.p);
+            check_launch(ctx, "clear_bits");
+        }
         HSAW_CUDA_CHECK(
             cudaMemcpyAsync(&ctx->h_scalars[0], d_out, 8, cudaMemcpyDeviceToHost, st));
         HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        collect_timings(ctx);
         *coverage = ctx->h_scalars[0];
     });
 }

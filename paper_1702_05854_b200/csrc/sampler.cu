@@ -499,6 +499,7 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
     auto go = [&](auto kernel) {
         int blocks = persistent_blocks(ctx, kernel, nbatches);
+        StageScope timer(ctx, HSAW_STAGE_ENCODE);
         kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
         check_launch(ctx, "encode_kernel");
     };
@@ -520,6 +521,7 @@ static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_
                    d_nodes,      d_edges,      d_status, d_nnodes, d_stats, d_cursor};
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
     int blocks = persistent_blocks(ctx, decode_kernel, nwalks);
+    StageScope timer(ctx, HSAW_STAGE_DECODE);
     decode_kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
     check_launch(ctx, "decode_kernel");
 }
@@ -554,8 +556,11 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     uint64_t want = (nwalks + kCheckWarps - 1) / kCheckWarps;
     uint64_t full = (uint64_t)ctx->sm_count * 3;  // 64 KB of tables per block: 3 blocks / SM
     int blocks = (int)(want < full ? want : full);
-    distinct_kernel<<<blocks, kCheckWarps * 32, smem, ctx->stream>>>(p);
-    check_launch(ctx, "distinct_kernel");
+    {
+        StageScope timer(ctx, HSAW_STAGE_DISTINCT);
+        distinct_kernel<<<blocks, kCheckWarps * 32, smem, ctx->stream>>>(p);
+        check_launch(ctx, "distinct_kernel");
+    }
     uint32_t* h = reinterpret_cast<uint32_t*>(ctx->h_scalars + 32);
     HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 8, cudaMemcpyDeviceToHost, ctx->stream));
     HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -579,8 +584,11 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
         d_toff.ensure_scratch(nlong + 1);
         HSAW_CUDA_CHECK(cudaMemcpyAsync(d_toff.p, toff.data(), 8ull * (nlong + 1),
                                         cudaMemcpyHostToDevice, ctx->stream));
-        distinct_long_kernel<<<nlong, 256, 0, ctx->stream>>>(p, nlong, d_toff.p, tables.p);
-        check_launch(ctx, "distinct_long_kernel");
+        {
+            StageScope timer(ctx, HSAW_STAGE_DISTINCT);
+            distinct_long_kernel<<<nlong, 256, 0, ctx->stream>>>(p, nlong, d_toff.p, tables.p);
+            check_launch(ctx, "distinct_long_kernel");
+        }
         HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 8, cudaMemcpyDeviceToHost, ctx->stream));
         HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     }

@@ -152,12 +152,15 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
         s->enc_batch.ensure_scratch(E);
         s->enc_seq.ensure_scratch(E);
         s->tmp_off.ensure_scratch(E + 1);
-        gather_encoded<<<blocks_for(slots, 256), 256, 0, st>>>(
-            nb, l, first_batch, s->count.p, s->first.p, s->slot_seed.p, s->slot_len.p,
-            s->enc_seed.p, s->enc_len.p, s->enc_batch.p, s->enc_seq.p);
-        check_launch(ctx, "gather_encoded");
-        HSAW_CUDA_CHECK(cudaMemsetAsync(s->enc_len.p + E, 0, 4, st));
-        exclusive_sum_u32_to_u64(ctx, s->enc_len.p, s->tmp_off.p, E + 1);
+        {
+            StageScope timer(ctx, HSAW_STAGE_COMPACT);
+            gather_encoded<<<blocks_for(slots, 256), 256, 0, st>>>(
+                nb, l, first_batch, s->count.p, s->first.p, s->slot_seed.p, s->slot_len.p,
+                s->enc_seed.p, s->enc_len.p, s->enc_batch.p, s->enc_seq.p);
+            check_launch(ctx, "gather_encoded");
+            HSAW_CUDA_CHECK(cudaMemsetAsync(s->enc_len.p + E, 0, 4, st));
+            exclusive_sum_u32_to_u64(ctx, s->enc_len.p, s->tmp_off.p, E + 1);
+        }
         const uint64_t T = read_u64(ctx, s->tmp_off.p + E);  // edges of all encoded walks
 
         // ---- K2 + K2b
@@ -175,11 +178,14 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
         s->voff.ensure_scratch(E + 1);
         uint32_t* mismatch = reinterpret_cast<uint32_t*>(s->stats.p + 9);
         HSAW_CUDA_CHECK(cudaMemsetAsync(mismatch, 0, 4, st));
-        mark_valid<<<blocks_for(E + 1, 256), 256, 0, st>>>(E, s->status.p, s->enc_len.p, vflag,
-                                                           vlen, mismatch);
-        check_launch(ctx, "mark_valid");
-        exclusive_sum_u32(ctx, vflag, s->vidx.p, E + 1);
-        exclusive_sum_u32_to_u64(ctx, vlen, s->voff.p, E + 1);
+        {
+            StageScope timer(ctx, HSAW_STAGE_COMPACT);
+            mark_valid<<<blocks_for(E + 1, 256), 256, 0, st>>>(E, s->status.p, s->enc_len.p, vflag,
+                                                               vlen, mismatch);
+            check_launch(ctx, "mark_valid");
+            exclusive_sum_u32(ctx, vflag, s->vidx.p, E + 1);
+            exclusive_sum_u32_to_u64(ctx, vlen, s->voff.p, E + 1);
+        }
         HSAW_CUDA_CHECK(
             cudaMemcpyAsync(ctx->h_scalars + 1, s->voff.p + E, 8, cudaMemcpyDeviceToHost, st));
         HSAW_CUDA_CHECK(
@@ -196,11 +202,14 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
         s->tag_batch.reserve(s->accepted + A + 1, st);
         s->tag_seq.reserve(s->accepted + A + 1, st);
         int cblocks = (int)std::min<uint64_t>((E + 7) / 8, (uint64_t)ctx->sm_count * 16);
-        compact_walks<<<cblocks, 256, 0, st>>>(
-            E, vflag, s->vidx.p, s->voff.p, s->tmp_off.p, s->tmp_nodes.p, s->tmp_edges.p,
-            s->enc_len.p, s->enc_batch.p, s->enc_seq.p, s->accepted, s->total_edges,
-            s->edge_off.p, s->nodes.p, s->edges.p, s->tag_batch.p, s->tag_seq.p);
-        check_launch(ctx, "compact_walks");
+        {
+            StageScope timer(ctx, HSAW_STAGE_COMPACT);
+            compact_walks<<<cblocks, 256, 0, st>>>(
+                E, vflag, s->vidx.p, s->voff.p, s->tmp_off.p, s->tmp_nodes.p, s->tmp_edges.p,
+                s->enc_len.p, s->enc_batch.p, s->enc_seq.p, s->accepted, s->total_edges,
+                s->edge_off.p, s->nodes.p, s->edges.p, s->tag_batch.p, s->tag_seq.p);
+            check_launch(ctx, "compact_walks");
+        }
     } else {
         HSAW_CUDA_CHECK(cudaMemsetAsync(s->vidx.p, 0, 4, st));
         s->edge_off.reserve(s->accepted + 1, st);
@@ -223,6 +232,7 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
                                         nb * 8, cudaMemcpyHostToDevice, st));
     }
     HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+    collect_timings(ctx);
 
     s->accepted += A;
     s->total_edges += VT;
