@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py — HSAWs/sec (and eSIA seconds-to-solution) of the B200 HSAW path.
+
+Contract: `python bench.py --gpus N --steps K --warmup W [--impl reference]` prints ONE JSON line.
+
+Workload at N=1 = BASELINE.json configs[1] ("C2"): R-MAT scale 20 (2^20 nodes, ~16.1 M edges after
+dedupe), LT weights 1/in-degree, 1 % suspects with p ~ U(0,1), stream seed 42, the reference's
+default sampler (Brent + window 2, 10 chained attempts per batch).
+A *step* = one pass of the sampling hot path over one batch range: 2^20 batches (10.49 M attempts)
+are generated (K1), replayed (K2), exactly rechecked (K2b) and compacted into the device-resident
+pool in the reference's (batch, seq) order. `value` = accepted (post-recheck) HSAWs per second over
+the K timed steps with the graph already resident in HBM. `e2e` = the same metric through the
+reference-facing host call with HOST buffers (graph arrays uploaded inside the timed region, result
+counters read back). The eSIA k=100 seconds-to-solution of the same config rides along in "esia".
+With --gpus N>1 (torchrun) the graph is replicated, every rank samples its own batch ranges (weak
+scaling, no data-path collective) and the rates are summed over ranks / max over ranks' time.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref: the unmodified
+/root/reference sources compiled by oracle/Makefile; the C restatement if that is absent) on the
+host cores with all hardware threads, on the same graph, metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "hsaw_per_sec"
+UNIT = "HSAW/s"
+STREAM_SEED = 42
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--scale", type=int, default=20, help="R-MAT scale (2^scale nodes)")
+    ap.add_argument("--edge-factor", type=float, default=16.0)
+    ap.add_argument("--batches", type=int, default=1 << 20, help="batches per step per GPU")
+    ap.add_argument("--esia-k", type=int, default=100)
+    ap.add_argument("--no-esia", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-target", type=int, default=300_000,
+                    help="HSAWs of the bounded CPU sample (cpu_baseline / reference arm step)")
+    return ap.parse_args()
+
+
+def workload_name(args, n, m):
+    return (f"C2 R-MAT scale {args.scale} ({n} nodes, {m} edges after dedupe), LT weights "
+            f"1/in-degree, {max(1, n // 100)} suspects p~U(0,1), stream seed {STREAM_SEED}, "
+            f"Brent+window(2), 10 attempts/batch")
+
+
+def make_inputs(args):
+    """The same CSR arrays go to the GPU path and to the CPU reference."""
+    from paper_1702_05854_b200 import hostapi
+    g = hostapi.Graph.rmat(args.scale, args.edge_factor, seed=1)
+    p_of = g.random_suspects(max(1, g.n // 100), seed=2)
+    return g, p_of
+
+
+class ClockSampler(threading.Thread):
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        super().__init__(daemon=True)
+        self.index, self.rows, self._halt = index, [], threading.Event()
+
+    def run(self):
+        while not self._halt.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._halt.wait(0.2)
+
+    def stop(self) -> dict:
+        self._halt.set()
+        self.join(timeout=6)
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows if len(r) >= 8
+                          for n, v in zip(names, r[4:8]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md, 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per K1 launch from the committed ncu capture, if one exists for this workload."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def cpu_reference_rate(args, g, p_of, target, seed, workers):
+    """Reference CPU stream_samples on the host cores -> (HSAW/s, accepted, attempts, kind)."""
+    from oracle import oracle
+    from oracle.oracle import Csr
+    off, src, cum, _, _ = g.arrays()
+    csr = Csr(g.n, g.m, off, src, cum, p_of)
+    if oracle.have_ref():
+        R = oracle.Ref()
+        with R.handles(csr) as hd:
+            t0 = time.perf_counter()
+            ns, at, _ = R.stream_samples(csr, target, seed=seed, workers=workers,
+                                         max_attempts=10**12, hd=hd, copy=False)
+            dt = time.perf_counter() - t0
+        return ns / dt, ns, at, "reference", workers, dt
+    P = oracle.Port()
+    t0 = time.perf_counter()
+    pool = P.stream_samples(csr, target, seed=seed, max_attempts=10**12)
+    dt = time.perf_counter() - t0
+    return pool.nsamples / dt, pool.nsamples, pool.attempts, "port", 1, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    g, p_of = make_inputs(args)
+    cores = os.cpu_count() or 1
+    total, elapsed, kind, used = 0, 0.0, "reference", cores
+    for step in range(args.warmup + args.steps):
+        rate, ns, at, kind, used, dt = cpu_reference_rate(args, g, p_of, args.cpu_target,
+                                                          STREAM_SEED + step, cores)
+        if step >= args.warmup:
+            total += ns
+            elapsed += dt
+    value = total / elapsed if elapsed > 0 else 0.0
+    sample = (f"each step: stream_samples to {args.cpu_target} HSAWs (fresh stream seed "
+              f"{STREAM_SEED}+step) with {used} worker threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * elapsed / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
+        "config": {"workload": workload_name(args, g.n, g.m), "step": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }))
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1702_05854_b200 import capi, hostapi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device — the HSAW path has no CPU fallback")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    g, p_of = make_inputs(args)  # identical on every rank (seeded generator): replicated graph
+    off, src, cum, _, _ = g.arrays()
+    ref_bytes = 8 * (g.n + 1) + 12 * g.m + 8 * g.n
+
+    tstream = torch.cuda.Stream()
+    dg = hostapi.DeviceGraph(g, p_of, device=local, cuda_stream=tstream.cuda_stream)
+    ctx = capi.Context.borrow(dg.ctx_handle(), g.n, g.m)
+    cfg = capi.SamplerCfg(max_attempts=10**15)
+    B = args.batches
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    stream = ctx.stream(seed=STREAM_SEED, cfg=cfg)
+    step_index = [0]
+
+    def one_step():
+        # weak scaling: global batch ranges are dealt round-robin to the ranks, each rank's
+        # ranges stay increasing; no collective on the data path
+        first = (step_index[0] * world + rank) * B
+        step_index[0] += 1
+        return stream.sample_range(first, B)
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    ctx.stage_times(reset=True)
+    stats0 = stream.stats()
+    launches0 = ctx.launches
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    accepted = 0
+    with torch.cuda.stream(tstream):
+        ev0.record(tstream)
+        for _ in range(args.steps):
+            accepted += one_step()
+        ev1.record(tstream)
+    barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    clock_info = clocks.stop()
+    stages = ctx.stage_times(reset=True)
+    stats1 = stream.stats()
+    launches = ctx.launches - launches0
+    delta = {k: stats1[k] - stats0[k] for k in stats1}
+
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    c = torch.tensor([accepted, delta["attempts"], delta["steps"] + delta["decode_steps"],
+                      launches], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    elapsed_ms = float(t.item())
+    tot_acc, tot_att, tot_steps, tot_launches = (float(x) for x in c.tolist())
+    value = tot_acc / (elapsed_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (K1 encode), rank 0's launches
+    peak, peak_src = measured_peak()
+    k1_ms, k1_n = stages["encode"]
+    alg_bytes_per_launch = delta["alg_bytes"] / max(k1_n, 1)
+    k1_avg_ms = k1_ms / max(k1_n, 1)
+    achieved = alg_bytes_per_launch / (k1_avg_ms / 1e3) / 1e9 if k1_avg_ms > 0 else 0.0
+    traffic = ncu_traffic()
+    roofline = {
+        "bound": "hbm", "kernel": "encode_kernel<Brent,2> (K1)", "achieved": achieved,
+        "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
+        "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+        "peak_source": peak_src,
+        "algorithmic_bytes_per_launch": alg_bytes_per_launch,
+        "bytes_per_step_formula": "28+8*ceil(log2 d) per successful pick (16 empty row, 24 no "
+                                  "live edge) + 8 per node arrival (SURVEY.md 8d)",
+        "kernel_avg_ms": k1_avg_ms, "launches_timed": k1_n,
+        "k1_walk_steps_per_s": delta["steps"] / (k1_ms / 1e3) if k1_ms > 0 else None,
+        "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
+        "k1_share_of_step": k1_ms / elapsed_ms if elapsed_ms > 0 else None,
+    }
+    stream.close()
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64",
+        "data": "synthetic",
+        "config": {
+            "workload": workload_name(args, g.n, g.m),
+            "step": f"{B} batches ({10 * B} attempts) per GPU: K1 encode + K2 decode + K2b exact "
+                    f"recheck + ordered compaction into the device pool",
+            "parallelism": f"walks sharded by batch range over {world} GPU(s), graph replicated",
+            "l2_policy": f"inputs larger than L2: {hsaw_mb(dg)} MB of node/edge records are "
+                         f"walked at random and every step uses fresh batches",
+            "graph_device_bytes": ctx.graph_bytes, "graph_reference_bytes": ref_bytes,
+        },
+        "attempts_per_sec": tot_att / (elapsed_ms / 1e3),
+        "walk_steps_per_sec": tot_steps / (elapsed_ms / 1e3),
+        "accept_rate": tot_acc / tot_att if tot_att else None,
+        "roofline": roofline, "clocks": clock_info, "gpu_launches": int(tot_launches),
+    }
+
+    # ---- end to end through the reference-facing host call, HOST buffers (rank 0's GPU only
+    # times its own share; ranks run the same call concurrently and the rates are summed)
+    target = max(1, int(accepted / max(args.steps, 1)))
+    e2e_acc, e2e_s = 0, 0.0
+    for i in range(max(1, min(args.steps, 5))):
+        barrier()
+        t0 = time.perf_counter()
+        with hostapi.DeviceGraph(g, p_of, device=local) as dg2:        # H2D of the CSR arrays
+            _, acc = dg2.sample(target, seed=STREAM_SEED + 1000 * rank + i,
+                                max_attempts=10**15)                   # ensure + counters (D2H)
+        torch.cuda.synchronize()
+        e2e_s += time.perf_counter() - t0
+        e2e_acc += acc
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    ce = torch.tensor([float(e2e_acc)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ce, op=dist.ReduceOp.SUM)
+    out["e2e"] = {
+        "value": float(ce.item()) / float(te.item()), "unit": UNIT,
+        "h2d_bytes_per_step": ref_bytes, "d2h_bytes_per_step": 16,
+        "call": f"DeviceGraph(g, vi) upload + SampleStream.ensure({target}) + counters_for "
+                f"(the `hsaw sample` path), per call",
+    }
+
+    # ---- eSIA seconds-to-solution on the same config (single GPU path)
+    if not args.no_esia and world == 1:
+        delta_ = 1.0 / g.n
+        r_dev = hostapi.interdict(g, p_of, 0, args.esia_k, 0.1, delta_, seed=STREAM_SEED,
+                                  max_attempts=10**15, dg=dg, want_json=True)
+        r_e2e = hostapi.interdict(g, p_of, 0, args.esia_k, 0.1, delta_, seed=STREAM_SEED,
+                                  max_attempts=10**15, device=local, want_json=True)
+        out["esia"] = {
+            "k": args.esia_k, "epsilon": 0.1, "delta": delta_,
+            "seconds_to_solution": r_dev["timing"]["wall_time_s"],
+            "seconds_to_solution_e2e": r_e2e["timing"]["wall_time_s"],
+            "breakdown_s": {k: r_dev["timing"][k] for k in ("sample_s", "greedy_s", "check_s")},
+            "iterations": r_dev["iterations"], "samples_used": r_dev["samples_used"],
+            "attempts": r_dev["attempts"], "coverage": r_dev["coverage"],
+            "passed_check": r_dev["passed_check"], "est_suspension": r_dev["est_suspension"],
+            "solution_head": r_dev["solution"][:5],
+            "same_result_e2e": all(r_dev[k] == r_e2e[k] for k in ("solution", "attempts", "coverage")),
+        }
+
+    # ---- CPU baseline beside it: rank 0, N=1 only, bounded sample
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        rate, ns, at, kind, used, dt = cpu_reference_rate(args, g, p_of, args.cpu_target,
+                                                          STREAM_SEED, cores)
+        out["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": used, "kind": kind,
+            "sample": f"stream_samples to {args.cpu_target} HSAWs on the same graph/suspects/seed "
+                      f"({ns} HSAWs, {at} attempts, {dt:.1f} s)",
+        }
+    elif rank == 0:
+        out["cpu_baseline"] = None
+    dg.close()
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def hsaw_mb(dg):
+    from paper_1702_05854_b200 import capi
+    return round(int(capi.lib().hsaw_gpu_graph_bytes(dg.ctx_handle())) / 1e6, 1)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

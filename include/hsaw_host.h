@@ -1,0 +1,89 @@
+/*
+ * hsaw_host.h — C view of the C++ host layer (paper_1702_05854_b200/host/hsaw_b200.hpp).
+ *
+ * The host layer is C++ (namespace hsaw, same entry points as the reference's
+ * /root/reference/proj/include/hsaw headers). These wrappers exist so that ctypes-based tests and
+ * bench.py can drive it; they add no behaviour. Status codes as in hsaw_gpu.h: 0 ok, 1
+ * std::invalid_argument, 2 hsaw::DataError, 3 hsaw::SamplingError, 4 std::out_of_range, 5 device.
+ */
+#ifndef HSAW_HOST_H
+#define HSAW_HOST_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* hsawh_last_error(void);
+
+/* ---- graphs (hsaw::ProbGraph handles) — proj/include/hsaw/graph.hpp:123-141 ---- */
+int hsawh_graph_load_edge_list(const char* path, int weight_mode, uint64_t seed, int symmetrize,
+                               const char* mapping_out, void** out);
+int hsawh_graph_build(uint32_t n, uint64_t nedges, const uint32_t* u, const uint32_t* v,
+                      const double* w, int weight_mode, uint64_t seed, void** out);
+int hsawh_graph_synth(uint32_t n, uint32_t density, uint64_t seed, void** out);
+int hsawh_graph_rmat(uint32_t scale, double edge_factor, uint64_t seed, void** out);
+int hsawh_graph_from_csr(uint32_t n, uint32_t m, const uint64_t* in_offsets,
+                         const uint32_t* in_src, const double* in_cum, void** out);
+int hsawh_graph_save_cache(const void* g, const char* path);
+int hsawh_graph_load_cache(const char* path, void** out);
+int hsawh_graph_save_edge_list(const void* g, const char* path);
+int hsawh_graph_validate(const void* g);
+void hsawh_graph_dims(const void* g, uint32_t* n, uint32_t* m);
+/* any pointer may be NULL */
+void hsawh_graph_copy(const void* g, uint64_t* in_offsets, uint32_t* in_src, double* in_cum,
+                      double* weight, uint32_t* edge_dst);
+void hsawh_graph_free(void* g);
+
+/* ---- suspects: dense p_of[n] out — graph.hpp:129-132 ---- */
+int hsawh_suspects_random(const void* g, uint32_t count, uint64_t seed, double* p_of);
+int hsawh_suspects_load(const char* path, const void* g, double* p_of);
+
+/* ---- schedule / stopping rule — proj/include/hsaw/coverage.hpp:61-92 ---- */
+/* out4 = {n_max, lambda, lambda1, (double)lambda_samples} */
+int hsawh_schedule(uint64_t M, uint32_t k, double eps, double delta, double* out4,
+                   uint32_t* t_max);
+int hsawh_check(double cov_r, double cov_rp, double n_rp, uint64_t M, uint32_t k, double eps,
+                double delta, uint32_t t, int* pass, double* eps_t);
+
+/* ---- device graph (hsaw::DeviceGraph) ---- */
+int hsawh_device_create(const void* g, const double* p_of, int device, void* cuda_stream,
+                        void** out);
+void hsawh_device_free(void* dg);
+void* hsawh_device_ctx(const void* dg); /* the hsaw_gpu_ctx* underneath */
+
+/* ---- eSIA / nSIA — proj/include/hsaw/interdiction.hpp:37-47 ---- */
+typedef struct hsawh_result {
+    uint32_t k, iterations;
+    uint64_t coverage, samples_used, attempts;
+    double est_suspension, wall_time_s, sample_s, greedy_s, check_s;
+    int32_t passed_check;
+} hsawh_result;
+/* dg NULL: upload inside the call (timed in wall_time_s). kind 0 = esia, 1 = nsia. cand NULL =
+ * all. json (nullable) receives to_json(result, false). */
+int hsawh_interdict(const void* dg, const void* g, const double* p_of, int kind,
+                    const uint32_t* cand, uint64_t ncand, uint32_t k, double eps, double delta,
+                    uint64_t seed, uint32_t batch_size, uint64_t max_attempts, int device,
+                    hsawh_result* out, uint32_t* solution, char* json, uint64_t json_cap);
+
+/* ---- `hsaw sample` equivalent: stream to `target`, return the counters — cli.cpp:267-290 ---- */
+int hsawh_sample(const void* dg, uint64_t target, uint64_t seed, uint64_t max_attempts,
+                 uint64_t* attempts, uint64_t* accepted);
+
+/* ---- reference-signature stream_samples with the pool copied out (drop-in check) ---- */
+int hsawh_stream_samples(const void* g, const double* p_of, uint64_t target, uint64_t seed,
+                         uint32_t batch_size, uint64_t max_attempts, void** pool_out);
+void hsawh_pool_stats(const void* pool, uint64_t* nsamples, uint64_t* attempts,
+                      uint64_t* total_edges);
+void hsawh_pool_copy(const void* pool, uint64_t* edge_off, uint32_t* nodes, uint32_t* edges,
+                     uint64_t* tag_worker, uint32_t* tag_seq);
+void hsawh_pool_free(void* pool);
+
+/* ---- CLI (proj/include/hsaw/cli.hpp) ---- */
+int hsawh_run_cli(int argc, const char** argv);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSAW_HOST_H */

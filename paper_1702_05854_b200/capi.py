@@ -152,10 +152,20 @@ class Context:
                                 "(this path has no CPU fallback)")
         self.n = self.m = 0
 
+    @classmethod
+    def borrow(cls, handle, n=0, m=0) -> "Context":
+        """Non-owning view of an existing hsaw_gpu_ctx* (e.g. the one inside a DeviceGraph)."""
+        self = cls.__new__(cls)
+        self.L = lib()
+        self.h = C.c_void_p(handle)
+        self.n, self.m = n, m
+        self._borrowed = True
+        return self
+
     def close(self):
-        if self.h:
+        if self.h and not getattr(self, "_borrowed", False):
             self.L.hsaw_gpu_ctx_destroy(self.h)
-            self.h = C.c_void_p()
+        self.h = C.c_void_p()
 
     def __enter__(self):
         return self

@@ -1,0 +1,264 @@
+// C wrappers over the C++ host layer (include/hsaw_host.h): handle marshalling and the
+// exception -> status mapping, nothing else.
+#include "hsaw_host.h"
+
+#include <cstring>
+#include <string>
+
+#include "hsaw_b200.hpp"
+
+using namespace hsaw;
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_error = e.what();
+        return 1;
+    } catch (const DataError& e) {
+        g_error = e.what();
+        return 2;
+    } catch (const SamplingError& e) {
+        g_error = e.what();
+        return 3;
+    } catch (const std::out_of_range& e) {
+        g_error = e.what();
+        return 4;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return 5;
+    }
+}
+
+const ProbGraph& G(const void* g) { return *static_cast<const ProbGraph*>(g); }
+
+SuspectSet dense_suspects(const ProbGraph& g, const double* p_of) {
+    std::vector<std::pair<NodeId, double>> mem;
+    for (NodeId v = 0; v < g.n; ++v)
+        if (p_of[v] != 0.0) mem.emplace_back(v, p_of[v]);
+    return SuspectSet::from_members(std::move(mem), g);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hsawh_last_error(void) { return g_error.c_str(); }
+
+int hsawh_graph_load_edge_list(const char* path, int weight_mode, uint64_t seed, int symmetrize,
+                               const char* mapping_out, void** out) {
+    return guarded([&] {
+        LoadOptions opts;
+        opts.symmetrize = symmetrize != 0;
+        if (mapping_out) opts.mapping_out = mapping_out;
+        *out = new ProbGraph(load_edge_list(path, static_cast<WeightMode>(weight_mode), seed, opts));
+    });
+}
+
+int hsawh_graph_build(uint32_t n, uint64_t nedges, const uint32_t* u, const uint32_t* v,
+                      const double* w, int weight_mode, uint64_t seed, void** out) {
+    return guarded([&] {
+        std::vector<std::tuple<NodeId, NodeId, double>> edges;
+        edges.reserve(nedges);
+        for (uint64_t i = 0; i < nedges; ++i) edges.emplace_back(u[i], v[i], w ? w[i] : 0.0);
+        *out = new ProbGraph(
+            build_graph(n, std::move(edges), static_cast<WeightMode>(weight_mode), seed));
+    });
+}
+
+int hsawh_graph_synth(uint32_t n, uint32_t density, uint64_t seed, void** out) {
+    return guarded([&] { *out = new ProbGraph(synth_graph(n, density, seed)); });
+}
+
+int hsawh_graph_rmat(uint32_t scale, double edge_factor, uint64_t seed, void** out) {
+    return guarded([&] { *out = new ProbGraph(rmat_graph(scale, edge_factor, seed)); });
+}
+
+int hsawh_graph_from_csr(uint32_t n, uint32_t m, const uint64_t* in_offsets,
+                         const uint32_t* in_src, const double* in_cum, void** out) {
+    return guarded([&] { *out = new ProbGraph(graph_from_csr(n, m, in_offsets, in_src, in_cum)); });
+}
+
+int hsawh_graph_save_cache(const void* g, const char* path) {
+    return guarded([&] { save_cache(G(g), path); });
+}
+int hsawh_graph_load_cache(const char* path, void** out) {
+    return guarded([&] { *out = new ProbGraph(load_cache(path)); });
+}
+int hsawh_graph_save_edge_list(const void* g, const char* path) {
+    return guarded([&] { save_edge_list(G(g), path); });
+}
+int hsawh_graph_validate(const void* g) {
+    return guarded([&] { G(g).validate(); });
+}
+
+void hsawh_graph_dims(const void* g, uint32_t* n, uint32_t* m) {
+    *n = G(g).n;
+    *m = G(g).m;
+}
+
+void hsawh_graph_copy(const void* gp, uint64_t* in_offsets, uint32_t* in_src, double* in_cum,
+                      double* weight, uint32_t* edge_dst) {
+    const ProbGraph& g = G(gp);
+    if (in_offsets) std::memcpy(in_offsets, g.in_offsets.data(), 8 * g.in_offsets.size());
+    if (in_src) std::memcpy(in_src, g.in_src.data(), 4 * g.in_src.size());
+    if (in_cum) std::memcpy(in_cum, g.in_cum.data(), 8 * g.in_cum.size());
+    if (weight) std::memcpy(weight, g.weight.data(), 8 * g.weight.size());
+    if (edge_dst) std::memcpy(edge_dst, g.edge_dst.data(), 4 * g.edge_dst.size());
+}
+
+void hsawh_graph_free(void* g) { delete static_cast<ProbGraph*>(g); }
+
+int hsawh_suspects_random(const void* g, uint32_t count, uint64_t seed, double* p_of) {
+    return guarded([&] {
+        SuspectSet vi = random_suspects(G(g), count, seed);
+        std::memcpy(p_of, vi.p_of.data(), 8 * vi.p_of.size());
+    });
+}
+
+int hsawh_suspects_load(const char* path, const void* g, double* p_of) {
+    return guarded([&] {
+        SuspectSet vi = load_suspects(path, G(g));
+        std::memcpy(p_of, vi.p_of.data(), 8 * vi.p_of.size());
+    });
+}
+
+int hsawh_schedule(uint64_t M, uint32_t k, double eps, double delta, double* out4,
+                   uint32_t* t_max) {
+    return guarded([&] {
+        Schedule s = compute_schedule_m(M, k, eps, delta);
+        out4[0] = s.n_max;
+        out4[1] = s.lambda;
+        out4[2] = s.lambda1;
+        out4[3] = static_cast<double>(s.lambda_samples());
+        *t_max = s.t_max;
+    });
+}
+
+int hsawh_check(double cov_r, double cov_rp, double n_rp, uint64_t M, uint32_t k, double eps,
+                double delta, uint32_t t, int* pass, double* eps_t) {
+    return guarded([&] {
+        CheckResult c = check_counts(cov_r, cov_rp, n_rp, compute_schedule_m(M, k, eps, delta), t);
+        *pass = c.pass ? 1 : 0;
+        *eps_t = c.eps_t;
+    });
+}
+
+int hsawh_device_create(const void* g, const double* p_of, int device, void* cuda_stream,
+                        void** out) {
+    return guarded([&] {
+        SuspectSet vi = dense_suspects(G(g), p_of);
+        *out = new DeviceGraph(G(g), vi, device, cuda_stream);
+    });
+}
+
+void hsawh_device_free(void* dg) { delete static_cast<DeviceGraph*>(dg); }
+
+void* hsawh_device_ctx(const void* dg) { return static_cast<const DeviceGraph*>(dg)->ctx(); }
+
+int hsawh_interdict(const void* dg, const void* g, const double* p_of, int kind,
+                    const uint32_t* cand, uint64_t ncand, uint32_t k, double eps, double delta,
+                    uint64_t seed, uint32_t batch_size, uint64_t max_attempts, int device,
+                    hsawh_result* out, uint32_t* solution, char* json, uint64_t json_cap) {
+    return guarded([&] {
+        const ItemKind ik = kind == 0 ? ItemKind::Edge : ItemKind::Node;
+        CandidateSet cs = cand ? CandidateSet::of(ik, std::vector<std::uint32_t>(cand, cand + ncand))
+                               : CandidateSet::all(ik);
+        InterdictionOptions opts;
+        opts.seed = seed;
+        opts.sampler.batch_size = batch_size;
+        opts.sampler.max_attempts = max_attempts;
+        opts.device = device;
+        InterdictionResult r;
+        if (dg) {
+            const auto& d = *static_cast<const DeviceGraph*>(dg);
+            r = kind == 0 ? esia(d, G(g), cs, k, eps, delta, opts)
+                          : nsia(d, G(g), cs, k, eps, delta, opts);
+        } else {
+            SuspectSet vi = dense_suspects(G(g), p_of);
+            r = kind == 0 ? esia(G(g), vi, cs, k, eps, delta, opts)
+                          : nsia(G(g), vi, cs, k, eps, delta, opts);
+        }
+        out->k = r.k;
+        out->iterations = r.iterations;
+        out->coverage = r.coverage;
+        out->samples_used = r.samples_used;
+        out->attempts = r.attempts;
+        out->est_suspension = r.est_suspension;
+        out->wall_time_s = r.wall_time_s;
+        out->sample_s = r.sample_s;
+        out->greedy_s = r.greedy_s;
+        out->check_s = r.check_s;
+        out->passed_check = r.passed_check ? 1 : 0;
+        std::memcpy(solution, r.solution.data(), 4 * r.solution.size());
+        if (json && json_cap) {
+            std::string j = to_json(r, false);
+            std::strncpy(json, j.c_str(), json_cap - 1);
+            json[json_cap - 1] = 0;
+        }
+    });
+}
+
+int hsawh_sample(const void* dg, uint64_t target, uint64_t seed, uint64_t max_attempts,
+                 uint64_t* attempts, uint64_t* accepted) {
+    return guarded([&] {
+        SamplerConfig cfg;
+        cfg.max_attempts = max_attempts;
+        SampleStream stream(*static_cast<const DeviceGraph*>(dg), seed, cfg);
+        stream.ensure(target);
+        auto c = stream.counters_for(target);
+        *attempts = c.attempts;
+        *accepted = c.accepted;
+    });
+}
+
+int hsawh_stream_samples(const void* g, const double* p_of, uint64_t target, uint64_t seed,
+                         uint32_t batch_size, uint64_t max_attempts, void** pool_out) {
+    return guarded([&] {
+        SuspectSet vi = dense_suspects(G(g), p_of);
+        SamplerConfig cfg;
+        cfg.batch_size = batch_size;
+        cfg.max_attempts = max_attempts;
+        *pool_out = new SamplePool(stream_samples(G(g), vi, 1, target, seed, cfg));
+    });
+}
+
+void hsawh_pool_stats(const void* pool, uint64_t* nsamples, uint64_t* attempts,
+                      uint64_t* total_edges) {
+    const auto& p = *static_cast<const SamplePool*>(pool);
+    *nsamples = p.samples.size();
+    *attempts = p.attempts;
+    uint64_t t = 0;
+    for (const auto& s : p.samples) t += s.edge_ids.size();
+    *total_edges = t;
+}
+
+void hsawh_pool_copy(const void* pool, uint64_t* edge_off, uint32_t* nodes, uint32_t* edges,
+                     uint64_t* tag_worker, uint32_t* tag_seq) {
+    const auto& p = *static_cast<const SamplePool*>(pool);
+    uint64_t eo = 0;
+    for (std::size_t w = 0; w < p.samples.size(); ++w) {
+        const auto& s = p.samples[w];
+        edge_off[w] = eo;
+        std::memcpy(nodes + eo + w, s.nodes.data(), 4 * s.nodes.size());
+        std::memcpy(edges + eo, s.edge_ids.data(), 4 * s.edge_ids.size());
+        eo += s.edge_ids.size();
+        if (tag_worker) tag_worker[w] = p.tags[w].worker_id;
+        if (tag_seq) tag_seq[w] = p.tags[w].seq;
+    }
+    edge_off[p.samples.size()] = eo;
+}
+
+void hsawh_pool_free(void* pool) { delete static_cast<SamplePool*>(pool); }
+
+int hsawh_run_cli(int argc, const char** argv) {
+    return run_cli(std::vector<std::string>(argv, argv + argc));
+}
+
+}  // extern "C"

@@ -1,0 +1,323 @@
+// `hsaw` command line on the device path: the subcommands and flags of the reference CLI that sit
+// on the hot path (interdict, sample, bench, synth — /root/reference/proj/src/cli.cpp:400-485), the
+// same JSON documents and the same exit codes (0 ok, 1 usage, 2 data, 3 runtime; cli.cpp:520-538).
+// The reference parses with CLI11 (not available here); this is a small flag parser with the same
+// spelling: `--name value` or `--name=value`. `--workers` is accepted and ignored (the GPU is the
+// worker pool); `--device N` is new. estimate / baseline / partition are outside the ported path.
+#include <chrono>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <set>
+#include <sstream>
+
+#include "hsaw_b200.hpp"
+
+namespace hsaw {
+
+namespace {
+
+struct UsageError : std::runtime_error {
+    explicit UsageError(const std::string& m) : std::runtime_error(m) {}
+};
+
+struct Flags {
+    std::map<std::string, std::string> values;
+    std::set<std::string> switches;
+
+    bool has(const std::string& name) const { return values.count(name) != 0; }
+    std::string str(const std::string& name, const std::string& dflt = "") const {
+        auto it = values.find(name);
+        return it == values.end() ? dflt : it->second;
+    }
+    std::uint64_t u64(const std::string& name, std::uint64_t dflt) const {
+        if (!has(name)) return dflt;
+        const std::string& v = values.at(name);
+        try {
+            std::size_t used = 0;
+            if (!v.empty() && v[0] == '-') throw UsageError("");
+            std::uint64_t x = std::stoull(v, &used);
+            if (used != v.size()) throw UsageError("");
+            return x;
+        } catch (...) {
+            throw UsageError("--" + name + ": expected a non-negative integer, got '" + v + "'");
+        }
+    }
+    double real(const std::string& name, double dflt) const {
+        if (!has(name)) return dflt;
+        const std::string& v = values.at(name);
+        try {
+            std::size_t used = 0;
+            double x = std::stod(v, &used);
+            if (used != v.size()) throw UsageError("");
+            return x;
+        } catch (...) {
+            throw UsageError("--" + name + ": expected a number, got '" + v + "'");
+        }
+    }
+    void require(const std::string& name) const {
+        if (!has(name)) throw UsageError("--" + name + " is required");
+    }
+};
+
+Flags parse_flags(const std::vector<std::string>& args, std::size_t from,
+                  const std::set<std::string>& valued, const std::set<std::string>& boolean) {
+    Flags f;
+    for (std::size_t i = from; i < args.size(); ++i) {
+        const std::string& a = args[i];
+        if (a.rfind("--", 0) != 0) throw UsageError("unexpected argument '" + a + "'");
+        std::string name = a.substr(2), value;
+        bool inline_value = false;
+        if (auto eq = name.find('='); eq != std::string::npos) {
+            value = name.substr(eq + 1);
+            name = name.substr(0, eq);
+            inline_value = true;
+        }
+        if (boolean.count(name)) {
+            f.switches.insert(name);
+            continue;
+        }
+        if (!valued.count(name)) throw UsageError("unknown option --" + name);
+        if (!inline_value) {
+            if (i + 1 >= args.size()) throw UsageError("--" + name + " needs a value");
+            value = args[++i];
+        }
+        f.values[name] = value;
+    }
+    return f;
+}
+
+WeightMode weight_mode(const std::string& w) {
+    if (w == "given") return WeightMode::Given;
+    if (w == "indegree") return WeightMode::InDegree;
+    if (w == "random-normalized") return WeightMode::RandomNormalized;
+    throw UsageError("--weights: expected given|indegree|random-normalized");
+}
+
+// GraphArgs::load, cli.cpp:38-48: binary caches load directly, else the edge list.
+ProbGraph load_graph(const Flags& f, std::uint64_t seed) {
+    const std::string path = f.str("graph");
+    {
+        std::ifstream probe(path, std::ios::binary);
+        char magic[5] = {};
+        if (probe.read(magic, 5) && std::string(magic, 5) == "HSAW1") return load_cache(path);
+    }
+    LoadOptions opts;
+    opts.symmetrize = f.switches.count("symmetrize") != 0;
+    return load_edge_list(path, weight_mode(f.str("weights", "indegree")), seed, opts);
+}
+
+SuspectSet load_suspect_args(const Flags& f, const ProbGraph& g, std::uint64_t seed) {
+    if (f.has("suspects")) return load_suspects(f.str("suspects"), g);
+    const std::uint64_t count = f.u64("random-suspects", 0);
+    if (count > 0) return random_suspects(g, static_cast<NodeId>(count), seed);
+    throw UsageError("one of --suspects or --random-suspects is required");
+}
+
+void emit(const std::string& text, const std::string& output) {
+    if (output.empty()) {
+        std::cout << text << '\n';
+        return;
+    }
+    std::ofstream f(output);
+    if (!f) throw DataError("cannot write output: " + output);
+    f << text << '\n';
+}
+
+// read_item_file, cli.cpp:95-136: one id per line, or "u v" naming an edge by its endpoints.
+std::vector<std::uint32_t> read_item_file(const std::string& path, ItemKind kind,
+                                          const ProbGraph& g) {
+    std::ifstream in(path);
+    if (!in) throw DataError("cannot open item file: " + path);
+    std::map<std::pair<NodeId, NodeId>, EdgeId> by_endpoints;
+    if (kind == ItemKind::Edge)
+        for (EdgeId e = 0; e < g.m; ++e) by_endpoints[g.endpoints(e)] = e;
+    std::vector<std::uint32_t> ids;
+    std::string line;
+    for (std::size_t lineno = 1; std::getline(in, line); ++lineno) {
+        std::istringstream row(line);
+        std::vector<std::uint64_t> nums;
+        for (std::uint64_t x; row >> x;) nums.push_back(x);
+        if (nums.empty()) continue;
+        if (nums.size() == 1) {
+            ids.push_back(static_cast<std::uint32_t>(nums[0]));
+        } else if (nums.size() == 2 && kind == ItemKind::Edge) {
+            auto it = by_endpoints.find({static_cast<NodeId>(nums[0]), static_cast<NodeId>(nums[1])});
+            if (it == by_endpoints.end())
+                throw DataError(path + ":" + std::to_string(lineno) + ": unknown edge " +
+                                std::to_string(nums[0]) + " -> " + std::to_string(nums[1]));
+            ids.push_back(it->second);
+        } else {
+            throw DataError(path + ":" + std::to_string(lineno) + ": malformed line");
+        }
+    }
+    return ids;
+}
+
+std::string json_real(double x) {
+    std::ostringstream s;
+    s.precision(17);
+    s << x;
+    return s.str();
+}
+
+const std::set<std::string> kGraphFlags = {"graph", "weights", "suspects", "random-suspects"};
+
+std::set<std::string> with(std::set<std::string> base, std::initializer_list<const char*> more) {
+    for (const char* m : more) base.insert(m);
+    return base;
+}
+
+int cmd_interdict(const Flags& f) {  // cli.cpp:138-160
+    f.require("graph");
+    f.require("k");
+    const std::uint64_t k = f.u64("k", 1);
+    if (k < 1) {
+        std::cerr << "error: --k must be at least 1\n";
+        return 1;
+    }
+    const std::uint64_t seed = f.u64("seed", 0);
+    ProbGraph g = load_graph(f, seed);
+    SuspectSet vi = load_suspect_args(f, g, seed);
+    const std::string mode = f.str("mode", "edge");
+    if (mode != "edge" && mode != "node") throw UsageError("--mode: expected edge|node");
+    const ItemKind kind = mode == "edge" ? ItemKind::Edge : ItemKind::Node;
+    CandidateSet cand = CandidateSet::all(kind);
+    const std::string cand_path = f.str("candidates", "all");
+    if (!cand_path.empty() && cand_path != "all")
+        cand = CandidateSet::of(kind, read_item_file(cand_path, kind, g));
+    InterdictionOptions opts;
+    opts.workers = static_cast<std::uint32_t>(f.u64("workers", 1));
+    opts.seed = seed;
+    opts.sampler.max_attempts = f.u64("max-attempts", 100'000'000);
+    opts.device = static_cast<int>(f.u64("device", 0));
+    const double eps = f.real("epsilon", 0.1), delta = f.real("delta", 0.1);
+    InterdictionResult res = kind == ItemKind::Edge
+                                 ? esia(g, vi, cand, static_cast<std::uint32_t>(k), eps, delta, opts)
+                                 : nsia(g, vi, cand, static_cast<std::uint32_t>(k), eps, delta, opts);
+    emit(to_json(res, f.switches.count("omit-timing") == 0), f.str("output"));
+    return 0;
+}
+
+int cmd_sample(const Flags& f) {  // cli.cpp:267-290
+    f.require("graph");
+    f.require("target");
+    const std::uint64_t seed = f.u64("seed", 0);
+    ProbGraph g = load_graph(f, seed);
+    SuspectSet vi = load_suspect_args(f, g, seed);
+    SamplerConfig cfg;
+    cfg.max_attempts = f.u64("max-attempts", 100'000'000);
+    const std::uint64_t target = f.u64("target", 0);
+    DeviceGraph dg(g, vi, static_cast<int>(f.u64("device", 0)));
+    SampleStream stream(dg, seed, cfg);
+    stream.ensure(target);
+    std::ostringstream j;
+    if (f.has("dump")) {  // only the dump needs the walks on the host
+        SamplePool pool = stream.to_pool(target);
+        std::ofstream df(f.str("dump"));
+        if (!df) throw DataError("cannot write dump: " + f.str("dump"));
+        dump_walks(pool, df);
+    }
+    const auto c = stream.counters_for(target);
+    if (c.attempts == 0) throw std::invalid_argument("estimate_influence: no attempts");
+    const double rate = static_cast<double>(c.accepted) / static_cast<double>(c.attempts);
+    j << "{\n  \"acceptance_rate\": " << json_real(rate) << ",\n  \"accepted\": " << c.accepted
+      << ",\n  \"attempts\": " << c.attempts << ",\n  \"est_influence\": "
+      << json_real(static_cast<double>(g.n) * static_cast<double>(c.accepted) /
+                   static_cast<double>(c.attempts))
+      << ",\n  \"target\": " << target << "\n}";
+    emit(j.str(), f.str("output"));
+    return 0;
+}
+
+int cmd_synth(const Flags& f) {  // cli.cpp:335-348
+    f.require("nodes");
+    const std::uint64_t seed = f.u64("seed", 0);
+    ProbGraph g = synth_graph(static_cast<NodeId>(f.u64("nodes", 0)),
+                              static_cast<std::uint32_t>(f.u64("density", 10)), seed);
+    if (f.has("out")) save_edge_list(g, f.str("out"));
+    if (f.has("cache")) save_cache(g, f.str("cache"));
+    std::cout << "{\n  \"edges\": " << g.m << ",\n  \"nodes\": " << g.n << ",\n  \"seed\": " << seed
+              << "\n}\n";
+    return 0;
+}
+
+int cmd_bench(const Flags& f) {  // cli.cpp:350-379, one device run instead of 1 / N workers
+    f.require("target");
+    const std::uint64_t seed = f.u64("seed", 0);
+    const std::uint64_t synth_nodes = f.u64("synth-nodes", 0);
+    ProbGraph g = synth_nodes > 0
+                      ? synth_graph(static_cast<NodeId>(synth_nodes),
+                                    static_cast<std::uint32_t>(f.u64("synth-density", 10)), seed)
+                      : (f.require("graph"), load_graph(f, seed));
+    SuspectSet vi = load_suspect_args(f, g, seed);
+    const std::uint64_t target = f.u64("target", 0);
+    DeviceGraph dg(g, vi, static_cast<int>(f.u64("device", 0)));
+    const auto t0 = std::chrono::steady_clock::now();
+    SampleStream stream(dg, seed);
+    stream.ensure(target);
+    const auto c = stream.counters_for(target);
+    const double secs =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::ostringstream j;
+    j << "{\n  \"edges\": " << g.m << ",\n  \"nodes\": " << g.n << ",\n  \"runs\": [\n    {\n"
+      << "      \"accepted\": " << c.accepted << ",\n      \"attempts\": " << c.attempts
+      << ",\n      \"attempts_per_sec\": " << json_real(static_cast<double>(c.attempts) / secs)
+      << ",\n      \"device\": " << f.u64("device", 0) << ",\n      \"seconds\": " << json_real(secs)
+      << "\n    }\n  ],\n  \"target\": " << target << "\n}";
+    emit(j.str(), f.str("output"));
+    return 0;
+}
+
+}  // namespace
+
+int run_cli(std::vector<std::string> args) {
+    try {
+        if (args.empty()) throw UsageError("a subcommand is required: interdict|sample|synth|bench");
+        const std::string& cmd = args[0];
+        if (cmd == "--help" || cmd == "-h") {
+            std::cout << "usage: hsaw interdict|sample|synth|bench [--flags]\n";
+            return 0;
+        }
+        if (cmd == "interdict")
+            return cmd_interdict(parse_flags(
+                args, 1,
+                with(kGraphFlags, {"mode", "k", "epsilon", "delta", "candidates", "workers", "seed",
+                                   "max-attempts", "output", "device"}),
+                {"symmetrize", "omit-timing"}));
+        if (cmd == "sample")
+            return cmd_sample(parse_flags(
+                args, 1,
+                with(kGraphFlags, {"target", "workers", "seed", "max-attempts", "dump", "output",
+                                   "device"}),
+                {"symmetrize"}));
+        if (cmd == "synth")
+            return cmd_synth(
+                parse_flags(args, 1, {"nodes", "density", "seed", "out", "cache"}, {}));
+        if (cmd == "bench")
+            return cmd_bench(parse_flags(
+                args, 1,
+                with(kGraphFlags, {"synth-nodes", "synth-density", "target", "workers", "seed",
+                                   "output", "device"}),
+                {}));
+        if (cmd == "estimate" || cmd == "baseline" || cmd == "partition")
+            throw UsageError("subcommand '" + cmd +
+                             "' is outside the device hot path (use the reference build)");
+        throw UsageError("unknown subcommand '" + cmd + "'");
+    } catch (const UsageError& e) {
+        std::cerr << "usage error: " << e.what() << '\n';
+        return 1;
+    } catch (const std::invalid_argument& e) {
+        std::cerr << "usage error: " << e.what() << '\n';
+        return 1;
+    } catch (const DataError& e) {
+        std::cerr << "data error: " << e.what() << '\n';
+        return 2;
+    } catch (const std::exception& e) {
+        std::cerr << "runtime error: " << e.what() << '\n';
+        return 3;
+    }
+}
+
+}  // namespace hsaw

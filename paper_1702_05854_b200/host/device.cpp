@@ -1,0 +1,313 @@
+// Device-backed halves of the reference interface: everything here forwards to the C-ABI of
+// include/hsaw_gpu.h and rethrows its status codes as the exception types the reference uses
+// (std::invalid_argument / DataError / SamplingError / std::out_of_range), so callers and the CLI
+// keep the reference's error behaviour (proj/src/cli.cpp:520-538).
+#include <algorithm>
+
+#include "hsaw_b200.hpp"
+#include "hsaw_gpu.h"
+
+namespace hsaw {
+
+namespace {
+
+void raise(int status, hsaw_gpu_ctx* ctx, const char* where) {
+    if (status == HSAW_OK) return;
+    std::string msg = std::string(where) + ": " + hsaw_gpu_last_error(ctx);
+    switch (status) {
+        case HSAW_EINVAL: throw std::invalid_argument(msg);
+        case HSAW_EDATA: throw DataError(msg);
+        case HSAW_EBUDGET: throw SamplingError(msg);
+        case HSAW_ERANGE: throw std::out_of_range(msg);
+        default: throw DeviceError(msg);
+    }
+}
+
+hsaw_sampler_cfg to_c(const SamplerConfig& cfg) {
+    hsaw_sampler_cfg c{};
+    c.heuristic = cfg.heuristic == CycleHeuristic::Brent   ? 0
+                  : cfg.heuristic == CycleHeuristic::Floyd ? 1
+                                                           : 2;
+    c.window = cfg.window;
+    c.batch_size = cfg.batch_size;
+    c.max_attempts = cfg.max_attempts;
+    return c;
+}
+
+// flat export -> vector<HsawSample>
+std::vector<HsawSample> unpack(std::uint64_t count, const std::vector<std::uint64_t>& edge_off,
+                               const std::vector<std::uint32_t>& nodes,
+                               const std::vector<std::uint32_t>& edges) {
+    std::vector<HsawSample> out(count);
+    for (std::uint64_t w = 0; w < count; ++w) {
+        const std::uint64_t a = edge_off[w], b = edge_off[w + 1];
+        out[w].nodes.assign(nodes.begin() + a + w, nodes.begin() + b + w + 1);
+        out[w].edge_ids.assign(edges.begin() + a, edges.begin() + b);
+    }
+    return out;
+}
+
+}  // namespace
+
+// ---- DeviceGraph --------------------------------------------------------------------------------
+DeviceGraph::DeviceGraph(const ProbGraph& g, const SuspectSet& vi, int device, void* cuda_stream)
+    : n_(g.n), m_(g.m) {
+    if (vi.p_of.size() != g.n) throw std::invalid_argument("suspect set does not match graph");
+    int rc = hsaw_gpu_ctx_create(device, cuda_stream, &ctx_);
+    if (rc != HSAW_OK)
+        throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");
+    rc = hsaw_gpu_graph_upload(ctx_, g.n, g.m, g.in_offsets.data(), g.in_src.data(),
+                               g.in_cum.data(), vi.p_of.data());
+    if (rc != HSAW_OK) {
+        std::string msg = hsaw_gpu_last_error(ctx_);
+        hsaw_gpu_ctx_destroy(ctx_);
+        ctx_ = nullptr;
+        if (rc == HSAW_EDATA) throw DataError(msg);
+        if (rc == HSAW_EINVAL) throw std::invalid_argument(msg);
+        throw DeviceError(msg);
+    }
+}
+
+DeviceGraph::~DeviceGraph() { hsaw_gpu_ctx_destroy(ctx_); }
+
+void DeviceGraph::set_suspects(const SuspectSet& vi) {
+    if (vi.p_of.size() != n_) throw std::invalid_argument("suspect set does not match graph");
+    raise(hsaw_gpu_suspects_upload(ctx_, vi.p_of.data()), ctx_, "set_suspects");
+}
+
+std::uint64_t DeviceGraph::device_bytes() const { return hsaw_gpu_graph_bytes(ctx_); }
+std::uint64_t DeviceGraph::launches() const { return hsaw_gpu_launch_count(ctx_); }
+
+std::vector<double> DeviceGraph::stage_ms(bool reset) const {
+    std::vector<double> ms(HSAW_STAGE_COUNT, 0.0);
+    raise(hsaw_gpu_stage_times(ctx_, ms.data(), nullptr, reset ? 1 : 0), ctx_, "stage_times");
+    return ms;
+}
+
+// ---- thread_sample / decode ---------------------------------------------------------------------
+std::vector<EncodedWalk> thread_sample(const DeviceGraph& dg, std::uint64_t worker_id,
+                                       std::uint32_t l, const SamplerConfig& cfg) {
+    SamplerConfig one = cfg;
+    one.batch_size = l;  // the batch length is the call's l, as in the reference signature
+    hsaw_sampler_cfg c = to_c(one);
+    std::vector<EncodedWalk> out;
+    if (l == 0) return out;
+    std::vector<std::uint64_t> seeds(l);
+    std::vector<std::uint32_t> lens(l);
+    std::uint32_t count = 0;
+    raise(hsaw_gpu_encode_batches(dg.ctx(), &c, worker_id, 1, seeds.data(), lens.data(), &count,
+                                  nullptr),
+          dg.ctx(), "thread_sample");
+    out.reserve(count);
+    for (std::uint32_t i = 0; i < count; ++i)
+        out.push_back(EncodedWalk{PrgState{seeds[i]}, lens[i], worker_id, i});
+    return out;
+}
+
+std::vector<EncodedWalk> thread_sample(const ProbGraph& g, const SuspectSet& vi,
+                                       std::uint64_t worker_id, std::uint32_t l,
+                                       const SamplerConfig& cfg) {
+    DeviceGraph dg(g, vi);
+    return thread_sample(dg, worker_id, l, cfg);
+}
+
+std::vector<std::optional<HsawSample>> DecodeContext::decode(std::span<const EncodedWalk> walks) {
+    const std::uint64_t nw = walks.size();
+    std::vector<std::optional<HsawSample>> out(nw);
+    if (nw == 0) return out;
+    std::vector<std::uint64_t> seeds(nw), edge_off(nw + 1, 0);
+    std::vector<std::uint32_t> lens(nw);
+    for (std::uint64_t w = 0; w < nw; ++w) {
+        seeds[w] = walks[w].seed.state;
+        lens[w] = walks[w].len;
+        edge_off[w + 1] = edge_off[w] + lens[w];
+    }
+    std::vector<std::uint32_t> nodes(edge_off[nw] + nw), edges(edge_off[nw] + 1);
+    std::vector<std::uint8_t> status(nw);
+    raise(hsaw_gpu_decode_walks(dg_.ctx(), nw, seeds.data(), lens.data(), edge_off.data(),
+                                nodes.data(), edges.data(), status.data()),
+          dg_.ctx(), "decode");
+    for (std::uint64_t w = 0; w < nw; ++w) {
+        if (status[w] == 2)  // proj/src/sampler.cpp:306-335
+            throw DataError("decode: replay disagrees with the encoded walk");
+        if (status[w] == 0) continue;  // cycle the generation heuristic missed
+        HsawSample s;
+        s.nodes.assign(nodes.begin() + edge_off[w] + w, nodes.begin() + edge_off[w + 1] + w + 1);
+        s.edge_ids.assign(edges.begin() + edge_off[w], edges.begin() + edge_off[w + 1]);
+        out[w] = std::move(s);
+    }
+    return out;
+}
+
+std::optional<HsawSample> DecodeContext::decode(const EncodedWalk& ew) {
+    return std::move(decode(std::span<const EncodedWalk>(&ew, 1))[0]);
+}
+
+// ---- SampleStream -------------------------------------------------------------------------------
+SampleStream::SampleStream(const DeviceGraph& dg, std::uint64_t seed, SamplerConfig cfg)
+    : dg_(dg) {
+    hsaw_sampler_cfg c = to_c(cfg);
+    raise(hsaw_gpu_stream_create(dg.ctx(), seed, &c, &s_), dg.ctx(), "SampleStream");
+}
+
+SampleStream::~SampleStream() { hsaw_gpu_stream_destroy(s_); }
+
+void SampleStream::ensure(std::uint64_t min_accepted) {
+    raise(hsaw_gpu_stream_ensure(s_, min_accepted), dg_.ctx(), "ensure");
+}
+
+std::uint64_t SampleStream::materialized() const {
+    std::uint64_t acc = 0;
+    raise(hsaw_gpu_stream_size(s_, &acc, nullptr, nullptr), dg_.ctx(), "stream_size");
+    return acc;
+}
+
+std::vector<std::uint64_t> SampleStream::stats() const {
+    std::vector<std::uint64_t> st(8, 0);
+    raise(hsaw_gpu_stream_stats(s_, st.data()), dg_.ctx(), "stream_stats");
+    return st;
+}
+
+std::vector<HsawSample> SampleStream::prefix(std::uint64_t offset, std::uint64_t count) const {
+    std::uint64_t total_edges = 0;
+    raise(hsaw_gpu_stream_slice_edges(s_, offset, count, &total_edges), dg_.ctx(), "prefix");
+    std::vector<std::uint64_t> edge_off(count + 1);
+    std::vector<std::uint32_t> nodes(total_edges + count + 1), edges(total_edges + 1);
+    raise(hsaw_gpu_stream_export(s_, offset, count, edge_off.data(), nodes.data(), edges.data(),
+                                 nullptr, nullptr),
+          dg_.ctx(), "prefix");
+    return unpack(count, edge_off, nodes, edges);
+}
+
+SampleStream::Counters SampleStream::counters_for(std::uint64_t min_accepted) const {
+    Counters c;
+    raise(hsaw_gpu_stream_counters(s_, min_accepted, &c.attempts, &c.accepted), dg_.ctx(),
+          "counters_for");
+    return c;
+}
+
+SamplePool SampleStream::to_pool(std::uint64_t min_accepted) const {
+    Counters c = counters_for(min_accepted);
+    SamplePool pool;
+    pool.attempts = c.attempts;
+    std::uint64_t total_edges = 0;
+    raise(hsaw_gpu_stream_slice_edges(s_, 0, c.accepted, &total_edges), dg_.ctx(), "to_pool");
+    std::vector<std::uint64_t> edge_off(c.accepted + 1), workers(c.accepted + 1);
+    std::vector<std::uint32_t> nodes(total_edges + c.accepted + 1), edges(total_edges + 1),
+        seqs(c.accepted + 1);
+    raise(hsaw_gpu_stream_export(s_, 0, c.accepted, edge_off.data(), nodes.data(), edges.data(),
+                                 workers.data(), seqs.data()),
+          dg_.ctx(), "to_pool");
+    pool.samples = unpack(c.accepted, edge_off, nodes, edges);
+    pool.tags.resize(c.accepted);
+    for (std::uint64_t w = 0; w < c.accepted; ++w) pool.tags[w] = WalkTag{workers[w], seqs[w]};
+    return pool;
+}
+
+SamplePool stream_samples(const DeviceGraph& dg, std::uint64_t target, std::uint64_t seed,
+                          const SamplerConfig& cfg) {
+    SampleStream stream(dg, seed, cfg);
+    stream.ensure(target);
+    return stream.to_pool(target);
+}
+
+SamplePool stream_samples(const ProbGraph& g, const SuspectSet& vi, std::uint32_t /*workers*/,
+                          std::uint64_t target, std::uint64_t seed, const SamplerConfig& cfg) {
+    DeviceGraph dg(g, vi);
+    return stream_samples(dg, target, seed, cfg);
+}
+
+double estimate_influence(const SamplePool& pool, NodeId n) {  // proj/src/sampler.cpp:503-508
+    if (pool.attempts == 0) throw std::invalid_argument("estimate_influence: no attempts");
+    return static_cast<double>(n) * static_cast<double>(pool.accepted()) /
+           static_cast<double>(pool.attempts);
+}
+
+void dump_walks(const SamplePool& pool, std::ostream& out) {  // "worker seq len v1 .. vl"
+    for (std::size_t i = 0; i < pool.samples.size(); ++i) {
+        out << pool.tags[i].worker_id << ' ' << pool.tags[i].seq << ' '
+            << pool.samples[i].edge_ids.size();
+        for (NodeId v : pool.samples[i].nodes) out << ' ' << v;
+        out << '\n';
+    }
+}
+
+// ---- CoverageIndex / greedy ---------------------------------------------------------------------
+namespace {
+
+std::uint64_t count_candidates(const CandidateSet& cand, std::uint32_t limit) {
+    if (!cand.ids) return limit;
+    std::vector<std::uint32_t> ids = *cand.ids;
+    for (std::uint32_t id : ids)
+        if (id >= limit)  // candidate_mask, proj/src/coverage.cpp:18-20
+            throw DataError("candidate id out of range: " + std::to_string(id));
+    std::sort(ids.begin(), ids.end());
+    return static_cast<std::uint64_t>(std::unique(ids.begin(), ids.end()) - ids.begin());
+}
+
+}  // namespace
+
+CoverageIndex::CoverageIndex(ItemKind kind, const SampleStream& stream, std::uint64_t offset,
+                             std::uint64_t count, const CandidateSet& cand, const ProbGraph& g)
+    : kind_(kind), ctx_(stream.device().ctx()), stream_(stream.handle()), offset_(offset),
+      count_(count), cand_(cand.ids) {
+    if (cand.kind != kind)  // proj/src/coverage.cpp:41-42
+        throw std::invalid_argument("candidate kind does not match index kind");
+    if (offset + count > stream.materialized())
+        throw std::out_of_range("sample stream prefix not materialized");
+    ncand_ = count_candidates(cand, kind == ItemKind::Edge ? g.m : g.n);
+}
+
+CoverageIndex::CoverageIndex(const DeviceGraph& dg,
+                             std::span<const std::vector<std::uint32_t>> item_sets,
+                             const CandidateSet& cand, const ProbGraph& g)
+    : kind_(cand.kind), ctx_(dg.ctx()), count_(item_sets.size()), cand_(cand.ids) {
+    const std::uint32_t limit = kind_ == ItemKind::Edge ? g.m : g.n;
+    ncand_ = count_candidates(cand, limit);
+    std::vector<std::uint64_t> off(item_sets.size() + 1, 0);
+    for (std::size_t i = 0; i < item_sets.size(); ++i) off[i + 1] = off[i] + item_sets[i].size();
+    std::vector<std::uint32_t> flat;
+    flat.reserve(off.back() + 1);
+    for (const auto& s : item_sets) flat.insert(flat.end(), s.begin(), s.end());
+    raise(hsaw_gpu_walkset_import(ctx_, limit, item_sets.size(), off.data(), flat.data(),
+                                  &walkset_),
+          ctx_, "CoverageIndex");
+}
+
+CoverageIndex::~CoverageIndex() { hsaw_gpu_walkset_destroy(walkset_); }
+
+std::uint64_t CoverageIndex::coverage_of(std::span<const std::uint32_t> items) const {
+    std::uint64_t cov = 0;
+    raise(hsaw_gpu_coverage_of(ctx_, stream_, walkset_,
+                               kind_ == ItemKind::Edge ? HSAW_KIND_EDGE : HSAW_KIND_NODE, offset_,
+                               count_, cand_ ? cand_->data() : nullptr, cand_ ? cand_->size() : 0,
+                               items.data(), items.size(), &cov),
+          ctx_, "coverage_of");
+    return cov;
+}
+
+struct GreedyAccess {
+    static GreedyResult run(const CoverageIndex& idx, std::uint32_t k) {
+        if (k > idx.ncand_)  // proj/src/coverage.cpp:93-94
+            throw std::invalid_argument("budget k exceeds candidate count");
+        GreedyResult res;
+        if (k == 0) return res;
+        res.solution.assign(k, 0);
+        // an explicit but empty candidate list must stay distinguishable from "all"
+        static const std::uint32_t none = 0;
+        const std::uint32_t* cand = idx.cand_ ? (idx.cand_->empty() ? &none : idx.cand_->data())
+                                              : nullptr;
+        raise(hsaw_gpu_greedy(idx.ctx_, idx.stream_, idx.walkset_,
+                              idx.kind_ == ItemKind::Edge ? HSAW_KIND_EDGE : HSAW_KIND_NODE,
+                              idx.offset_, idx.count_, cand, idx.cand_ ? idx.cand_->size() : 0, k,
+                              res.solution.data(), &res.coverage),
+              idx.ctx_, "greedy_max_cover");
+        return res;
+    }
+};
+
+GreedyResult greedy_max_cover(const CoverageIndex& idx, std::uint32_t k) {
+    return GreedyAccess::run(idx, k);
+}
+
+}  // namespace hsaw

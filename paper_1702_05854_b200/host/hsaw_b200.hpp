@@ -1,0 +1,354 @@
+// hsaw_b200.hpp — C++ host layer of the B200 HSAW path.
+//
+// Mirrors the public interface of the reference library (/root/reference/proj/include/hsaw/*.hpp)
+// for the eSIA/nSIA hot path — same names, argument meaning and error behaviour — so that code and
+// tests written against the reference read the same here. Everything that samples walks or runs
+// greedy max-cover executes on the GPU through the C-ABI in include/hsaw_gpu.h; loaders, the
+// sample-size schedule, the stopping rule and the doubling loop stay on the host, as north_star
+// item (4) asks. There is no CPU fallback: without a CUDA device the sampling entry points throw.
+//
+// Reference interface -> this header
+//   types.hpp        NodeId, EdgeId, ItemKind, DataError, SamplingError
+//   prng.hpp         PrgState, splitmix_next, prg_next, u01, pick_uniform_node, seed_from_worker
+//   graph.hpp        ProbGraph, SuspectSet, CandidateSet, WeightMode, LoadOptions, build_graph,
+//                    load_edge_list, load_suspects, random_suspects, synth_graph, save_edge_list,
+//                    save_cache, load_cache
+//   sampler.hpp      EncodedWalk, HsawSample, WalkTag, SamplePool, SamplerConfig, thread_sample,
+//                    DecodeContext, SampleStream, stream_samples, estimate_influence, dump_walks
+//   coverage.hpp     CoverageIndex, GreedyResult, greedy_max_cover, Schedule, ln_choose,
+//                    compute_schedule(_m), CheckResult, check_solution
+//   interdiction.hpp InterdictionResult, InterdictionOptions, esia, nsia, to_json
+//   cli.hpp          run_cli
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <ostream>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+struct hsaw_gpu_ctx;
+struct hsaw_gpu_stream;
+struct hsaw_gpu_walkset;
+
+namespace hsaw {
+
+// ---- types (proj/include/hsaw/types.hpp) --------------------------------------------------------
+using NodeId = std::uint32_t;
+using EdgeId = std::uint32_t;
+inline constexpr NodeId kInvalidNode = ~NodeId(0);
+
+enum class ItemKind { Edge, Node };
+inline const char* to_string(ItemKind k) { return k == ItemKind::Edge ? "edge" : "node"; }
+
+struct DataError : std::runtime_error {
+    explicit DataError(const std::string& m) : std::runtime_error(m) {}
+};
+struct SamplingError : std::runtime_error {
+    explicit SamplingError(const std::string& m) : std::runtime_error(m) {}
+};
+// Not in the reference: the device path failed (no GPU, CUDA error). Maps to CLI exit code 3.
+struct DeviceError : std::runtime_error {
+    explicit DeviceError(const std::string& m) : std::runtime_error(m) {}
+};
+
+// ---- prng (proj/include/hsaw/prng.hpp) — host copies used by the loaders and generators --------
+struct PrgState {
+    std::uint64_t state = 0x853C49E6748FEA9BULL;
+    friend bool operator==(const PrgState& a, const PrgState& b) { return a.state == b.state; }
+};
+struct SplitMixResult {
+    std::uint64_t state, output;
+};
+SplitMixResult splitmix_next(std::uint64_t state);
+std::uint64_t prg_next(PrgState& s);
+double u01(std::uint64_t output);
+NodeId pick_uniform_node(PrgState& s, NodeId n);
+PrgState seed_from_worker(std::uint64_t worker_id);
+
+// ---- graph (proj/include/hsaw/graph.hpp) --------------------------------------------------------
+struct ProbGraph {
+    NodeId n = 0;
+    EdgeId m = 0;
+    std::vector<std::uint64_t> in_offsets;  // n + 1
+    std::vector<NodeId> in_src;             // m, ascending per target
+    std::vector<double> in_cum;             // m, sequential per-row cumulative weights
+    std::vector<double> weight;             // m
+    std::vector<NodeId> edge_dst;           // m
+
+    std::pair<NodeId, NodeId> endpoints(EdgeId e) const { return {in_src[e], edge_dst[e]}; }
+    std::uint32_t in_degree(NodeId v) const {
+        return static_cast<std::uint32_t>(in_offsets[v + 1] - in_offsets[v]);
+    }
+    double total_in_weight(NodeId v) const {
+        return in_offsets[v + 1] > in_offsets[v] ? in_cum[in_offsets[v + 1] - 1] : 0.0;
+    }
+    void validate() const;  // throws DataError
+    std::vector<std::uint32_t> out_degrees() const;
+};
+
+struct SuspectSet {
+    std::vector<std::pair<NodeId, double>> members;  // sorted by node id
+    std::vector<double> p_of;                        // n, 0 = not a suspect
+    double p(NodeId v) const { return p_of[v]; }
+    bool is_suspect(NodeId v) const { return p_of[v] > 0.0; }
+    std::size_t size() const { return members.size(); }
+    static SuspectSet from_members(std::vector<std::pair<NodeId, double>> mem, const ProbGraph& g);
+};
+
+struct CandidateSet {
+    ItemKind kind = ItemKind::Edge;
+    std::optional<std::vector<std::uint32_t>> ids;  // nullopt = all items of the kind
+    static CandidateSet all(ItemKind k) { return CandidateSet{k, std::nullopt}; }
+    static CandidateSet of(ItemKind k, std::vector<std::uint32_t> v) {
+        return CandidateSet{k, std::move(v)};
+    }
+    std::size_t size(const ProbGraph& g) const {
+        return ids ? ids->size() : (kind == ItemKind::Edge ? g.m : g.n);
+    }
+    void validate(const ProbGraph& g) const;
+};
+
+enum class WeightMode { Given, InDegree, RandomNormalized };
+
+struct LoadOptions {
+    bool symmetrize = false;
+    std::string mapping_out;
+};
+
+ProbGraph build_graph(NodeId n, std::vector<std::tuple<NodeId, NodeId, double>> edges,
+                      WeightMode mode, std::uint64_t seed);
+ProbGraph load_edge_list(const std::string& path, WeightMode mode, std::uint64_t seed,
+                         const LoadOptions& opts = {});
+SuspectSet load_suspects(const std::string& path, const ProbGraph& g);
+SuspectSet random_suspects(const ProbGraph& g, NodeId count, std::uint64_t seed);
+ProbGraph synth_graph(NodeId n, std::uint32_t density, std::uint64_t seed);
+void save_edge_list(const ProbGraph& g, const std::string& path);
+void save_cache(const ProbGraph& g, const std::string& path);
+ProbGraph load_cache(const std::string& path);
+
+// Bench tooling (not in the reference): R-MAT(a,b,c,d) graph with 1/in-degree weights, built
+// without validate() because hub rows exceed its 1e-12 tolerance.
+ProbGraph rmat_graph(std::uint32_t scale, double edge_factor, std::uint64_t seed, double a = 0.57,
+                     double b = 0.19, double c = 0.19);
+// Direct CSR fill (in_offsets, in_src, in_cum given); weight/edge_dst derived; no validate().
+ProbGraph graph_from_csr(NodeId n, EdgeId m, const std::uint64_t* in_offsets, const NodeId* in_src,
+                         const double* in_cum);
+
+// ---- device binding (new: the reference has no device) -----------------------------------------
+// Owns one hsaw_gpu_ctx with the graph + suspects uploaded. Every sampling object below borrows it.
+class DeviceGraph {
+public:
+    DeviceGraph(const ProbGraph& g, const SuspectSet& vi, int device = 0,
+                void* cuda_stream = nullptr);
+    ~DeviceGraph();
+    DeviceGraph(const DeviceGraph&) = delete;
+    DeviceGraph& operator=(const DeviceGraph&) = delete;
+
+    void set_suspects(const SuspectSet& vi);  // new SuspectSet on the same graph
+    hsaw_gpu_ctx* ctx() const { return ctx_; }
+    NodeId n() const { return n_; }
+    EdgeId m() const { return m_; }
+    std::uint64_t device_bytes() const;
+    std::uint64_t launches() const;
+    // {encode, decode, distinct, compact, index, rounds, coverage, upload} milliseconds on device
+    std::vector<double> stage_ms(bool reset = false) const;
+
+private:
+    hsaw_gpu_ctx* ctx_ = nullptr;
+    NodeId n_ = 0;
+    EdgeId m_ = 0;
+};
+
+// ---- sampler (proj/include/hsaw/sampler.hpp) ----------------------------------------------------
+struct EncodedWalk {
+    PrgState seed;
+    std::uint32_t len = 0;
+    std::uint64_t worker_id = 0;
+    std::uint32_t seq = 0;
+};
+struct HsawSample {
+    std::vector<NodeId> nodes;
+    std::vector<EdgeId> edge_ids;
+    NodeId source() const { return nodes.front(); }
+    NodeId hit() const { return nodes.back(); }
+};
+struct WalkTag {
+    std::uint64_t worker_id = 0;
+    std::uint32_t seq = 0;
+};
+struct SamplePool {
+    std::vector<HsawSample> samples;
+    std::vector<WalkTag> tags;
+    std::uint64_t attempts = 0;
+    std::uint64_t accepted() const { return samples.size(); }
+};
+
+enum class CycleHeuristic { Brent, Floyd, None };  // Floyd is not offered on the device path
+
+struct SamplerConfig {
+    CycleHeuristic heuristic = CycleHeuristic::Brent;
+    std::uint32_t window = 2;
+    std::uint32_t batch_size = 10;
+    std::uint64_t max_attempts = 100'000'000;
+};
+
+// thread_sample (proj/src/sampler.cpp:267-290) on the device.
+std::vector<EncodedWalk> thread_sample(const DeviceGraph& dg, std::uint64_t worker_id,
+                                       std::uint32_t l, const SamplerConfig& cfg = {});
+std::vector<EncodedWalk> thread_sample(const ProbGraph& g, const SuspectSet& vi,
+                                       std::uint64_t worker_id, std::uint32_t l,
+                                       const SamplerConfig& cfg = {});
+
+// DecodeContext (proj/include/hsaw/sampler.hpp:85-100) on the device.
+class DecodeContext {
+public:
+    explicit DecodeContext(const DeviceGraph& dg) : dg_(dg) {}
+    std::optional<HsawSample> decode(const EncodedWalk& ew);  // throws DataError on mismatch
+    // Batched form: nullopt entries are walks dropped by the exact recheck.
+    std::vector<std::optional<HsawSample>> decode(std::span<const EncodedWalk> walks);
+
+private:
+    const DeviceGraph& dg_;
+};
+
+// SampleStream (proj/include/hsaw/sampler.hpp:133-163): decoded walks stay on the device.
+class SampleStream {
+public:
+    SampleStream(const DeviceGraph& dg, std::uint64_t seed, SamplerConfig cfg = {});
+    ~SampleStream();
+    SampleStream(const SampleStream&) = delete;
+    SampleStream& operator=(const SampleStream&) = delete;
+
+    void ensure(std::uint64_t min_accepted);  // throws SamplingError on budget exhaustion
+    // Host copy of samples [offset, offset + count); throws std::out_of_range like the reference.
+    std::vector<HsawSample> prefix(std::uint64_t offset, std::uint64_t count) const;
+    struct Counters {
+        std::uint64_t attempts = 0, accepted = 0;
+    };
+    Counters counters_for(std::uint64_t min_accepted) const;
+    SamplePool to_pool(std::uint64_t min_accepted) const;
+
+    std::uint64_t materialized() const;
+    hsaw_gpu_stream* handle() const { return s_; }
+    const DeviceGraph& device() const { return dg_; }
+    std::vector<std::uint64_t> stats() const;  // u64[8], see hsaw_gpu.h
+
+private:
+    const DeviceGraph& dg_;
+    hsaw_gpu_stream* s_ = nullptr;
+};
+
+SamplePool stream_samples(const DeviceGraph& dg, std::uint64_t target, std::uint64_t seed = 0,
+                          const SamplerConfig& cfg = {});
+// Reference signature; `workers` is accepted and ignored (the GPU is the worker pool).
+SamplePool stream_samples(const ProbGraph& g, const SuspectSet& vi, std::uint32_t workers,
+                          std::uint64_t target, std::uint64_t seed = 0,
+                          const SamplerConfig& cfg = {});
+double estimate_influence(const SamplePool& pool, NodeId n);
+void dump_walks(const SamplePool& pool, std::ostream& out);
+
+// ---- coverage (proj/include/hsaw/coverage.hpp) --------------------------------------------------
+// Device-resident coverage index: a range of a SampleStream (edge ids or nodes of each walk) or a
+// raw collection of item sets (the fixed-walk-set parity mode), restricted to the candidates.
+class CoverageIndex {
+public:
+    CoverageIndex(ItemKind kind, const SampleStream& stream, std::uint64_t offset,
+                  std::uint64_t count, const CandidateSet& cand, const ProbGraph& g);
+    CoverageIndex(const DeviceGraph& dg, std::span<const std::vector<std::uint32_t>> item_sets,
+                  const CandidateSet& cand, const ProbGraph& g);
+    ~CoverageIndex();
+    CoverageIndex(const CoverageIndex&) = delete;
+    CoverageIndex& operator=(const CoverageIndex&) = delete;
+
+    ItemKind kind() const { return kind_; }
+    std::uint32_t num_samples() const { return static_cast<std::uint32_t>(count_); }
+    std::uint64_t num_candidates() const { return ncand_; }
+    std::uint64_t coverage_of(std::span<const std::uint32_t> items) const;
+
+private:
+    friend struct GreedyAccess;
+    ItemKind kind_;
+    hsaw_gpu_ctx* ctx_ = nullptr;
+    hsaw_gpu_stream* stream_ = nullptr;
+    hsaw_gpu_walkset* walkset_ = nullptr;
+    std::uint64_t offset_ = 0, count_ = 0, ncand_ = 0;
+    std::optional<std::vector<std::uint32_t>> cand_;
+};
+
+struct GreedyResult {
+    std::vector<std::uint32_t> solution;
+    std::uint64_t coverage = 0;
+};
+GreedyResult greedy_max_cover(const CoverageIndex& idx, std::uint32_t k);
+
+struct Schedule {
+    double epsilon = 0, delta = 0;
+    std::uint32_t k = 0;
+    double lambda = 0, lambda1 = 0, n_max = 0;
+    std::uint32_t t_max = 1;
+    std::uint64_t lambda_samples() const;
+};
+double ln_choose(std::uint64_t M, std::uint64_t k);
+Schedule compute_schedule_m(std::uint64_t M, std::uint32_t k, double epsilon, double delta);
+Schedule compute_schedule(const ProbGraph& g, ItemKind kind, std::uint32_t k, double epsilon,
+                          double delta);
+
+struct CheckResult {
+    bool pass = false;
+    double eps_t = 0;
+};
+CheckResult check_solution(std::span<const std::uint32_t> solution, const CoverageIndex& idx_r,
+                           const CoverageIndex& idx_r_prime, const Schedule& sched,
+                           std::uint32_t t);
+// The arithmetic of check_solution on two coverage counts (used by both overloads and by tests).
+CheckResult check_counts(double cov_r, double cov_rp, double n_rp, const Schedule& sched,
+                         std::uint32_t t);
+
+// ---- interdiction (proj/include/hsaw/interdiction.hpp) ------------------------------------------
+struct InterdictionResult {
+    ItemKind kind = ItemKind::Edge;
+    std::uint32_t k = 0;
+    double epsilon = 0, delta = 0;
+    std::vector<std::uint32_t> solution;
+    double est_suspension = 0;
+    std::uint64_t coverage = 0, samples_used = 0, attempts = 0;
+    std::uint32_t iterations = 0;
+    bool passed_check = false;
+    double wall_time_s = 0;
+    // device-side breakdown (not serialised): sampling / greedy / check seconds of host wall time
+    double sample_s = 0, greedy_s = 0, check_s = 0;
+};
+
+struct InterdictionOptions {
+    std::uint32_t workers = 1;  // accepted for source compatibility; unused on the device path
+    std::uint64_t seed = 0;
+    SamplerConfig sampler;
+    int device = 0;
+};
+
+InterdictionResult esia(const ProbGraph& g, const SuspectSet& vi, const CandidateSet& cand,
+                        std::uint32_t k, double epsilon, double delta,
+                        const InterdictionOptions& opts = {});
+InterdictionResult nsia(const ProbGraph& g, const SuspectSet& vi, const CandidateSet& cand,
+                        std::uint32_t k, double epsilon, double delta,
+                        const InterdictionOptions& opts = {});
+// Same, on an already uploaded graph (upload excluded from wall_time_s).
+InterdictionResult esia(const DeviceGraph& dg, const ProbGraph& g, const CandidateSet& cand,
+                        std::uint32_t k, double epsilon, double delta,
+                        const InterdictionOptions& opts = {});
+InterdictionResult nsia(const DeviceGraph& dg, const ProbGraph& g, const CandidateSet& cand,
+                        std::uint32_t k, double epsilon, double delta,
+                        const InterdictionOptions& opts = {});
+
+std::string to_json(const InterdictionResult& r, bool include_timing = true);
+
+// ---- cli (proj/include/hsaw/cli.hpp) ------------------------------------------------------------
+int run_cli(std::vector<std::string> args);
+
+}  // namespace hsaw

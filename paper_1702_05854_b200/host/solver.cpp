@@ -1,0 +1,225 @@
+// Host side of eSIA / nSIA: the sample-size schedule, the out-of-sample stopping rule and the
+// doubling loop (north_star item 4 keeps these on the host). Sampling, greedy max-cover and the two
+// coverage counts of every iteration run on the device through DeviceGraph / SampleStream /
+// CoverageIndex. Follows /root/reference/proj/src/coverage.cpp:168-231 and interdiction.cpp:12-104;
+// the FP64 expressions keep the reference's operation order so that ceil(lambda), t_max and eps_t
+// come out bit-identical with the same libm.
+#include <charconv>
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <sstream>
+
+#include "hsaw_b200.hpp"
+
+namespace hsaw {
+
+// ---- schedule -----------------------------------------------------------------------------------
+double ln_choose(std::uint64_t M, std::uint64_t k) {  // coverage.cpp:168-173
+    double acc = 0.0;
+    for (std::uint64_t i = 1; i <= k; ++i)
+        acc += std::log(static_cast<double>(M - k + i) / static_cast<double>(i));
+    return acc;
+}
+
+std::uint64_t Schedule::lambda_samples() const {
+    return static_cast<std::uint64_t>(std::ceil(lambda));
+}
+
+Schedule compute_schedule_m(std::uint64_t M, std::uint32_t k, double epsilon, double delta) {
+    if (!(epsilon > 0.0) || epsilon >= 1.0) throw std::invalid_argument("epsilon must be in (0,1)");
+    if (!(delta > 0.0) || delta >= 1.0) throw std::invalid_argument("delta must be in (0,1)");
+    if (k < 1 || k > M) throw std::invalid_argument("budget k out of range");
+    Schedule out;
+    out.epsilon = epsilon;
+    out.delta = delta;
+    out.k = k;
+    const double two_minus_inv_e = 2.0 - 1.0 / std::exp(1.0);
+    const double c = two_minus_inv_e * two_minus_inv_e;
+    const double a = 2.0 + 2.0 * epsilon / 3.0;
+    const double eps_sq = epsilon * epsilon;
+    out.n_max = c * a * static_cast<double>(M) * (std::log(6.0 / delta) + ln_choose(M, k)) /
+                (static_cast<double>(k) * eps_sq);
+    const double lambda0 = a * std::log(3.0 / delta) / eps_sq;
+    const double rounds = std::ceil(std::log2(2.0 * out.n_max / lambda0));
+    out.t_max = rounds < 1.0 ? 1u : static_cast<std::uint32_t>(rounds);
+    out.lambda = a * std::log(3.0 * out.t_max / delta) / eps_sq;
+    out.lambda1 = 1.0 + (1.0 + epsilon) * a * std::log(3.0 * out.t_max / delta) / eps_sq;
+    return out;
+}
+
+Schedule compute_schedule(const ProbGraph& g, ItemKind kind, std::uint32_t k, double epsilon,
+                          double delta) {
+    return compute_schedule_m(kind == ItemKind::Edge ? g.m : g.n, k, epsilon, delta);
+}
+
+// ---- stopping rule ------------------------------------------------------------------------------
+CheckResult check_counts(double cov_r, double cov_rp, double n_rp, const Schedule& sched,
+                         std::uint32_t t) {  // coverage.cpp:218-230
+    if (cov_rp < sched.lambda1) return {false, std::numeric_limits<double>::infinity()};
+    const double eps = sched.epsilon;
+    const double doubling = std::ldexp(1.0, static_cast<int>(t) - 1);
+    const double one_me = 1.0 - 1.0 / std::exp(1.0);
+    const double eps1 = cov_r / cov_rp - 1.0;
+    const double eps2 = eps * std::sqrt(n_rp * (1.0 + eps) / (doubling * cov_rp));
+    const double eps3 = eps * std::sqrt(n_rp * (1.0 + eps) * (one_me - eps) /
+                                        ((1.0 + eps / 3.0) * doubling * cov_rp));
+    const double eps_t = (eps1 + eps2 + eps1 * eps2) * (one_me - eps) + one_me * eps3;
+    return {eps_t <= eps, eps_t};
+}
+
+CheckResult check_solution(std::span<const std::uint32_t> solution, const CoverageIndex& idx_r,
+                           const CoverageIndex& idx_r_prime, const Schedule& sched,
+                           std::uint32_t t) {
+    const auto cov_r = static_cast<double>(idx_r.coverage_of(solution));
+    const auto cov_rp = static_cast<double>(idx_r_prime.coverage_of(solution));
+    return check_counts(cov_r, cov_rp, static_cast<double>(idx_r_prime.num_samples()), sched, t);
+}
+
+// ---- doubling loop ------------------------------------------------------------------------------
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double seconds_since(Clock::time_point t0) {
+    return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+InterdictionResult run_on_device(const DeviceGraph& dg, const ProbGraph& g,
+                                 const CandidateSet& cand, std::uint32_t k, double epsilon,
+                                 double delta, const InterdictionOptions& opts) {
+    cand.validate(g);
+    if (k < 1 || k > cand.size(g))  // interdiction.cpp:17-18
+        throw std::invalid_argument("budget k must be in [1, |C|]");
+    const auto t0 = Clock::now();
+    const Schedule sched = compute_schedule(g, cand.kind, k, epsilon, delta);
+    const std::uint64_t base = sched.lambda_samples();
+
+    SampleStream stream(dg, opts.seed, opts.sampler);
+    InterdictionResult res;
+    res.kind = cand.kind;
+    res.k = k;
+    res.epsilon = epsilon;
+    res.delta = delta;
+
+    std::uint64_t size = 0;
+    GreedyResult picked;
+    CheckResult verdict;
+    std::uint32_t t = 0;
+    for (;;) {  // interdiction.cpp:36-47
+        ++t;
+        size = base << (t - 1);
+        auto ts = Clock::now();
+        stream.ensure(2 * size);
+        res.sample_s += seconds_since(ts);
+        // R_t = samples [0, size), R'_t = [size, 2 size): two views of the device-resident pool
+        CoverageIndex in_sample(cand.kind, stream, 0, size, cand, g);
+        CoverageIndex out_of_sample(cand.kind, stream, size, size, cand, g);
+        ts = Clock::now();
+        picked = greedy_max_cover(in_sample, k);
+        res.greedy_s += seconds_since(ts);
+        ts = Clock::now();
+        verdict = check_solution(picked.solution, in_sample, out_of_sample, sched, t);
+        res.check_s += seconds_since(ts);
+        if (verdict.pass || static_cast<double>(size) >= sched.n_max) break;
+    }
+
+    res.solution = picked.solution;
+    res.coverage = picked.coverage;
+    res.samples_used = 2 * size;
+    res.iterations = t;
+    res.passed_check = verdict.pass;
+    const auto counters = stream.counters_for(2 * size);
+    res.attempts = counters.attempts;
+    const double influence = static_cast<double>(g.n) * static_cast<double>(counters.accepted) /
+                             static_cast<double>(counters.attempts);
+    res.est_suspension =
+        influence * static_cast<double>(picked.coverage) / static_cast<double>(size);
+    res.wall_time_s = seconds_since(t0);
+    return res;
+}
+
+void require_kind(const CandidateSet& cand, ItemKind want, const char* msg) {
+    if (cand.kind != want) throw std::invalid_argument(msg);
+}
+
+}  // namespace
+
+InterdictionResult esia(const DeviceGraph& dg, const ProbGraph& g, const CandidateSet& cand,
+                        std::uint32_t k, double epsilon, double delta,
+                        const InterdictionOptions& opts) {
+    require_kind(cand, ItemKind::Edge, "esia requires an edge candidate set");
+    return run_on_device(dg, g, cand, k, epsilon, delta, opts);
+}
+
+InterdictionResult nsia(const DeviceGraph& dg, const ProbGraph& g, const CandidateSet& cand,
+                        std::uint32_t k, double epsilon, double delta,
+                        const InterdictionOptions& opts) {
+    require_kind(cand, ItemKind::Node, "nsia requires a node candidate set");
+    return run_on_device(dg, g, cand, k, epsilon, delta, opts);
+}
+
+InterdictionResult esia(const ProbGraph& g, const SuspectSet& vi, const CandidateSet& cand,
+                        std::uint32_t k, double epsilon, double delta,
+                        const InterdictionOptions& opts) {
+    require_kind(cand, ItemKind::Edge, "esia requires an edge candidate set");
+    const auto t0 = Clock::now();
+    DeviceGraph dg(g, vi, opts.device);
+    InterdictionResult res = run_on_device(dg, g, cand, k, epsilon, delta, opts);
+    res.wall_time_s = seconds_since(t0);  // upload included, like a host-to-result call
+    return res;
+}
+
+InterdictionResult nsia(const ProbGraph& g, const SuspectSet& vi, const CandidateSet& cand,
+                        std::uint32_t k, double epsilon, double delta,
+                        const InterdictionOptions& opts) {
+    require_kind(cand, ItemKind::Node, "nsia requires a node candidate set");
+    const auto t0 = Clock::now();
+    DeviceGraph dg(g, vi, opts.device);
+    InterdictionResult res = run_on_device(dg, g, cand, k, epsilon, delta, opts);
+    res.wall_time_s = seconds_since(t0);
+    return res;
+}
+
+// ---- JSON ---------------------------------------------------------------------------------------
+// Same document as nlohmann::json::dump(2) produces for the reference (interdiction.cpp:89-104):
+// keys in alphabetical order, two-space indent, one array element per line, doubles in shortest
+// round-trip form with a ".0" suffix when integral. tests/golden/interdict12.json is byte-stable.
+namespace {
+
+std::string json_number(double x) {
+    char buf[64];
+    auto res = std::to_chars(buf, buf + sizeof buf, x);
+    std::string s(buf, res.ptr);
+    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+    return s;
+}
+
+}  // namespace
+
+std::string to_json(const InterdictionResult& r, bool include_timing) {
+    std::ostringstream out;
+    out << "{\n";
+    out << "  \"attempts\": " << r.attempts << ",\n";
+    out << "  \"coverage\": " << r.coverage << ",\n";
+    out << "  \"delta\": " << json_number(r.delta) << ",\n";
+    out << "  \"epsilon\": " << json_number(r.epsilon) << ",\n";
+    out << "  \"est_suspension\": " << json_number(r.est_suspension) << ",\n";
+    out << "  \"iterations\": " << r.iterations << ",\n";
+    out << "  \"k\": " << r.k << ",\n";
+    out << "  \"kind\": \"" << to_string(r.kind) << "\",\n";
+    out << "  \"passed_check\": " << (r.passed_check ? "true" : "false") << ",\n";
+    out << "  \"samples_used\": " << r.samples_used << ",\n";
+    out << "  \"solution\": [";
+    if (r.solution.empty()) {
+        out << "]";
+    } else {
+        for (std::size_t i = 0; i < r.solution.size(); ++i)
+            out << (i ? ",\n    " : "\n    ") << r.solution[i];
+        out << "\n  ]";
+    }
+    if (include_timing) out << ",\n  \"wall_time_s\": " << json_number(r.wall_time_s);
+    out << "\n}";
+    return out.str();
+}
+
+}  // namespace hsaw

@@ -44,9 +44,13 @@ def main():
     gh = R.load_edge_list(f"{REFDATA}/fixture12.edges", mode=0)
     p = R.load_suspects(f"{REFDATA}/fixture12.suspects", gh)
     csr = R._to_csr(gh, p)
+    weight, edge_dst = R.graph_extra(gh)
     fx = dict(n=csr.n, m=csr.m, in_offsets=csr.in_offsets.tolist(), in_src=csr.in_src.tolist(),
               in_cum=[float.hex(float(x)) for x in csr.in_cum],
-              p_of=[float.hex(float(x)) for x in csr.p_of])
+              p_of=[float.hex(float(x)) for x in csr.p_of],
+              weight=[float.hex(float(x)) for x in weight], edge_dst=edge_dst.tolist())
+    # the reference test-suite's own byte-stable CLI golden (proj/tests/test_cli.cpp:242-251)
+    fx["interdict12_json_text"] = open("/root/reference/proj/tests/golden/interdict12.json").read()
     with R.handles(csr) as hd:
         kats = []
         for w in list(range(40, 60)) + [0, 1, 2**63, 2**64 - 1]:
