@@ -62,11 +62,21 @@ struct Error {
 
 [[noreturn]] inline void fail(int status, const std::string& msg) { throw Error{status, msg}; }
 
-// ---- device vector with amortised growth -------------------------------------------------------
+// ---- device memory: stream-ordered pool allocations ---------------------------------------------
+// All device buffers come from the device's default cudaMallocAsync pool (release threshold set to
+// "never" at context creation), ordered on the context stream: growing a scratch buffer or the
+// walk pool costs no device synchronisation and freed memory is reused by the next request.
+// The stream in effect is the one of the C-ABI call being served (set by guarded()).
+inline cudaStream_t& current_stream() {
+    static thread_local cudaStream_t st = nullptr;
+    return st;
+}
+
 template <class T>
 struct DevVec {
     T* p = nullptr;
     uint64_t size = 0, cap = 0;
+    cudaStream_t owner = nullptr;  // stream the buffer was allocated on
 
     DevVec() = default;
     DevVec(const DevVec&) = delete;
@@ -74,39 +84,45 @@ struct DevVec {
     ~DevVec() { release(); }
 
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, owner);
         p = nullptr;
         size = cap = 0;
     }
-    // Grows capacity (x1.5 steps) preserving the first `size` elements.
+    static T* alloc(uint64_t count, cudaStream_t st) {
+        T* np = nullptr;
+        HSAW_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&np), count * sizeof(T), st));
+        return np;
+    }
+    // Grows capacity (doubling) preserving the first `size` elements; stream-ordered, no sync.
     void reserve(uint64_t want, cudaStream_t st) {
         if (want <= cap) return;
-        uint64_t ncap = cap + cap / 2;
+        uint64_t ncap = cap * 2;
         if (ncap < want) ncap = want;
         if (ncap < 1024) ncap = 1024;
-        T* np = nullptr;
-        HSAW_CUDA_CHECK(cudaMalloc(&np, ncap * sizeof(T)));
+        T* np = alloc(ncap, st);
         if (p && size) {
             cudaError_t e = cudaMemcpyAsync(np, p, size * sizeof(T), cudaMemcpyDeviceToDevice, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) {
-                cudaFree(np);
+                cudaFreeAsync(np, st);
                 HSAW_CUDA_CHECK(e);
             }
         }
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
         p = np;
         cap = ncap;
+        owner = st;
     }
     // Scratch use: capacity only, contents undefined.
     void ensure_scratch(uint64_t want) {
         if (want <= cap) return;
-        if (p) cudaFree(p);
+        cudaStream_t st = current_stream();
+        if (p) cudaFreeAsync(p, owner);
         p = nullptr;
         cap = 0;
-        uint64_t ncap = want + want / 4;
-        HSAW_CUDA_CHECK(cudaMalloc(&p, ncap * sizeof(T)));
+        uint64_t ncap = want + want / 2;
+        p = alloc(ncap, st);
         cap = ncap;
+        owner = st;
     }
 };
 
@@ -139,6 +155,22 @@ struct hsaw_gpu_ctx {
     std::vector<Pending> pending;
     double stage_ms[HSAW_STAGE_COUNT] = {};
     uint64_t stage_launches[HSAW_STAGE_COUNT] = {};
+
+    void release_scratch() {
+        cub_tmp.release();
+        chk_list.release();
+        chk_counters.release();
+        g_cand_bits.release();
+        g_cnt.release();
+        g_fill.release();
+        g_inv.release();
+        g_covered.release();
+        g_solution.release();
+        g_query_bits.release();
+        g_pos.release();
+        g_partial.release();
+        g_gains.release();
+    }
 };
 
 namespace hsawgpu {
@@ -147,7 +179,10 @@ namespace hsawgpu {
 template <class F>
 int guarded(hsaw_gpu_ctx* ctx, F&& f) {
     try {
-        if (ctx) HSAW_CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (ctx) {
+            HSAW_CUDA_CHECK(cudaSetDevice(ctx->device));
+            current_stream() = ctx->stream;
+        }
         f();
         return HSAW_OK;
     } catch (const Error& e) {

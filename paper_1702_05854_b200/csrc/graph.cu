@@ -2,6 +2,8 @@
 // re-laid out by two kernels into the node/edge records the walk kernels read.
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 using namespace hsawgpu;
@@ -81,8 +83,8 @@ __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
 }
 
 void free_graph(hsaw_gpu_ctx* ctx) {
-    if (ctx->g.nodes) cudaFree(ctx->g.nodes);
-    if (ctx->g.edges) cudaFree(ctx->g.edges);
+    if (ctx->g.nodes) cudaFreeAsync(ctx->g.nodes, ctx->stream);
+    if (ctx->g.edges) cudaFreeAsync(ctx->g.edges, ctx->stream);
     ctx->g = DeviceGraph{};
     ctx->graph_bytes = 0;
 }
@@ -162,6 +164,18 @@ int hsaw_gpu_ctx_create(int device, void* cuda_stream, hsaw_gpu_ctx** out) {
         }
         HSAW_CUDA_CHECK(cudaMalloc(&ctx->d_scalars, 64 * sizeof(uint64_t)));
         HSAW_CUDA_CHECK(cudaMallocHost(&ctx->h_scalars, 64 * sizeof(uint64_t)));
+        // keep freed pool memory cached instead of returning it to the driver at every sync
+        cudaMemPool_t pool = nullptr;
+        HSAW_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t never = ~0ull;
+        HSAW_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &never));
+        // Random 16/32-byte record reads: ask L2 to fetch single 32-byte sectors from HBM rather
+        // than the default 64 bytes (HSAW_L2_FETCH=32|64|128 overrides, for A/B measurements).
+        size_t fetch = 32;
+        if (const char* env = std::getenv("HSAW_L2_FETCH")) fetch = (size_t)std::atoi(env);
+        if (fetch == 32 || fetch == 64 || fetch == 128)
+            cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, fetch);
+        cudaGetLastError();
     });
     if (rc != HSAW_OK) {
         hsaw_gpu_ctx_destroy(ctx);
@@ -180,7 +194,8 @@ void hsaw_gpu_ctx_destroy(hsaw_gpu_ctx* ctx) {
     free_graph(ctx);
     if (ctx->d_scalars) cudaFree(ctx->d_scalars);
     if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
-    ctx->cub_tmp.release();
+    ctx->release_scratch();  // stream-ordered frees must precede the stream's destruction
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -235,21 +250,22 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
         double *d_cum = nullptr, *d_p = nullptr;
         uint32_t* d_bad = nullptr;
         auto cleanup = [&] {
-            cudaFree(d_off);
-            cudaFree(d_src);
-            cudaFree(d_cum);
-            cudaFree(d_p);
-            cudaFree(d_bad);
+            if (d_off) cudaFreeAsync(d_off, st);
+            if (d_src) cudaFreeAsync(d_src, st);
+            if (d_cum) cudaFreeAsync(d_cum, st);
+            if (d_p) cudaFreeAsync(d_p, st);
+            if (d_bad) cudaFreeAsync(d_bad, st);
         };
         try {
-            HSAW_CUDA_CHECK(cudaMalloc(&ctx->g.nodes, (uint64_t)n * sizeof(NodeRec)));
             HSAW_CUDA_CHECK(
-                cudaMalloc(&ctx->g.edges, (uint64_t)(m ? m : 1) * sizeof(EdgeRec)));
-            HSAW_CUDA_CHECK(cudaMalloc(&d_off, ((uint64_t)n + 1) * 8));
-            HSAW_CUDA_CHECK(cudaMalloc(&d_src, (uint64_t)(m ? m : 1) * 4));
-            HSAW_CUDA_CHECK(cudaMalloc(&d_cum, (uint64_t)(m ? m : 1) * 8));
-            HSAW_CUDA_CHECK(cudaMalloc(&d_p, (uint64_t)n * 8));
-            HSAW_CUDA_CHECK(cudaMalloc(&d_bad, 4));
+                cudaMallocAsync((void**)&ctx->g.nodes, (uint64_t)n * sizeof(NodeRec), st));
+            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&ctx->g.edges,
+                                            (uint64_t)(m ? m : 1) * sizeof(EdgeRec), st));
+            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_off, ((uint64_t)n + 1) * 8, st));
+            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_src, (uint64_t)(m ? m : 1) * 4, st));
+            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_cum, (uint64_t)(m ? m : 1) * 8, st));
+            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, st));
+            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_bad, 4, st));
             HSAW_CUDA_CHECK(cudaMemcpyAsync(d_off, in_offsets, ((uint64_t)n + 1) * 8,
                                             cudaMemcpyHostToDevice, st));
             if (m) {
@@ -297,7 +313,7 @@ int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of) {
         if (!p_of) fail(HSAW_EINVAL, "suspects_upload: null array");
         uint32_t n = ctx->g.n;
         double* d_p = nullptr;
-        HSAW_CUDA_CHECK(cudaMalloc(&d_p, (uint64_t)n * 8));
+        HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, ctx->stream));
         cudaError_t e =
             cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, ctx->stream);
         if (e == cudaSuccess) {
@@ -306,7 +322,7 @@ int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of) {
             ++ctx->launches;
             e = cudaStreamSynchronize(ctx->stream);
         }
-        cudaFree(d_p);
+        cudaFreeAsync(d_p, ctx->stream);
         HSAW_CUDA_CHECK(e);
     });
 }

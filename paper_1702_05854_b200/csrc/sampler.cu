@@ -8,6 +8,8 @@
 // whose body is "one draw + at most one edge-record load + one node-record load" for every lane,
 // whatever phase of its walk the lane is in. Lanes that finish refill from a global cursor with a
 // warp-aggregated atomicAdd, so a warp never waits for its longest attempt.
+#include <cstdlib>
+
 #include "sampler.cuh"
 #include "walk.cuh"
 
@@ -16,6 +18,7 @@ namespace hsawgpu {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kDefaultEncodeBlocksPerSM = 5;  // 48 registers, no spills (ptxas -v)
 
 struct EncodeParams {
     const NodeRec* nodes;
@@ -109,26 +112,29 @@ __device__ __forceinline__ bool claim(uint64_t* cursor, uint64_t total, bool wan
 // ---- K1 ----------------------------------------------------------------------------------------
 // HEUR: 0 Brent, 2 None (CycleHeuristic, proj/include/hsaw/sampler.hpp:46). WIN: window width or
 // -1 for the runtime-width variant.
-template <int HEUR, int WIN>
-__global__ void __launch_bounds__(kThreads) encode_kernel(EncodeParams p) {
+template <int HEUR, int WIN, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) {
     const uint32_t lane = threadIdx.x & 31;
     const NodeRec* __restrict__ nodes = p.nodes;
     const EdgeRec* __restrict__ edges = p.edges;
 
-    uint64_t s = 0, snapshot = 0, bidx = 0;
+    uint64_t s = 0, snapshot = 0;
+    uint32_t bidx = 0;  // batch index within the launch (launches hold < 2^32 batches)
     uint32_t lo = 0, deg = 0;
     uint64_t tot = 0, scale = 0;
     uint32_t nedges = 0, att = 0, cnt = 0;
     bool have = false, fresh = true, drained = false;
     Window<WIN> win;
     uint32_t b_anchor = kInvalidNode, b_power = 1, b_lam = 0;
-    uint64_t st_draws = 0, st_steps = 0, st_bytes = 0, st_att = 0, st_acc = 0;
+    // per-lane work counters; 32 bits suffice for one launch's share of one lane, except bytes
+    uint32_t st_draws = 0, st_steps = 0, st_att = 0, st_acc = 0;
+    uint64_t st_bytes = 0;
 
     for (;;) {
         if (!drained) {
             uint64_t mine = 0;
             if (claim(p.cursor, p.nbatches, !have, lane, mine, drained)) {
-                bidx = mine;
+                bidx = (uint32_t)mine;
                 s = seed_from_worker(p.first_worker + mine);  // sampler.cpp:272
 #pragma unroll
                 for (int i = 0; i < 8; ++i) (void)prg_next(s);  // burn-in, sampler.cpp:273
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncodeParams p) {
                 accepted = k2 < rec.acc_thr;  // r <= p_of[u], sampler.cpp:34,57
             }
             if (accepted) {
-                uint64_t slot = bidx * p.l + cnt;  // seq = index among accepted, sampler.cpp:283
+                uint64_t slot = (uint64_t)bidx * p.l + cnt;  // seq = index among accepted, :283
                 p.out_seed[slot] = snapshot;
                 p.out_len[slot] = nedges;
                 ++cnt;
@@ -234,18 +240,16 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncodeParams p) {
         }
     }
 
-    st_draws = warp_sum(st_draws);
-    st_steps = warp_sum(st_steps);
-    st_bytes = warp_sum(st_bytes);
-    st_att = warp_sum(st_att);
-    st_acc = warp_sum(st_acc);
+    const uint64_t w_draws = warp_sum(st_draws), w_steps = warp_sum(st_steps);
+    const uint64_t w_bytes = warp_sum(st_bytes), w_att = warp_sum(st_att);
+    const uint64_t w_acc = warp_sum(st_acc);
     if (lane == 0 && p.stats) {
         auto* st = reinterpret_cast<unsigned long long*>(p.stats);
-        atomicAdd(st + ST_ATTEMPTS, (unsigned long long)st_att);
-        atomicAdd(st + ST_DRAWS, (unsigned long long)st_draws);
-        atomicAdd(st + ST_STEPS, (unsigned long long)st_steps);
-        atomicAdd(st + ST_BYTES, (unsigned long long)st_bytes);
-        atomicAdd(st + ST_ACCEPTED, (unsigned long long)st_acc);
+        atomicAdd(st + ST_ATTEMPTS, (unsigned long long)w_att);
+        atomicAdd(st + ST_DRAWS, (unsigned long long)w_draws);
+        atomicAdd(st + ST_STEPS, (unsigned long long)w_steps);
+        atomicAdd(st + ST_BYTES, (unsigned long long)w_bytes);
+        atomicAdd(st + ST_ACCEPTED, (unsigned long long)w_acc);
     }
 }
 
@@ -494,6 +498,7 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
                    uint64_t nbatches, uint64_t* d_seed, uint32_t* d_len, uint32_t* d_count,
                    uint64_t* d_stats, uint64_t* d_cursor) {
     if (nbatches == 0) return;
+    if (nbatches > 0xFFFFFFFFull) fail(HSAW_EINVAL, "encode: more than 2^32 batches per launch");
     EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, cfg.batch_size, cfg.window,
                    first_worker, nbatches, d_seed, d_len, d_count, d_stats, d_cursor};
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
@@ -504,12 +509,25 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
         check_launch(ctx, "encode_kernel");
     };
     bool brent = cfg.heuristic == 0;
-    if (cfg.window == 2)
-        brent ? go(encode_kernel<0, 2>) : go(encode_kernel<2, 2>);
-    else if (cfg.window == 0)
-        brent ? go(encode_kernel<0, 0>) : go(encode_kernel<2, 0>);
-    else
-        brent ? go(encode_kernel<0, -1>) : go(encode_kernel<2, -1>);
+    if (cfg.window == 2 && brent) {
+        // the default configuration: resident blocks per SM (register budget) is a tuning knob
+        static const int occ = [] {
+            const char* env = std::getenv("HSAW_K1_BLOCKS_PER_SM");
+            return env ? std::atoi(env) : kDefaultEncodeBlocksPerSM;
+        }();
+        if (occ >= 6)
+            go(encode_kernel<0, 2, 6>);
+        else if (occ == 5)
+            go(encode_kernel<0, 2, 5>);
+        else
+            go(encode_kernel<0, 2, 4>);
+    } else if (cfg.window == 2) {
+        go(encode_kernel<2, 2, 4>);
+    } else if (cfg.window == 0) {
+        brent ? go(encode_kernel<0, 0, 4>) : go(encode_kernel<2, 0, 4>);
+    } else {
+        brent ? go(encode_kernel<0, -1, 4>) : go(encode_kernel<2, -1, 4>);
+    }
 }
 
 static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
@@ -569,8 +587,9 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     if (nlong) {
         // rare path: size one global hash table per long walk, run one block per walk
         std::vector<uint32_t> pairs(2ull * nlong);
-        HSAW_CUDA_CHECK(cudaMemcpy(pairs.data(), ctx->chk_list.p, 8ull * nlong,
-                                   cudaMemcpyDeviceToHost));
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(pairs.data(), ctx->chk_list.p, 8ull * nlong,
+                                        cudaMemcpyDeviceToHost, ctx->stream));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         std::vector<uint64_t> toff(nlong + 1, 0);
         for (uint32_t i = 0; i < nlong; ++i) {
             uint64_t nn = pairs[2 * i + 1];

@@ -305,8 +305,8 @@ int hsaw_gpu_stream_create(hsaw_gpu_ctx* ctx, uint64_t seed, const hsaw_sampler_
 void hsaw_gpu_stream_destroy(hsaw_gpu_stream* s) {
     if (!s) return;
     cudaSetDevice(s->ctx->device);
-    cudaStreamSynchronize(s->ctx->stream);
-    delete s;
+    current_stream() = s->ctx->stream;
+    delete s;  // buffers go back to the pool in stream order
 }
 
 int hsaw_gpu_stream_ensure(hsaw_gpu_stream* s, uint64_t min_accepted) {
@@ -402,10 +402,13 @@ int hsaw_gpu_stream_slice_edges(const hsaw_gpu_stream* s, uint64_t off, uint64_t
     return guarded(s->ctx, [&] {
         if (off + cnt > s->accepted)
             fail(HSAW_ERANGE, "sample stream prefix not materialized");  // sampler.cpp:467-468
-        uint64_t eo[2] = {0, 0};
-        HSAW_CUDA_CHECK(cudaMemcpy(&eo[0], s->edge_off.p + off, 8, cudaMemcpyDeviceToHost));
-        HSAW_CUDA_CHECK(cudaMemcpy(&eo[1], s->edge_off.p + off + cnt, 8, cudaMemcpyDeviceToHost));
-        *total_edges = eo[1] - eo[0];
+        hsaw_gpu_ctx* ctx = s->ctx;
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], s->edge_off.p + off, 8,
+                                        cudaMemcpyDeviceToHost, ctx->stream));
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[1], s->edge_off.p + off + cnt, 8,
+                                        cudaMemcpyDeviceToHost, ctx->stream));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        *total_edges = ctx->h_scalars[1] - ctx->h_scalars[0];
     });
 }
 
@@ -443,7 +446,10 @@ int hsaw_gpu_stream_export(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
 int hsaw_gpu_stream_stats(const hsaw_gpu_stream* s, uint64_t* stats) {
     if (!s || !stats) return HSAW_EINVAL;
     return guarded(s->ctx, [&] {
-        HSAW_CUDA_CHECK(cudaMemcpy(stats, s->stats.p, 64, cudaMemcpyDeviceToHost));
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(s->ctx->h_scalars, s->stats.p, 64, cudaMemcpyDeviceToHost,
+                                        s->ctx->stream));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(s->ctx->stream));
+        for (int i = 0; i < 8; ++i) stats[i] = s->ctx->h_scalars[i];
         stats[hsawgpu::ST_DROPPED] = s->dropped;
     });
 }

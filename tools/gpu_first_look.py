@@ -1,49 +1,57 @@
-"""Dev script: first timing look at the sampler and greedy stages on the C2 R-MAT shape."""
+"""Dev script: timing look at the sampler / greedy stages and the eSIA host loop on an R-MAT shape.
+Usage: python tools/gpu_first_look.py [scale] [batches] [esia_k]   (env knobs: HSAW_L2_FETCH,
+HSAW_K1_BLOCKS_PER_SM)"""
 import json
+import os
 import sys
 import time
-import os
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 
-from paper_1702_05854_b200 import capi, rmat
+from paper_1702_05854_b200 import capi, hostapi
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 20
+esia_k = int(sys.argv[3]) if len(sys.argv) > 3 else 100
+tag = {k: os.environ.get(k) for k in ("HSAW_L2_FETCH", "HSAW_K1_BLOCKS_PER_SM") if os.environ.get(k)}
 t = time.time()
-g = rmat.rmat_graph(scale, 16)
-print(f"graph n={g.n} m={g.m} gen {time.time()-t:.1f}s", flush=True)
-with capi.Context(0) as ctx:
-    t = time.time()
-    ctx.upload_graph(g.n, g.m, g.in_offsets, g.in_src, g.in_cum, g.p_of)
-    print(f"upload {time.time()-t:.3f}s graph_bytes={ctx.graph_bytes/1e6:.1f} MB", flush=True)
-    for rep in range(3):
-        with ctx.stream(seed=42, cfg=capi.SamplerCfg(max_attempts=10**12)) as st:
-            ctx.stage_times(reset=True)
-            t = time.time()
-            acc = st.sample_range(0, nb)
-            wall = time.time() - t
-            stg = ctx.stage_times(reset=True)
-            stats = st.stats()
-            k1 = stg["encode"][0] / 1e3
-            print(json.dumps(dict(rep=rep, batches=nb, accepted=acc, wall_s=round(wall, 4),
-                                  stages_ms={k: round(v[0], 3) for k, v in stg.items()},
-                                  stats=stats,
-                                  k1_steps_per_s=stats["steps"] / k1 if k1 else None,
-                                  k1_alg_GBs=stats["alg_bytes"] / k1 / 1e9 if k1 else None,
-                                  hsaw_per_s_wall=acc / wall)), flush=True)
-            if rep == 2:
-                size = acc // 2
-                for kind in (0, 1):
-                    ctx.stage_times(reset=True)
-                    t = time.time()
-                    sol, cov = ctx.greedy(100, stream=st, kind=kind, off=0, cnt=size)
-                    c2 = ctx.coverage_of(sol, stream=st, kind=kind, off=size, cnt=size)
-                    wall = time.time() - t
-                    stg = ctx.stage_times(reset=True)
-                    print(json.dumps(dict(greedy_kind=kind, walks=size, cov=cov, cov_rp=c2,
-                                          wall_s=round(wall, 4), sol_head=sol[:5].tolist(),
-                                          stages_ms={k: round(v[0], 3) for k, v in stg.items()})),
-                          flush=True)
-    print("launches", ctx.launches)
+g = hostapi.Graph.rmat(scale, 16, seed=1)
+p_of = g.random_suspects(max(1, g.n // 100), seed=2)
+print(f"graph n={g.n} m={g.m} gen {time.time()-t:.1f}s knobs={tag}", flush=True)
+t = time.time()
+dg = hostapi.DeviceGraph(g, p_of)
+print(f"upload {time.time()-t:.3f}s", flush=True)
+ctx = capi.Context.borrow(dg.ctx_handle(), g.n, g.m)
+for rep in range(3):
+    with ctx.stream(seed=42, cfg=capi.SamplerCfg(max_attempts=10**12)) as st:
+        ctx.stage_times(reset=True)
+        t = time.time()
+        acc = st.sample_range(0, nb)
+        wall = time.time() - t
+        stg = ctx.stage_times(reset=True)
+        stats = st.stats()
+        k1 = stg["encode"][0] / 1e3
+        if rep:
+            print(json.dumps(dict(rep=rep, accepted=acc, wall_ms=round(wall * 1e3, 2),
+                                  stages_ms={k: round(v[0], 3) for k, v in stg.items() if v[1]},
+                                  k1_Gsteps=round(stats["steps"] / k1 / 1e9, 2),
+                                  k1_alg_GBs=round(stats["alg_bytes"] / k1 / 1e9, 1),
+                                  k2_Gsteps=round(stats["decode_steps"] / stg["decode"][0] / 1e6, 2),
+                                  hsaw_per_s_wall=round(acc / wall / 1e6, 2))), flush=True)
+for rep in range(2):
+    ctx.stage_times(reset=True)
+    r = hostapi.interdict(g, p_of, 0, esia_k, 0.1, 1.0 / g.n, seed=42, max_attempts=10**15, dg=dg,
+                          want_json=True)
+    stg = ctx.stage_times(reset=True)
+    print(json.dumps(dict(esia_rep=rep, timing={k: round(v, 4) for k, v in r["timing"].items()},
+                          it=r["iterations"], samples=r["samples_used"], cov=r["coverage"],
+                          stages_ms={k: round(v[0], 2) for k, v in stg.items() if v[1]})), flush=True)
+t = time.time()
+with hostapi.DeviceGraph(g, p_of) as dg2:
+    t1 = time.time()
+    at, ac = dg2.sample(1_500_000, seed=7, max_attempts=10**15)
+    t2 = time.time()
+print(json.dumps(dict(e2e_upload_s=round(t1 - t, 4), e2e_sample_s=round(t2 - t1, 4),
+                      e2e_total_s=round(time.time() - t, 4), accepted=ac)))
+dg.close()
