@@ -192,6 +192,10 @@ enum {
  * nullable); reset != 0 zeroes the accumulators afterwards. Synchronises the stream. */
 int hsaw_gpu_stage_times(hsaw_gpu_ctx* ctx, double* ms, uint64_t* count, int reset);
 
+/* Process-wide device-allocation counters: out[0] host seconds spent in pool allocations,
+ * out[1] calls, out[2] bytes requested (as doubles). */
+void hsaw_gpu_debug_counters(double* out3);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,8 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_launch_count.argtypes = [vp]
     L.hsaw_gpu_launch_count.restype = C.c_uint64
     L.hsaw_gpu_stage_times.argtypes = [vp, f64p, u64p, C.c_int]
+    L.hsaw_gpu_debug_counters.argtypes = [f64p]
+    L.hsaw_gpu_debug_counters.restype = None
     L.hsaw_gpu_encode_batches.argtypes = [vp, C.POINTER(SamplerCfg), C.c_uint64, C.c_uint64, u64p,
                                           u32p, u32p, u64p]
     L.hsaw_gpu_decode_walks.argtypes = [vp, C.c_uint64, u64p, u32p, u64p, u32p, u32p, u8p]
@@ -113,8 +115,14 @@ EXPORTS = (
     "hsaw_gpu_stream_counters", "hsaw_gpu_stream_local_cut", "hsaw_gpu_stream_slice_edges",
     "hsaw_gpu_stream_export", "hsaw_gpu_stream_stats", "hsaw_gpu_walkset_import",
     "hsaw_gpu_walkset_destroy", "hsaw_gpu_greedy", "hsaw_gpu_coverage_of",
-    "hsaw_gpu_launch_count", "hsaw_gpu_stage_times",
+    "hsaw_gpu_launch_count", "hsaw_gpu_stage_times", "hsaw_gpu_debug_counters",
 )
+
+
+def alloc_counters() -> dict:
+    out = np.zeros(3, dtype=np.float64)
+    lib().hsaw_gpu_debug_counters(_p(out, f64p))
+    return dict(seconds=float(out[0]), calls=int(out[1]), bytes=int(out[2]))
 
 
 @dataclass

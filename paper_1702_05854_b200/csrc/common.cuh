@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <utility>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -72,6 +74,25 @@ inline cudaStream_t& current_stream() {
     return st;
 }
 
+// Host-side cost of pool allocations (debug counters, read through hsaw_gpu_debug_counters).
+struct AllocStats {
+    double seconds = 0;
+    uint64_t calls = 0, bytes = 0;
+};
+inline AllocStats& alloc_stats() {
+    static AllocStats s;
+    return s;
+}
+
+// Allocation sizes are rounded up to 1/8-octave classes (<= 12.5 % slack) so that buffers freed
+// by one round / stream are exact-fit candidates for the next and the pool does not fragment.
+inline uint64_t size_class(uint64_t bytes) {
+    if (bytes <= (1ull << 16)) return 1ull << 16;
+    int top = 63 - __builtin_clzll(bytes);
+    uint64_t step = 1ull << (top - 3);
+    return (bytes + step - 1) & ~(step - 1);
+}
+
 template <class T>
 struct DevVec {
     T* p = nullptr;
@@ -88,9 +109,23 @@ struct DevVec {
         p = nullptr;
         size = cap = 0;
     }
-    static T* alloc(uint64_t count, cudaStream_t st) {
+    void swap(DevVec& o) {
+        std::swap(p, o.p);
+        std::swap(size, o.size);
+        std::swap(cap, o.cap);
+        std::swap(owner, o.owner);
+    }
+    // `count` is rounded up in place to the size class actually allocated.
+    static T* alloc(uint64_t& count, cudaStream_t st) {
         T* np = nullptr;
-        HSAW_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&np), count * sizeof(T), st));
+        uint64_t bytes = size_class(count * sizeof(T));
+        count = bytes / sizeof(T);
+        auto t0 = std::chrono::steady_clock::now();
+        HSAW_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&np), bytes, st));
+        AllocStats& a = alloc_stats();
+        a.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        a.calls += 1;
+        a.bytes += bytes;
         return np;
     }
     // Grows capacity (doubling) preserving the first `size` elements; stream-ordered, no sync.
@@ -126,6 +161,30 @@ struct DevVec {
     }
 };
 
+// Per-chunk scratch of the sample stream (stream.cu). Lives in the context so that consecutive
+// streams on one graph (the doubling loop is re-run per esia() call) reuse it without allocating.
+struct SamplerScratch {
+    DevVec<uint64_t> slot_seed, enc_seed, tmp_off, voff, enc_batch;
+    DevVec<uint32_t> slot_len, count, first, enc_len, enc_seq, tmp_nodes, tmp_edges, vidx;
+    DevVec<uint8_t> status;
+    void release() {
+        slot_seed.release(); enc_seed.release(); tmp_off.release(); voff.release();
+        enc_batch.release(); slot_len.release(); count.release(); first.release();
+        enc_len.release(); enc_seq.release(); tmp_nodes.release(); tmp_edges.release();
+        vidx.release(); status.release();
+    }
+};
+
+// Walk-pool buffers handed back by a destroyed stream, taken over by the next one.
+struct PoolCache {
+    DevVec<uint64_t> edge_off, tag_batch, accepted_after_batch;
+    DevVec<uint32_t> nodes, edges, tag_seq;
+    void release() {
+        edge_off.release(); tag_batch.release(); accepted_after_batch.release();
+        nodes.release(); edges.release(); tag_seq.release();
+    }
+};
+
 }  // namespace hsawgpu
 
 // ---- the context (opaque to C callers) ---------------------------------------------------------
@@ -141,6 +200,8 @@ struct hsaw_gpu_ctx {
     // reusable scratch
     hsawgpu::DevVec<unsigned char> cub_tmp;
     hsawgpu::DevVec<uint32_t> chk_list, chk_counters;  // distinctness-check scratch
+    hsawgpu::SamplerScratch samp;                        // per-chunk sampler scratch
+    hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
     // greedy / coverage scratch (greedy.cu), reused across the doubling iterations
     hsawgpu::DevVec<uint32_t> g_cand_bits, g_cnt, g_fill, g_inv, g_covered, g_solution, g_query_bits;
     hsawgpu::DevVec<uint64_t> g_pos, g_partial, g_gains;
@@ -157,6 +218,8 @@ struct hsaw_gpu_ctx {
     uint64_t stage_launches[HSAW_STAGE_COUNT] = {};
 
     void release_scratch() {
+        samp.release();
+        pool_cache.release();
         cub_tmp.release();
         chk_list.release();
         chk_counters.release();

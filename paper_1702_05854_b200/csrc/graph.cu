@@ -214,6 +214,13 @@ int hsaw_gpu_ctx_sync(hsaw_gpu_ctx* ctx) {
 uint64_t hsaw_gpu_graph_bytes(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->graph_bytes : 0; }
 uint64_t hsaw_gpu_launch_count(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+void hsaw_gpu_debug_counters(double* out3) {
+    const AllocStats& a = alloc_stats();
+    out3[0] = a.seconds;
+    out3[1] = (double)a.calls;
+    out3[2] = (double)a.bytes;
+}
+
 int hsaw_gpu_stage_times(hsaw_gpu_ctx* ctx, double* ms, uint64_t* count, int reset) {
     if (!ctx) return HSAW_EINVAL;
     return guarded(ctx, [&] {

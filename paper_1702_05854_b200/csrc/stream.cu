@@ -131,66 +131,67 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     const uint32_t l = s->cfg.batch_size;
     const uint64_t slots = nb * l;
     if (slots > 0xFFFFFFF0ull) fail(HSAW_EINVAL, "stream: chunk too large for 32-bit walk ids");
+    SamplerScratch& x = ctx->samp;  // chunk scratch is shared by all streams of the context
 
     // ---- K1
-    s->slot_seed.ensure_scratch(slots + 1);
-    s->slot_len.ensure_scratch(slots + 1);
-    s->count.ensure_scratch(nb + 1);
-    s->first.ensure_scratch(nb + 1);
-    HSAW_CUDA_CHECK(cudaMemsetAsync(s->count.p + nb, 0, 4, st));
-    launch_encode(ctx, s->cfg, s->seed + first_batch, nb, s->slot_seed.p, s->slot_len.p,
-                  s->count.p, s->stats.p, s->stats.p + 8);
-    exclusive_sum_u32(ctx, s->count.p, s->first.p, nb + 1);
-    const uint64_t E = read_u32(ctx, s->first.p + nb);  // encoded (heuristically accepted) walks
+    x.slot_seed.ensure_scratch(slots + 1);
+    x.slot_len.ensure_scratch(slots + 1);
+    x.count.ensure_scratch(nb + 1);
+    x.first.ensure_scratch(nb + 1);
+    HSAW_CUDA_CHECK(cudaMemsetAsync(x.count.p + nb, 0, 4, st));
+    launch_encode(ctx, s->cfg, s->seed + first_batch, nb, x.slot_seed.p, x.slot_len.p,
+                  x.count.p, s->stats.p, s->stats.p + 8);
+    exclusive_sum_u32(ctx, x.count.p, x.first.p, nb + 1);
+    const uint64_t E = read_u32(ctx, x.first.p + nb);  // encoded (heuristically accepted) walks
 
     uint64_t A = 0, VT = 0;
-    s->vidx.ensure_scratch(E + 1);
+    x.vidx.ensure_scratch(E + 1);
     if (E > 0) {
         // ---- dense (batch, seq) order
-        s->enc_seed.ensure_scratch(E);
-        s->enc_len.ensure_scratch(E + 1);
-        s->enc_batch.ensure_scratch(E);
-        s->enc_seq.ensure_scratch(E);
-        s->tmp_off.ensure_scratch(E + 1);
+        x.enc_seed.ensure_scratch(E);
+        x.enc_len.ensure_scratch(E + 1);
+        x.enc_batch.ensure_scratch(E);
+        x.enc_seq.ensure_scratch(E);
+        x.tmp_off.ensure_scratch(E + 1);
         {
             StageScope timer(ctx, HSAW_STAGE_COMPACT);
             gather_encoded<<<blocks_for(slots, 256), 256, 0, st>>>(
-                nb, l, first_batch, s->count.p, s->first.p, s->slot_seed.p, s->slot_len.p,
-                s->enc_seed.p, s->enc_len.p, s->enc_batch.p, s->enc_seq.p);
+                nb, l, first_batch, x.count.p, x.first.p, x.slot_seed.p, x.slot_len.p,
+                x.enc_seed.p, x.enc_len.p, x.enc_batch.p, x.enc_seq.p);
             check_launch(ctx, "gather_encoded");
-            HSAW_CUDA_CHECK(cudaMemsetAsync(s->enc_len.p + E, 0, 4, st));
-            exclusive_sum_u32_to_u64(ctx, s->enc_len.p, s->tmp_off.p, E + 1);
+            HSAW_CUDA_CHECK(cudaMemsetAsync(x.enc_len.p + E, 0, 4, st));
+            exclusive_sum_u32_to_u64(ctx, x.enc_len.p, x.tmp_off.p, E + 1);
         }
-        const uint64_t T = read_u64(ctx, s->tmp_off.p + E);  // edges of all encoded walks
+        const uint64_t T = read_u64(ctx, x.tmp_off.p + E);  // edges of all encoded walks
 
         // ---- K2 + K2b
-        s->tmp_nodes.ensure_scratch(T + E);
-        s->tmp_edges.ensure_scratch(T + 1);
-        s->status.ensure_scratch(E);
-        launch_decode(ctx, E, s->enc_seed.p, s->enc_len.p, s->tmp_off.p, s->tmp_nodes.p,
-                      s->tmp_edges.p, s->status.p, s->stats.p, s->stats.p + 8);
-        s->dropped += launch_distinct_check(ctx, E, s->tmp_off.p, s->tmp_nodes.p, s->status.p);
+        x.tmp_nodes.ensure_scratch(T + E);
+        x.tmp_edges.ensure_scratch(T + 1);
+        x.status.ensure_scratch(E);
+        launch_decode(ctx, E, x.enc_seed.p, x.enc_len.p, x.tmp_off.p, x.tmp_nodes.p,
+                      x.tmp_edges.p, x.status.p, s->stats.p, s->stats.p + 8);
+        s->dropped += launch_distinct_check(ctx, E, x.tmp_off.p, x.tmp_nodes.p, x.status.p);
 
         // ---- compaction offsets. The slot arrays are dead after the gather and hold
         // slots + 1 >= E + 1 entries, so they double as the valid-flag / valid-length scan inputs.
-        uint32_t* vflag = s->slot_len.p;
-        uint32_t* vlen = reinterpret_cast<uint32_t*>(s->slot_seed.p);
-        s->voff.ensure_scratch(E + 1);
+        uint32_t* vflag = x.slot_len.p;
+        uint32_t* vlen = reinterpret_cast<uint32_t*>(x.slot_seed.p);
+        x.voff.ensure_scratch(E + 1);
         uint32_t* mismatch = reinterpret_cast<uint32_t*>(s->stats.p + 9);
         HSAW_CUDA_CHECK(cudaMemsetAsync(mismatch, 0, 4, st));
         {
             StageScope timer(ctx, HSAW_STAGE_COMPACT);
-            mark_valid<<<blocks_for(E + 1, 256), 256, 0, st>>>(E, s->status.p, s->enc_len.p, vflag,
+            mark_valid<<<blocks_for(E + 1, 256), 256, 0, st>>>(E, x.status.p, x.enc_len.p, vflag,
                                                                vlen, mismatch);
             check_launch(ctx, "mark_valid");
-            exclusive_sum_u32(ctx, vflag, s->vidx.p, E + 1);
-            exclusive_sum_u32_to_u64(ctx, vlen, s->voff.p, E + 1);
+            exclusive_sum_u32(ctx, vflag, x.vidx.p, E + 1);
+            exclusive_sum_u32_to_u64(ctx, vlen, x.voff.p, E + 1);
         }
         HSAW_CUDA_CHECK(
-            cudaMemcpyAsync(ctx->h_scalars + 1, s->voff.p + E, 8, cudaMemcpyDeviceToHost, st));
+            cudaMemcpyAsync(ctx->h_scalars + 1, x.voff.p + E, 8, cudaMemcpyDeviceToHost, st));
         HSAW_CUDA_CHECK(
             cudaMemcpyAsync(ctx->h_scalars + 2, mismatch, 4, cudaMemcpyDeviceToHost, st));
-        A = read_u32(ctx, s->vidx.p + E);
+        A = read_u32(ctx, x.vidx.p + E);
         VT = ctx->h_scalars[1];
         if (*reinterpret_cast<uint32_t*>(ctx->h_scalars + 2) != 0)
             fail(HSAW_EDATA, "decode: replay disagreed with generation (internal error)");
@@ -205,13 +206,13 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
         {
             StageScope timer(ctx, HSAW_STAGE_COMPACT);
             compact_walks<<<cblocks, 256, 0, st>>>(
-                E, vflag, s->vidx.p, s->voff.p, s->tmp_off.p, s->tmp_nodes.p, s->tmp_edges.p,
-                s->enc_len.p, s->enc_batch.p, s->enc_seq.p, s->accepted, s->total_edges,
+                E, vflag, x.vidx.p, x.voff.p, x.tmp_off.p, x.tmp_nodes.p, x.tmp_edges.p,
+                x.enc_len.p, x.enc_batch.p, x.enc_seq.p, s->accepted, s->total_edges,
                 s->edge_off.p, s->nodes.p, s->edges.p, s->tag_batch.p, s->tag_seq.p);
             check_launch(ctx, "compact_walks");
         }
     } else {
-        HSAW_CUDA_CHECK(cudaMemsetAsync(s->vidx.p, 0, 4, st));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(x.vidx.p, 0, 4, st));
         s->edge_off.reserve(s->accepted + 1, st);
         uint64_t te = s->total_edges;
         HSAW_CUDA_CHECK(
@@ -224,7 +225,7 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->accepted_after_batch.reserve(s->local_batches + nb, st);
     if (E > 0) {
         batch_cumulative<<<blocks_for(nb, 256), 256, 0, st>>>(
-            nb, s->first.p, s->vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches);
+            nb, x.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches);
         check_launch(ctx, "batch_cumulative");
     } else {
         std::vector<uint64_t> flat(nb, s->accepted);
@@ -290,6 +291,16 @@ int hsaw_gpu_stream_create(hsaw_gpu_ctx* ctx, uint64_t seed, const hsaw_sampler_
         try {
             s->stats.ensure_scratch(16);
             HSAW_CUDA_CHECK(cudaMemsetAsync(s->stats.p, 0, 16 * 8, ctx->stream));
+            // recycle the walk-pool buffers of the previous stream on this context, if any
+            PoolCache& pc = ctx->pool_cache;
+            s->edge_off.swap(pc.edge_off);
+            s->nodes.swap(pc.nodes);
+            s->edges.swap(pc.edges);
+            s->tag_batch.swap(pc.tag_batch);
+            s->tag_seq.swap(pc.tag_seq);
+            s->accepted_after_batch.swap(pc.accepted_after_batch);
+            s->edge_off.size = s->nodes.size = s->edges.size = 0;
+            s->tag_batch.size = s->tag_seq.size = s->accepted_after_batch.size = 0;
             s->edge_off.reserve(1024, ctx->stream);
             HSAW_CUDA_CHECK(cudaMemsetAsync(s->edge_off.p, 0, 8, ctx->stream));
             s->edge_off.size = 1;
@@ -306,7 +317,17 @@ void hsaw_gpu_stream_destroy(hsaw_gpu_stream* s) {
     if (!s) return;
     cudaSetDevice(s->ctx->device);
     current_stream() = s->ctx->stream;
-    delete s;  // buffers go back to the pool in stream order
+    // hand the walk-pool buffers to the context for the next stream (keep the larger set)
+    PoolCache& pc = s->ctx->pool_cache;
+    if (s->nodes.cap >= pc.nodes.cap) {
+        pc.edge_off.swap(s->edge_off);
+        pc.nodes.swap(s->nodes);
+        pc.edges.swap(s->edges);
+        pc.tag_batch.swap(s->tag_batch);
+        pc.tag_seq.swap(s->tag_seq);
+        pc.accepted_after_batch.swap(s->accepted_after_batch);
+    }
+    delete s;  // whatever is left goes back to the device pool in stream order
 }
 
 int hsaw_gpu_stream_ensure(hsaw_gpu_stream* s, uint64_t min_accepted) {

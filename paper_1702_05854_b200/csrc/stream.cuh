@@ -29,9 +29,4 @@ struct hsaw_gpu_stream {
     hsawgpu::DevVec<uint64_t> stats;  // u64[8] + cursor scratch
     uint64_t dropped = 0;             // walks removed by the exact recheck
 
-    // per-chunk scratch (reused)
-    hsawgpu::DevVec<uint64_t> slot_seed, enc_seed, tmp_off, voff;
-    hsawgpu::DevVec<uint32_t> slot_len, count, first, enc_len, enc_seq, tmp_nodes, tmp_edges, vidx;
-    hsawgpu::DevVec<uint64_t> enc_batch;
-    hsawgpu::DevVec<uint8_t> status;
 };

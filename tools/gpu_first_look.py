@@ -39,11 +39,12 @@ for rep in range(3):
                                   k1_alg_GBs=round(stats["alg_bytes"] / k1 / 1e9, 1),
                                   k2_Gsteps=round(stats["decode_steps"] / stg["decode"][0] / 1e6, 2),
                                   hsaw_per_s_wall=round(acc / wall / 1e6, 2))), flush=True)
-for rep in range(2):
+for rep in range(5):
     ctx.stage_times(reset=True)
     r = hostapi.interdict(g, p_of, 0, esia_k, 0.1, 1.0 / g.n, seed=42, max_attempts=10**15, dg=dg,
                           want_json=True)
     stg = ctx.stage_times(reset=True)
+    print("alloc", capi.alloc_counters())
     print(json.dumps(dict(esia_rep=rep, timing={k: round(v, 4) for k, v in r["timing"].items()},
                           it=r["iterations"], samples=r["samples_used"], cov=r["coverage"],
                           stages_ms={k: round(v[0], 2) for k, v in stg.items() if v[1]})), flush=True)
