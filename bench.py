@@ -317,14 +317,21 @@ def run_b200(args):
     # ---- eSIA seconds-to-solution on the same config (single GPU path)
     if not args.no_esia and world == 1:
         delta_ = 1.0 / g.n
-        r_dev = hostapi.interdict(g, p_of, 0, args.esia_k, 0.1, delta_, seed=STREAM_SEED,
-                                  max_attempts=10**15, dg=dg, want_json=True)
-        r_e2e = hostapi.interdict(g, p_of, 0, args.esia_k, 0.1, delta_, seed=STREAM_SEED,
-                                  max_attempts=10**15, device=local, want_json=True)
+        runs = [hostapi.interdict(g, p_of, 0, args.esia_k, 0.1, delta_, seed=STREAM_SEED,
+                                  max_attempts=10**15, dg=dg, want_json=True) for _ in range(3)]
+        r_dev = runs[-1]
+        e2e_runs = [hostapi.interdict(g, p_of, 0, args.esia_k, 0.1, delta_, seed=STREAM_SEED,
+                                      max_attempts=10**15, device=local, want_json=True)
+                    for _ in range(2)]
+        r_e2e = e2e_runs[-1]
         out["esia"] = {
             "k": args.esia_k, "epsilon": 0.1, "delta": delta_,
+            # graph resident in HBM; first call pays one-time pool allocations, later calls reuse
             "seconds_to_solution": r_dev["timing"]["wall_time_s"],
+            "seconds_to_solution_first_call": runs[0]["timing"]["wall_time_s"],
+            # host ProbGraph in, InterdictionResult out (upload + context creation inside)
             "seconds_to_solution_e2e": r_e2e["timing"]["wall_time_s"],
+            "seconds_to_solution_e2e_first_call": e2e_runs[0]["timing"]["wall_time_s"],
             "breakdown_s": {k: r_dev["timing"][k] for k in ("sample_s", "greedy_s", "check_s")},
             "iterations": r_dev["iterations"], "samples_used": r_dev["samples_used"],
             "attempts": r_dev["attempts"], "coverage": r_dev["coverage"],
