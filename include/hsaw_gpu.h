@@ -170,6 +170,32 @@ int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                          const uint32_t* cand_ids, uint64_t ncand, const uint32_t* items,
                          uint64_t nitems, uint64_t* coverage);
 
+/* ---- stepwise greedy for sharded (multi-GPU) solves ---------------------------------------- */
+
+/* The rounds of greedy_max_cover split into steps so that ranks holding disjoint shards of R_t can
+ * keep one replicated vector of marginal-gain counts:
+ *   begin   local histogram of this rank's walks [off, off+cnt) into d_counts (DEVICE memory owned
+ *           by the caller, u32[limit + 4], e.g. a torch tensor) + local inverted index;
+ *           the caller then all-reduces d_counts (sum) across ranks, in place;
+ *   select  argmax (largest count, smallest id) over d_counts -> host; identical on every rank;
+ *   cover   marks this rank's uncovered walks containing `item` covered, decrements d_counts for
+ *           their candidate items and appends every decremented item id to d_list (DEVICE, caller
+ *           owned, capacity list_cap >= hsaw_gpu_rounds_occurrences); n_out = entries written;
+ *   apply   replays a peer's decrement list (DEVICE pointer) on this rank's d_counts.
+ * After each round every rank has applied every rank's list, so the replicas stay identical and
+ * the selections equal the single-GPU greedy (proj/src/coverage.cpp:91-138) bit for bit. */
+typedef struct hsaw_gpu_rounds hsaw_gpu_rounds;
+int hsaw_gpu_rounds_begin(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
+                          const hsaw_gpu_walkset* walkset, int kind, uint64_t off, uint64_t cnt,
+                          const uint32_t* cand_ids, uint64_t ncand, uint32_t* d_counts,
+                          hsaw_gpu_rounds** out);
+uint64_t hsaw_gpu_rounds_occurrences(const hsaw_gpu_rounds* g);
+int hsaw_gpu_rounds_select(hsaw_gpu_rounds* g, uint32_t* item, uint64_t* gain);
+int hsaw_gpu_rounds_cover(hsaw_gpu_rounds* g, uint32_t item, uint32_t* d_list, uint64_t list_cap,
+                          uint64_t* n_out);
+int hsaw_gpu_rounds_apply(hsaw_gpu_rounds* g, const uint32_t* d_items, uint64_t n);
+void hsaw_gpu_rounds_end(hsaw_gpu_rounds* g);
+
 /* ---- instrumentation ------------------------------------------------------------------------ */
 
 /* Number of kernel launches this context has issued since creation (bench.py "gpu_launches"). */

@@ -101,6 +101,15 @@ def lib() -> C.CDLL:
                                   C.c_uint32, u32p, u64p]
     L.hsaw_gpu_coverage_of.argtypes = [vp, vp, vp, C.c_int, C.c_uint64, C.c_uint64, u32p,
                                        C.c_uint64, u32p, C.c_uint64, u64p]
+    L.hsaw_gpu_rounds_begin.argtypes = [vp, vp, vp, C.c_int, C.c_uint64, C.c_uint64, u32p,
+                                        C.c_uint64, vp, C.POINTER(vp)]
+    L.hsaw_gpu_rounds_occurrences.argtypes = [vp]
+    L.hsaw_gpu_rounds_occurrences.restype = C.c_uint64
+    L.hsaw_gpu_rounds_select.argtypes = [vp, u32p, u64p]
+    L.hsaw_gpu_rounds_cover.argtypes = [vp, C.c_uint32, vp, C.c_uint64, u64p]
+    L.hsaw_gpu_rounds_apply.argtypes = [vp, vp, C.c_uint64]
+    L.hsaw_gpu_rounds_end.argtypes = [vp]
+    L.hsaw_gpu_rounds_end.restype = None
     _LIB = L
     return L
 
@@ -116,6 +125,8 @@ EXPORTS = (
     "hsaw_gpu_stream_export", "hsaw_gpu_stream_stats", "hsaw_gpu_walkset_import",
     "hsaw_gpu_walkset_destroy", "hsaw_gpu_greedy", "hsaw_gpu_coverage_of",
     "hsaw_gpu_launch_count", "hsaw_gpu_stage_times", "hsaw_gpu_debug_counters",
+    "hsaw_gpu_rounds_begin", "hsaw_gpu_rounds_occurrences", "hsaw_gpu_rounds_select",
+    "hsaw_gpu_rounds_cover", "hsaw_gpu_rounds_apply", "hsaw_gpu_rounds_end",
 )
 
 
@@ -387,3 +398,42 @@ class WalkSet:
 
     def __exit__(self, *a):
         self.close()
+
+
+class Rounds:
+    """hsaw_gpu_rounds: greedy max-cover split into host-visible steps (sharded solves).
+    d_counts / list buffers are raw DEVICE pointers owned by the caller (e.g. torch tensors)."""
+
+    def __init__(self, ctx: Context, d_counts_ptr: int, *, stream=None, walkset=None,
+                 kind=KIND_EDGE, off=0, cnt=0, cand=None):
+        self.ctx, self.L = ctx, ctx.L
+        ca = None if cand is None else np.ascontiguousarray(cand, dtype=np.uint32)
+        if ca is not None and ca.size == 0:
+            ca_ptr, nc = C.cast(C.c_void_p(1), u32p), 0
+        else:
+            ca_ptr, nc = _p(ca, u32p), 0 if ca is None else ca.size
+        self.h = C.c_void_p()
+        ctx._chk(self.L.hsaw_gpu_rounds_begin(ctx.h, stream.h if stream is not None else None,
+                                              walkset.h if walkset is not None else None, kind,
+                                              off, cnt, ca_ptr, nc, C.c_void_p(d_counts_ptr),
+                                              C.byref(self.h)))
+        self.occurrences = int(self.L.hsaw_gpu_rounds_occurrences(self.h))
+
+    def select(self):
+        item, gain = C.c_uint32(), C.c_uint64()
+        self.ctx._chk(self.L.hsaw_gpu_rounds_select(self.h, C.byref(item), C.byref(gain)))
+        return item.value, gain.value
+
+    def cover(self, item: int, d_list_ptr: int, list_cap: int) -> int:
+        n = C.c_uint64()
+        self.ctx._chk(self.L.hsaw_gpu_rounds_cover(self.h, item, C.c_void_p(d_list_ptr), list_cap,
+                                                   C.byref(n)))
+        return n.value
+
+    def apply(self, d_items_ptr: int, n: int):
+        self.ctx._chk(self.L.hsaw_gpu_rounds_apply(self.h, C.c_void_p(d_items_ptr), n))
+
+    def close(self):
+        if self.h:
+            self.L.hsaw_gpu_rounds_end(self.h)
+            self.h = C.c_void_p()

@@ -24,6 +24,10 @@ struct hsaw_gpu_walkset {
 };
 
 namespace {
+struct WalkView;
+}
+
+namespace {
 
 // Walks [w0, w0 + cnt) of either source. Walk w occupies items[off[w] + add*w, off[w+1] + add*(w+1)).
 struct WalkView {
@@ -199,6 +203,68 @@ __global__ void __launch_bounds__(256) count_covered(WalkView v,
         if (__any_sync(kFullMask, hit) && lane == 0) ++mine;
     }
     if (lane == 0 && mine) atomicAdd(out, (unsigned long long)mine);
+}
+
+// ---- stepwise session (sharded solves): the same round split into host-visible steps -----------
+// select_final: reduce the partial maxima to the winner (item, gain) for the host.
+__global__ void __launch_bounds__(256) select_final(const uint64_t* __restrict__ partial,
+                                                    uint32_t npartial, uint64_t* __restrict__ out) {
+    __shared__ uint64_t smem[32];
+    uint64_t best = 0;
+    for (uint32_t i = threadIdx.x; i < npartial; i += blockDim.x) {
+        uint64_t k = partial[i];
+        best = k > best ? k : best;
+    }
+    best = block_max_u64(best, smem);
+    if (threadIdx.x == 0) {
+        out[0] = best >> 32;                                 // gain
+        out[1] = best ? 0xFFFFFFFFu - (uint32_t)best : 0xFFFFFFFFu;  // item
+    }
+}
+
+// cover_item: like cover_winner for a host-chosen item, and every decrement is also appended to
+// `list` (warp-aggregated) so that peer ranks can replay it on their replica of the counts.
+__global__ void __launch_bounds__(256) cover_item(WalkView v, uint32_t item,
+                                                  const uint32_t* __restrict__ cand_bits,
+                                                  const uint64_t* __restrict__ pos,
+                                                  const uint32_t* __restrict__ inv,
+                                                  uint32_t* __restrict__ cnt,
+                                                  uint32_t* __restrict__ covered,
+                                                  uint32_t* __restrict__ list, uint64_t list_cap,
+                                                  unsigned long long* __restrict__ list_count) {
+    uint64_t lb = pos[item], le = pos[item + 1];
+    uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = lb + warp; i < le; i += nwarps) {
+        uint32_t lw = inv[i];
+        uint32_t old = 0;
+        if (lane == 0) old = atomicOr(&covered[lw >> 5], 1u << (lw & 31));
+        old = __shfl_sync(kFullMask, old, 0);
+        if (old & (1u << (lw & 31))) continue;
+        uint64_t w = v.w0 + lw;
+        uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
+        for (uint64_t p0 = b; p0 < e; p0 += 32) {
+            uint64_t p = p0 + lane;
+            uint32_t it = p < e ? v.items[p] : 0xFFFFFFFFu;
+            bool dec = p < e && it < v.limit && is_cand(cand_bits, it);
+            if (dec) atomicSub(&cnt[it], 1u);
+            unsigned m = __ballot_sync(kFullMask, dec);
+            if (m) {
+                unsigned long long base = 0;
+                if (lane == (uint32_t)(__ffs(m) - 1)) base = atomicAdd(list_count, (unsigned long long)__popc(m));
+                base = __shfl_sync(kFullMask, base, __ffs(m) - 1);
+                uint64_t slot = base + __popc(m & ((1u << lane) - 1));
+                if (dec && slot < list_cap) list[slot] = it;
+            }
+        }
+    }
+}
+
+__global__ void apply_decrements(const uint32_t* __restrict__ items, uint64_t n, uint32_t limit,
+                                 uint32_t* __restrict__ cnt) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && items[i] < limit) atomicSub(&cnt[items[i]], 1u);
 }
 
 WalkView make_view(const hsaw_gpu_stream* s, const hsaw_gpu_walkset* ws, int kind, uint64_t off,
@@ -441,6 +507,154 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         }
         *coverage = cov;
     });
+}
+
+// ---- stepwise greedy session -------------------------------------------------------------------
+struct hsaw_gpu_rounds {
+    hsaw_gpu_ctx* ctx = nullptr;
+    WalkView v{};
+    uint32_t limit = 0;
+    uint32_t* d_counts = nullptr;  // caller-owned: global marginal-gain counts after all-reduce
+    bool has_cand = false;
+    DevVec<uint32_t> cand_bits, fill, inv, covered;
+    DevVec<uint64_t> pos, partial, scalars;
+    uint64_t occurrences = 0;
+    uint32_t npartial = 0;
+};
+
+int hsaw_gpu_rounds_begin(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
+                          const hsaw_gpu_walkset* walkset, int kind, uint64_t off, uint64_t cnt,
+                          const uint32_t* cand_ids, uint64_t ncand, uint32_t* d_counts,
+                          hsaw_gpu_rounds** out) {
+    if (!ctx || !out) return HSAW_EINVAL;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        if (!d_counts) fail(HSAW_EINVAL, "greedy_begin: null counts buffer");
+        WalkView v = make_view(stream, walkset, kind, off, cnt);
+        if (cnt > 0xFFFFFFFFull) fail(HSAW_EINVAL, "greedy_begin: more than 2^32 walks");
+        auto* g = new hsaw_gpu_rounds;
+        try {
+            g->ctx = ctx;
+            g->v = v;
+            g->limit = v.limit;
+            g->d_counts = d_counts;
+            g->has_cand = cand_ids != nullptr;
+            cudaStream_t st = ctx->stream;
+            std::vector<uint32_t> sorted;
+            (void)prepare_candidates(ctx, v.limit, cand_ids, ncand, sorted, g->cand_bits);
+            const uint32_t* d_cand = g->has_cand ? g->cand_bits.p : nullptr;
+            const uint64_t limit = v.limit;
+            g->fill.ensure_scratch(limit + 4);
+            g->pos.ensure_scratch(limit + 2);
+            g->scalars.ensure_scratch(4);
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, (limit + 4) * 4, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(g->fill.p, 0, (limit + 4) * 4, st));
+            uint64_t p0 = 0, p1 = 0;
+            if (cnt) view_span(ctx, v, &p0, &p1);
+            const int wide = ctx->sm_count * 8;
+            {
+                StageScope timer(ctx, HSAW_STAGE_INDEX);
+                if (p1 > p0) {
+                    int hb = (int)std::min<uint64_t>((p1 - p0 + 255) / 256, (uint64_t)wide);
+                    item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_counts);
+                    check_launch(ctx, "item_histogram");
+                }
+                exclusive_sum_u32_to_u64(ctx, d_counts, g->pos.p, limit + 1);
+            }
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], g->pos.p + limit, 8,
+                                            cudaMemcpyDeviceToHost, st));
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+            g->occurrences = ctx->h_scalars[0];
+            g->inv.ensure_scratch(g->occurrences + 1);
+            if (g->occurrences) {
+                StageScope timer(ctx, HSAW_STAGE_INDEX);
+                int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
+                scatter_inverted<<<sb, 256, 0, st>>>(v, d_cand, g->pos.p, g->fill.p, g->inv.p);
+                check_launch(ctx, "scatter_inverted");
+            }
+            uint64_t cov_words = (cnt + 31) / 32 + 1;
+            g->covered.ensure_scratch(cov_words);
+            HSAW_CUDA_CHECK(cudaMemsetAsync(g->covered.p, 0, cov_words * 4, st));
+            g->npartial = (uint32_t)std::min<uint64_t>((limit / 4 + 255) / 256 + 1, (uint64_t)wide);
+            g->partial.ensure_scratch(g->npartial);
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+            collect_timings(ctx);
+        } catch (...) {
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+uint64_t hsaw_gpu_rounds_occurrences(const hsaw_gpu_rounds* g) { return g ? g->occurrences : 0; }
+
+int hsaw_gpu_rounds_select(hsaw_gpu_rounds* g, uint32_t* item, uint64_t* gain) {
+    if (!g || !item || !gain) return HSAW_EINVAL;
+    hsaw_gpu_ctx* ctx = g->ctx;
+    return guarded(ctx, [&] {
+        cudaStream_t st = ctx->stream;
+        {
+            StageScope timer(ctx, HSAW_STAGE_ROUNDS);
+            argmax_partial<<<g->npartial, 256, 0, st>>>(g->d_counts, g->limit, g->partial.p);
+            check_launch(ctx, "argmax_partial");
+            select_final<<<1, 256, 0, st>>>(g->partial.p, g->npartial, g->scalars.p);
+            check_launch(ctx, "select_final");
+        }
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], g->scalars.p, 16,
+                                        cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        collect_timings(ctx);
+        *gain = ctx->h_scalars[0];
+        *item = (uint32_t)ctx->h_scalars[1];
+    });
+}
+
+int hsaw_gpu_rounds_cover(hsaw_gpu_rounds* g, uint32_t item, uint32_t* d_list, uint64_t list_cap,
+                          uint64_t* n_out) {
+    if (!g || !n_out) return HSAW_EINVAL;
+    hsaw_gpu_ctx* ctx = g->ctx;
+    return guarded(ctx, [&] {
+        if (item >= g->limit) fail(HSAW_EINVAL, "greedy_cover: item out of range");
+        if (list_cap && !d_list) fail(HSAW_EINVAL, "greedy_cover: null list buffer");
+        cudaStream_t st = ctx->stream;
+        auto* d_count = reinterpret_cast<unsigned long long*>(g->scalars.p + 2);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_count, 0, 8, st));
+        if (g->occurrences) {
+            StageScope timer(ctx, HSAW_STAGE_ROUNDS);
+            cover_item<<<ctx->sm_count * 2, 256, 0, st>>>(
+                g->v, item, g->has_cand ? g->cand_bits.p : nullptr, g->pos.p, g->inv.p,
+                g->d_counts, g->covered.p, d_list, list_cap, d_count);
+            check_launch(ctx, "cover_item");
+        }
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(&ctx->h_scalars[0], d_count, 8, cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        collect_timings(ctx);
+        *n_out = ctx->h_scalars[0];
+        if (*n_out > list_cap) fail(HSAW_EINVAL, "greedy_cover: decrement list buffer too small");
+    });
+}
+
+int hsaw_gpu_rounds_apply(hsaw_gpu_rounds* g, const uint32_t* d_items, uint64_t n) {
+    if (!g) return HSAW_EINVAL;
+    hsaw_gpu_ctx* ctx = g->ctx;
+    return guarded(ctx, [&] {
+        if (n == 0) return;
+        if (!d_items) fail(HSAW_EINVAL, "greedy_apply: null items");
+        StageScope timer(ctx, HSAW_STAGE_ROUNDS);
+        apply_decrements<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(d_items, n, g->limit,
+                                                                              g->d_counts);
+        check_launch(ctx, "apply_decrements");
+    });
+}
+
+void hsaw_gpu_rounds_end(hsaw_gpu_rounds* g) {
+    if (!g) return;
+    cudaSetDevice(g->ctx->device);
+    current_stream() = g->ctx->stream;
+    cudaStreamSynchronize(g->ctx->stream);
+    delete g;
 }
 
 int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,

@@ -1,0 +1,354 @@
+"""Sharded (multi-GPU) eSIA / nSIA: one process per GPU, graph replicated, walks sharded by batch
+range, `torch.distributed` for the plumbing.
+
+What is distributed and what is not:
+  * batches (worker id = seed + b) are independent, so each round's batch range is split into
+    `world` contiguous blocks; rank r samples block r on its GPU and keeps its walks local. The
+    global (batch, seq) order is then round-major, rank-major — exactly the single-stream order
+    (proj/src/sampler.cpp:452-460) — so R_t = global prefix [0, size) and R'_t = [size, 2 size) are
+    *contiguous local ranges* on every rank (`Layout.local_range`).
+  * exchange steps: (1) all-gather of per-block accepted counts after each round (w integers);
+    (2) greedy: one all-reduce(sum) of the marginal-gain count vector per call, then per round an
+    all-gather of the (sparse) decrement lists, so every rank keeps an identical replica of the
+    counts and picks the same winner; (3) scalar all-reduces for coverage_of; (4) one broadcast for
+    counters_for. No walk ever crosses NVLink.
+  * schedule, stopping rule and the doubling loop are the host functions of the single-GPU path
+    (hostapi.schedule / hostapi.check), so results are identical for every world size.
+
+The device work goes through an *engine* (GpuEngine below, on the C-ABI). The orchestration itself
+is engine-agnostic, which is how tests/test_sharded_cpu.py runs it with world_size 2 over gloo on a
+CPU-only box against a test-side engine.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .capi import (HSAW_EBUDGET, HSAW_EDATA, HSAW_EINVAL, HSAW_ERANGE, KIND_EDGE, KIND_NODE,
+                   HsawError)
+
+
+# ---- communication plumbing -----------------------------------------------------------------------
+class Comm:
+    """Thin wrapper over a torch.distributed group (NCCL on GPUs, gloo in CPU tests)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.on = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if self.on else 0
+        self.world = dist.get_world_size(group) if self.on else 1
+        self.backend = dist.get_backend(group) if self.on else "none"
+
+    def _staged(self, t: torch.Tensor) -> torch.Tensor:
+        # gloo cannot all-gather CUDA tensors: stage through the host in that (test-only) setup
+        return t.cpu() if (self.backend == "gloo" and t.is_cuda) else t
+
+    def allgather_ints(self, values: list[int]) -> list[list[int]]:
+        if self.world == 1:
+            return [list(values)]
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        mine = torch.tensor(values, dtype=torch.int64, device=dev)
+        out = [torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(out, mine, group=self.group)
+        return [[int(x) for x in o.tolist()] for o in out]
+
+    def allreduce_sum_(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world == 1:
+            return t
+        s = self._staged(t)
+        dist.all_reduce(s, op=dist.ReduceOp.SUM, group=self.group)
+        if s is not t:
+            t.copy_(s)
+        return t
+
+    def allgather_var(self, t: torch.Tensor) -> list[torch.Tensor]:
+        """All-gather of 1-D tensors of different lengths (lengths first, then padded payloads)."""
+        if self.world == 1:
+            return [t]
+        lens = [x[0] for x in self.allgather_ints([int(t.numel())])]
+        cap = max(max(lens), 1)
+        s = self._staged(t)
+        pad = torch.zeros(cap, dtype=t.dtype, device=s.device)
+        pad[: t.numel()] = s
+        out = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(out, pad, group=self.group)
+        return [o[:n].to(t.device) for o, n in zip(out, lens)]
+
+    def broadcast_ints(self, values: list[int], src: int) -> list[int]:
+        if self.world == 1:
+            return list(values)
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor(values, dtype=torch.int64, device=dev)
+        dist.broadcast(t, src=dist.get_global_rank(self.group, src) if self.group else src,
+                       group=self.group)
+        return [int(x) for x in t.tolist()]
+
+
+# ---- global order bookkeeping (pure host logic) ------------------------------------------------
+@dataclass
+class Round:
+    first_batch: int
+    sizes: list[int]      # batches given to each rank (contiguous blocks, in rank order)
+    accepted: list[int]   # decoded walks each rank's block produced
+
+    def block_start(self, r: int) -> int:
+        return self.first_batch + sum(self.sizes[:r])
+
+
+@dataclass
+class Layout:
+    """Where the global (batch, seq) order lives: per round, per rank."""
+
+    world: int
+    rounds: list[Round] = field(default_factory=list)
+
+    @property
+    def accepted(self) -> int:
+        return sum(sum(r.accepted) for r in self.rounds)
+
+    @property
+    def batches(self) -> int:
+        return sum(sum(r.sizes) for r in self.rounds)
+
+    @staticmethod
+    def split(first_batch: int, batches: int, world: int) -> list[int]:
+        base, rem = divmod(batches, world)
+        return [base + (1 if r < rem else 0) for r in range(world)]
+
+    def count_below(self, rank: int, x: int) -> int:
+        """Number of `rank`'s walks whose global position is < x."""
+        g, total = 0, 0
+        for rd in self.rounds:
+            for r in range(self.world):
+                a = rd.accepted[r]
+                if r == rank:
+                    total += min(max(x - g, 0), a)
+                g += a
+        return total
+
+    def local_range(self, rank: int, off: int, cnt: int) -> tuple[int, int]:
+        """Global walks [off, off+cnt) -> this rank's contiguous local range (offset, count)."""
+        lo = self.count_below(rank, off)
+        return lo, self.count_below(rank, off + cnt) - lo
+
+    def locate(self, target: int):
+        """Block (round index, rank) inside which the cumulative accepted count reaches target,
+        with the global count before that block; None if not materialised."""
+        g = 0
+        for j, rd in enumerate(self.rounds):
+            for r in range(self.world):
+                if g + rd.accepted[r] >= target:
+                    return j, r, g
+                g += rd.accepted[r]
+        return None
+
+
+# ---- the device-side worker of one rank ----------------------------------------------------------
+class GpuEngine:
+    """One rank's GPU through the C-ABI (capi). Buffers exchanged with peers are torch tensors."""
+
+    def __init__(self, ctx, seed: int, cfg=None):
+        from . import capi
+        self.capi, self.ctx = capi, ctx
+        self.cfg = cfg or capi.SamplerCfg()
+        self.batch_size = self.cfg.batch_size
+        self.max_attempts = self.cfg.max_attempts
+        big = capi.SamplerCfg(self.cfg.heuristic, self.cfg.window, self.cfg.batch_size, 2**62)
+        self.stream = ctx.stream(seed=seed, cfg=big)  # the budget is enforced globally, not here
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def close(self):
+        self.stream.close()
+
+    def limit(self, kind: int) -> int:
+        return self.ctx.m if kind == KIND_EDGE else self.ctx.n
+
+    def sample_range(self, first_batch: int, nbatches: int) -> int:
+        return self.stream.sample_range(first_batch, nbatches) if nbatches else 0
+
+    def local_cut(self, min_local: int):
+        return self.stream.local_cut(min_local)
+
+    def coverage_of(self, items, kind, off, cnt, cand) -> int:
+        if cnt == 0:
+            return 0
+        return self.ctx.coverage_of(items, stream=self.stream, kind=kind, off=off, cnt=cnt,
+                                    cand=cand)
+
+    class _Rounds:
+        def __init__(self, eng, kind, off, cnt, cand):
+            self.eng = eng
+            limit = eng.limit(kind)
+            self.counts = torch.zeros(limit + 4, dtype=torch.int32, device=eng.device)
+            torch.cuda.current_stream().synchronize()
+            self.r = eng.capi.Rounds(eng.ctx, self.counts.data_ptr(), stream=eng.stream, kind=kind,
+                                     off=off, cnt=cnt, cand=cand)
+            self.list = torch.empty(max(self.r.occurrences, 1), dtype=torch.int32,
+                                    device=eng.device)
+            torch.cuda.current_stream().synchronize()
+
+        def select(self):
+            torch.cuda.current_stream().synchronize()  # counts may have been all-reduced by torch
+            return self.r.select()
+
+        def cover(self, item) -> torch.Tensor:
+            n = self.r.cover(item, self.list.data_ptr(), self.list.numel())
+            return self.list[:n]
+
+        def apply(self, items: torch.Tensor):
+            if items.numel():
+                items = items.contiguous()
+                torch.cuda.current_stream().synchronize()
+                self.r.apply(items.data_ptr(), items.numel())
+                self.eng.ctx.sync()
+
+        def close(self):
+            self.r.close()
+
+    def begin_rounds(self, kind, off, cnt, cand):
+        return GpuEngine._Rounds(self, kind, off, cnt, cand)
+
+
+# ---- the sharded sample stream + solver ----------------------------------------------------------
+class ShardedSolver:
+    """SampleStream + greedy + the doubling loop over `comm.world` engines (one per process)."""
+
+    def __init__(self, engine, comm: Comm | None = None):
+        self.eng = engine
+        self.comm = comm or Comm()
+        self.layout = Layout(self.comm.world)
+        self.next_batch = 0
+        self.grow = 4096
+        self.local_accepted = 0
+
+    # -- SampleStream::ensure (proj/src/sampler.cpp:388-463), sharded
+    def ensure(self, min_accepted: int):
+        bs, w = self.eng.batch_size, self.comm.world
+        while self.layout.accepted < min_accepted:
+            attempts_so_far = self.next_batch * bs
+            budget_left = max(self.eng.max_attempts - attempts_so_far, 0)
+            max_batches = budget_left // bs
+            if max_batches == 0:
+                raise HsawError(HSAW_EBUDGET, "attempt budget exhausted while sampling walks; "
+                                              "suspects may be unreachable")
+            have = self.layout.accepted
+            if have == 0:
+                batches, self.grow = self.grow, min(self.grow * 8, 1 << 22)
+            else:
+                rate = have / attempts_so_far
+                batches = int((min_accepted - have) / (rate * bs) * 1.1) + 64
+            batches = max(min(batches, max_batches), 1)
+            sizes = Layout.split(self.next_batch, batches, w)
+            rd = Round(self.next_batch, sizes, [0] * w)
+            got = self.eng.sample_range(rd.block_start(self.comm.rank), sizes[self.comm.rank])
+            rd.accepted = [x[0] for x in self.comm.allgather_ints([got])]
+            self.local_accepted += got
+            self.layout.rounds.append(rd)
+            self.next_batch += batches
+
+    # -- SampleStream::counters_for (sampler.cpp:472-482), sharded
+    def counters_for(self, min_accepted: int):
+        if min_accepted == 0:
+            return 0, 0
+        where = self.layout.locate(min_accepted)
+        if where is None:
+            raise HsawError(HSAW_ERANGE, "sample stream target not materialized")
+        j, owner, before = where
+        rd = self.layout.rounds[j]
+        vals = [0, 0]
+        if self.comm.rank == owner:
+            local_before = sum(r.accepted[owner] for r in self.layout.rounds[:j])
+            batches_before = sum(r.sizes[owner] for r in self.layout.rounds[:j])
+            nb, acc = self.eng.local_cut(local_before + (min_accepted - before))
+            in_block = nb - batches_before
+            global_batches = (rd.block_start(owner) + in_block)  # batches are numbered from 0
+            vals = [global_batches * self.eng.batch_size, before + (acc - local_before)]
+        vals = self.comm.broadcast_ints(vals, owner)
+        return vals[0], vals[1]
+
+    # -- CoverageIndex::coverage_of on global walks [off, off+cnt)
+    def coverage_of(self, items, kind, off, cnt, cand=None) -> int:
+        lo, n = self.layout.local_range(self.comm.rank, off, cnt)
+        local = self.eng.coverage_of(items, kind, lo, n, cand)
+        t = torch.tensor([local], dtype=torch.int64)
+        if self.comm.backend == "nccl":
+            t = t.cuda()
+        return int(self.comm.allreduce_sum_(t).item())
+
+    # -- greedy_max_cover on global walks [0, size) (proj/src/coverage.cpp:91-138), sharded
+    def greedy(self, k: int, kind: int, size: int, cand=None):
+        limit = self.eng.limit(kind)
+        cand_sorted = None
+        if cand is not None:
+            ca = np.asarray(cand, dtype=np.int64)
+            if ca.size and (ca.max() >= limit or ca.min() < 0):
+                raise HsawError(HSAW_EDATA, "candidate id out of range")
+            cand_sorted = np.unique(ca)
+        ncand = limit if cand_sorted is None else int(cand_sorted.size)
+        if k > ncand:
+            raise HsawError(HSAW_EINVAL, "budget k exceeds candidate count")
+        lo, n = self.layout.local_range(self.comm.rank, 0, size)
+        rounds = self.eng.begin_rounds(kind, lo, n, cand)
+        try:
+            self.comm.allreduce_sum_(rounds.counts)  # local histograms -> global marginal gains
+            solution, coverage = [], 0
+            while len(solution) < k:
+                item, gain = rounds.select()
+                if gain == 0:
+                    break
+                solution.append(item)
+                coverage += gain
+                mine = rounds.cover(item)
+                for r, lst in enumerate(self.comm.allgather_var(mine)):
+                    if r != self.comm.rank:
+                        rounds.apply(lst)
+        finally:
+            rounds.close()
+        # zero-gain slots: smallest unselected candidates (coverage.cpp:101-106,155)
+        chosen = set(solution)
+        c = 0
+        while len(solution) < k:
+            cid = int(cand_sorted[c]) if cand_sorted is not None else c
+            c += 1
+            if cid not in chosen:
+                solution.append(cid)
+                chosen.add(cid)
+        return solution, coverage
+
+    # -- run_interdiction (proj/src/interdiction.cpp:12-67), sharded
+    def interdict(self, n_nodes: int, kind: int, k: int, eps: float, delta: float, cand=None):
+        from . import hostapi
+        limit = self.eng.limit(kind)
+        if cand is not None:
+            ca = list(cand)
+            if len(ca) == 0:
+                raise HsawError(HSAW_EDATA, "candidate set is empty")
+            if any(c >= limit for c in ca) or len(set(ca)) != len(ca):
+                raise HsawError(HSAW_EDATA, "candidate id out of range or duplicated")
+        csize = limit if cand is None else len(cand)
+        if csize == 0:
+            raise HsawError(HSAW_EDATA, "candidate set is empty")
+        if k < 1 or k > csize:
+            raise HsawError(HSAW_EINVAL, "budget k must be in [1, |C|]")
+        sched = hostapi.schedule(limit, k, eps, delta)
+        lam = sched["lambda_samples"]
+        t = 0
+        while True:
+            t += 1
+            size = lam << (t - 1)
+            self.ensure(2 * size)
+            solution, coverage = self.greedy(k, kind, size, cand)
+            cov_r = self.coverage_of(solution, kind, 0, size, cand)
+            cov_rp = self.coverage_of(solution, kind, size, size, cand)
+            ok, _ = hostapi.check(cov_r, cov_rp, size, limit, k, eps, delta, t)
+            if ok or float(size) >= sched["n_max"]:
+                break
+        attempts, accepted = self.counters_for(2 * size)
+        influence = float(n_nodes) * float(accepted) / float(attempts)
+        return dict(kind="edge" if kind == KIND_EDGE else "node", k=k, epsilon=eps, delta=delta,
+                    solution=[int(x) for x in solution],
+                    est_suspension=influence * float(coverage) / float(size), coverage=coverage,
+                    samples_used=2 * size, attempts=attempts, iterations=t, passed_check=bool(ok))

@@ -1,0 +1,95 @@
+"""TEST INFRASTRUCTURE: a CPU stand-in for sharded.GpuEngine built on the oracle, so that the
+multi-rank orchestration (paper_1702_05854_b200/sharded.py) can run with world_size 2 over gloo on
+a box without GPUs. Same interface as GpuEngine; never used by the product."""
+import numpy as np
+import torch
+
+
+class CpuEngine:
+    def __init__(self, port, csr, seed, batch_size=10, max_attempts=100_000_000):
+        self.port, self.csr, self.seed = port, csr, seed
+        self.batch_size, self.max_attempts = batch_size, max_attempts
+        self.walk_nodes, self.walk_edges = [], []
+        self.accepted_after_batch = []
+        self.last_end = 0
+
+    def close(self):
+        pass
+
+    def limit(self, kind):
+        return self.csr.m if kind == 0 else self.csr.n
+
+    def sample_range(self, first_batch, nbatches):
+        assert first_batch >= self.last_end, "ranges must be increasing"
+        before = len(self.walk_nodes)
+        for b in range(first_batch, first_batch + nbatches):
+            seeds, lens = self.port.thread_sample(self.csr, (self.seed + b) % 2**64,
+                                                  self.batch_size)
+            for s, ln in zip(seeds, lens):
+                dec = self.port.decode(self.csr, int(s), int(ln))
+                if dec is not None:
+                    self.walk_nodes.append(dec[0])
+                    self.walk_edges.append(dec[1])
+            self.accepted_after_batch.append(len(self.walk_nodes))
+        self.last_end = first_batch + nbatches
+        return len(self.walk_nodes) - before
+
+    def local_cut(self, min_local):
+        for i, a in enumerate(self.accepted_after_batch):
+            if a >= min_local:
+                return i + 1, a
+        raise RuntimeError("local cut beyond materialised batches")
+
+    def _items(self, kind, w):
+        return self.walk_edges[w] if kind == 0 else self.walk_nodes[w]
+
+    def coverage_of(self, items, kind, off, cnt, cand):
+        q = set(int(x) for x in items)
+        if cand is not None:
+            q &= set(int(c) for c in cand)
+        return sum(1 for w in range(off, off + cnt) if q.intersection(self._items(kind, w).tolist()))
+
+    class _Rounds:
+        def __init__(self, eng, kind, off, cnt, cand):
+            limit = eng.limit(kind)
+            self.is_cand = np.ones(limit, dtype=bool)
+            if cand is not None:
+                self.is_cand[:] = False
+                self.is_cand[np.asarray(cand, dtype=np.int64)] = True
+            self.walks = [eng._items(kind, w) for w in range(off, off + cnt)]
+            self.walks = [w[self.is_cand[w]] for w in self.walks]
+            self.counts = torch.zeros(limit + 4, dtype=torch.int32)
+            self.by_item = {}
+            for i, w in enumerate(self.walks):
+                for it in w.tolist():
+                    self.counts[it] += 1
+                    self.by_item.setdefault(it, []).append(i)
+            self.covered = np.zeros(len(self.walks), dtype=bool)
+
+        def select(self):
+            c = self.counts.numpy()
+            best = int(c.max())
+            if best <= 0:
+                return 0xFFFFFFFF, 0
+            return int(np.flatnonzero(c == best)[0]), best
+
+        def cover(self, item):
+            out = []
+            for i in self.by_item.get(item, []):
+                if self.covered[i]:
+                    continue
+                self.covered[i] = True
+                for it in self.walks[i].tolist():
+                    self.counts[it] -= 1
+                    out.append(it)
+            return torch.tensor(out, dtype=torch.int32)
+
+        def apply(self, items):
+            for it in items.tolist():
+                self.counts[it] -= 1
+
+        def close(self):
+            pass
+
+    def begin_rounds(self, kind, off, cnt, cand):
+        return CpuEngine._Rounds(self, kind, off, cnt, cand)
