@@ -167,7 +167,14 @@ struct SamplerScratch {
     DevVec<uint64_t> slot_seed, enc_seed, tmp_off, voff, enc_batch;
     DevVec<uint32_t> slot_len, count, first, enc_len, enc_seq, tmp_nodes, tmp_edges, vidx;
     DevVec<uint8_t> status;
+    // fused path: pair-log arena written by K1, per-slot log offsets, per-walk log pointers,
+    // replay space + selection list for walks whose log overflowed
+    DevVec<uint2> arena, replay;
+    DevVec<uint32_t> slot_log, ovf_pairs, sel;
+    DevVec<uint64_t> enc_src;
     void release() {
+        arena.release(); replay.release(); slot_log.release(); ovf_pairs.release();
+        sel.release(); enc_src.release();
         slot_seed.release(); enc_seed.release(); tmp_off.release(); voff.release();
         enc_batch.release(); slot_len.release(); count.release(); first.release();
         enc_len.release(); enc_seq.release(); tmp_nodes.release(); tmp_edges.release();

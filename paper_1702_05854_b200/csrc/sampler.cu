@@ -19,6 +19,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kDefaultEncodeBlocksPerSM = 5;  // 48 registers, no spills (ptxas -v)
+constexpr int kDefaultRecordBlocksPerSM = 4;  // recording variant: see profiles/README.md
 
 struct EncodeParams {
     const NodeRec* nodes;
@@ -33,7 +34,26 @@ struct EncodeParams {
     uint32_t* out_count;
     uint64_t* stats;   // u64[8]
     uint64_t* cursor;  // next batch index of this launch
+    // recording variant (REC): accepted walks are logged as (node, edge id) pairs while they are
+    // generated, so the replay kernel is only needed for the few walks that outgrow their chunk
+    uint2* arena;            // pair log, carved into kLogChunk-pair chunks by atomicAdd
+    uint32_t arena_cap;      // pairs
+    uint32_t* arena_cursor;  // next free chunk (pairs)
+    uint32_t* out_log;       // per (batch, seq) slot: first pair of the walk, or kLogOverflow
 };
+
+constexpr uint32_t kLogChunk = 1024;    // pairs per chunk (8 KB)
+constexpr uint32_t kLogReserve = 256;   // a new attempt starts only with this much room left
+constexpr uint32_t kLogOverflow = 0xFFFFFFFFu;
+
+// 256-bit store of one full 32-byte sector (four pairs).
+__device__ __forceinline__ void store_sector(uint2* dst, uint2 a, uint2 b, uint2 c, uint2 d) {
+    uint64_t x0 = (uint64_t)a.x | ((uint64_t)a.y << 32), x1 = (uint64_t)b.x | ((uint64_t)b.y << 32);
+    uint64_t x2 = (uint64_t)c.x | ((uint64_t)c.y << 32), x3 = (uint64_t)d.x | ((uint64_t)d.y << 32);
+    asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(dst), "l"(x0), "l"(x1), "l"(x2),
+                 "l"(x3)
+                 : "memory");
+}
 
 // WindowFilter (proj/src/sampler.cpp:65-86) as a shift register of the last W pushed nodes: the
 // ring buffer's content is exactly that set, and contains() only asks for membership.
@@ -112,8 +132,26 @@ __device__ __forceinline__ bool claim(uint64_t* cursor, uint64_t total, bool wan
 // ---- K1 ----------------------------------------------------------------------------------------
 // HEUR: 0 Brent, 2 None (CycleHeuristic, proj/include/hsaw/sampler.hpp:46). WIN: window width or
 // -1 for the runtime-width variant.
-template <int HEUR, int WIN, int MINB>
+template <int HEUR, int WIN, int MINB, bool REC>
 __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) {
+    // REC: per-thread staging of four pairs, slot-major so 8-byte accesses are conflict-free
+    __shared__ uint2 stage[REC ? 4 : 1][REC ? kThreads : 1];
+    uint32_t lpos = 0, lend = 0, astart = 0;  // log write position / chunk end / attempt start
+    bool rec_ok = false, arena_dead = false;
+    auto flush = [&](uint32_t base) {
+        store_sector(p.arena + base, stage[0][threadIdx.x], stage[1][threadIdx.x],
+                     stage[2][threadIdx.x], stage[3][threadIdx.x]);
+    };
+    auto log_pair = [&](uint32_t node, uint32_t edge) {
+        if (!REC || !rec_ok) return;
+        if (lpos == lend) {  // the walk outgrew its chunk: it will be replayed instead
+            rec_ok = false;
+            return;
+        }
+        stage[lpos & 3][threadIdx.x] = make_uint2(node, edge);
+        if ((lpos & 3) == 3) flush(lpos & ~3u);
+        ++lpos;
+    };
     const uint32_t lane = threadIdx.x & 31;
     const NodeRec* __restrict__ nodes = p.nodes;
     const EdgeRec* __restrict__ edges = p.edges;
@@ -158,6 +196,22 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             walking = true;
             st_draws += 1;
             st_att += 1;
+            if (REC) {
+                lpos = (lpos + 3) & ~3u;  // every walk starts on a sector boundary
+                if (lend - lpos < kLogReserve && !arena_dead) {
+                    uint32_t base = atomicAdd(p.arena_cursor, kLogChunk);
+                    if (base <= p.arena_cap - kLogChunk) {
+                        lpos = base;
+                        lend = base + kLogChunk;
+                    } else {
+                        arena_dead = true;  // arena exhausted: remaining walks are replayed
+                        lpos = lend = 0;
+                    }
+                }
+                astart = lpos;
+                rec_ok = lend - lpos >= kLogReserve;
+                log_pair(u, kInvalidNode);
+            }
         } else {
             walking = false;
             if (nedges < p.n) {  // len_cap = g.n, sampler.cpp:43,281
@@ -167,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                 bool live = deg != 0 && k < tot;  // graph.hpp:66
                 st_bytes += pick_alg_bytes(deg, live);
                 if (live) {
-                    (void)pick_slot(edges, lo, deg, scale, k, u);
+                    const uint32_t slot_in_row = pick_slot(edges, lo, deg, scale, k, u);
                     bool cyc = win.contains(u);  // sampler.cpp:180
                     if (HEUR == 0 && !cyc) {     // BrentState::check, sampler.cpp:100-108
                         if (u == b_anchor) {
@@ -181,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                     if (!cyc) {
                         ++nedges;  // resolve(), sampler.cpp:54
                         walking = true;
+                        log_pair(u, lo + slot_in_row);
                     }
                 }
             }
@@ -200,6 +255,15 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                 uint64_t slot = (uint64_t)bidx * p.l + cnt;  // seq = index among accepted, :283
                 p.out_seed[slot] = snapshot;
                 p.out_len[slot] = nedges;
+                if (REC) {
+                    if (rec_ok) {
+                        if (lpos & 3) flush(lpos & ~3u);  // last, partially filled sector
+                        p.out_log[slot] = astart;
+                        astart = lpos;                    // keep the walk: later rewinds stop here
+                    } else {
+                        p.out_log[slot] = kLogOverflow;
+                    }
+                }
                 ++cnt;
                 st_acc += 1;
             } else {
@@ -231,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
         }
         if (attempt_done) {
             fresh = true;
+            if (REC) lpos = astart;  // failed attempt: reuse its log space (no-op after accept)
             if (++att == p.l) {
                 p.out_count[bidx] = cnt;
                 have = false;
@@ -268,14 +333,20 @@ struct DecodeParams {
     uint32_t* nnodes;  // nullable: nodes written per walk (only needed for foreign encodings)
     uint64_t* stats;
     uint64_t* cursor;
+    // PAIRS mode (replay of walks whose log overflowed): work item i is walk sel[i] and its
+    // (node, edge id) pairs go to pair_dst[sel[i]]
+    const uint32_t* sel;
+    uint2* const* pair_dst;
 };
 
+template <bool PAIRS>
 __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
     const uint32_t lane = threadIdx.x & 31;
     const NodeRec* __restrict__ nodes = p.nodes;
     const EdgeRec* __restrict__ edges = p.edges;
 
     uint64_t s = 0, w = 0, base = 0;
+    uint2* pairs = nullptr;
     uint32_t lo = 0, deg = 0, len = 0, nedges = 0;
     uint64_t tot = 0, scale = 0;
     bool have = false, fresh = true, drained = false;
@@ -285,10 +356,13 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
         if (!drained) {
             uint64_t mine = 0;
             if (claim(p.cursor, p.nwalks, !have, lane, mine, drained)) {
-                w = mine;
+                w = PAIRS ? p.sel[mine] : mine;
                 s = p.seed[w];
                 len = p.len[w];
-                base = p.edge_off[w];
+                if (PAIRS)
+                    pairs = p.pair_dst[w];
+                else
+                    base = p.edge_off[w];
                 fresh = true;
                 have = true;
             }
@@ -308,7 +382,10 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
                 uint64_t k = draw53(s);
                 u = start_node(k, p.n);
                 nedges = 0;
-                p.out_nodes[base + w] = u;
+                if (PAIRS)
+                    pairs[0] = make_uint2(u, kInvalidNode);
+                else
+                    p.out_nodes[base + w] = u;
                 arrived = true;
             }
         } else {
@@ -322,9 +399,14 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
                     verdict = 2;
                 } else {
                     uint32_t slot = pick_slot(edges, lo, deg, scale, k, u);
-                    p.out_edges[base + nedges] = lo + slot;
-                    ++nedges;
-                    p.out_nodes[base + w + nedges] = u;
+                    if (PAIRS) {
+                        ++nedges;
+                        pairs[nedges] = make_uint2(u, lo + slot);
+                    } else {
+                        p.out_edges[base + nedges] = lo + slot;
+                        ++nedges;
+                        p.out_nodes[base + w + nedges] = u;
+                    }
                     arrived = true;
                 }
             }
@@ -370,6 +452,9 @@ struct CheckParams {
     const uint64_t* edge_off;
     const uint32_t* nodes;
     const uint32_t* nnodes;  // nullable: default len + 1
+    // pair-log source (fused path): walk w = pair_src[w][0 .. lens[w]] (.x = node)
+    const uint2* const* pair_src;
+    const uint32_t* lens;
     uint8_t* status;
     uint32_t* long_list;   // (walk id, node count) pairs needing the long path
     uint32_t* long_count;  // [0] long walks queued, [1] walks dropped (status 1 -> 0)
@@ -380,6 +465,14 @@ __device__ __forceinline__ uint32_t node_hash(uint32_t v, uint32_t bits) {
     return (v * 2654435761u) >> (32 - bits);
 }
 
+template <bool PAIRS>
+__device__ __forceinline__ uint32_t walk_node(const CheckParams& p, uint64_t w, uint64_t base,
+                                              uint32_t i) {
+    if (PAIRS) return p.pair_src[w][i].x;
+    return p.nodes[base + i];
+}
+
+template <bool PAIRS>
 __global__ void __launch_bounds__(kCheckWarps * 32) distinct_kernel(CheckParams p) {
     extern __shared__ uint32_t tables[];  // kCheckWarps x kTableSize
     const uint32_t lane = threadIdx.x & 31;
@@ -391,13 +484,15 @@ __global__ void __launch_bounds__(kCheckWarps * 32) distinct_kernel(CheckParams 
     for (uint64_t w = warp; w < p.nwalks; w += nwarps) {
         uint8_t st = p.status[w];
         if (st == 0) continue;
-        uint64_t base = p.edge_off[w] + w;
-        uint32_t nn = p.nnodes ? p.nnodes[w] : (uint32_t)(p.edge_off[w + 1] - p.edge_off[w]) + 1;
+        uint64_t base = PAIRS ? 0 : p.edge_off[w] + w;
+        uint32_t nn = PAIRS ? p.lens[w] + 1
+                            : (p.nnodes ? p.nnodes[w]
+                                        : (uint32_t)(p.edge_off[w + 1] - p.edge_off[w]) + 1);
         bool dup = false;
         if (nn <= 1) {
             // a single node cannot repeat
         } else if (nn <= 32) {
-            uint32_t v = lane < nn ? p.nodes[base + lane] : 0;
+            uint32_t v = lane < nn ? walk_node<PAIRS>(p, w, base, lane) : 0;
             unsigned valid = nn == 32 ? kFullMask : ((1u << nn) - 1);
             unsigned same = __match_any_sync(kFullMask, v) & valid & ~(1u << lane);
             dup = __any_sync(kFullMask, lane < nn && same != 0);
@@ -408,7 +503,7 @@ __global__ void __launch_bounds__(kCheckWarps * 32) distinct_kernel(CheckParams 
             __syncwarp();
             bool mydup = false;
             for (uint32_t i = lane; i < nn; i += 32) {
-                uint32_t v = p.nodes[base + i];
+                uint32_t v = walk_node<PAIRS>(p, w, base, i);
                 uint32_t h = node_hash(v, bits);
                 for (;;) {
                     uint32_t old = atomicCAS(&tab[h], kInvalidNode, v);
@@ -441,13 +536,14 @@ __global__ void __launch_bounds__(kCheckWarps * 32) distinct_kernel(CheckParams 
 }
 
 // Long walks (> kSmemNodes nodes): one block per walk, hash set in global scratch.
+template <bool PAIRS>
 __global__ void __launch_bounds__(256) distinct_long_kernel(CheckParams p, uint32_t nlong,
                                                             const uint64_t* table_off,
                                                             uint32_t* tables) {
     uint32_t i = blockIdx.x;
     if (i >= nlong) return;
     uint32_t w = p.long_list[2 * i];
-    uint64_t base = p.edge_off[w] + w;
+    uint64_t base = PAIRS ? 0 : p.edge_off[w] + w;
     uint32_t nn = p.long_list[2 * i + 1];
     uint32_t* tab = tables + table_off[i];
     uint64_t size = table_off[i + 1] - table_off[i];  // power of two >= 2*nn
@@ -456,7 +552,7 @@ __global__ void __launch_bounds__(256) distinct_long_kernel(CheckParams p, uint3
     __syncthreads();
     bool mydup = false;
     for (uint32_t j = threadIdx.x; j < nn; j += blockDim.x) {
-        uint32_t v = p.nodes[base + j];
+        uint32_t v = walk_node<PAIRS>(p, w, base, j);
         uint64_t h = node_hash(v, bits);
         for (;;) {
             uint32_t old = atomicCAS(&tab[h], kInvalidNode, v);
@@ -494,13 +590,23 @@ void validate_cfg(const hsaw_sampler_cfg& cfg) {
     if (cfg.batch_size == 0) fail(HSAW_EINVAL, "sampler: batch_size must be positive");
 }
 
+// rec == nullptr: plain encode. Otherwise accepted walks are logged into rec->arena.
 void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t first_worker,
                    uint64_t nbatches, uint64_t* d_seed, uint32_t* d_len, uint32_t* d_count,
-                   uint64_t* d_stats, uint64_t* d_cursor) {
+                   uint64_t* d_stats, uint64_t* d_cursor, const EncodeRecord* rec) {
     if (nbatches == 0) return;
     if (nbatches > 0xFFFFFFFFull) fail(HSAW_EINVAL, "encode: more than 2^32 batches per launch");
     EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, cfg.batch_size, cfg.window,
-                   first_worker, nbatches, d_seed, d_len, d_count, d_stats, d_cursor};
+                   first_worker, nbatches, d_seed, d_len, d_count, d_stats, d_cursor,
+                   nullptr, 0, nullptr, nullptr};
+    if (rec) {
+        if (rec->arena_cap < kLogChunk) fail(HSAW_EINVAL, "encode: record arena too small");
+        p.arena = rec->arena;
+        p.arena_cap = rec->arena_cap;
+        p.arena_cursor = rec->arena_cursor;
+        p.out_log = rec->out_log;
+        HSAW_CUDA_CHECK(cudaMemsetAsync(rec->arena_cursor, 0, 4, ctx->stream));
+    }
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
     auto go = [&](auto kernel) {
         int blocks = persistent_blocks(ctx, kernel, nbatches);
@@ -508,26 +614,42 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
         kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
         check_launch(ctx, "encode_kernel");
     };
-    bool brent = cfg.heuristic == 0;
+    const bool brent = cfg.heuristic == 0;
+    const bool r = rec != nullptr;
     if (cfg.window == 2 && brent) {
         // the default configuration: resident blocks per SM (register budget) is a tuning knob
         static const int occ = [] {
             const char* env = std::getenv("HSAW_K1_BLOCKS_PER_SM");
-            return env ? std::atoi(env) : kDefaultEncodeBlocksPerSM;
+            return env ? std::atoi(env) : 0;
         }();
-        if (occ >= 6)
-            go(encode_kernel<0, 2, 6>);
-        else if (occ == 5)
-            go(encode_kernel<0, 2, 5>);
+        const int want = occ ? occ : (r ? kDefaultRecordBlocksPerSM : kDefaultEncodeBlocksPerSM);
+        if (want >= 6)
+            r ? go(encode_kernel<0, 2, 6, true>) : go(encode_kernel<0, 2, 6, false>);
+        else if (want == 5)
+            r ? go(encode_kernel<0, 2, 5, true>) : go(encode_kernel<0, 2, 5, false>);
         else
-            go(encode_kernel<0, 2, 4>);
+            r ? go(encode_kernel<0, 2, 4, true>) : go(encode_kernel<0, 2, 4, false>);
     } else if (cfg.window == 2) {
-        go(encode_kernel<2, 2, 4>);
+        r ? go(encode_kernel<2, 2, 4, true>) : go(encode_kernel<2, 2, 4, false>);
     } else if (cfg.window == 0) {
-        brent ? go(encode_kernel<0, 0, 4>) : go(encode_kernel<2, 0, 4>);
+        if (brent)
+            r ? go(encode_kernel<0, 0, 4, true>) : go(encode_kernel<0, 0, 4, false>);
+        else
+            r ? go(encode_kernel<2, 0, 4, true>) : go(encode_kernel<2, 0, 4, false>);
     } else {
-        brent ? go(encode_kernel<0, -1, 4>) : go(encode_kernel<2, -1, 4>);
+        if (brent)
+            r ? go(encode_kernel<0, -1, 4, true>) : go(encode_kernel<0, -1, 4, false>);
+        else
+            r ? go(encode_kernel<2, -1, 4, true>) : go(encode_kernel<2, -1, 4, false>);
     }
+}
+
+uint32_t record_chunk_pairs() { return kLogChunk; }
+uint32_t record_overflow_marker() { return kLogOverflow; }
+
+// Lanes of one resident wave of the default recording kernel (each may hold one open chunk).
+uint64_t record_resident_lanes(hsaw_gpu_ctx* ctx) {
+    return (uint64_t)persistent_blocks(ctx, encode_kernel<0, 2, 4, true>, ~0ull >> 8) * kThreads;
 }
 
 static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
@@ -536,11 +658,12 @@ static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_
                                uint32_t* d_nnodes, uint64_t* d_stats, uint64_t* d_cursor) {
     if (nwalks == 0) return;
     DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, nwalks,   d_seed,  d_len,   d_edge_off,
-                   d_nodes,      d_edges,      d_status, d_nnodes, d_stats, d_cursor};
+                   d_nodes,      d_edges,      d_status, d_nnodes, d_stats, d_cursor, nullptr,
+                   nullptr};
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
-    int blocks = persistent_blocks(ctx, decode_kernel, nwalks);
+    int blocks = persistent_blocks(ctx, decode_kernel<false>, nwalks);
     StageScope timer(ctx, HSAW_STAGE_DECODE);
-    decode_kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+    decode_kernel<false><<<blocks, kThreads, 0, ctx->stream>>>(p);
     check_launch(ctx, "decode_kernel");
 }
 
@@ -551,10 +674,28 @@ void launch_decode(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
                        nullptr, d_stats, d_cursor);
 }
 
-// Shared by the stream path (nnodes == nullptr) and decode_walks (foreign encodings).
+// Replay of the `nsel` walks listed in d_sel (indices into the encoded arrays) as pair logs.
+void launch_decode_pairs(hsaw_gpu_ctx* ctx, uint64_t nsel, const uint32_t* d_sel,
+                         const uint64_t* d_seed, const uint32_t* d_len, uint2* const* d_pair_dst,
+                         uint8_t* d_status, uint64_t* d_stats, uint64_t* d_cursor) {
+    if (nsel == 0) return;
+    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, nsel,    d_seed,  d_len,    nullptr,
+                   nullptr,      nullptr,      d_status, nullptr, d_stats, d_cursor, d_sel,
+                   d_pair_dst};
+    HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
+    int blocks = persistent_blocks(ctx, decode_kernel<true>, nsel);
+    StageScope timer(ctx, HSAW_STAGE_DECODE);
+    decode_kernel<true><<<blocks, kThreads, 0, ctx->stream>>>(p);
+    check_launch(ctx, "decode_kernel<pairs>");
+}
+
+// Exact recheck on either node source. Classic: d_edge_off/d_nodes(/d_nnodes). Pair logs:
+// d_pair_src + d_lens.
+template <bool PAIRS>
 static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
                                     const uint64_t* d_edge_off, const uint32_t* d_nodes,
-                                    const uint32_t* d_nnodes, uint8_t* d_status) {
+                                    const uint32_t* d_nnodes, const uint2* const* d_pair_src,
+                                    const uint32_t* d_lens, uint8_t* d_status) {
     if (nwalks == 0) return 0;
     if (nwalks > 0xFFFFFFFFull) fail(HSAW_EINVAL, "distinct check: more than 2^32 walks per call");
     const uint32_t long_cap = 1u << 16;
@@ -562,12 +703,12 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     ctx->chk_counters.ensure_scratch(2);
     uint32_t* counters = ctx->chk_counters.p;
     HSAW_CUDA_CHECK(cudaMemsetAsync(counters, 0, 8, ctx->stream));
-    CheckParams p{nwalks, d_edge_off, d_nodes, d_nnodes, d_status, ctx->chk_list.p, counters,
-                  long_cap};
+    CheckParams p{nwalks,  d_edge_off,      d_nodes,  d_nnodes, d_pair_src, d_lens,
+                  d_status, ctx->chk_list.p, counters, long_cap};
     const int smem = kCheckWarps * kTableSize * 4;
     static bool attr_set = false;
     if (!attr_set) {
-        HSAW_CUDA_CHECK(cudaFuncSetAttribute(distinct_kernel,
+        HSAW_CUDA_CHECK(cudaFuncSetAttribute(distinct_kernel<PAIRS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr_set = true;
     }
@@ -576,7 +717,7 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     int blocks = (int)(want < full ? want : full);
     {
         StageScope timer(ctx, HSAW_STAGE_DISTINCT);
-        distinct_kernel<<<blocks, kCheckWarps * 32, smem, ctx->stream>>>(p);
+        distinct_kernel<PAIRS><<<blocks, kCheckWarps * 32, smem, ctx->stream>>>(p);
         check_launch(ctx, "distinct_kernel");
     }
     uint32_t* h = reinterpret_cast<uint32_t*>(ctx->h_scalars + 32);
@@ -605,7 +746,8 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
                                         cudaMemcpyHostToDevice, ctx->stream));
         {
             StageScope timer(ctx, HSAW_STAGE_DISTINCT);
-            distinct_long_kernel<<<nlong, 256, 0, ctx->stream>>>(p, nlong, d_toff.p, tables.p);
+            distinct_long_kernel<PAIRS><<<nlong, 256, 0, ctx->stream>>>(p, nlong, d_toff.p,
+                                                                        tables.p);
             check_launch(ctx, "distinct_long_kernel");
         }
         HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -616,7 +758,15 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
 
 uint32_t launch_distinct_check(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_edge_off,
                                const uint32_t* d_nodes, uint8_t* d_status) {
-    return distinct_check_impl(ctx, nwalks, d_edge_off, d_nodes, nullptr, d_status);
+    return distinct_check_impl<false>(ctx, nwalks, d_edge_off, d_nodes, nullptr, nullptr, nullptr,
+                                      d_status);
+}
+
+uint32_t launch_distinct_check_pairs(hsaw_gpu_ctx* ctx, uint64_t nwalks,
+                                     const uint2* const* d_pair_src, const uint32_t* d_lens,
+                                     uint8_t* d_status) {
+    return distinct_check_impl<true>(ctx, nwalks, nullptr, nullptr, nullptr, d_pair_src, d_lens,
+                                     d_status);
 }
 
 }  // namespace hsawgpu
@@ -645,7 +795,7 @@ int hsaw_gpu_encode_batches(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg* cfg,
         HSAW_CUDA_CHECK(cudaMemsetAsync(d_seed.p, 0, slots * 8, ctx->stream));
         HSAW_CUDA_CHECK(cudaMemsetAsync(d_len.p, 0, slots * 4, ctx->stream));
         launch_encode(ctx, *cfg, first_worker_id, nbatches, d_seed.p, d_len.p, d_count.p,
-                      d_stats.p, d_stats.p + 8);
+                      d_stats.p, d_stats.p + 8, nullptr);
         HSAW_CUDA_CHECK(
             cudaMemcpyAsync(out_seed, d_seed.p, slots * 8, cudaMemcpyDeviceToHost, ctx->stream));
         HSAW_CUDA_CHECK(
@@ -695,7 +845,8 @@ int hsaw_gpu_decode_walks(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* se
         HSAW_CUDA_CHECK(cudaMemsetAsync(d_edges.p, 0xFF, (total + 1) * 4, st));
         launch_decode_impl(ctx, nwalks, d_seed.p, d_len.p, d_off.p, d_nodes.p, d_edges.p,
                            d_status.p, d_nn.p, d_scal.p, d_scal.p + 8);
-        (void)distinct_check_impl(ctx, nwalks, d_off.p, d_nodes.p, d_nn.p, d_status.p);
+        (void)distinct_check_impl<false>(ctx, nwalks, d_off.p, d_nodes.p, d_nn.p, nullptr, nullptr,
+                                         d_status.p);
         HSAW_CUDA_CHECK(cudaMemcpyAsync(out_nodes, d_nodes.p, (total + nwalks) * 4,
                                         cudaMemcpyDeviceToHost, st));
         if (total)

@@ -4,6 +4,8 @@
 // so prefixes of the pool are pure functions of (graph, suspects, seed) exactly as in the reference.
 #include "stream.cuh"
 
+#include <cstdlib>
+
 #include "sampler.cuh"
 
 using namespace hsawgpu;
@@ -82,6 +84,80 @@ __global__ void compact_walks(uint64_t nwalks, const uint32_t* __restrict__ vfla
         edge_off[base_walk + vidx[nwalks]] = base_edge + voff[nwalks];
 }
 
+// ---- fused path: K1 logged the walks as (node, edge id) pairs while generating them ------------
+// (batch, seq) slots -> dense encoded list, plus where each walk's pair log lives. Walks whose log
+// overflowed get a null source here and are marked for replay.
+__global__ void gather_recorded(uint64_t nbatches, uint32_t l, uint64_t first_global_batch,
+                                const uint32_t* __restrict__ count,
+                                const uint32_t* __restrict__ first,
+                                const uint64_t* __restrict__ slot_seed,
+                                const uint32_t* __restrict__ slot_len,
+                                const uint32_t* __restrict__ slot_log, const uint2* arena,
+                                uint32_t overflow_marker, uint64_t* __restrict__ enc_seed,
+                                uint32_t* __restrict__ enc_len, uint64_t* __restrict__ enc_batch,
+                                uint32_t* __restrict__ enc_seq, const uint2** __restrict__ enc_src,
+                                uint32_t* __restrict__ ovf_pairs) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nbatches * l) return;
+    uint64_t b = i / l;
+    uint32_t j = (uint32_t)(i - b * l);
+    if (j >= count[b]) return;
+    uint32_t dst = first[b] + j;
+    uint32_t len = slot_len[i], lg = slot_log[i];
+    enc_seed[dst] = slot_seed[i];
+    enc_len[dst] = len;
+    enc_batch[dst] = first_global_batch + b;
+    enc_seq[dst] = j;
+    bool ovf = lg == overflow_marker;
+    enc_src[dst] = ovf ? nullptr : arena + lg;
+    ovf_pairs[dst] = ovf ? ((len + 1 + 3) & ~3u) : 0;  // replay space, sector aligned
+}
+
+// Overflowed walks: point them at their slice of the replay buffer and list them for K2.
+__global__ void place_overflow(uint64_t nwalks, const uint32_t* __restrict__ ovf_pairs,
+                               const uint64_t* __restrict__ ovf_off, uint2* replay_base,
+                               const uint2** __restrict__ enc_src, uint32_t* __restrict__ sel,
+                               uint32_t* __restrict__ nsel) {
+    uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwalks || ovf_pairs[w] == 0) return;
+    enc_src[w] = replay_base + ovf_off[w];
+    sel[atomicAdd(nsel, 1u)] = (uint32_t)w;  // order is irrelevant: each entry is independent work
+}
+
+// One warp per decoded walk: pair log -> final node / edge arrays of the pool.
+__global__ void compact_pairs(uint64_t nwalks, const uint32_t* __restrict__ vflag,
+                              const uint32_t* __restrict__ vidx, const uint64_t* __restrict__ voff,
+                              const uint2* const* __restrict__ enc_src,
+                              const uint32_t* __restrict__ enc_len,
+                              const uint64_t* __restrict__ enc_batch,
+                              const uint32_t* __restrict__ enc_seq, uint64_t base_walk,
+                              uint64_t base_edge, uint64_t* __restrict__ edge_off,
+                              uint32_t* __restrict__ nodes, uint32_t* __restrict__ edges,
+                              uint64_t* __restrict__ tag_batch, uint32_t* __restrict__ tag_seq) {
+    uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w = warp; w < nwalks; w += nwarps) {
+        if (!vflag[w]) continue;
+        uint64_t dw = base_walk + vidx[w];
+        uint64_t de = base_edge + voff[w];
+        uint32_t len = enc_len[w];
+        const uint2* src = enc_src[w];
+        if (lane == 0) {
+            edge_off[dw] = de;
+            tag_batch[dw] = enc_batch[w];
+            tag_seq[dw] = enc_seq[w];
+        }
+        for (uint32_t i = lane; i <= len; i += 32) {
+            uint2 pr = src[i];
+            nodes[de + dw + i] = pr.x;
+            if (i) edges[de + i - 1] = pr.y;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        edge_off[base_walk + vidx[nwalks]] = base_edge + voff[nwalks];
+}
+
 // accepted_after_batch (sampler.cpp:459) for the batches of this chunk.
 __global__ void batch_cumulative(uint64_t nbatches, const uint32_t* __restrict__ first,
                                  const uint32_t* __restrict__ vidx, uint64_t base_walk,
@@ -140,7 +216,7 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     x.first.ensure_scratch(nb + 1);
     HSAW_CUDA_CHECK(cudaMemsetAsync(x.count.p + nb, 0, 4, st));
     launch_encode(ctx, s->cfg, s->seed + first_batch, nb, x.slot_seed.p, x.slot_len.p,
-                  x.count.p, s->stats.p, s->stats.p + 8);
+                  x.count.p, s->stats.p, s->stats.p + 8, nullptr);
     exclusive_sum_u32(ctx, x.count.p, x.first.p, nb + 1);
     const uint64_t E = read_u32(ctx, x.first.p + nb);  // encoded (heuristically accepted) walks
 
@@ -246,13 +322,183 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->accepted_after_batch.size = s->local_batches;
 }
 
+// Fused variant of sample_chunk: K1 records the walks while generating them, so the replay kernel
+// only runs for walks that outgrew their log chunk. Same outputs, same order.
+void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
+    hsaw_gpu_ctx* ctx = s->ctx;
+    cudaStream_t st = ctx->stream;
+    const uint32_t l = s->cfg.batch_size;
+    const uint64_t slots = nb * l;
+    if (slots > 0xFFFFFFF0ull) fail(HSAW_EINVAL, "stream: chunk too large for 32-bit walk ids");
+    SamplerScratch& x = ctx->samp;
+
+    // ---- arena sizing: one open chunk per resident lane + the expected volume of accepted walks
+    // (observed pairs per attempt so far, with slack). Too small is safe: overflow -> replay.
+    const uint64_t chunk = record_chunk_pairs();
+    const uint64_t lanes = std::min<uint64_t>(record_resident_lanes(ctx), nb);
+    double per_attempt = s->pairs_per_attempt > 0 ? s->pairs_per_attempt : 24.0;
+    uint64_t want = lanes * chunk + (uint64_t)((double)slots * per_attempt * 1.5) + 64 * chunk;
+    want = std::min<uint64_t>(want, 0xFFFF0000ull);
+    x.arena.ensure_scratch(want);
+    uint32_t arena_cap = (uint32_t)std::min<uint64_t>(x.arena.cap, 0xFFFF0000ull);
+    // test hook: a deliberately tiny arena exercises the "arena exhausted -> replay" path
+    if (const char* env = std::getenv("HSAW_ARENA_MAX_PAIRS")) {
+        uint64_t cap = std::strtoull(env, nullptr, 10);
+        if (cap >= chunk && cap < arena_cap) arena_cap = (uint32_t)cap;
+    }
+
+    // ---- K1 (recording)
+    x.slot_seed.ensure_scratch(slots + 1);
+    x.slot_len.ensure_scratch(slots + 1);
+    x.slot_log.ensure_scratch(slots + 1);
+    x.count.ensure_scratch(nb + 1);
+    x.first.ensure_scratch(nb + 1);
+    HSAW_CUDA_CHECK(cudaMemsetAsync(x.count.p + nb, 0, 4, st));
+    uint32_t* arena_cursor = reinterpret_cast<uint32_t*>(s->stats.p + 10);
+    EncodeRecord rec{x.arena.p, arena_cap, arena_cursor, x.slot_log.p};
+    launch_encode(ctx, s->cfg, s->seed + first_batch, nb, x.slot_seed.p, x.slot_len.p, x.count.p,
+                  s->stats.p, s->stats.p + 8, &rec);
+    exclusive_sum_u32(ctx, x.count.p, x.first.p, nb + 1);
+    HSAW_CUDA_CHECK(
+        cudaMemcpyAsync(ctx->h_scalars + 1, arena_cursor, 4, cudaMemcpyDeviceToHost, st));
+    const uint64_t E = read_u32(ctx, x.first.p + nb);
+    const uint64_t arena_used = *reinterpret_cast<uint32_t*>(ctx->h_scalars + 1);
+    // running estimate for the next chunk's arena (chunk granularity overestimates a little)
+    double seen = (double)arena_used / (double)slots;
+    s->pairs_per_attempt = s->pairs_per_attempt > 0 ? 0.5 * (s->pairs_per_attempt + seen) : seen;
+
+    uint64_t A = 0, VT = 0;
+    x.vidx.ensure_scratch(E + 1);
+    if (E > 0) {
+        x.enc_seed.ensure_scratch(E);
+        x.enc_len.ensure_scratch(E + 1);
+        x.enc_batch.ensure_scratch(E);
+        x.enc_seq.ensure_scratch(E);
+        x.enc_src.ensure_scratch(E);
+        x.ovf_pairs.ensure_scratch(E + 1);
+        x.tmp_off.ensure_scratch(E + 1);
+        x.status.ensure_scratch(E);
+        uint32_t* nsel = reinterpret_cast<uint32_t*>(s->stats.p + 11);
+        {
+            StageScope timer(ctx, HSAW_STAGE_COMPACT);
+            gather_recorded<<<blocks_for(slots, 256), 256, 0, st>>>(
+                nb, l, first_batch, x.count.p, x.first.p, x.slot_seed.p, x.slot_len.p,
+                x.slot_log.p, x.arena.p, record_overflow_marker(), x.enc_seed.p, x.enc_len.p,
+                x.enc_batch.p, x.enc_seq.p, reinterpret_cast<const uint2**>(x.enc_src.p),
+                x.ovf_pairs.p);
+            check_launch(ctx, "gather_recorded");
+            HSAW_CUDA_CHECK(cudaMemsetAsync(x.ovf_pairs.p + E, 0, 4, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(nsel, 0, 4, st));
+            exclusive_sum_u32_to_u64(ctx, x.ovf_pairs.p, x.tmp_off.p, E + 1);
+            // recorded walks are complete by construction
+            HSAW_CUDA_CHECK(cudaMemsetAsync(x.status.p, 1, E, st));
+        }
+        const uint64_t OV = read_u64(ctx, x.tmp_off.p + E);  // pairs to replay (usually 0)
+        if (OV > 0) {
+            x.replay.ensure_scratch(OV);
+            x.sel.ensure_scratch(E);
+            place_overflow<<<blocks_for(E, 256), 256, 0, st>>>(
+                E, x.ovf_pairs.p, x.tmp_off.p, x.replay.p,
+                reinterpret_cast<const uint2**>(x.enc_src.p), x.sel.p, nsel);
+            check_launch(ctx, "place_overflow");
+            const uint64_t nreplay = read_u32(ctx, nsel);
+            launch_decode_pairs(ctx, nreplay, x.sel.p, x.enc_seed.p, x.enc_len.p,
+                                reinterpret_cast<uint2* const*>(x.enc_src.p), x.status.p,
+                                s->stats.p, s->stats.p + 8);
+            s->replayed += nreplay;
+        }
+        // ---- K2b on the pair logs
+        s->dropped += launch_distinct_check_pairs(
+            ctx, E, reinterpret_cast<const uint2* const*>(x.enc_src.p), x.enc_len.p, x.status.p);
+
+        uint32_t* vflag = x.slot_len.p;  // slot arrays are dead after the gather (>= E + 1 entries)
+        uint32_t* vlen = reinterpret_cast<uint32_t*>(x.slot_seed.p);
+        x.voff.ensure_scratch(E + 1);
+        uint32_t* mismatch = reinterpret_cast<uint32_t*>(s->stats.p + 9);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(mismatch, 0, 4, st));
+        {
+            StageScope timer(ctx, HSAW_STAGE_COMPACT);
+            mark_valid<<<blocks_for(E + 1, 256), 256, 0, st>>>(E, x.status.p, x.enc_len.p, vflag,
+                                                               vlen, mismatch);
+            check_launch(ctx, "mark_valid");
+            exclusive_sum_u32(ctx, vflag, x.vidx.p, E + 1);
+            exclusive_sum_u32_to_u64(ctx, vlen, x.voff.p, E + 1);
+        }
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(ctx->h_scalars + 1, x.voff.p + E, 8, cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(ctx->h_scalars + 2, mismatch, 4, cudaMemcpyDeviceToHost, st));
+        A = read_u32(ctx, x.vidx.p + E);
+        VT = ctx->h_scalars[1];
+        if (*reinterpret_cast<uint32_t*>(ctx->h_scalars + 2) != 0)
+            fail(HSAW_EDATA, "decode: replay disagreed with generation (internal error)");
+
+        s->edge_off.reserve(s->accepted + A + 1, st);
+        s->nodes.reserve(s->total_edges + VT + s->accepted + A, st);
+        s->edges.reserve(s->total_edges + VT + 1, st);
+        s->tag_batch.reserve(s->accepted + A + 1, st);
+        s->tag_seq.reserve(s->accepted + A + 1, st);
+        int cblocks = (int)std::min<uint64_t>((E + 7) / 8, (uint64_t)ctx->sm_count * 16);
+        {
+            StageScope timer(ctx, HSAW_STAGE_COMPACT);
+            compact_pairs<<<cblocks, 256, 0, st>>>(
+                E, vflag, x.vidx.p, x.voff.p, reinterpret_cast<const uint2* const*>(x.enc_src.p),
+                x.enc_len.p, x.enc_batch.p, x.enc_seq.p, s->accepted, s->total_edges,
+                s->edge_off.p, s->nodes.p, s->edges.p, s->tag_batch.p, s->tag_seq.p);
+            check_launch(ctx, "compact_pairs");
+        }
+    } else {
+        HSAW_CUDA_CHECK(cudaMemsetAsync(x.vidx.p, 0, 4, st));
+        s->edge_off.reserve(s->accepted + 1, st);
+        uint64_t te = s->total_edges;
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(s->edge_off.p + s->accepted, &te, 8, cudaMemcpyHostToDevice, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+
+    s->accepted_after_batch.size = s->local_batches;
+    s->accepted_after_batch.reserve(s->local_batches + nb, st);
+    if (E > 0) {
+        batch_cumulative<<<blocks_for(nb, 256), 256, 0, st>>>(
+            nb, x.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches);
+        check_launch(ctx, "batch_cumulative");
+    } else {
+        std::vector<uint64_t> flat(nb, s->accepted);
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(s->accepted_after_batch.p + s->local_batches, flat.data(),
+                                        nb * 8, cudaMemcpyHostToDevice, st));
+    }
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+    collect_timings(ctx);
+
+    s->accepted += A;
+    s->total_edges += VT;
+    s->local_batches += nb;
+    s->edge_off.size = s->accepted + 1;
+    s->nodes.size = s->total_edges + s->accepted;
+    s->edges.size = s->total_edges;
+    s->tag_batch.size = s->accepted;
+    s->tag_seq.size = s->accepted;
+    s->accepted_after_batch.size = s->local_batches;
+}
+
+bool fused_enabled() {
+    static const bool on = [] {
+        const char* env = std::getenv("HSAW_FUSED");
+        return env ? std::atoi(env) != 0 : true;
+    }();
+    return on;
+}
+
 void sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches) {
     if (first_batch < s->last_batch_end)
         fail(HSAW_EINVAL, "stream: batch ranges must be issued in increasing order");
     uint64_t done = 0;
     while (done < nbatches) {
         uint64_t nb = std::min(nbatches - done, kMaxChunkBatches);
-        sample_chunk(s, first_batch + done, nb);
+        if (fused_enabled())
+            sample_chunk_fused(s, first_batch + done, nb);
+        else
+            sample_chunk(s, first_batch + done, nb);
         done += nb;
         s->last_batch_end = first_batch + done;
     }
@@ -472,6 +718,7 @@ int hsaw_gpu_stream_stats(const hsaw_gpu_stream* s, uint64_t* stats) {
         HSAW_CUDA_CHECK(cudaStreamSynchronize(s->ctx->stream));
         for (int i = 0; i < 8; ++i) stats[i] = s->ctx->h_scalars[i];
         stats[hsawgpu::ST_DROPPED] = s->dropped;
+        stats[hsawgpu::ST_SPARE] = s->replayed;  // walks that overflowed their log and were replayed
     });
 }
 

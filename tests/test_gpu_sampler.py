@@ -365,3 +365,47 @@ def test_upload_rejects_bad_graphs(ctx, gpu_lib):
     with pytest.raises(gpu_lib.HsawError) as e:
         ctx.upload_graph(3, 2, [0, 2, 2, 2], [1, 2], [0.6, 0.4], [0, 0, 1.0])
     assert e.value.status == gpu_lib.HSAW_EDATA  # cumulative weights decrease
+
+
+# ---- fused recording path (K1 logs walks while generating them) ---------------------------------
+def test_fused_overflow_and_arena_exhaustion(ctx, port, monkeypatch):
+    """Walks that outgrow their log chunk, and walks generated after the arena ran out, must be
+    replayed by K2 and land in the pool exactly like recorded ones."""
+    csr = make_csr(small_graphs()["uniform2000"])
+    upload(ctx, csr)
+    exp = port.stream_samples(csr, 4000, seed=11)
+    monkeypatch.setenv("HSAW_ARENA_MAX_PAIRS", "4096")  # four chunks for thousands of lanes
+    with ctx.stream(seed=11) as st:
+        st.ensure(4000)
+        got = st.to_pool(4000)
+        assert st.stats()["spare"] > 0  # some walks took the replay path
+    pools_equal(got, exp)
+    monkeypatch.delenv("HSAW_ARENA_MAX_PAIRS")
+    with ctx.stream(seed=11) as st:
+        st.ensure(4000)
+        pools_equal(st.to_pool(4000), exp)
+
+
+def test_unfused_path_still_matches(gpu_lib, port, monkeypatch):
+    """HSAW_FUSED=0 keeps the encode -> replay pipeline selectable (A/B measurements)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import numpy as np\n"
+        "from conftest import make_csr\n"
+        "from oracle.oracle import Port\n"
+        "from paper_1702_05854_b200 import capi, rmat\n"
+        "csr = make_csr(rmat.rmat_graph(12, 8, seed=3, suspect_frac=0.02))\n"
+        "exp = Port().stream_samples(csr, 3000, seed=5)\n"
+        "with capi.Context(0) as ctx:\n"
+        "    ctx.upload_graph(csr.n, csr.m, csr.in_offsets, csr.in_src, csr.in_cum, csr.p_of)\n"
+        "    with ctx.stream(seed=5) as st:\n"
+        "        st.ensure(3000); got = st.to_pool(3000)\n"
+        "assert got.attempts == exp.attempts and np.array_equal(got.nodes, exp.nodes)\n"
+        "assert np.array_equal(got.edges, exp.edges) and np.array_equal(got.tag_seq, exp.tag_seq)\n"
+        "print('ok')\n"
+    ) % (__import__("conftest").ROOT, __import__("os").path.join(__import__("conftest").ROOT, "tests"))
+    env = dict(__import__("os").environ, HSAW_FUSED="0")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
