@@ -218,8 +218,8 @@ def run_b200(args):
         one_step()
     barrier()
     ctx.stage_times(reset=True)
-    stats0 = stream.stats()
     launches0 = ctx.launches
+    first_timed_step = step_index[0]
     clocks = ClockSampler(local)
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -233,13 +233,20 @@ def run_b200(args):
     elapsed_ms = ev0.elapsed_time(ev1)
     clock_info = clocks.stop()
     stages = ctx.stage_times(reset=True)
-    stats1 = stream.stats()
     launches = ctx.launches - launches0
-    delta = {k: stats1[k] - stats0[k] for k in stats1}
+    # Algorithmic work of exactly the timed batch ranges, counted by an untimed instrumented pass
+    # (the production kernels run with the counters compiled out).
+    delta = {k: 0 for k in capi.STAT_NAMES}
+    for st_i in range(first_timed_step, first_timed_step + args.steps):
+        first = (st_i * world + rank) * B
+        one = ctx.encode_stats(STREAM_SEED + first, B, cfg)
+        for k in delta:
+            delta[k] += one[k]
+    decode_steps = stream.stats()["decode_steps"]
 
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
-    c = torch.tensor([accepted, delta["attempts"], delta["steps"] + delta["decode_steps"],
-                      launches], dtype=torch.float64, device="cuda")
+    c = torch.tensor([accepted, delta["attempts"], delta["steps"], launches],
+                     dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(c, op=dist.ReduceOp.SUM)

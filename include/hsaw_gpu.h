@@ -86,6 +86,12 @@ int hsaw_gpu_encode_batches(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg* cfg,
                             uint64_t first_worker_id, uint64_t nbatches, uint64_t* out_seed,
                             uint32_t* out_len, uint32_t* out_count, uint64_t* stats);
 
+/* Instrumentation only: the work counters of the same batch range without producing output
+ * (u64[8] as above). Used by bench.py to attribute algorithmic bytes to timed launches whose
+ * production kernels run with counters compiled out. */
+int hsaw_gpu_encode_stats(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg* cfg, uint64_t first_worker_id,
+                          uint64_t nbatches, uint64_t* stats);
+
 /* DecodeContext::decode for an array of encoded walks (proj/src/sampler.cpp:295-338).
  * edge_off u64[nwalks+1] must be the exclusive prefix sum of lens. Walk w gets nodes
  * [edge_off[w]+w, edge_off[w+1]+w+1) and edges [edge_off[w], edge_off[w+1]).
@@ -135,6 +141,10 @@ int hsaw_gpu_stream_slice_edges(const hsaw_gpu_stream* s, uint64_t off, uint64_t
 int hsaw_gpu_stream_export(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
                            uint64_t* edge_off, uint32_t* nodes, uint32_t* edges,
                            uint64_t* tag_worker, uint32_t* tag_seq);
+
+/* Turns the K1 work counters (draws, picks, algorithmic bytes) on or off for this stream. They
+ * cost registers in the hot kernel, so they are off unless requested (or HSAW_STATS=1). */
+int hsaw_gpu_stream_collect_stats(hsaw_gpu_stream* s, int on);
 
 /* Sampler work counters accumulated over the stream's life (u64[8], as in encode_batches; [5] =
  * decode picks, [6] = walks dropped by the exact recheck). */

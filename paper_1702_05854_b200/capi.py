@@ -82,6 +82,7 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_debug_counters.restype = None
     L.hsaw_gpu_encode_batches.argtypes = [vp, C.POINTER(SamplerCfg), C.c_uint64, C.c_uint64, u64p,
                                           u32p, u32p, u64p]
+    L.hsaw_gpu_encode_stats.argtypes = [vp, C.POINTER(SamplerCfg), C.c_uint64, C.c_uint64, u64p]
     L.hsaw_gpu_decode_walks.argtypes = [vp, C.c_uint64, u64p, u32p, u64p, u32p, u32p, u8p]
     L.hsaw_gpu_stream_create.argtypes = [vp, C.c_uint64, C.POINTER(SamplerCfg), C.POINTER(vp)]
     L.hsaw_gpu_stream_destroy.argtypes = [vp]
@@ -94,6 +95,7 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_stream_slice_edges.argtypes = [vp, C.c_uint64, C.c_uint64, u64p]
     L.hsaw_gpu_stream_export.argtypes = [vp, C.c_uint64, C.c_uint64, u64p, u32p, u32p, u64p, u32p]
     L.hsaw_gpu_stream_stats.argtypes = [vp, u64p]
+    L.hsaw_gpu_stream_collect_stats.argtypes = [vp, C.c_int]
     L.hsaw_gpu_walkset_import.argtypes = [vp, C.c_uint32, C.c_uint64, u64p, u32p, C.POINTER(vp)]
     L.hsaw_gpu_walkset_destroy.argtypes = [vp]
     L.hsaw_gpu_walkset_destroy.restype = None
@@ -119,10 +121,11 @@ EXPORTS = (
     "hsaw_gpu_ctx_create", "hsaw_gpu_ctx_destroy", "hsaw_gpu_last_error",
     "hsaw_gpu_ctx_cuda_stream", "hsaw_gpu_ctx_sync", "hsaw_gpu_graph_upload",
     "hsaw_gpu_suspects_upload", "hsaw_gpu_graph_bytes", "hsaw_gpu_encode_batches",
+    "hsaw_gpu_encode_stats",
     "hsaw_gpu_decode_walks", "hsaw_gpu_stream_create", "hsaw_gpu_stream_destroy",
     "hsaw_gpu_stream_ensure", "hsaw_gpu_stream_sample_range", "hsaw_gpu_stream_size",
     "hsaw_gpu_stream_counters", "hsaw_gpu_stream_local_cut", "hsaw_gpu_stream_slice_edges",
-    "hsaw_gpu_stream_export", "hsaw_gpu_stream_stats", "hsaw_gpu_walkset_import",
+    "hsaw_gpu_stream_export", "hsaw_gpu_stream_stats", "hsaw_gpu_stream_collect_stats", "hsaw_gpu_walkset_import",
     "hsaw_gpu_walkset_destroy", "hsaw_gpu_greedy", "hsaw_gpu_coverage_of",
     "hsaw_gpu_launch_count", "hsaw_gpu_stage_times", "hsaw_gpu_debug_counters",
     "hsaw_gpu_rounds_begin", "hsaw_gpu_rounds_occurrences", "hsaw_gpu_rounds_select",
@@ -248,6 +251,14 @@ class Context:
         return (seeds[: nbatches * l].reshape(nbatches, l), lens[: nbatches * l].reshape(nbatches, l),
                 counts[:nbatches], dict(zip(STAT_NAMES, (int(x) for x in stats))))
 
+    def encode_stats(self, first_worker, nbatches, cfg: SamplerCfg | None = None) -> dict:
+        """Work counters (attempts, draws, picks, algorithmic bytes, ...) of a batch range."""
+        cfg = cfg or SamplerCfg()
+        stats = np.zeros(8, dtype=np.uint64)
+        self._chk(self.L.hsaw_gpu_encode_stats(self.h, C.byref(cfg), first_worker, nbatches,
+                                               _p(stats, u64p)))
+        return dict(zip(STAT_NAMES, (int(x) for x in stats)))
+
     def decode_walks(self, seeds, lens):
         seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
         lens = np.ascontiguousarray(lens, dtype=np.uint32)
@@ -348,6 +359,9 @@ class Stream:
         self.ctx._chk(self.L.hsaw_gpu_stream_local_cut(self.h, min_local, C.byref(nb),
                                                        C.byref(ac)))
         return nb.value, ac.value
+
+    def collect_stats(self, on: bool = True):
+        self.ctx._chk(self.L.hsaw_gpu_stream_collect_stats(self.h, int(on)))
 
     def stats(self) -> dict:
         st = np.zeros(8, dtype=np.uint64)

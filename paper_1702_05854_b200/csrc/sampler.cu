@@ -8,6 +8,7 @@
 // whose body is "one draw + at most one edge-record load + one node-record load" for every lane,
 // whatever phase of its walk the lane is in. Lanes that finish refill from a global cursor with a
 // warp-aggregated atomicAdd, so a warp never waits for its longest attempt.
+#include <algorithm>
 #include <cstdlib>
 
 #include "sampler.cuh"
@@ -19,7 +20,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kDefaultEncodeBlocksPerSM = 5;  // 48 registers, no spills (ptxas -v)
-constexpr int kDefaultRecordBlocksPerSM = 4;  // recording variant: see profiles/README.md
+constexpr int kDefaultRecordBlocksPerSM = 5;  // recording, counters off: 48 registers, no spills
 
 struct EncodeParams {
     const NodeRec* nodes;
@@ -42,17 +43,21 @@ struct EncodeParams {
     uint32_t* out_log;       // per (batch, seq) slot: first pair of the walk, or kLogOverflow
 };
 
-constexpr uint32_t kLogChunk = 1024;    // pairs per chunk (8 KB)
-constexpr uint32_t kLogReserve = 256;   // a new attempt starts only with this much room left
+constexpr uint32_t kLogChunk = 2048;    // pairs per chunk (16 KB)
+constexpr uint32_t kLogReserve = 512;   // a new attempt starts only with this much room left
 constexpr uint32_t kLogOverflow = 0xFFFFFFFFu;
 
 // 256-bit store of one full 32-byte sector (four pairs).
+template <bool STREAMING>
 __device__ __forceinline__ void store_sector(uint2* dst, uint2 a, uint2 b, uint2 c, uint2 d) {
     uint64_t x0 = (uint64_t)a.x | ((uint64_t)a.y << 32), x1 = (uint64_t)b.x | ((uint64_t)b.y << 32);
     uint64_t x2 = (uint64_t)c.x | ((uint64_t)c.y << 32), x3 = (uint64_t)d.x | ((uint64_t)d.y << 32);
-    asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(dst), "l"(x0), "l"(x1), "l"(x2),
-                 "l"(x3)
-                 : "memory");
+    if (STREAMING)  // evict-first: the log is written once and read once, keep it out of L2's way
+        asm volatile("st.global.cs.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(dst), "l"(x0), "l"(x1),
+                     "l"(x2), "l"(x3));
+    else
+        asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(dst), "l"(x0), "l"(x1),
+                     "l"(x2), "l"(x3));
 }
 
 // WindowFilter (proj/src/sampler.cpp:65-86) as a shift register of the last W pushed nodes: the
@@ -132,15 +137,17 @@ __device__ __forceinline__ bool claim(uint64_t* cursor, uint64_t total, bool wan
 // ---- K1 ----------------------------------------------------------------------------------------
 // HEUR: 0 Brent, 2 None (CycleHeuristic, proj/include/hsaw/sampler.hpp:46). WIN: window width or
 // -1 for the runtime-width variant.
-template <int HEUR, int WIN, int MINB, bool REC>
+// REC: 0 plain encode, 1 record walks (default stores), 2 record with streaming (.cs) stores.
+// STATS: per-lane work counters (draws, picks, algorithmic bytes) for instrumentation runs.
+template <int HEUR, int WIN, int MINB, int REC, bool STATS>
 __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) {
     // REC: per-thread staging of four pairs, slot-major so 8-byte accesses are conflict-free
     __shared__ uint2 stage[REC ? 4 : 1][REC ? kThreads : 1];
     uint32_t lpos = 0, lend = 0, astart = 0;  // log write position / chunk end / attempt start
     bool rec_ok = false, arena_dead = false;
     auto flush = [&](uint32_t base) {
-        store_sector(p.arena + base, stage[0][threadIdx.x], stage[1][threadIdx.x],
-                     stage[2][threadIdx.x], stage[3][threadIdx.x]);
+        store_sector<REC == 2>(p.arena + base, stage[0][threadIdx.x], stage[1][threadIdx.x],
+                               stage[2][threadIdx.x], stage[3][threadIdx.x]);
     };
     auto log_pair = [&](uint32_t node, uint32_t edge) {
         if (!REC || !rec_ok) return;
@@ -194,8 +201,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             u = start_node(k, p.n);  // sampler.cpp:24
             nedges = 0;
             walking = true;
-            st_draws += 1;
-            st_att += 1;
+            if (STATS) st_draws += 1;
+            if (STATS) st_att += 1;
             if (REC) {
                 lpos = (lpos + 3) & ~3u;  // every walk starts on a sector boundary
                 if (lend - lpos < kLogReserve && !arena_dead) {
@@ -216,10 +223,10 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             walking = false;
             if (nedges < p.n) {  // len_cap = g.n, sampler.cpp:43,281
                 uint64_t k = draw53(s);
-                st_draws += 1;
-                st_steps += 1;
+                if (STATS) st_draws += 1;
+                if (STATS) st_steps += 1;
                 bool live = deg != 0 && k < tot;  // graph.hpp:66
-                st_bytes += pick_alg_bytes(deg, live);
+                if (STATS) st_bytes += pick_alg_bytes(deg, live);
                 if (live) {
                     const uint32_t slot_in_row = pick_slot(edges, lo, deg, scale, k, u);
                     bool cyc = win.contains(u);  // sampler.cpp:180
@@ -244,11 +251,11 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
         bool attempt_done = true;
         if (walking) {
             NodeRec rec = load_node(nodes, u);
-            st_bytes += 8;  // p_of[u]
+            if (STATS) st_bytes += 8;  // p_of[u]
             bool accepted = false;
             if (rec.acc_thr != 0) {  // is_suspect, sampler.cpp:32,55
                 uint64_t k2 = draw53(s);
-                st_draws += 1;
+                if (STATS) st_draws += 1;
                 accepted = k2 < rec.acc_thr;  // r <= p_of[u], sampler.cpp:34,57
             }
             if (accepted) {
@@ -265,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                     }
                 }
                 ++cnt;
-                st_acc += 1;
+                if (STATS) st_acc += 1;
             } else {
                 lo = rec.lo;
                 deg = rec.deg;
@@ -285,9 +292,9 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                     // the length cap stops it before drawing: settle it now, saving an iteration.
                     if (nedges < p.n) {
                         (void)prg_next(s);
-                        st_draws += 1;
-                        st_steps += 1;
-                        st_bytes += 16;
+                        if (STATS) st_draws += 1;
+                        if (STATS) st_steps += 1;
+                        if (STATS) st_bytes += 16;
                     }
                     attempt_done = true;
                 }
@@ -305,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
         }
     }
 
+    if (!STATS) return;
     const uint64_t w_draws = warp_sum(st_draws), w_steps = warp_sum(st_steps);
     const uint64_t w_bytes = warp_sum(st_bytes), w_att = warp_sum(st_att);
     const uint64_t w_acc = warp_sum(st_acc);
@@ -593,7 +601,8 @@ void validate_cfg(const hsaw_sampler_cfg& cfg) {
 // rec == nullptr: plain encode. Otherwise accepted walks are logged into rec->arena.
 void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t first_worker,
                    uint64_t nbatches, uint64_t* d_seed, uint32_t* d_len, uint32_t* d_count,
-                   uint64_t* d_stats, uint64_t* d_cursor, const EncodeRecord* rec) {
+                   uint64_t* d_stats, uint64_t* d_cursor, const EncodeRecord* rec,
+                   bool with_stats) {
     if (nbatches == 0) return;
     if (nbatches > 0xFFFFFFFFull) fail(HSAW_EINVAL, "encode: more than 2^32 batches per launch");
     EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, cfg.batch_size, cfg.window,
@@ -615,41 +624,55 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
         check_launch(ctx, "encode_kernel");
     };
     const bool brent = cfg.heuristic == 0;
-    const bool r = rec != nullptr;
     if (cfg.window == 2 && brent) {
-        // the default configuration: resident blocks per SM (register budget) is a tuning knob
-        static const int occ = [] {
+        // The default configuration gets the tuned variants: resident blocks per SM (register
+        // budget), recording mode and instrumentation are compile-time parameters.
+        static const int occ_env = [] {
             const char* env = std::getenv("HSAW_K1_BLOCKS_PER_SM");
             return env ? std::atoi(env) : 0;
         }();
-        const int want = occ ? occ : (r ? kDefaultRecordBlocksPerSM : kDefaultEncodeBlocksPerSM);
-        if (want >= 6)
-            r ? go(encode_kernel<0, 2, 6, true>) : go(encode_kernel<0, 2, 6, false>);
-        else if (want == 5)
-            r ? go(encode_kernel<0, 2, 5, true>) : go(encode_kernel<0, 2, 5, false>);
-        else
-            r ? go(encode_kernel<0, 2, 4, true>) : go(encode_kernel<0, 2, 4, false>);
-    } else if (cfg.window == 2) {
-        r ? go(encode_kernel<2, 2, 4, true>) : go(encode_kernel<2, 2, 4, false>);
-    } else if (cfg.window == 0) {
-        if (brent)
-            r ? go(encode_kernel<0, 0, 4, true>) : go(encode_kernel<0, 0, 4, false>);
-        else
-            r ? go(encode_kernel<2, 0, 4, true>) : go(encode_kernel<2, 0, 4, false>);
+        static const int store_mode = [] {  // 1 default stores, 2 streaming (.cs) stores
+            const char* env = std::getenv("HSAW_LOG_STORE");
+            return env && std::atoi(env) == 1 ? 1 : 2;
+        }();
+        const int mode = rec ? store_mode : 0;
+        const bool five = (occ_env ? occ_env : (rec ? kDefaultRecordBlocksPerSM
+                                                    : kDefaultEncodeBlocksPerSM)) >= 5;
+        const int key = mode * 4 + (five ? 2 : 0) + (with_stats ? 1 : 0);
+        switch (key) {
+            case 0: go(encode_kernel<0, 2, 4, 0, false>); break;
+            case 1: go(encode_kernel<0, 2, 4, 0, true>); break;
+            case 2: go(encode_kernel<0, 2, 5, 0, false>); break;
+            case 3: go(encode_kernel<0, 2, 5, 0, true>); break;
+            case 4: go(encode_kernel<0, 2, 4, 1, false>); break;
+            case 5: go(encode_kernel<0, 2, 4, 1, true>); break;
+            case 6: go(encode_kernel<0, 2, 5, 1, false>); break;
+            case 7: go(encode_kernel<0, 2, 5, 1, true>); break;
+            case 8: go(encode_kernel<0, 2, 4, 2, false>); break;
+            case 9: go(encode_kernel<0, 2, 4, 2, true>); break;
+            case 10: go(encode_kernel<0, 2, 5, 2, false>); break;
+            default: go(encode_kernel<0, 2, 5, 2, true>); break;
+        }
     } else {
-        if (brent)
-            r ? go(encode_kernel<0, -1, 4, true>) : go(encode_kernel<0, -1, 4, false>);
+        // other SamplerConfig values: correctness paths, instrumented, never recording
+        if (rec) fail(HSAW_EINVAL, "encode: recording is only built for the default sampler config");
+        if (cfg.window == 2)
+            go(encode_kernel<2, 2, 4, 0, true>);
+        else if (cfg.window == 0)
+            brent ? go(encode_kernel<0, 0, 4, 0, true>) : go(encode_kernel<2, 0, 4, 0, true>);
         else
-            r ? go(encode_kernel<2, -1, 4, true>) : go(encode_kernel<2, -1, 4, false>);
+            brent ? go(encode_kernel<0, -1, 4, 0, true>) : go(encode_kernel<2, -1, 4, 0, true>);
     }
 }
+
+bool record_supported(const hsaw_sampler_cfg& cfg) { return cfg.heuristic == 0 && cfg.window == 2; }
 
 uint32_t record_chunk_pairs() { return kLogChunk; }
 uint32_t record_overflow_marker() { return kLogOverflow; }
 
 // Lanes of one resident wave of the default recording kernel (each may hold one open chunk).
 uint64_t record_resident_lanes(hsaw_gpu_ctx* ctx) {
-    return (uint64_t)persistent_blocks(ctx, encode_kernel<0, 2, 4, true>, ~0ull >> 8) * kThreads;
+    return (uint64_t)persistent_blocks(ctx, encode_kernel<0, 2, 4, 2, false>, ~0ull >> 8) * kThreads;
 }
 
 static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
@@ -795,7 +818,7 @@ int hsaw_gpu_encode_batches(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg* cfg,
         HSAW_CUDA_CHECK(cudaMemsetAsync(d_seed.p, 0, slots * 8, ctx->stream));
         HSAW_CUDA_CHECK(cudaMemsetAsync(d_len.p, 0, slots * 4, ctx->stream));
         launch_encode(ctx, *cfg, first_worker_id, nbatches, d_seed.p, d_len.p, d_count.p,
-                      d_stats.p, d_stats.p + 8, nullptr);
+                      d_stats.p, d_stats.p + 8, nullptr, true);
         HSAW_CUDA_CHECK(
             cudaMemcpyAsync(out_seed, d_seed.p, slots * 8, cudaMemcpyDeviceToHost, ctx->stream));
         HSAW_CUDA_CHECK(
@@ -806,6 +829,36 @@ int hsaw_gpu_encode_batches(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg* cfg,
             HSAW_CUDA_CHECK(
                 cudaMemcpyAsync(stats, d_stats.p, 64, cudaMemcpyDeviceToHost, ctx->stream));
         HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int hsaw_gpu_encode_stats(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg* cfg, uint64_t first_worker_id,
+                          uint64_t nbatches, uint64_t* stats) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (!cfg || !stats) fail(HSAW_EINVAL, "encode_stats: null argument");
+        if (!ctx->g.nodes) fail(HSAW_EINVAL, "encode_stats: no graph uploaded");
+        validate_cfg(*cfg);
+        for (int i = 0; i < 8; ++i) stats[i] = 0;
+        if (nbatches == 0) return;
+        const uint64_t kChunk = 1ull << 22;
+        DevVec<uint64_t> d_seed, d_stats;
+        DevVec<uint32_t> d_len, d_count;
+        uint64_t per = std::min(nbatches, kChunk);
+        d_seed.ensure_scratch(per * cfg->batch_size);
+        d_len.ensure_scratch(per * cfg->batch_size);
+        d_count.ensure_scratch(per);
+        d_stats.ensure_scratch(9);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_stats.p, 0, 72, ctx->stream));
+        for (uint64_t done = 0; done < nbatches; done += per) {
+            uint64_t nb = std::min(per, nbatches - done);
+            launch_encode(ctx, *cfg, first_worker_id + done, nb, d_seed.p, d_len.p, d_count.p,
+                          d_stats.p, d_stats.p + 8, nullptr, true);
+        }
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(ctx->h_scalars, d_stats.p, 64, cudaMemcpyDeviceToHost,
+                                        ctx->stream));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < 8; ++i) stats[i] = ctx->h_scalars[i];
     });
 }
 

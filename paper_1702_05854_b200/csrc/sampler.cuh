@@ -29,7 +29,10 @@ uint64_t record_resident_lanes(hsaw_gpu_ctx* ctx);
 
 void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t first_worker,
                    uint64_t nbatches, uint64_t* d_seed, uint32_t* d_len, uint32_t* d_count,
-                   uint64_t* d_stats, uint64_t* d_cursor, const EncodeRecord* rec);
+                   uint64_t* d_stats, uint64_t* d_cursor, const EncodeRecord* rec,
+                   bool with_stats);
+// Recording is built for the default SamplerConfig (Brent + window 2) only.
+bool record_supported(const hsaw_sampler_cfg& cfg);
 
 // K2: replay nwalks encoded walks into nodes/edges at edge_off (exclusive sum of lens).
 // d_status[w]: 1 replayed, 2 mismatch. d_cursor: one zeroed u64 of scratch.

@@ -216,7 +216,7 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     x.first.ensure_scratch(nb + 1);
     HSAW_CUDA_CHECK(cudaMemsetAsync(x.count.p + nb, 0, 4, st));
     launch_encode(ctx, s->cfg, s->seed + first_batch, nb, x.slot_seed.p, x.slot_len.p,
-                  x.count.p, s->stats.p, s->stats.p + 8, nullptr);
+                  x.count.p, s->stats.p, s->stats.p + 8, nullptr, s->collect_stats);
     exclusive_sum_u32(ctx, x.count.p, x.first.p, nb + 1);
     const uint64_t E = read_u32(ctx, x.first.p + nb);  // encoded (heuristically accepted) walks
 
@@ -357,7 +357,7 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     uint32_t* arena_cursor = reinterpret_cast<uint32_t*>(s->stats.p + 10);
     EncodeRecord rec{x.arena.p, arena_cap, arena_cursor, x.slot_log.p};
     launch_encode(ctx, s->cfg, s->seed + first_batch, nb, x.slot_seed.p, x.slot_len.p, x.count.p,
-                  s->stats.p, s->stats.p + 8, &rec);
+                  s->stats.p, s->stats.p + 8, &rec, s->collect_stats);
     exclusive_sum_u32(ctx, x.count.p, x.first.p, nb + 1);
     HSAW_CUDA_CHECK(
         cudaMemcpyAsync(ctx->h_scalars + 1, arena_cursor, 4, cudaMemcpyDeviceToHost, st));
@@ -495,7 +495,7 @@ void sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches) {
     uint64_t done = 0;
     while (done < nbatches) {
         uint64_t nb = std::min(nbatches - done, kMaxChunkBatches);
-        if (fused_enabled())
+        if (fused_enabled() && record_supported(s->cfg))
             sample_chunk_fused(s, first_batch + done, nb);
         else
             sample_chunk(s, first_batch + done, nb);
@@ -534,6 +534,7 @@ int hsaw_gpu_stream_create(hsaw_gpu_ctx* ctx, uint64_t seed, const hsaw_sampler_
         s->ctx = ctx;
         s->seed = seed;
         s->cfg = *cfg;
+        if (const char* env = std::getenv("HSAW_STATS")) s->collect_stats = std::atoi(env) != 0;
         try {
             s->stats.ensure_scratch(16);
             HSAW_CUDA_CHECK(cudaMemsetAsync(s->stats.p, 0, 16 * 8, ctx->stream));
@@ -710,6 +711,12 @@ int hsaw_gpu_stream_export(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
     });
 }
 
+int hsaw_gpu_stream_collect_stats(hsaw_gpu_stream* s, int on) {
+    if (!s) return HSAW_EINVAL;
+    s->collect_stats = on != 0;
+    return HSAW_OK;
+}
+
 int hsaw_gpu_stream_stats(const hsaw_gpu_stream* s, uint64_t* stats) {
     if (!s || !stats) return HSAW_EINVAL;
     return guarded(s->ctx, [&] {
@@ -717,6 +724,10 @@ int hsaw_gpu_stream_stats(const hsaw_gpu_stream* s, uint64_t* stats) {
                                         s->ctx->stream));
         HSAW_CUDA_CHECK(cudaStreamSynchronize(s->ctx->stream));
         for (int i = 0; i < 8; ++i) stats[i] = s->ctx->h_scalars[i];
+        if (!s->collect_stats) {  // work counters were not collected: fill what the host knows
+            stats[hsawgpu::ST_ATTEMPTS] = s->local_batches * s->cfg.batch_size;
+            stats[hsawgpu::ST_ACCEPTED] = s->accepted + s->dropped;
+        }
         stats[hsawgpu::ST_DROPPED] = s->dropped;
         stats[hsawgpu::ST_SPARE] = s->replayed;  // walks that overflowed their log and were replayed
     });

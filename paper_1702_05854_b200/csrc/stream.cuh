@@ -28,6 +28,7 @@ struct hsaw_gpu_stream {
 
     hsawgpu::DevVec<uint64_t> stats;  // u64[8] + cursor scratch
     uint64_t dropped = 0;             // walks removed by the exact recheck
+    bool collect_stats = false;       // K1 work counters (draws/picks/bytes): instrumentation only
     uint64_t replayed = 0;            // fused path: walks whose log overflowed (replayed by K2)
     double pairs_per_attempt = 0;     // fused path: running arena-volume estimate
 

@@ -25,21 +25,27 @@ print(f"upload {time.time()-t:.3f}s", flush=True)
 ctx = capi.Context.borrow(dg.ctx_handle(), g.n, g.m)
 for rep in range(3):
     with ctx.stream(seed=42, cfg=capi.SamplerCfg(max_attempts=10**12)) as st:
+        st.collect_stats(os.environ.get("LOOK_STATS", "0") == "1")
         ctx.stage_times(reset=True)
         t = time.time()
         acc = st.sample_range(0, nb)
         wall = time.time() - t
         stg = ctx.stage_times(reset=True)
         stats = st.stats()
+        if not stats["steps"]:
+            ws = ctx.encode_stats(42, nb)
+            stats["steps"], stats["alg_bytes"] = ws["steps"], ws["alg_bytes"]
+            ctx.stage_times(reset=True)
         k1 = stg["encode"][0] / 1e3
         if rep:
             print(json.dumps(dict(rep=rep, accepted=acc, wall_ms=round(wall * 1e3, 2),
                                   stages_ms={k: round(v[0], 3) for k, v in stg.items() if v[1]},
                                   k1_Gsteps=round(stats["steps"] / k1 / 1e9, 2),
                                   k1_alg_GBs=round(stats["alg_bytes"] / k1 / 1e9, 1),
-                                  k2_Gsteps=round(stats["decode_steps"] / stg["decode"][0] / 1e6, 2),
-                                  hsaw_per_s_wall=round(acc / wall / 1e6, 2))), flush=True)
-for rep in range(5):
+                                  
+                                  hsaw_per_s_wall=round(acc / wall / 1e6, 2), replayed=stats['spare'],
+                                  dropped=stats['dropped'])), flush=True)
+for rep in range(3):
     ctx.stage_times(reset=True)
     r = hostapi.interdict(g, p_of, 0, esia_k, 0.1, 1.0 / g.n, seed=42, max_attempts=10**15, dg=dg,
                           want_json=True)
