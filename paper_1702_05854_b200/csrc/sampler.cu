@@ -46,6 +46,7 @@ struct EncodeParams {
 constexpr uint32_t kLogChunk = 2048;    // pairs per chunk (16 KB)
 constexpr uint32_t kLogReserve = 512;   // a new attempt starts only with this much room left
 constexpr uint32_t kLogOverflow = 0xFFFFFFFFu;
+constexpr uint32_t kStage = 16;         // pairs staged per thread in shared memory (128 bytes)
 
 // 256-bit store of one full 32-byte sector (four pairs).
 template <bool STREAMING>
@@ -141,13 +142,20 @@ __device__ __forceinline__ bool claim(uint64_t* cursor, uint64_t total, bool wan
 // STATS: per-lane work counters (draws, picks, algorithmic bytes) for instrumentation runs.
 template <int HEUR, int WIN, int MINB, int REC, bool STATS>
 __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) {
-    // REC: per-thread staging of four pairs, slot-major so 8-byte accesses are conflict-free
-    __shared__ uint2 stage[REC ? 4 : 1][REC ? kThreads : 1];
+    // REC: every thread stages kStage pairs (128 bytes) in shared memory, slot-major so the
+    // 8-byte accesses are conflict-free, and flushes whole 128-byte lines: short failed attempts
+    // never reach global memory and the log stream stays burst-friendly for HBM.
+    __shared__ uint2 stage[REC ? kStage : 1][REC ? kThreads : 1];
     uint32_t lpos = 0, lend = 0, astart = 0;  // log write position / chunk end / attempt start
     bool rec_ok = false, arena_dead = false;
-    auto flush = [&](uint32_t base) {
-        store_sector<REC == 2>(p.arena + base, stage[0][threadIdx.x], stage[1][threadIdx.x],
-                               stage[2][threadIdx.x], stage[3][threadIdx.x]);
+    // writes the staged pairs of line `base` (kStage-aligned), sectors [0, nsect)
+    auto flush = [&](uint32_t base, uint32_t nsect) {
+#pragma unroll
+        for (uint32_t q = 0; q < kStage / 4; ++q)
+            if (q < nsect)
+                store_sector<REC == 2>(p.arena + base + 4 * q, stage[4 * q][threadIdx.x],
+                                       stage[4 * q + 1][threadIdx.x], stage[4 * q + 2][threadIdx.x],
+                                       stage[4 * q + 3][threadIdx.x]);
     };
     auto log_pair = [&](uint32_t node, uint32_t edge) {
         if (!REC || !rec_ok) return;
@@ -155,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             rec_ok = false;
             return;
         }
-        stage[lpos & 3][threadIdx.x] = make_uint2(node, edge);
-        if ((lpos & 3) == 3) flush(lpos & ~3u);
+        stage[lpos & (kStage - 1)][threadIdx.x] = make_uint2(node, edge);
+        if ((lpos & (kStage - 1)) == kStage - 1) flush(lpos & ~(kStage - 1), kStage / 4);
         ++lpos;
     };
     const uint32_t lane = threadIdx.x & 31;
@@ -204,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             if (STATS) st_draws += 1;
             if (STATS) st_att += 1;
             if (REC) {
-                lpos = (lpos + 3) & ~3u;  // every walk starts on a sector boundary
+                lpos = (lpos + kStage - 1) & ~(kStage - 1);  // walks start on a 128-byte line
                 if (lend - lpos < kLogReserve && !arena_dead) {
                     uint32_t base = atomicAdd(p.arena_cursor, kLogChunk);
                     if (base <= p.arena_cap - kLogChunk) {
@@ -264,7 +272,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                 p.out_len[slot] = nedges;
                 if (REC) {
                     if (rec_ok) {
-                        if (lpos & 3) flush(lpos & ~3u);  // last, partially filled sector
+                        if (lpos & (kStage - 1))  // last, partially filled line
+                            flush(lpos & ~(kStage - 1), ((lpos & (kStage - 1)) + 3) / 4);
                         p.out_log[slot] = astart;
                         astart = lpos;                    // keep the walk: later rewinds stop here
                     } else {
