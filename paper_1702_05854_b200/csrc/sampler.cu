@@ -20,7 +20,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kDefaultEncodeBlocksPerSM = 5;  // 48 registers, no spills (ptxas -v)
-constexpr int kDefaultRecordBlocksPerSM = 5;  // recording, counters off: 48 registers, no spills
+constexpr int kDefaultRecordBlocksPerSM = 4;  // recording: 4 x 32 KB staging, measured best
 
 struct EncodeParams {
     const NodeRec* nodes;
@@ -43,8 +43,8 @@ struct EncodeParams {
     uint32_t* out_log;       // per (batch, seq) slot: first pair of the walk, or kLogOverflow
 };
 
-constexpr uint32_t kLogChunk = 2048;    // pairs per chunk (16 KB)
-constexpr uint32_t kLogReserve = 512;   // a new attempt starts only with this much room left
+constexpr uint32_t kLogChunk = 4096;    // pairs per chunk (32 KB)
+constexpr uint32_t kLogReserve = 1024;  // a new attempt starts only with this much room left
 constexpr uint32_t kLogOverflow = 0xFFFFFFFFu;
 constexpr uint32_t kStage = 16;         // pairs staged per thread in shared memory (128 bytes)
 
@@ -628,6 +628,10 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
     auto go = [&](auto kernel) {
         int blocks = persistent_blocks(ctx, kernel, nbatches);
+        if (const char* env = std::getenv("HSAW_K1_GRID_BLOCKS_PER_SM")) {  // A/B knob
+            int cap = std::atoi(env) * ctx->sm_count;
+            if (cap > 0 && blocks > cap) blocks = cap;
+        }
         StageScope timer(ctx, HSAW_STAGE_ENCODE);
         kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
         check_launch(ctx, "encode_kernel");
