@@ -206,7 +206,7 @@ struct hsaw_gpu_ctx {
     std::string last_error;
     // reusable scratch
     hsawgpu::DevVec<unsigned char> cub_tmp;
-    hsawgpu::DevVec<uint32_t> chk_list, chk_counters;  // distinctness-check scratch
+    hsawgpu::DevVec<uint32_t> chk_list, chk_mid, chk_counters;  // distinctness-check scratch
     hsawgpu::SamplerScratch samp;                        // per-chunk sampler scratch
     hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
     // greedy / coverage scratch (greedy.cu), reused across the doubling iterations
@@ -229,6 +229,7 @@ struct hsaw_gpu_ctx {
         pool_cache.release();
         cub_tmp.release();
         chk_list.release();
+        chk_mid.release();
         chk_counters.release();
         g_cand_bits.release();
         g_cnt.release();

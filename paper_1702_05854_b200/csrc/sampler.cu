@@ -460,9 +460,12 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
 // Verdict to reproduce (sampler.cpp:318-337): the walk is dropped iff its replayed nodes are not
 // pairwise distinct. One warp per walk; <= 32 nodes: one __match_any_sync; <= kSmemNodes: an
 // open-addressing hash set in shared memory; longer walks are queued for distinct_long_kernel.
-constexpr int kCheckWarps = 4;
-constexpr uint32_t kTableSize = 4096;              // u32 slots per warp
-constexpr uint32_t kSmemNodes = kTableSize / 2;    // load factor <= 0.5
+// Two table sizes: the main pass keeps 56 warps per SM resident with 4 KB tables (walks of up to
+// 512 nodes); the few longer walks are queued for a second pass with 16 KB tables, and walks beyond
+// that for the block-per-walk kernel.
+constexpr int kCheckWarps = 8, kMidWarps = 4;
+constexpr uint32_t kTableSize = 1024, kMidTableSize = 4096;  // u32 slots per warp
+constexpr uint32_t kSmemNodes = kMidTableSize / 2;           // largest walk handled in shared memory
 
 struct CheckParams {
     uint64_t nwalks;
@@ -474,8 +477,11 @@ struct CheckParams {
     const uint32_t* lens;
     uint8_t* status;
     uint32_t* long_list;   // (walk id, node count) pairs needing the long path
-    uint32_t* long_count;  // [0] long walks queued, [1] walks dropped (status 1 -> 0)
+    uint32_t* long_count;  // [0] long walks queued, [1] walks dropped (status 1 -> 0), [2] mid queued
     uint32_t long_cap;
+    uint32_t* mid_list;    // walk ids queued for the 16 KB-table pass
+    uint32_t mid_cap;
+    const uint32_t* sel;   // non-null: the work items are sel[0 .. nwalks)
 };
 
 __device__ __forceinline__ uint32_t node_hash(uint32_t v, uint32_t bits) {
@@ -489,16 +495,17 @@ __device__ __forceinline__ uint32_t walk_node(const CheckParams& p, uint64_t w, 
     return p.nodes[base + i];
 }
 
-template <bool PAIRS>
-__global__ void __launch_bounds__(kCheckWarps * 32) distinct_kernel(CheckParams p) {
-    extern __shared__ uint32_t tables[];  // kCheckWarps x kTableSize
+template <bool PAIRS, uint32_t TABLE, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
+    extern __shared__ uint32_t tables[];  // WARPS x TABLE
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
-    uint32_t* tab = tables + wib * kTableSize;
-    uint64_t warp = (uint64_t)blockIdx.x * kCheckWarps + wib;
-    uint64_t nwarps = (uint64_t)gridDim.x * kCheckWarps;
+    uint32_t* tab = tables + wib * TABLE;
+    uint64_t warp = (uint64_t)blockIdx.x * WARPS + wib;
+    uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
     uint32_t dropped = 0;
-    for (uint64_t w = warp; w < p.nwalks; w += nwarps) {
+    for (uint64_t item = warp; item < p.nwalks; item += nwarps) {
+        const uint64_t w = p.sel ? p.sel[item] : item;
         uint8_t st = p.status[w];
         if (st == 0) continue;
         uint64_t base = PAIRS ? 0 : p.edge_off[w] + w;
@@ -513,7 +520,7 @@ __global__ void __launch_bounds__(kCheckWarps * 32) distinct_kernel(CheckParams 
             unsigned valid = nn == 32 ? kFullMask : ((1u << nn) - 1);
             unsigned same = __match_any_sync(kFullMask, v) & valid & ~(1u << lane);
             dup = __any_sync(kFullMask, lane < nn && same != 0);
-        } else if (nn <= kSmemNodes) {
+        } else if (nn <= TABLE / 2) {
             uint32_t bits = 32 - __clz(2 * nn - 1);  // table of >= 2*nn slots
             uint32_t size = 1u << bits;
             for (uint32_t i = lane; i < size; i += 32) tab[i] = kInvalidNode;
@@ -534,6 +541,12 @@ __global__ void __launch_bounds__(kCheckWarps * 32) distinct_kernel(CheckParams 
             }
             dup = __any_sync(kFullMask, mydup);
             __syncwarp();
+        } else if (nn <= kSmemNodes) {  // too long for this pass's table: queue for the mid pass
+            if (lane == 0) {
+                uint32_t at = atomicAdd(p.long_count + 2, 1u);
+                if (at < p.mid_cap) p.mid_list[at] = (uint32_t)w;
+            }
+            continue;
         } else {
             if (lane == 0) {
                 uint32_t at = atomicAdd(p.long_count, 1u);
@@ -735,30 +748,51 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     if (nwalks == 0) return 0;
     if (nwalks > 0xFFFFFFFFull) fail(HSAW_EINVAL, "distinct check: more than 2^32 walks per call");
     const uint32_t long_cap = 1u << 16;
+    const uint32_t mid_cap = (uint32_t)std::min<uint64_t>(nwalks, 1u << 22);
     ctx->chk_list.ensure_scratch(2ull * long_cap);
-    ctx->chk_counters.ensure_scratch(2);
+    ctx->chk_mid.ensure_scratch(mid_cap);
+    ctx->chk_counters.ensure_scratch(4);
     uint32_t* counters = ctx->chk_counters.p;
-    HSAW_CUDA_CHECK(cudaMemsetAsync(counters, 0, 8, ctx->stream));
-    CheckParams p{nwalks,  d_edge_off,      d_nodes,  d_nnodes, d_pair_src, d_lens,
-                  d_status, ctx->chk_list.p, counters, long_cap};
-    const int smem = kCheckWarps * kTableSize * 4;
+    HSAW_CUDA_CHECK(cudaMemsetAsync(counters, 0, 16, ctx->stream));
+    CheckParams p{nwalks,   d_edge_off,      d_nodes,  d_nnodes, d_pair_src,      d_lens,
+                  d_status, ctx->chk_list.p, counters, long_cap, ctx->chk_mid.p, mid_cap,
+                  nullptr};
+    auto main_kernel = distinct_kernel<PAIRS, kTableSize, kCheckWarps>;
+    auto mid_kernel = distinct_kernel<PAIRS, kMidTableSize, kMidWarps>;
+    const int smem_main = kCheckWarps * kTableSize * 4, smem_mid = kMidWarps * kMidTableSize * 4;
     static bool attr_set = false;
     if (!attr_set) {
-        HSAW_CUDA_CHECK(cudaFuncSetAttribute(distinct_kernel<PAIRS>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        HSAW_CUDA_CHECK(cudaFuncSetAttribute(mid_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_mid));
         attr_set = true;
     }
-    uint64_t want = (nwalks + kCheckWarps - 1) / kCheckWarps;
-    uint64_t full = (uint64_t)ctx->sm_count * 3;  // 64 KB of tables per block: 3 blocks / SM
-    int blocks = (int)(want < full ? want : full);
+    uint32_t* h = reinterpret_cast<uint32_t*>(ctx->h_scalars + 32);
     {
+        uint64_t want = (nwalks + kCheckWarps - 1) / kCheckWarps;
+        uint64_t full = (uint64_t)ctx->sm_count * 7;  // 32 KB of tables per block: 7 blocks / SM
+        int blocks = (int)(want < full ? want : full);
         StageScope timer(ctx, HSAW_STAGE_DISTINCT);
-        distinct_kernel<PAIRS><<<blocks, kCheckWarps * 32, smem, ctx->stream>>>(p);
+        main_kernel<<<blocks, kCheckWarps * 32, smem_main, ctx->stream>>>(p);
         check_launch(ctx, "distinct_kernel");
     }
-    uint32_t* h = reinterpret_cast<uint32_t*>(ctx->h_scalars + 32);
-    HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 16, cudaMemcpyDeviceToHost, ctx->stream));
     HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (h[2] > mid_cap) fail(HSAW_ECUDA, "distinct check: mid-size walk queue overflow");
+    if (h[2]) {  // walks of 513..2048 nodes: second pass with 16 KB tables over the queued ids
+        CheckParams q = p;
+        q.nwalks = h[2];
+        q.sel = ctx->chk_mid.p;
+        uint64_t want = ((uint64_t)h[2] + kMidWarps - 1) / kMidWarps;
+        uint64_t full = (uint64_t)ctx->sm_count * 3;
+        int blocks = (int)(want < full ? want : full);
+        {
+            StageScope timer(ctx, HSAW_STAGE_DISTINCT);
+            mid_kernel<<<blocks, kMidWarps * 32, smem_mid, ctx->stream>>>(q);
+            check_launch(ctx, "distinct_kernel<mid>");
+        }
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 16, cudaMemcpyDeviceToHost, ctx->stream));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    }
     uint32_t nlong = h[0];
     if (nlong > long_cap) fail(HSAW_ECUDA, "distinct check: too many long walks in one round");
     if (nlong) {
