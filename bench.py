@@ -257,18 +257,23 @@ def run_b200(args):
     # ---- roofline of the dominant kernel (K1 encode), rank 0's launches
     peak, peak_src = measured_peak()
     k1_ms, k1_n = stages["encode"]
-    alg_bytes_per_launch = delta["alg_bytes"] / max(k1_n, 1)
+    # K1 also materialises the accepted walks (8 B per walk item logged while walking); the
+    # replay pass the reference needs for that (its K2) is not re-counted
+    log_bytes = 8 * delta["spare"]
+    alg_bytes_per_launch = (delta["alg_bytes"] + log_bytes) / max(k1_n, 1)
     k1_avg_ms = k1_ms / max(k1_n, 1)
     achieved = alg_bytes_per_launch / (k1_avg_ms / 1e3) / 1e9 if k1_avg_ms > 0 else 0.0
     traffic = ncu_traffic()
     roofline = {
-        "bound": "hbm", "kernel": "encode_kernel<Brent,2> (K1)", "achieved": achieved,
+        "bound": "hbm", "kernel": "encode_kernel<Brent,2,record> (K1, walk generation + materialisation)", "achieved": achieved,
         "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
         "peak_source": peak_src,
         "algorithmic_bytes_per_launch": alg_bytes_per_launch,
         "bytes_per_step_formula": "28+8*ceil(log2 d) per successful pick (16 empty row, 24 no "
-                                  "live edge) + 8 per node arrival (SURVEY.md 8d)",
+                                  "live edge) + 8 per node arrival (SURVEY.md 8d) + 8 per item "
+                                  "of an accepted walk (logged by the same kernel)",
+        "walk_log_bytes_per_launch": log_bytes / max(k1_n, 1),
         "kernel_avg_ms": k1_avg_ms, "launches_timed": k1_n,
         "k1_walk_steps_per_s": delta["steps"] / (k1_ms / 1e3) if k1_ms > 0 else None,
         "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
@@ -283,8 +288,8 @@ def run_b200(args):
         "data": "synthetic",
         "config": {
             "workload": workload_name(args, g.n, g.m),
-            "step": f"{B} batches ({10 * B} attempts) per GPU: K1 encode + K2 decode + K2b exact "
-                    f"recheck + ordered compaction into the device pool",
+            "step": f"{B} batches ({10 * B} attempts) per GPU: K1 encode+record, K2b exact recheck, "
+                    f"ordered compaction into the device pool (K2 replay only on log overflow)",
             "parallelism": f"walks sharded by batch range over {world} GPU(s), graph replicated",
             "l2_policy": f"inputs larger than L2: {hsaw_mb(dg)} MB of node/edge records are "
                          f"walked at random and every step uses fresh batches",

@@ -81,7 +81,8 @@ uint64_t hsaw_gpu_graph_bytes(const hsaw_gpu_ctx* ctx);
 /* thread_sample for a range of batches (proj/src/sampler.cpp:267-290; worker ids
  * first_worker_id + b, b in [0, nbatches)): out_count[b] accepted attempts of batch b, their
  * (seed, len) in out_seed/out_len[b * batch_size + seq]. Bit-exact with the reference stream.
- * stats (nullable) u64[8]: {attempts, draws, steps(picks), alg_bytes, accepted, 0, 0, 0}. */
+ * stats (nullable) u64[8]: {attempts, draws, steps(picks), alg_bytes, accepted, 0, 0,
+ * walk_items = sum of (len + 1) over the accepted walks}. */
 int hsaw_gpu_encode_batches(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg* cfg,
                             uint64_t first_worker_id, uint64_t nbatches, uint64_t* out_seed,
                             uint32_t* out_len, uint32_t* out_count, uint64_t* stats);
@@ -147,7 +148,8 @@ int hsaw_gpu_stream_export(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
 int hsaw_gpu_stream_collect_stats(hsaw_gpu_stream* s, int on);
 
 /* Sampler work counters accumulated over the stream's life (u64[8], as in encode_batches; [5] =
- * decode picks, [6] = walks dropped by the exact recheck). */
+ * replay (K2) picks, [6] = walks dropped by the exact recheck, [7] = walks whose log overflowed
+ * and were replayed). [1]-[3] stay 0 unless hsaw_gpu_stream_collect_stats is on. */
 int hsaw_gpu_stream_stats(const hsaw_gpu_stream* s, uint64_t* stats);
 
 /* ---- fixed walk sets (fixed-walk-set parity mode) ------------------------------------------- */

@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
     uint32_t b_anchor = kInvalidNode, b_power = 1, b_lam = 0;
     // per-lane work counters; 32 bits suffice for one launch's share of one lane, except bytes
     uint32_t st_draws = 0, st_steps = 0, st_att = 0, st_acc = 0;
-    uint64_t st_bytes = 0;
+    uint64_t st_bytes = 0, st_pairs = 0;
 
     for (;;) {
         if (!drained) {
@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                 }
                 ++cnt;
                 if (STATS) st_acc += 1;
+                if (STATS) st_pairs += nedges + 1;  // items of the accepted walk (8 B each logged)
             } else {
                 lo = rec.lo;
                 deg = rec.deg;
@@ -333,6 +334,10 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
         atomicAdd(st + ST_BYTES, (unsigned long long)w_bytes);
         atomicAdd(st + ST_ACCEPTED, (unsigned long long)w_acc);
     }
+    const uint64_t w_pairs = warp_sum(st_pairs);
+    if (lane == 0 && p.stats)
+        atomicAdd(reinterpret_cast<unsigned long long*>(p.stats) + ST_SPARE,
+                  (unsigned long long)w_pairs);
 }
 
 // ---- K2 ----------------------------------------------------------------------------------------
