@@ -204,15 +204,19 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
 
-    stream = ctx.stream(seed=STREAM_SEED, cfg=cfg)
     step_index = [0]
+    replay_counts = []
 
     def one_step():
-        # weak scaling: global batch ranges are dealt round-robin to the ranks, each rank's
-        # ranges stay increasing; no collective on the data path
+        # weak scaling: global batch ranges are dealt round-robin to the ranks; no collective on
+        # the data path. Each step samples its range into a fresh SampleStream, so the walk pool
+        # of the previous step is recycled instead of growing without bound over K steps.
         first = (step_index[0] * world + rank) * B
         step_index[0] += 1
-        return stream.sample_range(first, B)
+        with ctx.stream(seed=STREAM_SEED, cfg=cfg) as st:
+            got = st.sample_range(first, B)
+            replay_counts.append(st.stats()["spare"])
+        return got
 
     for _ in range(args.warmup):
         one_step()
@@ -242,7 +246,6 @@ def run_b200(args):
         one = ctx.encode_stats(STREAM_SEED + first, B, cfg)
         for k in delta:
             delta[k] += one[k]
-    decode_steps = stream.stats()["decode_steps"]
 
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
     c = torch.tensor([accepted, delta["attempts"], delta["steps"], launches],
@@ -279,8 +282,6 @@ def run_b200(args):
         "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
         "k1_share_of_step": k1_ms / elapsed_ms if elapsed_ms > 0 else None,
     }
-    stream.close()
-
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / max(args.steps, 1),
@@ -298,6 +299,7 @@ def run_b200(args):
         "attempts_per_sec": tot_att / (elapsed_ms / 1e3),
         "walk_steps_per_sec": tot_steps / (elapsed_ms / 1e3),
         "accept_rate": tot_acc / tot_att if tot_att else None,
+        "walks_replayed_after_log_overflow": int(sum(replay_counts[-args.steps:])),
         "roofline": roofline, "clocks": clock_info, "gpu_launches": int(tot_launches),
     }
 

@@ -211,7 +211,7 @@ struct hsaw_gpu_ctx {
     hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
     // greedy / coverage scratch (greedy.cu), reused across the doubling iterations
     hsawgpu::DevVec<uint32_t> g_cand_bits, g_cnt, g_fill, g_inv, g_covered, g_solution, g_query_bits;
-    hsawgpu::DevVec<uint64_t> g_pos, g_partial, g_gains;
+    hsawgpu::DevVec<uint64_t> g_pos, g_partial, g_gains, g_blkmax;
     uint64_t* d_scalars = nullptr;  // 64 u64 of device scratch for counters / cursors
     uint64_t* h_scalars = nullptr;  // pinned mirror
     // per-stage device time, measured with CUDA events on `stream` around the kernels themselves
@@ -241,6 +241,7 @@ struct hsaw_gpu_ctx {
         g_pos.release();
         g_partial.release();
         g_gains.release();
+        g_blkmax.release();
     }
 };
 

@@ -70,6 +70,7 @@ __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
             EdgeRec r;
             r.thr = ge_threshold(c);
             r.src = src[e];
+            if (r.src >= n) atomicMin(bad_row + 1, v);  // source id out of range
             uint64_t prev = 0;
             if (e > lo) {
                 double cp = cum[e - 1];
@@ -279,8 +280,6 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             fail(HSAW_EDATA, "graph: offsets do not cover edge range");
         for (uint32_t v = 0; v < n; ++v)
             if (in_offsets[v + 1] < in_offsets[v]) fail(HSAW_EDATA, "graph: offsets not monotone");
-        for (uint32_t e = 0; e < m; ++e)
-            if (in_src[e] >= n) fail(HSAW_EDATA, "graph: source id out of range");
         free_graph(ctx);
         cudaStream_t st = ctx->stream;
         uint64_t* d_off = nullptr;
@@ -303,7 +302,7 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_src, (uint64_t)(m ? m : 1) * 4, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_cum, (uint64_t)(m ? m : 1) * 8, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, st));
-            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_bad, 4, st));
+            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_bad, 8, st));
             HSAW_CUDA_CHECK(cudaMemcpyAsync(d_off, in_offsets, ((uint64_t)n + 1) * 8,
                                             cudaMemcpyHostToDevice, st));
             if (m) {
@@ -313,7 +312,7 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
                     cudaMemcpyAsync(d_cum, in_cum, (uint64_t)m * 8, cudaMemcpyHostToDevice, st));
             }
             HSAW_CUDA_CHECK(cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, st));
-            HSAW_CUDA_CHECK(cudaMemsetAsync(d_bad, 0xFF, 4, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_bad, 0xFF, 8, st));
             {
                 StageScope timer(ctx, HSAW_STAGE_UPLOAD);
                 build_node_records<<<(n + 255) / 256, 256, 0, st>>>(n, d_off, d_cum, d_p,
@@ -326,9 +325,13 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
                     check_launch(ctx, "build_edge_records");
                 }
             }
-            uint32_t bad = 0;
-            HSAW_CUDA_CHECK(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+            uint32_t both[2] = {0, 0};
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(both, d_bad, 8, cudaMemcpyDeviceToHost, st));
             HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+            const uint32_t bad = both[0], bad_src = both[1];
+            if (bad_src != 0xFFFFFFFFu)
+                fail(HSAW_EDATA, "graph: source id out of range in the row of node " +
+                                     std::to_string(bad_src));
             if (bad != 0xFFFFFFFFu)
                 fail(HSAW_EDATA, "graph: cumulative weights not increasing at node " +
                                      std::to_string(bad));

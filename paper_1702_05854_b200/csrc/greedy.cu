@@ -139,6 +139,79 @@ __global__ void __launch_bounds__(256) argmax_partial(const uint32_t* __restrict
     if (threadIdx.x == 0) partial[blockIdx.x] = best;
 }
 
+// ---- lazy block maxima (CELF at block granularity) ---------------------------------------------
+// Counts only ever decrease during a greedy run, so a block maximum computed earlier is an upper
+// bound of the block's true maximum. Each round re-tightens only the block holding the largest
+// bound until that bound is exact — then it is the global argmax — instead of scanning all
+// `limit` counters (16 M for C2 edges, 1.47 G at the Twitter shape) every round. Keys are
+// count << 32 | ~id, unique per item, so the (largest gain, smallest id) order is preserved.
+constexpr uint32_t kMaxBlockItems = 2048;
+
+__device__ __forceinline__ uint64_t gain_key(uint32_t count, uint32_t id) {
+    return count ? ((uint64_t)count << 32) | (0xFFFFFFFFu - id) : 0;
+}
+
+// blkmax[b] = exact max key of items [b * 2048, (b + 1) * 2048)
+__global__ void __launch_bounds__(256) block_maxima(const uint32_t* __restrict__ cnt,
+                                                    uint32_t limit, uint64_t* __restrict__ blkmax) {
+    __shared__ uint64_t smem[32];
+    const uint64_t base = (uint64_t)blockIdx.x * kMaxBlockItems;
+    uint64_t best = 0;
+    for (uint32_t i = threadIdx.x; i < kMaxBlockItems; i += blockDim.x) {
+        uint64_t id = base + i;
+        if (id < limit) {
+            uint64_t k = gain_key(cnt[id], (uint32_t)id);
+            best = k > best ? k : best;
+        }
+    }
+    best = block_max_u64(best, smem);
+    if (threadIdx.x == 0) blkmax[blockIdx.x] = best;
+}
+
+// One CTA: repeat { take the block with the largest bound; recompute it exactly } until the
+// largest bound is exact. Writes the winner key to out[0] (0 = no positive gain left).
+__global__ void __launch_bounds__(1024) select_lazy(const uint32_t* __restrict__ cnt,
+                                                    uint32_t limit, uint64_t* __restrict__ blkmax,
+                                                    uint32_t nblk, uint64_t* __restrict__ out) {
+    __shared__ uint64_t smem[32];
+    __shared__ uint32_t s_blk;
+    for (;;) {
+        uint64_t best = 0;
+        uint32_t best_b = 0;
+        for (uint32_t b = threadIdx.x; b < nblk; b += blockDim.x) {
+            uint64_t k = blkmax[b];
+            if (k > best) {
+                best = k;
+                best_b = b;
+            }
+        }
+        const uint64_t top = block_max_u64(best, smem);
+        if (top == 0) {
+            if (threadIdx.x == 0) out[0] = 0;
+            return;
+        }
+        if (best == top) s_blk = best_b;  // keys are unique: exactly one thread holds the top
+        __syncthreads();
+        const uint32_t blk = s_blk;
+        const uint64_t base = (uint64_t)blk * kMaxBlockItems;
+        uint64_t exact = 0;
+        for (uint32_t i = threadIdx.x; i < kMaxBlockItems; i += blockDim.x) {
+            uint64_t id = base + i;
+            if (id < limit) {
+                uint64_t k = gain_key(cnt[id], (uint32_t)id);
+                exact = k > exact ? k : exact;
+            }
+        }
+        exact = block_max_u64(exact, smem);
+        if (exact == top) {  // the bound was exact: every other block is bounded below it
+            if (threadIdx.x == 0) out[0] = top;
+            return;
+        }
+        if (threadIdx.x == 0) blkmax[blk] = exact;  // tighten and look again
+        __syncthreads();
+    }
+}
+
 // K5: every block re-reduces the partial maxima (identical result), then the blocks share the
 // winner's inverted list: one warp per listed walk, claimed through an atomicOr on the covered
 // bitmap, decrementing the counts of the walk's candidate items.
@@ -438,10 +511,16 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         uint64_t cov_words = (cnt + 31) / 32 + 1;
         d_cov.ensure_scratch(cov_words);
         HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
-        const uint32_t npartial =
-            (uint32_t)std::min<uint64_t>(((uint64_t)limit / 4 + 255) / 256 + 1, (uint64_t)wide);
-        DevVec<uint64_t>& d_partial = ctx->g_partial;
-        d_partial.ensure_scratch(npartial);
+        const uint32_t nblk = (uint32_t)(((uint64_t)limit + kMaxBlockItems - 1) / kMaxBlockItems);
+        DevVec<uint64_t>& d_partial = ctx->g_partial;  // [0] = winner key of the round
+        DevVec<uint64_t>& d_blkmax = ctx->g_blkmax;
+        d_partial.ensure_scratch(4);
+        d_blkmax.ensure_scratch(nblk + 1);
+        if (occurrences) {
+            StageScope timer(ctx, HSAW_STAGE_ROUNDS);
+            block_maxima<<<nblk, 256, 0, st>>>(d_cnt.p, limit, d_blkmax.p);
+            check_launch(ctx, "block_maxima");
+        }
         DevVec<uint32_t>& d_sol = ctx->g_solution;
         DevVec<uint64_t>& d_gain = ctx->g_gains;
         d_sol.ensure_scratch(k);
@@ -456,9 +535,9 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             {
                 StageScope timer(ctx, HSAW_STAGE_ROUNDS);
                 for (uint32_t r = done; r < done + group; ++r) {
-                    argmax_partial<<<npartial, 256, 0, st>>>(d_cnt.p, limit, d_partial.p);
-                    check_launch(ctx, "argmax_partial");
-                    cover_winner<<<cover_blocks, 256, 0, st>>>(v, d_partial.p, npartial, d_cand,
+                    select_lazy<<<1, 1024, 0, st>>>(d_cnt.p, limit, d_blkmax.p, nblk, d_partial.p);
+                    check_launch(ctx, "select_lazy");
+                    cover_winner<<<cover_blocks, 256, 0, st>>>(v, d_partial.p, 1, d_cand,
                                                                d_pos.p, d_inv.p, d_cnt.p, d_cov.p,
                                                                r, d_sol.p, d_gain.p);
                     check_launch(ctx, "cover_winner");
@@ -520,6 +599,7 @@ struct hsaw_gpu_rounds {
     DevVec<uint64_t> pos, partial, scalars;
     uint64_t occurrences = 0;
     uint32_t npartial = 0;
+    bool maxima_ready = false;
 };
 
 int hsaw_gpu_rounds_begin(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
@@ -546,7 +626,7 @@ int hsaw_gpu_rounds_begin(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             const uint64_t limit = v.limit;
             g->fill.ensure_scratch(limit + 4);
             g->pos.ensure_scratch(limit + 2);
-            g->scalars.ensure_scratch(4);
+            g->scalars.ensure_scratch(8);
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, (limit + 4) * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(g->fill.p, 0, (limit + 4) * 4, st));
             uint64_t p0 = 0, p1 = 0;
@@ -575,8 +655,8 @@ int hsaw_gpu_rounds_begin(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             uint64_t cov_words = (cnt + 31) / 32 + 1;
             g->covered.ensure_scratch(cov_words);
             HSAW_CUDA_CHECK(cudaMemsetAsync(g->covered.p, 0, cov_words * 4, st));
-            g->npartial = (uint32_t)std::min<uint64_t>((limit / 4 + 255) / 256 + 1, (uint64_t)wide);
-            g->partial.ensure_scratch(g->npartial);
+            g->npartial = (uint32_t)((limit + kMaxBlockItems - 1) / kMaxBlockItems);  // blocks
+            g->partial.ensure_scratch(g->npartial + 1);  // block maxima, built at the first select
             HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
             collect_timings(ctx);
         } catch (...) {
@@ -596,9 +676,15 @@ int hsaw_gpu_rounds_select(hsaw_gpu_rounds* g, uint32_t* item, uint64_t* gain) {
         cudaStream_t st = ctx->stream;
         {
             StageScope timer(ctx, HSAW_STAGE_ROUNDS);
-            argmax_partial<<<g->npartial, 256, 0, st>>>(g->d_counts, g->limit, g->partial.p);
-            check_launch(ctx, "argmax_partial");
-            select_final<<<1, 256, 0, st>>>(g->partial.p, g->npartial, g->scalars.p);
+            if (!g->maxima_ready) {  // after the caller's all-reduce of the counts
+                block_maxima<<<g->npartial, 256, 0, st>>>(g->d_counts, g->limit, g->partial.p);
+                check_launch(ctx, "block_maxima");
+                g->maxima_ready = true;
+            }
+            select_lazy<<<1, 1024, 0, st>>>(g->d_counts, g->limit, g->partial.p, g->npartial,
+                                            g->scalars.p + 3);
+            check_launch(ctx, "select_lazy");
+            select_final<<<1, 256, 0, st>>>(g->scalars.p + 3, 1, g->scalars.p);
             check_launch(ctx, "select_final");
         }
         HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], g->scalars.p, 16,
