@@ -102,6 +102,14 @@ struct DevVec {
     DevVec() = default;
     DevVec(const DevVec&) = delete;
     DevVec& operator=(const DevVec&) = delete;
+    DevVec(DevVec&& o) noexcept { swap(o); }
+    DevVec& operator=(DevVec&& o) noexcept {
+        if (this != &o) {
+            release();
+            swap(o);
+        }
+        return *this;
+    }
     ~DevVec() { release(); }
 
     void release() {
@@ -206,6 +214,8 @@ struct hsaw_gpu_ctx {
     std::string last_error;
     // reusable scratch
     hsawgpu::DevVec<unsigned char> cub_tmp;
+    hsawgpu::DevVec<hsawgpu::NodeRec> g_nodes_store;  // backing store of g.nodes / g.edges
+    hsawgpu::DevVec<hsawgpu::EdgeRec> g_edges_store;
     hsawgpu::DevVec<uint32_t> chk_list, chk_mid, chk_counters;  // distinctness-check scratch
     hsawgpu::SamplerScratch samp;                        // per-chunk sampler scratch
     hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
@@ -224,7 +234,46 @@ struct hsaw_gpu_ctx {
     double stage_ms[HSAW_STAGE_COUNT] = {};
     uint64_t stage_launches[HSAW_STAGE_COUNT] = {};
 
+    // Swaps every reusable device buffer with `o` (used to park the buffers of a dying context in
+    // a per-device cache and to hand them to the next context: a fresh DeviceGraph per call — the
+    // host-buffer e2e path — then allocates nothing in steady state).
+    void swap_buffers(hsaw_gpu_ctx& o) {
+        g_nodes_store.swap(o.g_nodes_store);
+        g_edges_store.swap(o.g_edges_store);
+        cub_tmp.swap(o.cub_tmp);
+        chk_list.swap(o.chk_list);
+        chk_mid.swap(o.chk_mid);
+        chk_counters.swap(o.chk_counters);
+        std::swap(samp, o.samp);
+        std::swap(pool_cache, o.pool_cache);
+        g_cand_bits.swap(o.g_cand_bits);
+        g_cnt.swap(o.g_cnt);
+        g_fill.swap(o.g_fill);
+        g_inv.swap(o.g_inv);
+        g_covered.swap(o.g_covered);
+        g_solution.swap(o.g_solution);
+        g_query_bits.swap(o.g_query_bits);
+        g_pos.swap(o.g_pos);
+        g_partial.swap(o.g_partial);
+        g_gains.swap(o.g_gains);
+        g_blkmax.swap(o.g_blkmax);
+    }
+    template <class F>
+    void for_each_buffer(F&& f) {
+        f(g_nodes_store); f(g_edges_store); f(cub_tmp); f(chk_list); f(chk_mid); f(chk_counters);
+        f(samp.slot_seed); f(samp.enc_seed); f(samp.tmp_off); f(samp.voff); f(samp.enc_batch);
+        f(samp.slot_len); f(samp.count); f(samp.first); f(samp.enc_len); f(samp.enc_seq);
+        f(samp.tmp_nodes); f(samp.tmp_edges); f(samp.vidx); f(samp.status); f(samp.arena);
+        f(samp.replay); f(samp.slot_log); f(samp.ovf_pairs); f(samp.sel); f(samp.enc_src);
+        f(pool_cache.edge_off); f(pool_cache.tag_batch); f(pool_cache.accepted_after_batch);
+        f(pool_cache.nodes); f(pool_cache.edges); f(pool_cache.tag_seq);
+        f(g_cand_bits); f(g_cnt); f(g_fill); f(g_inv); f(g_covered); f(g_solution);
+        f(g_query_bits); f(g_pos); f(g_partial); f(g_gains); f(g_blkmax);
+    }
+
     void release_scratch() {
+        g_nodes_store.release();
+        g_edges_store.release();
         samp.release();
         pool_cache.release();
         cub_tmp.release();

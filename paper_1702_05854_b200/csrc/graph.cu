@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -114,11 +116,50 @@ void pin_node_records_in_l2(hsaw_gpu_ctx* ctx) {
         cudaGetLastError();
 }
 
-void free_graph(hsaw_gpu_ctx* ctx) {
-    if (ctx->g.nodes) cudaFreeAsync(ctx->g.nodes, ctx->stream);
-    if (ctx->g.edges) cudaFreeAsync(ctx->g.edges, ctx->stream);
+void free_graph(hsaw_gpu_ctx* ctx) {  // the backing stores keep their capacity for the next upload
     ctx->g = DeviceGraph{};
     ctx->graph_bytes = 0;
+}
+
+// Per-device parking lot for the device buffers of destroyed contexts (see swap_buffers).
+struct Parked {
+    std::mutex mu;
+    std::map<int, hsaw_gpu_ctx*> by_device;
+    ~Parked() {
+        // process teardown: the CUDA context may already be gone, so the buffers are abandoned
+        for (auto& kv : by_device)
+            kv.second->for_each_buffer([](auto& v) {
+                v.p = nullptr;
+                v.cap = v.size = 0;
+            });
+    }
+};
+Parked& parked() {
+    static Parked p;
+    return p;
+}
+
+void adopt_parked_buffers(hsaw_gpu_ctx* ctx) {
+    Parked& pk = parked();
+    std::lock_guard<std::mutex> lock(pk.mu);
+    auto it = pk.by_device.find(ctx->device);
+    if (it == pk.by_device.end()) return;
+    ctx->swap_buffers(*it->second);
+    ctx->for_each_buffer([&](auto& v) { v.owner = ctx->stream; });
+}
+
+void park_buffers(hsaw_gpu_ctx* ctx) {
+    Parked& pk = parked();
+    std::lock_guard<std::mutex> lock(pk.mu);
+    hsaw_gpu_ctx*& slot = pk.by_device[ctx->device];
+    if (!slot) slot = new hsaw_gpu_ctx;  // holder object: only its buffers are used
+    slot->for_each_buffer([](auto& v) {   // drop whatever an earlier context left (no stream: sync free)
+        if (v.p) cudaFree(v.p);
+        v.p = nullptr;
+        v.cap = v.size = 0;
+    });
+    slot->swap_buffers(*ctx);
+    slot->for_each_buffer([](auto& v) { v.owner = nullptr; });
 }
 
 }  // namespace
@@ -194,6 +235,7 @@ int hsaw_gpu_ctx_create(int device, void* cuda_stream, hsaw_gpu_ctx** out) {
             HSAW_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
             ctx->own_stream = true;
         }
+        adopt_parked_buffers(ctx);
         HSAW_CUDA_CHECK(cudaMalloc(&ctx->d_scalars, 64 * sizeof(uint64_t)));
         HSAW_CUDA_CHECK(cudaMallocHost(&ctx->h_scalars, 64 * sizeof(uint64_t)));
         // keep freed pool memory cached instead of returning it to the driver at every sync
@@ -226,7 +268,9 @@ void hsaw_gpu_ctx_destroy(hsaw_gpu_ctx* ctx) {
     free_graph(ctx);
     if (ctx->d_scalars) cudaFree(ctx->d_scalars);
     if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
-    ctx->release_scratch();  // stream-ordered frees must precede the stream's destruction
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    park_buffers(ctx);       // keep the device buffers for the next context on this device
+    ctx->release_scratch();  // (now empty) stream-ordered frees precede the stream's destruction
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -294,10 +338,10 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             if (d_bad) cudaFreeAsync(d_bad, st);
         };
         try {
-            HSAW_CUDA_CHECK(
-                cudaMallocAsync((void**)&ctx->g.nodes, (uint64_t)n * sizeof(NodeRec), st));
-            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&ctx->g.edges,
-                                            (uint64_t)(m ? m : 1) * sizeof(EdgeRec), st));
+            ctx->g_nodes_store.ensure_scratch(n);
+            ctx->g_edges_store.ensure_scratch(m ? m : 1);
+            ctx->g.nodes = ctx->g_nodes_store.p;
+            ctx->g.edges = ctx->g_edges_store.p;
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_off, ((uint64_t)n + 1) * 8, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_src, (uint64_t)(m ? m : 1) * 4, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_cum, (uint64_t)(m ? m : 1) * 8, st));
