@@ -307,15 +307,17 @@ def run_b200(args):
     # times its own share; ranks run the same call concurrently and the rates are summed)
     target = max(1, int(accepted / max(args.steps, 1)))
     e2e_acc, e2e_s = 0, 0.0
-    for i in range(max(1, min(args.steps, 5))):
+    e2e_calls = max(1, min(args.steps, 5))
+    for i in range(-min(args.warmup, 2), e2e_calls):  # negative i: untimed warm-up calls
         barrier()
         t0 = time.perf_counter()
         with hostapi.DeviceGraph(g, p_of, device=local) as dg2:        # H2D of the CSR arrays
-            _, acc = dg2.sample(target, seed=STREAM_SEED + 1000 * rank + i,
+            _, acc = dg2.sample(target, seed=STREAM_SEED + 1000 * rank + i + 100,
                                 max_attempts=10**15)                   # ensure + counters (D2H)
         torch.cuda.synchronize()
-        e2e_s += time.perf_counter() - t0
-        e2e_acc += acc
+        if i >= 0:
+            e2e_s += time.perf_counter() - t0
+            e2e_acc += acc
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     ce = torch.tensor([float(e2e_acc)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -326,6 +328,7 @@ def run_b200(args):
         "h2d_bytes_per_step": ref_bytes, "d2h_bytes_per_step": 16,
         "call": f"DeviceGraph(g, vi) upload + SampleStream.ensure({target}) + counters_for "
                 f"(the `hsaw sample` path), per call",
+        "calls_timed": e2e_calls, "ms_per_call": 1e3 * float(te.item()) / e2e_calls,
     }
 
     # ---- eSIA seconds-to-solution on the same config (single GPU path)
