@@ -34,13 +34,22 @@ struct __align__(32) NodeRec {
 };
 static_assert(sizeof(NodeRec) == 32, "node record must be one 32-byte sector");
 
-// One 16-byte record per in-edge, in CSR (edge id) order.
-struct __align__(16) EdgeRec {
-    uint64_t thr;      // ceil(in_cum[e] * 2^53): slot e is picked iff thr[e-1] <= k < thr[e]
-    uint32_t src;      // in_src[e]
-    uint32_t prev_hi;  // thr[e-1] >> 21 (0 for the first slot of a row): one-load verification
+// One 32-byte sector per in-edge, in CSR (edge id) order. Besides the pick threshold it carries the
+// row header of the edge's SOURCE node, so that in the common case (source is not a suspect and its
+// total in-weight is within 2^32 draw units of 1) the walk continues from the edge record alone:
+// one dependent sector read per step instead of two. Anything else (suspect source, rows whose
+// weights sum well below 1) falls back to the node record — same results, one more load.
+struct __align__(32) EdgeRec {
+    uint64_t thr;          // ceil(in_cum[e] * 2^53): slot e is picked iff thr[e-1] <= k < thr[e]
+    uint32_t src;          // in_src[e]
+    uint32_t prev_hi;      // thr[e-1] >> 21 (0 for the first slot of a row): one-load verification
+    uint32_t src_lo;       // NodeRec(src).lo
+    uint32_t src_deg;      // NodeRec(src).deg
+    uint32_t src_deficit;  // 2^53 - NodeRec(src).tot_thr when kEdgeSimple is set
+    uint32_t flags;        // kEdgeSuspect: src is a suspect; kEdgeSimple: header fields are usable
 };
-static_assert(sizeof(EdgeRec) == 16, "edge record must be 16 bytes");
+static_assert(sizeof(EdgeRec) == 32, "edge record must be one 32-byte sector");
+constexpr uint32_t kEdgeSuspect = 1u, kEdgeSimple = 2u;
 
 struct DeviceGraph {
     uint32_t n = 0, m = 0;

@@ -57,11 +57,33 @@ __global__ void update_accept_thresholds(uint32_t n, const double* __restrict__ 
     out[v].acc_thr = accept_threshold(p_of[v]);
 }
 
-// One thread per edge slot; row membership via edge_row (filled by mark_rows + scan would cost a
-// pass, so rows are walked by one warp each instead: lanes stride the row).
+// Row header of node u as the edge records carry it: simple iff the total-weight threshold is
+// within 2^32 draw units of 2^53 (always the case for 1/d rows) or the row is empty.
+__device__ __forceinline__ void source_header(const uint64_t* __restrict__ off,
+                                              const double* __restrict__ cum,
+                                              const double* __restrict__ p_of, uint32_t u,
+                                              EdgeRec& r) {
+    uint64_t lo = off[u], hi = off[u + 1];
+    r.src_lo = (uint32_t)lo;
+    r.src_deg = (uint32_t)(hi - lo);
+    r.src_deficit = 0;
+    r.flags = p_of[u] > 0.0 ? kEdgeSuspect : 0u;
+    if (hi == lo) {
+        r.flags |= kEdgeSimple;
+    } else {
+        uint64_t deficit = (1ull << 53) - ge_threshold(cum[hi - 1]);
+        if (deficit <= 0xFFFFFFFFull) {
+            r.src_deficit = (uint32_t)deficit;
+            r.flags |= kEdgeSimple;
+        }
+    }
+}
+
+// One warp per row, lanes stride the row's slots.
 __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
                                    const uint32_t* __restrict__ src, const double* __restrict__ cum,
-                                   EdgeRec* __restrict__ out, uint32_t* __restrict__ bad_row) {
+                                   const double* __restrict__ p_of, EdgeRec* __restrict__ out,
+                                   uint32_t* __restrict__ bad_row) {
     uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t lane = threadIdx.x & 31;
     uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -72,7 +94,6 @@ __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
             EdgeRec r;
             r.thr = ge_threshold(c);
             r.src = src[e];
-            if (r.src >= n) atomicMin(bad_row + 1, v);  // source id out of range
             uint64_t prev = 0;
             if (e > lo) {
                 double cp = cum[e - 1];
@@ -81,9 +102,25 @@ __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
             }
             uint64_t ph = prev >> 21;
             r.prev_hi = ph > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ph;
+            if (r.src >= n) {
+                atomicMin(bad_row + 1, v);  // source id out of range
+                r.src_lo = r.src_deg = r.src_deficit = r.flags = 0;
+            } else {
+                source_header(off, cum, p_of, r.src, r);
+            }
             out[e] = r;
         }
     }
+}
+
+// New suspect set on the same graph: refresh the suspect bit the edge records carry.
+__global__ void update_edge_suspect_flags(uint32_t m, const double* __restrict__ p_of,
+                                          EdgeRec* __restrict__ edges) {
+    uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    uint32_t f = edges[e].flags & ~kEdgeSuspect;
+    if (p_of[edges[e].src] > 0.0) f |= kEdgeSuspect;
+    edges[e].flags = f;
 }
 
 // Every walk step reads one node record and one edge record. The node records are the smaller,
@@ -364,7 +401,7 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
                 check_launch(ctx, "build_node_records");
                 if (m) {
                     int blocks = ctx->sm_count * 8;
-                    build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum,
+                    build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p,
                                                                ctx->g.edges, d_bad);
                     check_launch(ctx, "build_edge_records");
                 }
@@ -406,6 +443,11 @@ int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of) {
             update_accept_thresholds<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, d_p,
                                                                                ctx->g.nodes);
             ++ctx->launches;
+            if (ctx->g.m) {
+                update_edge_suspect_flags<<<(ctx->g.m + 255) / 256, 256, 0, ctx->stream>>>(
+                    ctx->g.m, d_p, ctx->g.edges);
+                ++ctx->launches;
+            }
             e = cudaStreamSynchronize(ctx->stream);
         }
         cudaFreeAsync(d_p, ctx->stream);

@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
 
         // ---- one step of this lane's current attempt (run_walk_attempt, sampler.cpp:147-204)
         uint32_t u = 0;
-        bool walking;
+        bool walking, from_edge = false;
+        EdgeRec erec;
         if (fresh) {
             snapshot = s;  // Seed_h, sampler.cpp:155,277
             uint64_t k = draw53(s);
@@ -236,7 +237,9 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                 bool live = deg != 0 && k < tot;  // graph.hpp:66
                 if (STATS) st_bytes += pick_alg_bytes(deg, live);
                 if (live) {
-                    const uint32_t slot_in_row = pick_slot(edges, lo, deg, scale, k, u);
+                    const uint32_t slot_in_row = pick_slot(edges, lo, deg, scale, k, erec);
+                    u = erec.src;
+                    from_edge = true;
                     bool cyc = win.contains(u);  // sampler.cpp:180
                     if (HEUR == 0 && !cyc) {     // BrentState::check, sampler.cpp:100-108
                         if (u == b_anchor) {
@@ -258,13 +261,20 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
 
         bool attempt_done = true;
         if (walking) {
-            NodeRec rec = load_node(nodes, u);
             if (STATS) st_bytes += 8;  // p_of[u]
+            NodeRec rec;
             bool accepted = false;
-            if (rec.acc_thr != 0) {  // is_suspect, sampler.cpp:32,55
-                uint64_t k2 = draw53(s);
-                if (STATS) st_draws += 1;
-                accepted = k2 < rec.acc_thr;  // r <= p_of[u], sampler.cpp:34,57
+            // Common case: u is not a suspect (no acceptance draw) and the edge record already
+            // holds u's row header, so the walk continues without touching u's node record.
+            if (from_edge && header_from_edge(erec, rec.lo, rec.deg, rec.tot_thr, rec.scale)) {
+                rec.acc_thr = 0;
+            } else {
+                rec = load_node(nodes, u);
+                if (rec.acc_thr != 0) {  // is_suspect, sampler.cpp:32,55
+                    uint64_t k2 = draw53(s);
+                    if (STATS) st_draws += 1;
+                    accepted = k2 < rec.acc_thr;  // r <= p_of[u], sampler.cpp:34,57
+                }
             }
             if (accepted) {
                 uint64_t slot = (uint64_t)bidx * p.l + cnt;  // seq = index among accepted, :283
@@ -394,7 +404,8 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
 
         uint32_t verdict = 0;  // 0 keep walking, 1 decoded, 2 mismatch
         uint32_t u = 0;
-        bool arrived = false;
+        bool arrived = false, from_edge = false;
+        EdgeRec erec;
         if (fresh) {
             if (s == 0) {
                 verdict = 2;  // "decode: zero seed state", sampler.cpp:306
@@ -420,7 +431,9 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
                 if (deg == 0 || k >= tot) {
                     verdict = 2;
                 } else {
-                    uint32_t slot = pick_slot(edges, lo, deg, scale, k, u);
+                    uint32_t slot = pick_slot(edges, lo, deg, scale, k, erec);
+                    u = erec.src;
+                    from_edge = true;
                     if (PAIRS) {
                         ++nedges;
                         pairs[nedges] = make_uint2(u, lo + slot);
@@ -434,9 +447,14 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
             }
         }
         if (arrived) {
-            NodeRec rec = load_node(nodes, u);
+            NodeRec rec;
             bool hit = false;
-            if (rec.acc_thr != 0) hit = draw53(s) < rec.acc_thr;
+            if (from_edge && header_from_edge(erec, rec.lo, rec.deg, rec.tot_thr, rec.scale)) {
+                rec.acc_thr = 0;
+            } else {
+                rec = load_node(nodes, u);
+                if (rec.acc_thr != 0) hit = draw53(s) < rec.acc_thr;
+            }
             if (hit) {
                 verdict = nedges == len ? 1 : 2;  // sampler.cpp:311-314, 329-332
             } else if (nedges >= len) {

@@ -60,12 +60,18 @@ __device__ __forceinline__ NodeRec load_node(const NodeRec* __restrict__ nodes, 
 }
 
 __device__ __forceinline__ EdgeRec load_edge(const EdgeRec* __restrict__ edges, uint64_t e) {
-    uint64_t a, b;
-    asm volatile("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(edges + e));
+    uint64_t a, b, c, d;
+    asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(edges + e));
     EdgeRec r;
     r.thr = a;
     r.src = (uint32_t)b;
     r.prev_hi = (uint32_t)(b >> 32);
+    r.src_lo = (uint32_t)c;
+    r.src_deg = (uint32_t)(c >> 32);
+    r.src_deficit = (uint32_t)d;
+    r.flags = (uint32_t)(d >> 32);
     return r;
 }
 
@@ -81,14 +87,14 @@ __device__ __forceinline__ uint32_t ceil_log2(uint32_t d) {  // d >= 1
 // single load cannot prove falls back to a binary search over the row.
 __device__ __forceinline__ uint32_t pick_slot(const EdgeRec* __restrict__ edges, uint32_t lo,
                                               uint32_t deg, uint64_t scale, uint64_t k,
-                                              uint32_t& src_out) {
+                                              EdgeRec& rec_out) {
     uint64_t gq = __umul64hi(k << 11, scale) >> 31;
     uint32_t g = gq >= deg ? deg - 1 : (uint32_t)gq;
     EdgeRec rec = load_edge(edges, (uint64_t)lo + g);
     bool below = k < rec.thr;
     bool above_prev = g == 0 || (uint32_t)(k >> 21) > rec.prev_hi;
     if (below && above_prev) {
-        src_out = rec.src;
+        rec_out = rec;
         return g;
     }
     // slow path: exact first index with k < thr, restricted to the side the probe ruled in
@@ -110,9 +116,20 @@ __device__ __forceinline__ uint32_t pick_slot(const EdgeRec* __restrict__ edges,
         else
             a = mid + 1;
     }
-    rec = load_edge(edges, (uint64_t)lo + a);
-    src_out = rec.src;
+    rec_out = load_edge(edges, (uint64_t)lo + a);
     return a;
+}
+
+// Row header of the picked edge's source node, when the edge record carries a usable one.
+// Returns false when the node record must be read instead (suspect source or non-simple row).
+__device__ __forceinline__ bool header_from_edge(const EdgeRec& rec, uint32_t& lo, uint32_t& deg,
+                                                 uint64_t& tot, uint64_t& scale) {
+    if ((rec.flags & (kEdgeSimple | kEdgeSuspect)) != kEdgeSimple) return false;
+    lo = rec.src_lo;
+    deg = rec.src_deg;
+    tot = deg ? (1ull << 53) - rec.src_deficit : 0;
+    scale = (uint64_t)deg << 31;  // guess hint for a row whose weights sum to ~1
+    return true;
 }
 
 // Algorithmic bytes of one pick in the reference layout:
