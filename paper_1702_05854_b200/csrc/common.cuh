@@ -220,6 +220,7 @@ struct hsaw_gpu_ctx {
     hsawgpu::DeviceGraph g;
     uint64_t graph_bytes = 0;
     uint64_t launches = 0;
+    uint64_t greedy_full_index_reruns = 0;  // thresholded index was too optimistic (diagnostic)
     std::string last_error;
     // reusable scratch
     hsawgpu::DevVec<unsigned char> cub_tmp;

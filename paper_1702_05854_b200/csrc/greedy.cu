@@ -66,7 +66,8 @@ __global__ void item_histogram(WalkView v, uint64_t p0, uint64_t p1,
 // K3b: one warp per walk; slot order inside an item's list is irrelevant (set semantics).
 __global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ cand_bits,
                                  const uint64_t* __restrict__ pos, uint32_t* __restrict__ fill,
-                                 uint32_t* __restrict__ inv) {
+                                 uint32_t* __restrict__ inv, const uint32_t* __restrict__ cnt,
+                                 uint32_t min_count) {
     uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t lane = threadIdx.x & 31;
     uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -75,12 +76,39 @@ __global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ cand_b
         uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
         for (uint64_t p = b + lane; p < e; p += 32) {
             uint32_t item = v.items[p];
-            if (item < v.limit && is_cand(cand_bits, item)) {
+            // only items that can still win a round are indexed (min_count, see hsaw_gpu_greedy)
+            if (item < v.limit && is_cand(cand_bits, item) && cnt[item] >= min_count) {
                 uint32_t slot = atomicAdd(&fill[item], 1u);
                 inv[pos[item] + slot] = (uint32_t)i;
             }
         }
     }
+}
+
+// Occurrences per count value (counts >= kCountBins - 1 share the last bin): lets the host pick the
+// smallest count worth indexing.
+constexpr uint32_t kCountBins = 1024;
+__global__ void __launch_bounds__(256) count_of_counts(const uint32_t* __restrict__ cnt,
+                                                       uint32_t limit,
+                                                       unsigned long long* __restrict__ occ_bins) {
+    __shared__ unsigned long long bins[kCountBins];
+    for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x) bins[i] = 0;
+    __syncthreads();
+    uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < limit; i += stride) {
+        uint32_t c = cnt[i];
+        if (c) atomicAdd(&bins[c < kCountBins ? c : kCountBins - 1], (unsigned long long)c);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x)
+        if (bins[i]) atomicAdd(&occ_bins[i], bins[i]);
+}
+
+// pos input: counts below the threshold take no inverted-list space
+__global__ void threshold_counts(const uint32_t* __restrict__ cnt, uint64_t n, uint32_t min_count,
+                                 uint32_t* __restrict__ out) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = cnt[i] >= min_count ? cnt[i] : 0;
 }
 
 __device__ __forceinline__ uint64_t block_max_u64(uint64_t v, uint64_t* smem) {
@@ -146,6 +174,7 @@ __global__ void __launch_bounds__(256) argmax_partial(const uint32_t* __restrict
 // `limit` counters (16 M for C2 edges, 1.47 G at the Twitter shape) every round. Keys are
 // count << 32 | ~id, unique per item, so the (largest gain, smallest id) order is preserved.
 constexpr uint32_t kMaxBlockItems = 2048;
+constexpr uint32_t kUnindexed = 0xFFFFFFFEu;  // round marker: winner below the index threshold
 
 __device__ __forceinline__ uint64_t gain_key(uint32_t count, uint32_t id) {
     return count ? ((uint64_t)count << 32) | (0xFFFFFFFFu - id) : 0;
@@ -223,7 +252,8 @@ __global__ void __launch_bounds__(256) cover_winner(WalkView v, const uint64_t* 
                                                     uint32_t* __restrict__ cnt,
                                                     uint32_t* __restrict__ covered,
                                                     uint32_t round, uint32_t* __restrict__ solution,
-                                                    uint64_t* __restrict__ gains) {
+                                                    uint64_t* __restrict__ gains,
+                                                    uint32_t min_indexed) {
     __shared__ uint64_t smem[32];
     uint64_t best = 0;
     for (uint32_t i = threadIdx.x; i < npartial; i += blockDim.x) {
@@ -233,11 +263,15 @@ __global__ void __launch_bounds__(256) cover_winner(WalkView v, const uint64_t* 
     best = block_max_u64(best, smem);
     uint32_t gain = (uint32_t)(best >> 32);
     uint32_t item = 0xFFFFFFFFu - (uint32_t)best;
+    // A winner below the indexing threshold has no inverted list: report it (kUnindexed) and
+    // stop; the host rebuilds the full index. Items above the threshold are always indexed
+    // because counts only decrease.
+    const bool unindexed = gain != 0 && gain < min_indexed;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        solution[round] = gain ? item : 0xFFFFFFFFu;
+        solution[round] = unindexed ? kUnindexed : (gain ? item : 0xFFFFFFFFu);
         gains[round] = gain;
     }
-    if (gain == 0) return;
+    if (gain == 0 || unindexed) return;
     uint64_t lb = pos[item], le = pos[item + 1];
     uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t lane = threadIdx.x & 31;
@@ -471,91 +505,139 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         *coverage = 0;
         if (k == 0) return;
 
-        // ---- K3: marginal-gain counts
+        // ---- one greedy run with inverted lists for items whose count is >= min_count
+        // (0 = choose from the count distribution). Returns false when a round's winner fell below
+        // the threshold, i.e. the run must be repeated with the full index (min_count 1).
         DevVec<uint32_t>& d_cnt = ctx->g_cnt;
         DevVec<uint32_t>& d_fill = ctx->g_fill;
         DevVec<uint64_t>& d_pos = ctx->g_pos;
+        DevVec<uint32_t>& d_inv = ctx->g_inv;
+        DevVec<uint32_t>& d_cov = ctx->g_covered;
+        DevVec<uint64_t>& d_partial = ctx->g_partial;  // [0] = winner key of the round
+        DevVec<uint64_t>& d_blkmax = ctx->g_blkmax;
+        DevVec<uint32_t>& d_sol = ctx->g_solution;
+        DevVec<uint64_t>& d_gain = ctx->g_gains;
         d_cnt.ensure_scratch((uint64_t)limit + 4);
         d_fill.ensure_scratch((uint64_t)limit + 4);
         d_pos.ensure_scratch((uint64_t)limit + 2);
-        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
-        HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
+        const uint32_t nblk = (uint32_t)(((uint64_t)limit + kMaxBlockItems - 1) / kMaxBlockItems);
+        d_partial.ensure_scratch(kCountBins + 4);
+        d_blkmax.ensure_scratch(nblk + 1);
+        d_sol.ensure_scratch(k);
+        d_gain.ensure_scratch(k);
+        uint64_t cov_words = (cnt + 31) / 32 + 1;
+        d_cov.ensure_scratch(cov_words);
+        std::vector<uint32_t> h_sol(k, 0xFFFFFFFFu);
+        std::vector<uint64_t> h_gain(k, 0);
         uint64_t p0 = 0, p1 = 0;
         if (cnt) view_span(ctx, v, &p0, &p1);
         const int wide = ctx->sm_count * 8;
-        {
-            StageScope timer(ctx, HSAW_STAGE_INDEX);
+        const int cover_blocks = ctx->sm_count * 2;
+        uint32_t done = 0;
+
+        auto run = [&](uint32_t min_count) -> bool {
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
+            // ---- K3: marginal-gain counts
             if (p1 > p0) {
+                StageScope timer(ctx, HSAW_STAGE_INDEX);
                 int hb = (int)std::min<uint64_t>((p1 - p0 + 255) / 256, (uint64_t)wide);
                 item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt.p);
                 check_launch(ctx, "item_histogram");
             }
-            // ---- K3b: inverted index by counting sort
-            exclusive_sum_u32_to_u64(ctx, d_cnt.p, d_pos.p, (uint64_t)limit + 1);
-        }
-        uint64_t occurrences = 0;
-        HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], d_pos.p + limit, 8,
-                                        cudaMemcpyDeviceToHost, st));
-        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
-        occurrences = ctx->h_scalars[0];
-        DevVec<uint32_t>& d_inv = ctx->g_inv;
-        d_inv.ensure_scratch(occurrences + 1);
-        if (occurrences) {
-            StageScope timer(ctx, HSAW_STAGE_INDEX);
-            int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
-            scatter_inverted<<<sb, 256, 0, st>>>(v, d_cand, d_pos.p, d_fill.p, d_inv.p);
-            check_launch(ctx, "scatter_inverted");
-        }
-        // ---- rounds
-        DevVec<uint32_t>& d_cov = ctx->g_covered;
-        uint64_t cov_words = (cnt + 31) / 32 + 1;
-        d_cov.ensure_scratch(cov_words);
-        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
-        const uint32_t nblk = (uint32_t)(((uint64_t)limit + kMaxBlockItems - 1) / kMaxBlockItems);
-        DevVec<uint64_t>& d_partial = ctx->g_partial;  // [0] = winner key of the round
-        DevVec<uint64_t>& d_blkmax = ctx->g_blkmax;
-        d_partial.ensure_scratch(4);
-        d_blkmax.ensure_scratch(nblk + 1);
-        if (occurrences) {
-            StageScope timer(ctx, HSAW_STAGE_ROUNDS);
-            block_maxima<<<nblk, 256, 0, st>>>(d_cnt.p, limit, d_blkmax.p);
-            check_launch(ctx, "block_maxima");
-        }
-        DevVec<uint32_t>& d_sol = ctx->g_solution;
-        DevVec<uint64_t>& d_gain = ctx->g_gains;
-        d_sol.ensure_scratch(k);
-        d_gain.ensure_scratch(k);
-        std::vector<uint32_t> h_sol(k, 0xFFFFFFFFu);
-        std::vector<uint64_t> h_gain(k, 0);
-        const int cover_blocks = ctx->sm_count * 2;
-        uint32_t done = 0;
-        bool exhausted = occurrences == 0;
-        while (done < k && !exhausted) {
-            uint32_t group = std::min<uint32_t>(k - done, 64);
-            {
-                StageScope timer(ctx, HSAW_STAGE_ROUNDS);
-                for (uint32_t r = done; r < done + group; ++r) {
-                    select_lazy<<<1, 1024, 0, st>>>(d_cnt.p, limit, d_blkmax.p, nblk, d_partial.p);
-                    check_launch(ctx, "select_lazy");
-                    cover_winner<<<cover_blocks, 256, 0, st>>>(v, d_partial.p, 1, d_cand,
-                                                               d_pos.p, d_inv.p, d_cnt.p, d_cov.p,
-                                                               r, d_sol.p, d_gain.p);
-                    check_launch(ctx, "cover_winner");
+            if (min_count == 0) {
+                // Index only what can win: the smallest count whose items (and everything above)
+                // make up at most 1/8 of all occurrences. Small inputs index everything.
+                auto* d_bins = reinterpret_cast<unsigned long long*>(d_partial.p + 4);
+                HSAW_CUDA_CHECK(cudaMemsetAsync(d_bins, 0, kCountBins * 8, st));
+                {
+                    StageScope timer(ctx, HSAW_STAGE_INDEX);
+                    count_of_counts<<<wide, 256, 0, st>>>(d_cnt.p, limit, d_bins);
+                    check_launch(ctx, "count_of_counts");
+                }
+                std::vector<uint64_t> bins(kCountBins);
+                HSAW_CUDA_CHECK(cudaMemcpyAsync(bins.data(), d_bins, kCountBins * 8,
+                                                cudaMemcpyDeviceToHost, st));
+                HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+                uint64_t total = 0;
+                for (uint64_t b : bins) total += b;
+                min_count = 1;
+                if (total > (1ull << 20)) {
+                    uint64_t above = 0;
+                    min_count = kCountBins - 1;
+                    for (uint32_t c = kCountBins - 1; c >= 1; --c) {
+                        if (above + bins[c] > total / 8) break;
+                        above += bins[c];
+                        min_count = c;
+                    }
                 }
             }
-            HSAW_CUDA_CHECK(cudaMemcpyAsync(h_sol.data() + done, d_sol.p + done, group * 4ull,
-                                            cudaMemcpyDeviceToHost, st));
-            HSAW_CUDA_CHECK(cudaMemcpyAsync(h_gain.data() + done, d_gain.p + done, group * 8ull,
+            // ---- K3b: inverted lists (counting sort) of the items at or above min_count
+            uint32_t* d_thr = d_fill.p;  // reused as the scan input, re-zeroed below
+            {
+                StageScope timer(ctx, HSAW_STAGE_INDEX);
+                uint64_t n1 = (uint64_t)limit + 1;
+                threshold_counts<<<(unsigned)((n1 + 255) / 256), 256, 0, st>>>(d_cnt.p, n1,
+                                                                                 min_count, d_thr);
+                check_launch(ctx, "threshold_counts");
+                exclusive_sum_u32_to_u64(ctx, d_thr, d_pos.p, n1);
+                HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
+            }
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], d_pos.p + limit, 8,
                                             cudaMemcpyDeviceToHost, st));
             HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
-            for (uint32_t r = done; r < done + group; ++r) {
-                if (h_gain[r] == 0) {
-                    exhausted = true;
-                    done = r;
-                    break;
-                }
+            const uint64_t indexed = ctx->h_scalars[0];
+            d_inv.ensure_scratch(indexed + 1);
+            if (indexed) {
+                StageScope timer(ctx, HSAW_STAGE_INDEX);
+                int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
+                scatter_inverted<<<sb, 256, 0, st>>>(v, d_cand, d_pos.p, d_fill.p, d_inv.p,
+                                                     d_cnt.p, min_count);
+                check_launch(ctx, "scatter_inverted");
             }
-            if (!exhausted) done += group;
+            // ---- rounds
+            if (p1 > p0) {
+                StageScope timer(ctx, HSAW_STAGE_ROUNDS);
+                block_maxima<<<nblk, 256, 0, st>>>(d_cnt.p, limit, d_blkmax.p);
+                check_launch(ctx, "block_maxima");
+            }
+            done = 0;
+            bool exhausted = p1 == p0;
+            while (done < k && !exhausted) {
+                uint32_t group = std::min<uint32_t>(k - done, 64);
+                {
+                    StageScope timer(ctx, HSAW_STAGE_ROUNDS);
+                    for (uint32_t r = done; r < done + group; ++r) {
+                        select_lazy<<<1, 1024, 0, st>>>(d_cnt.p, limit, d_blkmax.p, nblk,
+                                                        d_partial.p);
+                        check_launch(ctx, "select_lazy");
+                        cover_winner<<<cover_blocks, 256, 0, st>>>(
+                            v, d_partial.p, 1, d_cand, d_pos.p, d_inv.p, d_cnt.p, d_cov.p, r,
+                            d_sol.p, d_gain.p, min_count);
+                        check_launch(ctx, "cover_winner");
+                    }
+                }
+                HSAW_CUDA_CHECK(cudaMemcpyAsync(h_sol.data() + done, d_sol.p + done, group * 4ull,
+                                                cudaMemcpyDeviceToHost, st));
+                HSAW_CUDA_CHECK(cudaMemcpyAsync(h_gain.data() + done, d_gain.p + done,
+                                                group * 8ull, cudaMemcpyDeviceToHost, st));
+                HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+                for (uint32_t r = done; r < done + group; ++r) {
+                    if (h_sol[r] == kUnindexed) return false;  // needs the full index
+                    if (h_gain[r] == 0) {
+                        exhausted = true;
+                        done = r;
+                        break;
+                    }
+                }
+                if (!exhausted) done += group;
+            }
+            return true;
+        };
+        if (!run(0)) {
+            ++ctx->greedy_full_index_reruns;
+            if (!run(1)) fail(HSAW_ECUDA, "greedy: full index run reported an unindexed winner");
         }
         collect_timings(ctx);
         // ---- zero-gain padding: smallest unselected candidates in ascending order
@@ -649,7 +731,8 @@ int hsaw_gpu_rounds_begin(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             if (g->occurrences) {
                 StageScope timer(ctx, HSAW_STAGE_INDEX);
                 int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
-                scatter_inverted<<<sb, 256, 0, st>>>(v, d_cand, g->pos.p, g->fill.p, g->inv.p);
+                scatter_inverted<<<sb, 256, 0, st>>>(v, d_cand, g->pos.p, g->fill.p, g->inv.p,
+                                                     d_counts, 1u);
                 check_launch(ctx, "scatter_inverted");
             }
             uint64_t cov_words = (cnt + 31) / 32 + 1;

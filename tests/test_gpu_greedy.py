@@ -130,3 +130,25 @@ def test_greedy_is_monotone_submodular(ctx, synth3000):  # test_coverage.cpp:95-
             cs, cb = cov(small), cov(big)
             assert cs <= cb
             assert cov(np.append(small, x)) - cs >= cov(np.append(big, x)) - cb
+
+
+def test_thresholded_index_falls_back_to_full(ctx, port):
+    """Large flat instance: the inverted index is first built only for high-count items; with k
+    large enough the winners drop below that threshold and the run must restart with the full
+    index — selections still bit-exact with the oracle."""
+    rng = np.random.Generator(np.random.PCG64(3))
+    limit, nsets = 60_000, 1_300_000
+    items = rng.integers(0, limit, size=nsets).astype(np.uint32)
+    off = np.arange(nsets + 1, dtype=np.uint64)
+    k = 12_000
+    exp_sol, exp_cov = port.greedy(limit, off, items, k)
+    with ctx.walkset(limit, off, items) as ws:
+        sol, cov = ctx.greedy(k, walkset=ws)
+    assert cov == exp_cov and sol.tolist() == exp_sol.tolist()
+    # and a skewed one where the threshold holds (no fallback needed)
+    z = np.minimum(rng.zipf(1.2, size=nsets * 2) - 1, limit - 1).astype(np.uint32)
+    off2 = np.arange(0, 2 * nsets + 1, 2, dtype=np.uint64)
+    exp_sol, exp_cov = port.greedy(limit, off2, z, 40)
+    with ctx.walkset(limit, off2, z) as ws:
+        sol, cov = ctx.greedy(40, walkset=ws)
+    assert cov == exp_cov and sol.tolist() == exp_sol.tolist()
