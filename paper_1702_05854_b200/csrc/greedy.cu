@@ -10,6 +10,8 @@
 // is zero are padded with the smallest unselected candidate ids (host side).
 #include <algorithm>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 #include "stream.cuh"
 
@@ -60,6 +62,16 @@ __global__ void item_histogram(WalkView v, uint64_t p0, uint64_t p1,
     for (uint64_t p = p0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < p1; p += stride) {
         uint32_t item = v.items[p];
         if (item < v.limit && is_cand(cand_bits, item)) atomicAdd(&cnt[item], 1u);
+    }
+}
+
+// K3 on a plain key array (the radix-partitioned copy of the items, see partitioned_histogram).
+__global__ void key_histogram(const uint32_t* __restrict__ keys, uint64_t n, uint32_t limit,
+                              const uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ cnt) {
+    uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+        uint32_t item = keys[p];
+        if (item < limit && is_cand(cand_bits, item)) atomicAdd(&cnt[item], 1u);
     }
 }
 
@@ -539,12 +551,35 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
-            // ---- K3: marginal-gain counts
+            // ---- K3: marginal-gain counts. When the counters do not fit L2, random atomics go to
+            // HBM one 32-byte sector at a time; one 8-bit radix pass on the items' top bits first
+            // makes consecutive items fall into one ~1/256 window of the counters, which L2 holds.
             if (p1 > p0) {
                 StageScope timer(ctx, HSAW_STAGE_INDEX);
-                int hb = (int)std::min<uint64_t>((p1 - p0 + 255) / 256, (uint64_t)wide);
-                item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt.p);
-                check_launch(ctx, "item_histogram");
+                const uint64_t nitems = p1 - p0;
+                int hb = (int)std::min<uint64_t>((nitems + 255) / 256, (uint64_t)wide);
+                const bool partition = (uint64_t)limit * 4 > (48ull << 20) && nitems > (1ull << 22) &&
+                                       nitems < (1ull << 33);
+                if (partition) {
+                    DevVec<uint32_t>& d_sorted = ctx->g_sorted;
+                    d_sorted.ensure_scratch(nitems);
+                    int top = 32 - __builtin_clz(limit - 1);
+                    int begin_bit = std::max(0, top - 8);
+                    size_t bytes = 0;
+                    HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
+                        nullptr, bytes, v.items + p0, d_sorted.p, (int64_t)nitems, begin_bit, top,
+                        st));
+                    ctx->cub_tmp.ensure_scratch(bytes ? bytes : 1);
+                    HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
+                        ctx->cub_tmp.p, bytes, v.items + p0, d_sorted.p, (int64_t)nitems,
+                        begin_bit, top, st));
+                    ++ctx->launches;
+                    key_histogram<<<hb, 256, 0, st>>>(d_sorted.p, nitems, limit, d_cand, d_cnt.p);
+                    check_launch(ctx, "key_histogram");
+                } else {
+                    item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt.p);
+                    check_launch(ctx, "item_histogram");
+                }
             }
             if (min_count == 0) {
                 // Index only what can win: the smallest count whose items (and everything above)

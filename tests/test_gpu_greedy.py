@@ -152,3 +152,16 @@ def test_thresholded_index_falls_back_to_full(ctx, port):
     with ctx.walkset(limit, off2, z) as ws:
         sol, cov = ctx.greedy(40, walkset=ws)
     assert cov == exp_cov and sol.tolist() == exp_sol.tolist()
+
+
+def test_partitioned_histogram_large_id_space(ctx, port):
+    """Id spaces whose counters do not fit L2 take the radix-partitioned histogram path."""
+    rng = np.random.Generator(np.random.PCG64(9))
+    limit, nsets = 13_500_000, 2_400_000
+    z = ((np.minimum(rng.zipf(1.15, size=nsets * 2), 10**7) * 2654435761) % limit).astype(np.uint32)
+    off = np.arange(0, 2 * nsets + 1, 2, dtype=np.uint64)
+    exp_sol, exp_cov = port.greedy(limit, off, z, 25)
+    with ctx.walkset(limit, off, z) as ws:
+        sol, cov = ctx.greedy(25, walkset=ws)
+        assert cov == exp_cov and sol.tolist() == exp_sol.tolist()
+        assert ctx.coverage_of(sol, walkset=ws) == port.coverage_of(limit, off, z, sol)
