@@ -231,6 +231,7 @@ struct hsaw_gpu_ctx {
     hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
     // greedy / coverage scratch (greedy.cu), reused across the doubling iterations
     hsawgpu::DevVec<uint32_t> g_cand_bits, g_cnt, g_fill, g_inv, g_covered, g_solution, g_query_bits;
+    hsawgpu::DevVec<uint32_t> g_indexed_bits;  // items that own an inverted list
     hsawgpu::DevVec<uint32_t> g_sorted;  // radix-partitioned copy of the items (large id spaces)
     hsawgpu::DevVec<uint64_t> g_pos, g_partial, g_gains, g_blkmax;
     uint64_t* d_scalars = nullptr;  // 64 u64 of device scratch for counters / cursors
@@ -269,6 +270,7 @@ struct hsaw_gpu_ctx {
         g_gains.swap(o.g_gains);
         g_blkmax.swap(o.g_blkmax);
         g_sorted.swap(o.g_sorted);
+        g_indexed_bits.swap(o.g_indexed_bits);
     }
     template <class F>
     void for_each_buffer(F&& f) {
@@ -281,6 +283,7 @@ struct hsaw_gpu_ctx {
         f(pool_cache.nodes); f(pool_cache.edges); f(pool_cache.tag_seq);
         f(g_cand_bits); f(g_cnt); f(g_fill); f(g_inv); f(g_covered); f(g_solution);
         f(g_query_bits); f(g_pos); f(g_partial); f(g_gains); f(g_blkmax); f(g_sorted);
+        f(g_indexed_bits);
     }
 
     void release_scratch() {
@@ -304,6 +307,7 @@ struct hsaw_gpu_ctx {
         g_gains.release();
         g_blkmax.release();
         g_sorted.release();
+        g_indexed_bits.release();
     }
 };
 

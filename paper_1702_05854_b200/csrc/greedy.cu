@@ -76,10 +76,26 @@ __global__ void key_histogram(const uint32_t* __restrict__ keys, uint64_t n, uin
 }
 
 // K3b: one warp per walk; slot order inside an item's list is irrelevant (set semantics).
-__global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ cand_bits,
+// One bit per item: is it indexed (candidate with count >= min_count)? The bitmap (limit / 8
+// bytes) stays in L2, so the scatter pass needs no random HBM read per item to find that out.
+__global__ void mark_indexed(const uint32_t* __restrict__ cnt, uint32_t limit, uint32_t min_count,
+                             uint32_t* __restrict__ bits) {
+    uint64_t word = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t base = word * 32;
+    if (base >= limit) return;
+    uint32_t w = 0;
+#pragma unroll 8
+    for (uint32_t j = 0; j < 32; ++j) {
+        uint64_t id = base + j;
+        // count > 0 already implies "candidate": the histogram only counts candidates
+        if (id < limit && cnt[id] >= min_count && cnt[id] != 0) w |= 1u << j;
+    }
+    bits[word] = w;
+}
+
+__global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ indexed_bits,
                                  const uint64_t* __restrict__ pos, uint32_t* __restrict__ fill,
-                                 uint32_t* __restrict__ inv, const uint32_t* __restrict__ cnt,
-                                 uint32_t min_count) {
+                                 uint32_t* __restrict__ inv) {
     uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t lane = threadIdx.x & 31;
     uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -89,7 +105,7 @@ __global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ cand_b
         for (uint64_t p = b + lane; p < e; p += 32) {
             uint32_t item = v.items[p];
             // only items that can still win a round are indexed (min_count, see hsaw_gpu_greedy)
-            if (item < v.limit && is_cand(cand_bits, item) && cnt[item] >= min_count) {
+            if (item < v.limit && ((indexed_bits[item >> 5] >> (item & 31)) & 1u)) {
                 uint32_t slot = atomicAdd(&fill[item], 1u);
                 inv[pos[item] + slot] = (uint32_t)i;
             }
@@ -627,8 +643,13 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             if (indexed) {
                 StageScope timer(ctx, HSAW_STAGE_INDEX);
                 int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
-                scatter_inverted<<<sb, 256, 0, st>>>(v, d_cand, d_pos.p, d_fill.p, d_inv.p,
-                                                     d_cnt.p, min_count);
+                DevVec<uint32_t>& d_ibits = ctx->g_indexed_bits;
+                uint64_t words = ((uint64_t)limit + 31) / 32;
+                d_ibits.ensure_scratch(words + 1);
+                mark_indexed<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(d_cnt.p, limit,
+                                                                             min_count, d_ibits.p);
+                check_launch(ctx, "mark_indexed");
+                scatter_inverted<<<sb, 256, 0, st>>>(v, d_ibits.p, d_pos.p, d_fill.p, d_inv.p);
                 check_launch(ctx, "scatter_inverted");
             }
             // ---- rounds
@@ -712,7 +733,7 @@ struct hsaw_gpu_rounds {
     uint32_t limit = 0;
     uint32_t* d_counts = nullptr;  // caller-owned: global marginal-gain counts after all-reduce
     bool has_cand = false;
-    DevVec<uint32_t> cand_bits, fill, inv, covered;
+    DevVec<uint32_t> cand_bits, fill, inv, covered, indexed_bits;
     DevVec<uint64_t> pos, partial, scalars;
     uint64_t occurrences = 0;
     uint32_t npartial = 0;
@@ -766,8 +787,13 @@ int hsaw_gpu_rounds_begin(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             if (g->occurrences) {
                 StageScope timer(ctx, HSAW_STAGE_INDEX);
                 int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
-                scatter_inverted<<<sb, 256, 0, st>>>(v, d_cand, g->pos.p, g->fill.p, g->inv.p,
-                                                     d_counts, 1u);
+                uint64_t words = (limit + 31) / 32;
+                g->indexed_bits.ensure_scratch(words + 1);
+                mark_indexed<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(
+                    d_counts, (uint32_t)limit, 1u, g->indexed_bits.p);
+                check_launch(ctx, "mark_indexed");
+                scatter_inverted<<<sb, 256, 0, st>>>(v, g->indexed_bits.p, g->pos.p, g->fill.p,
+                                                     g->inv.p);
                 check_launch(ctx, "scatter_inverted");
             }
             uint64_t cov_words = (cnt + 31) / 32 + 1;
