@@ -122,10 +122,24 @@ __global__ void __launch_bounds__(256) count_of_counts(const uint32_t* __restric
     __shared__ unsigned long long bins[kCountBins];
     for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x) bins[i] = 0;
     __syncthreads();
+    // almost every non-zero count is tiny: keep those in registers instead of hammering one
+    // shared-memory address with atomics
+    unsigned long long small[5] = {0, 0, 0, 0, 0};
     uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < limit; i += stride) {
         uint32_t c = cnt[i];
-        if (c) atomicAdd(&bins[c < kCountBins ? c : kCountBins - 1], (unsigned long long)c);
+        if (c == 0) continue;
+        if (c <= 4)
+            small[c] += c;
+        else
+            atomicAdd(&bins[c < kCountBins ? c : kCountBins - 1], (unsigned long long)c);
+    }
+#pragma unroll
+    for (int c = 1; c <= 4; ++c) {
+        unsigned long long v = small[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&bins[c], v);
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x)
