@@ -51,10 +51,25 @@ struct __align__(32) EdgeRec {
 static_assert(sizeof(EdgeRec) == 32, "edge record must be one 32-byte sector");
 constexpr uint32_t kEdgeSuspect = 1u, kEdgeSimple = 2u;
 
+// Compact layout: when 4 m + 8 n bytes fit in L2, a step reads in_src[e] (4 bytes)
+// and the 8-byte row header of the source instead of a 32-byte edge record, and both arrays stay
+// L2 resident. Header word w = deg (25 bits) | margin exponent mb (6 bits) | suspect (1 bit).
+// A row is "arithmetic" when its thresholds sit within a margin of the ideal (i+1) * 2^53 / deg
+// grid (always the case for 1/d rows): then slot = (k * deg) >> 53 is exact for every draw whose
+// fractional part keeps 2^mb clear of a slot boundary, and the thresholds are never read. Draws
+// inside the margin and rows with mb == kHdrSlow take the exact path (node record + binary search
+// over thr[]), so arbitrary weights stay bit-exact, only slower.
+constexpr uint32_t kHdrDegBits = 25, kHdrDegMask = (1u << kHdrDegBits) - 1, kHdrSlow = 63;
+constexpr int kLayoutFat = 0, kLayoutCompact = 1;
+
 struct DeviceGraph {
     uint32_t n = 0, m = 0;
+    int layout = kLayoutFat;
     NodeRec* nodes = nullptr;
-    EdgeRec* edges = nullptr;
+    EdgeRec* edges = nullptr;         // fat layout only
+    uint2* hdr = nullptr;             // compact layout: (lo, w) per node
+    uint32_t* src = nullptr;          // compact layout: in_src as uploaded
+    uint64_t* thr = nullptr;          // compact layout: ceil(in_cum * 2^53), exact path only
 };
 
 // ---- errors ------------------------------------------------------------------------------------
@@ -226,6 +241,8 @@ struct hsaw_gpu_ctx {
     hsawgpu::DevVec<unsigned char> cub_tmp;
     hsawgpu::DevVec<hsawgpu::NodeRec> g_nodes_store;  // backing store of g.nodes / g.edges
     hsawgpu::DevVec<hsawgpu::EdgeRec> g_edges_store;
+    hsawgpu::DevVec<uint32_t> g_compact_store;  // compact layout: 2 n header words, then m sources
+    hsawgpu::DevVec<uint64_t> g_thr_store;      // compact layout: pick thresholds (exact path)
     hsawgpu::DevVec<uint32_t> chk_list, chk_mid, chk_counters;  // distinctness-check scratch
     hsawgpu::SamplerScratch samp;                        // per-chunk sampler scratch
     hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
@@ -252,6 +269,8 @@ struct hsaw_gpu_ctx {
     void swap_buffers(hsaw_gpu_ctx& o) {
         g_nodes_store.swap(o.g_nodes_store);
         g_edges_store.swap(o.g_edges_store);
+        g_compact_store.swap(o.g_compact_store);
+        g_thr_store.swap(o.g_thr_store);
         cub_tmp.swap(o.cub_tmp);
         chk_list.swap(o.chk_list);
         chk_mid.swap(o.chk_mid);
@@ -274,7 +293,7 @@ struct hsaw_gpu_ctx {
     }
     template <class F>
     void for_each_buffer(F&& f) {
-        f(g_nodes_store); f(g_edges_store); f(cub_tmp); f(chk_list); f(chk_mid); f(chk_counters);
+        f(g_nodes_store); f(g_edges_store); f(g_compact_store); f(g_thr_store); f(cub_tmp); f(chk_list); f(chk_mid); f(chk_counters);
         f(samp.slot_seed); f(samp.enc_seed); f(samp.tmp_off); f(samp.voff); f(samp.enc_batch);
         f(samp.slot_len); f(samp.count); f(samp.first); f(samp.enc_len); f(samp.enc_seq);
         f(samp.tmp_nodes); f(samp.tmp_edges); f(samp.vidx); f(samp.status); f(samp.arena);
@@ -289,6 +308,8 @@ struct hsaw_gpu_ctx {
     void release_scratch() {
         g_nodes_store.release();
         g_edges_store.release();
+        g_compact_store.release();
+        g_thr_store.release();
         samp.release();
         pool_cache.release();
         cub_tmp.release();

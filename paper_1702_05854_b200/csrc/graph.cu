@@ -113,6 +113,62 @@ __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
     }
 }
 
+// Compact layout: thresholds (exact path only), validation, and per row the margin inside which the
+// arithmetic pick (k * deg) >> 53 may disagree with the thresholds. With err_i the distance of
+// threshold i from the ideal grid in units of 1/deg, err_i = |thr[i] * deg - (i+1) * 2^53|, every
+// draw whose guess differs from the threshold-defined slot has frac(k * deg / 2^53) < max err or
+// > 2^53 - max err (walk.cuh, pick_arith). The last threshold is the total-weight one, so "no live
+// edge" draws (k >= thr[deg-1]) fall inside the margin as well. One warp per row.
+__global__ void build_compact(uint32_t n, const uint64_t* __restrict__ off,
+                              const uint32_t* __restrict__ src, const double* __restrict__ cum,
+                              const double* __restrict__ p_of, uint64_t* __restrict__ thr,
+                              uint2* __restrict__ hdr, uint32_t* __restrict__ bad_row,
+                              int force_exact) {
+    uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint64_t kSat = 1ull << 62;
+    for (uint32_t v = warp; v < n; v += nwarps) {
+        uint64_t lo = off[v], hi = off[v + 1];
+        uint64_t d = hi - lo;
+        uint64_t maxerr = 0;
+        for (uint64_t e = lo + lane; e < hi; e += 32) {
+            double c = cum[e];
+            uint64_t t = ge_threshold(c);
+            thr[e] = t;
+            if (e > lo && !(c >= cum[e - 1])) atomicMin(bad_row, v);  // decreasing or NaN
+            if (src[e] >= n) atomicMin(bad_row + 1, v);               // source id out of range
+            unsigned __int128 a = (unsigned __int128)t * d;
+            unsigned __int128 b = (unsigned __int128)(e - lo + 1) << 53;
+            unsigned __int128 diff = a > b ? a - b : b - a;
+            uint64_t err = diff >= kSat ? kSat : (uint64_t)diff;
+            maxerr = err > maxerr ? err : maxerr;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t other = __shfl_xor_sync(kFullMask, maxerr, o);
+            maxerr = other > maxerr ? other : maxerr;
+        }
+        if (lane == 0) {
+            uint64_t need = maxerr + d + 1;  // margin in units of 1/deg, with slack
+            uint32_t mb = 64 - __clzll((long long)need);  // 2^mb > need
+            if (mb > 52 || d > kHdrDegMask || force_exact) mb = kHdrSlow;
+            uint32_t w = (uint32_t)(d > kHdrDegMask ? kHdrDegMask : d) | (mb << kHdrDegBits) |
+                         (p_of[v] > 0.0 ? 0x80000000u : 0u);
+            hdr[v] = make_uint2((uint32_t)lo, w);
+        }
+    }
+}
+
+__global__ void update_hdr_suspect_flags(uint32_t n, const double* __restrict__ p_of,
+                                         uint2* __restrict__ hdr) {
+    uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    uint32_t w = hdr[v].y & 0x7FFFFFFFu;
+    if (p_of[v] > 0.0) w |= 0x80000000u;
+    hdr[v].y = w;
+}
+
 // New suspect set on the same graph: refresh the suspect bit the edge records carry.
 __global__ void update_edge_suspect_flags(uint32_t m, const double* __restrict__ p_of,
                                           EdgeRec* __restrict__ edges) {
@@ -151,6 +207,21 @@ void pin_node_records_in_l2(hsaw_gpu_ctx* ctx) {
     if (cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr) !=
         cudaSuccess)
         cudaGetLastError();
+}
+
+// Layout choice: the compact arrays when they fit in L2, else fat edge records.
+// HSAW_LAYOUT=compact|fat overrides.
+int choose_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
+    if (const char* env = std::getenv("HSAW_LAYOUT")) {
+        if (env[0] == 'c') return kLayoutCompact;
+        if (env[0] == 'f') return kLayoutFat;
+    }
+    int l2 = 0;
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device) != cudaSuccess) {
+        cudaGetLastError();
+        l2 = 0;
+    }
+    return 4ull * m + 8ull * n <= (uint64_t)l2 ? kLayoutCompact : kLayoutFat;
 }
 
 void free_graph(hsaw_gpu_ctx* ctx) {  // the backing stores keep their capacity for the next upload
@@ -374,21 +445,34 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             if (d_p) cudaFreeAsync(d_p, st);
             if (d_bad) cudaFreeAsync(d_bad, st);
         };
+        const int layout = choose_layout(ctx, n, m);
+        const bool compact = layout == kLayoutCompact;
         try {
             ctx->g_nodes_store.ensure_scratch(n);
-            ctx->g_edges_store.ensure_scratch(m ? m : 1);
             ctx->g.nodes = ctx->g_nodes_store.p;
-            ctx->g.edges = ctx->g_edges_store.p;
+            ctx->g.layout = layout;
+            if (compact) {
+                // header words first (8-byte aligned), then the sources exactly as uploaded
+                ctx->g_compact_store.ensure_scratch(2ull * n + (m ? m : 1));
+                ctx->g_thr_store.ensure_scratch(m ? m : 1);
+                ctx->g.hdr = reinterpret_cast<uint2*>(ctx->g_compact_store.p);
+                ctx->g.src = ctx->g_compact_store.p + 2ull * n;
+                ctx->g.thr = ctx->g_thr_store.p;
+            } else {
+                ctx->g_edges_store.ensure_scratch(m ? m : 1);
+                ctx->g.edges = ctx->g_edges_store.p;
+            }
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_off, ((uint64_t)n + 1) * 8, st));
-            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_src, (uint64_t)(m ? m : 1) * 4, st));
+            if (!compact)
+                HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_src, (uint64_t)(m ? m : 1) * 4, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_cum, (uint64_t)(m ? m : 1) * 8, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_bad, 8, st));
             HSAW_CUDA_CHECK(cudaMemcpyAsync(d_off, in_offsets, ((uint64_t)n + 1) * 8,
                                             cudaMemcpyHostToDevice, st));
             if (m) {
-                HSAW_CUDA_CHECK(
-                    cudaMemcpyAsync(d_src, in_src, (uint64_t)m * 4, cudaMemcpyHostToDevice, st));
+                HSAW_CUDA_CHECK(cudaMemcpyAsync(compact ? ctx->g.src : d_src, in_src,
+                                                (uint64_t)m * 4, cudaMemcpyHostToDevice, st));
                 HSAW_CUDA_CHECK(
                     cudaMemcpyAsync(d_cum, in_cum, (uint64_t)m * 8, cudaMemcpyHostToDevice, st));
             }
@@ -399,8 +483,14 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
                 build_node_records<<<(n + 255) / 256, 256, 0, st>>>(n, d_off, d_cum, d_p,
                                                                     ctx->g.nodes);
                 check_launch(ctx, "build_node_records");
-                if (m) {
-                    int blocks = ctx->sm_count * 8;
+                int blocks = ctx->sm_count * 8;
+                if (compact) {
+                    const char* env = std::getenv("HSAW_FORCE_EXACT");  // test hook: exact picks
+                    build_compact<<<blocks, 256, 0, st>>>(n, d_off, ctx->g.src, d_cum, d_p,
+                                                          ctx->g.thr, ctx->g.hdr, d_bad,
+                                                          env && std::atoi(env) != 0);
+                    check_launch(ctx, "build_compact");
+                } else if (m) {
                     build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p,
                                                                ctx->g.edges, d_bad);
                     check_launch(ctx, "build_edge_records");
@@ -424,8 +514,12 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
         cleanup();
         ctx->g.n = n;
         ctx->g.m = m;
-        ctx->graph_bytes = (uint64_t)n * sizeof(NodeRec) + (uint64_t)m * sizeof(EdgeRec);
-        pin_node_records_in_l2(ctx);
+        if (compact) {
+            ctx->graph_bytes = (uint64_t)n * (sizeof(NodeRec) + 8) + (uint64_t)m * 12;
+        } else {
+            ctx->graph_bytes = (uint64_t)n * sizeof(NodeRec) + (uint64_t)m * sizeof(EdgeRec);
+            pin_node_records_in_l2(ctx);
+        }
     });
 }
 
@@ -443,7 +537,11 @@ int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of) {
             update_accept_thresholds<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, d_p,
                                                                                ctx->g.nodes);
             ++ctx->launches;
-            if (ctx->g.m) {
+            if (ctx->g.layout == kLayoutCompact) {
+                update_hdr_suspect_flags<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, d_p,
+                                                                                   ctx->g.hdr);
+                ++ctx->launches;
+            } else if (ctx->g.m) {
                 update_edge_suspect_flags<<<(ctx->g.m + 255) / 256, 256, 0, ctx->stream>>>(
                     ctx->g.m, d_p, ctx->g.edges);
                 ++ctx->launches;

@@ -25,6 +25,9 @@ constexpr int kDefaultRecordBlocksPerSM = 4;  // recording: 4 x 32 KB staging, m
 struct EncodeParams {
     const NodeRec* nodes;
     const EdgeRec* edges;
+    const uint2* hdr;      // compact layout (DeviceGraph)
+    const uint32_t* src;
+    const uint64_t* thr;
     uint32_t n;
     uint32_t l;       // attempts per batch
     uint32_t window;  // runtime width for the generic kernel
@@ -140,7 +143,8 @@ __device__ __forceinline__ bool claim(uint64_t* cursor, uint64_t total, bool wan
 // -1 for the runtime-width variant.
 // REC: 0 plain encode, 1 record walks (default stores), 2 record with streaming (.cs) stores.
 // STATS: per-lane work counters (draws, picks, algorithmic bytes) for instrumentation runs.
-template <int HEUR, int WIN, int MINB, int REC, bool STATS>
+// LAYOUT: kLayoutFat (32-byte edge records) or kLayoutCompact (in_src + 8-byte row headers).
+template <int HEUR, int WIN, int MINB, int REC, bool STATS, int LAYOUT>
 __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) {
     // REC: every thread stages kStage pairs (128 bytes) in shared memory, slot-major so the
     // 8-byte accesses are conflict-free, and flushes whole 128-byte lines: short failed attempts
@@ -174,7 +178,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
     uint64_t s = 0, snapshot = 0;
     uint32_t bidx = 0;  // batch index within the launch (launches hold < 2^32 batches)
     uint32_t lo = 0, deg = 0;
-    uint64_t tot = 0, scale = 0;
+    uint64_t tot = 0, scale = 0;  // fat layout: total-weight threshold and guess scale of the row
+    uint32_t hw = 0, cur = 0;     // compact layout: header word and id of the current node
     uint32_t nedges = 0, att = 0, cnt = 0;
     bool have = false, fresh = true, drained = false;
     Window<WIN> win;
@@ -234,12 +239,28 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                 uint64_t k = draw53(s);
                 if (STATS) st_draws += 1;
                 if (STATS) st_steps += 1;
-                bool live = deg != 0 && k < tot;  // graph.hpp:66
-                if (STATS) st_bytes += pick_alg_bytes(deg, live);
+                bool live;
+                uint32_t slot_in_row = 0;
+                if (LAYOUT == kLayoutCompact) {
+                    uint32_t true_deg = deg;
+                    if (deg == 0)
+                        live = false;
+                    else if (pick_arith(hw, k, slot_in_row))
+                        live = true;
+                    else  // draw inside the row's margin, or not an arithmetic row: exact path
+                        live = pick_exact(nodes, p.thr, cur, k, lo, true_deg, slot_in_row);
+                    if (STATS) st_bytes += pick_alg_bytes(true_deg, live);
+                    if (live) u = load_src(p.src, (uint64_t)lo + slot_in_row);
+                } else {
+                    live = deg != 0 && k < tot;  // graph.hpp:66
+                    if (STATS) st_bytes += pick_alg_bytes(deg, live);
+                    if (live) {
+                        slot_in_row = pick_slot(edges, lo, deg, scale, k, erec);
+                        u = erec.src;
+                        from_edge = true;
+                    }
+                }
                 if (live) {
-                    const uint32_t slot_in_row = pick_slot(edges, lo, deg, scale, k, erec);
-                    u = erec.src;
-                    from_edge = true;
                     bool cyc = win.contains(u);  // sampler.cpp:180
                     if (HEUR == 0 && !cyc) {     // BrentState::check, sampler.cpp:100-108
                         if (u == b_anchor) {
@@ -263,10 +284,24 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
         if (walking) {
             if (STATS) st_bytes += 8;  // p_of[u]
             NodeRec rec;
+            uint32_t new_hw = 0;
             bool accepted = false;
-            // Common case: u is not a suspect (no acceptance draw) and the edge record already
-            // holds u's row header, so the walk continues without touching u's node record.
-            if (from_edge && header_from_edge(erec, rec.lo, rec.deg, rec.tot_thr, rec.scale)) {
+            if (LAYOUT == kLayoutCompact) {
+                // 8-byte row header of u; the node record is only read for suspects
+                const uint2 h = load_hdr(p.hdr, u);
+                rec.lo = h.x;
+                rec.deg = hdr_deg(h.y);
+                new_hw = h.y;
+                if (hdr_suspect(h.y)) {  // is_suspect, sampler.cpp:32,55
+                    const NodeRec full = load_node(nodes, u);
+                    uint64_t k2 = draw53(s);
+                    if (STATS) st_draws += 1;
+                    accepted = k2 < full.acc_thr;  // r <= p_of[u], sampler.cpp:34,57
+                }
+            } else if (from_edge &&
+                       header_from_edge(erec, rec.lo, rec.deg, rec.tot_thr, rec.scale)) {
+                // Common case: u is not a suspect (no acceptance draw) and the edge record already
+                // holds u's row header, so the walk continues without touching u's node record.
                 rec.acc_thr = 0;
             } else {
                 rec = load_node(nodes, u);
@@ -296,8 +331,13 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             } else {
                 lo = rec.lo;
                 deg = rec.deg;
-                tot = rec.tot_thr;
-                scale = rec.scale;
+                if (LAYOUT == kLayoutCompact) {
+                    hw = new_hw;
+                    cur = u;
+                } else {
+                    tot = rec.tot_thr;
+                    scale = rec.scale;
+                }
                 if (fresh) {
                     win.reset(p.window, u);  // sampler.cpp:166-169
                     b_anchor = u;
@@ -354,6 +394,9 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
 struct DecodeParams {
     const NodeRec* nodes;
     const EdgeRec* edges;
+    const uint2* hdr;  // compact layout (DeviceGraph)
+    const uint32_t* src;
+    const uint64_t* thr;
     uint32_t n;
     uint64_t nwalks;
     const uint64_t* seed;
@@ -371,7 +414,7 @@ struct DecodeParams {
     uint2* const* pair_dst;
 };
 
-template <bool PAIRS>
+template <bool PAIRS, int LAYOUT>
 __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
     const uint32_t lane = threadIdx.x & 31;
     const NodeRec* __restrict__ nodes = p.nodes;
@@ -381,6 +424,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
     uint2* pairs = nullptr;
     uint32_t lo = 0, deg = 0, len = 0, nedges = 0;
     uint64_t tot = 0, scale = 0;
+    uint32_t hw = 0, cur = 0;  // compact layout: header word and id of the current node
     bool have = false, fresh = true, drained = false;
     uint64_t st_steps = 0;
 
@@ -428,12 +472,28 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
             } else {
                 uint64_t k = draw53(s);
                 st_steps += 1;
-                if (deg == 0 || k >= tot) {
+                bool live;
+                uint32_t slot = 0;
+                if (LAYOUT == kLayoutCompact) {
+                    uint32_t true_deg = deg;
+                    if (deg == 0)
+                        live = false;
+                    else if (pick_arith(hw, k, slot))
+                        live = true;
+                    else
+                        live = pick_exact(nodes, p.thr, cur, k, lo, true_deg, slot);
+                    if (live) u = load_src(p.src, (uint64_t)lo + slot);
+                } else {
+                    live = deg != 0 && k < tot;
+                    if (live) {
+                        slot = pick_slot(edges, lo, deg, scale, k, erec);
+                        u = erec.src;
+                        from_edge = true;
+                    }
+                }
+                if (!live) {
                     verdict = 2;
                 } else {
-                    uint32_t slot = pick_slot(edges, lo, deg, scale, k, erec);
-                    u = erec.src;
-                    from_edge = true;
                     if (PAIRS) {
                         ++nedges;
                         pairs[nedges] = make_uint2(u, lo + slot);
@@ -448,8 +508,16 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
         }
         if (arrived) {
             NodeRec rec;
+            uint32_t new_hw = 0;
             bool hit = false;
-            if (from_edge && header_from_edge(erec, rec.lo, rec.deg, rec.tot_thr, rec.scale)) {
+            if (LAYOUT == kLayoutCompact) {
+                const uint2 h = load_hdr(p.hdr, u);
+                rec.lo = h.x;
+                rec.deg = hdr_deg(h.y);
+                new_hw = h.y;
+                if (hdr_suspect(h.y)) hit = draw53(s) < load_node(nodes, u).acc_thr;
+            } else if (from_edge &&
+                       header_from_edge(erec, rec.lo, rec.deg, rec.tot_thr, rec.scale)) {
                 rec.acc_thr = 0;
             } else {
                 rec = load_node(nodes, u);
@@ -462,8 +530,13 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
             } else {
                 lo = rec.lo;
                 deg = rec.deg;
-                tot = rec.tot_thr;
-                scale = rec.scale;
+                if (LAYOUT == kLayoutCompact) {
+                    hw = new_hw;
+                    cur = u;
+                } else {
+                    tot = rec.tot_thr;
+                    scale = rec.scale;
+                }
                 fresh = false;
             }
         }
@@ -650,9 +723,14 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
                    bool with_stats) {
     if (nbatches == 0) return;
     if (nbatches > 0xFFFFFFFFull) fail(HSAW_EINVAL, "encode: more than 2^32 batches per launch");
-    EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, cfg.batch_size, cfg.window,
-                   first_worker, nbatches, d_seed, d_len, d_count, d_stats, d_cursor,
-                   nullptr, 0, nullptr, nullptr};
+    EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, ctx->g.src, ctx->g.thr, ctx->g.n,
+                   cfg.batch_size, cfg.window, first_worker, nbatches, d_seed, d_len, d_count,
+                   d_stats, d_cursor, nullptr, 0, nullptr, nullptr};
+    const bool compact = ctx->g.layout == kLayoutCompact;
+// one instantiation per graph layout
+#define HSAW_GO(H, W, B, R, S)                                                   \
+    (compact ? go(encode_kernel<H, W, B, R, S, kLayoutCompact>)                  \
+             : go(encode_kernel<H, W, B, R, S, kLayoutFat>))
     if (rec) {
         if (rec->arena_cap < kLogChunk) fail(HSAW_EINVAL, "encode: record arena too small");
         p.arena = rec->arena;
@@ -689,29 +767,30 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
                                                     : kDefaultEncodeBlocksPerSM)) >= 5;
         const int key = mode * 4 + (five ? 2 : 0) + (with_stats ? 1 : 0);
         switch (key) {
-            case 0: go(encode_kernel<0, 2, 4, 0, false>); break;
-            case 1: go(encode_kernel<0, 2, 4, 0, true>); break;
-            case 2: go(encode_kernel<0, 2, 5, 0, false>); break;
-            case 3: go(encode_kernel<0, 2, 5, 0, true>); break;
-            case 4: go(encode_kernel<0, 2, 4, 1, false>); break;
-            case 5: go(encode_kernel<0, 2, 4, 1, true>); break;
-            case 6: go(encode_kernel<0, 2, 5, 1, false>); break;
-            case 7: go(encode_kernel<0, 2, 5, 1, true>); break;
-            case 8: go(encode_kernel<0, 2, 4, 2, false>); break;
-            case 9: go(encode_kernel<0, 2, 4, 2, true>); break;
-            case 10: go(encode_kernel<0, 2, 5, 2, false>); break;
-            default: go(encode_kernel<0, 2, 5, 2, true>); break;
+            case 0: HSAW_GO(0, 2, 4, 0, false); break;
+            case 1: HSAW_GO(0, 2, 4, 0, true); break;
+            case 2: HSAW_GO(0, 2, 5, 0, false); break;
+            case 3: HSAW_GO(0, 2, 5, 0, true); break;
+            case 4: HSAW_GO(0, 2, 4, 1, false); break;
+            case 5: HSAW_GO(0, 2, 4, 1, true); break;
+            case 6: HSAW_GO(0, 2, 5, 1, false); break;
+            case 7: HSAW_GO(0, 2, 5, 1, true); break;
+            case 8: HSAW_GO(0, 2, 4, 2, false); break;
+            case 9: HSAW_GO(0, 2, 4, 2, true); break;
+            case 10: HSAW_GO(0, 2, 5, 2, false); break;
+            default: HSAW_GO(0, 2, 5, 2, true); break;
         }
     } else {
         // other SamplerConfig values: correctness paths, instrumented, never recording
         if (rec) fail(HSAW_EINVAL, "encode: recording is only built for the default sampler config");
         if (cfg.window == 2)
-            go(encode_kernel<2, 2, 4, 0, true>);
+            HSAW_GO(2, 2, 4, 0, true);
         else if (cfg.window == 0)
-            brent ? go(encode_kernel<0, 0, 4, 0, true>) : go(encode_kernel<2, 0, 4, 0, true>);
+            brent ? HSAW_GO(0, 0, 4, 0, true) : HSAW_GO(2, 0, 4, 0, true);
         else
-            brent ? go(encode_kernel<0, -1, 4, 0, true>) : go(encode_kernel<2, -1, 4, 0, true>);
+            brent ? HSAW_GO(0, -1, 4, 0, true) : HSAW_GO(2, -1, 4, 0, true);
     }
+#undef HSAW_GO
 }
 
 bool record_supported(const hsaw_sampler_cfg& cfg) { return cfg.heuristic == 0 && cfg.window == 2; }
@@ -721,7 +800,8 @@ uint32_t record_overflow_marker() { return kLogOverflow; }
 
 // Lanes of one resident wave of the default recording kernel (each may hold one open chunk).
 uint64_t record_resident_lanes(hsaw_gpu_ctx* ctx) {
-    return (uint64_t)persistent_blocks(ctx, encode_kernel<0, 2, 4, 2, false>, ~0ull >> 8) * kThreads;
+    return (uint64_t)persistent_blocks(ctx, encode_kernel<0, 2, 4, 2, false, kLayoutFat>,
+                                       ~0ull >> 8) * kThreads;
 }
 
 static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
@@ -729,14 +809,20 @@ static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_
                                uint32_t* d_nodes, uint32_t* d_edges, uint8_t* d_status,
                                uint32_t* d_nnodes, uint64_t* d_stats, uint64_t* d_cursor) {
     if (nwalks == 0) return;
-    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, nwalks,   d_seed,  d_len,   d_edge_off,
-                   d_nodes,      d_edges,      d_status, d_nnodes, d_stats, d_cursor, nullptr,
-                   nullptr};
+    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, ctx->g.src, ctx->g.thr, ctx->g.n,
+                   nwalks,       d_seed,       d_len,      d_edge_off, d_nodes,    d_edges,
+                   d_status,     d_nnodes,     d_stats,    d_cursor,   nullptr,    nullptr};
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
-    int blocks = persistent_blocks(ctx, decode_kernel<false>, nwalks);
-    StageScope timer(ctx, HSAW_STAGE_DECODE);
-    decode_kernel<false><<<blocks, kThreads, 0, ctx->stream>>>(p);
-    check_launch(ctx, "decode_kernel");
+    auto go = [&](auto kernel) {
+        int blocks = persistent_blocks(ctx, kernel, nwalks);
+        StageScope timer(ctx, HSAW_STAGE_DECODE);
+        kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+        check_launch(ctx, "decode_kernel");
+    };
+    if (ctx->g.layout == kLayoutCompact)
+        go(decode_kernel<false, kLayoutCompact>);
+    else
+        go(decode_kernel<false, kLayoutFat>);
 }
 
 void launch_decode(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
@@ -751,14 +837,20 @@ void launch_decode_pairs(hsaw_gpu_ctx* ctx, uint64_t nsel, const uint32_t* d_sel
                          const uint64_t* d_seed, const uint32_t* d_len, uint2* const* d_pair_dst,
                          uint8_t* d_status, uint64_t* d_stats, uint64_t* d_cursor) {
     if (nsel == 0) return;
-    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.n, nsel,    d_seed,  d_len,    nullptr,
-                   nullptr,      nullptr,      d_status, nullptr, d_stats, d_cursor, d_sel,
-                   d_pair_dst};
+    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, ctx->g.src, ctx->g.thr, ctx->g.n,
+                   nsel,         d_seed,       d_len,      nullptr,    nullptr,    nullptr,
+                   d_status,     nullptr,      d_stats,    d_cursor,   d_sel,      d_pair_dst};
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
-    int blocks = persistent_blocks(ctx, decode_kernel<true>, nsel);
-    StageScope timer(ctx, HSAW_STAGE_DECODE);
-    decode_kernel<true><<<blocks, kThreads, 0, ctx->stream>>>(p);
-    check_launch(ctx, "decode_kernel<pairs>");
+    auto go = [&](auto kernel) {
+        int blocks = persistent_blocks(ctx, kernel, nsel);
+        StageScope timer(ctx, HSAW_STAGE_DECODE);
+        kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+        check_launch(ctx, "decode_kernel<pairs>");
+    };
+    if (ctx->g.layout == kLayoutCompact)
+        go(decode_kernel<true, kLayoutCompact>);
+    else
+        go(decode_kernel<true, kLayoutFat>);
 }
 
 // Exact recheck on either node source. Classic: d_edge_off/d_nodes(/d_nnodes). Pair logs:

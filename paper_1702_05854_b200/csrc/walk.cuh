@@ -132,6 +132,58 @@ __device__ __forceinline__ bool header_from_edge(const EdgeRec& rec, uint32_t& l
     return true;
 }
 
+// ---- compact layout ------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t hdr_deg(uint32_t w) { return w & kHdrDegMask; }
+__device__ __forceinline__ uint32_t hdr_mb(uint32_t w) { return (w >> kHdrDegBits) & 63u; }
+__device__ __forceinline__ bool hdr_suspect(uint32_t w) { return (w >> 31) != 0; }
+
+__device__ __forceinline__ uint2 load_hdr(const uint2* __restrict__ hdr, uint32_t v) {
+    uint2 h;
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(h.x), "=r"(h.y) : "l"(hdr + v));
+    return h;
+}
+
+__device__ __forceinline__ uint32_t load_src(const uint32_t* __restrict__ src, uint64_t e) {
+    uint32_t u;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(u) : "l"(src + e));
+    return u;
+}
+
+// Live-edge pick on an arithmetic row without touching the thresholds: slot = (k * deg) >> 53.
+// Returns true when the draw is provably live and the slot exact, i.e. the fractional part of
+// k * deg / 2^53 keeps the row's margin 2^mb clear of both slot boundaries (graph.cu,
+// build_compact: the margin covers the distance of every threshold, the total-weight threshold
+// included, from the ideal grid). deg < 2^25, k < 2^53: the product needs 78 bits.
+__device__ __forceinline__ bool pick_arith(uint32_t w, uint64_t k, uint32_t& slot) {
+    const uint32_t deg = hdr_deg(w);
+    const uint64_t plo = k * deg, phi = __umul64hi(k, (uint64_t)deg);
+    slot = (uint32_t)((plo >> 53) | (phi << 11));
+    const uint64_t frac = plo & ((1ull << 53) - 1);
+    const uint64_t margin = 1ull << hdr_mb(w);  // mb == kHdrSlow: 2^63, never satisfied
+    return frac >= margin && frac <= (1ull << 53) - margin;
+}
+
+// Exact path of the compact layout: pick_live_in_edge (graph.hpp:61-80) from the node record and
+// the threshold array. Returns false for "no edge"; else lo/slot of the first i with k < thr.
+__device__ __noinline__ bool pick_exact(const NodeRec* __restrict__ nodes,
+                                        const uint64_t* __restrict__ thr, uint32_t v, uint64_t k,
+                                        uint32_t& lo, uint32_t& deg, uint32_t& slot) {
+    NodeRec r = load_node(nodes, v);
+    lo = r.lo;
+    deg = r.deg;
+    if (r.deg == 0 || k >= r.tot_thr) return false;
+    uint32_t a = 0, b = r.deg - 1;  // answer in [a, b]; k < thr[b] holds (thr[deg-1] == tot_thr)
+    while (a < b) {
+        uint32_t mid = a + (b - a) / 2;
+        if (k < __ldg(thr + (uint64_t)r.lo + mid))
+            b = mid;
+        else
+            a = mid + 1;
+    }
+    slot = a;
+    return true;
+}
+
 // Algorithmic bytes of one pick in the reference layout:
 // empty row 16; r >= total 24; success 28 + 8*ceil(log2 d). p_of (8) is added when resolve runs.
 __device__ __forceinline__ uint32_t pick_alg_bytes(uint32_t deg, bool success) {

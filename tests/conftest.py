@@ -82,9 +82,23 @@ def gpu_lib():
     return capi
 
 
-@pytest.fixture()
-def ctx(gpu_lib):
-    """A fresh device context per test (the CUDA extension must be present: no fallback)."""
+# Device graph layouts, chosen at upload time: the L2-resident compact arrays with
+# arithmetic picks, the same with every pick forced through the exact threshold path, and the fat
+# 32-byte edge records used when the graph outgrows L2. Every parity test runs on all three.
+LAYOUTS = {
+    "compact": {"HSAW_LAYOUT": "compact"},
+    "compact-exact": {"HSAW_LAYOUT": "compact", "HSAW_FORCE_EXACT": "1"},
+    "fat": {"HSAW_LAYOUT": "fat"},
+}
+
+
+@pytest.fixture(params=list(LAYOUTS))
+def ctx(request, gpu_lib, monkeypatch):
+    """A fresh device context per test and graph layout (the CUDA extension must be present: no
+    fallback)."""
+    monkeypatch.delenv("HSAW_FORCE_EXACT", raising=False)
+    for k, v in LAYOUTS[request.param].items():
+        monkeypatch.setenv(k, v)
     c = gpu_lib.Context(0)
     yield c
     c.close()
