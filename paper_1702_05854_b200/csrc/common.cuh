@@ -53,7 +53,9 @@ constexpr uint32_t kEdgeSuspect = 1u, kEdgeSimple = 2u;
 
 // Compact layout: when 4 m + 8 n bytes fit in L2, a step reads in_src[e] (4 bytes)
 // and the 8-byte row header of the source instead of a 32-byte edge record, and both arrays stay
-// L2 resident. Header word w = deg (25 bits) | margin exponent mb (6 bits) | suspect (1 bit).
+// L2 resident (the headers are 16 bytes: row start, w, and the top 32 bits of the acceptance
+// threshold, so one gather settles an arrival). w = deg (25 bits) | margin exponent mb (6 bits) |
+// suspect (1 bit).
 // A row is "arithmetic" when its thresholds sit within a margin of the ideal (i+1) * 2^53 / deg
 // grid (always the case for 1/d rows): then slot = (k * deg) >> 53 is exact for every draw whose
 // fractional part keeps 2^mb clear of a slot boundary, and the thresholds are never read. Draws
@@ -67,7 +69,8 @@ struct DeviceGraph {
     int layout = kLayoutFat;
     NodeRec* nodes = nullptr;
     EdgeRec* edges = nullptr;         // fat layout only
-    uint2* hdr = nullptr;             // compact layout: (lo, w) per node
+    uint4* hdr = nullptr;             // compact layout: (lo, w, acceptance code, 0) per node;
+                                      // code 0 = not a suspect, else (acc_thr >> 21) + 1
     uint32_t* src = nullptr;          // compact layout: in_src as uploaded
     uint64_t* thr = nullptr;          // compact layout: ceil(in_cum * 2^53), exact path only
 };
@@ -241,7 +244,7 @@ struct hsaw_gpu_ctx {
     hsawgpu::DevVec<unsigned char> cub_tmp;
     hsawgpu::DevVec<hsawgpu::NodeRec> g_nodes_store;  // backing store of g.nodes / g.edges
     hsawgpu::DevVec<hsawgpu::EdgeRec> g_edges_store;
-    hsawgpu::DevVec<uint32_t> g_compact_store;  // compact layout: 2 n header words, then m sources
+    hsawgpu::DevVec<uint32_t> g_compact_store;  // compact layout: 4 n header words, then m sources
     hsawgpu::DevVec<uint64_t> g_thr_store;      // compact layout: pick thresholds (exact path)
     hsawgpu::DevVec<uint32_t> chk_list, chk_mid, chk_counters;  // distinctness-check scratch
     hsawgpu::SamplerScratch samp;                        // per-chunk sampler scratch

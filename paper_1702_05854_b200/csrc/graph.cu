@@ -119,10 +119,20 @@ __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
 // draw whose guess differs from the threshold-defined slot has frac(k * deg / 2^53) < max err or
 // > 2^53 - max err (walk.cuh, pick_arith). The last threshold is the total-weight one, so "no live
 // edge" draws (k >= thr[deg-1]) fall inside the margin as well. One warp per row.
+// Top 32 bits of the acceptance threshold, biased by one so that 0 means "not a suspect": with
+// A = acc32 - 1 and h = k >> 21, h < A accepts and h > A rejects; h == A (2^-32 of the draws) and
+// the saturated code 0xFFFFFFFF are settled against the exact threshold in the node record.
+__device__ __forceinline__ uint32_t accept_code(double p) {
+    uint64_t t = accept_threshold(p);
+    if (t == 0) return 0;
+    uint64_t a = (t >> 21) + 1;
+    return a >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)a;
+}
+
 __global__ void build_compact(uint32_t n, const uint64_t* __restrict__ off,
                               const uint32_t* __restrict__ src, const double* __restrict__ cum,
                               const double* __restrict__ p_of, uint64_t* __restrict__ thr,
-                              uint2* __restrict__ hdr, uint32_t* __restrict__ bad_row,
+                              uint4* __restrict__ hdr, uint32_t* __restrict__ bad_row,
                               int force_exact) {
     uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t lane = threadIdx.x & 31;
@@ -155,18 +165,19 @@ __global__ void build_compact(uint32_t n, const uint64_t* __restrict__ off,
             if (mb > 52 || d > kHdrDegMask || force_exact) mb = kHdrSlow;
             uint32_t w = (uint32_t)(d > kHdrDegMask ? kHdrDegMask : d) | (mb << kHdrDegBits) |
                          (p_of[v] > 0.0 ? 0x80000000u : 0u);
-            hdr[v] = make_uint2((uint32_t)lo, w);
+            hdr[v] = make_uint4((uint32_t)lo, w, accept_code(p_of[v]), 0u);
         }
     }
 }
 
 __global__ void update_hdr_suspect_flags(uint32_t n, const double* __restrict__ p_of,
-                                         uint2* __restrict__ hdr) {
+                                         uint4* __restrict__ hdr) {
     uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     uint32_t w = hdr[v].y & 0x7FFFFFFFu;
     if (p_of[v] > 0.0) w |= 0x80000000u;
     hdr[v].y = w;
+    hdr[v].z = accept_code(p_of[v]);
 }
 
 // New suspect set on the same graph: refresh the suspect bit the edge records carry.
@@ -221,7 +232,7 @@ int choose_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
         cudaGetLastError();
         l2 = 0;
     }
-    return 4ull * m + 8ull * n <= (uint64_t)l2 ? kLayoutCompact : kLayoutFat;
+    return 4ull * m + 16ull * n <= (uint64_t)l2 ? kLayoutCompact : kLayoutFat;
 }
 
 void free_graph(hsaw_gpu_ctx* ctx) {  // the backing stores keep their capacity for the next upload
@@ -453,10 +464,10 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             ctx->g.layout = layout;
             if (compact) {
                 // header words first (8-byte aligned), then the sources exactly as uploaded
-                ctx->g_compact_store.ensure_scratch(2ull * n + (m ? m : 1));
+                ctx->g_compact_store.ensure_scratch(4ull * n + (m ? m : 1));
                 ctx->g_thr_store.ensure_scratch(m ? m : 1);
-                ctx->g.hdr = reinterpret_cast<uint2*>(ctx->g_compact_store.p);
-                ctx->g.src = ctx->g_compact_store.p + 2ull * n;
+                ctx->g.hdr = reinterpret_cast<uint4*>(ctx->g_compact_store.p);
+                ctx->g.src = ctx->g_compact_store.p + 4ull * n;
                 ctx->g.thr = ctx->g_thr_store.p;
             } else {
                 ctx->g_edges_store.ensure_scratch(m ? m : 1);
@@ -515,7 +526,7 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
         ctx->g.n = n;
         ctx->g.m = m;
         if (compact) {
-            ctx->graph_bytes = (uint64_t)n * (sizeof(NodeRec) + 8) + (uint64_t)m * 12;
+            ctx->graph_bytes = (uint64_t)n * (sizeof(NodeRec) + 16) + (uint64_t)m * 12;
         } else {
             ctx->graph_bytes = (uint64_t)n * sizeof(NodeRec) + (uint64_t)m * sizeof(EdgeRec);
             pin_node_records_in_l2(ctx);
@@ -538,8 +549,8 @@ int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of) {
                                                                                ctx->g.nodes);
             ++ctx->launches;
             if (ctx->g.layout == kLayoutCompact) {
-                update_hdr_suspect_flags<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, d_p,
-                                                                                   ctx->g.hdr);
+                update_hdr_suspect_flags<<<(n + 255) / 256, 256, 0, ctx->stream>>>(
+                    n, d_p, ctx->g.hdr);
                 ++ctx->launches;
             } else if (ctx->g.m) {
                 update_edge_suspect_flags<<<(ctx->g.m + 255) / 256, 256, 0, ctx->stream>>>(

@@ -25,7 +25,7 @@ constexpr int kDefaultRecordBlocksPerSM = 4;  // recording: 4 x 32 KB staging, m
 struct EncodeParams {
     const NodeRec* nodes;
     const EdgeRec* edges;
-    const uint2* hdr;      // compact layout (DeviceGraph)
+    const uint4* hdr;      // compact layout (DeviceGraph)
     const uint32_t* src;
     const uint64_t* thr;
     uint32_t n;
@@ -44,6 +44,7 @@ struct EncodeParams {
     uint32_t arena_cap;      // pairs
     uint32_t* arena_cursor;  // next free chunk (pairs)
     uint32_t* out_log;       // per (batch, seq) slot: first pair of the walk, or kLogOverflow
+    uint32_t debug;          // TEMP A/B: bit0 skip log STG, bit1 skip staging, bit2 skip slot writes
 };
 
 constexpr uint32_t kLogChunk = 4096;    // pairs per chunk (32 KB)
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                     else if (pick_arith(hw, k, slot_in_row))
                         live = true;
                     else  // draw inside the row's margin, or not an arithmetic row: exact path
-                        live = pick_exact(nodes, p.thr, cur, k, lo, true_deg, slot_in_row);
+                        live = pick_exact(nodes, p.thr, cur, k, true_deg, slot_in_row);
                     if (STATS) st_bytes += pick_alg_bytes(true_deg, live);
                     if (live) u = load_src(p.src, (uint64_t)lo + slot_in_row);
                 } else {
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             bool accepted = false;
             if (LAYOUT == kLayoutCompact) {
                 // 8-byte row header of u; the node record is only read for suspects
-                const uint2 h = load_hdr(p.hdr, u);
+                const uint4 h = load_hdr(p.hdr, u);
                 rec.lo = h.x;
                 rec.deg = hdr_deg(h.y);
                 new_hw = h.y;
@@ -390,11 +391,216 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                   (unsigned long long)w_pairs);
 }
 
+// ---- K1, production variant ----------------------------------------------------------------------
+// The default sampler configuration (Brent + window 2, recording) on the compact layout. Same
+// stream, same outputs as encode_kernel; organised around the measured limits of the generic
+// kernel once the graph is L2 resident (profiles/README.md): instruction issue, and memory waits
+// taken by a single lane while the rest of the warp idles.
+//  * one draw per iteration for every lane, hoisted out of the start / step branches;
+//  * per step two dependent L2 gathers (in_src[e], then the 16-byte header of the source) and
+//    nothing else: suspects are settled from the 32-bit acceptance code in the header, the node
+//    record is read only for the 2^-32 ambiguous draws;
+//  * the pair log is staged per thread in shared memory (rotated so that the per-step stores of a
+//    warp and the line read-back are both conflict free) and full 128-byte lines are written out
+//    by the whole warp at the end of the iteration instead of 45 instructions run by one lane.
+constexpr int kFastBlocksPerSM = 5;
+
+// STAGE: pairs staged per thread (one line of STAGE * 8 bytes per write-out).
+template <int MINB, int STAGE>
+__global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodeParams p) {
+    __shared__ uint2 stage[kThreads * STAGE];  // [thread][(pos + lane) % STAGE]
+    __shared__ uint64_t snap[kThreads];         // Seed_h of the running attempt
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp0 = tid & ~31u;
+    const NodeRec* __restrict__ nodes = p.nodes;
+
+    uint64_t s = 0;
+    uint32_t bidx = 0, att = 0, cnt = 0;
+    uint32_t lo = 0, hw = 0;                   // row start and header word of the current node
+    uint32_t r0 = kInvalidNode, r1 = kInvalidNode;  // window(2): r0 is the current node
+    uint32_t b_anchor = kInvalidNode, b_power = 1, b_lam = 0;
+    uint32_t nedges = 0;
+    uint32_t lpos = 0, lend = 0, astart = 0;
+    bool have = false, fresh = true, drained = false, rec_ok = false, arena_dead = false;
+
+    for (;;) {
+        if (!drained) {
+            uint64_t mine = 0;
+            if (claim(p.cursor, p.nbatches, !have, lane, mine, drained)) {
+                bidx = (uint32_t)mine;
+                s = seed_from_worker(p.first_worker + mine);  // sampler.cpp:272
+#pragma unroll
+                for (int i = 0; i < 8; ++i) (void)prg_next(s);  // burn-in, sampler.cpp:273
+                att = 0;
+                cnt = 0;
+                fresh = true;
+                have = true;
+            }
+        }
+        if (!__any_sync(kFullMask, have)) break;
+
+        uint32_t flush_n = 0, flush_base = 0;  // pairs of a staged line to write out below
+        bool arrive = false;
+        uint32_t u = 0, edge = kInvalidNode;
+        if (have) {
+            const uint64_t s_before = s;
+            const uint64_t k = draw53(s);  // start draw or pick draw
+            if (fresh) {
+                snap[tid] = s_before;     // Seed_h, sampler.cpp:155,277
+                u = start_node(k, p.n);  // sampler.cpp:24
+                nedges = 0;
+                lpos = (lpos + STAGE - 1) & ~(STAGE - 1);  // walks start on a 128-byte line
+                if (lend - lpos < kLogReserve && !arena_dead) {
+                    uint32_t base = atomicAdd(p.arena_cursor, kLogChunk);
+                    if (base <= p.arena_cap - kLogChunk) {
+                        lpos = base;
+                        lend = base + kLogChunk;
+                    } else {
+                        arena_dead = true;  // arena exhausted: remaining walks are replayed
+                        lpos = lend = 0;
+                    }
+                }
+                astart = lpos;
+                rec_ok = lend - lpos >= kLogReserve;
+                arrive = true;
+            } else if (nedges >= p.n) {
+                s = s_before;  // len_cap = g.n stops before drawing, sampler.cpp:43,281
+            } else {
+                // rows with deg == 0 never get here: they are settled on arrival (below)
+                uint32_t slot = 0;
+                bool live = pick_arith(hw, k, slot);
+                if (!live) {  // draw inside the row's margin, or not an arithmetic row
+                    const int64_t ex = pick_exact_slot(nodes, p.thr, r0, k);
+                    live = ex >= 0;
+                    slot = (uint32_t)ex;
+                }
+                if (live) {
+                    u = load_src(p.src, (uint64_t)lo + slot);
+                    bool cyc = (u == r0) | (u == r1);  // sampler.cpp:180
+                    if (!cyc) {                        // BrentState::check, sampler.cpp:100-108
+                        if (u == b_anchor) {
+                            cyc = true;
+                        } else if (++b_lam == b_power) {
+                            b_anchor = u;
+                            b_power <<= 1;
+                            b_lam = 0;
+                        }
+                    }
+                    if (!cyc) {
+                        ++nedges;  // resolve(), sampler.cpp:54
+                        edge = lo + slot;
+                        arrive = true;
+                    }
+                }
+            }
+        }
+        __syncwarp();  // starting and stepping lanes arrive together: one header read per iteration
+
+        bool done = true;
+        if (arrive) {
+            const uint4 h = load_hdr(p.hdr, u);
+            const uint32_t a32 = h.z;
+            if (rec_ok && !(p.debug & 2)) {
+                if (lpos == lend) {  // the walk outgrew its chunk: it will be replayed
+                    rec_ok = false;
+                } else {
+                    stage[tid * STAGE + ((lpos + lane) & (STAGE - 1))] = make_uint2(u, edge);
+                    ++lpos;
+                    if ((lpos & (STAGE - 1)) == 0) {
+                        flush_n = STAGE;
+                        flush_base = lpos - STAGE;
+                    }
+                }
+            }
+            bool accepted = false;
+            if (a32 != 0) {  // is_suspect, sampler.cpp:32,55
+                const uint64_t k2 = draw53(s);
+                const uint32_t k2h = (uint32_t)(k2 >> 21);
+                if (a32 != 0xFFFFFFFFu && k2h != a32 - 1)
+                    accepted = k2h < a32 - 1;
+                else  // r <= p_of[u] against the exact threshold, sampler.cpp:34,57
+                    accepted = k2 < load_node(nodes, u).acc_thr;
+            }
+            if (accepted) {
+                const uint64_t out = (uint64_t)bidx * p.l + cnt;  // seq, sampler.cpp:283
+                if (!(p.debug & 4)) {
+                p.out_seed[out] = snap[tid];
+                p.out_len[out] = nedges;
+                }
+                if (rec_ok && !(p.debug & 4)) {
+                    if (lpos & (STAGE - 1)) {  // last, partially filled line: whole sectors
+                        flush_n = ((lpos & (STAGE - 1)) + 3) & ~3u;
+                        flush_base = lpos & ~(STAGE - 1);
+                    }
+                    p.out_log[out] = astart;
+                    astart = lpos;  // keep the walk: later rewinds stop here
+                } else {
+                    p.out_log[out] = kLogOverflow;
+                }
+                ++cnt;
+            } else {
+                lo = h.x;
+                hw = h.y;
+                if (fresh) {  // win.reset / brent.reset, sampler.cpp:166-169
+                    r1 = kInvalidNode;
+                    b_anchor = u;
+                    b_power = 1;
+                    b_lam = 0;
+                } else {
+                    r1 = r0;  // win.push, sampler.cpp:200
+                }
+                r0 = u;
+                done = false;
+                if (hdr_deg(hw) == 0) {
+                    // the next pick fails after exactly one draw (empty row) unless the
+                    // length cap stops it before drawing: settle it now
+                    if (nedges < p.n) (void)prg_next(s);
+                    done = true;
+                }
+            }
+        }
+        if (have) {
+            if (done) {
+                fresh = true;
+                lpos = astart;  // failed attempt: reuse its log space (no-op after an accept)
+                if (++att == p.l) {
+                    p.out_count[bidx] = cnt;
+                    have = false;
+                }
+            } else {
+                fresh = false;
+            }
+        }
+
+        // warp-cooperative write-out of the staged lines that filled up in this iteration: every
+        // group of STAGE lanes takes one pending lane per trip and stores its line as one request
+        unsigned fm = __ballot_sync(kFullMask, flush_n != 0);
+        while (fm) {
+            int mine = -1;
+#pragma unroll
+            for (uint32_t g = 0; g < 32 / STAGE; ++g) {
+                const int l = fm ? __ffs(fm) - 1 : -1;
+                fm &= fm - 1;
+                if (lane / STAGE == g) mine = l;
+            }
+            const int src_lane = mine < 0 ? 0 : mine;
+            const uint32_t base = __shfl_sync(kFullMask, flush_base, src_lane);
+            const uint32_t npairs = __shfl_sync(kFullMask, flush_n, src_lane);
+            const uint32_t j = lane % STAGE;
+            if (mine >= 0 && j < npairs && !(p.debug & 1)) {
+                const uint2 pr = stage[(warp0 + src_lane) * STAGE + ((j + src_lane) & (STAGE - 1))];
+                asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p.arena + base + j),
+                             "r"(pr.x), "r"(pr.y));
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // ---- K2 ----------------------------------------------------------------------------------------
 struct DecodeParams {
     const NodeRec* nodes;
     const EdgeRec* edges;
-    const uint2* hdr;  // compact layout (DeviceGraph)
+    const uint4* hdr;  // compact layout (DeviceGraph)
     const uint32_t* src;
     const uint64_t* thr;
     uint32_t n;
@@ -481,7 +687,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
                     else if (pick_arith(hw, k, slot))
                         live = true;
                     else
-                        live = pick_exact(nodes, p.thr, cur, k, lo, true_deg, slot);
+                        live = pick_exact(nodes, p.thr, cur, k, true_deg, slot);
                     if (live) u = load_src(p.src, (uint64_t)lo + slot);
                 } else {
                     live = deg != 0 && k < tot;
@@ -511,7 +717,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
             uint32_t new_hw = 0;
             bool hit = false;
             if (LAYOUT == kLayoutCompact) {
-                const uint2 h = load_hdr(p.hdr, u);
+                const uint4 h = load_hdr(p.hdr, u);
                 rec.lo = h.x;
                 rec.deg = hdr_deg(h.y);
                 new_hw = h.y;
@@ -723,9 +929,10 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
                    bool with_stats) {
     if (nbatches == 0) return;
     if (nbatches > 0xFFFFFFFFull) fail(HSAW_EINVAL, "encode: more than 2^32 batches per launch");
-    EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, ctx->g.src, ctx->g.thr, ctx->g.n,
-                   cfg.batch_size, cfg.window, first_worker, nbatches, d_seed, d_len, d_count,
-                   d_stats, d_cursor, nullptr, 0, nullptr, nullptr};
+    EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, ctx->g.src, ctx->g.thr,
+                   ctx->g.n, cfg.batch_size, cfg.window, first_worker, nbatches, d_seed, d_len, d_count,
+                   d_stats, d_cursor, nullptr, 0, nullptr, nullptr, 0};
+    if (const char* env = std::getenv("HSAW_K1_DEBUG")) p.debug = (uint32_t)std::atoi(env);
     const bool compact = ctx->g.layout == kLayoutCompact;
 // one instantiation per graph layout
 #define HSAW_GO(H, W, B, R, S)                                                   \
@@ -751,7 +958,41 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
         check_launch(ctx, "encode_kernel");
     };
     const bool brent = cfg.heuristic == 0;
-    if (cfg.window == 2 && brent) {
+    static const bool fast_off = [] {  // A/B knob: HSAW_K1_GENERIC=1 keeps the generic kernel
+        const char* env = std::getenv("HSAW_K1_GENERIC");
+        return env && std::atoi(env) != 0;
+    }();
+    if (cfg.window == 2 && brent && compact && rec && !with_stats && !fast_off) {
+        // Resident blocks per SM are capped explicitly and the shared-memory carve-out is sized
+        // for exactly that many blocks: what is left of the 228 KB stays L1, which serves the
+        // hub rows (HSAW_K1_FAST_BLOCKS: A/B knob).
+        static const int fast_blocks = [] {
+            const char* env = std::getenv("HSAW_K1_FAST_BLOCKS");
+            int b = env ? std::atoi(env) : kFastBlocksPerSM;
+            return b < 1 ? 1 : (b > 6 ? 6 : b);
+        }();
+        static const int fast_stage = [] {  // A/B knob: pairs staged per thread (8 or 16)
+            const char* env = std::getenv("HSAW_K1_FAST_STAGE");
+            return env && std::atoi(env) == 16 ? 16 : 8;
+        }();
+        auto run = [&](auto kernel) {
+            cudaFuncAttributes fa{};
+            HSAW_CUDA_CHECK(cudaFuncGetAttributes(&fa, kernel));
+            const int smem_kb = (int)((fa.sharedSizeBytes + 1024 + 1023) / 1024) * fast_blocks;
+            int carve = (smem_kb * 100 + 227) / 228;
+            HSAW_CUDA_CHECK(cudaFuncSetAttribute(
+                kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve > 100 ? 100 : carve));
+            int blocks = persistent_blocks(ctx, kernel, nbatches);
+            blocks = std::min(blocks, fast_blocks * ctx->sm_count);
+            StageScope timer(ctx, HSAW_STAGE_ENCODE);
+            kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+            check_launch(ctx, "encode_compact_kernel");
+        };
+        if (fast_stage == 16)
+            run(encode_compact_kernel<4, 16>);
+        else
+            run(encode_compact_kernel<4, 8>);
+    } else if (cfg.window == 2 && brent) {
         // The default configuration gets the tuned variants: resident blocks per SM (register
         // budget), recording mode and instrumentation are compile-time parameters.
         static const int occ_env = [] {
@@ -800,8 +1041,9 @@ uint32_t record_overflow_marker() { return kLogOverflow; }
 
 // Lanes of one resident wave of the default recording kernel (each may hold one open chunk).
 uint64_t record_resident_lanes(hsaw_gpu_ctx* ctx) {
-    return (uint64_t)persistent_blocks(ctx, encode_kernel<0, 2, 4, 2, false, kLayoutFat>,
-                                       ~0ull >> 8) * kThreads;
+    int a = persistent_blocks(ctx, encode_kernel<0, 2, 4, 2, false, kLayoutFat>, ~0ull >> 8);
+    int b = 6 * ctx->sm_count;  // upper bound of encode_compact_kernel's resident blocks
+    return (uint64_t)std::max(a, b) * kThreads;
 }
 
 static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,

@@ -137,9 +137,12 @@ __device__ __forceinline__ uint32_t hdr_deg(uint32_t w) { return w & kHdrDegMask
 __device__ __forceinline__ uint32_t hdr_mb(uint32_t w) { return (w >> kHdrDegBits) & 63u; }
 __device__ __forceinline__ bool hdr_suspect(uint32_t w) { return (w >> 31) != 0; }
 
-__device__ __forceinline__ uint2 load_hdr(const uint2* __restrict__ hdr, uint32_t v) {
-    uint2 h;
-    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(h.x), "=r"(h.y) : "l"(hdr + v));
+// (lo, w, acceptance code, 0): one 16-byte gather per arrival
+__device__ __forceinline__ uint4 load_hdr(const uint4* __restrict__ hdr, uint32_t v) {
+    uint4 h;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(h.x), "=r"(h.y), "=r"(h.z), "=r"(h.w)
+                 : "l"(hdr + v));
     return h;
 }
 
@@ -164,14 +167,13 @@ __device__ __forceinline__ bool pick_arith(uint32_t w, uint64_t k, uint32_t& slo
 }
 
 // Exact path of the compact layout: pick_live_in_edge (graph.hpp:61-80) from the node record and
-// the threshold array. Returns false for "no edge"; else lo/slot of the first i with k < thr.
-__device__ __noinline__ bool pick_exact(const NodeRec* __restrict__ nodes,
-                                        const uint64_t* __restrict__ thr, uint32_t v, uint64_t k,
-                                        uint32_t& lo, uint32_t& deg, uint32_t& slot) {
+// the threshold array. Returns -1 for "no edge", else the first slot i with k < thr[lo + i].
+// Everything is passed and returned by value so that callers keep their walk state in registers.
+__device__ __noinline__ int64_t pick_exact_slot(const NodeRec* __restrict__ nodes,
+                                                const uint64_t* __restrict__ thr, uint32_t v,
+                                                uint64_t k) {
     NodeRec r = load_node(nodes, v);
-    lo = r.lo;
-    deg = r.deg;
-    if (r.deg == 0 || k >= r.tot_thr) return false;
+    if (r.deg == 0 || k >= r.tot_thr) return -1;
     uint32_t a = 0, b = r.deg - 1;  // answer in [a, b]; k < thr[b] holds (thr[deg-1] == tot_thr)
     while (a < b) {
         uint32_t mid = a + (b - a) / 2;
@@ -180,7 +182,17 @@ __device__ __noinline__ bool pick_exact(const NodeRec* __restrict__ nodes,
         else
             a = mid + 1;
     }
-    slot = a;
+    return (int64_t)a;
+}
+
+// Same, also reporting the row's true degree (the header field saturates at 2^25 - 1).
+__device__ __forceinline__ bool pick_exact(const NodeRec* __restrict__ nodes,
+                                           const uint64_t* __restrict__ thr, uint32_t v, uint64_t k,
+                                           uint32_t& deg, uint32_t& slot) {
+    int64_t r = pick_exact_slot(nodes, thr, v, k);
+    deg = load_node(nodes, v).deg;
+    if (r < 0) return false;
+    slot = (uint32_t)r;
     return true;
 }
 
