@@ -4,8 +4,11 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 
@@ -190,6 +193,136 @@ __global__ void update_edge_suspect_flags(uint32_t m, const double* __restrict__
     edges[e].flags = f;
 }
 
+// ---- per-device facts, queried once (cudaGetDeviceProperties costs milliseconds) -----------------
+struct DeviceInfo {
+    int sm_count = 0, l2_bytes = 0;
+    size_t max_persist = 0, max_window = 0;
+};
+const DeviceInfo& device_info(int device) {
+    static std::mutex mu;
+    static std::map<int, DeviceInfo> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(device);
+    if (it != cache.end()) return it->second;
+    DeviceInfo d;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess) d.sm_count = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device) == cudaSuccess) d.l2_bytes = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess)
+        d.max_persist = (size_t)v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, device) == cudaSuccess)
+        d.max_window = (size_t)v;
+    cudaGetLastError();
+    // keep freed pool memory cached instead of returning it to the driver at every sync
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t never = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &never);
+    }
+    cudaGetLastError();
+    return cache.emplace(device, d).first->second;
+}
+
+// ---- host -> device copies of pageable arrays ---------------------------------------------------
+// The reference hands over plain std::vector storage. A single cudaMemcpy from pageable memory
+// runs at ~10 GB/s (one driver thread staging through pinned buffers); here a few host threads
+// stage 4 MB chunks into a process-wide ring of pinned buffers and issue the DMA themselves, so
+// the copy runs at host-memory speed. The consumer stream waits on the copiers' last events.
+class StagedCopier {
+public:
+    struct Job {
+        void* dst;
+        const void* src;
+        size_t bytes;
+    };
+    static constexpr size_t kChunk = 4u << 20;
+    static constexpr int kMaxThreads = 6, kSlotsPerThread = 2;
+
+    // Copies all jobs; returns false (nothing copied) when the ring cannot be set up.
+    static bool run(int device, cudaStream_t consumer, const std::vector<Job>& jobs) {
+        static std::mutex mu;  // one staged copy at a time per process
+        std::lock_guard<std::mutex> lock(mu);
+        State& st = state(device);
+        if (!st.ok) return false;
+        struct Piece {
+            char* dst;
+            const char* src;
+            size_t bytes;
+        };
+        std::vector<Piece> pieces;
+        for (const Job& j : jobs)
+            for (size_t o = 0; o < j.bytes; o += kChunk)
+                pieces.push_back({(char*)j.dst + o, (const char*)j.src + o,
+                                  std::min(kChunk, j.bytes - o)});
+        if (pieces.empty()) return true;
+        const int nthreads = (int)std::min<size_t>(st.nthreads, pieces.size());
+        // the copies must not overtake earlier work on the consumer stream that uses the targets
+        cudaEventRecord(st.gate, consumer);
+        std::vector<cudaError_t> errs(nthreads, cudaSuccess);
+        auto work = [&](int t) {
+            cudaSetDevice(device);
+            cudaStream_t s = st.streams[t];
+            cudaStreamWaitEvent(s, st.gate, 0);
+            int turn = 0;
+            for (size_t i = t; i < pieces.size(); i += nthreads, ++turn) {
+                const int slot = t * kSlotsPerThread + (turn % kSlotsPerThread);
+                if (turn >= kSlotsPerThread) cudaEventSynchronize(st.slot_done[slot]);
+                std::memcpy(st.pinned[slot], pieces[i].src, pieces[i].bytes);
+                cudaError_t e = cudaMemcpyAsync(pieces[i].dst, st.pinned[slot], pieces[i].bytes,
+                                                cudaMemcpyHostToDevice, s);
+                if (e != cudaSuccess) errs[t] = e;
+                cudaEventRecord(st.slot_done[slot], s);
+            }
+            cudaEventRecord(st.thread_done[t], s);
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nthreads; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool) th.join();
+        for (int t = 0; t < nthreads; ++t) {
+            cudaStreamWaitEvent(consumer, st.thread_done[t], 0);
+            if (errs[t] != cudaSuccess) HSAW_CUDA_CHECK(errs[t]);
+        }
+        // the pinned ring is reused by the next call: its DMA reads must have finished by then
+        for (int t = 0; t < nthreads; ++t) cudaEventSynchronize(st.thread_done[t]);
+        return true;
+    }
+
+private:
+    struct State {
+        bool ok = false;
+        int nthreads = 0;
+        void* pinned[kMaxThreads * kSlotsPerThread] = {};
+        cudaEvent_t slot_done[kMaxThreads * kSlotsPerThread] = {};
+        cudaEvent_t thread_done[kMaxThreads] = {};
+        cudaStream_t streams[kMaxThreads] = {};
+        cudaEvent_t gate = nullptr;
+    };
+    static State& state(int device) {
+        static std::map<int, State> per_device;
+        State& st = per_device[device];
+        if (st.nthreads) return st;
+        int want = 4;
+        if (const char* env = std::getenv("HSAW_UPLOAD_THREADS")) want = std::atoi(env);
+        unsigned hw = std::thread::hardware_concurrency();
+        if (hw && (unsigned)want > hw) want = (int)hw;
+        st.nthreads = std::max(1, std::min(want, kMaxThreads));
+        bool ok = want > 0;
+        for (int i = 0; ok && i < st.nthreads * kSlotsPerThread; ++i) {
+            ok = cudaHostAlloc(&st.pinned[i], kChunk, cudaHostAllocDefault) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&st.slot_done[i], cudaEventDisableTiming) == cudaSuccess;
+        }
+        for (int t = 0; ok && t < st.nthreads; ++t) {
+            ok = cudaStreamCreateWithFlags(&st.streams[t], cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&st.thread_done[t], cudaEventDisableTiming) == cudaSuccess;
+        }
+        if (ok) ok = cudaEventCreateWithFlags(&st.gate, cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) cudaGetLastError();
+        st.ok = ok;
+        return st;
+    }
+};
+
 // Every walk step reads one node record and one edge record. The node records are the smaller,
 // reused half (32 n bytes: 32 MB at 1 M nodes, hubs are hot at any size), so they get the
 // persisting share of the 126 MB L2 through an access-policy window on the context stream, while
@@ -197,10 +330,9 @@ __global__ void update_edge_suspect_flags(uint32_t m, const double* __restrict__
 void pin_node_records_in_l2(hsaw_gpu_ctx* ctx) {
     if (const char* env = std::getenv("HSAW_L2_PERSIST"))
         if (std::atoi(env) == 0) return;
-    cudaDeviceProp prop{};
-    if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) return;
-    size_t max_persist = (size_t)prop.persistingL2CacheMaxSize;
-    size_t max_window = (size_t)prop.accessPolicyMaxWindowSize;
+    const DeviceInfo& di = device_info(ctx->device);
+    size_t max_persist = di.max_persist;
+    size_t max_window = di.max_window;
     if (max_persist == 0 || max_window == 0) return;
     size_t bytes = (size_t)ctx->g.n * sizeof(NodeRec);
     size_t carve = std::min(bytes, max_persist);
@@ -227,12 +359,8 @@ int choose_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
         if (env[0] == 'c') return kLayoutCompact;
         if (env[0] == 'f') return kLayoutFat;
     }
-    int l2 = 0;
-    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device) != cudaSuccess) {
-        cudaGetLastError();
-        l2 = 0;
-    }
-    return 4ull * m + 16ull * n <= (uint64_t)l2 ? kLayoutCompact : kLayoutFat;
+    const uint64_t l2 = (uint64_t)device_info(ctx->device).l2_bytes;
+    return 4ull * m + 16ull * n <= l2 ? kLayoutCompact : kLayoutFat;
 }
 
 void free_graph(hsaw_gpu_ctx* ctx) {  // the backing stores keep their capacity for the next upload
@@ -265,6 +393,8 @@ void adopt_parked_buffers(hsaw_gpu_ctx* ctx) {
     if (it == pk.by_device.end()) return;
     ctx->swap_buffers(*it->second);
     ctx->for_each_buffer([&](auto& v) { v.owner = ctx->stream; });
+    std::swap(ctx->d_scalars, it->second->d_scalars);  // scalar scratch (device + pinned mirror)
+    std::swap(ctx->h_scalars, it->second->h_scalars);
 }
 
 void park_buffers(hsaw_gpu_ctx* ctx) {
@@ -279,6 +409,8 @@ void park_buffers(hsaw_gpu_ctx* ctx) {
     });
     slot->swap_buffers(*ctx);
     slot->for_each_buffer([](auto& v) { v.owner = nullptr; });
+    if (!slot->d_scalars) std::swap(slot->d_scalars, ctx->d_scalars);
+    if (!slot->h_scalars) std::swap(slot->h_scalars, ctx->h_scalars);
 }
 
 }  // namespace
@@ -345,9 +477,8 @@ int hsaw_gpu_ctx_create(int device, void* cuda_stream, hsaw_gpu_ctx** out) {
     auto* ctx = new hsaw_gpu_ctx;
     ctx->device = device;
     int rc = guarded(ctx, [&] {
-        cudaDeviceProp prop{};
-        HSAW_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
-        ctx->sm_count = prop.multiProcessorCount;
+        ctx->sm_count = device_info(device).sm_count;
+        if (ctx->sm_count <= 0) fail(HSAW_ECUDA, "cannot query the device");
         if (cuda_stream) {
             ctx->stream = static_cast<cudaStream_t>(cuda_stream);
         } else {
@@ -355,20 +486,9 @@ int hsaw_gpu_ctx_create(int device, void* cuda_stream, hsaw_gpu_ctx** out) {
             ctx->own_stream = true;
         }
         adopt_parked_buffers(ctx);
-        HSAW_CUDA_CHECK(cudaMalloc(&ctx->d_scalars, 64 * sizeof(uint64_t)));
-        HSAW_CUDA_CHECK(cudaMallocHost(&ctx->h_scalars, 64 * sizeof(uint64_t)));
-        // keep freed pool memory cached instead of returning it to the driver at every sync
-        cudaMemPool_t pool = nullptr;
-        HSAW_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
-        uint64_t never = ~0ull;
-        HSAW_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &never));
-        // Random 16/32-byte record reads: ask L2 to fetch single 32-byte sectors from HBM rather
-        // than the default 64 bytes (HSAW_L2_FETCH=32|64|128 overrides, for A/B measurements).
-        size_t fetch = 32;
-        if (const char* env = std::getenv("HSAW_L2_FETCH")) fetch = (size_t)std::atoi(env);
-        if (fetch == 32 || fetch == 64 || fetch == 128)
-            cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, fetch);
-        cudaGetLastError();
+        if (!ctx->d_scalars) HSAW_CUDA_CHECK(cudaMalloc(&ctx->d_scalars, 64 * sizeof(uint64_t)));
+        if (!ctx->h_scalars)
+            HSAW_CUDA_CHECK(cudaMallocHost(&ctx->h_scalars, 64 * sizeof(uint64_t)));
     });
     if (rc != HSAW_OK) {
         hsaw_gpu_ctx_destroy(ctx);
@@ -385,10 +505,9 @@ void hsaw_gpu_ctx_destroy(hsaw_gpu_ctx* ctx) {
     collect_timings(ctx);
     for (cudaEvent_t e : ctx->free_events) cudaEventDestroy(e);
     free_graph(ctx);
+    park_buffers(ctx);       // keep the device buffers for the next context on this device
     if (ctx->d_scalars) cudaFree(ctx->d_scalars);
     if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    park_buffers(ctx);       // keep the device buffers for the next context on this device
     ctx->release_scratch();  // (now empty) stream-ordered frees precede the stream's destruction
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -479,15 +598,21 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_cum, (uint64_t)(m ? m : 1) * 8, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_bad, 8, st));
-            HSAW_CUDA_CHECK(cudaMemcpyAsync(d_off, in_offsets, ((uint64_t)n + 1) * 8,
-                                            cudaMemcpyHostToDevice, st));
+            std::vector<StagedCopier::Job> jobs;
+            jobs.push_back({d_off, in_offsets, ((uint64_t)n + 1) * 8});
             if (m) {
-                HSAW_CUDA_CHECK(cudaMemcpyAsync(compact ? ctx->g.src : d_src, in_src,
-                                                (uint64_t)m * 4, cudaMemcpyHostToDevice, st));
-                HSAW_CUDA_CHECK(
-                    cudaMemcpyAsync(d_cum, in_cum, (uint64_t)m * 8, cudaMemcpyHostToDevice, st));
+                jobs.push_back({compact ? ctx->g.src : d_src, in_src, (uint64_t)m * 4});
+                jobs.push_back({d_cum, in_cum, (uint64_t)m * 8});
             }
-            HSAW_CUDA_CHECK(cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, st));
+            jobs.push_back({d_p, p_of, (uint64_t)n * 8});
+            uint64_t total_bytes = 0;
+            for (const auto& j : jobs) total_bytes += j.bytes;
+            // large uploads: multi-threaded staging through pinned memory; small ones (and the
+            // fallback when the ring cannot be set up) go through plain pageable copies
+            if (total_bytes < (16u << 20) || !StagedCopier::run(ctx->device, st, jobs))
+                for (const auto& j : jobs)
+                    HSAW_CUDA_CHECK(
+                        cudaMemcpyAsync(j.dst, j.src, j.bytes, cudaMemcpyHostToDevice, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_bad, 0xFF, 8, st));
             {
                 StageScope timer(ctx, HSAW_STAGE_UPLOAD);

@@ -44,7 +44,6 @@ struct EncodeParams {
     uint32_t arena_cap;      // pairs
     uint32_t* arena_cursor;  // next free chunk (pairs)
     uint32_t* out_log;       // per (batch, seq) slot: first pair of the walk, or kLogOverflow
-    uint32_t debug;          // TEMP A/B: bit0 skip log STG, bit1 skip staging, bit2 skip slot writes
 };
 
 constexpr uint32_t kLogChunk = 4096;    // pairs per chunk (32 KB)
@@ -499,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodePa
         if (arrive) {
             const uint4 h = load_hdr(p.hdr, u);
             const uint32_t a32 = h.z;
-            if (rec_ok && !(p.debug & 2)) {
+            if (rec_ok) {
                 if (lpos == lend) {  // the walk outgrew its chunk: it will be replayed
                     rec_ok = false;
                 } else {
@@ -522,11 +521,9 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodePa
             }
             if (accepted) {
                 const uint64_t out = (uint64_t)bidx * p.l + cnt;  // seq, sampler.cpp:283
-                if (!(p.debug & 4)) {
                 p.out_seed[out] = snap[tid];
                 p.out_len[out] = nedges;
-                }
-                if (rec_ok && !(p.debug & 4)) {
+                if (rec_ok) {
                     if (lpos & (STAGE - 1)) {  // last, partially filled line: whole sectors
                         flush_n = ((lpos & (STAGE - 1)) + 3) & ~3u;
                         flush_base = lpos & ~(STAGE - 1);
@@ -586,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodePa
             const uint32_t base = __shfl_sync(kFullMask, flush_base, src_lane);
             const uint32_t npairs = __shfl_sync(kFullMask, flush_n, src_lane);
             const uint32_t j = lane % STAGE;
-            if (mine >= 0 && j < npairs && !(p.debug & 1)) {
+            if (mine >= 0 && j < npairs) {
                 const uint2 pr = stage[(warp0 + src_lane) * STAGE + ((j + src_lane) & (STAGE - 1))];
                 asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p.arena + base + j),
                              "r"(pr.x), "r"(pr.y));
@@ -931,8 +928,7 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
     if (nbatches > 0xFFFFFFFFull) fail(HSAW_EINVAL, "encode: more than 2^32 batches per launch");
     EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, ctx->g.src, ctx->g.thr,
                    ctx->g.n, cfg.batch_size, cfg.window, first_worker, nbatches, d_seed, d_len, d_count,
-                   d_stats, d_cursor, nullptr, 0, nullptr, nullptr, 0};
-    if (const char* env = std::getenv("HSAW_K1_DEBUG")) p.debug = (uint32_t)std::atoi(env);
+                   d_stats, d_cursor, nullptr, 0, nullptr, nullptr};
     const bool compact = ctx->g.layout == kLayoutCompact;
 // one instantiation per graph layout
 #define HSAW_GO(H, W, B, R, S)                                                   \
@@ -971,9 +967,9 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
             int b = env ? std::atoi(env) : kFastBlocksPerSM;
             return b < 1 ? 1 : (b > 6 ? 6 : b);
         }();
-        static const int fast_stage = [] {  // A/B knob: pairs staged per thread (8 or 16)
+        static const int fast_stage = [] {  // A/B knob: pairs staged per thread (4, 8 or 16)
             const char* env = std::getenv("HSAW_K1_FAST_STAGE");
-            return env && std::atoi(env) == 16 ? 16 : 8;
+            return env ? std::atoi(env) : 8;
         }();
         auto run = [&](auto kernel) {
             cudaFuncAttributes fa{};
@@ -990,6 +986,8 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
         };
         if (fast_stage == 16)
             run(encode_compact_kernel<4, 16>);
+        else if (fast_stage == 4)
+            run(encode_compact_kernel<4, 4>);
         else
             run(encode_compact_kernel<4, 8>);
     } else if (cfg.window == 2 && brent) {

@@ -4,6 +4,7 @@
 // so prefixes of the pool are pure functions of (graph, suspects, seed) exactly as in the reference.
 #include "stream.cuh"
 
+#include <cmath>
 #include <cstdlib>
 
 #include "sampler.cuh"
@@ -598,9 +599,13 @@ int hsaw_gpu_stream_ensure(hsaw_gpu_stream* s, uint64_t min_accepted) {
                 batches = s->grow;
                 s->grow = std::min<uint64_t>(s->grow * 8, 1ull << 22);
             } else {
+                // expected batches for the remainder plus ~4 sigma of the accepted count (a
+                // shortfall only costs one more small round; the reference's 1.1 factor would
+                // over-sample every call by 10 %)
                 double rate = (double)s->accepted / (double)attempts_so_far;
                 double est = (double)need / (rate * (double)bs);
-                batches = (uint64_t)(est * 1.1) + 64;
+                double sigma = std::sqrt((double)need / rate) / (double)bs;
+                batches = (uint64_t)(est * 1.005 + 4.0 * sigma) + 16;
             }
             batches = std::max<uint64_t>(std::min(batches, max_batches), 1);
             sample_range(s, s->next_batch, batches);
