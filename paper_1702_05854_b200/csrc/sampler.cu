@@ -794,74 +794,112 @@ __device__ __forceinline__ uint32_t walk_node(const CheckParams& p, uint64_t w, 
     return p.nodes[base + i];
 }
 
-template <bool PAIRS, uint32_t TABLE, int WARPS>
+// Work is dealt in groups of 32 consecutive walks per warp: lane j reads the metadata of walk j of
+// the group (coalesced), the walks are then processed one by one with their metadata broadcast by
+// shuffles, and every lane has up to four node reads in flight before the first insert, so a walk
+// costs one exposed memory latency per 128 nodes instead of one per 32.
+// GROUP: walks dealt to a warp at a time (32 for the bulk pass; 1 for the short queues of long
+// walks, where 32 serial long walks per warp would leave most of the GPU idle).
+template <bool PAIRS, uint32_t TABLE, int WARPS, uint32_t GROUP>
 __global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
     extern __shared__ uint32_t tables[];  // WARPS x TABLE
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     uint32_t* tab = tables + wib * TABLE;
-    uint64_t warp = (uint64_t)blockIdx.x * WARPS + wib;
-    uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
+    const uint64_t warp = (uint64_t)blockIdx.x * WARPS + wib;
+    const uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
+    const uint64_t ngroups = (p.nwalks + GROUP - 1) / GROUP;
     uint32_t dropped = 0;
-    for (uint64_t item = warp; item < p.nwalks; item += nwarps) {
-        const uint64_t w = p.sel ? p.sel[item] : item;
-        uint8_t st = p.status[w];
-        if (st == 0) continue;
-        uint64_t base = PAIRS ? 0 : p.edge_off[w] + w;
-        uint32_t nn = PAIRS ? p.lens[w] + 1
-                            : (p.nnodes ? p.nnodes[w]
-                                        : (uint32_t)(p.edge_off[w + 1] - p.edge_off[w]) + 1);
-        bool dup = false;
-        if (nn <= 1) {
-            // a single node cannot repeat
-        } else if (nn <= 32) {
-            uint32_t v = lane < nn ? walk_node<PAIRS>(p, w, base, lane) : 0;
-            unsigned valid = nn == 32 ? kFullMask : ((1u << nn) - 1);
-            unsigned same = __match_any_sync(kFullMask, v) & valid & ~(1u << lane);
-            dup = __any_sync(kFullMask, lane < nn && same != 0);
-        } else if (nn <= TABLE / 2) {
-            uint32_t bits = 32 - __clz(2 * nn - 1);  // table of >= 2*nn slots
-            uint32_t size = 1u << bits;
-            for (uint32_t i = lane; i < size; i += 32) tab[i] = kInvalidNode;
-            __syncwarp();
-            bool mydup = false;
-            for (uint32_t i = lane; i < nn; i += 32) {
-                uint32_t v = walk_node<PAIRS>(p, w, base, i);
-                uint32_t h = node_hash(v, bits);
-                for (;;) {
-                    uint32_t old = atomicCAS(&tab[h], kInvalidNode, v);
-                    if (old == kInvalidNode) break;
-                    if (old == v) {
-                        mydup = true;
-                        break;
-                    }
-                    h = (h + 1) & (size - 1);
+    for (uint64_t grp = warp; grp < ngroups; grp += nwarps) {
+        const uint64_t item = grp * GROUP + lane;
+        uint64_t my_w = 0, my_src = 0;  // walk id; pair-log pointer or offset into p.nodes
+        uint32_t my_nn = 0;
+        uint8_t my_st = 0;
+        if (lane < GROUP && item < p.nwalks) {
+            my_w = p.sel ? p.sel[item] : item;
+            my_st = p.status[my_w];
+            if (my_st != 0) {
+                if (PAIRS) {
+                    my_nn = p.lens[my_w] + 1;
+                    my_src = reinterpret_cast<uint64_t>(p.pair_src[my_w]);
+                } else {
+                    my_nn = p.nnodes ? p.nnodes[my_w]
+                                     : (uint32_t)(p.edge_off[my_w + 1] - p.edge_off[my_w]) + 1;
+                    my_src = p.edge_off[my_w] + my_w;
                 }
             }
-            dup = __any_sync(kFullMask, mydup);
-            __syncwarp();
-        } else if (nn <= kSmemNodes) {  // too long for this pass's table: queue for the mid pass
-            if (lane == 0) {
-                uint32_t at = atomicAdd(p.long_count + 2, 1u);
-                if (at < p.mid_cap) p.mid_list[at] = (uint32_t)w;
-            }
-            continue;
-        } else {
-            if (lane == 0) {
-                uint32_t at = atomicAdd(p.long_count, 1u);
-                if (at < p.long_cap) {
-                    p.long_list[2 * at] = (uint32_t)w;
-                    p.long_list[2 * at + 1] = nn;
-                }
-            }
-            continue;
         }
-        if (dup) {
-            if (lane == 0) p.status[w] = 0;
-            if (st == 1) ++dropped;
+        unsigned todo = __ballot_sync(kFullMask, my_nn > 1);  // a single node cannot repeat
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t nn = __shfl_sync(kFullMask, my_nn, j);
+            const uint64_t srcv = __shfl_sync(kFullMask, my_src, j);
+            auto node_at = [&](uint32_t i) -> uint32_t {
+                if (PAIRS) return __ldg(&reinterpret_cast<const uint2*>(srcv)[i].x);
+                return __ldg(p.nodes + srcv + i);
+            };
+            bool dup = false;
+            if (nn <= 32) {
+                uint32_t v = lane < nn ? node_at(lane) : 0;
+                unsigned valid = nn == 32 ? kFullMask : ((1u << nn) - 1);
+                unsigned same = __match_any_sync(kFullMask, v) & valid & ~(1u << lane);
+                dup = __any_sync(kFullMask, lane < nn && same != 0);
+            } else if (nn <= TABLE / 2) {
+                const uint32_t bits = 32 - __clz(2 * nn - 1);  // table of >= 2*nn slots
+                const uint32_t size = 1u << bits;
+                bool mydup = false;
+                for (uint32_t c = 0; c < nn; c += 128) {
+                    uint32_t v[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t i = c + q * 32 + lane;
+                        v[q] = i < nn ? node_at(i) : kInvalidNode;
+                    }
+                    if (c == 0) {  // the clears overlap the reads in flight
+                        for (uint32_t i = lane; i < size; i += 32) tab[i] = kInvalidNode;
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (c + q * 32 + lane >= nn) continue;
+                        uint32_t h = node_hash(v[q], bits);
+                        for (;;) {
+                            uint32_t old = atomicCAS(&tab[h], kInvalidNode, v[q]);
+                            if (old == kInvalidNode) break;
+                            if (old == v[q]) {
+                                mydup = true;
+                                break;
+                            }
+                            h = (h + 1) & (size - 1);
+                        }
+                    }
+                }
+                dup = __any_sync(kFullMask, mydup);
+                __syncwarp();
+            } else {
+                const uint32_t w32 = (uint32_t)__shfl_sync(kFullMask, my_w, j);
+                if (lane == 0) {
+                    if (nn <= kSmemNodes) {  // too long for this pass's table: the mid pass
+                        uint32_t at = atomicAdd(p.long_count + 2, 1u);
+                        if (at < p.mid_cap) p.mid_list[at] = w32;
+                    } else {
+                        uint32_t at = atomicAdd(p.long_count, 1u);
+                        if (at < p.long_cap) {
+                            p.long_list[2 * at] = w32;
+                            p.long_list[2 * at + 1] = nn;
+                        }
+                    }
+                }
+                continue;
+            }
+            if (dup && (int)lane == j) {  // the lane that owns the walk's metadata records the verdict
+                p.status[my_w] = 0;
+                if (my_st == 1) ++dropped;
+            }
         }
     }
-    if (lane == 0 && dropped) atomicAdd(p.long_count + 1, dropped);
+    if (dropped) atomicAdd(p.long_count + 1, dropped);
 }
 
 // Long walks (> kSmemNodes nodes): one block per walk, hash set in global scratch.
@@ -1112,8 +1150,8 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     CheckParams p{nwalks,   d_edge_off,      d_nodes,  d_nnodes, d_pair_src,      d_lens,
                   d_status, ctx->chk_list.p, counters, long_cap, ctx->chk_mid.p, mid_cap,
                   nullptr};
-    auto main_kernel = distinct_kernel<PAIRS, kTableSize, kCheckWarps>;
-    auto mid_kernel = distinct_kernel<PAIRS, kMidTableSize, kMidWarps>;
+    auto main_kernel = distinct_kernel<PAIRS, kTableSize, kCheckWarps, 32>;
+    auto mid_kernel = distinct_kernel<PAIRS, kMidTableSize, kMidWarps, 1>;
     const int smem_main = kCheckWarps * kTableSize * 4, smem_mid = kMidWarps * kMidTableSize * 4;
     static bool attr_set = false;
     if (!attr_set) {
@@ -1123,7 +1161,7 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     }
     uint32_t* h = reinterpret_cast<uint32_t*>(ctx->h_scalars + 32);
     {
-        uint64_t want = (nwalks + kCheckWarps - 1) / kCheckWarps;
+        uint64_t want = ((nwalks + 31) / 32 + kCheckWarps - 1) / kCheckWarps;  // 32 walks per warp
         uint64_t full = (uint64_t)ctx->sm_count * 7;  // 32 KB of tables per block: 7 blocks / SM
         int blocks = (int)(want < full ? want : full);
         StageScope timer(ctx, HSAW_STAGE_DISTINCT);
