@@ -846,7 +846,10 @@ __global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
                 unsigned same = __match_any_sync(kFullMask, v) & valid & ~(1u << lane);
                 dup = __any_sync(kFullMask, lane < nn && same != 0);
             } else if (nn <= TABLE / 2) {
-                const uint32_t bits = 32 - __clz(2 * nn - 1);  // table of >= 2*nn slots
+                // table of >= 4*nn slots where the warp's share allows it, else >= 2*nn: lanes
+                // probe in lockstep, so the longest probe sequence of the 32 sets the pace
+                uint32_t bits = 32 - __clz(4 * nn - 1);
+                if ((1u << bits) > TABLE) --bits;
                 const uint32_t size = 1u << bits;
                 bool mydup = false;
                 for (uint32_t c = 0; c < nn; c += 128) {
