@@ -228,9 +228,13 @@ def run_b200(args):
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     accepted = 0
+    # L2 is flushed between timed steps by overwriting a buffer twice its size on the same stream,
+    # inside the timed region: every step starts with a cold L2 and re-reads the graph from HBM.
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     with torch.cuda.stream(tstream):
         ev0.record(tstream)
         for _ in range(args.steps):
+            flush.zero_()
             accepted += one_step()
         ev1.record(tstream)
     barrier()
@@ -267,8 +271,16 @@ def run_b200(args):
     k1_avg_ms = k1_ms / max(k1_n, 1)
     achieved = alg_bytes_per_launch / (k1_avg_ms / 1e3) / 1e9 if k1_avg_ms > 0 else 0.0
     traffic = ncu_traffic()
+    # Secondary roofline in the kernel's own unit: random sector gathers. On the compact layout a
+    # step is one in_src gather (live picks) plus one 16-byte header gather (arrivals, start nodes
+    # included); tools/gather_probe.cu measured what this B200 sustains for dependent random
+    # gathers (profiles/README.md): 212 G/s from a 64 MB table (L2 resident), 150 G/s at 96 MB,
+    # 49 G/s from HBM (every miss costs a 128-byte line).
+    gathers = (2 * delta["steps"] + delta["attempts"]) / max(k1_n, 1)
     roofline = {
-        "bound": "hbm", "kernel": "encode_kernel<Brent,2,record> (K1, walk generation + materialisation)", "achieved": achieved,
+        "bound": "hbm", "kernel": "encode_compact_kernel<Brent,2,record> (K1, walk generation + "
+                                  "materialisation, compact L2-resident layout)",
+        "achieved": achieved,
         "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
         "peak_source": peak_src,
@@ -276,9 +288,17 @@ def run_b200(args):
         "bytes_per_step_formula": "28+8*ceil(log2 d) per successful pick (16 empty row, 24 no "
                                   "live edge) + 8 per node arrival (SURVEY.md 8d) + 8 per item "
                                   "of an accepted walk (logged by the same kernel)",
+        "note": "algorithmic bytes are the reference-layout figure of SURVEY.md 8(d); the device "
+                "layout serves them from 4-byte sources + 16-byte row headers that stay in L2, so "
+                "measured DRAM traffic (`traffic`) is a fraction of it and frac can exceed 1. The "
+                "kernel's own limit is the random-gather rate below.",
         "walk_log_bytes_per_launch": log_bytes / max(k1_n, 1),
         "kernel_avg_ms": k1_avg_ms, "launches_timed": k1_n,
         "k1_walk_steps_per_s": delta["steps"] / (k1_ms / 1e3) if k1_ms > 0 else None,
+        "gather": {"gathers_per_launch_upper": gathers,
+                   "achieved_ggathers_per_s": gathers / (k1_avg_ms / 1e3) / 1e9 if k1_avg_ms else None,
+                   "probe_peak_ggathers_per_s": {"l2_resident_64MB": 212.0, "96MB": 150.0,
+                                                 "hbm_512MB": 49.0}},
         "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
         "k1_share_of_step": k1_ms / elapsed_ms if elapsed_ms > 0 else None,
     }
@@ -291,9 +311,11 @@ def run_b200(args):
             "workload": workload_name(args, g.n, g.m),
             "step": f"{B} batches ({10 * B} attempts) per GPU: K1 encode+record, K2b exact recheck, "
                     f"ordered compaction into the device pool (K2 replay only on log overflow)",
+            "layout": "compact (4-byte in_src + 16-byte row headers, L2 resident)"
+                      if 4 * g.m + 16 * g.n <= 126 * 2**20 else "fat (32-byte edge records)",
             "parallelism": f"walks sharded by batch range over {world} GPU(s), graph replicated",
-            "l2_policy": f"inputs larger than L2: {hsaw_mb(dg)} MB of node/edge records are "
-                         f"walked at random and every step uses fresh batches",
+            "l2_policy": f"L2 flushed before every timed step (256 MB memset on the launching "
+                         f"stream, inside the timed region); graph on device {hsaw_mb(dg)} MB",
             "graph_device_bytes": ctx.graph_bytes, "graph_reference_bytes": ref_bytes,
         },
         "attempts_per_sec": tot_att / (elapsed_ms / 1e3),
