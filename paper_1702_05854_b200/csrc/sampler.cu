@@ -1006,7 +1006,7 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
         static const int fast_blocks = [] {
             const char* env = std::getenv("HSAW_K1_FAST_BLOCKS");
             int b = env ? std::atoi(env) : kFastBlocksPerSM;
-            return b < 1 ? 1 : (b > 6 ? 6 : b);
+            return b < 1 ? 1 : (b > 8 ? 8 : b);
         }();
         static const int fast_stage = [] {  // A/B knob: pairs staged per thread (4, 8 or 16)
             const char* env = std::getenv("HSAW_K1_FAST_STAGE");
@@ -1029,6 +1029,8 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
             run(encode_compact_kernel<4, 16>);
         else if (fast_stage == 4)
             run(encode_compact_kernel<4, 4>);
+        else if (fast_blocks >= 6)
+            run(encode_compact_kernel<6, 8>);  // 40 registers
         else
             run(encode_compact_kernel<4, 8>);
     } else if (cfg.window == 2 && brent) {

@@ -409,3 +409,22 @@ def test_unfused_path_still_matches(gpu_lib, port, monkeypatch):
     env = dict(__import__("os").environ, HSAW_FUSED="0")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("threads", ["4", "0"])
+def test_large_upload_staged_and_plain(ctx, port, monkeypatch, threads):
+    """Uploads of >= 16 MB go through the multi-threaded pinned staging ring (graph.cu,
+    StagedCopier); HSAW_UPLOAD_THREADS=0 keeps plain pageable copies. Same pool either way, equal
+    to the oracle's stream (proj/src/sampler.cpp:388-463)."""
+    from paper_1702_05854_b200 import rmat
+    monkeypatch.setenv("HSAW_UPLOAD_THREADS", threads)
+    g = rmat.rmat_graph(17, 12, seed=9, suspect_frac=0.01)
+    csr = make_csr(g)
+    assert 8 * (csr.n + 1) + 12 * csr.m + 8 * csr.n >= 16 << 20
+    upload(ctx, csr)
+    with ctx.stream(seed=5) as st:
+        st.ensure(3000)
+        got = st.to_pool(3000)
+    exp = port.stream_samples(csr, 3000, seed=5)
+    assert got.attempts == exp.attempts and got.nsamples == exp.nsamples
+    assert np.array_equal(got.nodes, exp.nodes) and np.array_equal(got.edges, exp.edges)
