@@ -71,6 +71,29 @@ int hsaw_gpu_ctx_sync(hsaw_gpu_ctx* ctx);
  * exact integer thresholds. HSAW_EDATA if a row's cumulative array decreases. */
 int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* in_offsets,
                           const uint32_t* in_src, const double* in_cum, const double* p_of);
+
+/* Replaces build_graph (proj/src/graph.cpp:112-199, declared proj/include/hsaw/graph.hpp:123-125)
+ * for WeightMode::Given (weight_mode 0, edge_w required) and ::InDegree (weight_mode 1, edge_w
+ * ignored): the edge list (edge_u[i] -> edge_v[i]) is sorted on the device into the canonical
+ * (target, source) order, edge id = CSR position, and every row's in_cum is the SEQUENTIAL FP64
+ * sum the reference computes, so all outputs are bit-identical to the reference's ProbGraph
+ * fields: in_offsets u64[n+1], in_src u32[ne], in_cum f64[ne], and optionally weight f64[ne],
+ * edge_dst u32[ne] (NULL to skip). Data errors return HSAW_EDATA with the reference's messages
+ * ("edge endpoint out of range", "self-loop u -> v", "weight w out of (0,1] on edge u -> v",
+ * "duplicate edge u -> v", "in-weight sum s > 1 at node v", and validate()'s "graph: in-weight sum
+ * ..." / "graph: cumulative weights not increasing ..."). WeightMode::RandomNormalized (one global
+ * xorshift stream over all rows) is not built on the device: HSAW_EINVAL. */
+int hsaw_gpu_csr_build(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t* edge_u,
+                       const uint32_t* edge_v, const double* edge_w, int weight_mode,
+                       uint64_t* out_in_offsets, uint32_t* out_in_src, double* out_in_cum,
+                       double* out_weight, uint32_t* out_edge_dst);
+
+/* build_graph + hsaw_gpu_graph_upload in one step, without the CSR ever visiting the host: the
+ * edge list goes up (8 or 16 bytes per edge instead of 12 + 8 n / m), is sorted and summed on the
+ * device and re-laid out for the walk kernels. Same errors as hsaw_gpu_csr_build. */
+int hsaw_gpu_graph_build_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t* edge_u,
+                                const uint32_t* edge_v, const double* edge_w, int weight_mode,
+                                const double* p_of);
 /* Same, but p_of replaced later without re-uploading the CSR (new SuspectSet on the same graph). */
 int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of);
 /* Bytes of device memory held by the uploaded graph. */

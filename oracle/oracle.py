@@ -644,3 +644,57 @@ class Ref:
             out["json"] = buf.value.decode()
             out["wall_time_s"] = res.wall_time_s
         return out
+
+
+# ---- build_graph restatement (numpy) ----------------------------------------------------------------
+class BuildError(RuntimeError):
+    """DataError of build_graph / validate (proj/src/graph.cpp:20), message as the reference's."""
+
+
+def build_graph_np(n, u, v, w=None, mode=1):
+    """Restatement of build_graph (proj/src/graph.cpp:112-199) + validate (:70-104) for
+    WeightMode::Given (mode 0) and ::InDegree (mode 1): canonical (target, source) order, edge id =
+    CSR position, per-row SEQUENTIAL float64 cumulative sums (np.add.accumulate adds left to right,
+    like `cum += w`). Returns (in_offsets, in_src, in_cum, weight, edge_dst). Test infrastructure."""
+    u = np.asarray(u, dtype=np.uint32)
+    v = np.asarray(v, dtype=np.uint32)
+    ne = u.size
+    given = mode == 0
+    wv = None if w is None else np.asarray(w, dtype=np.float64)
+    for i in range(ne):  # graph.cpp:115-123, in input order
+        a, b = int(u[i]), int(v[i])
+        if a >= n or b >= n:
+            raise BuildError("edge endpoint out of range")
+        if a == b:
+            raise BuildError(f"self-loop {a} -> {b}")
+        if given and (not (wv[i] > 0.0) or wv[i] > 1.0):
+            raise BuildError(f"weight {wv[i]:f} out of (0,1] on edge {a} -> {b}")
+    order = np.lexsort((u, v))  # by target, then source (:125-128)
+    su, sv = u[order], v[order]
+    for i in range(1, ne):  # :129-134
+        if su[i] == su[i - 1] and sv[i] == sv[i - 1]:
+            raise BuildError(f"duplicate edge {int(su[i])} -> {int(sv[i])}")
+    off = np.zeros(n + 1, dtype=np.uint64)
+    np.add.at(off, sv.astype(np.int64) + 1, 1)
+    off = np.cumsum(off).astype(np.uint64)
+    cum = np.zeros(ne, dtype=np.float64)
+    weight = np.zeros(ne, dtype=np.float64)
+    sw = wv[order] if given else None
+    for x in range(n):  # :149-193
+        lo, hi = int(off[x]), int(off[x + 1])
+        if hi == lo:
+            continue
+        weight[lo:hi] = sw[lo:hi] if given else 1.0 / float(hi - lo)
+        cum[lo:hi] = np.add.accumulate(weight[lo:hi])
+        if given and cum[hi - 1] > 1.0 + 1e-12:
+            raise BuildError(f"in-weight sum {cum[hi - 1]:f} > 1 at node {x}")
+    for x in range(n):  # validate(), :79-103
+        lo, hi = int(off[x]), int(off[x + 1])
+        prev = 0.0
+        for i in range(lo, hi):
+            if not (cum[i] > prev):
+                raise BuildError(f"graph: cumulative weights not increasing at node {x}")
+            prev = cum[i]
+        if hi > lo and cum[hi - 1] > 1.0 + 1e-12:
+            raise BuildError(f"graph: in-weight sum {cum[hi - 1]:f} > 1 at node {x}")
+    return off, su.copy(), cum, weight, sv.copy()

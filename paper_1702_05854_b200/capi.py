@@ -73,6 +73,10 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_ctx_sync.argtypes = [vp]
     L.hsaw_gpu_graph_upload.argtypes = [vp, C.c_uint32, C.c_uint32, u64p, u32p, f64p, f64p]
     L.hsaw_gpu_suspects_upload.argtypes = [vp, f64p]
+    L.hsaw_gpu_csr_build.argtypes = [vp, C.c_uint32, C.c_uint64, u32p, u32p, f64p, C.c_int, u64p,
+                                     u32p, f64p, f64p, u32p]
+    L.hsaw_gpu_graph_build_upload.argtypes = [vp, C.c_uint32, C.c_uint64, u32p, u32p, f64p,
+                                              C.c_int, f64p]
     L.hsaw_gpu_graph_bytes.argtypes = [vp]
     L.hsaw_gpu_graph_bytes.restype = C.c_uint64
     L.hsaw_gpu_launch_count.argtypes = [vp]
@@ -120,6 +124,7 @@ def lib() -> C.CDLL:
 EXPORTS = (
     "hsaw_gpu_ctx_create", "hsaw_gpu_ctx_destroy", "hsaw_gpu_last_error",
     "hsaw_gpu_ctx_cuda_stream", "hsaw_gpu_ctx_sync", "hsaw_gpu_graph_upload",
+    "hsaw_gpu_csr_build", "hsaw_gpu_graph_build_upload",
     "hsaw_gpu_suspects_upload", "hsaw_gpu_graph_bytes", "hsaw_gpu_encode_batches",
     "hsaw_gpu_encode_stats",
     "hsaw_gpu_decode_walks", "hsaw_gpu_stream_create", "hsaw_gpu_stream_destroy",
@@ -231,6 +236,37 @@ class Context:
         self._chk(self.L.hsaw_gpu_graph_upload(self.h, n, m, _p(in_offsets, u64p),
                                                _p(in_src, u32p), _p(in_cum, f64p), _p(p_of, f64p)))
         self.n, self.m = n, m
+
+    def build_csr(self, n, edge_u, edge_v, edge_w=None, weight_mode=1, aux=True):
+        """build_graph on the device (proj/src/graph.cpp:112-199): returns (in_offsets, in_src,
+        in_cum, weight, edge_dst) as host arrays. weight_mode 0 Given, 1 InDegree."""
+        edge_u = np.ascontiguousarray(edge_u, dtype=np.uint32)
+        edge_v = np.ascontiguousarray(edge_v, dtype=np.uint32)
+        ne = int(edge_u.size)
+        assert edge_v.shape == (ne,)
+        w = None if edge_w is None else np.ascontiguousarray(edge_w, dtype=np.float64)
+        off = np.zeros(n + 1, dtype=np.uint64)
+        src = np.zeros(ne, dtype=np.uint32)
+        cum = np.zeros(ne, dtype=np.float64)
+        wt = np.zeros(ne, dtype=np.float64) if aux else None
+        dst = np.zeros(ne, dtype=np.uint32) if aux else None
+        self._chk(self.L.hsaw_gpu_csr_build(
+            self.h, n, ne, _p(edge_u, u32p), _p(edge_v, u32p), _p(w, f64p) if w is not None else None,
+            weight_mode, _p(off, u64p), _p(src, u32p), _p(cum, f64p),
+            _p(wt, f64p) if aux else None, _p(dst, u32p) if aux else None))
+        return off, src, cum, wt, dst
+
+    def build_upload_graph(self, n, edge_u, edge_v, p_of, edge_w=None, weight_mode=1):
+        """Edge list -> device graph without a host CSR (hsaw_gpu_graph_build_upload)."""
+        edge_u = np.ascontiguousarray(edge_u, dtype=np.uint32)
+        edge_v = np.ascontiguousarray(edge_v, dtype=np.uint32)
+        p_of = np.ascontiguousarray(p_of, dtype=np.float64)
+        ne = int(edge_u.size)
+        w = None if edge_w is None else np.ascontiguousarray(edge_w, dtype=np.float64)
+        self._chk(self.L.hsaw_gpu_graph_build_upload(
+            self.h, n, ne, _p(edge_u, u32p), _p(edge_v, u32p),
+            _p(w, f64p) if w is not None else None, weight_mode, _p(p_of, f64p)))
+        self.n, self.m = n, ne
 
     def upload_suspects(self, p_of):
         p_of = np.ascontiguousarray(p_of, dtype=np.float64)

@@ -404,6 +404,19 @@ inline void collect_timings(hsaw_gpu_ctx* ctx) {
     cudaGetLastError();
 }
 
+// ---- graph installation (graph.cu), shared with the device CSR builder (build.cu) ----------------
+struct CopyJob {
+    void* dst;
+    const void* src;
+    size_t bytes;
+};
+void copy_to_device(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs);
+void copy_to_host(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs);
+bool prepare_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m);
+void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_off,
+                   const uint32_t* d_src, const double* d_cum, const double* d_p);
+void release_graph(hsaw_gpu_ctx* ctx);
+
 // exclusive prefix sums (CUB) on the context stream; out may have a wider type than in
 void exclusive_sum_u32_to_u64(hsaw_gpu_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t count);
 void exclusive_sum_u32(hsaw_gpu_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t count);

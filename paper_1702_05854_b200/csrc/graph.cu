@@ -230,16 +230,15 @@ const DeviceInfo& device_info(int device) {
 // the copy runs at host-memory speed. The consumer stream waits on the copiers' last events.
 class StagedCopier {
 public:
-    struct Job {
-        void* dst;
-        const void* src;
-        size_t bytes;
-    };
+    using Job = hsawgpu::CopyJob;
     static constexpr size_t kChunk = 4u << 20;
     static constexpr int kMaxThreads = 6, kSlotsPerThread = 2;
 
     // Copies all jobs; returns false (nothing copied) when the ring cannot be set up.
-    static bool run(int device, cudaStream_t consumer, const std::vector<Job>& jobs) {
+    // to_device: pageable host -> device; otherwise device -> pageable host (the call returns
+    // once the host arrays are complete).
+    static bool run(int device, cudaStream_t consumer, const std::vector<Job>& jobs,
+                    bool to_device = true) {
         static std::mutex mu;  // one staged copy at a time per process
         std::lock_guard<std::mutex> lock(mu);
         State& st = state(device);
@@ -264,14 +263,38 @@ public:
             cudaStream_t s = st.streams[t];
             cudaStreamWaitEvent(s, st.gate, 0);
             int turn = 0;
-            for (size_t i = t; i < pieces.size(); i += nthreads, ++turn) {
-                const int slot = t * kSlotsPerThread + (turn % kSlotsPerThread);
-                if (turn >= kSlotsPerThread) cudaEventSynchronize(st.slot_done[slot]);
-                std::memcpy(st.pinned[slot], pieces[i].src, pieces[i].bytes);
-                cudaError_t e = cudaMemcpyAsync(pieces[i].dst, st.pinned[slot], pieces[i].bytes,
-                                                cudaMemcpyHostToDevice, s);
-                if (e != cudaSuccess) errs[t] = e;
-                cudaEventRecord(st.slot_done[slot], s);
+            if (to_device) {
+                for (size_t i = t; i < pieces.size(); i += nthreads, ++turn) {
+                    const int slot = t * kSlotsPerThread + (turn % kSlotsPerThread);
+                    if (turn >= kSlotsPerThread) cudaEventSynchronize(st.slot_done[slot]);
+                    std::memcpy(st.pinned[slot], pieces[i].src, pieces[i].bytes);
+                    cudaError_t e = cudaMemcpyAsync(pieces[i].dst, st.pinned[slot],
+                                                    pieces[i].bytes, cudaMemcpyHostToDevice, s);
+                    if (e != cudaSuccess) errs[t] = e;
+                    cudaEventRecord(st.slot_done[slot], s);
+                }
+            } else {
+                // device -> pinned slot (DMA), then pinned -> pageable by this thread, one chunk
+                // behind so the DMA of chunk i+1 overlaps the host copy of chunk i
+                size_t prev = pieces.size();
+                int prev_slot = 0;
+                for (size_t i = t; i < pieces.size(); i += nthreads, ++turn) {
+                    const int slot = t * kSlotsPerThread + (turn % kSlotsPerThread);
+                    cudaError_t e = cudaMemcpyAsync(st.pinned[slot], pieces[i].src, pieces[i].bytes,
+                                                    cudaMemcpyDeviceToHost, s);
+                    if (e != cudaSuccess) errs[t] = e;
+                    cudaEventRecord(st.slot_done[slot], s);
+                    if (prev != pieces.size()) {
+                        cudaEventSynchronize(st.slot_done[prev_slot]);
+                        std::memcpy(pieces[prev].dst, st.pinned[prev_slot], pieces[prev].bytes);
+                    }
+                    prev = i;
+                    prev_slot = slot;
+                }
+                if (prev != pieces.size()) {
+                    cudaEventSynchronize(st.slot_done[prev_slot]);
+                    std::memcpy(pieces[prev].dst, st.pinned[prev_slot], pieces[prev].bytes);
+                }
             }
             cudaEventRecord(st.thread_done[t], s);
         };
@@ -467,6 +490,99 @@ void exclusive_sum_u8_to_u32(hsaw_gpu_ctx* ctx, const uint8_t* in, uint32_t* out
 
 }  // namespace hsawgpu
 
+namespace hsawgpu {
+
+// Large transfers: multi-threaded staging through pinned memory; small ones (and the fallback when
+// the ring cannot be set up) go through plain pageable copies on the context stream.
+void copy_to_device(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs) {
+    uint64_t total = 0;
+    for (const auto& j : jobs) total += j.bytes;
+    if (total >= (16u << 20) && StagedCopier::run(ctx->device, ctx->stream, jobs, true)) return;
+    for (const auto& j : jobs)
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(j.dst, j.src, j.bytes, cudaMemcpyHostToDevice, ctx->stream));
+}
+
+// Device -> host; returns with the host arrays complete.
+void copy_to_host(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs) {
+    uint64_t total = 0;
+    for (const auto& j : jobs) total += j.bytes;
+    if (total >= (16u << 20) && StagedCopier::run(ctx->device, ctx->stream, jobs, false)) return;
+    for (const auto& j : jobs)
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(j.dst, j.src, j.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+}
+
+// Chooses the layout for an (n, m) graph and points ctx->g at (re)allocated stores. Returns true
+// for the compact layout, whose `src` array is filled by the caller (as uploaded / as built).
+bool prepare_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
+    const int layout = choose_layout(ctx, n, m);
+    const bool compact = layout == kLayoutCompact;
+    ctx->g_nodes_store.ensure_scratch(n);
+    ctx->g.nodes = ctx->g_nodes_store.p;
+    ctx->g.layout = layout;
+    if (compact) {
+        // header words first (16-byte aligned), then the sources
+        ctx->g_compact_store.ensure_scratch(4ull * n + (m ? m : 1));
+        ctx->g_thr_store.ensure_scratch(m ? m : 1);
+        ctx->g.hdr = reinterpret_cast<uint4*>(ctx->g_compact_store.p);
+        ctx->g.src = ctx->g_compact_store.p + 4ull * n;
+        ctx->g.thr = ctx->g_thr_store.p;
+    } else {
+        ctx->g_edges_store.ensure_scratch(m ? m : 1);
+        ctx->g.edges = ctx->g_edges_store.p;
+    }
+    return compact;
+}
+
+// Re-lays a device-resident CSR (the reference's arrays) out into the walk kernels' records.
+// For the compact layout d_src must be ctx->g.src. Synchronises; throws HSAW_EDATA on bad rows.
+void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_off,
+                   const uint32_t* d_src, const double* d_cum, const double* d_p) {
+    cudaStream_t st = ctx->stream;
+    const bool compact = ctx->g.layout == kLayoutCompact;
+    uint32_t* d_bad = reinterpret_cast<uint32_t*>(ctx->d_scalars + 60);
+    HSAW_CUDA_CHECK(cudaMemsetAsync(d_bad, 0xFF, 8, st));
+    {
+        StageScope timer(ctx, HSAW_STAGE_UPLOAD);
+        build_node_records<<<(n + 255) / 256, 256, 0, st>>>(n, d_off, d_cum, d_p, ctx->g.nodes);
+        check_launch(ctx, "build_node_records");
+        int blocks = ctx->sm_count * 8;
+        if (compact) {
+            const char* env = std::getenv("HSAW_FORCE_EXACT");  // test hook: exact picks only
+            build_compact<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p, ctx->g.thr,
+                                                  ctx->g.hdr, d_bad, env && std::atoi(env) != 0);
+            check_launch(ctx, "build_compact");
+        } else if (m) {
+            build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p, ctx->g.edges,
+                                                       d_bad);
+            check_launch(ctx, "build_edge_records");
+        }
+    }
+    uint32_t both[2] = {0, 0};
+    HSAW_CUDA_CHECK(cudaMemcpyAsync(both, d_bad, 8, cudaMemcpyDeviceToHost, st));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (both[1] != 0xFFFFFFFFu)
+        fail(HSAW_EDATA,
+             "graph: source id out of range in the row of node " + std::to_string(both[1]));
+    if (both[0] != 0xFFFFFFFFu)
+        fail(HSAW_EDATA,
+             "graph: cumulative weights not increasing at node " + std::to_string(both[0]));
+    ctx->g.n = n;
+    ctx->g.m = m;
+    if (compact) {
+        ctx->graph_bytes = (uint64_t)n * (sizeof(NodeRec) + 16) + (uint64_t)m * 12;
+    } else {
+        ctx->graph_bytes = (uint64_t)n * sizeof(NodeRec) + (uint64_t)m * sizeof(EdgeRec);
+        pin_node_records_in_l2(ctx);
+    }
+}
+
+void release_graph(hsaw_gpu_ctx* ctx) { free_graph(ctx); }
+
+}  // namespace hsawgpu
+
 extern "C" {
 
 int hsaw_gpu_ctx_create(int device, void* cuda_stream, hsaw_gpu_ctx** out) {
@@ -570,95 +686,35 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
         uint64_t* d_off = nullptr;
         uint32_t* d_src = nullptr;
         double *d_cum = nullptr, *d_p = nullptr;
-        uint32_t* d_bad = nullptr;
         auto cleanup = [&] {
             if (d_off) cudaFreeAsync(d_off, st);
             if (d_src) cudaFreeAsync(d_src, st);
             if (d_cum) cudaFreeAsync(d_cum, st);
             if (d_p) cudaFreeAsync(d_p, st);
-            if (d_bad) cudaFreeAsync(d_bad, st);
         };
-        const int layout = choose_layout(ctx, n, m);
-        const bool compact = layout == kLayoutCompact;
         try {
-            ctx->g_nodes_store.ensure_scratch(n);
-            ctx->g.nodes = ctx->g_nodes_store.p;
-            ctx->g.layout = layout;
-            if (compact) {
-                // header words first (8-byte aligned), then the sources exactly as uploaded
-                ctx->g_compact_store.ensure_scratch(4ull * n + (m ? m : 1));
-                ctx->g_thr_store.ensure_scratch(m ? m : 1);
-                ctx->g.hdr = reinterpret_cast<uint4*>(ctx->g_compact_store.p);
-                ctx->g.src = ctx->g_compact_store.p + 4ull * n;
-                ctx->g.thr = ctx->g_thr_store.p;
-            } else {
-                ctx->g_edges_store.ensure_scratch(m ? m : 1);
-                ctx->g.edges = ctx->g_edges_store.p;
-            }
+            const bool compact = prepare_layout(ctx, n, m);
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_off, ((uint64_t)n + 1) * 8, st));
             if (!compact)
                 HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_src, (uint64_t)(m ? m : 1) * 4, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_cum, (uint64_t)(m ? m : 1) * 8, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, st));
-            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_bad, 8, st));
-            std::vector<StagedCopier::Job> jobs;
+            std::vector<CopyJob> jobs;
             jobs.push_back({d_off, in_offsets, ((uint64_t)n + 1) * 8});
             if (m) {
+                // the compact layout keeps the sources exactly as uploaded
                 jobs.push_back({compact ? ctx->g.src : d_src, in_src, (uint64_t)m * 4});
                 jobs.push_back({d_cum, in_cum, (uint64_t)m * 8});
             }
             jobs.push_back({d_p, p_of, (uint64_t)n * 8});
-            uint64_t total_bytes = 0;
-            for (const auto& j : jobs) total_bytes += j.bytes;
-            // large uploads: multi-threaded staging through pinned memory; small ones (and the
-            // fallback when the ring cannot be set up) go through plain pageable copies
-            if (total_bytes < (16u << 20) || !StagedCopier::run(ctx->device, st, jobs))
-                for (const auto& j : jobs)
-                    HSAW_CUDA_CHECK(
-                        cudaMemcpyAsync(j.dst, j.src, j.bytes, cudaMemcpyHostToDevice, st));
-            HSAW_CUDA_CHECK(cudaMemsetAsync(d_bad, 0xFF, 8, st));
-            {
-                StageScope timer(ctx, HSAW_STAGE_UPLOAD);
-                build_node_records<<<(n + 255) / 256, 256, 0, st>>>(n, d_off, d_cum, d_p,
-                                                                    ctx->g.nodes);
-                check_launch(ctx, "build_node_records");
-                int blocks = ctx->sm_count * 8;
-                if (compact) {
-                    const char* env = std::getenv("HSAW_FORCE_EXACT");  // test hook: exact picks
-                    build_compact<<<blocks, 256, 0, st>>>(n, d_off, ctx->g.src, d_cum, d_p,
-                                                          ctx->g.thr, ctx->g.hdr, d_bad,
-                                                          env && std::atoi(env) != 0);
-                    check_launch(ctx, "build_compact");
-                } else if (m) {
-                    build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p,
-                                                               ctx->g.edges, d_bad);
-                    check_launch(ctx, "build_edge_records");
-                }
-            }
-            uint32_t both[2] = {0, 0};
-            HSAW_CUDA_CHECK(cudaMemcpyAsync(both, d_bad, 8, cudaMemcpyDeviceToHost, st));
-            HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
-            const uint32_t bad = both[0], bad_src = both[1];
-            if (bad_src != 0xFFFFFFFFu)
-                fail(HSAW_EDATA, "graph: source id out of range in the row of node " +
-                                     std::to_string(bad_src));
-            if (bad != 0xFFFFFFFFu)
-                fail(HSAW_EDATA, "graph: cumulative weights not increasing at node " +
-                                     std::to_string(bad));
+            copy_to_device(ctx, jobs);
+            install_graph(ctx, n, m, d_off, compact ? ctx->g.src : d_src, d_cum, d_p);
         } catch (...) {
             cleanup();
             free_graph(ctx);
             throw;
         }
         cleanup();
-        ctx->g.n = n;
-        ctx->g.m = m;
-        if (compact) {
-            ctx->graph_bytes = (uint64_t)n * (sizeof(NodeRec) + 16) + (uint64_t)m * 12;
-        } else {
-            ctx->graph_bytes = (uint64_t)n * sizeof(NodeRec) + (uint64_t)m * sizeof(EdgeRec);
-            pin_node_records_in_l2(ctx);
-        }
     });
 }
 
