@@ -22,6 +22,10 @@ int hsawh_graph_load_edge_list(const char* path, int weight_mode, uint64_t seed,
                                const char* mapping_out, void** out);
 int hsawh_graph_build(uint32_t n, uint64_t nedges, const uint32_t* u, const uint32_t* v,
                       const double* w, int weight_mode, uint64_t seed, void** out);
+/* hsaw::build_graph_device: build_graph with the sort / sums / validation on the GPU
+ * (hsaw_gpu_csr_build); weight_mode 0 Given, 1 InDegree. */
+int hsawh_graph_build_device(uint32_t n, uint64_t nedges, const uint32_t* u, const uint32_t* v,
+                             const double* w, int weight_mode, int device, void** out);
 int hsawh_graph_synth(uint32_t n, uint32_t density, uint64_t seed, void** out);
 int hsawh_graph_rmat(uint32_t scale, double edge_factor, uint64_t seed, void** out);
 int hsawh_graph_from_csr(uint32_t n, uint32_t m, const uint64_t* in_offsets,

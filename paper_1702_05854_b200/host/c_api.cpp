@@ -72,6 +72,14 @@ int hsawh_graph_build(uint32_t n, uint64_t nedges, const uint32_t* u, const uint
     });
 }
 
+int hsawh_graph_build_device(uint32_t n, uint64_t nedges, const uint32_t* u, const uint32_t* v,
+                             const double* w, int weight_mode, int device, void** out) {
+    return guarded([&] {
+        *out = new ProbGraph(build_graph_device(n, nedges, u, v, w,
+                                                static_cast<WeightMode>(weight_mode), device));
+    });
+}
+
 int hsawh_graph_synth(uint32_t n, uint32_t density, uint64_t seed, void** out) {
     return guarded([&] { *out = new ProbGraph(synth_graph(n, density, seed)); });
 }

@@ -49,6 +49,47 @@ std::vector<HsawSample> unpack(std::uint64_t count, const std::vector<std::uint6
 
 }  // namespace
 
+// ---- build_graph on the device -------------------------------------------------------------------
+ProbGraph build_graph_device(NodeId n, std::uint64_t nedges, const NodeId* u, const NodeId* v,
+                             const double* w, WeightMode mode, int device) {
+    if (mode == WeightMode::RandomNormalized)
+        throw std::invalid_argument("build_graph_device: RandomNormalized is built on the host");
+    hsaw_gpu_ctx* ctx = nullptr;
+    if (hsaw_gpu_ctx_create(device, nullptr, &ctx) != HSAW_OK)
+        throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");
+    ProbGraph g;
+    g.n = n;
+    g.m = static_cast<EdgeId>(nedges);
+    g.in_offsets.resize(static_cast<std::size_t>(n) + 1);
+    g.in_src.resize(nedges);
+    g.in_cum.resize(nedges);
+    g.weight.resize(nedges);
+    g.edge_dst.resize(nedges);
+    int rc = hsaw_gpu_csr_build(ctx, n, nedges, u, v, w, mode == WeightMode::Given ? 0 : 1,
+                                g.in_offsets.data(), g.in_src.data(), g.in_cum.data(),
+                                g.weight.data(), g.edge_dst.data());
+    std::string msg = rc == HSAW_OK ? std::string() : std::string(hsaw_gpu_last_error(ctx));
+    hsaw_gpu_ctx_destroy(ctx);
+    if (rc == HSAW_EDATA) throw DataError(msg);  // the reference's own messages, unprefixed
+    if (rc == HSAW_EINVAL) throw std::invalid_argument(msg);
+    if (rc != HSAW_OK) throw DeviceError(msg);
+    return g;
+}
+
+ProbGraph build_graph_device(NodeId n, const std::vector<std::tuple<NodeId, NodeId, double>>& edges,
+                             WeightMode mode, std::uint64_t seed, int device) {
+    if (mode == WeightMode::RandomNormalized) return build_graph(n, edges, mode, seed);
+    std::vector<NodeId> u(edges.size()), v(edges.size());
+    std::vector<double> w(mode == WeightMode::Given ? edges.size() : 0);
+    for (std::size_t i = 0; i < edges.size(); ++i) {
+        u[i] = std::get<0>(edges[i]);
+        v[i] = std::get<1>(edges[i]);
+        if (mode == WeightMode::Given) w[i] = std::get<2>(edges[i]);
+    }
+    return build_graph_device(n, edges.size(), u.data(), v.data(),
+                              mode == WeightMode::Given ? w.data() : nullptr, mode, device);
+}
+
 // ---- DeviceGraph --------------------------------------------------------------------------------
 DeviceGraph::DeviceGraph(const ProbGraph& g, const SuspectSet& vi, int device, void* cuda_stream)
     : n_(g.n), m_(g.m) {

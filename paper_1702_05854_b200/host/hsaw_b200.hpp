@@ -142,6 +142,16 @@ ProbGraph graph_from_csr(NodeId n, EdgeId m, const std::uint64_t* in_offsets, co
 
 // ---- device binding (new: the reference has no device) -----------------------------------------
 // Owns one hsaw_gpu_ctx with the graph + suspects uploaded. Every sampling object below borrows it.
+// build_graph (proj/include/hsaw/graph.hpp:123-125) with the sort, the per-row sequential sums and
+// the validation run on the GPU (hsaw_gpu_csr_build): same ProbGraph, bit for bit, same DataError
+// messages, for WeightMode::Given and ::InDegree. RandomNormalized falls through to build_graph's
+// host loop (one global draw stream). Throws DeviceError without a CUDA device.
+ProbGraph build_graph_device(NodeId n, const std::vector<std::tuple<NodeId, NodeId, double>>& edges,
+                             WeightMode mode, std::uint64_t seed = 0, int device = 0);
+// Same from flat arrays (w may be null unless mode == Given).
+ProbGraph build_graph_device(NodeId n, std::uint64_t nedges, const NodeId* u, const NodeId* v,
+                             const double* w, WeightMode mode, int device = 0);
+
 class DeviceGraph {
 public:
     DeviceGraph(const ProbGraph& g, const SuspectSet& vi, int device = 0,

@@ -39,6 +39,8 @@ def lib() -> C.CDLL:
     L.hsawh_last_error.restype = C.c_char_p
     L.hsawh_graph_load_edge_list.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int, C.c_char_p, vpp]
     L.hsawh_graph_build.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, f64p, C.c_int, C.c_uint64, vpp]
+    L.hsawh_graph_build_device.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, f64p, C.c_int,
+                                           C.c_int, vpp]
     L.hsawh_graph_synth.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, vpp]
     L.hsawh_graph_rmat.argtypes = [C.c_uint32, C.c_double, C.c_uint64, vpp]
     L.hsawh_graph_from_csr.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p, vpp]
@@ -115,6 +117,15 @@ class Graph:
         wa = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
         return cls._new(lib().hsawh_graph_build, n, u.size, _p(u, u32p), _p(v, u32p),
                         _p(wa, f64p), mode, seed)
+
+    @classmethod
+    def build_device(cls, n, u, v, w=None, mode=WEIGHT_INDEGREE, device=0):
+        """hsaw::build_graph_device: same ProbGraph as build(), sorted and summed on the GPU."""
+        u = np.ascontiguousarray(u, dtype=np.uint32)
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        wa = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+        return cls._new(lib().hsawh_graph_build_device, n, u.size, _p(u, u32p), _p(v, u32p),
+                        _p(wa, f64p), mode, device)
 
     @classmethod
     def synth(cls, n, density, seed):

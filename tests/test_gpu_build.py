@@ -96,3 +96,21 @@ def test_build_upload_samples_like_uploaded_csr(ctx, port, bg):
     exp = port.stream_samples(csr, 2000, seed=9)
     assert got.attempts == exp.attempts and got.nsamples == exp.nsamples
     assert np.array_equal(got.nodes, exp.nodes) and np.array_equal(got.edges, exp.edges)
+
+
+@pytest.mark.parametrize("name", ["indeg_hub", "given"])
+def test_host_layer_build_graph_device(bg, name):
+    """hsaw::build_graph_device (host layer, C++): the same ProbGraph as the reference's build_graph
+    — every field, bit for bit — and the reference's DataError on bad input."""
+    from paper_1702_05854_b200 import hostapi
+    n, mode = int(bg[f"{name}_n"][0]), int(bg[f"{name}_mode"][0])
+    w = bg[f"{name}_w"] if mode == 0 else None
+    g = hostapi.Graph.build_device(n, bg[f"{name}_u"], bg[f"{name}_v"], w, mode)
+    off, src, cum, wt, dst = g.arrays()
+    assert np.array_equal(off, bg[f"{name}_off"]) and np.array_equal(src, bg[f"{name}_src"])
+    assert cum.tobytes() == bg[f"{name}_cum"].tobytes()
+    assert wt.tobytes() == bg[f"{name}_weight"].tobytes() and np.array_equal(dst, bg[f"{name}_dst"])
+    g.validate()
+    with pytest.raises(hostapi.HsawError) as e:
+        hostapi.Graph.build_device(3, np.array([0, 2, 0]), np.array([1, 1, 1]))
+    assert "duplicate edge 0 -> 1" in str(e.value)
