@@ -189,9 +189,25 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device — the HSAW path has no CPU fallback")
+    # Test hook (one-GPU boxes): HSAW_BENCH_ONE_GPU=1 puts every rank on cuda:0 and swaps NCCL for
+    # gloo, so the N > 1 control flow can be exercised where only one device exists.
+    one_gpu = os.environ.get("HSAW_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def all_reduce(t, op):
+        if one_gpu:  # gloo reduces host tensors
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op)
 
     g, p_of = make_inputs(args)  # identical on every rank (seeded generator): replicated graph
     off, src, cum, _, _ = g.arrays()
@@ -268,8 +284,8 @@ def run_b200(args):
     c = torch.tensor([accepted, delta["attempts"], delta["steps"], launches],
                      dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        all_reduce(t, dist.ReduceOp.MAX)
+        all_reduce(c, dist.ReduceOp.SUM)
     elapsed_ms = float(t.item())
     tot_acc, tot_att, tot_steps, tot_launches = (float(x) for x in c.tolist())
     value = tot_acc / (elapsed_ms / 1e3)
@@ -359,8 +375,8 @@ def run_b200(args):
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     ce = torch.tensor([float(e2e_acc)], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        dist.all_reduce(ce, op=dist.ReduceOp.SUM)
+        all_reduce(te, dist.ReduceOp.MAX)
+        all_reduce(ce, dist.ReduceOp.SUM)
     out["e2e"] = {
         "value": float(ce.item()) / float(te.item()), "unit": UNIT,
         "h2d_bytes_per_step": ref_bytes, "d2h_bytes_per_step": 16,
@@ -400,6 +416,40 @@ def run_b200(args):
             }
         except Exception as exc:  # e.g. the walk pool of a huge instance outgrowing HBM
             out[args.solver] = {"k": args.esia_k, "error": str(exc)[:300]}
+
+    # ---- N > 1: the sharded solve (walks sharded by batch range, marginal-gain counts combined
+    # over NCCL; paper_1702_05854_b200/sharded.py). Every rank runs it; device-timed, max over ranks.
+    if not args.no_esia and world > 1:
+        from paper_1702_05854_b200.sharded import Comm, GpuEngine, ShardedSolver
+        kind = 0 if args.solver == "esia" else 1
+        try:
+            res, secs = None, []
+            for _ in range(2):  # first run pays one-time allocations
+                eng = GpuEngine(ctx, seed=STREAM_SEED, cfg=cfg)
+                try:
+                    barrier()
+                    s0, s1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                    s0.record(tstream)
+                    with torch.cuda.stream(tstream):
+                        res = ShardedSolver(eng, Comm()).interdict(g.n, kind, args.esia_k, 0.1,
+                                                                   1.0 / g.n)
+                    s1.record(tstream)
+                    barrier()
+                    secs.append(s0.elapsed_time(s1) / 1e3)
+                finally:
+                    eng.close()
+            tt = torch.tensor([secs[-1]], dtype=torch.float64, device="cuda")
+            all_reduce(tt, dist.ReduceOp.MAX)
+            out[args.solver] = {
+                "k": args.esia_k, "epsilon": 0.1, "delta": 1.0 / g.n, "sharded_over": world,
+                "seconds_to_solution": float(tt.item()), "seconds_to_solution_first_call": secs[0],
+                "iterations": res["iterations"], "samples_used": res["samples_used"],
+                "attempts": res["attempts"], "coverage": res["coverage"],
+                "passed_check": res["passed_check"], "est_suspension": res["est_suspension"],
+                "solution_head": res["solution"][:5],
+            }
+        except Exception as exc:
+            out[args.solver] = {"k": args.esia_k, "sharded_over": world, "error": str(exc)[:300]}
 
     # ---- CPU baseline beside it: rank 0, N=1 only, bounded sample
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -156,7 +156,22 @@ struct DevVec {
         uint64_t bytes = size_class(count * sizeof(T));
         count = bytes / sizeof(T);
         auto t0 = std::chrono::steady_clock::now();
-        HSAW_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&np), bytes, st));
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&np), bytes, st);
+        if (e == cudaErrorMemoryAllocation) {
+            // The pool never returns memory on its own (release threshold "never"): cached blocks
+            // of other size classes may be what stands in the way. Hand them back and retry once.
+            cudaGetLastError();
+            cudaStreamSynchronize(st);
+            int dev = 0;
+            cudaMemPool_t pool = nullptr;
+            if (cudaGetDevice(&dev) == cudaSuccess &&
+                cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+                cudaMemPoolTrimTo(pool, 0);
+            e = cudaMallocAsync(reinterpret_cast<void**>(&np), bytes, st);
+        }
+        if (e != cudaSuccess)
+            throw ::hsawgpu::Error{HSAW_ECUDA, "device allocation of " + std::to_string(bytes) +
+                                                   " bytes: " + cudaGetErrorString(e)};
         AllocStats& a = alloc_stats();
         a.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         a.calls += 1;

@@ -364,9 +364,7 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
         cudaMemcpyAsync(ctx->h_scalars + 1, arena_cursor, 4, cudaMemcpyDeviceToHost, st));
     const uint64_t E = read_u32(ctx, x.first.p + nb);
     const uint64_t arena_used = *reinterpret_cast<uint32_t*>(ctx->h_scalars + 1);
-    // running estimate for the next chunk's arena (chunk granularity overestimates a little)
-    double seen = (double)arena_used / (double)slots;
-    s->pairs_per_attempt = s->pairs_per_attempt > 0 ? 0.5 * (s->pairs_per_attempt + seen) : seen;
+    (void)arena_used;
 
     uint64_t A = 0, VT = 0;
     x.vidx.ensure_scratch(E + 1);
@@ -470,6 +468,12 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     }
     HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
     collect_timings(ctx);
+
+    // Running estimate for the next chunk's arena: pairs that stay in the log are those of the
+    // kept walks (plus the ones the recheck dropped and line padding, hence the slack). The arena
+    // cursor itself is no measure: it advances a whole chunk per lane however little is logged.
+    const double seen = 1.25 * (double)(VT + A + 8 * A) / (double)slots;
+    s->pairs_per_attempt = s->pairs_per_attempt > 0 ? 0.5 * (s->pairs_per_attempt + seen) : seen;
 
     s->accepted += A;
     s->total_edges += VT;
