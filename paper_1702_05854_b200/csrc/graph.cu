@@ -350,21 +350,33 @@ private:
 // reused half (32 n bytes: 32 MB at 1 M nodes, hubs are hot at any size), so they get the
 // persisting share of the 126 MB L2 through an access-policy window on the context stream, while
 // everything else (edge records, walk logs) streams through the rest. HSAW_L2_PERSIST=0 disables.
+void pin_in_l2(hsaw_gpu_ctx* ctx, const void* base, size_t bytes);
+
 void pin_node_records_in_l2(hsaw_gpu_ctx* ctx) {
+    pin_in_l2(ctx, ctx->g.nodes, (size_t)ctx->g.n * sizeof(NodeRec));
+}
+
+// Compact layout: the headers and sources (one allocation) are the hot, reused data; the walk
+// logs, slot arrays and pool writes stream through. The window marks the former persisting and
+// everything else on the stream streaming, so the log traffic cannot evict the graph.
+void pin_compact_graph_in_l2(hsaw_gpu_ctx* ctx) {
+    pin_in_l2(ctx, ctx->g.hdr, (size_t)ctx->g.n * 16 + (size_t)ctx->g.m * 4);
+}
+
+void pin_in_l2(hsaw_gpu_ctx* ctx, const void* base, size_t bytes) {
     if (const char* env = std::getenv("HSAW_L2_PERSIST"))
         if (std::atoi(env) == 0) return;
     const DeviceInfo& di = device_info(ctx->device);
     size_t max_persist = di.max_persist;
     size_t max_window = di.max_window;
     if (max_persist == 0 || max_window == 0) return;
-    size_t bytes = (size_t)ctx->g.n * sizeof(NodeRec);
     size_t carve = std::min(bytes, max_persist);
     if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) != cudaSuccess) {
         cudaGetLastError();
         return;
     }
     cudaStreamAttrValue attr{};
-    attr.accessPolicyWindow.base_ptr = ctx->g.nodes;
+    attr.accessPolicyWindow.base_ptr = const_cast<void*>(base);
     attr.accessPolicyWindow.num_bytes = std::min(bytes, max_window);
     attr.accessPolicyWindow.hitRatio =
         (float)std::min(1.0, (double)carve / (double)attr.accessPolicyWindow.num_bytes);
@@ -573,6 +585,8 @@ void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_
     ctx->g.m = m;
     if (compact) {
         ctx->graph_bytes = (uint64_t)n * (sizeof(NodeRec) + 16) + (uint64_t)m * 12;
+        if (const char* env = std::getenv("HSAW_L2_PIN_COMPACT"))  // A/B knob
+            if (std::atoi(env) != 0) pin_compact_graph_in_l2(ctx);
     } else {
         ctx->graph_bytes = (uint64_t)n * sizeof(NodeRec) + (uint64_t)m * sizeof(EdgeRec);
         pin_node_records_in_l2(ctx);

@@ -246,6 +246,26 @@ __global__ void __launch_bounds__(1024) select_lazy(const uint32_t* __restrict__
                                                     uint32_t nblk, uint64_t* __restrict__ out) {
     __shared__ uint64_t smem[32];
     __shared__ uint32_t s_blk;
+    // The block of the previous round's winner holds the stalest bound there is (the winner's own
+    // key, now covered): tighten it up front instead of spending a whole scan to find that out.
+    // (Whatever out[0] holds, recomputing a valid block's maximum exactly is always sound.)
+    const uint64_t prev = out[0];
+    const uint32_t hint = (0xFFFFFFFFu - (uint32_t)prev) / kMaxBlockItems;
+    if (prev != 0 && hint < nblk) {
+        const uint32_t blk = hint;
+        const uint64_t base = (uint64_t)blk * kMaxBlockItems;
+        uint64_t exact = 0;
+        for (uint32_t i = threadIdx.x; i < kMaxBlockItems; i += blockDim.x) {
+            uint64_t id = base + i;
+            if (id < limit) {
+                uint64_t k = gain_key(cnt[id], (uint32_t)id);
+                exact = k > exact ? k : exact;
+            }
+        }
+        exact = block_max_u64(exact, smem);
+        if (threadIdx.x == 0) blkmax[blk] = exact;
+        __syncthreads();
+    }
     for (;;) {
         uint64_t best = 0;
         uint32_t best_b = 0;
@@ -581,6 +601,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_partial.p, 0, 8, st));  // no previous winner yet
             // ---- K3: marginal-gain counts. When the counters do not fit L2, random atomics go to
             // HBM one 32-byte sector at a time; one 8-bit radix pass on the items' top bits first
             // makes consecutive items fall into one ~1/256 window of the counters, which L2 holds.

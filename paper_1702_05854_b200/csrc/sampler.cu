@@ -570,6 +570,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodePa
 
         // warp-cooperative write-out of the staged lines that filled up in this iteration: every
         // group of STAGE lanes takes one pending lane per trip and stores its line as one request
+        __syncwarp();  // the staged pairs of this iteration are visible to the whole warp
         unsigned fm = __ballot_sync(kFullMask, flush_n != 0);
         while (fm) {
             int mine = -1;
