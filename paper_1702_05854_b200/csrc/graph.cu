@@ -231,8 +231,23 @@ const DeviceInfo& device_info(int device) {
 class StagedCopier {
 public:
     using Job = hsawgpu::CopyJob;
-    static constexpr size_t kChunk = 4u << 20;
-    static constexpr int kMaxThreads = 6, kSlotsPerThread = 2;
+    static constexpr int kMaxThreads = 8, kMaxSlots = 4;
+    static size_t chunk_bytes() {  // HSAW_UPLOAD_CHUNK_MB: A/B knob
+        static const size_t v = [] {
+            const char* env = std::getenv("HSAW_UPLOAD_CHUNK_MB");
+            int mb = env ? std::atoi(env) : 4;
+            return (size_t)std::max(1, std::min(mb, 64)) << 20;
+        }();
+        return v;
+    }
+    static int slots_per_thread() {  // HSAW_UPLOAD_SLOTS: A/B knob
+        static const int v = [] {
+            const char* env = std::getenv("HSAW_UPLOAD_SLOTS");
+            int k = env ? std::atoi(env) : 2;
+            return std::max(2, std::min(k, kMaxSlots));
+        }();
+        return v;
+    }
 
     // Copies all jobs; returns false (nothing copied) when the ring cannot be set up.
     // to_device: pageable host -> device; otherwise device -> pageable host (the call returns
@@ -248,6 +263,8 @@ public:
             const char* src;
             size_t bytes;
         };
+        const size_t kChunk = chunk_bytes();
+        const int kSlotsPerThread = slots_per_thread();
         std::vector<Piece> pieces;
         for (const Job& j : jobs)
             for (size_t o = 0; o < j.bytes; o += kChunk)
@@ -315,8 +332,8 @@ private:
     struct State {
         bool ok = false;
         int nthreads = 0;
-        void* pinned[kMaxThreads * kSlotsPerThread] = {};
-        cudaEvent_t slot_done[kMaxThreads * kSlotsPerThread] = {};
+        void* pinned[kMaxThreads * kMaxSlots] = {};
+        cudaEvent_t slot_done[kMaxThreads * kMaxSlots] = {};
         cudaEvent_t thread_done[kMaxThreads] = {};
         cudaStream_t streams[kMaxThreads] = {};
         cudaEvent_t gate = nullptr;
@@ -331,8 +348,8 @@ private:
         if (hw && (unsigned)want > hw) want = (int)hw;
         st.nthreads = std::max(1, std::min(want, kMaxThreads));
         bool ok = want > 0;
-        for (int i = 0; ok && i < st.nthreads * kSlotsPerThread; ++i) {
-            ok = cudaHostAlloc(&st.pinned[i], kChunk, cudaHostAllocDefault) == cudaSuccess &&
+        for (int i = 0; ok && i < st.nthreads * slots_per_thread(); ++i) {
+            ok = cudaHostAlloc(&st.pinned[i], chunk_bytes(), cudaHostAllocDefault) == cudaSuccess &&
                  cudaEventCreateWithFlags(&st.slot_done[i], cudaEventDisableTiming) == cudaSuccess;
         }
         for (int t = 0; ok && t < st.nthreads; ++t) {
