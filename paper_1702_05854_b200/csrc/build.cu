@@ -275,14 +275,12 @@ int hsaw_gpu_graph_build_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, cons
         try {
             if (n == 0) fail(HSAW_EDATA, "graph: no nodes");
             if (ne > 0xFFFFFFFEull) fail(HSAW_EINVAL, "build: edge ids are 32-bit (types.hpp:10)");
-            const bool compact = prepare_layout(ctx, n, (uint32_t)ne);
+            prepare_layout(ctx, n, (uint32_t)ne);
             DeviceCsr csr;
-            build_device_csr(ctx, n, ne, edge_u, edge_v, edge_w, weight_mode, false,
-                             compact ? ctx->g.src : nullptr, csr);
+            build_device_csr(ctx, n, ne, edge_u, edge_v, edge_w, weight_mode, false, nullptr, csr);
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, st));
             HSAW_CUDA_CHECK(cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, st));
-            install_graph(ctx, n, (uint32_t)ne, csr.off.p, compact ? ctx->g.src : csr.src.p,
-                          csr.cum.p, d_p);
+            install_graph(ctx, n, (uint32_t)ne, csr.off.p, csr.src.p, csr.cum.p, d_p);
         } catch (...) {
             if (d_p) cudaFreeAsync(d_p, st);
             release_graph(ctx);

@@ -71,7 +71,13 @@ struct DeviceGraph {
     EdgeRec* edges = nullptr;         // fat layout only
     uint4* hdr = nullptr;             // compact layout: (lo, w, acceptance code, 0) per node;
                                       // code 0 = not a suspect, else (acc_thr >> 21) + 1
-    uint32_t* src = nullptr;          // compact layout: in_src as uploaded
+    // compact layout: in_src with a "dead end" flag per entry (the source has an empty in-row and
+    // is not a suspect: the walk ends there and its header is never read). src_bits selects the
+    // form: 21 = three entries per 64-bit word (20-bit node id + flag; n <= 2^20: 2.67 bytes per
+    // edge, the hot set of C2 drops from 80 to 59 MB), 32 = one u32 per entry with the flag in
+    // bit 31 (n <= 2^31), 0 = plain u32 without flags (HSAW_PACK=0, A/B runs).
+    uint32_t* src = nullptr;
+    uint32_t src_bits = 0;
     uint64_t* thr = nullptr;          // compact layout: ceil(in_cum * 2^53), exact path only
 };
 
@@ -428,6 +434,12 @@ struct CopyJob {
 void copy_to_device(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs);
 void copy_to_host(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs);
 bool prepare_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m);
+// Kernel-side view of DeviceGraph::src (passed by value in the kernel parameter structs).
+struct SrcRef {
+    const uint32_t* p;
+    uint32_t bits;
+};
+inline SrcRef src_ref(const DeviceGraph& g) { return SrcRef{g.src, g.src_bits}; }
 void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_off,
                    const uint32_t* d_src, const double* d_cum, const double* d_p);
 void release_graph(hsaw_gpu_ctx* ctx);

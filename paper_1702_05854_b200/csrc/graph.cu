@@ -173,6 +173,63 @@ __global__ void build_compact(uint32_t n, const uint64_t* __restrict__ off,
     }
 }
 
+// Sources of the compact layout with their dead-end flags (DeviceGraph::src_bits): one thread per
+// 64-bit word of three 21-bit entries, or per 32-bit entry.
+__device__ __forceinline__ bool dead_end(uint32_t u, uint32_t n, const uint64_t* __restrict__ off,
+                                         const double* __restrict__ p_of) {
+    return u < n && off[u + 1] == off[u] && !(p_of[u] > 0.0);
+}
+
+__global__ void pack_sources21(uint64_t m, uint32_t n, const uint32_t* __restrict__ src,
+                               const uint64_t* __restrict__ off, const double* __restrict__ p_of,
+                               uint64_t* __restrict__ out) {
+    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (3 * q >= m) return;
+    uint64_t w = 0;
+    for (uint32_t r = 0; r < 3; ++r) {
+        const uint64_t e = 3 * q + r;
+        if (e >= m) break;
+        const uint32_t u = src[e];
+        uint64_t v = u & 0xFFFFFu;
+        if (dead_end(u, n, off, p_of)) v |= 1u << 20;
+        w |= v << (21 * r);
+    }
+    out[q] = w;
+}
+
+__global__ void flag_sources32(uint64_t m, uint32_t n, const uint32_t* __restrict__ src,
+                               const uint64_t* __restrict__ off, const double* __restrict__ p_of,
+                               uint32_t* __restrict__ out) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    const uint32_t u = src[e];
+    out[e] = dead_end(u, n, off, p_of) ? (u | 0x80000000u) : u;
+}
+
+// New suspect set on the same graph: recompute the dead-end flags in place (the in-degree comes
+// from the row headers).
+__global__ void reflag_sources(uint64_t m, const uint4* __restrict__ hdr,
+                               const double* __restrict__ p_of, uint32_t bits,
+                               uint32_t* __restrict__ src) {
+    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    auto dead = [&](uint32_t u) { return (hdr[u].y & kHdrDegMask) == 0 && !(p_of[u] > 0.0); };
+    if (bits == 21) {
+        if (3 * q >= m) return;
+        uint64_t* words = reinterpret_cast<uint64_t*>(src);
+        const uint64_t in = words[q];
+        uint64_t w = 0;
+        for (uint32_t r = 0; r < 3 && 3 * q + r < m; ++r) {
+            const uint32_t u = (uint32_t)(in >> (21 * r)) & 0xFFFFFu;
+            w |= ((uint64_t)u | (dead(u) ? 1u << 20 : 0u)) << (21 * r);
+        }
+        words[q] = w;
+    } else {
+        if (q >= m) return;
+        const uint32_t u = src[q] & 0x7FFFFFFFu;
+        src[q] = dead(u) ? (u | 0x80000000u) : u;
+    }
+}
+
 __global__ void update_hdr_suspect_flags(uint32_t n, const double* __restrict__ p_of,
                                          uint4* __restrict__ hdr) {
     uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -544,7 +601,7 @@ void copy_to_host(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs) {
 }
 
 // Chooses the layout for an (n, m) graph and points ctx->g at (re)allocated stores. Returns true
-// for the compact layout, whose `src` array is filled by the caller (as uploaded / as built).
+// for the compact layout.
 bool prepare_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
     const int layout = choose_layout(ctx, n, m);
     const bool compact = layout == kLayoutCompact;
@@ -552,8 +609,18 @@ bool prepare_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
     ctx->g.nodes = ctx->g_nodes_store.p;
     ctx->g.layout = layout;
     if (compact) {
+        // sources with dead-end flags: 21-bit entries (three per 64-bit word) while ids fit in 20
+        // bits, else 32-bit entries; HSAW_PACK=0 keeps plain sources without flags (A/B runs)
+        uint32_t bits = n <= (1u << 20) ? 21 : (n <= (1u << 31) ? 32 : 0);
+        if (const char* env = std::getenv("HSAW_PACK")) {
+            const int v = std::atoi(env);
+            if (v == 0) bits = 0;
+            if (v == 32 && bits == 21) bits = 32;
+        }
+        ctx->g.src_bits = bits;
+        const uint64_t src_words = bits == 21 ? 2 * (((uint64_t)m + 2) / 3) + 2 : (m ? m : 1);
         // header words first (16-byte aligned), then the sources
-        ctx->g_compact_store.ensure_scratch(4ull * n + (m ? m : 1));
+        ctx->g_compact_store.ensure_scratch(4ull * n + src_words);
         ctx->g_thr_store.ensure_scratch(m ? m : 1);
         ctx->g.hdr = reinterpret_cast<uint4*>(ctx->g_compact_store.p);
         ctx->g.src = ctx->g_compact_store.p + 4ull * n;
@@ -566,7 +633,7 @@ bool prepare_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
 }
 
 // Re-lays a device-resident CSR (the reference's arrays) out into the walk kernels' records.
-// For the compact layout d_src must be ctx->g.src. Synchronises; throws HSAW_EDATA on bad rows.
+// Synchronises; throws HSAW_EDATA on bad rows.
 void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_off,
                    const uint32_t* d_src, const double* d_cum, const double* d_p) {
     cudaStream_t st = ctx->stream;
@@ -583,6 +650,19 @@ void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_
             build_compact<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p, ctx->g.thr,
                                                   ctx->g.hdr, d_bad, env && std::atoi(env) != 0);
             check_launch(ctx, "build_compact");
+            if (m && ctx->g.src_bits == 21) {
+                const uint64_t words = ((uint64_t)m + 2) / 3;
+                pack_sources21<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(
+                    m, n, d_src, d_off, d_p, reinterpret_cast<uint64_t*>(ctx->g.src));
+                check_launch(ctx, "pack_sources21");
+            } else if (m && ctx->g.src_bits == 32) {
+                flag_sources32<<<(unsigned)(((uint64_t)m + 255) / 256), 256, 0, st>>>(
+                    m, n, d_src, d_off, d_p, ctx->g.src);
+                check_launch(ctx, "flag_sources32");
+            } else if (m) {
+                HSAW_CUDA_CHECK(cudaMemcpyAsync(ctx->g.src, d_src, (uint64_t)m * 4,
+                                                cudaMemcpyDeviceToDevice, st));
+            }
         } else if (m) {
             build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p, ctx->g.edges,
                                                        d_bad);
@@ -601,7 +681,9 @@ void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_
     ctx->g.n = n;
     ctx->g.m = m;
     if (compact) {
-        ctx->graph_bytes = (uint64_t)n * (sizeof(NodeRec) + 16) + (uint64_t)m * 12;
+        const uint64_t src_bytes =
+            ctx->g.src_bits == 21 ? 8 * (((uint64_t)m + 2) / 3) : (uint64_t)m * 4;
+        ctx->graph_bytes = (uint64_t)n * (sizeof(NodeRec) + 16) + (uint64_t)m * 8 + src_bytes;
         if (const char* env = std::getenv("HSAW_L2_PIN_COMPACT"))  // A/B knob
             if (std::atoi(env) != 0) pin_compact_graph_in_l2(ctx);
     } else {
@@ -724,22 +806,20 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             if (d_p) cudaFreeAsync(d_p, st);
         };
         try {
-            const bool compact = prepare_layout(ctx, n, m);
+            prepare_layout(ctx, n, m);
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_off, ((uint64_t)n + 1) * 8, st));
-            if (!compact)
-                HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_src, (uint64_t)(m ? m : 1) * 4, st));
+            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_src, (uint64_t)(m ? m : 1) * 4, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_cum, (uint64_t)(m ? m : 1) * 8, st));
             HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, st));
             std::vector<CopyJob> jobs;
             jobs.push_back({d_off, in_offsets, ((uint64_t)n + 1) * 8});
             if (m) {
-                // the compact layout keeps the sources exactly as uploaded
-                jobs.push_back({compact ? ctx->g.src : d_src, in_src, (uint64_t)m * 4});
+                jobs.push_back({d_src, in_src, (uint64_t)m * 4});
                 jobs.push_back({d_cum, in_cum, (uint64_t)m * 8});
             }
             jobs.push_back({d_p, p_of, (uint64_t)n * 8});
             copy_to_device(ctx, jobs);
-            install_graph(ctx, n, m, d_off, compact ? ctx->g.src : d_src, d_cum, d_p);
+            install_graph(ctx, n, m, d_off, d_src, d_cum, d_p);
         } catch (...) {
             cleanup();
             free_graph(ctx);
@@ -767,6 +847,13 @@ int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of) {
                 update_hdr_suspect_flags<<<(n + 255) / 256, 256, 0, ctx->stream>>>(
                     n, d_p, ctx->g.hdr);
                 ++ctx->launches;
+                if (ctx->g.m && ctx->g.src_bits) {
+                    const uint64_t items =
+                        ctx->g.src_bits == 21 ? ((uint64_t)ctx->g.m + 2) / 3 : (uint64_t)ctx->g.m;
+                    reflag_sources<<<(unsigned)((items + 255) / 256), 256, 0, ctx->stream>>>(
+                        ctx->g.m, ctx->g.hdr, d_p, ctx->g.src_bits, ctx->g.src);
+                    ++ctx->launches;
+                }
             } else if (ctx->g.m) {
                 update_edge_suspect_flags<<<(ctx->g.m + 255) / 256, 256, 0, ctx->stream>>>(
                     ctx->g.m, d_p, ctx->g.edges);

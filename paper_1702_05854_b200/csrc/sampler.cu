@@ -26,7 +26,7 @@ struct EncodeParams {
     const NodeRec* nodes;
     const EdgeRec* edges;
     const uint4* hdr;      // compact layout (DeviceGraph)
-    const uint32_t* src;
+    SrcRef src;
     const uint64_t* thr;
     uint32_t n;
     uint32_t l;       // attempts per batch
@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                     else  // draw inside the row's margin, or not an arithmetic row: exact path
                         live = pick_exact(nodes, p.thr, cur, k, true_deg, slot_in_row);
                     if (STATS) st_bytes += pick_alg_bytes(true_deg, live);
-                    if (live) u = load_src(p.src, (uint64_t)lo + slot_in_row);
+                    bool dead_end;
+                    if (live) u = load_src(p.src, (uint64_t)lo + slot_in_row, dead_end);
                 } else {
                     live = deg != 0 && k < tot;  // graph.hpp:66
                     if (STATS) st_bytes += pick_alg_bytes(deg, live);
@@ -405,11 +406,12 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
 constexpr int kFastBlocksPerSM = 5;
 
 // STAGE: pairs staged per thread (one line of STAGE * 8 bytes per write-out).
-template <int MINB, int STAGE>
+// SRC_BITS: form of the source array (DeviceGraph::src_bits), a compile-time constant here.
+template <int MINB, int STAGE, int SRC_BITS>
 __global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodeParams p) {
-    __shared__ uint2 stage[kThreads * STAGE];  // [thread][(pos + lane) % STAGE]
+    __shared__ __align__(16) uint2 stage[kThreads * STAGE];  // [thread][(pos + 2 lane) % STAGE]
     __shared__ uint64_t snap[kThreads];         // Seed_h of the running attempt
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp0 = tid & ~31u;
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
     const NodeRec* __restrict__ nodes = p.nodes;
 
     uint64_t s = 0;
@@ -473,7 +475,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodePa
                     slot = (uint32_t)ex;
                 }
                 if (live) {
-                    u = load_src(p.src, (uint64_t)lo + slot);
+                    bool dead_end;
+                    u = load_src_as<SRC_BITS>(p.src.p, (uint64_t)lo + slot, dead_end);
                     bool cyc = (u == r0) | (u == r1);  // sampler.cpp:180
                     if (!cyc) {                        // BrentState::check, sampler.cpp:100-108
                         if (u == b_anchor) {
@@ -486,8 +489,15 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodePa
                     }
                     if (!cyc) {
                         ++nedges;  // resolve(), sampler.cpp:54
-                        edge = lo + slot;
-                        arrive = true;
+                        if (dead_end) {
+                            // u is no suspect (no acceptance draw) and has no in-edges: the next
+                            // pick fails after exactly one draw unless the length cap stops it
+                            // before drawing. Settled here, without reading u's header.
+                            if (nedges < p.n) (void)prg_next(s);
+                        } else {
+                            edge = lo + slot;
+                            arrive = true;
+                        }
                     }
                 }
             }
@@ -502,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodePa
                 if (lpos == lend) {  // the walk outgrew its chunk: it will be replayed
                     rec_ok = false;
                 } else {
-                    stage[tid * STAGE + ((lpos + lane) & (STAGE - 1))] = make_uint2(u, edge);
+                    stage[tid * STAGE + ((lpos + 2 * lane) & (STAGE - 1))] = make_uint2(u, edge);
                     ++lpos;
                     if ((lpos & (STAGE - 1)) == 0) {
                         flush_n = STAGE;
@@ -568,29 +578,26 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_compact_kernel(EncodePa
             }
         }
 
-        // warp-cooperative write-out of the staged lines that filled up in this iteration: every
-        // group of STAGE lanes takes one pending lane per trip and stores its line as one request
-        __syncwarp();  // the staged pairs of this iteration are visible to the whole warp
-        unsigned fm = __ballot_sync(kFullMask, flush_n != 0);
-        while (fm) {
-            int mine = -1;
+        // write-out of the staged line that filled up in this iteration (or of the last, partial
+        // line of an accepted walk, whole sectors): every such lane copies its own 64 bytes with
+        // 128-bit shared loads and 256-bit streaming stores; the lanes that have nothing to write
+        // just sit the few instructions out
+        if (flush_n != 0) {
+            uint2* dst = p.arena + flush_base;
 #pragma unroll
-            for (uint32_t g = 0; g < 32 / STAGE; ++g) {
-                const int l = fm ? __ffs(fm) - 1 : -1;
-                fm &= fm - 1;
-                if (lane / STAGE == g) mine = l;
-            }
-            const int src_lane = mine < 0 ? 0 : mine;
-            const uint32_t base = __shfl_sync(kFullMask, flush_base, src_lane);
-            const uint32_t npairs = __shfl_sync(kFullMask, flush_n, src_lane);
-            const uint32_t j = lane % STAGE;
-            if (mine >= 0 && j < npairs) {
-                const uint2 pr = stage[(warp0 + src_lane) * STAGE + ((j + src_lane) & (STAGE - 1))];
-                asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p.arena + base + j),
-                             "r"(pr.x), "r"(pr.y));
+            for (uint32_t q = 0; q < STAGE / 4; ++q) {
+                if (4 * q < flush_n) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(
+                        &stage[tid * STAGE + ((4 * q + 2 * lane) & (STAGE - 1))]);
+                    const uint4 b = *reinterpret_cast<const uint4*>(
+                        &stage[tid * STAGE + ((4 * q + 2 + 2 * lane) & (STAGE - 1))]);
+                    asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(
+                                     dst + 4 * q),
+                                 "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y),
+                                 "r"(b.z), "r"(b.w));
+                }
             }
         }
-        __syncwarp();
     }
 }
 
@@ -599,7 +606,7 @@ struct DecodeParams {
     const NodeRec* nodes;
     const EdgeRec* edges;
     const uint4* hdr;  // compact layout (DeviceGraph)
-    const uint32_t* src;
+    SrcRef src;
     const uint64_t* thr;
     uint32_t n;
     uint64_t nwalks;
@@ -686,7 +693,8 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
                         live = true;
                     else
                         live = pick_exact(nodes, p.thr, cur, k, true_deg, slot);
-                    if (live) u = load_src(p.src, (uint64_t)lo + slot);
+                    bool dead_end;
+                    if (live) u = load_src(p.src, (uint64_t)lo + slot, dead_end);
                 } else {
                     live = deg != 0 && k < tot;
                     if (live) {
@@ -968,7 +976,7 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
                    bool with_stats) {
     if (nbatches == 0) return;
     if (nbatches > 0xFFFFFFFFull) fail(HSAW_EINVAL, "encode: more than 2^32 batches per launch");
-    EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, ctx->g.src, ctx->g.thr,
+    EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, src_ref(ctx->g), ctx->g.thr,
                    ctx->g.n, cfg.batch_size, cfg.window, first_worker, nbatches, d_seed, d_len, d_count,
                    d_stats, d_cursor, nullptr, 0, nullptr, nullptr};
     const bool compact = ctx->g.layout == kLayoutCompact;
@@ -1009,7 +1017,7 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
             int b = env ? std::atoi(env) : kFastBlocksPerSM;
             return b < 1 ? 1 : (b > 8 ? 8 : b);
         }();
-        static const int fast_stage = [] {  // A/B knob: pairs staged per thread (4, 8 or 16)
+        static const int fast_stage = [] {  // A/B knob: pairs staged per thread (8 or 16)
             const char* env = std::getenv("HSAW_K1_FAST_STAGE");
             return env ? std::atoi(env) : 8;
         }();
@@ -1026,14 +1034,18 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
             kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
             check_launch(ctx, "encode_compact_kernel");
         };
-        if (fast_stage == 16)
-            run(encode_compact_kernel<4, 16>);
-        else if (fast_stage == 4)
-            run(encode_compact_kernel<4, 4>);
-        else if (fast_blocks >= 6)
-            run(encode_compact_kernel<6, 8>);  // 40 registers
-        else
-            run(encode_compact_kernel<4, 8>);
+        const uint32_t sb = ctx->g.src_bits;
+        if (fast_stage == 16) {
+            sb == 21 ? run(encode_compact_kernel<4, 16, 21>)
+                     : sb == 32 ? run(encode_compact_kernel<4, 16, 32>)
+                                : run(encode_compact_kernel<4, 16, 0>);
+        } else if (fast_blocks >= 6 && sb == 21) {
+            run(encode_compact_kernel<6, 8, 21>);  // 40 registers (A/B)
+        } else {
+            sb == 21 ? run(encode_compact_kernel<4, 8, 21>)
+                     : sb == 32 ? run(encode_compact_kernel<4, 8, 32>)
+                                : run(encode_compact_kernel<4, 8, 0>);
+        }
     } else if (cfg.window == 2 && brent) {
         // The default configuration gets the tuned variants: resident blocks per SM (register
         // budget), recording mode and instrumentation are compile-time parameters.
@@ -1093,7 +1105,7 @@ static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_
                                uint32_t* d_nodes, uint32_t* d_edges, uint8_t* d_status,
                                uint32_t* d_nnodes, uint64_t* d_stats, uint64_t* d_cursor) {
     if (nwalks == 0) return;
-    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, ctx->g.src, ctx->g.thr, ctx->g.n,
+    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, src_ref(ctx->g), ctx->g.thr, ctx->g.n,
                    nwalks,       d_seed,       d_len,      d_edge_off, d_nodes,    d_edges,
                    d_status,     d_nnodes,     d_stats,    d_cursor,   nullptr,    nullptr};
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
@@ -1121,7 +1133,7 @@ void launch_decode_pairs(hsaw_gpu_ctx* ctx, uint64_t nsel, const uint32_t* d_sel
                          const uint64_t* d_seed, const uint32_t* d_len, uint2* const* d_pair_dst,
                          uint8_t* d_status, uint64_t* d_stats, uint64_t* d_cursor) {
     if (nsel == 0) return;
-    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, ctx->g.src, ctx->g.thr, ctx->g.n,
+    DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, src_ref(ctx->g), ctx->g.thr, ctx->g.n,
                    nsel,         d_seed,       d_len,      nullptr,    nullptr,    nullptr,
                    d_status,     nullptr,      d_stats,    d_cursor,   d_sel,      d_pair_dst};
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));

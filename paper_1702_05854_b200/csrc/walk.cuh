@@ -146,10 +146,36 @@ __device__ __forceinline__ uint4 load_hdr(const uint4* __restrict__ hdr, uint32_
     return h;
 }
 
-__device__ __forceinline__ uint32_t load_src(const uint32_t* __restrict__ src, uint64_t e) {
+// in_src[e] of the compact layout: one gather, whatever the form (DeviceGraph::src_bits).
+// BITS is a compile-time constant in the production kernel and s.bits elsewhere.
+template <int BITS>
+__device__ __forceinline__ uint32_t load_src_as(const uint32_t* __restrict__ p, uint64_t e,
+                                                bool& dead) {
+    if (BITS == 21) {  // three 21-bit entries per 64-bit word; e < 2^32
+        const uint32_t q = __umulhi((uint32_t)e, 0xAAAAAAABu) >> 1;  // e / 3
+        const uint32_t r = (uint32_t)e - 3 * q;
+        uint64_t w;
+        asm volatile("ld.global.nc.u64 %0, [%1];"
+                     : "=l"(w)
+                     : "l"(reinterpret_cast<const uint64_t*>(p) + q));
+        const uint32_t v = (uint32_t)(w >> (21 * r)) & 0x1FFFFFu;
+        dead = (v >> 20) != 0;
+        return v & 0xFFFFFu;
+    }
     uint32_t u;
-    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(u) : "l"(src + e));
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(u) : "l"(p + e));
+    if (BITS == 32) {
+        dead = (u >> 31) != 0;
+        return u & 0x7FFFFFFFu;
+    }
+    dead = false;
     return u;
+}
+
+__device__ __forceinline__ uint32_t load_src(const SrcRef& s, uint64_t e, bool& dead) {
+    if (s.bits == 21) return load_src_as<21>(s.p, e, dead);
+    if (s.bits == 32) return load_src_as<32>(s.p, e, dead);
+    return load_src_as<0>(s.p, e, dead);
 }
 
 // Live-edge pick on an arithmetic row without touching the thresholds: slot = (k * deg) >> 53.
@@ -161,9 +187,13 @@ __device__ __forceinline__ bool pick_arith(uint32_t w, uint64_t k, uint32_t& slo
     const uint32_t deg = hdr_deg(w);
     const uint64_t plo = k * deg, phi = __umul64hi(k, (uint64_t)deg);
     slot = (uint32_t)((plo >> 53) | (phi << 11));
-    const uint64_t frac = plo & ((1ull << 53) - 1);
-    const uint64_t margin = 1ull << hdr_mb(w);  // mb == kHdrSlow: 2^63, never satisfied
-    return frac >= margin && frac <= (1ull << 53) - margin;
+    // margin test on the top 32 bits of the 53-bit fraction: fh >= mh and fh <= ~mh imply
+    // 2^mb <= frac <= 2^53 - 2^mb (mh = 2^max(mb - 21, 0)); the few draws this rounds into the
+    // margin take the exact path like the others. mb > 52 (kHdrSlow): never satisfied.
+    const uint32_t mb = hdr_mb(w);
+    const uint32_t mh = mb > 52 ? 0xFFFFFFFFu : (1u << (mb > 21 ? mb - 21 : 0));
+    const uint32_t fh = (uint32_t)(plo >> 21);
+    return fh >= mh && fh <= ~mh;
 }
 
 // Exact path of the compact layout: pick_live_in_edge (graph.hpp:61-80) from the node record and

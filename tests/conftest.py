@@ -84,9 +84,10 @@ def gpu_lib():
 
 # Device graph layouts, chosen at upload time: the L2-resident compact arrays with
 # arithmetic picks, the same with every pick forced through the exact threshold path, and the fat
-# 32-byte edge records used when the graph outgrows L2. Every parity test runs on all three.
+# 32-byte edge records used when the graph outgrows L2. Every parity test runs on all of them.
 LAYOUTS = {
-    "compact": {"HSAW_LAYOUT": "compact"},
+    "compact": {"HSAW_LAYOUT": "compact"},  # bit-packed sources with dead-end flags
+    "compact-plain": {"HSAW_LAYOUT": "compact", "HSAW_PACK": "0"},  # plain 32-bit sources
     "compact-exact": {"HSAW_LAYOUT": "compact", "HSAW_FORCE_EXACT": "1"},
     "fat": {"HSAW_LAYOUT": "fat"},
 }
@@ -97,6 +98,7 @@ def ctx(request, gpu_lib, monkeypatch):
     """A fresh device context per test and graph layout (the CUDA extension must be present: no
     fallback)."""
     monkeypatch.delenv("HSAW_FORCE_EXACT", raising=False)
+    monkeypatch.delenv("HSAW_PACK", raising=False)
     for k, v in LAYOUTS[request.param].items():
         monkeypatch.setenv(k, v)
     c = gpu_lib.Context(0)

@@ -31,7 +31,7 @@ def _digest(pool):
 
 
 def _sample(gpu_lib, monkeypatch, csr, env, ranges):
-    for k in ("HSAW_LAYOUT", "HSAW_FORCE_EXACT", "HSAW_K1_GENERIC", "HSAW_FUSED"):
+    for k in ("HSAW_LAYOUT", "HSAW_FORCE_EXACT", "HSAW_K1_GENERIC", "HSAW_FUSED", "HSAW_PACK"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -49,6 +49,7 @@ def test_stream_is_independent_of_layout_kernel_and_chunking(gpu_lib, monkeypatc
     ref = _digest(_sample(gpu_lib, monkeypatch, csr, {"HSAW_LAYOUT": "compact"}, whole))
     variants = {
         "fat layout": ({"HSAW_LAYOUT": "fat"}, whole),
+        "plain 32-bit sources": ({"HSAW_LAYOUT": "compact", "HSAW_PACK": "0"}, whole),
         "generic K1 on the compact layout": ({"HSAW_LAYOUT": "compact", "HSAW_K1_GENERIC": "1"}, whole),
         "encode + replay instead of recording": ({"HSAW_LAYOUT": "compact", "HSAW_FUSED": "0"}, whole),
         "three uneven ranges": ({"HSAW_LAYOUT": "compact"},
