@@ -258,6 +258,11 @@ struct hsaw_gpu_ctx {
     bool own_stream = false;
     hsawgpu::DeviceGraph g;
     uint64_t graph_bytes = 0;
+    // L2 access-policy window over the compact graph (headers + sources), attached to the K1
+    // launches only: those lines are marked persisting, so the walk-log stream of the same kernel
+    // cannot evict them, while every other kernel on the stream keeps normal caching.
+    cudaAccessPolicyWindow k1_window{};
+    bool k1_window_on = false;
     uint64_t launches = 0;
     uint64_t greedy_full_index_reruns = 0;  // thresholded index was too optimistic (diagnostic)
     std::string last_error;

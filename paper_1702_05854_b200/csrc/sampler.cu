@@ -1031,7 +1031,18 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
             int blocks = persistent_blocks(ctx, kernel, nbatches);
             blocks = std::min(blocks, fast_blocks * ctx->sm_count);
             StageScope timer(ctx, HSAW_STAGE_ENCODE);
-            kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(blocks);
+            lc.blockDim = dim3(kThreads);
+            lc.stream = ctx->stream;
+            cudaLaunchAttribute attr{};
+            if (ctx->k1_window_on) {  // keep the graph's L2 lines through the kernel's log stream
+                attr.id = cudaLaunchAttributeAccessPolicyWindow;
+                attr.val.accessPolicyWindow = ctx->k1_window;
+                lc.attrs = &attr;
+                lc.numAttrs = 1;
+            }
+            HSAW_CUDA_CHECK(cudaLaunchKernelEx(&lc, kernel, p));
             check_launch(ctx, "encode_compact_kernel");
         };
         const uint32_t sb = ctx->g.src_bits;
