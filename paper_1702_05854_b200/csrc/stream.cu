@@ -486,6 +486,8 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->accepted_after_batch.size = s->local_batches;
 }
 
+bool ctx_has_window(const hsaw_gpu_ctx* ctx) { return ctx->k1_window_on; }
+
 bool fused_enabled() {
     static const bool on = [] {
         const char* env = std::getenv("HSAW_FUSED");
@@ -508,6 +510,9 @@ void sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches) {
         s->last_batch_end = first_batch + done;
     }
     s->last_batch_end = first_batch + nbatches;
+    // sampling is over for this call: the graph lines K1 kept persisting go back to normal, the
+    // greedy / coverage kernels that follow want the whole L2 for their counters
+    if (ctx_has_window(s->ctx)) cudaCtxResetPersistingL2Cache();
 }
 
 void local_cut(const hsaw_gpu_stream* s, uint64_t min_count, uint64_t* idx, uint64_t* value) {
