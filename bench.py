@@ -341,7 +341,9 @@ def run_b200(args):
             "workload": workload_name(args, g.n, g.m),
             "step": f"{B} batches ({10 * B} attempts) per GPU: K1 encode+record, K2b exact recheck, "
                     f"ordered compaction into the device pool (K2 replay only on log overflow)",
-            "layout": "compact (4-byte in_src + 16-byte row headers, L2 resident)"
+            "layout": ("compact (in_src packed three 21-bit entries per 64-bit word + 16-byte row "
+                       "headers, L2 resident)" if g.n <= 2**20 else
+                       "compact (4-byte in_src + 16-byte row headers; headers L2 resident)")
                       if 16 * g.n <= 126 * 2**20 else "fat (32-byte edge records)",
             "parallelism": f"walks sharded by batch range over {world} GPU(s), graph replicated",
             "l2_policy": (f"L2 flushed before every timed step (256 MB memset on the launching "
