@@ -1,7 +1,7 @@
 // Greedy max-cover on device-resident walks (kernels K3-K6):
 //   K3  item_histogram     marginal-gain counts = occurrences of each candidate item in R_t
 //   K3b scatter_inverted   item -> walks inverted index (counting sort: histogram, scan, scatter)
-//   K4  argmax_partial     per-block max of (count desc, id asc) keys
+//   K4  block_maxima / select_lazy   lazily maintained block maxima of (count desc, id asc) keys
 //   K5  cover_winner       final argmax + mark the winner's walks covered + decrement the counts
 //                          of every other item in those walks
 //   K6  count_covered      CoverageIndex::coverage_of
@@ -176,37 +176,6 @@ __device__ __forceinline__ uint64_t block_max_u64(uint64_t v, uint64_t* smem) {
     v = smem[0];
     __syncthreads();
     return v;
-}
-
-// K4: key = count << 32 | ~id, so the max key is (largest count, smallest id); count 0 -> key 0.
-__global__ void __launch_bounds__(256) argmax_partial(const uint32_t* __restrict__ cnt,
-                                                      uint32_t limit,
-                                                      uint64_t* __restrict__ partial) {
-    __shared__ uint64_t smem[32];
-    uint64_t best = 0;
-    uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
-    const uint32_t limit4 = limit & ~3u;
-    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < limit4;
-         i += stride) {
-        uint4 c = *reinterpret_cast<const uint4*>(cnt + i);
-        uint32_t id = (uint32_t)i;
-        uint64_t k0 = c.x ? ((uint64_t)c.x << 32) | (0xFFFFFFFFu - id) : 0;
-        uint64_t k1 = c.y ? ((uint64_t)c.y << 32) | (0xFFFFFFFFu - (id + 1)) : 0;
-        uint64_t k2 = c.z ? ((uint64_t)c.z << 32) | (0xFFFFFFFFu - (id + 2)) : 0;
-        uint64_t k3 = c.w ? ((uint64_t)c.w << 32) | (0xFFFFFFFFu - (id + 3)) : 0;
-        k0 = k1 > k0 ? k1 : k0;
-        k2 = k3 > k2 ? k3 : k2;
-        k0 = k2 > k0 ? k2 : k0;
-        best = k0 > best ? k0 : best;
-    }
-    if (blockIdx.x == 0 && threadIdx.x < (limit - limit4)) {
-        uint32_t id = limit4 + threadIdx.x;
-        uint32_t c = cnt[id];
-        uint64_t k = c ? ((uint64_t)c << 32) | (0xFFFFFFFFu - id) : 0;
-        best = k > best ? k : best;
-    }
-    best = block_max_u64(best, smem);
-    if (threadIdx.x == 0) partial[blockIdx.x] = best;
 }
 
 // ---- lazy block maxima (CELF at block granularity) ---------------------------------------------
