@@ -82,39 +82,76 @@ __device__ __forceinline__ void source_header(const uint64_t* __restrict__ off,
     }
 }
 
-// One warp per row, lanes stride the row's slots.
+// Edge records of the slots first, first + stride, ... of row v.
+__device__ __forceinline__ void edge_row_slice(uint32_t v, uint32_t n, uint64_t lo, uint64_t hi,
+                                               uint32_t first, uint32_t stride,
+                                               const uint64_t* __restrict__ off,
+                                               const uint32_t* __restrict__ src,
+                                               const double* __restrict__ cum,
+                                               const double* __restrict__ p_of,
+                                               EdgeRec* __restrict__ out,
+                                               uint32_t* __restrict__ bad_row) {
+    for (uint64_t e = lo + first; e < hi; e += stride) {
+        double c = cum[e];
+        EdgeRec r;
+        r.thr = ge_threshold(c);
+        r.src = src[e];
+        uint64_t prev = 0;
+        if (e > lo) {
+            double cp = cum[e - 1];
+            prev = ge_threshold(cp);
+            if (!(c >= cp)) atomicMin(bad_row, v);  // decreasing or NaN cumulative weights
+        }
+        uint64_t ph = prev >> 21;
+        r.prev_hi = ph > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ph;
+        if (r.src >= n) {
+            atomicMin(bad_row + 1, v);  // source id out of range
+            r.src_lo = r.src_deg = r.src_deficit = r.flags = 0;
+        } else {
+            source_header(off, cum, p_of, r.src, r);
+        }
+        out[e] = r;
+    }
+}
+
+// One warp per row, lanes stride the row's slots; rows longer than 2048 slots are queued for
+// build_edge_records_big (one block per row) so that hub rows are not a single warp's tail.
 __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
                                    const uint32_t* __restrict__ src, const double* __restrict__ cum,
                                    const double* __restrict__ p_of, EdgeRec* __restrict__ out,
-                                   uint32_t* __restrict__ bad_row) {
+                                   uint32_t* __restrict__ bad_row, uint32_t* __restrict__ big_rows,
+                                   uint32_t* __restrict__ big_count, uint32_t big_cap) {
     uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t lane = threadIdx.x & 31;
     uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t v = warp; v < n; v += nwarps) {
         uint64_t lo = off[v], hi = off[v + 1];
-        for (uint64_t e = lo + lane; e < hi; e += 32) {
-            double c = cum[e];
-            EdgeRec r;
-            r.thr = ge_threshold(c);
-            r.src = src[e];
-            uint64_t prev = 0;
-            if (e > lo) {
-                double cp = cum[e - 1];
-                prev = ge_threshold(cp);
-                if (!(c >= cp)) atomicMin(bad_row, v);  // decreasing or NaN cumulative weights
+        if (hi - lo > 2048) {
+            uint32_t at = 0;
+            if (lane == 0) at = atomicAdd(big_count, 1u);
+            at = __shfl_sync(kFullMask, at, 0);
+            if (at < big_cap) {
+                if (lane == 0) big_rows[at] = v;
+                continue;
             }
-            uint64_t ph = prev >> 21;
-            r.prev_hi = ph > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ph;
-            if (r.src >= n) {
-                atomicMin(bad_row + 1, v);  // source id out of range
-                r.src_lo = r.src_deg = r.src_deficit = r.flags = 0;
-            } else {
-                source_header(off, cum, p_of, r.src, r);
-            }
-            out[e] = r;
         }
+        edge_row_slice(v, n, lo, hi, lane, 32, off, src, cum, p_of, out, bad_row);
     }
 }
+
+__global__ void __launch_bounds__(256) build_edge_records_big(
+    uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ src,
+    const double* __restrict__ cum, const double* __restrict__ p_of, EdgeRec* __restrict__ out,
+    uint32_t* __restrict__ bad_row, const uint32_t* __restrict__ big_rows,
+    const uint32_t* __restrict__ big_count, uint32_t big_cap) {
+    const uint32_t count = min(*big_count, big_cap);
+    for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+        const uint32_t v = big_rows[i];
+        edge_row_slice(v, n, off[v], off[v + 1], threadIdx.x, blockDim.x, off, src, cum, p_of, out,
+                       bad_row);
+    }
+}
+
 
 // Compact layout: thresholds (exact path only), validation, and per row the margin inside which the
 // arithmetic pick (k * deg) >> 53 may disagree with the thresholds. With err_i the distance of
@@ -132,44 +169,102 @@ __device__ __forceinline__ uint32_t accept_code(double p) {
     return a >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)a;
 }
 
+// Row slice [first, first + stride, ...) of row v: thresholds, validation, largest grid error.
+__device__ __forceinline__ uint64_t compact_row_slice(uint32_t v, uint32_t n, uint64_t lo,
+                                                      uint64_t hi, uint32_t first, uint32_t stride,
+                                                      const uint32_t* __restrict__ src,
+                                                      const double* __restrict__ cum,
+                                                      uint64_t* __restrict__ thr,
+                                                      uint32_t* __restrict__ bad_row) {
+    const uint64_t kSat = 1ull << 62;
+    const uint64_t d = hi - lo;
+    uint64_t maxerr = 0;
+    for (uint64_t e = lo + first; e < hi; e += stride) {
+        double c = cum[e];
+        uint64_t t = ge_threshold(c);
+        thr[e] = t;
+        if (e > lo && !(c >= cum[e - 1])) atomicMin(bad_row, v);  // decreasing or NaN
+        if (src[e] >= n) atomicMin(bad_row + 1, v);               // source id out of range
+        unsigned __int128 a = (unsigned __int128)t * d;
+        unsigned __int128 b = (unsigned __int128)(e - lo + 1) << 53;
+        unsigned __int128 diff = a > b ? a - b : b - a;
+        uint64_t err = diff >= kSat ? kSat : (uint64_t)diff;
+        maxerr = err > maxerr ? err : maxerr;
+    }
+    return maxerr;
+}
+
+__device__ __forceinline__ void write_header(uint32_t v, uint64_t lo, uint64_t d, uint64_t maxerr,
+                                             const double* __restrict__ p_of,
+                                             uint4* __restrict__ hdr, int force_exact) {
+    uint64_t need = maxerr + d + 1;               // margin in units of 1/deg, with slack
+    uint32_t mb = 64 - __clzll((long long)need);  // 2^mb > need
+    if (mb > 52 || d > kHdrDegMask || force_exact) mb = kHdrSlow;
+    uint32_t w = (uint32_t)(d > kHdrDegMask ? kHdrDegMask : d) | (mb << kHdrDegBits) |
+                 (p_of[v] > 0.0 ? 0x80000000u : 0u);
+    hdr[v] = make_uint4((uint32_t)lo, w, accept_code(p_of[v]), 0u);
+}
+
+// One warp per row; rows longer than kBigRow are queued for build_compact_big (a single warp
+// walking a 38 k-edge hub row was the whole kernel's tail: 1.5 ms for 16 M edges).
+constexpr uint64_t kBigRow = 2048;
+
 __global__ void build_compact(uint32_t n, const uint64_t* __restrict__ off,
                               const uint32_t* __restrict__ src, const double* __restrict__ cum,
                               const double* __restrict__ p_of, uint64_t* __restrict__ thr,
                               uint4* __restrict__ hdr, uint32_t* __restrict__ bad_row,
-                              int force_exact) {
+                              int force_exact, uint32_t* __restrict__ big_rows,
+                              uint32_t* __restrict__ big_count, uint32_t big_cap) {
     uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t lane = threadIdx.x & 31;
     uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint64_t kSat = 1ull << 62;
     for (uint32_t v = warp; v < n; v += nwarps) {
         uint64_t lo = off[v], hi = off[v + 1];
-        uint64_t d = hi - lo;
-        uint64_t maxerr = 0;
-        for (uint64_t e = lo + lane; e < hi; e += 32) {
-            double c = cum[e];
-            uint64_t t = ge_threshold(c);
-            thr[e] = t;
-            if (e > lo && !(c >= cum[e - 1])) atomicMin(bad_row, v);  // decreasing or NaN
-            if (src[e] >= n) atomicMin(bad_row + 1, v);               // source id out of range
-            unsigned __int128 a = (unsigned __int128)t * d;
-            unsigned __int128 b = (unsigned __int128)(e - lo + 1) << 53;
-            unsigned __int128 diff = a > b ? a - b : b - a;
-            uint64_t err = diff >= kSat ? kSat : (uint64_t)diff;
-            maxerr = err > maxerr ? err : maxerr;
+        if (hi - lo > kBigRow) {
+            uint32_t at = 0;
+            if (lane == 0) at = atomicAdd(big_count, 1u);
+            at = __shfl_sync(kFullMask, at, 0);
+            if (at < big_cap) {
+                if (lane == 0) big_rows[at] = v;
+                continue;
+            }  // queue full: fall through and do it here
         }
+        uint64_t maxerr = compact_row_slice(v, n, lo, hi, lane, 32, src, cum, thr, bad_row);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             uint64_t other = __shfl_xor_sync(kFullMask, maxerr, o);
             maxerr = other > maxerr ? other : maxerr;
         }
-        if (lane == 0) {
-            uint64_t need = maxerr + d + 1;  // margin in units of 1/deg, with slack
-            uint32_t mb = 64 - __clzll((long long)need);  // 2^mb > need
-            if (mb > 52 || d > kHdrDegMask || force_exact) mb = kHdrSlow;
-            uint32_t w = (uint32_t)(d > kHdrDegMask ? kHdrDegMask : d) | (mb << kHdrDegBits) |
-                         (p_of[v] > 0.0 ? 0x80000000u : 0u);
-            hdr[v] = make_uint4((uint32_t)lo, w, accept_code(p_of[v]), 0u);
+        if (lane == 0) write_header(v, lo, hi - lo, maxerr, p_of, hdr, force_exact);
+    }
+}
+
+// One block per queued row.
+__global__ void __launch_bounds__(256) build_compact_big(
+    uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ src,
+    const double* __restrict__ cum, const double* __restrict__ p_of, uint64_t* __restrict__ thr,
+    uint4* __restrict__ hdr, uint32_t* __restrict__ bad_row, int force_exact,
+    const uint32_t* __restrict__ big_rows, const uint32_t* __restrict__ big_count,
+    uint32_t big_cap) {
+    __shared__ uint64_t smax[8];
+    const uint32_t count = min(*big_count, big_cap);
+    for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+        const uint32_t v = big_rows[i];
+        const uint64_t lo = off[v], hi = off[v + 1];
+        uint64_t maxerr =
+            compact_row_slice(v, n, lo, hi, threadIdx.x, blockDim.x, src, cum, thr, bad_row);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t other = __shfl_xor_sync(kFullMask, maxerr, o);
+            maxerr = other > maxerr ? other : maxerr;
         }
+        if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = maxerr;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < 8; ++w) maxerr = smax[w] > maxerr ? smax[w] : maxerr;
+            write_header(v, lo, hi - lo, maxerr, p_of, hdr, force_exact);
+        }
+        __syncthreads();
     }
 }
 
@@ -667,11 +762,22 @@ void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_
         build_node_records<<<(n + 255) / 256, 256, 0, st>>>(n, d_off, d_cum, d_p, ctx->g.nodes);
         check_launch(ctx, "build_node_records");
         int blocks = ctx->sm_count * 8;
+        const uint32_t big_cap = 1u << 16;
+        ctx->chk_list.ensure_scratch(big_cap + 1);  // [0] = count, then the queued row ids
+        uint32_t* big_count = ctx->chk_list.p;
+        uint32_t* big_rows = ctx->chk_list.p + 1;
+        HSAW_CUDA_CHECK(cudaMemsetAsync(big_count, 0, 4, st));
         if (compact) {
             const char* env = std::getenv("HSAW_FORCE_EXACT");  // test hook: exact picks only
+            const int force = env && std::atoi(env) != 0;
             build_compact<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p, ctx->g.thr,
-                                                  ctx->g.hdr, d_bad, env && std::atoi(env) != 0);
+                                                  ctx->g.hdr, d_bad, force, big_rows, big_count,
+                                                  big_cap);
             check_launch(ctx, "build_compact");
+            build_compact_big<<<ctx->sm_count * 2, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p,
+                                                                 ctx->g.thr, ctx->g.hdr, d_bad,
+                                                                 force, big_rows, big_count, big_cap);
+            check_launch(ctx, "build_compact_big");
             if (m && ctx->g.src_bits == 21) {
                 const uint64_t words = ((uint64_t)m + 2) / 3;
                 pack_sources21<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(
@@ -687,8 +793,11 @@ void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_
             }
         } else if (m) {
             build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p, ctx->g.edges,
-                                                       d_bad);
+                                                       d_bad, big_rows, big_count, big_cap);
             check_launch(ctx, "build_edge_records");
+            build_edge_records_big<<<ctx->sm_count * 2, 256, 0, st>>>(
+                n, d_off, d_src, d_cum, d_p, ctx->g.edges, d_bad, big_rows, big_count, big_cap);
+            check_launch(ctx, "build_edge_records_big");
         }
     }
     uint32_t both[2] = {0, 0};
