@@ -278,7 +278,7 @@ int hsaw_gpu_graph_build_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, cons
             prepare_layout(ctx, n, (uint32_t)ne);
             DeviceCsr csr;
             build_device_csr(ctx, n, ne, edge_u, edge_v, edge_w, weight_mode, false, nullptr, csr);
-            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, st));
+            d_p = static_cast<double*>(pool_alloc((uint64_t)n * 8, st));
             HSAW_CUDA_CHECK(cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, st));
             install_graph(ctx, n, (uint32_t)ne, csr.off.p, csr.src.p, csr.cum.p, d_p);
         } catch (...) {

@@ -126,6 +126,27 @@ inline uint64_t size_class(uint64_t bytes) {
     return (bytes + step - 1) & ~(step - 1);
 }
 
+// cudaMallocAsync with one retry after handing the pool's cached blocks back to the driver (the
+// pool never releases memory on its own: release threshold "never").
+inline void* pool_alloc(uint64_t bytes, cudaStream_t st) {
+    void* np = nullptr;
+    cudaError_t e = cudaMallocAsync(&np, bytes, st);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        cudaStreamSynchronize(st);
+        int dev = 0;
+        cudaMemPool_t pool = nullptr;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+            cudaMemPoolTrimTo(pool, 0);
+        e = cudaMallocAsync(&np, bytes, st);
+    }
+    if (e != cudaSuccess)
+        throw ::hsawgpu::Error{HSAW_ECUDA, "device allocation of " + std::to_string(bytes) +
+                                               " bytes: " + cudaGetErrorString(e)};
+    return np;
+}
+
 template <class T>
 struct DevVec {
     T* p = nullptr;
@@ -162,22 +183,7 @@ struct DevVec {
         uint64_t bytes = size_class(count * sizeof(T));
         count = bytes / sizeof(T);
         auto t0 = std::chrono::steady_clock::now();
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&np), bytes, st);
-        if (e == cudaErrorMemoryAllocation) {
-            // The pool never returns memory on its own (release threshold "never"): cached blocks
-            // of other size classes may be what stands in the way. Hand them back and retry once.
-            cudaGetLastError();
-            cudaStreamSynchronize(st);
-            int dev = 0;
-            cudaMemPool_t pool = nullptr;
-            if (cudaGetDevice(&dev) == cudaSuccess &&
-                cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
-                cudaMemPoolTrimTo(pool, 0);
-            e = cudaMallocAsync(reinterpret_cast<void**>(&np), bytes, st);
-        }
-        if (e != cudaSuccess)
-            throw ::hsawgpu::Error{HSAW_ECUDA, "device allocation of " + std::to_string(bytes) +
-                                                   " bytes: " + cudaGetErrorString(e)};
+        np = static_cast<T*>(pool_alloc(bytes, st));
         AllocStats& a = alloc_stats();
         a.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         a.calls += 1;

@@ -937,10 +937,10 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
         };
         try {
             prepare_layout(ctx, n, m);
-            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_off, ((uint64_t)n + 1) * 8, st));
-            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_src, (uint64_t)(m ? m : 1) * 4, st));
-            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_cum, (uint64_t)(m ? m : 1) * 8, st));
-            HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, st));
+            d_off = static_cast<uint64_t*>(pool_alloc(((uint64_t)n + 1) * 8, st));
+            d_src = static_cast<uint32_t*>(pool_alloc((uint64_t)(m ? m : 1) * 4, st));
+            d_cum = static_cast<double*>(pool_alloc((uint64_t)(m ? m : 1) * 8, st));
+            d_p = static_cast<double*>(pool_alloc((uint64_t)n * 8, st));
             std::vector<CopyJob> jobs;
             jobs.push_back({d_off, in_offsets, ((uint64_t)n + 1) * 8});
             if (m) {
@@ -966,7 +966,7 @@ int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of) {
         if (!p_of) fail(HSAW_EINVAL, "suspects_upload: null array");
         uint32_t n = ctx->g.n;
         double* d_p = nullptr;
-        HSAW_CUDA_CHECK(cudaMallocAsync((void**)&d_p, (uint64_t)n * 8, ctx->stream));
+        d_p = static_cast<double*>(pool_alloc((uint64_t)n * 8, ctx->stream));
         cudaError_t e =
             cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, ctx->stream);
         if (e == cudaSuccess) {

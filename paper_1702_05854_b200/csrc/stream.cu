@@ -602,7 +602,12 @@ int hsaw_gpu_stream_ensure(hsaw_gpu_stream* s, uint64_t min_accepted) {
                      "attempt budget exhausted while sampling walks; suspects may be unreachable");
             // round size: only a speed knob (sampler.cpp:406-421) — pools are cut at whole-batch
             // prefixes by accepted count, so over-materialising never changes a result
-            uint64_t need = min_accepted - s->accepted;
+            // A round of up to ~2^17 batches costs the same few hundred microseconds (one
+            // resident wave of K1 plus the fixed host round trips), so when sampling is needed at
+            // all, aim for at least kFloor walks: the early, small iterations of the doubling
+            // loop then find their samples already there.
+            constexpr uint64_t kFloor = 1ull << 18;
+            uint64_t need = std::max(min_accepted, kFloor) - s->accepted;
             uint64_t batches;
             if (s->accepted == 0) {
                 batches = s->grow;
