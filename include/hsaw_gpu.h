@@ -205,6 +205,18 @@ int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                          const uint32_t* cand_ids, uint64_t ncand, const uint32_t* items,
                          uint64_t nitems, uint64_t* coverage);
 
+/* An upper bound of CoverageIndex::coverage_of(S) (proj/src/coverage.cpp:76-89) over EVERY set S of
+ * at most k candidate items, on the walks [off, off + cnt): the sum of the k largest per-item
+ * occurrence counts (capped at cnt). The doubling loop uses it on R'_t before running greedy:
+ * check_solution (coverage.cpp:216-217) fails whenever Cov_R'(solution) < Lambda_1, so an iteration
+ * whose bound is below Lambda_1 — and that is not the last one allowed by N_max — cannot pass
+ * whatever greedy selects, and its greedy run and coverage counts are skipped. Results are
+ * unchanged: only the final iteration's solution is ever reported (interdiction.cpp:36-61). */
+int hsaw_gpu_coverage_upper_bound(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
+                                  const hsaw_gpu_walkset* walkset, int kind, uint64_t off,
+                                  uint64_t cnt, const uint32_t* cand_ids, uint64_t ncand,
+                                  uint32_t k, uint64_t* bound);
+
 /* ---- stepwise greedy for sharded (multi-GPU) solves ---------------------------------------- */
 
 /* The rounds of greedy_max_cover split into steps so that ranks holding disjoint shards of R_t can

@@ -107,6 +107,8 @@ def lib() -> C.CDLL:
                                   C.c_uint32, u32p, u64p]
     L.hsaw_gpu_coverage_of.argtypes = [vp, vp, vp, C.c_int, C.c_uint64, C.c_uint64, u32p,
                                        C.c_uint64, u32p, C.c_uint64, u64p]
+    L.hsaw_gpu_coverage_upper_bound.argtypes = [vp, vp, vp, C.c_int, C.c_uint64, C.c_uint64, u32p,
+                                                C.c_uint64, C.c_uint32, u64p]
     L.hsaw_gpu_rounds_begin.argtypes = [vp, vp, vp, C.c_int, C.c_uint64, C.c_uint64, u32p,
                                         C.c_uint64, vp, C.POINTER(vp)]
     L.hsaw_gpu_rounds_occurrences.argtypes = [vp]
@@ -132,6 +134,7 @@ EXPORTS = (
     "hsaw_gpu_stream_counters", "hsaw_gpu_stream_local_cut", "hsaw_gpu_stream_slice_edges",
     "hsaw_gpu_stream_export", "hsaw_gpu_stream_stats", "hsaw_gpu_stream_collect_stats", "hsaw_gpu_walkset_import",
     "hsaw_gpu_walkset_destroy", "hsaw_gpu_greedy", "hsaw_gpu_coverage_of",
+    "hsaw_gpu_coverage_upper_bound",
     "hsaw_gpu_launch_count", "hsaw_gpu_stage_times", "hsaw_gpu_debug_counters",
     "hsaw_gpu_rounds_begin", "hsaw_gpu_rounds_occurrences", "hsaw_gpu_rounds_select",
     "hsaw_gpu_rounds_cover", "hsaw_gpu_rounds_apply", "hsaw_gpu_rounds_end",
@@ -345,6 +348,21 @@ class Context:
                                               _p(it, u32p) if it.size else None, it.size,
                                               C.byref(cov)))
         return cov.value
+
+
+    def coverage_upper_bound(self, k, *, stream=None, walkset=None, kind=KIND_EDGE, off=0,
+                             cnt=None, cand=None):
+        """Upper bound of coverage_of over every set of <= k candidates (sum of the k largest
+        per-item occurrence counts)."""
+        src = stream if stream is not None else walkset
+        cnt = src.count - off if cnt is None else cnt
+        ca = None if cand is None else np.ascontiguousarray(cand, dtype=np.uint32)
+        ub = C.c_uint64()
+        self._chk(self.L.hsaw_gpu_coverage_upper_bound(
+            self.h, stream.h if stream is not None else None,
+            walkset.h if walkset is not None else None, kind, off, cnt, _p(ca, u32p),
+            0 if ca is None else ca.size, k, C.byref(ub)))
+        return ub.value
 
 
 class Stream:

@@ -473,6 +473,44 @@ uint64_t prepare_candidates(hsaw_gpu_ctx* ctx, uint32_t limit, const uint32_t* c
 
 }  // namespace
 
+// K3: occurrences of every candidate item in the walks' item range [p0, p1) -> cnt[item] (cnt is
+// zeroed by the caller). When the counters do not fit L2, random atomics go to
+// HBM one 32-byte sector at a time; one 8-bit radix pass on the items' top bits first
+// makes consecutive items fall into one ~1/256 window of the counters, which L2 holds.
+static void histogram_counts(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t p0, uint64_t p1,
+                             const uint32_t* d_cand, uint32_t* d_cnt) {
+    cudaStream_t st = ctx->stream;
+    const uint32_t limit = v.limit;
+    const int wide = ctx->sm_count * 8;
+    if (p1 > p0) {
+        StageScope timer(ctx, HSAW_STAGE_INDEX);
+        const uint64_t nitems = p1 - p0;
+        int hb = (int)std::min<uint64_t>((nitems + 255) / 256, (uint64_t)wide);
+        const bool partition = (uint64_t)limit * 4 > (48ull << 20) && nitems > (1ull << 22) &&
+                               nitems < (1ull << 33);
+        if (partition) {
+            DevVec<uint32_t>& d_sorted = ctx->g_sorted;
+            d_sorted.ensure_scratch(nitems);
+            int top = 32 - __builtin_clz(limit - 1);
+            int begin_bit = std::max(0, top - 8);
+            size_t bytes = 0;
+            HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
+                nullptr, bytes, v.items + p0, d_sorted.p, (int64_t)nitems, begin_bit, top,
+                st));
+            ctx->cub_tmp.ensure_scratch(bytes ? bytes : 1);
+            HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
+                ctx->cub_tmp.p, bytes, v.items + p0, d_sorted.p, (int64_t)nitems,
+                begin_bit, top, st));
+            ++ctx->launches;
+            key_histogram<<<hb, 256, 0, st>>>(d_sorted.p, nitems, limit, d_cand, d_cnt);
+            check_launch(ctx, "key_histogram");
+        } else {
+            item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt);
+            check_launch(ctx, "item_histogram");
+        }
+    }
+}
+
 extern "C" {
 
 int hsaw_gpu_walkset_import(hsaw_gpu_ctx* ctx, uint32_t limit, uint64_t nsets,
@@ -571,36 +609,8 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_partial.p, 0, 8, st));  // no previous winner yet
-            // ---- K3: marginal-gain counts. When the counters do not fit L2, random atomics go to
-            // HBM one 32-byte sector at a time; one 8-bit radix pass on the items' top bits first
-            // makes consecutive items fall into one ~1/256 window of the counters, which L2 holds.
-            if (p1 > p0) {
-                StageScope timer(ctx, HSAW_STAGE_INDEX);
-                const uint64_t nitems = p1 - p0;
-                int hb = (int)std::min<uint64_t>((nitems + 255) / 256, (uint64_t)wide);
-                const bool partition = (uint64_t)limit * 4 > (48ull << 20) && nitems > (1ull << 22) &&
-                                       nitems < (1ull << 33);
-                if (partition) {
-                    DevVec<uint32_t>& d_sorted = ctx->g_sorted;
-                    d_sorted.ensure_scratch(nitems);
-                    int top = 32 - __builtin_clz(limit - 1);
-                    int begin_bit = std::max(0, top - 8);
-                    size_t bytes = 0;
-                    HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
-                        nullptr, bytes, v.items + p0, d_sorted.p, (int64_t)nitems, begin_bit, top,
-                        st));
-                    ctx->cub_tmp.ensure_scratch(bytes ? bytes : 1);
-                    HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
-                        ctx->cub_tmp.p, bytes, v.items + p0, d_sorted.p, (int64_t)nitems,
-                        begin_bit, top, st));
-                    ++ctx->launches;
-                    key_histogram<<<hb, 256, 0, st>>>(d_sorted.p, nitems, limit, d_cand, d_cnt.p);
-                    check_launch(ctx, "key_histogram");
-                } else {
-                    item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt.p);
-                    check_launch(ctx, "item_histogram");
-                }
-            }
+            // ---- K3: marginal-gain counts
+            histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
             if (min_count == 0) {
                 // Index only what can win: the smallest count whose items (and everything above)
                 // make up at most 1/8 of all occurrences. Small inputs index everything.
@@ -889,6 +899,55 @@ void hsaw_gpu_rounds_end(hsaw_gpu_rounds* g) {
     current_stream() = g->ctx->stream;
     cudaStreamSynchronize(g->ctx->stream);
     delete g;
+}
+
+int hsaw_gpu_coverage_upper_bound(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
+                                  const hsaw_gpu_walkset* walkset, int kind, uint64_t off,
+                                  uint64_t cnt, const uint32_t* cand_ids, uint64_t ncand,
+                                  uint32_t k, uint64_t* bound) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (!bound) fail(HSAW_EINVAL, "coverage_upper_bound: null output");
+        WalkView v = make_view(stream, walkset, kind, off, cnt);
+        *bound = 0;
+        if (cnt == 0 || k == 0) return;
+        cudaStream_t st = ctx->stream;
+        const uint32_t limit = v.limit;
+        std::vector<uint32_t> cand_sorted;
+        DevVec<uint32_t>& cand_bits = ctx->g_cand_bits;
+        (void)prepare_candidates(ctx, limit, cand_ids, ncand, cand_sorted, cand_bits);
+        const uint32_t* d_cand = cand_ids ? cand_bits.p : nullptr;
+        DevVec<uint32_t>& d_cnt = ctx->g_cnt;
+        DevVec<uint64_t>& d_partial = ctx->g_partial;
+        d_cnt.ensure_scratch((uint64_t)limit + 4);
+        d_partial.ensure_scratch(kCountBins + 4);
+        uint64_t p0 = 0, p1 = 0;
+        view_span(ctx, v, &p0, &p1);
+        if (p1 == p0) return;
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
+        histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
+        auto* d_bins = reinterpret_cast<unsigned long long*>(d_partial.p + 4);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_bins, 0, kCountBins * 8, st));
+        {
+            StageScope timer(ctx, HSAW_STAGE_INDEX);
+            count_of_counts<<<ctx->sm_count * 8, 256, 0, st>>>(d_cnt.p, limit, d_bins);
+            check_launch(ctx, "count_of_counts");
+        }
+        std::vector<uint64_t> bins(kCountBins);
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(bins.data(), d_bins, kCountBins * 8, cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        collect_timings(ctx);
+        // bins[c] = c * (#items occurring c times); the last bin sums every count >= kCountBins-1
+        // and is taken whole without using up any of the k slots, so the result stays a bound
+        uint64_t total = bins[kCountBins - 1], left = k;
+        for (uint32_t c = kCountBins - 2; c >= 1 && left > 0; --c) {
+            uint64_t items = bins[c] / c;
+            uint64_t take = std::min(items, left);
+            total += take * c;
+            left -= take;
+        }
+        *bound = std::min<uint64_t>(total, cnt);
+    });
 }
 
 int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,

@@ -317,6 +317,16 @@ CoverageIndex::CoverageIndex(const DeviceGraph& dg,
 
 CoverageIndex::~CoverageIndex() { hsaw_gpu_walkset_destroy(walkset_); }
 
+std::uint64_t CoverageIndex::coverage_upper_bound(std::uint32_t k) const {
+    std::uint64_t ub = 0;
+    raise(hsaw_gpu_coverage_upper_bound(ctx_, stream_, walkset_,
+                                        kind_ == ItemKind::Edge ? HSAW_KIND_EDGE : HSAW_KIND_NODE,
+                                        offset_, count_, cand_ ? cand_->data() : nullptr,
+                                        cand_ ? cand_->size() : 0, k, &ub),
+          ctx_, "coverage_upper_bound");
+    return ub;
+}
+
 std::uint64_t CoverageIndex::coverage_of(std::span<const std::uint32_t> items) const {
     std::uint64_t cov = 0;
     raise(hsaw_gpu_coverage_of(ctx_, stream_, walkset_,

@@ -280,6 +280,9 @@ public:
     std::uint32_t num_samples() const { return static_cast<std::uint32_t>(count_); }
     std::uint64_t num_candidates() const { return ncand_; }
     std::uint64_t coverage_of(std::span<const std::uint32_t> items) const;
+    // Upper bound of coverage_of over every set of at most k candidates (sum of the k largest
+    // per-item occurrence counts); lets the doubling loop skip iterations that cannot pass.
+    std::uint64_t coverage_upper_bound(std::uint32_t k) const;
 
 private:
     friend struct GreedyAccess;

@@ -6,6 +6,7 @@
 // come out bit-identical with the same libm.
 #include <charconv>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <sstream>
@@ -105,6 +106,8 @@ InterdictionResult run_on_device(const DeviceGraph& dg, const ProbGraph& g,
     GreedyResult picked;
     CheckResult verdict;
     std::uint32_t t = 0;
+    const char* skip_env = std::getenv("HSAW_SKIP_BOUND");
+    const bool skip_by_bound = !(skip_env && std::atoi(skip_env) == 0);
     for (;;) {  // interdiction.cpp:36-47
         ++t;
         size = base << (t - 1);
@@ -114,6 +117,17 @@ InterdictionResult run_on_device(const DeviceGraph& dg, const ProbGraph& g,
         // R_t = samples [0, size), R'_t = [size, 2 size): two views of the device-resident pool
         CoverageIndex in_sample(cand.kind, stream, 0, size, cand, g);
         CoverageIndex out_of_sample(cand.kind, stream, size, size, cand, g);
+        // check_solution fails whenever Cov_R'(solution) < Lambda_1 (coverage.cpp:216-217). If
+        // even the k most frequent candidates of R'_t cannot reach Lambda_1 — and this is not the
+        // last iteration N_max allows — the iteration cannot pass whatever greedy picks: skip its
+        // greedy run and coverage counts. Only the final iteration's solution is ever reported
+        // (interdiction.cpp:49-61), so the result is unchanged. HSAW_SKIP_BOUND=0 disables.
+        if (skip_by_bound && static_cast<double>(size) < sched.n_max) {
+            ts = Clock::now();
+            const auto bound = static_cast<double>(out_of_sample.coverage_upper_bound(k));
+            res.check_s += seconds_since(ts);
+            if (bound < sched.lambda1) continue;
+        }
         ts = Clock::now();
         picked = greedy_max_cover(in_sample, k);
         res.greedy_s += seconds_since(ts);

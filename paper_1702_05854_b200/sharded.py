@@ -178,6 +178,12 @@ class GpuEngine:
         return self.ctx.coverage_of(items, stream=self.stream, kind=kind, off=off, cnt=cnt,
                                     cand=cand)
 
+    def coverage_upper_bound(self, k, kind, off, cnt, cand) -> int:
+        if cnt == 0:
+            return 0
+        return self.ctx.coverage_upper_bound(k, stream=self.stream, kind=kind, off=off, cnt=cnt,
+                                             cand=cand)
+
     class _Rounds:
         def __init__(self, eng, kind, off, cnt, cand):
             self.eng = eng
@@ -278,6 +284,18 @@ class ShardedSolver:
             t = t.cuda()
         return int(self.comm.allreduce_sum_(t).item())
 
+    def coverage_upper_bound(self, k, kind, off, cnt, cand=None) -> int:
+        """Upper bound of coverage_of over every k candidates on global walks [off, off+cnt): the
+        sum over ranks of the local bounds (each rank's k most frequent items bound its share of
+        any k-set). Engines without the primitive report 'no bound' (cnt)."""
+        fn = getattr(self.eng, "coverage_upper_bound", None)
+        lo, n = self.layout.local_range(self.comm.rank, off, cnt)
+        local = n if fn is None else fn(k, kind, lo, n, cand)
+        t = torch.tensor([local], dtype=torch.int64)
+        if self.comm.backend == "nccl":
+            t = t.cuda()
+        return int(self.comm.allreduce_sum_(t).item())
+
     # -- greedy_max_cover on global walks [0, size) (proj/src/coverage.cpp:91-138), sharded
     def greedy(self, k: int, kind: int, size: int, cand=None):
         limit = self.eng.limit(kind)
@@ -340,6 +358,11 @@ class ShardedSolver:
             t += 1
             size = lam << (t - 1)
             self.ensure(2 * size)
+            # an iteration whose R'_t cannot reach Lambda_1 with any k candidates cannot pass the
+            # check (coverage.cpp:216-217): skip its greedy run unless N_max ends the loop here
+            if float(size) < sched["n_max"] and \
+                    self.coverage_upper_bound(k, kind, size, size, cand) < sched["lambda1"]:
+                continue
             solution, coverage = self.greedy(k, kind, size, cand)
             cov_r = self.coverage_of(solution, kind, 0, size, cand)
             cov_rp = self.coverage_of(solution, kind, size, size, cand)

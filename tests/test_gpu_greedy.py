@@ -165,3 +165,28 @@ def test_partitioned_histogram_large_id_space(ctx, port):
         sol, cov = ctx.greedy(25, walkset=ws)
         assert cov == exp_cov and sol.tolist() == exp_sol.tolist()
         assert ctx.coverage_of(sol, walkset=ws) == port.coverage_of(limit, off, z, sol)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_coverage_upper_bound(ctx, port, synth3000, kind):
+    """hsaw_gpu_coverage_upper_bound: the sum of the k largest per-item occurrence counts (capped at
+    the number of walks) — never below what any k candidates, greedy's included, can cover."""
+    upload(ctx, synth3000)
+    with ctx.stream(seed=11) as st:
+        st.ensure(4000)
+        pool = st.to_pool(4000)
+        nw = 3000
+        so, it = port.stream_samples(synth3000, 4000, seed=11).item_sets(kind)
+        items = it[: int(so[nw])]
+        limit = synth3000.m if kind == 0 else synth3000.n
+        counts = np.bincount(items, minlength=limit)
+        for k in (1, 5, 40):
+            ub = ctx.coverage_upper_bound(k, stream=st, kind=kind, off=0, cnt=nw)
+            assert ub == min(int(np.sort(counts)[::-1][:k].sum()), nw)
+            sol, cov = ctx.greedy(k, stream=st, kind=kind, off=0, cnt=nw)
+            assert cov <= ub
+            assert ctx.coverage_of(sol, stream=st, kind=kind, off=0, cnt=nw) <= ub
+        cand = np.arange(0, limit, 7, dtype=np.uint32)
+        ub = ctx.coverage_upper_bound(3, stream=st, kind=kind, off=0, cnt=nw, cand=cand)
+        assert ub == min(int(np.sort(counts[cand])[::-1][:3].sum()), nw)
+        assert pool.nsamples >= nw

@@ -160,3 +160,16 @@ def test_cli_interdict_byte_stable(host, golden, tmp_path):
     rc = host.run_cli(["interdict", "--graph", str(edges), "--weights", "given", "--suspects",
                        str(sus), "--k", "3", "--max-attempts", "50"])
     assert rc == 3  # SamplingError -> runtime error
+
+
+@pytest.mark.parametrize("kind,k", [(0, 20), (1, 10)])
+def test_bound_skip_does_not_change_results(host, synth3000, monkeypatch, kind, k):
+    """Iterations whose R'_t cannot reach Lambda_1 skip greedy (solver.cpp): same InterdictionResult
+    as running every iteration in full, as the reference does (interdiction.cpp:36-47)."""
+    g = host.Graph.from_csr(synth3000.n, synth3000.m, synth3000.in_offsets, synth3000.in_src,
+                            synth3000.in_cum)
+    monkeypatch.setenv("HSAW_SKIP_BOUND", "0")
+    full = host.interdict(g, synth3000.p_of, kind, k, 0.1, 0.05, seed=5)
+    monkeypatch.delenv("HSAW_SKIP_BOUND")
+    fast = host.interdict(g, synth3000.p_of, kind, k, 0.1, 0.05, seed=5)
+    assert full == fast and full["iterations"] >= 2
