@@ -9,6 +9,7 @@
 // number of still-uncovered walks containing it, ties to the smallest id; rounds whose best gain
 // is zero are padded with the smallest unselected candidate ids (host side).
 #include <algorithm>
+#include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -320,6 +321,124 @@ __global__ void __launch_bounds__(256) cover_winner(WalkView v, const uint64_t* 
             if (it < v.limit && is_cand(cand_bits, it)) atomicSub(&cnt[it], 1u);
         }
     }
+}
+
+// ---- the tail of a greedy run in one CTA ---------------------------------------------------------
+// Selected gains never increase from one round to the next (submodularity), and once the winner's
+// inverted list is a few thousand walks a whole grid is wasted on it: a round is then ~15 us of
+// launch and reduction latency around ~1 us of work. This kernel runs rounds [first, k) back to
+// back in ONE block of 1024 threads: the lazy block maxima live in shared memory (nblk * 8 bytes),
+// selection is select_lazy's, the cover is cover_winner's with the block's 32 warps, and nothing
+// leaves the SM between rounds except the count atomics (read back with ld.global.cg).
+// It stops — reporting how many rounds it completed in done_out — at a zero gain, at a winner
+// below the indexing threshold, or at a winner whose list is longer than max_list (the host then
+// runs that round with the grid-wide kernels and comes back).
+__global__ void __launch_bounds__(1024) greedy_tail_kernel(
+    WalkView v, const uint32_t* __restrict__ cand_bits, const uint64_t* __restrict__ pos,
+    const uint32_t* __restrict__ inv, uint32_t* cnt, uint32_t* covered, uint64_t* blkmax,
+    uint32_t nblk, uint32_t first, uint32_t k, uint32_t* __restrict__ solution,
+    uint64_t* __restrict__ gains, uint32_t min_indexed, uint32_t max_list,
+    uint32_t* __restrict__ done_out) {
+    // s_max[b]: upper bound of block b's maximum key; s_exact bit b: the bound IS the maximum.
+    // A bound is made exact by recomputing the block and stays exact until the item that attains
+    // it is decremented (decrements of other items cannot change a maximum), which the cover
+    // phase detects by comparing ids — so a block that surfaces as the top again usually needs no
+    // recomputation at all.
+    extern __shared__ uint64_t s_max[];
+    uint32_t* s_exact = reinterpret_cast<uint32_t*>(s_max + nblk);
+    __shared__ uint64_t smem[32];
+    __shared__ uint32_t s_blk;
+    const uint32_t limit = v.limit;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (uint32_t b = threadIdx.x; b < nblk; b += blockDim.x) s_max[b] = blkmax[b];
+    for (uint32_t b = threadIdx.x; b < (nblk + 31) / 32; b += blockDim.x) s_exact[b] = 0;
+    __syncthreads();
+    uint32_t r = first;
+    for (; r < k; ++r) {
+        // ---- selection: the block holding the largest bound, tightened until that bound is exact
+        uint64_t top;
+        for (;;) {
+            uint64_t best = 0;
+            uint32_t best_b = 0;
+            for (uint32_t b = threadIdx.x; b < nblk; b += blockDim.x) {
+                uint64_t key = s_max[b];
+                if (key > best) {
+                    best = key;
+                    best_b = b;
+                }
+            }
+            top = block_max_u64(best, smem);
+            if (top == 0) break;
+            if (best == top) s_blk = best_b;  // keys are unique
+            __syncthreads();
+            const uint32_t blk = s_blk;
+            if ((s_exact[blk >> 5] >> (blk & 31)) & 1u) break;  // known exact: the global argmax
+            const uint64_t base = (uint64_t)blk * kMaxBlockItems;
+            uint64_t exact = 0;
+            for (uint32_t i = threadIdx.x; i < kMaxBlockItems; i += blockDim.x) {
+                uint64_t id = base + i;
+                if (id < limit) {
+                    uint64_t key = gain_key(__ldcg(cnt + id), (uint32_t)id);
+                    exact = key > exact ? key : exact;
+                }
+            }
+            exact = block_max_u64(exact, smem);
+            if (threadIdx.x == 0) {
+                s_max[blk] = exact;
+                s_exact[blk >> 5] |= 1u << (blk & 31);
+            }
+            __syncthreads();
+            if (exact == top) break;
+        }
+        const uint32_t gain = (uint32_t)(top >> 32);
+        const uint32_t item = 0xFFFFFFFFu - (uint32_t)top;
+        const bool unindexed = gain != 0 && gain < min_indexed;
+        uint64_t lb = 0, le = 0;
+        if (gain != 0 && !unindexed) {
+            lb = pos[item];
+            le = pos[item + 1];
+        }
+        const bool too_long = le - lb > max_list;
+        if (gain == 0 || unindexed) {  // report the round like cover_winner does, then stop
+            if (threadIdx.x == 0) {
+                solution[r] = unindexed ? kUnindexed : 0xFFFFFFFFu;
+                gains[r] = gain;
+            }
+            ++r;
+            break;
+        }
+        if (too_long) break;  // round r is left to the grid-wide kernels
+        if (threadIdx.x == 0) {
+            solution[r] = item;
+            gains[r] = gain;
+        }
+        // ---- cover: the block's warps share the winner's inverted list, one walk per warp at a
+        // time (lane-parallel claiming and a shared-memory queue of claimed walks were both
+        // measured slower: the round is a chain of ~7 dependent memory round trips either way)
+        for (uint64_t i = lb + warp; i < le; i += nwarps) {
+            uint32_t lw = inv[i];
+            uint32_t old = 0;
+            if (lane == 0) old = atomicOr(&covered[lw >> 5], 1u << (lw & 31));
+            old = __shfl_sync(kFullMask, old, 0);
+            if (old & (1u << (lw & 31))) continue;  // already covered
+            uint64_t w = v.w0 + lw;
+            uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
+            for (uint64_t q = b + lane; q < e; q += 32) {
+                uint32_t it = v.items[q];
+                if (it < limit && is_cand(cand_bits, it)) {
+                    atomicSub(&cnt[it], 1u);
+                    const uint32_t blk = it / kMaxBlockItems;
+                    if ((uint32_t)s_max[blk] == 0xFFFFFFFFu - it)  // the item attaining the bound
+                        atomicAnd(&s_exact[blk >> 5], ~(1u << (blk & 31)));
+                }
+            }
+        }
+        __threadfence();
+        __syncthreads();
+    }
+    // hand the bounds back to the grid-wide kernels and report progress
+    for (uint32_t b = threadIdx.x; b < nblk; b += blockDim.x) blkmax[b] = s_max[b];
+    if (threadIdx.x == 0) *done_out = r;
 }
 
 // K6: one warp per walk; a walk counts once if any of its items is in the query bitmap.
@@ -674,9 +793,44 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             }
             done = 0;
             bool exhausted = p1 == p0;
+            // Rounds with long lists go to the grid-wide kernel pair, a few at a time; as soon as
+            // the lists are short the single-CTA tail kernel takes all remaining rounds in one
+            // launch (it hands a round back if its list is too long after all).
+            static const bool tail_off = [] {
+                const char* env = std::getenv("HSAW_GREEDY_TAIL");  // A/B knob
+                return env && std::atoi(env) == 0;
+            }();
+            const uint32_t kMaxTailList = 4096;
+            const size_t tail_smem = (size_t)nblk * 8 + ((size_t)nblk + 31) / 32 * 4;
+            const bool tail_ok = !tail_off && tail_smem <= (200u << 10);
+            static size_t tail_smem_set = 0;
+            if (tail_ok && tail_smem > tail_smem_set) {
+                HSAW_CUDA_CHECK(cudaFuncSetAttribute(greedy_tail_kernel,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)std::max<size_t>(tail_smem, 48u << 10)));
+                tail_smem_set = std::max<size_t>(tail_smem, 48u << 10);
+            }
+            uint32_t* d_done = reinterpret_cast<uint32_t*>(d_partial.p + 2);
+            bool try_tail = tail_ok;
             while (done < k && !exhausted) {
-                uint32_t group = std::min<uint32_t>(k - done, 64);
-                {
+                uint32_t upto;
+                if (try_tail) {
+                    HSAW_CUDA_CHECK(cudaMemsetAsync(d_done, 0, 4, st));
+                    {
+                        StageScope timer(ctx, HSAW_STAGE_ROUNDS);
+                        greedy_tail_kernel<<<1, 1024, tail_smem, st>>>(
+                            v, d_cand, d_pos.p, d_inv.p, d_cnt.p, d_cov.p, d_blkmax.p, nblk, done,
+                            k, d_sol.p, d_gain.p, min_count, kMaxTailList, d_done);
+                        check_launch(ctx, "greedy_tail_kernel");
+                    }
+                    uint32_t h_done = 0;
+                    HSAW_CUDA_CHECK(
+                        cudaMemcpyAsync(&h_done, d_done, 4, cudaMemcpyDeviceToHost, st));
+                    HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+                    upto = h_done;
+                    try_tail = false;  // if rounds are left, the next one has a long list
+                } else {
+                    uint32_t group = std::min<uint32_t>(k - done, tail_ok ? 4 : 64);
                     StageScope timer(ctx, HSAW_STAGE_ROUNDS);
                     for (uint32_t r = done; r < done + group; ++r) {
                         select_lazy<<<1, 1024, 0, st>>>(d_cnt.p, limit, d_blkmax.p, nblk,
@@ -687,21 +841,27 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                             d_sol.p, d_gain.p, min_count);
                         check_launch(ctx, "cover_winner");
                     }
+                    upto = done + group;
+                    try_tail = tail_ok;
                 }
-                HSAW_CUDA_CHECK(cudaMemcpyAsync(h_sol.data() + done, d_sol.p + done, group * 4ull,
-                                                cudaMemcpyDeviceToHost, st));
-                HSAW_CUDA_CHECK(cudaMemcpyAsync(h_gain.data() + done, d_gain.p + done,
-                                                group * 8ull, cudaMemcpyDeviceToHost, st));
-                HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
-                for (uint32_t r = done; r < done + group; ++r) {
+                if (upto > done) {
+                    HSAW_CUDA_CHECK(cudaMemcpyAsync(h_sol.data() + done, d_sol.p + done,
+                                                    (upto - done) * 4ull, cudaMemcpyDeviceToHost,
+                                                    st));
+                    HSAW_CUDA_CHECK(cudaMemcpyAsync(h_gain.data() + done, d_gain.p + done,
+                                                    (upto - done) * 8ull, cudaMemcpyDeviceToHost,
+                                                    st));
+                    HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+                }
+                uint32_t r = done;
+                for (; r < upto; ++r) {
                     if (h_sol[r] == kUnindexed) return false;  // needs the full index
                     if (h_gain[r] == 0) {
                         exhausted = true;
-                        done = r;
                         break;
                     }
                 }
-                if (!exhausted) done += group;
+                done = r;
             }
             return true;
         };
