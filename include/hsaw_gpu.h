@@ -243,6 +243,29 @@ int hsaw_gpu_rounds_cover(hsaw_gpu_rounds* g, uint32_t item, uint32_t* d_list, u
 int hsaw_gpu_rounds_apply(hsaw_gpu_rounds* g, const uint32_t* d_items, uint64_t n);
 void hsaw_gpu_rounds_end(hsaw_gpu_rounds* g);
 
+/* ---- paired LT forward simulation ----------------------------------------- */
+
+/* The run loop of estimate_suspension (proj/src/evaluation.cpp:228-237) and lt_forward_simulate
+ * (proj/include/hsaw/evaluation.hpp:25-26, evaluation.cpp:202-207) for `nruns` consecutive runs on
+ * ONE xorshift64* stream: run i draws the seed set (members ascending) and one live in-edge per
+ * node (draw_realization, :49-59) and counts the infected nodes on the original graph (full[i])
+ * and on the residual graph without the removal set (residual[i]; count_infected, :65-108).
+ * *prg_state is PrgState::state before the first run and is advanced exactly as the reference
+ * would (nruns * (|V_I| + n) draws). kind: HSAW_KIND_EDGE / HSAW_KIND_NODE select what removal_ids
+ * name (RemovalSet, evaluation.hpp:16-21; ids out of range: HSAW_EDATA); kind -1 = no removal
+ * (residual, if given, repeats full). Results are bit-exact with the sequential reference. */
+int hsaw_gpu_paired_runs(hsaw_gpu_ctx* ctx, int kind, const uint32_t* removal_ids, uint64_t nids,
+                         uint64_t* prg_state, uint64_t nruns, uint32_t* full, uint32_t* residual);
+
+/* estimate_suspension (evaluation.hpp:36-39, evaluation.cpp:209-242): stopping-rule estimate of
+ * the influence suspension of a removal set. Same argument checks and order (HSAW_EINVAL for
+ * epsilon/delta outside (0,1), HSAW_EDATA for a bad id), same early return for an empty set, same
+ * draw cap (10^9 draws), same value/capped/runs and the same final *prg_state. Runs are simulated
+ * in device batches; the FP64 accumulation runs on the host one run at a time, in order. */
+int hsaw_gpu_estimate_suspension(hsaw_gpu_ctx* ctx, int kind, const uint32_t* removal_ids,
+                                 uint64_t nids, double epsilon, double delta, uint64_t* prg_state,
+                                 double* value, int* capped, uint64_t* runs);
+
 /* ---- instrumentation ------------------------------------------------------------------------ */
 
 /* Number of kernel launches this context has issued since creation (bench.py "gpu_launches"). */
@@ -259,7 +282,8 @@ enum {
     HSAW_STAGE_ROUNDS = 5,   /* K4/K5 greedy rounds */
     HSAW_STAGE_COVERAGE = 6, /* K6 coverage_of */
     HSAW_STAGE_UPLOAD = 7,   /* graph transform kernels */
-    HSAW_STAGE_COUNT = 8
+    HSAW_STAGE_SIMULATE = 8, /* paired forward simulation (realize + pointer jumping + counts) */
+    HSAW_STAGE_COUNT = 9
 };
 /* ms[HSAW_STAGE_COUNT] accumulated milliseconds, count[HSAW_STAGE_COUNT] timed regions (both
  * nullable); reset != 0 zeroes the accumulators afterwards. Synchronises the stream. */

@@ -84,6 +84,15 @@ void hsawh_pool_copy(const void* pool, uint64_t* edge_off, uint32_t* nodes, uint
                      uint64_t* tag_worker, uint32_t* tag_seq);
 void hsawh_pool_free(void* pool);
 
+/* ---- paired forward simulation — proj/include/hsaw/evaluation.hpp:25-39 ---- */
+/* dg NULL: the reference signatures (g, vi) with the upload inside the call. *state is
+ * PrgState::state, advanced as the reference advances it. kind 0 edge / 1 node removal. */
+int hsawh_lt_forward_simulate(const void* dg, const void* g, const double* p_of, uint64_t* state,
+                              uint32_t* infected);
+int hsawh_estimate_suspension(const void* dg, const void* g, const double* p_of, int kind,
+                              const uint32_t* ids, uint64_t nids, double eps, double delta,
+                              uint64_t* state, double* value, int* capped, uint64_t* runs);
+
 /* ---- CLI (proj/include/hsaw/cli.hpp) ---- */
 int hsawh_run_cli(int argc, const char** argv);
 

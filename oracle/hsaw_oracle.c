@@ -844,3 +844,167 @@ int orc_interdict(const orc_graph* g, int kind, const uint32_t* cand_ids, uint64
     stream_free(&st, 0);
     return 0;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * paired LT forward simulation — proj/src/evaluation.cpp:19-108,195-242
+ * ---------------------------------------------------------------------------------------- */
+
+#define ORC_NO_EDGE 0xFFFFFFFFu
+
+typedef struct { /* SimContext, evaluation.cpp:20-46 */
+    uint8_t* in_x;
+    uint32_t* choice;
+    uint8_t* node_gone;
+    uint8_t* edge_gone;
+    int8_t* status;
+    uint32_t* stack;
+} sim_ctx;
+
+static int sim_init(sim_ctx* c, const orc_graph* g) {
+    c->in_x = (uint8_t*)calloc(g->n ? g->n : 1, 1);
+    c->choice = (uint32_t*)malloc(sizeof(uint32_t) * (g->n ? g->n : 1));
+    c->node_gone = (uint8_t*)calloc(g->n ? g->n : 1, 1);
+    c->edge_gone = (uint8_t*)calloc(g->m ? g->m : 1, 1);
+    c->status = (int8_t*)malloc(g->n ? g->n : 1);
+    c->stack = (uint32_t*)malloc(sizeof(uint32_t) * (g->n ? g->n : 1));
+    return c->in_x && c->choice && c->node_gone && c->edge_gone && c->status && c->stack;
+}
+
+static void sim_free(sim_ctx* c) {
+    free(c->in_x); free(c->choice); free(c->node_gone); free(c->edge_gone);
+    free(c->status); free(c->stack);
+}
+
+/* SimContext::set_removal, evaluation.cpp:35-45. edge_dst[e] is the row that holds slot e
+ * (build_graph, graph.cpp:150-192), recovered here from the offsets. */
+static void sim_set_removal(sim_ctx* c, const orc_graph* g, int kind, const uint32_t* ids,
+                            uint64_t nids) {
+    if (kind == 0) {
+        for (uint64_t i = 0; i < nids; ++i) c->edge_gone[ids[i]] = 1;
+    } else {
+        for (uint64_t i = 0; i < nids; ++i) c->node_gone[ids[i]] = 1;
+        for (uint32_t v = 0; v < g->n; ++v)
+            for (uint64_t e = g->in_offsets[v]; e < g->in_offsets[v + 1]; ++e)
+                if (c->node_gone[g->in_src[e]] || c->node_gone[v]) c->edge_gone[e] = 1;
+    }
+}
+
+/* draw_realization, evaluation.cpp:49-59: members ascending (the nodes with p_of > 0,
+ * SuspectSet::from_members graph.cpp:266-283), then one pick per node ascending. */
+static void sim_draw(const orc_graph* g, uint64_t* state, sim_ctx* c) {
+    memset(c->in_x, 0, g->n);
+    for (uint32_t v = 0; v < g->n; ++v)
+        if (g->p_of[v] != 0.0)
+            if (orc_u01(orc_prg_next(state)) <= g->p_of[v]) c->in_x[v] = 1;
+    for (uint32_t v = 0; v < g->n; ++v) {
+        uint32_t src, e;
+        c->choice[v] = orc_pick_live_in_edge(state, g, v, &src, &e) ? e : ORC_NO_EDGE;
+    }
+}
+
+/* count_infected, evaluation.cpp:65-108 */
+static uint32_t sim_count(const orc_graph* g, sim_ctx* c, int residual) {
+    const int8_t kUnknown = -1, kInProgress = -2;
+    memset(c->status, kUnknown, g->n);
+    uint32_t count = 0;
+    for (uint32_t v0 = 0; v0 < g->n; ++v0) {
+        if (c->status[v0] >= 0) {
+            count += (uint32_t)c->status[v0];
+            continue;
+        }
+        uint64_t sp = 0;
+        uint32_t cur = v0;
+        int8_t verdict;
+        for (;;) {
+            if (c->status[cur] >= 0) { verdict = c->status[cur]; break; }
+            if (c->status[cur] == kInProgress) { verdict = 0; break; }
+            if (residual && c->node_gone[cur]) { verdict = 0; break; }
+            if (c->in_x[cur]) { verdict = 1; break; }
+            uint32_t e = c->choice[cur];
+            if (e == ORC_NO_EDGE || (residual && c->edge_gone[e])) { verdict = 0; break; }
+            c->status[cur] = kInProgress;
+            c->stack[sp++] = cur;
+            cur = g->in_src[e];
+        }
+        if (c->status[cur] < 0) c->status[cur] = verdict;
+        for (uint64_t i = 0; i < sp; ++i) c->status[c->stack[i]] = verdict;
+        count += (uint32_t)verdict;
+    }
+    return count;
+}
+
+/* lt_forward_simulate, evaluation.cpp:202-207 */
+uint32_t orc_lt_forward_simulate(const orc_graph* g, uint64_t* state) {
+    sim_ctx c;
+    if (!sim_init(&c, g)) { sim_free(&c); return 0; }
+    sim_draw(g, state, &c);
+    uint32_t r = sim_count(g, &c, 0);
+    sim_free(&c);
+    return r;
+}
+
+static int removal_valid(const orc_graph* g, int kind, const uint32_t* ids, uint64_t nids) {
+    uint32_t limit = kind == 0 ? g->m : g->n; /* RemovalSet::validate, evaluation.cpp:195-200 */
+    for (uint64_t i = 0; i < nids; ++i)
+        if (ids[i] >= limit) return 0;
+    return 1;
+}
+
+/* The paired runs of the estimate_suspension loop body (evaluation.cpp:233-236) for a fixed
+ * number of runs: full[i] / residual[i] of run i on one shared stream. status 0 / 2. */
+int orc_paired_runs(const orc_graph* g, int kind, const uint32_t* ids, uint64_t nids,
+                    uint64_t* state, uint64_t nruns, uint32_t* full, uint32_t* residual) {
+    if (!removal_valid(g, kind, ids, nids)) return 2;
+    sim_ctx c;
+    if (!sim_init(&c, g)) { sim_free(&c); return 4; }
+    sim_set_removal(&c, g, kind, ids, nids);
+    for (uint64_t r = 0; r < nruns; ++r) {
+        sim_draw(g, state, &c);
+        full[r] = sim_count(g, &c, 0);
+        residual[r] = sim_count(g, &c, 1);
+    }
+    sim_free(&c);
+    return 0;
+}
+
+/* estimate_suspension, evaluation.cpp:209-242. status 0 ok, 1 invalid argument, 2 DataError. */
+int orc_estimate_suspension(const orc_graph* g, int kind, const uint32_t* ids, uint64_t nids,
+                            double epsilon, double delta, uint64_t* state, orc_suspension* out) {
+    if (!(epsilon > 0.0) || epsilon >= 1.0) return 1;
+    if (!(delta > 0.0) || delta >= 1.0) return 1;
+    if (!removal_valid(g, kind, ids, nids)) return 2;
+    out->value = 0.0; out->capped = 0; out->runs = 0;
+    if (nids == 0) return 0; /* :218 */
+
+    sim_ctx c;
+    if (!sim_init(&c, g)) { sim_free(&c); return 4; }
+    sim_set_removal(&c, g, kind, ids, nids);
+
+    double upsilon = 4.0 * (exp(1.0) - 2.0) * log(2.0 / delta) * (1.0 + epsilon) /
+                     (epsilon * epsilon);
+    uint64_t members = 0;
+    for (uint32_t v = 0; v < g->n; ++v) members += g->p_of[v] != 0.0;
+    uint64_t draws_per_run = members + g->n;
+    uint64_t max_runs = 1000000000ull / draws_per_run; /* kDrawCap, :17 */
+    if (max_runs < 1) max_runs = 1;
+
+    double sum = 0.0;
+    uint64_t runs = 0;
+    while (sum < upsilon) {
+        if (runs >= max_runs) {
+            out->value = 0.0; out->capped = 1; out->runs = runs;
+            sim_free(&c);
+            return 0;
+        }
+        sim_draw(g, state, &c);
+        uint32_t full = sim_count(g, &c, 0);
+        uint32_t residual = sim_count(g, &c, 1);
+        sum += (double)(full - residual) / (double)g->n;
+        ++runs;
+    }
+    out->value = (double)g->n * upsilon / (double)runs;
+    out->capped = 0;
+    out->runs = runs;
+    sim_free(&c);
+    return 0;
+}

@@ -121,6 +121,10 @@ class _OrcResult(C.Structure):
                 ("est_suspension", C.c_double), ("passed_check", C.c_int)]
 
 
+class _OrcSuspension(C.Structure):
+    _fields_ = [("value", C.c_double), ("capped", C.c_int), ("runs", C.c_uint64)]
+
+
 class _RefResult(C.Structure):
     _fields_ = [("k", C.c_uint32), ("iterations", C.c_uint32), ("coverage", C.c_uint64),
                 ("samples_used", C.c_uint64), ("attempts", C.c_uint64),
@@ -189,6 +193,13 @@ class Port:
         L.orc_interdict.argtypes = [C.POINTER(_OrcGraph), C.c_int, u32p, C.c_uint64, C.c_uint32,
                                     C.c_double, C.c_double, C.c_uint64, C.POINTER(_OrcCfg),
                                     C.POINTER(_OrcResult), u32p]
+        L.orc_lt_forward_simulate.restype = C.c_uint32
+        L.orc_lt_forward_simulate.argtypes = [C.POINTER(_OrcGraph), u64p]
+        L.orc_paired_runs.argtypes = [C.POINTER(_OrcGraph), C.c_int, u32p, C.c_uint64, u64p,
+                                      C.c_uint64, u32p, u32p]
+        L.orc_estimate_suspension.argtypes = [C.POINTER(_OrcGraph), C.c_int, u32p, C.c_uint64,
+                                              C.c_double, C.c_double, u64p,
+                                              C.POINTER(_OrcSuspension)]
 
     # -- prng
     def splitmix_next(self, state):
@@ -317,6 +328,41 @@ class Port:
                     coverage=res.coverage, samples_used=res.samples_used, attempts=res.attempts,
                     iterations=res.iterations, passed_check=bool(res.passed_check))
 
+    # -- paired LT forward simulation (proj/src/evaluation.cpp:49-108,202-242)
+    def lt_forward_simulate(self, csr, state):
+        """-> (infected, state_after)"""
+        g = self._g(csr)
+        s = C.c_uint64(state)
+        r = self.L.orc_lt_forward_simulate(C.byref(g), C.byref(s))
+        return int(r), s.value
+
+    def paired_runs(self, csr, kind, ids, state, nruns):
+        """-> (full u32[nruns], residual u32[nruns], state_after)"""
+        g = self._g(csr)
+        a = np.ascontiguousarray(ids, dtype=np.uint32)
+        buf = a if a.size else np.zeros(1, dtype=np.uint32)
+        full = np.zeros(max(nruns, 1), dtype=np.uint32)
+        res = np.zeros(max(nruns, 1), dtype=np.uint32)
+        s = C.c_uint64(state)
+        rc = self.L.orc_paired_runs(C.byref(g), kind, _p(buf, u32p), a.size, C.byref(s), nruns,
+                                    _p(full, u32p), _p(res, u32p))
+        if rc:
+            raise OracleError(rc, "paired_runs")
+        return full[:nruns], res[:nruns], s.value
+
+    def estimate_suspension(self, csr, kind, ids, eps, delta, state):
+        """-> dict(value, capped, runs, state)"""
+        g = self._g(csr)
+        a = np.ascontiguousarray(ids, dtype=np.uint32)
+        buf = a if a.size else np.zeros(1, dtype=np.uint32)
+        s = C.c_uint64(state)
+        out = _OrcSuspension()
+        rc = self.L.orc_estimate_suspension(C.byref(g), kind, _p(buf, u32p), a.size, eps, delta,
+                                            C.byref(s), C.byref(out))
+        if rc:
+            raise OracleError(rc, "estimate_suspension")
+        return dict(value=out.value, capped=bool(out.capped), runs=int(out.runs), state=s.value)
+
 
 def _copy_pool(stats_fn, copy_fn, h) -> PoolData:
     ns, at, te = C.c_uint64(), C.c_uint64(), C.c_uint64()
@@ -396,6 +442,11 @@ class Ref:
                                     C.c_uint32, C.c_double, C.c_double, C.c_uint32, C.c_uint64,
                                     C.c_uint32, C.c_uint64, C.POINTER(_RefResult), u32p,
                                     C.c_char_p, C.c_uint64]
+
+        L.ref_lt_forward_simulate.argtypes = [C.c_void_p, C.c_void_p, u64p, u32p]
+        L.ref_estimate_suspension.argtypes = [C.c_void_p, C.c_void_p, C.c_int, u32p, C.c_uint64,
+                                              C.c_double, C.c_double, u64p, f64p,
+                                              C.POINTER(C.c_int), u64p]
 
     def _chk(self, rc, what):
         if rc:
@@ -644,6 +695,35 @@ class Ref:
             out["json"] = buf.value.decode()
             out["wall_time_s"] = res.wall_time_s
         return out
+
+    # -- paired LT forward simulation (proj/include/hsaw/evaluation.hpp:25-39)
+    def lt_forward_simulate(self, csr, state, hd=None):
+        def run(h):
+            s, out = C.c_uint64(state), C.c_uint32()
+            self._chk(self.L.ref_lt_forward_simulate(h.g, h.vi, C.byref(s), C.byref(out)),
+                      "lt_forward_simulate")
+            return int(out.value), s.value
+
+        if hd is not None:
+            return run(hd)
+        with self.handles(csr) as h:
+            return run(h)
+
+    def estimate_suspension(self, csr, kind, ids, eps, delta, state, hd=None):
+        a = np.ascontiguousarray(ids, dtype=np.uint32)
+        buf = a if a.size else np.zeros(1, dtype=np.uint32)
+
+        def run(h):
+            s, v, cp, runs = C.c_uint64(state), C.c_double(), C.c_int(), C.c_uint64()
+            self._chk(self.L.ref_estimate_suspension(h.g, h.vi, kind, _p(buf, u32p), a.size, eps,
+                                                     delta, C.byref(s), C.byref(v), C.byref(cp),
+                                                     C.byref(runs)), "estimate_suspension")
+            return dict(value=v.value, capped=bool(cp.value), runs=int(runs.value), state=s.value)
+
+        if hd is not None:
+            return run(hd)
+        with self.handles(csr) as h:
+            return run(h)
 
 
 # ---- build_graph restatement (numpy) ----------------------------------------------------------------

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "hsaw/coverage.hpp"
+#include "hsaw/evaluation.hpp"
 #include "hsaw/graph.hpp"
 #include "hsaw/interdiction.hpp"
 #include "hsaw/prng.hpp"
@@ -449,6 +450,35 @@ int ref_interdict(void* gp, void* vip, int kind, const std::uint32_t* cand_ids,
             std::strncpy(json, j.c_str(), json_cap - 1);
             json[json_cap - 1] = 0;
         }
+    });
+}
+
+// ---- paired LT forward simulation (proj/include/hsaw/evaluation.hpp:16-39) ----
+int ref_lt_forward_simulate(void* gp, void* vip, std::uint64_t* state,
+                            std::uint32_t* infected) {
+    return guarded([&] {
+        PrgState s{*state};
+        *infected = lt_forward_simulate(*static_cast<ProbGraph*>(gp),
+                                        *static_cast<SuspectSet*>(vip), s);
+        *state = s.state;
+    });
+}
+int ref_estimate_suspension(void* gp, void* vip, int kind,
+                            const std::uint32_t* ids, std::uint64_t nids,
+                            double epsilon, double delta, std::uint64_t* state,
+                            double* value, int* capped, std::uint64_t* runs) {
+    return guarded([&] {
+        RemovalSet r;
+        r.kind = kind == 0 ? ItemKind::Edge : ItemKind::Node;
+        r.ids.assign(ids, ids + nids);
+        PrgState s{*state};
+        SuspensionEstimate e = estimate_suspension(
+            *static_cast<ProbGraph*>(gp), *static_cast<SuspectSet*>(vip), r,
+            epsilon, delta, s);
+        *state = s.state;
+        *value = e.value;
+        *capped = e.capped ? 1 : 0;
+        *runs = e.runs;
     });
 }
 

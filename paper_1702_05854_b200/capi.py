@@ -21,7 +21,8 @@ f64p = C.POINTER(C.c_double)
 HSAW_OK, HSAW_EINVAL, HSAW_EDATA, HSAW_EBUDGET, HSAW_ERANGE, HSAW_ECUDA = range(6)
 KIND_EDGE, KIND_NODE = 0, 1
 
-STAGE_NAMES = ("encode", "decode", "distinct", "compact", "index", "rounds", "coverage", "upload")
+STAGE_NAMES = ("encode", "decode", "distinct", "compact", "index", "rounds", "coverage", "upload",
+               "simulate")
 STAT_NAMES = ("attempts", "draws", "steps", "alg_bytes", "accepted", "decode_steps", "dropped",
               "spare")
 
@@ -118,6 +119,9 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_rounds_apply.argtypes = [vp, vp, C.c_uint64]
     L.hsaw_gpu_rounds_end.argtypes = [vp]
     L.hsaw_gpu_rounds_end.restype = None
+    L.hsaw_gpu_paired_runs.argtypes = [vp, C.c_int, u32p, C.c_uint64, u64p, C.c_uint64, u32p, u32p]
+    L.hsaw_gpu_estimate_suspension.argtypes = [vp, C.c_int, u32p, C.c_uint64, C.c_double,
+                                               C.c_double, u64p, f64p, C.POINTER(C.c_int), u64p]
     _LIB = L
     return L
 
@@ -138,6 +142,7 @@ EXPORTS = (
     "hsaw_gpu_launch_count", "hsaw_gpu_stage_times", "hsaw_gpu_debug_counters",
     "hsaw_gpu_rounds_begin", "hsaw_gpu_rounds_occurrences", "hsaw_gpu_rounds_select",
     "hsaw_gpu_rounds_cover", "hsaw_gpu_rounds_apply", "hsaw_gpu_rounds_end",
+    "hsaw_gpu_paired_runs", "hsaw_gpu_estimate_suspension",
 )
 
 
@@ -220,10 +225,37 @@ class Context:
 
     def stage_times(self, reset: bool = False) -> dict:
         """{stage: (ms, timed regions)} measured with CUDA events around the kernels."""
-        ms = np.zeros(8, dtype=np.float64)
-        cnt = np.zeros(8, dtype=np.uint64)
+        ms = np.zeros(len(STAGE_NAMES), dtype=np.float64)
+        cnt = np.zeros(len(STAGE_NAMES), dtype=np.uint64)
         self._chk(self.L.hsaw_gpu_stage_times(self.h, _p(ms, f64p), _p(cnt, u64p), int(reset)))
         return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(STAGE_NAMES)}
+
+    # -- paired LT forward simulation (proj/src/evaluation.cpp:49-108,202-242)
+    def paired_runs(self, kind, ids, state, nruns):
+        """-> (full u32[nruns], residual u32[nruns], state_after). kind -1: no removal."""
+        a = np.ascontiguousarray([] if ids is None else ids, dtype=np.uint32)
+        buf = a if a.size else np.zeros(1, dtype=np.uint32)
+        full = np.zeros(max(nruns, 1), dtype=np.uint32)
+        res = np.zeros(max(nruns, 1), dtype=np.uint32)
+        s = C.c_uint64(state)
+        self._chk(self.L.hsaw_gpu_paired_runs(self.h, kind, _p(buf, u32p), a.size, C.byref(s),
+                                              nruns, _p(full, u32p), _p(res, u32p)))
+        return full[:nruns], res[:nruns], s.value
+
+    def lt_forward_simulate(self, state):
+        """lt_forward_simulate(g, vi, s): -> (infected, state_after)."""
+        full, _, after = self.paired_runs(-1, None, state, 1)
+        return int(full[0]), after
+
+    def estimate_suspension(self, kind, ids, eps, delta, state):
+        """-> dict(value, capped, runs, state) like SuspensionEstimate + the advanced PrgState."""
+        a = np.ascontiguousarray(ids, dtype=np.uint32)
+        buf = a if a.size else np.zeros(1, dtype=np.uint32)
+        s, v, cp, runs = C.c_uint64(state), C.c_double(), C.c_int(), C.c_uint64()
+        self._chk(self.L.hsaw_gpu_estimate_suspension(self.h, kind, _p(buf, u32p), a.size, eps,
+                                                      delta, C.byref(s), C.byref(v), C.byref(cp),
+                                                      C.byref(runs)))
+        return dict(value=v.value, capped=bool(cp.value), runs=int(runs.value), state=s.value)
 
     @property
     def graph_bytes(self) -> int:

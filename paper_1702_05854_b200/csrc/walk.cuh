@@ -199,7 +199,7 @@ __device__ __forceinline__ bool pick_arith(uint32_t w, uint64_t k, uint32_t& slo
 // Exact path of the compact layout: pick_live_in_edge (graph.hpp:61-80) from the node record and
 // the threshold array. Returns -1 for "no edge", else the first slot i with k < thr[lo + i].
 // Everything is passed and returned by value so that callers keep their walk state in registers.
-__device__ __noinline__ int64_t pick_exact_slot(const NodeRec* __restrict__ nodes,
+static __device__ __noinline__ int64_t pick_exact_slot(const NodeRec* __restrict__ nodes,
                                                 const uint64_t* __restrict__ thr, uint32_t v,
                                                 uint64_t k) {
     NodeRec r = load_node(nodes, v);

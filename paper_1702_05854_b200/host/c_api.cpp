@@ -265,6 +265,42 @@ void hsawh_pool_copy(const void* pool, uint64_t* edge_off, uint32_t* nodes, uint
 
 void hsawh_pool_free(void* pool) { delete static_cast<SamplePool*>(pool); }
 
+int hsawh_lt_forward_simulate(const void* dg, const void* g, const double* p_of, uint64_t* state,
+                              uint32_t* infected) {
+    return guarded([&] {
+        PrgState s{*state};
+        if (dg) {
+            *infected = lt_forward_simulate(*static_cast<const DeviceGraph*>(dg), s);
+        } else {
+            SuspectSet vi = dense_suspects(G(g), p_of);
+            *infected = lt_forward_simulate(G(g), vi, s);
+        }
+        *state = s.state;
+    });
+}
+
+int hsawh_estimate_suspension(const void* dg, const void* g, const double* p_of, int kind,
+                              const uint32_t* ids, uint64_t nids, double eps, double delta,
+                              uint64_t* state, double* value, int* capped, uint64_t* runs) {
+    return guarded([&] {
+        RemovalSet r;
+        r.kind = kind == 0 ? ItemKind::Edge : ItemKind::Node;
+        r.ids.assign(ids, ids + nids);
+        PrgState s{*state};
+        SuspensionEstimate e;
+        if (dg) {
+            e = estimate_suspension(*static_cast<const DeviceGraph*>(dg), r, eps, delta, s);
+        } else {
+            SuspectSet vi = dense_suspects(G(g), p_of);
+            e = estimate_suspension(G(g), vi, r, eps, delta, s);
+        }
+        *state = s.state;
+        *value = e.value;
+        *capped = e.capped ? 1 : 0;
+        *runs = e.runs;
+    });
+}
+
 int hsawh_run_cli(int argc, const char** argv) {
     return run_cli(std::vector<std::string>(argv, argv + argc));
 }

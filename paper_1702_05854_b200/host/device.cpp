@@ -362,3 +362,74 @@ GreedyResult greedy_max_cover(const CoverageIndex& idx, std::uint32_t k) {
 }
 
 }  // namespace hsaw
+
+// ---- evaluation: paired forward simulation (proj/src/evaluation.cpp:195-242) ---------------------
+namespace hsaw {
+
+namespace {
+void raise_eval(int status, hsaw_gpu_ctx* ctx) {  // the reference's own messages, unprefixed
+    if (status == HSAW_OK) return;
+    std::string msg = hsaw_gpu_last_error(ctx);
+    switch (status) {
+        case HSAW_EINVAL: throw std::invalid_argument(msg);
+        case HSAW_EDATA: throw DataError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+int kind_code(ItemKind k) { return k == ItemKind::Edge ? HSAW_KIND_EDGE : HSAW_KIND_NODE; }
+}  // namespace
+
+void RemovalSet::validate(const ProbGraph& g) const {
+    std::uint32_t limit = kind == ItemKind::Edge ? g.m : g.n;
+    for (std::uint32_t id : ids)
+        if (id >= limit) throw DataError("removal id out of range: " + std::to_string(id));
+}
+
+std::uint32_t lt_forward_simulate(const DeviceGraph& dg, PrgState& s) {
+    std::uint32_t full = 0;
+    raise_eval(hsaw_gpu_paired_runs(dg.ctx(), -1, nullptr, 0, &s.state, 1, &full, nullptr), dg.ctx());
+    return full;
+}
+
+std::uint32_t lt_forward_simulate(const ProbGraph& g, const SuspectSet& vi, PrgState& s) {
+    DeviceGraph dg(g, vi);
+    return lt_forward_simulate(dg, s);
+}
+
+PairedRuns paired_runs(const DeviceGraph& dg, const RemovalSet& removal, std::uint64_t runs,
+                       PrgState& s) {
+    PairedRuns out;
+    out.full.resize(runs);
+    out.residual.resize(runs);
+    raise_eval(hsaw_gpu_paired_runs(dg.ctx(), kind_code(removal.kind), removal.ids.data(),
+                                    removal.ids.size(), &s.state, runs, out.full.data(),
+                                    out.residual.data()),
+               dg.ctx());
+    return out;
+}
+
+SuspensionEstimate estimate_suspension(const DeviceGraph& dg, const RemovalSet& removal,
+                                       double epsilon, double delta, PrgState& s) {
+    SuspensionEstimate e;
+    int capped = 0;
+    raise_eval(hsaw_gpu_estimate_suspension(dg.ctx(), kind_code(removal.kind), removal.ids.data(),
+                                            removal.ids.size(), epsilon, delta, &s.state, &e.value,
+                                            &capped, &e.runs),
+               dg.ctx());
+    e.capped = capped != 0;
+    return e;
+}
+
+SuspensionEstimate estimate_suspension(const ProbGraph& g, const SuspectSet& vi,
+                                       const RemovalSet& removal, double epsilon, double delta,
+                                       PrgState& s) {
+    // argument checks before any device work, in the reference's order (evaluation.cpp:214-218)
+    if (!(epsilon > 0.0) || epsilon >= 1.0) throw std::invalid_argument("epsilon must be in (0,1)");
+    if (!(delta > 0.0) || delta >= 1.0) throw std::invalid_argument("delta must be in (0,1)");
+    removal.validate(g);
+    if (removal.ids.empty()) return {0.0, false, 0};
+    DeviceGraph dg(g, vi);
+    return estimate_suspension(dg, removal, epsilon, delta, s);
+}
+
+}  // namespace hsaw

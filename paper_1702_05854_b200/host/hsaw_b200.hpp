@@ -18,6 +18,8 @@
 //   coverage.hpp     CoverageIndex, GreedyResult, greedy_max_cover, Schedule, ln_choose,
 //                    compute_schedule(_m), CheckResult, check_solution
 //   interdiction.hpp InterdictionResult, InterdictionOptions, esia, nsia, to_json
+//   evaluation.hpp   RemovalSet, SuspensionEstimate, lt_forward_simulate, estimate_suspension
+//                    (the paired forward simulation; baselines / brute force are out of scope)
 //   cli.hpp          run_cli
 #pragma once
 
@@ -360,6 +362,36 @@ InterdictionResult nsia(const DeviceGraph& dg, const ProbGraph& g, const Candida
                         const InterdictionOptions& opts = {});
 
 std::string to_json(const InterdictionResult& r, bool include_timing = true);
+
+// ---- evaluation (proj/include/hsaw/evaluation.hpp:16-39) ----------------------------------------
+// The step after the path: forward LT simulation of a removal set, paired runs on the original and
+// the residual graph sharing one realisation. Every run executes on the device
+// (hsaw_gpu_paired_runs / hsaw_gpu_estimate_suspension) and reproduces the reference's single
+// sequential PRG stream bit for bit; `s` is advanced exactly as the reference advances it.
+struct RemovalSet {
+    ItemKind kind = ItemKind::Edge;
+    std::vector<std::uint32_t> ids;
+    void validate(const ProbGraph& g) const;  // throws DataError("removal id out of range: ...")
+};
+struct SuspensionEstimate {
+    double value = 0;
+    bool capped = false;  // draw cap hit before the stopping rule fired
+    std::uint64_t runs = 0;
+};
+std::uint32_t lt_forward_simulate(const DeviceGraph& dg, PrgState& s);
+std::uint32_t lt_forward_simulate(const ProbGraph& g, const SuspectSet& vi, PrgState& s);
+SuspensionEstimate estimate_suspension(const DeviceGraph& dg, const RemovalSet& removal,
+                                       double epsilon, double delta, PrgState& s);
+SuspensionEstimate estimate_suspension(const ProbGraph& g, const SuspectSet& vi,
+                                       const RemovalSet& removal, double epsilon, double delta,
+                                       PrgState& s);
+// The paired runs themselves (not in the reference's interface; its loop body,
+// proj/src/evaluation.cpp:233-236): infected counts of `runs` consecutive runs.
+struct PairedRuns {
+    std::vector<std::uint32_t> full, residual;
+};
+PairedRuns paired_runs(const DeviceGraph& dg, const RemovalSet& removal, std::uint64_t runs,
+                       PrgState& s);
 
 // ---- cli (proj/include/hsaw/cli.hpp) ------------------------------------------------------------
 int run_cli(std::vector<std::string> args);

@@ -68,6 +68,9 @@ def lib() -> C.CDLL:
                                   C.c_double, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int,
                                   C.POINTER(Result), u32p, C.c_char_p, C.c_uint64]
     L.hsawh_sample.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p]
+    L.hsawh_lt_forward_simulate.argtypes = [vp, vp, f64p, u64p, u32p]
+    L.hsawh_estimate_suspension.argtypes = [vp, vp, f64p, C.c_int, u32p, C.c_uint64, C.c_double,
+                                            C.c_double, u64p, f64p, C.POINTER(C.c_int), u64p]
     L.hsawh_stream_samples.argtypes = [vp, f64p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, vpp]
     L.hsawh_pool_stats.argtypes = [vp, u64p, u64p, u64p]
     L.hsawh_pool_stats.restype = None
@@ -220,8 +223,8 @@ class DeviceGraph:
 
     def stage_times(self, reset=False) -> dict:
         from . import capi
-        ms = np.zeros(8, dtype=np.float64)
-        cnt = np.zeros(8, dtype=np.uint64)
+        ms = np.zeros(len(capi.STAGE_NAMES), dtype=np.float64)
+        cnt = np.zeros(len(capi.STAGE_NAMES), dtype=np.uint64)
         rc = capi.lib().hsaw_gpu_stage_times(self.ctx_handle(), _p(ms, f64p), _p(cnt, u64p),
                                              int(reset))
         if rc:
@@ -264,6 +267,28 @@ def interdict(graph: Graph, p_of, kind, k, eps, delta, seed=0, cand=None, batch_
         out["timing"] = dict(wall_time_s=res.wall_time_s, sample_s=res.sample_s,
                              greedy_s=res.greedy_s, check_s=res.check_s)
     return out
+
+
+def lt_forward_simulate(graph: Graph, p_of, state, dg: DeviceGraph | None = None):
+    """hsaw::lt_forward_simulate(g, vi, s) -> (infected, state_after)."""
+    p = np.ascontiguousarray(p_of, dtype=np.float64)
+    s, out = C.c_uint64(state), C.c_uint32()
+    _chk(lib().hsawh_lt_forward_simulate(dg.h if dg is not None else None, graph.h, _p(p, f64p),
+                                         C.byref(s), C.byref(out)))
+    return int(out.value), s.value
+
+
+def estimate_suspension(graph: Graph, p_of, kind, ids, eps, delta, state,
+                        dg: DeviceGraph | None = None) -> dict:
+    """hsaw::estimate_suspension(g, vi, removal, eps, delta, s) -> dict(value, capped, runs, state)."""
+    p = np.ascontiguousarray(p_of, dtype=np.float64)
+    a = np.ascontiguousarray(ids, dtype=np.uint32)
+    buf = a if a.size else np.zeros(1, dtype=np.uint32)
+    s, v, cp, runs = C.c_uint64(state), C.c_double(), C.c_int(), C.c_uint64()
+    _chk(lib().hsawh_estimate_suspension(dg.h if dg is not None else None, graph.h, _p(p, f64p),
+                                         kind, _p(buf, u32p), a.size, eps, delta, C.byref(s),
+                                         C.byref(v), C.byref(cp), C.byref(runs)))
+    return dict(value=v.value, capped=bool(cp.value), runs=int(runs.value), state=s.value)
 
 
 def stream_samples(graph: Graph, p_of, target, seed=0, batch_size=10, max_attempts=100_000_000):
