@@ -54,6 +54,8 @@ def parse_args():
     ap.add_argument("--solver", default="esia", choices=["esia", "nsia"],
                     help="interdiction driver timed beside the sampler (edge or node candidates)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-suspension", action="store_true",
+                    help="skip the forward-simulation leg (estimate_suspension of the solution)")
     ap.add_argument("--no-l2-flush", action="store_true",
                     help="A/B only: skip the L2 flush between timed steps")
     ap.add_argument("--cpu-target", type=int, default=300_000,
@@ -427,6 +429,64 @@ def run_b200(args):
             }
         except Exception as exc:  # e.g. the walk pool of a huge instance outgrowing HBM
             out[args.solver] = {"k": args.esia_k, "error": str(exc)[:300]}
+
+    # ---- the step after the path: paired LT forward simulation of the solution
+    # just found, on the same resident graph. Informational; not part of `value`.
+    if (not args.no_esia and not args.no_suspension and world == 1
+            and isinstance(out.get(args.solver), dict) and "error" not in out[args.solver]):
+        try:
+            kind = 0 if args.solver == "esia" else 1
+            sol = np.asarray(r_dev["solution"], dtype=np.uint32)
+            members = int(np.count_nonzero(p_of))
+            nruns = int(max(8, min(256, (1 << 27) // (g.n + members))))
+            ctx.paired_runs(kind, sol, 7, min(nruns, 8))  # warm-up: tables, scratch
+            ctx.stage_times(reset=True)
+            t0 = time.perf_counter()
+            full, res, _ = ctx.paired_runs(kind, sol, 7, nruns)
+            wall = time.perf_counter() - t0
+            sim_ms, _ = ctx.stage_times(reset=True)["simulate"]
+            t0 = time.perf_counter()
+            est = ctx.estimate_suspension(kind, sol, 0.1, 0.1, 7)
+            est_s = time.perf_counter() - t0
+            out["suspension"] = {
+                "call": "hsaw_gpu_paired_runs / hsaw_gpu_estimate_suspension on the solution "
+                        "(proj/src/evaluation.cpp:209-242), graph resident",
+                "runs_timed": nruns, "draws_per_run": g.n + members,
+                "paired_runs_per_sec": nruns / wall,
+                "draws_per_sec_device": nruns * (g.n + members) / (sim_ms / 1e3),
+                "device_ms_per_run": sim_ms / nruns,
+                "mean_full": float(full.mean()), "mean_residual": float(res.mean()),
+                "estimate": {"epsilon": 0.1, "delta": 0.1, "value": est["value"],
+                             "capped": est["capped"], "runs": est["runs"], "seconds": est_s},
+            }
+            if rank == 0 and not args.no_cpu_baseline:
+                from oracle import oracle
+                from oracle.oracle import Csr
+                off, src, cum, _, _ = g.arrays()
+                csr = Csr(g.n, g.m, off, src, cum, p_of)
+                cpu_runs = 3
+                if oracle.have_ref():
+                    R = oracle.Ref()
+                    with R.handles(csr) as hd:
+                        t0, s_ = time.perf_counter(), 7
+                        for _ in range(cpu_runs):
+                            _, s_ = R.lt_forward_simulate(csr, s_, hd=hd)
+                        dt = time.perf_counter() - t0
+                    cpu_kind = "reference"
+                else:
+                    P = oracle.Port()
+                    t0, s_ = time.perf_counter(), 7
+                    for _ in range(cpu_runs):
+                        _, s_ = P.lt_forward_simulate(csr, s_)
+                    dt = time.perf_counter() - t0
+                    cpu_kind = "port"
+                out["suspension"]["cpu_baseline"] = {
+                    "runs_per_sec": cpu_runs / dt, "cores": 1, "kind": cpu_kind,
+                    "sample": f"{cpu_runs} x lt_forward_simulate (one realisation + one count; a "
+                              f"paired run does two counts), single-threaded like the reference",
+                }
+        except Exception as exc:
+            out["suspension"] = {"error": str(exc)[:300]}
 
     # ---- N > 1: the sharded solve (walks sharded by batch range, marginal-gain counts combined
     # over NCCL; paper_1702_05854_b200/sharded.py). Every rank runs it; device-timed, max over ranks.

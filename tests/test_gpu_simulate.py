@@ -177,3 +177,66 @@ def test_full_size_runs_match_oracle(gpu_lib, port, monkeypatch):
         assert np.array_equal(full[2:], f2) and np.array_equal(res[2:], r2) and e2 == end
         same, same_res, _ = ctx.paired_runs(0, np.zeros(0, dtype=np.uint32), st, 3)
         assert np.array_equal(same, full[:3]) and np.array_equal(same_res, same)
+
+
+def _two_node():  # proj/tests/oracles.hpp:130-137
+    from oracle.oracle import Csr
+    return Csr(2, 1, np.array([0, 1, 1], dtype=np.uint64), np.array([1], dtype=np.uint32),
+               np.array([0.5]), np.array([0.0, 1.0]))
+
+
+def test_reference_test_cases(ctx, port):  # proj/tests/test_evaluation.cpp:13-66
+    from oracle.oracle import Csr
+    chain = Csr(3, 2, np.array([0, 0, 1, 2], dtype=np.uint64), np.array([0, 1], dtype=np.uint32),
+                np.array([1.0, 1.0]), np.array([1.0, 0.0, 0.0]))
+    upload(ctx, chain)
+    full, _, _ = ctx.paired_runs(-1, None, 3, 100)
+    assert np.all(full == 3)  # "deterministic chain infects everyone"
+    from paper_1702_05854_b200 import rmat
+    g = rmat.uniform_graph(30, 3, seed=1, suspect_count=1)
+    g.p_of[:] = 0.0  # "no suspects, no infection": a run is n draws, no member draws
+    upload(ctx, make_csr(g))
+    full, _, after = ctx.paired_runs(-1, None, 5, 100)
+    assert np.all(full == 0)
+    assert after == port.paired_runs(make_csr(g), 0, [], 5, 100)[2]
+    two = _two_node()
+    upload(ctx, two)
+    runs = 1_000_000  # "two-node mean tends to 1.5", all runs in one call
+    full, _, after = ctx.paired_runs(-1, None, 11, runs)
+    assert abs(full.mean() - 1.5) < 0.0075
+    want = port.paired_runs(two, 0, [], 11, runs)
+    assert np.array_equal(full, want[0]) and after == want[2]
+    for kind, ids, truth in ((0, [0], 0.5), (1, [1], 1.5), (1, [0], 0.5)):
+        e = ctx.estimate_suspension(kind, ids, 0.05, 0.05, 21)
+        assert abs(e["value"] - truth) / truth < 0.05
+        assert e == port.estimate_suspension(two, kind, ids, 0.05, 0.05, 21)
+
+
+def test_host_layer_signatures(eval_golden, synth3000):
+    """hsaw::lt_forward_simulate / estimate_suspension of the C++ host layer, both the reference
+    signatures (g, vi, ...) and the DeviceGraph overloads."""
+    from paper_1702_05854_b200 import hostapi
+    g = hostapi.Graph.from_csr(synth3000.n, synth3000.m, synth3000.in_offsets, synth3000.in_src,
+                               synth3000.in_cum)
+    gold = eval_golden["synth3000"]
+    f = gold["lt_forward_simulate"]
+    with hostapi.DeviceGraph(g, synth3000.p_of) as dg:
+        s, got = f["state0"], []
+        for _ in f["infected"]:
+            cnt, s = hostapi.lt_forward_simulate(g, synth3000.p_of, s, dg=dg)
+            got.append(cnt)
+        assert got == f["infected"] and s == f["state_after"]
+        for c in gold["estimate_suspension"][:4]:
+            e = hostapi.estimate_suspension(g, synth3000.p_of, c["kind"], c["ids"], c["epsilon"],
+                                            c["delta"], c["state0"], dg=dg)
+            assert e == dict(value=float.fromhex(c["value"]), capped=c["capped"], runs=c["runs"],
+                             state=c["state_after"])
+    cnt, s = hostapi.lt_forward_simulate(g, synth3000.p_of, f["state0"])
+    assert cnt == f["infected"][0]
+    c = gold["estimate_suspension"][2]
+    e = hostapi.estimate_suspension(g, synth3000.p_of, c["kind"], c["ids"], c["epsilon"],
+                                    c["delta"], c["state0"])
+    assert e["runs"] == c["runs"] and e["value"] == float.fromhex(c["value"])
+    with pytest.raises(hostapi.HsawError) as ei:
+        hostapi.estimate_suspension(g, synth3000.p_of, 0, [synth3000.m], 0.3, 0.2, 1)
+    assert ei.value.status == 2
