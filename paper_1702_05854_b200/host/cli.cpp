@@ -1,9 +1,10 @@
 // `hsaw` command line on the device path: the subcommands and flags of the reference CLI that sit
-// on the hot path (interdict, sample, bench, synth — /root/reference/proj/src/cli.cpp:400-485), the
+// on the hot path (interdict, sample, bench, synth, estimate — /root/reference/proj/src/cli.cpp:400-485), the
 // same JSON documents and the same exit codes (0 ok, 1 usage, 2 data, 3 runtime; cli.cpp:520-538).
 // The reference parses with CLI11 (not available here); this is a small flag parser with the same
 // spelling: `--name value` or `--name=value`. `--workers` is accepted and ignored (the GPU is the
-// worker pool); `--device N` is new. estimate / baseline / partition are outside the ported path.
+// worker pool); `--device N` is new. baseline / partition are outside the ported path.
+#include <charconv>
 #include <chrono>
 #include <cstdlib>
 #include <fstream>
@@ -162,6 +163,15 @@ std::string json_real(double x) {
     return s.str();
 }
 
+// nlohmann's number form: shortest round-trip, ".0" when integral (as to_json in solver.cpp)
+std::string json_shortest(double x) {
+    char buf[64];
+    auto res = std::to_chars(buf, buf + sizeof buf, x);
+    std::string s(buf, res.ptr);
+    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+    return s;
+}
+
 const std::set<std::string> kGraphFlags = {"graph", "weights", "suspects", "random-suspects"};
 
 std::set<std::string> with(std::set<std::string> base, std::initializer_list<const char*> more) {
@@ -231,6 +241,38 @@ int cmd_sample(const Flags& f) {  // cli.cpp:267-290
     return 0;
 }
 
+int cmd_estimate(const Flags& f) {  // cli.cpp:162-185
+    f.require("graph");
+    f.require("removal");
+    const std::uint64_t seed = f.u64("seed", 0);
+    ProbGraph g = load_graph(f, seed);
+    SuspectSet vi = load_suspect_args(f, g, seed);
+    const std::string mode = f.str("mode", "edge");
+    if (mode != "edge" && mode != "node") throw UsageError("--mode: expected edge|node");
+    RemovalSet removal;
+    removal.kind = mode == "edge" ? ItemKind::Edge : ItemKind::Node;
+    removal.ids = read_item_file(f.str("removal"), removal.kind, g);
+    removal.validate(g);
+    const double eps = f.real("epsilon", 0.1), delta = f.real("delta", 0.1);
+    PrgState s = seed_from_worker(seed);
+    SuspensionEstimate est;
+    // argument checks first, as the reference does before any simulation (evaluation.cpp:214-218)
+    if (!(eps > 0.0) || eps >= 1.0) throw std::invalid_argument("epsilon must be in (0,1)");
+    if (!(delta > 0.0) || delta >= 1.0) throw std::invalid_argument("delta must be in (0,1)");
+    if (!removal.ids.empty()) {
+        DeviceGraph dg(g, vi, static_cast<int>(f.u64("device", 0)));
+        est = estimate_suspension(dg, removal, eps, delta, s);
+    }
+    std::ostringstream j;  // nlohmann object: keys sorted, dump(2)
+    j << "{\n  \"capped\": " << (est.capped ? "true" : "false") << ",\n  \"delta\": "
+      << json_shortest(delta) << ",\n  \"epsilon\": " << json_shortest(eps) << ",\n  \"kind\": \""
+      << to_string(removal.kind) << "\",\n  \"removed\": " << removal.ids.size()
+      << ",\n  \"runs\": " << est.runs << ",\n  \"suspension\": " << json_shortest(est.value)
+      << "\n}";
+    emit(j.str(), f.str("output"));
+    return 0;
+}
+
 int cmd_synth(const Flags& f) {  // cli.cpp:335-348
     f.require("nodes");
     const std::uint64_t seed = f.u64("seed", 0);
@@ -274,10 +316,10 @@ int cmd_bench(const Flags& f) {  // cli.cpp:350-379, one device run instead of 1
 
 int run_cli(std::vector<std::string> args) {
     try {
-        if (args.empty()) throw UsageError("a subcommand is required: interdict|sample|synth|bench");
+        if (args.empty()) throw UsageError("a subcommand is required: interdict|sample|estimate|synth|bench");
         const std::string& cmd = args[0];
         if (cmd == "--help" || cmd == "-h") {
-            std::cout << "usage: hsaw interdict|sample|synth|bench [--flags]\n";
+            std::cout << "usage: hsaw interdict|sample|estimate|synth|bench [--flags]\n";
             return 0;
         }
         if (cmd == "interdict")
@@ -301,7 +343,12 @@ int run_cli(std::vector<std::string> args) {
                 with(kGraphFlags, {"synth-nodes", "synth-density", "target", "workers", "seed",
                                    "output", "device"}),
                 {}));
-        if (cmd == "estimate" || cmd == "baseline" || cmd == "partition")
+        if (cmd == "estimate")
+            return cmd_estimate(parse_flags(
+                args, 1,
+                with(kGraphFlags, {"mode", "removal", "epsilon", "delta", "seed", "output", "device"}),
+                {"symmetrize"}));
+        if (cmd == "baseline" || cmd == "partition")
             throw UsageError("subcommand '" + cmd +
                              "' is outside the device hot path (use the reference build)");
         throw UsageError("unknown subcommand '" + cmd + "'");

@@ -240,3 +240,39 @@ def test_host_layer_signatures(eval_golden, synth3000):
     with pytest.raises(hostapi.HsawError) as ei:
         hostapi.estimate_suspension(g, synth3000.p_of, 0, [synth3000.m], 0.3, 0.2, 1)
     assert ei.value.status == 2
+
+
+def test_cli_estimate(tmp_path, fixture12, eval_golden, golden):
+    """`hsaw estimate` (proj/src/cli.cpp:162-185): same JSON document as the reference prints."""
+    from paper_1702_05854_b200 import hostapi
+    fx = golden["fixture12_given"]
+    edges = tmp_path / "f12.edges"
+    with open(edges, "w") as f:
+        for e in range(fx["m"]):
+            f.write(f"{fx['in_src'][e]} {fx['edge_dst'][e]} {float.fromhex(fx['weight'][e])!r}\n")
+    sus = tmp_path / "f12.suspects"
+    with open(sus, "w") as f:
+        for v, p in enumerate(fixture12.p_of):
+            if p:
+                f.write(f"{v} {float(p)!r}\n")
+    rem = tmp_path / "removal.txt"
+    ids = [1, 5, 7]
+    rem.write_text("".join(f"{i}\n" for i in ids))
+    out = tmp_path / "est.json"
+    rc = hostapi.run_cli(["estimate", "--graph", str(edges), "--weights", "given", "--suspects",
+                          str(sus), "--mode", "edge", "--removal", str(rem), "--epsilon", "0.3",
+                          "--delta", "0.2", "--seed", "7", "--output", str(out)])
+    assert rc == 0
+    doc = json.loads(out.read_text())
+    # oracle: PrgState s = seed_from_worker(seed) (cli.cpp:173)
+    from oracle.oracle import Port
+    P = Port()
+    want = P.estimate_suspension(fixture12, 0, ids, 0.3, 0.2, P.seed_from_worker(7))
+    assert doc == dict(kind="edge", removed=3, epsilon=0.3, delta=0.2, suspension=want["value"],
+                       capped=want["capped"], runs=want["runs"])
+    assert list(doc) == sorted(doc)  # nlohmann object order
+    assert hostapi.run_cli(["estimate", "--graph", str(edges), "--weights", "given", "--suspects",
+                            str(sus), "--removal", str(rem), "--epsilon", "1.5"]) == 1
+    rem.write_text("999\n")
+    assert hostapi.run_cli(["estimate", "--graph", str(edges), "--weights", "given", "--suspects",
+                            str(sus), "--removal", str(rem)]) == 2
