@@ -94,6 +94,22 @@ int hsaw_gpu_csr_build(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_
 int hsaw_gpu_graph_build_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t* edge_u,
                                 const uint32_t* edge_v, const double* edge_w, int weight_mode,
                                 const double* p_of);
+
+/* Binary ingest: the HSAW1 cache format (save_cache / load_cache, proj/src/graph.cpp:383-430).
+ * `body` points at the bytes that follow the 21-byte header ("HSAW1", n, m as LE u64): (n + 1) u64
+ * offsets, m u64-widened sources, m f64 bit patterns, all little endian, as they lie in the file
+ * (any alignment). The device decodes them, runs load_cache's sequential per-row cumulative sums
+ * (:417-424) and the checks of ProbGraph::validate() (:70-104, HSAW_EDATA with the reference's
+ * message for the first offending row).
+ * hsaw_gpu_cache_decode returns the ProbGraph arrays (out_weight / out_edge_dst nullable);
+ * hsaw_gpu_graph_cache_upload installs the graph on the device without any host CSR (p_of NULL =
+ * no suspects yet; hsaw_gpu_suspects_upload sets them later). */
+int hsaw_gpu_cache_decode(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const void* body,
+                          uint64_t* out_in_offsets, uint32_t* out_in_src, double* out_in_cum,
+                          double* out_weight, uint32_t* out_edge_dst);
+int hsaw_gpu_graph_cache_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const void* body,
+                                const double* p_of);
+
 /* Same, but p_of replaced later without re-uploading the CSR (new SuspectSet on the same graph). */
 int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of);
 /* Bytes of device memory held by the uploaded graph. */

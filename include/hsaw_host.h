@@ -57,6 +57,13 @@ int hsawh_device_create(const void* g, const double* p_of, int device, void* cud
 void hsawh_device_free(void* dg);
 void* hsawh_device_ctx(const void* dg); /* the hsaw_gpu_ctx* underneath */
 
+/* Binary ingest on the device (graph.hpp:139-141 load_cache): hsaw::load_cache_device returns the
+ * same ProbGraph as load_cache; hsaw::DeviceGraph::from_cache goes file -> resident graph with no
+ * host CSR (no suspects until hsawh_device_set_suspects). */
+int hsawh_graph_load_cache_device(const char* path, int device, void** out);
+int hsawh_device_from_cache(const char* path, int device, void* cuda_stream, void** out);
+int hsawh_device_set_suspects(void* dg, const void* g, const double* p_of);
+
 /* ---- eSIA / nSIA — proj/include/hsaw/interdiction.hpp:37-47 ---- */
 typedef struct hsawh_result {
     uint32_t k, iterations;

@@ -78,6 +78,8 @@ def lib() -> C.CDLL:
                                      u32p, f64p, f64p, u32p]
     L.hsaw_gpu_graph_build_upload.argtypes = [vp, C.c_uint32, C.c_uint64, u32p, u32p, f64p,
                                               C.c_int, f64p]
+    L.hsaw_gpu_cache_decode.argtypes = [vp, C.c_uint32, C.c_uint32, vp, u64p, u32p, f64p, f64p, u32p]
+    L.hsaw_gpu_graph_cache_upload.argtypes = [vp, C.c_uint32, C.c_uint32, vp, f64p]
     L.hsaw_gpu_graph_bytes.argtypes = [vp]
     L.hsaw_gpu_graph_bytes.restype = C.c_uint64
     L.hsaw_gpu_launch_count.argtypes = [vp]
@@ -143,6 +145,7 @@ EXPORTS = (
     "hsaw_gpu_rounds_begin", "hsaw_gpu_rounds_occurrences", "hsaw_gpu_rounds_select",
     "hsaw_gpu_rounds_cover", "hsaw_gpu_rounds_apply", "hsaw_gpu_rounds_end",
     "hsaw_gpu_paired_runs", "hsaw_gpu_estimate_suspension",
+    "hsaw_gpu_cache_decode", "hsaw_gpu_graph_cache_upload",
 )
 
 
@@ -270,6 +273,40 @@ class Context:
         assert p_of.shape == (n,)
         self._chk(self.L.hsaw_gpu_graph_upload(self.h, n, m, _p(in_offsets, u64p),
                                                _p(in_src, u32p), _p(in_cum, f64p), _p(p_of, f64p)))
+        self.n, self.m = n, m
+
+    @staticmethod
+    def _cache_header(image: bytes):
+        """(n, m) from an HSAW1 image (graph.cpp:398-405); the host layer owns the file errors."""
+        if len(image) < 21 or image[:5] != b"HSAW1":
+            raise HsawError(HSAW_EDATA, "bad cache magic")
+        n = int.from_bytes(image[5:13], "little") & 0xFFFFFFFF
+        m = int.from_bytes(image[13:21], "little") & 0xFFFFFFFF
+        if len(image) < 21 + 8 * (n + 1 + 2 * m):
+            raise HsawError(HSAW_EDATA, "truncated cache")
+        return n, m
+
+    def decode_cache(self, image: bytes, aux=True):
+        """load_cache on the device: (in_offsets, in_src, in_cum, weight, edge_dst) host arrays."""
+        n, m = self._cache_header(image)
+        buf = np.frombuffer(image, dtype=np.uint8)
+        off = np.zeros(n + 1, dtype=np.uint64)
+        src = np.zeros(max(m, 1), dtype=np.uint32)
+        cum = np.zeros(max(m, 1), dtype=np.float64)
+        wt = np.zeros(max(m, 1), dtype=np.float64) if aux else None
+        dst = np.zeros(max(m, 1), dtype=np.uint32) if aux else None
+        self._chk(self.L.hsaw_gpu_cache_decode(
+            self.h, n, m, C.c_void_p(buf.ctypes.data + 21), _p(off, u64p), _p(src, u32p),
+            _p(cum, f64p), _p(wt, f64p) if aux else None, _p(dst, u32p) if aux else None))
+        return off, src[:m], cum[:m], (wt[:m] if aux else None), (dst[:m] if aux else None)
+
+    def upload_cache(self, image: bytes, p_of=None):
+        """HSAW1 image -> graph resident and ready to sample, no host CSR."""
+        n, m = self._cache_header(image)
+        buf = np.frombuffer(image, dtype=np.uint8)
+        p = None if p_of is None else np.ascontiguousarray(p_of, dtype=np.float64)
+        self._chk(self.L.hsaw_gpu_graph_cache_upload(self.h, n, m, C.c_void_p(buf.ctypes.data + 21),
+                                                     _p(p, f64p) if p is not None else None))
         self.n, self.m = n, m
 
     def build_csr(self, n, edge_u, edge_v, edge_w=None, weight_mode=1, aux=True):

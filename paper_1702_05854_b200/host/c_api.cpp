@@ -265,6 +265,21 @@ void hsawh_pool_copy(const void* pool, uint64_t* edge_off, uint32_t* nodes, uint
 
 void hsawh_pool_free(void* pool) { delete static_cast<SamplePool*>(pool); }
 
+int hsawh_graph_load_cache_device(const char* path, int device, void** out) {
+    return guarded([&] { *out = new ProbGraph(load_cache_device(path, device)); });
+}
+
+int hsawh_device_from_cache(const char* path, int device, void* cuda_stream, void** out) {
+    return guarded([&] { *out = DeviceGraph::from_cache(path, device, cuda_stream).release(); });
+}
+
+int hsawh_device_set_suspects(void* dg, const void* g, const double* p_of) {
+    return guarded([&] {
+        SuspectSet vi = dense_suspects(G(g), p_of);
+        static_cast<DeviceGraph*>(dg)->set_suspects(vi);
+    });
+}
+
 int hsawh_lt_forward_simulate(const void* dg, const void* g, const double* p_of, uint64_t* state,
                               uint32_t* infected) {
     return guarded([&] {

@@ -102,7 +102,9 @@ ProbGraph load_graph(const Flags& f, std::uint64_t seed) {
     {
         std::ifstream probe(path, std::ios::binary);
         char magic[5] = {};
-        if (probe.read(magic, 5) && std::string(magic, 5) == "HSAW1") return load_cache(path);
+        // binary caches are decoded, summed and validated on the device (same ProbGraph, same errors)
+        if (probe.read(magic, 5) && std::string(magic, 5) == "HSAW1")
+            return load_cache_device(path, static_cast<int>(f.u64("device", 0)));
     }
     LoadOptions opts;
     opts.symmetrize = f.switches.count("symmetrize") != 0;

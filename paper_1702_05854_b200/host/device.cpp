@@ -2,7 +2,13 @@
 // include/hsaw_gpu.h and rethrows its status codes as the exception types the reference uses
 // (std::invalid_argument / DataError / SamplingError / std::out_of_range), so callers and the CLI
 // keep the reference's error behaviour (proj/src/cli.cpp:520-538).
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <cstring>
 
 #include "hsaw_b200.hpp"
 #include "hsaw_gpu.h"
@@ -88,6 +94,104 @@ ProbGraph build_graph_device(NodeId n, const std::vector<std::tuple<NodeId, Node
     }
     return build_graph_device(n, edges.size(), u.data(), v.data(),
                               mode == WeightMode::Given ? w.data() : nullptr, mode, device);
+}
+
+// ---- binary ingest on the device -------------------------------------------------------------------
+namespace {
+
+// The HSAW1 file mapped read-only; header checks with load_cache's own messages
+// (proj/src/graph.cpp:398-416: "cannot open cache", "bad cache magic in", "truncated cache").
+struct MappedCache {
+    void* base = MAP_FAILED;
+    std::size_t bytes = 0;
+    NodeId n = 0;
+    EdgeId m = 0;
+    const unsigned char* body = nullptr;
+
+    explicit MappedCache(const std::string& path) {
+        int fd = ::open(path.c_str(), O_RDONLY);
+        if (fd < 0) throw DataError("cannot open cache: " + path);
+        struct stat st {};
+        if (::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode)) {
+            ::close(fd);
+            throw DataError("cannot open cache: " + path);
+        }
+        bytes = static_cast<std::size_t>(st.st_size);
+        if (bytes) base = ::mmap(nullptr, bytes, PROT_READ, MAP_PRIVATE, fd, 0);
+        ::close(fd);
+        const auto* b = static_cast<const unsigned char*>(base);
+        if (base == MAP_FAILED || bytes < 5 || std::memcmp(b, "HSAW1", 5) != 0) {
+            unmap();
+            throw DataError("bad cache magic in " + path);
+        }
+        auto le64 = [&](std::size_t at) {
+            std::uint64_t x = 0;
+            for (int i = 0; i < 8; ++i)
+                x |= static_cast<std::uint64_t>(at + i < bytes ? b[at + i] : 0xFF) << (8 * i);
+            return x;
+        };
+        n = static_cast<NodeId>(le64(5));   // static_cast<NodeId>(get_u64(f)), graph.cpp:403
+        m = static_cast<EdgeId>(le64(13));
+        const std::uint64_t need = 21 + 8 * (static_cast<std::uint64_t>(n) + 1 + 2ull * m);
+        if (bytes < need) {
+            unmap();
+            throw DataError("truncated cache: " + path);
+        }
+        ::madvise(base, bytes, MADV_SEQUENTIAL);
+        body = b + 21;
+    }
+    void unmap() {
+        if (base != MAP_FAILED) ::munmap(base, bytes);
+        base = MAP_FAILED;
+    }
+    ~MappedCache() { unmap(); }
+    MappedCache(const MappedCache&) = delete;
+    MappedCache& operator=(const MappedCache&) = delete;
+};
+
+}  // namespace
+
+ProbGraph load_cache_device(const std::string& path, int device) {
+    MappedCache file(path);
+    hsaw_gpu_ctx* ctx = nullptr;
+    if (hsaw_gpu_ctx_create(device, nullptr, &ctx) != HSAW_OK)
+        throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");
+    ProbGraph g;
+    g.n = file.n;
+    g.m = file.m;
+    g.in_offsets.resize(static_cast<std::size_t>(g.n) + 1);
+    g.in_src.resize(g.m);
+    g.in_cum.resize(g.m);
+    g.weight.resize(g.m);
+    g.edge_dst.resize(g.m);
+    int rc = hsaw_gpu_cache_decode(ctx, g.n, g.m, file.body, g.in_offsets.data(), g.in_src.data(),
+                                   g.in_cum.data(), g.weight.data(), g.edge_dst.data());
+    std::string msg = rc == HSAW_OK ? std::string() : std::string(hsaw_gpu_last_error(ctx));
+    hsaw_gpu_ctx_destroy(ctx);
+    if (rc == HSAW_EDATA) throw DataError(msg);  // validate()'s own messages, unprefixed
+    if (rc == HSAW_EINVAL) throw std::invalid_argument(msg);
+    if (rc != HSAW_OK) throw DeviceError(msg);
+    return g;
+}
+
+std::unique_ptr<DeviceGraph> DeviceGraph::from_cache(const std::string& path, int device,
+                                                     void* cuda_stream) {
+    MappedCache file(path);
+    std::unique_ptr<DeviceGraph> dg(new DeviceGraph());
+    if (hsaw_gpu_ctx_create(device, cuda_stream, &dg->ctx_) != HSAW_OK) {
+        dg->ctx_ = nullptr;
+        throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");
+    }
+    dg->n_ = file.n;
+    dg->m_ = file.m;
+    int rc = hsaw_gpu_graph_cache_upload(dg->ctx_, file.n, file.m, file.body, nullptr);
+    if (rc != HSAW_OK) {
+        std::string msg = hsaw_gpu_last_error(dg->ctx_);
+        if (rc == HSAW_EDATA) throw DataError(msg);
+        if (rc == HSAW_EINVAL) throw std::invalid_argument(msg);
+        throw DeviceError(msg);
+    }
+    return dg;
 }
 
 // ---- DeviceGraph --------------------------------------------------------------------------------

@@ -154,10 +154,19 @@ ProbGraph build_graph_device(NodeId n, const std::vector<std::tuple<NodeId, Node
 ProbGraph build_graph_device(NodeId n, std::uint64_t nedges, const NodeId* u, const NodeId* v,
                              const double* w, WeightMode mode, int device = 0);
 
+// load_cache (proj/include/hsaw/graph.hpp:139-141) with the decode, the per-row cumulative sums and
+// validate() on the GPU (hsaw_gpu_cache_decode): the file is mapped and shipped as it lies on disk.
+// Same ProbGraph bit for bit, same DataError messages.
+ProbGraph load_cache_device(const std::string& path, int device = 0);
+
 class DeviceGraph {
 public:
     DeviceGraph(const ProbGraph& g, const SuspectSet& vi, int device = 0,
                 void* cuda_stream = nullptr);
+    // HSAW1 cache file -> graph resident on the device, no host CSR (hsaw_gpu_graph_cache_upload).
+    // No suspects yet: call set_suspects() before sampling.
+    static std::unique_ptr<DeviceGraph> from_cache(const std::string& path, int device = 0,
+                                                   void* cuda_stream = nullptr);
     ~DeviceGraph();
     DeviceGraph(const DeviceGraph&) = delete;
     DeviceGraph& operator=(const DeviceGraph&) = delete;
@@ -172,6 +181,7 @@ public:
     std::vector<double> stage_ms(bool reset = false) const;
 
 private:
+    DeviceGraph() = default;
     hsaw_gpu_ctx* ctx_ = nullptr;
     NodeId n_ = 0;
     EdgeId m_ = 0;

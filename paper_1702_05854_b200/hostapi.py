@@ -68,6 +68,9 @@ def lib() -> C.CDLL:
                                   C.c_double, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int,
                                   C.POINTER(Result), u32p, C.c_char_p, C.c_uint64]
     L.hsawh_sample.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p]
+    L.hsawh_graph_load_cache_device.argtypes = [C.c_char_p, C.c_int, vpp]
+    L.hsawh_device_from_cache.argtypes = [C.c_char_p, C.c_int, vp, vpp]
+    L.hsawh_device_set_suspects.argtypes = [vp, vp, f64p]
     L.hsawh_lt_forward_simulate.argtypes = [vp, vp, f64p, u64p, u32p]
     L.hsawh_estimate_suspension.argtypes = [vp, vp, f64p, C.c_int, u32p, C.c_uint64, C.c_double,
                                             C.c_double, u64p, f64p, C.POINTER(C.c_int), u64p]
@@ -149,6 +152,11 @@ class Graph:
     def load_cache(cls, path):
         return cls._new(lib().hsawh_graph_load_cache, str(path).encode())
 
+    @classmethod
+    def load_cache_device(cls, path, device=0):
+        """hsaw::load_cache_device: load_cache with decode / sums / validate() on the GPU."""
+        return cls._new(lib().hsawh_graph_load_cache_device, str(path).encode(), device)
+
     def save_cache(self, path):
         _chk(lib().hsawh_graph_save_cache(self.h, str(path).encode()))
 
@@ -206,6 +214,21 @@ class DeviceGraph:
         _chk(lib().hsawh_device_create(graph.h, _p(self.p_of, f64p), device,
                                        C.c_void_p(cuda_stream) if cuda_stream else None,
                                        C.byref(self.h)))
+
+    @classmethod
+    def from_cache(cls, path, device=0, cuda_stream: int | None = None) -> "DeviceGraph":
+        """hsaw::DeviceGraph::from_cache: HSAW1 file -> resident graph, no host CSR, no suspects."""
+        self = cls.__new__(cls)
+        self.graph, self.p_of, self.h = None, None, C.c_void_p()
+        _chk(lib().hsawh_device_from_cache(str(path).encode(), device,
+                                           C.c_void_p(cuda_stream) if cuda_stream else None,
+                                           C.byref(self.h)))
+        return self
+
+    def set_suspects(self, graph: "Graph", p_of):
+        self.graph = graph
+        self.p_of = np.ascontiguousarray(p_of, dtype=np.float64)
+        _chk(lib().hsawh_device_set_suspects(self.h, graph.h, _p(self.p_of, f64p)))
 
     def close(self):
         if self.h:
