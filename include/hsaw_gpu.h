@@ -273,6 +273,12 @@ void hsaw_gpu_rounds_end(hsaw_gpu_rounds* g);
 int hsaw_gpu_paired_runs(hsaw_gpu_ctx* ctx, int kind, const uint32_t* removal_ids, uint64_t nids,
                          uint64_t* prg_state, uint64_t nruns, uint32_t* full, uint32_t* residual);
 
+/* PrgState::state after `draws` calls of prg_next (proj/include/hsaw/prng.hpp:41-48) without
+ * making them: the state update is linear over GF(2), so this is a 64x64 bit-matrix power applied
+ * to the state. Pure host arithmetic (no device needed); lets a caller address any run of a
+ * simulation stream directly, e.g. to shard the runs of hsaw_gpu_paired_runs over several GPUs. */
+uint64_t hsaw_gpu_prg_jump(uint64_t prg_state, uint64_t draws);
+
 /* estimate_suspension (evaluation.hpp:36-39, evaluation.cpp:209-242): stopping-rule estimate of
  * the influence suspension of a removal set. Same argument checks and order (HSAW_EINVAL for
  * epsilon/delta outside (0,1), HSAW_EDATA for a bad id), same early return for an empty set, same

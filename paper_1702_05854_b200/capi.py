@@ -122,6 +122,8 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_rounds_end.argtypes = [vp]
     L.hsaw_gpu_rounds_end.restype = None
     L.hsaw_gpu_paired_runs.argtypes = [vp, C.c_int, u32p, C.c_uint64, u64p, C.c_uint64, u32p, u32p]
+    L.hsaw_gpu_prg_jump.argtypes = [C.c_uint64, C.c_uint64]
+    L.hsaw_gpu_prg_jump.restype = C.c_uint64
     L.hsaw_gpu_estimate_suspension.argtypes = [vp, C.c_int, u32p, C.c_uint64, C.c_double,
                                                C.c_double, u64p, f64p, C.POINTER(C.c_int), u64p]
     _LIB = L
@@ -145,8 +147,13 @@ EXPORTS = (
     "hsaw_gpu_rounds_begin", "hsaw_gpu_rounds_occurrences", "hsaw_gpu_rounds_select",
     "hsaw_gpu_rounds_cover", "hsaw_gpu_rounds_apply", "hsaw_gpu_rounds_end",
     "hsaw_gpu_paired_runs", "hsaw_gpu_estimate_suspension",
-    "hsaw_gpu_cache_decode", "hsaw_gpu_graph_cache_upload",
+    "hsaw_gpu_cache_decode", "hsaw_gpu_graph_cache_upload", "hsaw_gpu_prg_jump",
 )
+
+
+def prg_jump(state: int, draws: int) -> int:
+    """PrgState.state after `draws` xorshift64* steps (GF(2) jump-ahead; host arithmetic only)."""
+    return int(lib().hsaw_gpu_prg_jump(state, draws))
 
 
 def alloc_counters() -> dict:

@@ -184,6 +184,14 @@ class GpuEngine:
         return self.ctx.coverage_upper_bound(k, stream=self.stream, kind=kind, off=off, cnt=cnt,
                                              cand=cand)
 
+    def paired_runs(self, kind, ids, state0, first_run, nruns, draws_per_run):
+        """Runs [first_run, first_run + nruns) of the simulation stream that starts at state0."""
+        if nruns == 0:
+            return np.zeros(0, dtype=np.uint32), np.zeros(0, dtype=np.uint32)
+        s = self.capi.prg_jump(state0, first_run * draws_per_run)
+        full, res, _ = self.ctx.paired_runs(kind, ids, s, nruns)
+        return full, res
+
     class _Rounds:
         def __init__(self, eng, kind, off, cnt, cand):
             self.eng = eng
@@ -337,6 +345,64 @@ class ShardedSolver:
         return solution, coverage
 
     # -- run_interdiction (proj/src/interdiction.cpp:12-67), sharded
+    # ---- estimate_suspension (proj/src/evaluation.cpp:209-242), runs sharded over the ranks -------
+    def estimate_suspension(self, n_nodes: int, members: int, kind: int, ids, eps: float,
+                            delta: float, state: int, batch_runs: int | None = None) -> dict:
+        """Paired forward simulation with each device batch of runs split into `world` contiguous
+        run ranges (every run is addressed by its stream position, capi.prg_jump). Exchange step:
+        one all-gather of the per-run (full, residual) counts per batch; every rank then replays
+        the reference's FP64 accumulation in run order, so value / capped / runs / state are the
+        single-GPU (and reference) results for every world size."""
+        import math
+
+        from . import capi
+        if not (eps > 0.0) or eps >= 1.0:
+            raise HsawError(HSAW_EINVAL, "epsilon must be in (0,1)")
+        if not (delta > 0.0) or delta >= 1.0:
+            raise HsawError(HSAW_EINVAL, "delta must be in (0,1)")
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        limit = self.eng.limit(kind)
+        for x in ids.tolist():
+            if x >= limit:
+                raise HsawError(HSAW_EDATA, f"removal id out of range: {x}")
+        if ids.size == 0:
+            return dict(value=0.0, capped=False, runs=0, state=state)
+        upsilon = 4.0 * (math.exp(1.0) - 2.0) * math.log(2.0 / delta) * (1.0 + eps) / (eps * eps)
+        d = members + n_nodes
+        max_runs = max(1, 1_000_000_000 // d)
+        cap = batch_runs or max(self.comm.world, (self.comm.world << 25) // d)
+        total, runs, capped = 0.0, 0, False
+        while total < upsilon:
+            if runs >= max_runs:
+                capped = True
+                break
+            want = 64 * self.comm.world
+            if runs:
+                want = 2 * runs
+                if total > 0.0:
+                    want = int((upsilon - total) / (total / runs) * 1.05) + 16
+            b = max(1, min(cap, max(want, 16), max_runs - runs))
+            sizes = Layout.split(0, b, self.comm.world)
+            first = runs + sum(sizes[: self.comm.rank])
+            full, res = self.eng.paired_runs(kind, ids, state, first, sizes[self.comm.rank], d)
+            mine = torch.from_numpy(np.stack([full, res]).astype(np.int64).reshape(-1))
+            parts = self.comm.allgather_var(mine.to(self._exchange_device()))
+            for part in parts:  # rank order = run order
+                fr = part.cpu().numpy().reshape(2, -1)
+                for f, r in zip(fr[0].tolist(), fr[1].tolist()):
+                    if not total < upsilon:
+                        break
+                    total += float(f - r) / float(n_nodes)
+                    runs += 1
+        out_state = capi.prg_jump(state, runs * d)
+        if capped:
+            return dict(value=0.0, capped=True, runs=runs, state=out_state)
+        return dict(value=float(n_nodes) * upsilon / float(runs), capped=False, runs=runs,
+                    state=out_state)
+
+    def _exchange_device(self):
+        return "cuda" if self.comm.backend == "nccl" else "cpu"
+
     def interdict(self, n_nodes: int, kind: int, k: int, eps: float, delta: float, cand=None):
         from . import hostapi
         limit = self.eng.limit(kind)

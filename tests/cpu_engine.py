@@ -40,6 +40,14 @@ class CpuEngine:
                 return i + 1, a
         raise RuntimeError("local cut beyond materialised batches")
 
+    def paired_runs(self, kind, ids, state0, first_run, nruns, draws_per_run):
+        from paper_1702_05854_b200 import capi  # host-only jump-ahead helper of the C-ABI
+        if nruns == 0:
+            return np.zeros(0, dtype=np.uint32), np.zeros(0, dtype=np.uint32)
+        s = capi.prg_jump(state0, first_run * draws_per_run)
+        full, res, _ = self.port.paired_runs(self.csr, kind, ids, s, nruns)
+        return full, res
+
     def _items(self, kind, w):
         return self.walk_edges[w] if kind == 0 else self.walk_nodes[w]
 

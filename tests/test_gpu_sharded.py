@@ -26,6 +26,27 @@ def test_world1_equals_single_gpu_path(ctx, gpu_lib, golden, synth3000):
         assert res == golden["synth3000"][key]
 
 
+def test_world1_estimate_suspension_equals_reference_golden(ctx, synth3000):
+    """ShardedSolver.estimate_suspension on the device engine: run ranges addressed by stream
+    position (capi.prg_jump) give the reference's value / runs / state."""
+    import json
+    from paper_1702_05854_b200.sharded import GpuEngine, ShardedSolver
+    with open(os.path.join(GOLDEN_DIR, "evaluation_vectors.json")) as f:
+        cases = json.load(f)["synth3000"]["estimate_suspension"]
+    upload(ctx, synth3000)
+    members = int(np.count_nonzero(synth3000.p_of))
+    eng = GpuEngine(ctx, seed=0)
+    try:
+        for c in cases[:4]:
+            got = ShardedSolver(eng).estimate_suspension(synth3000.n, members, c["kind"], c["ids"],
+                                                         c["epsilon"], c["delta"], c["state0"],
+                                                         batch_runs=777)
+            assert got == dict(value=float.fromhex(c["value"]), capped=c["capped"],
+                               runs=c["runs"], state=c["state_after"])
+    finally:
+        eng.close()
+
+
 def test_rounds_session_matches_fused_greedy(ctx, gpu_lib, synth3000):
     """The stepwise rounds API alone (one rank) equals hsaw_gpu_greedy."""
     import torch

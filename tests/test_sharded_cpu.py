@@ -76,6 +76,11 @@ def _worker(rank, world, port_no, case, out_q):
                 res = "no error"
             except Exception as e:  # noqa: BLE001
                 res = getattr(e, "status", repr(e))
+        elif "removal" in case:
+            members = int(np.count_nonzero(csr.p_of))
+            res = solver.estimate_suspension(csr.n, members, case["kind"], case["removal"],
+                                             case["eps"], case["delta"], case["state"],
+                                             batch_runs=case.get("batch_runs"))
         elif "target" in case:
             solver.ensure(case["target"])
             res = dict(counters=solver.counters_for(case["target"]),
@@ -125,3 +130,37 @@ def test_sharded_counters_and_budget(golden, port, synth3000):
     res = run_case(dict(graph="fixture12", seed=1, target=10**6, max_attempts=3000,
                         expect_budget=True))
     assert res[0] == res[1] == 3  # SamplingError on every rank
+
+
+def test_prg_jump_equals_stepping(port):
+    """capi.prg_jump (GF(2) jump-ahead of xorshift64*, host arithmetic of the C-ABI library)."""
+    from paper_1702_05854_b200 import capi
+    s = port.seed_from_worker(3)
+    x = s
+    for i in range(1, 200):
+        x, _ = port.prg_next(x)
+        assert capi.prg_jump(s, i) == x
+    assert capi.prg_jump(s, 0) == s
+    a = capi.prg_jump(s, 10**12 + 7)
+    assert capi.prg_jump(capi.prg_jump(s, 10**12), 7) == a
+
+
+def test_sharded_estimate_suspension_matches_reference_golden():
+    import json
+    with open(os.path.join(GOLDEN_DIR, "evaluation_vectors.json")) as f:
+        ev = json.load(f)
+    # synth3000, edge removal, eps 0.3: 4024 runs in the reference
+    c = ev["synth3000"]["estimate_suspension"][0]
+    want = dict(value=float.fromhex(c["value"]), capped=c["capped"], runs=c["runs"],
+                state=c["state_after"])
+    res = run_case(dict(graph="synth3000", seed=0, kind=c["kind"], removal=c["ids"],
+                        eps=c["epsilon"], delta=c["delta"], state=c["state0"], batch_runs=1000))
+    assert res[0] == res[1] == want
+    # fixture12 node removal on three ranks, small uneven batches
+    c = ev["fixture12_given"]["estimate_suspension"][3]
+    want = dict(value=float.fromhex(c["value"]), capped=c["capped"], runs=c["runs"],
+                state=c["state_after"])
+    res = run_case(dict(graph="fixture12", seed=0, kind=c["kind"], removal=c["ids"],
+                        eps=c["epsilon"], delta=c["delta"], state=c["state0"], batch_runs=101),
+                   world=3)
+    assert res[0] == res[1] == res[2] == want
