@@ -95,6 +95,28 @@ int hsaw_gpu_graph_build_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, cons
                                 const uint32_t* edge_v, const double* edge_w, int weight_mode,
                                 const double* p_of);
 
+/* Text ingest: the parsing and id-remap half of load_edge_list (proj/src/graph.cpp:29-59 parse_line,
+ * :201-241) on the device. `text` is the whole edge-list file. Lines are split at '\n', tokenised
+ * at C-locale whitespace; blank and '#' lines are skipped; an edge line is "u v" or "u v w".
+ * The device handles the plain grammar (unsigned decimal ids of <= 19 digits; weights
+ * digits[.digits][e[+-]digits] with <= 19 significant digits in the normal range, converted to
+ * the correctly rounded double std::stod returns). If any line is outside it (signs, hex floats,
+ * inf/nan, overlong numbers, malformed lines, a missing weight when weight_required) nothing is
+ * guessed: *host_line is set to the 1-based number of the first such line and no handle is
+ * returned; the caller re-reads the file with the host parser, which words the errors.
+ * weight_required: WeightMode::Given (:216-218). weight_values: also convert the weights (else they
+ * are only validated and returned as 0.0, for modes that ignore them). On success *nedges edge
+ * lines in file order, *nids distinct raw ids, *identity = raw ids are already 0..nids-1 (:236).
+ * hsaw_gpu_edge_text_fetch copies out dense endpoints (rank of the raw id among the sorted ids,
+ * :232-241), weights and the sorted raw ids (the node map, :254-260); every pointer nullable. */
+typedef struct hsaw_gpu_edge_text hsaw_gpu_edge_text;
+int hsaw_gpu_edge_text_parse(hsaw_gpu_ctx* ctx, const char* text, uint64_t bytes,
+                             int weight_required, int weight_values, hsaw_gpu_edge_text** out,
+                             uint64_t* nedges, uint64_t* nids, int* identity, uint64_t* host_line);
+int hsaw_gpu_edge_text_fetch(hsaw_gpu_edge_text* el, uint32_t* edge_u, uint32_t* edge_v,
+                             double* edge_w, uint64_t* raw_ids);
+void hsaw_gpu_edge_text_free(hsaw_gpu_edge_text* el);
+
 /* Binary ingest: the HSAW1 cache format (save_cache / load_cache, proj/src/graph.cpp:383-430).
  * `body` points at the bytes that follow the 21-byte header ("HSAW1", n, m as LE u64): (n + 1) u64
  * offsets, m u64-widened sources, m f64 bit patterns, all little endian, as they lie in the file

@@ -61,6 +61,11 @@ void* hsawh_device_ctx(const void* dg); /* the hsaw_gpu_ctx* underneath */
  * same ProbGraph as load_cache; hsaw::DeviceGraph::from_cache goes file -> resident graph with no
  * host CSR (no suspects until hsawh_device_set_suspects). */
 int hsawh_graph_load_cache_device(const char* path, int device, void** out);
+/* hsaw::load_edge_list_device: load_edge_list (graph.hpp:126-128) with parse / remap / build on the
+ * GPU; files outside the device parser's plain grammar go through the host parser unchanged. */
+int hsawh_graph_load_edge_list_device(const char* path, int weight_mode, uint64_t seed,
+                                      int symmetrize, const char* mapping_out, int device,
+                                      void** out);
 int hsawh_device_from_cache(const char* path, int device, void* cuda_stream, void** out);
 int hsawh_device_set_suspects(void* dg, const void* g, const double* p_of);
 

@@ -80,6 +80,11 @@ def lib() -> C.CDLL:
                                               C.c_int, f64p]
     L.hsaw_gpu_cache_decode.argtypes = [vp, C.c_uint32, C.c_uint32, vp, u64p, u32p, f64p, f64p, u32p]
     L.hsaw_gpu_graph_cache_upload.argtypes = [vp, C.c_uint32, C.c_uint32, vp, f64p]
+    L.hsaw_gpu_edge_text_parse.argtypes = [vp, C.c_char_p, C.c_uint64, C.c_int, C.c_int,
+                                           C.POINTER(vp), u64p, u64p, C.POINTER(C.c_int), u64p]
+    L.hsaw_gpu_edge_text_fetch.argtypes = [vp, u32p, u32p, f64p, u64p]
+    L.hsaw_gpu_edge_text_free.argtypes = [vp]
+    L.hsaw_gpu_edge_text_free.restype = None
     L.hsaw_gpu_graph_bytes.argtypes = [vp]
     L.hsaw_gpu_graph_bytes.restype = C.c_uint64
     L.hsaw_gpu_launch_count.argtypes = [vp]
@@ -148,6 +153,7 @@ EXPORTS = (
     "hsaw_gpu_rounds_cover", "hsaw_gpu_rounds_apply", "hsaw_gpu_rounds_end",
     "hsaw_gpu_paired_runs", "hsaw_gpu_estimate_suspension",
     "hsaw_gpu_cache_decode", "hsaw_gpu_graph_cache_upload", "hsaw_gpu_prg_jump",
+    "hsaw_gpu_edge_text_parse", "hsaw_gpu_edge_text_fetch", "hsaw_gpu_edge_text_free",
 )
 
 
@@ -281,6 +287,30 @@ class Context:
         self._chk(self.L.hsaw_gpu_graph_upload(self.h, n, m, _p(in_offsets, u64p),
                                                _p(in_src, u32p), _p(in_cum, f64p), _p(p_of, f64p)))
         self.n, self.m = n, m
+
+    def parse_edge_text(self, text: bytes, weight_required=False, weight_values=True):
+        """Device half of load_edge_list: -> dict(u, v, w, raw_ids, identity) or dict(host_line=N)
+        when line N is outside the plain grammar and the host parser must take over."""
+        h = C.c_void_p()
+        ne, nids, ident, hl = C.c_uint64(), C.c_uint64(), C.c_int(), C.c_uint64()
+        self._chk(self.L.hsaw_gpu_edge_text_parse(self.h, text, len(text), int(weight_required),
+                                                  int(weight_values), C.byref(h), C.byref(ne),
+                                                  C.byref(nids), C.byref(ident), C.byref(hl)))
+        if hl.value:
+            return dict(host_line=int(hl.value))
+        ne, nids = ne.value, nids.value
+        u = np.zeros(max(ne, 1), dtype=np.uint32)
+        v = np.zeros(max(ne, 1), dtype=np.uint32)
+        w = np.zeros(max(ne, 1), dtype=np.float64)
+        ids = np.zeros(max(nids, 1), dtype=np.uint64)
+        if h:
+            try:
+                self._chk(self.L.hsaw_gpu_edge_text_fetch(h, _p(u, u32p), _p(v, u32p),
+                                                          _p(w, f64p), _p(ids, u64p)))
+            finally:
+                self.L.hsaw_gpu_edge_text_free(h)
+        return dict(u=u[:ne], v=v[:ne], w=w[:ne], raw_ids=ids[:nids], identity=bool(ident.value),
+                    host_line=0)
 
     @staticmethod
     def _cache_header(image: bytes):

@@ -265,6 +265,18 @@ void hsawh_pool_copy(const void* pool, uint64_t* edge_off, uint32_t* nodes, uint
 
 void hsawh_pool_free(void* pool) { delete static_cast<SamplePool*>(pool); }
 
+int hsawh_graph_load_edge_list_device(const char* path, int weight_mode, uint64_t seed,
+                                      int symmetrize, const char* mapping_out, int device,
+                                      void** out) {
+    return guarded([&] {
+        LoadOptions opts;
+        opts.symmetrize = symmetrize != 0;
+        if (mapping_out) opts.mapping_out = mapping_out;
+        *out = new ProbGraph(load_edge_list_device(path, static_cast<WeightMode>(weight_mode), seed,
+                                                   opts, device));
+    });
+}
+
 int hsawh_graph_load_cache_device(const char* path, int device, void** out) {
     return guarded([&] { *out = new ProbGraph(load_cache_device(path, device)); });
 }

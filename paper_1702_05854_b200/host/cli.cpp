@@ -108,7 +108,10 @@ ProbGraph load_graph(const Flags& f, std::uint64_t seed) {
     }
     LoadOptions opts;
     opts.symmetrize = f.switches.count("symmetrize") != 0;
-    return load_edge_list(path, weight_mode(f.str("weights", "indegree")), seed, opts);
+    // text edge lists are parsed, re-ranked, sorted and summed on the device; anything outside the
+    // device parser's plain grammar goes through the host parser inside this call
+    return load_edge_list_device(path, weight_mode(f.str("weights", "indegree")), seed, opts,
+                                 static_cast<int>(f.u64("device", 0)));
 }
 
 SuspectSet load_suspect_args(const Flags& f, const ProbGraph& g, std::uint64_t seed) {

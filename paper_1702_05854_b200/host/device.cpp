@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <fstream>
 
 #include "hsaw_b200.hpp"
 #include "hsaw_gpu.h"
@@ -150,6 +151,75 @@ struct MappedCache {
 };
 
 }  // namespace
+
+// ---- text ingest on the device --------------------------------------------------------------------
+ProbGraph load_edge_list_device(const std::string& path, WeightMode mode, std::uint64_t seed,
+                                const LoadOptions& opts, int device) {
+    if (opts.symmetrize) return load_edge_list(path, mode, seed, opts);  // host dedupe of tuples
+    int fd = ::open(path.c_str(), O_RDONLY);
+    if (fd < 0) throw DataError("cannot open edge list: " + path);
+    struct stat st {};
+    if (::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode)) {
+        ::close(fd);
+        return load_edge_list(path, mode, seed, opts);  // pipes etc.: stream through the host parser
+    }
+    const std::size_t bytes = static_cast<std::size_t>(st.st_size);
+    void* base = bytes ? ::mmap(nullptr, bytes, PROT_READ, MAP_PRIVATE, fd, 0) : nullptr;
+    ::close(fd);
+    if (bytes && base == MAP_FAILED) return load_edge_list(path, mode, seed, opts);
+    struct Unmap {
+        void* p;
+        std::size_t n;
+        ~Unmap() {
+            if (p && n) ::munmap(p, n);
+        }
+    } unmap{base, bytes};
+    if (bytes) ::madvise(base, bytes, MADV_SEQUENTIAL);
+
+    hsaw_gpu_ctx* ctx = nullptr;
+    if (hsaw_gpu_ctx_create(device, nullptr, &ctx) != HSAW_OK)
+        throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");
+    struct CtxGuard {
+        hsaw_gpu_ctx* c;
+        ~CtxGuard() { hsaw_gpu_ctx_destroy(c); }
+    } guard{ctx};
+
+    hsaw_gpu_edge_text* el = nullptr;
+    std::uint64_t ne = 0, nids = 0, host_line = 0;
+    int identity = 0;
+    const bool given = mode == WeightMode::Given;
+    int rc = hsaw_gpu_edge_text_parse(ctx, static_cast<const char*>(base), bytes, given ? 1 : 0,
+                                      given ? 1 : 0, &el, &ne, &nids, &identity, &host_line);
+    if (rc != HSAW_OK) raise(rc, ctx, "load_edge_list");
+    // a line the device does not parse: the host parser decides what it is and words the error
+    if (host_line != 0) return load_edge_list(path, mode, seed, opts);
+    if (ne == 0) throw DataError(path + ": no edges");  // graph.cpp:231
+    struct ElGuard {
+        hsaw_gpu_edge_text* e;
+        ~ElGuard() { hsaw_gpu_edge_text_free(e); }
+    } el_guard{el};
+
+    std::vector<NodeId> u(ne), v(ne);
+    std::vector<double> w(given ? ne : 0);
+    const bool write_map = !identity || !opts.mapping_out.empty();  // graph.cpp:254
+    std::vector<std::uint64_t> raw_ids(write_map ? nids : 0);
+    rc = hsaw_gpu_edge_text_fetch(el, u.data(), v.data(), given ? w.data() : nullptr,
+                                  write_map ? raw_ids.data() : nullptr);
+    if (rc != HSAW_OK) raise(rc, ctx, "load_edge_list");
+    if (write_map) {
+        const std::string map_path = opts.mapping_out.empty() ? path + ".nodemap" : opts.mapping_out;
+        std::ofstream mf(map_path);
+        if (!mf) throw DataError("cannot write node map: " + map_path);
+        for (std::size_t i = 0; i < raw_ids.size(); ++i) mf << raw_ids[i] << ' ' << i << '\n';
+    }
+    const NodeId n = static_cast<NodeId>(nids);
+    if (mode == WeightMode::RandomNormalized) {  // one global draw stream over the rows: host
+        std::vector<std::tuple<NodeId, NodeId, double>> edges(ne);
+        for (std::size_t i = 0; i < ne; ++i) edges[i] = {u[i], v[i], 0.0};
+        return build_graph(n, std::move(edges), mode, seed);
+    }
+    return build_graph_device(n, ne, u.data(), v.data(), given ? w.data() : nullptr, mode, device);
+}
 
 ProbGraph load_cache_device(const std::string& path, int device) {
     MappedCache file(path);

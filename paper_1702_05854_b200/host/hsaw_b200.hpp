@@ -154,6 +154,14 @@ ProbGraph build_graph_device(NodeId n, const std::vector<std::tuple<NodeId, Node
 ProbGraph build_graph_device(NodeId n, std::uint64_t nedges, const NodeId* u, const NodeId* v,
                              const double* w, WeightMode mode, int device = 0);
 
+// load_edge_list (proj/include/hsaw/graph.hpp:126-128) with the text parse, the id remap, the sort,
+// the per-row sums and the validation on the GPU (hsaw_gpu_edge_text_parse + hsaw_gpu_csr_build).
+// Same ProbGraph, same node-map file, same DataErrors: a file with any line outside the device
+// parser's plain grammar (or opts.symmetrize, or WeightMode::RandomNormalized's host draw stream)
+// is handed to load_edge_list / build_graph unchanged.
+ProbGraph load_edge_list_device(const std::string& path, WeightMode mode, std::uint64_t seed,
+                                const LoadOptions& opts = {}, int device = 0);
+
 // load_cache (proj/include/hsaw/graph.hpp:139-141) with the decode, the per-row cumulative sums and
 // validate() on the GPU (hsaw_gpu_cache_decode): the file is mapped and shipped as it lies on disk.
 // Same ProbGraph bit for bit, same DataError messages.

@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
                                   C.c_double, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int,
                                   C.POINTER(Result), u32p, C.c_char_p, C.c_uint64]
     L.hsawh_sample.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p]
+    L.hsawh_graph_load_edge_list_device.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int,
+                                                    C.c_char_p, C.c_int, vpp]
     L.hsawh_graph_load_cache_device.argtypes = [C.c_char_p, C.c_int, vpp]
     L.hsawh_device_from_cache.argtypes = [C.c_char_p, C.c_int, vp, vpp]
     L.hsawh_device_set_suspects.argtypes = [vp, vp, f64p]
@@ -151,6 +153,13 @@ class Graph:
     @classmethod
     def load_cache(cls, path):
         return cls._new(lib().hsawh_graph_load_cache, str(path).encode())
+
+    @classmethod
+    def load_edge_list_device(cls, path, mode=1, seed=0, symmetrize=False, mapping_out=None,
+                              device=0):
+        """hsaw::load_edge_list_device: text parse, id remap and build_graph on the GPU."""
+        return cls._new(lib().hsawh_graph_load_edge_list_device, str(path).encode(), mode, seed,
+                        int(symmetrize), str(mapping_out).encode() if mapping_out else None, device)
 
     @classmethod
     def load_cache_device(cls, path, device=0):
