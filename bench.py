@@ -54,6 +54,10 @@ def parse_args():
     ap.add_argument("--solver", default="esia", choices=["esia", "nsia"],
                     help="interdiction driver timed beside the sampler (edge or node candidates)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ingest", action="store_true",
+                    help="also time the step before the path (SURVEY 8f row 1): HSAW1 cache and "
+                         "edge-list text of a graph of this size -> ProbGraph / resident graph, "
+                         "device loaders vs the host loaders, the reference's loaders as cpu_baseline")
     ap.add_argument("--no-suspension", action="store_true",
                     help="skip the forward-simulation leg (estimate_suspension of the solution)")
     ap.add_argument("--no-l2-flush", action="store_true",
@@ -488,6 +492,13 @@ def run_b200(args):
         except Exception as exc:
             out["suspension"] = {"error": str(exc)[:300]}
 
+    # ---- the step before the path, on request: file -> graph
+    if args.ingest and world == 1:
+        try:
+            out["ingest"] = ingest_leg(args, rank == 0 and not args.no_cpu_baseline)
+        except Exception as exc:
+            out["ingest"] = {"error": str(exc)[:300]}
+
     # ---- N > 1: the sharded solve (walks sharded by batch range, marginal-gain counts combined
     # over NCCL; paper_1702_05854_b200/sharded.py). Every rank runs it; device-timed, max over ranks.
     if not args.no_esia and world > 1:
@@ -539,6 +550,54 @@ def run_b200(args):
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def ingest_leg(args, with_cpu_baseline: bool) -> dict:
+    """HSAW1 cache / edge-list text of a uniform graph with the workload's node and edge counts
+    (validate() rejects R-MAT hub rows in 1/d mode) in /dev/shm: device loaders, host
+    loaders, and - cpu_baseline - the reference's own load_cache / load_edge_list."""
+    import tempfile
+
+    from paper_1702_05854_b200 import hostapi
+
+    def timed(fn, *a, **k):
+        t0 = time.perf_counter()
+        r = fn(*a, **k)
+        dt = time.perf_counter() - t0
+        if hasattr(r, "close"):
+            r.close()
+        return dt
+
+    g = hostapi.Graph.synth(1 << args.scale, int(args.edge_factor), 3)
+    res = {"graph": f"synth_graph(2^{args.scale}, {int(args.edge_factor)}, seed 3): {g.n} nodes, {g.m} edges"}
+    with tempfile.TemporaryDirectory(dir="/dev/shm" if os.path.isdir("/dev/shm") else None) as tmp:
+        cache, text = os.path.join(tmp, "g.hsaw1"), os.path.join(tmp, "g.edges")
+        g.save_cache(cache)
+        g.save_edge_list(text)
+        res["cache_bytes"], res["text_bytes"] = os.path.getsize(cache), os.path.getsize(text)
+        timed(hostapi.DeviceGraph.from_cache, cache)  # warm-up: context, pools, pinned staging
+        res["cache_to_resident_graph_s"] = min(timed(hostapi.DeviceGraph.from_cache, cache)
+                                               for _ in range(3))
+        res["cache_to_probgraph_device_s"] = min(timed(hostapi.Graph.load_cache_device, cache)
+                                                 for _ in range(2))
+        res["cache_to_probgraph_host_s"] = timed(hostapi.Graph.load_cache, cache)
+        timed(hostapi.Graph.load_edge_list_device, text, mode=1)
+        res["text_to_probgraph_device_s"] = min(
+            timed(hostapi.Graph.load_edge_list_device, text, mode=1) for _ in range(2))
+        res["text_to_probgraph_host_s"] = timed(hostapi.Graph.load_edge_list, text, mode=1)
+        if with_cpu_baseline:
+            from oracle import oracle
+            if oracle.have_ref():
+                R = oracle.Ref()
+                t0 = time.perf_counter()
+                R.graph_free(R.load_cache(cache))
+                t1 = time.perf_counter()
+                R.graph_free(R.load_edge_list(text, mode=1))
+                t2 = time.perf_counter()
+                res["cpu_baseline"] = {"kind": "reference", "cores": 1, "load_cache_s": t1 - t0,
+                                       "load_edge_list_s": t2 - t1,
+                                       "sample": "the same two files, one call each"}
+    return res
 
 
 def hsaw_mb(dg):

@@ -151,12 +151,15 @@ def test_argument_errors_follow_the_reference(ctx, fixture12, gpu_lib):
     assert e == dict(value=0.0, capped=False, runs=0, state=st)
 
 
-def test_full_size_runs_match_oracle(gpu_lib, port, monkeypatch):
-    """C2 shape (R-MAT scale 20, 16 M edges): two paired runs against the oracle, default layout."""
+@pytest.mark.parametrize("layout", ["compact", "fat"])
+def test_full_size_runs_match_oracle(gpu_lib, port, monkeypatch, layout):
+    """C2 shape (R-MAT scale 20, 16 M edges): two paired runs against the oracle on the L2-resident
+    compact layout (the default at this size) and on the fat layout the larger shapes use."""
     from oracle.oracle import Csr
     from paper_1702_05854_b200 import hostapi
     for k in ("HSAW_LAYOUT", "HSAW_FORCE_EXACT", "HSAW_PACK"):
         monkeypatch.delenv(k, raising=False)
+    monkeypatch.setenv("HSAW_LAYOUT", layout)
     g = hostapi.Graph.rmat(20, 16.0, seed=1)
     p_of = g.random_suspects(g.n // 100, seed=2)
     off, src, cum, _, _ = g.arrays()

@@ -1,5 +1,4 @@
-"""Cache ingest timing at C2 shape: host load_cache (+ upload) vs device ingest, and the
-reference's own load_cache where oracle/_ref is present (CPU baseline; test infrastructure)."""
+"""Cache ingest timing at C2 shape: host load_cache (+ upload) vs device ingest (the reference's own loader is timed by `bench.py --ingest`, cpu_baseline leg)."""
 import json
 import os
 import sys
@@ -37,16 +36,6 @@ def main():
         out["host_upload_s"] = best(lambda: hostapi.DeviceGraph(h, p_of))
         out["device_load_cache_s"] = best(lambda: hostapi.Graph.load_cache_device(path))
         out["device_from_cache_s"] = best(lambda: hostapi.DeviceGraph.from_cache(path))
-        try:
-            from oracle import oracle
-            if oracle.have_ref():
-                R = oracle.Ref()
-                t0 = time.perf_counter()
-                gh = R.load_cache(path)
-                out["reference_load_cache_s"] = time.perf_counter() - t0
-                R.graph_free(gh)
-        except Exception as e:  # noqa: BLE001
-            out["reference_load_cache_error"] = str(e)[:200]
     out["file_to_resident_speedup_vs_host_path"] = (
         (out["host_load_cache_s"] + out["host_upload_s"]) / out["device_from_cache_s"])
     print(json.dumps(out))

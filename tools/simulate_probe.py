@@ -43,6 +43,7 @@ def main():
         ms, regions = ctx.stage_times(reset=True)["simulate"]
         draws = args.runs * (g.n + int(np.count_nonzero(p_of)))
         print(json.dumps({"n": g.n, "m": g.m, "runs": args.runs, "wall_s": wall,
+                          "layout": os.environ.get("HSAW_LAYOUT", "default"),
                           "device_ms": ms, "batches": regions, "launches": ctx.launches - l0,
                           "draws": draws, "gdraws_per_s_device": draws / ms / 1e6,
                           "mean_full": float(full.mean()), "mean_residual": float(res.mean())}))

@@ -1,5 +1,5 @@
-"""Edge-list text ingest timing at C2 shape: host load_edge_list vs load_edge_list_device, and the
-reference's own load_edge_list where oracle/_ref is present (CPU baseline; test infrastructure).
+"""Edge-list text ingest timing at C2 shape: host load_edge_list vs load_edge_list_device (the reference's own
+loader is timed by `bench.py --ingest`, cpu_baseline leg).
 The file is what save_edge_list writes ("u v %.17g"), read back in 1/in-degree mode."""
 import json
 import os
@@ -33,19 +33,6 @@ def main():
             except hostapi.HsawError as e:
                 out[name] = time.perf_counter() - t0
                 out[name.replace("_s", "_error")] = str(e)[:120]
-        try:
-            from oracle import oracle
-            if oracle.have_ref():
-                R = oracle.Ref()
-                t0 = time.perf_counter()
-                try:
-                    gh = R.load_edge_list(path, mode=1)
-                    R.graph_free(gh)
-                except Exception as e:  # noqa: BLE001
-                    out["reference_error"] = str(e)[:120]
-                out["reference_load_edge_list_s"] = time.perf_counter() - t0
-        except Exception as e:  # noqa: BLE001
-            out["reference_load_edge_list_error"] = str(e)[:200]
     print(json.dumps(out))
 
 
