@@ -127,3 +127,17 @@ def test_full_size_cache_round_trip(tmp_path):
             dg.set_suspects(g, p_of)
             with hostapi.DeviceGraph(g, p_of) as dg2:
                 assert dg.sample(100000, seed=42) == dg2.sample(100000, seed=42)
+
+
+def test_edgeless_cache(tmp_path):
+    """A cache with nodes but no edges (offsets all zero) loads the same way on both paths."""
+    import struct
+    from paper_1702_05854_b200 import hostapi
+    path = tmp_path / "empty.hsaw1"
+    path.write_bytes(b"HSAW1" + struct.pack("<QQ", 3, 0) + struct.pack("<4Q", 0, 0, 0, 0))
+    a, b = hostapi.Graph.load_cache(path), hostapi.Graph.load_cache_device(path)
+    assert (a.n, a.m) == (b.n, b.m) == (3, 0)
+    assert np.array_equal(a.arrays()[0], b.arrays()[0])
+    with hostapi.DeviceGraph.from_cache(path) as dg:
+        dg.set_suspects(a, np.array([0.5, 0.0, 1.0]))
+        assert dg.sample(10, seed=1)[1] >= 10

@@ -279,3 +279,25 @@ def test_cli_estimate(tmp_path, fixture12, eval_golden, golden):
     rem.write_text("999\n")
     assert hostapi.run_cli(["estimate", "--graph", str(edges), "--weights", "given", "--suspects",
                             str(sus), "--removal", str(rem)]) == 2
+
+
+def test_degenerate_graphs(ctx, port):
+    """One node, no edges, no suspects, zero runs: the corner cases of the stream arithmetic."""
+    from oracle.oracle import Csr
+    one = Csr(1, 0, np.zeros(2, dtype=np.uint64), np.zeros(0, dtype=np.uint32), np.zeros(0),
+              np.array([0.75]))
+    upload(ctx, one)
+    st = port.seed_from_worker(2)
+    want = port.paired_runs(one, 1, [0], st, 500)
+    got = ctx.paired_runs(1, [0], st, 500)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]) and got[2] == want[2]
+    assert ctx.estimate_suspension(1, [0], 0.3, 0.2, st) == port.estimate_suspension(one, 1, [0], 0.3, 0.2, st)
+    full, res, after = ctx.paired_runs(1, [0], st, 0)
+    assert full.size == 0 and after == st
+    iso = Csr(5, 0, np.zeros(6, dtype=np.uint64), np.zeros(0, dtype=np.uint32), np.zeros(0),
+              np.array([0.0, 1.0, 0.0, 0.5, 0.0]))
+    upload(ctx, iso)
+    want = port.paired_runs(iso, 1, [1, 1, 3], st, 64)  # duplicate ids in the removal set
+    got = ctx.paired_runs(1, [1, 1, 3], st, 64)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]) and got[2] == want[2]
+    assert np.all(got[1] == 0) and np.all(got[0] >= 1)
