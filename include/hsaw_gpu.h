@@ -115,6 +115,11 @@ int hsaw_gpu_edge_text_parse(hsaw_gpu_ctx* ctx, const char* text, uint64_t bytes
                              uint64_t* nedges, uint64_t* nids, int* identity, uint64_t* host_line);
 int hsaw_gpu_edge_text_fetch(hsaw_gpu_edge_text* el, uint32_t* edge_u, uint32_t* edge_v,
                              double* edge_w, uint64_t* raw_ids);
+/* build_graph + hsaw_gpu_graph_upload on the parsed edges where they lie on the device: text file ->
+ * graph resident and ready to sample, no host CSR and no host edge list. weight_mode 0 Given (the
+ * parse must have converted the weights) / 1 InDegree; p_of NULL = no suspects yet. Same errors as
+ * hsaw_gpu_csr_build. */
+int hsaw_gpu_edge_text_install(hsaw_gpu_edge_text* el, int weight_mode, const double* p_of);
 void hsaw_gpu_edge_text_free(hsaw_gpu_edge_text* el);
 
 /* Binary ingest: the HSAW1 cache format (save_cache / load_cache, proj/src/graph.cpp:383-430).

@@ -67,6 +67,10 @@ int hsawh_graph_load_edge_list_device(const char* path, int weight_mode, uint64_
                                       int symmetrize, const char* mapping_out, int device,
                                       void** out);
 int hsawh_device_from_cache(const char* path, int device, void* cuda_stream, void** out);
+/* hsaw::DeviceGraph::from_edge_list: text file -> resident graph; *out NULL when the file needs
+ * the host loader (outside the device parser's plain grammar, RandomNormalized, empty). */
+int hsawh_device_from_edge_list(const char* path, int weight_mode, int device, void* cuda_stream,
+                                void** out);
 int hsawh_device_set_suspects(void* dg, const void* g, const double* p_of);
 
 /* ---- eSIA / nSIA — proj/include/hsaw/interdiction.hpp:37-47 ---- */

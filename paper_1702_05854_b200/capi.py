@@ -83,6 +83,7 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_edge_text_parse.argtypes = [vp, C.c_char_p, C.c_uint64, C.c_int, C.c_int,
                                            C.POINTER(vp), u64p, u64p, C.POINTER(C.c_int), u64p]
     L.hsaw_gpu_edge_text_fetch.argtypes = [vp, u32p, u32p, f64p, u64p]
+    L.hsaw_gpu_edge_text_install.argtypes = [vp, C.c_int, f64p]
     L.hsaw_gpu_edge_text_free.argtypes = [vp]
     L.hsaw_gpu_edge_text_free.restype = None
     L.hsaw_gpu_graph_bytes.argtypes = [vp]
@@ -154,6 +155,7 @@ EXPORTS = (
     "hsaw_gpu_paired_runs", "hsaw_gpu_estimate_suspension",
     "hsaw_gpu_cache_decode", "hsaw_gpu_graph_cache_upload", "hsaw_gpu_prg_jump",
     "hsaw_gpu_edge_text_parse", "hsaw_gpu_edge_text_fetch", "hsaw_gpu_edge_text_free",
+    "hsaw_gpu_edge_text_install",
 )
 
 
@@ -311,6 +313,26 @@ class Context:
                 self.L.hsaw_gpu_edge_text_free(h)
         return dict(u=u[:ne], v=v[:ne], w=w[:ne], raw_ids=ids[:nids], identity=bool(ident.value),
                     host_line=0)
+
+    def upload_edge_text(self, text: bytes, weight_mode=1, p_of=None):
+        """Edge-list text -> graph resident and ready to sample (no host CSR). Returns (n, m), or
+        None when a line is outside the device parser's plain grammar (host loader's business)."""
+        h = C.c_void_p()
+        ne, nids, ident, hl = C.c_uint64(), C.c_uint64(), C.c_int(), C.c_uint64()
+        given = weight_mode == 0
+        self._chk(self.L.hsaw_gpu_edge_text_parse(self.h, text, len(text), int(given), int(given),
+                                                  C.byref(h), C.byref(ne), C.byref(nids),
+                                                  C.byref(ident), C.byref(hl)))
+        if hl.value or not h:
+            return None
+        try:
+            p = None if p_of is None else np.ascontiguousarray(p_of, dtype=np.float64)
+            self._chk(self.L.hsaw_gpu_edge_text_install(h, weight_mode,
+                                                        _p(p, f64p) if p is not None else None))
+        finally:
+            self.L.hsaw_gpu_edge_text_free(h)
+        self.n, self.m = int(nids.value), int(ne.value)
+        return self.n, self.m
 
     @staticmethod
     def _cache_header(image: bytes):

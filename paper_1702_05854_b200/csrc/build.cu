@@ -111,9 +111,11 @@ struct DeviceCsr {
 // Builds the CSR on the device. want_aux: also produce weight[] and edge_dst[]. When `src_out` is
 // given the sorted sources are written there (the compact layout's own array) instead of csr.src.
 // Throws HSAW_EDATA with the reference's message on bad input.
+// on_device: edge_u / edge_v / edge_w are device arrays already (the text parser's output); they are
+// used in place and single elements are copied back only to word an error.
 void build_device_csr(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t* edge_u,
                       const uint32_t* edge_v, const double* edge_w, int weight_mode, bool want_aux,
-                      uint32_t* src_out, DeviceCsr& csr) {
+                      uint32_t* src_out, DeviceCsr& csr, bool on_device = false) {
     if (n == 0) fail(HSAW_EDATA, "graph: no nodes");
     if (ne > 0xFFFFFFFEull) fail(HSAW_EINVAL, "build: edge ids are 32-bit (types.hpp:10)");
     if (weight_mode != 0 && weight_mode != 1)
@@ -127,8 +129,10 @@ void build_device_csr(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t
     DevVec<uint32_t> d_u, d_v;
     DevVec<uint64_t> keys_in, keys_out;
     DevVec<uint32_t> vals_in;
-    d_u.ensure_scratch(cap);
-    d_v.ensure_scratch(cap);
+    if (!on_device) {
+        d_u.ensure_scratch(cap);
+        d_v.ensure_scratch(cap);
+    }
     keys_in.ensure_scratch(cap);
     keys_out.ensure_scratch(cap);
     vals_in.ensure_scratch(cap);
@@ -140,7 +144,7 @@ void build_device_csr(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t
         csr.weight.ensure_scratch(cap);
         csr.dst.ensure_scratch(cap);
     }
-    if (given) csr.w_in.ensure_scratch(cap);
+    if (given && !on_device) csr.w_in.ensure_scratch(cap);
     uint32_t* d_err = reinterpret_cast<uint32_t*>(ctx->d_scalars + 56);
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_err, 0xFF, E_COUNT * 4, st));
 
@@ -152,14 +156,21 @@ void build_device_csr(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t
         return;
     }
 
-    std::vector<CopyJob> jobs{{d_u.p, edge_u, ne * 4}, {d_v.p, edge_v, ne * 4}};
-    if (given) jobs.push_back({csr.w_in.p, edge_w, ne * 8});
-    copy_to_device(ctx, jobs);
+    const uint32_t* in_u = edge_u;
+    const uint32_t* in_v = edge_v;
+    const double* in_w = given ? edge_w : nullptr;
+    if (!on_device) {
+        std::vector<CopyJob> jobs{{d_u.p, edge_u, ne * 4}, {d_v.p, edge_v, ne * 4}};
+        if (given) jobs.push_back({csr.w_in.p, edge_w, ne * 8});
+        copy_to_device(ctx, jobs);
+        in_u = d_u.p;
+        in_v = d_v.p;
+        in_w = given ? csr.w_in.p : nullptr;
+    }
     {
         StageScope timer(ctx, HSAW_STAGE_UPLOAD);
         const unsigned eb = (unsigned)((ne + 255) / 256);
-        edge_keys<<<eb, 256, 0, st>>>(ne, n, d_u.p, d_v.p, given ? csr.w_in.p : nullptr, keys_in.p,
-                                      vals_in.p, d_err);
+        edge_keys<<<eb, 256, 0, st>>>(ne, n, in_u, in_v, in_w, keys_in.p, vals_in.p, d_err);
         check_launch(ctx, "edge_keys");
         int node_bits = 32 - __builtin_clz(n > 1 ? n - 1 : 1);
         int end_bit = std::min(64, 32 + node_bits);
@@ -183,11 +194,22 @@ void build_device_csr(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t
     HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
     if (err[E_INPUT] != kNone) {
         const uint64_t i = err[E_INPUT];
-        const uint32_t a = edge_u[i], b = edge_v[i];
+        uint32_t a = 0, b = 0;
+        double wi = 0.0;
+        if (on_device) {
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(&a, in_u + i, 4, cudaMemcpyDeviceToHost, st));
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(&b, in_v + i, 4, cudaMemcpyDeviceToHost, st));
+            if (in_w) HSAW_CUDA_CHECK(cudaMemcpyAsync(&wi, in_w + i, 8, cudaMemcpyDeviceToHost, st));
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        } else {
+            a = edge_u[i];
+            b = edge_v[i];
+            if (given) wi = edge_w[i];
+        }
         if (a >= n || b >= n) fail(HSAW_EDATA, "edge endpoint out of range");
         if (a == b)
             fail(HSAW_EDATA, "self-loop " + std::to_string(a) + " -> " + std::to_string(b));
-        fail(HSAW_EDATA, "weight " + d2s(edge_w[i]) + " out of (0,1] on edge " +
+        fail(HSAW_EDATA, "weight " + d2s(wi) + " out of (0,1] on edge " +
                              std::to_string(a) + " -> " + std::to_string(b));
     }
     if (err[E_DUP] != kNone) {
@@ -200,7 +222,7 @@ void build_device_csr(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t
     {
         StageScope timer(ctx, HSAW_STAGE_UPLOAD);
         row_weights<<<(n + 127) / 128, 128, 0, st>>>(n, csr.off.p, csr.vals.p,
-                                                     given ? csr.w_in.p : nullptr, csr.cum.p,
+                                                     in_w, csr.cum.p,
                                                      want_aux ? csr.weight.p : nullptr, d_err);
         check_launch(ctx, "row_weights");
     }
@@ -236,6 +258,35 @@ void build_device_csr(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t
     }
 }
 
+void build_and_install(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t* edge_u,
+                       const uint32_t* edge_v, const double* edge_w, int weight_mode,
+                       const double* host_p_of, bool on_device) {
+    release_graph(ctx);
+    cudaStream_t st = ctx->stream;
+    double* d_p = nullptr;
+    try {
+        if (n == 0) fail(HSAW_EDATA, "graph: no nodes");
+        if (ne > 0xFFFFFFFEull) fail(HSAW_EINVAL, "build: edge ids are 32-bit (types.hpp:10)");
+        prepare_layout(ctx, n, (uint32_t)ne);
+        DeviceCsr csr;
+        build_device_csr(ctx, n, ne, edge_u, edge_v, edge_w, weight_mode, false, nullptr, csr,
+                         on_device);
+        d_p = static_cast<double*>(pool_alloc((uint64_t)n * 8, st));
+        if (host_p_of)
+            HSAW_CUDA_CHECK(
+                cudaMemcpyAsync(d_p, host_p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, st));
+        else
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_p, 0, (uint64_t)n * 8, st));
+        install_graph(ctx, n, (uint32_t)ne, csr.off.p, csr.src.p, csr.cum.p, d_p);
+    } catch (...) {
+        if (d_p) cudaFreeAsync(d_p, st);
+        release_graph(ctx);
+        throw;
+    }
+    cudaFreeAsync(d_p, st);
+    collect_timings(ctx);
+}
+
 }  // namespace hsawgpu
 
 extern "C" {
@@ -269,25 +320,7 @@ int hsaw_gpu_graph_build_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, cons
     if (!ctx) return HSAW_EINVAL;
     return guarded(ctx, [&] {
         if (!p_of) fail(HSAW_EINVAL, "graph_build_upload: null suspect array");
-        release_graph(ctx);
-        cudaStream_t st = ctx->stream;
-        double* d_p = nullptr;
-        try {
-            if (n == 0) fail(HSAW_EDATA, "graph: no nodes");
-            if (ne > 0xFFFFFFFEull) fail(HSAW_EINVAL, "build: edge ids are 32-bit (types.hpp:10)");
-            prepare_layout(ctx, n, (uint32_t)ne);
-            DeviceCsr csr;
-            build_device_csr(ctx, n, ne, edge_u, edge_v, edge_w, weight_mode, false, nullptr, csr);
-            d_p = static_cast<double*>(pool_alloc((uint64_t)n * 8, st));
-            HSAW_CUDA_CHECK(cudaMemcpyAsync(d_p, p_of, (uint64_t)n * 8, cudaMemcpyHostToDevice, st));
-            install_graph(ctx, n, (uint32_t)ne, csr.off.p, csr.src.p, csr.cum.p, d_p);
-        } catch (...) {
-            if (d_p) cudaFreeAsync(d_p, st);
-            release_graph(ctx);
-            throw;
-        }
-        cudaFreeAsync(d_p, st);
-        collect_timings(ctx);
+        build_and_install(ctx, n, ne, edge_u, edge_v, edge_w, weight_mode, p_of, false);
     });
 }
 

@@ -454,6 +454,11 @@ inline SrcRef src_ref(const DeviceGraph& g) { return SrcRef{g.src, g.src_bits}; 
 void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_off,
                    const uint32_t* d_src, const double* d_cum, const double* d_p);
 void release_graph(hsaw_gpu_ctx* ctx);
+// Device CSR builder (build.cu): edge list -> resident graph in the chosen layout. on_device: the
+// edge arrays are device pointers (the text parser's output) instead of host arrays.
+void build_and_install(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t* edge_u,
+                       const uint32_t* edge_v, const double* edge_w, int weight_mode,
+                       const double* host_p_of, bool on_device);
 
 // exclusive prefix sums (CUB) on the context stream; out may have a wider type than in
 void exclusive_sum_u32_to_u64(hsaw_gpu_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t count);

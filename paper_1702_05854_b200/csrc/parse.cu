@@ -88,7 +88,7 @@ __device__ bool parse_id(const char* t, uint32_t len, uint64_t& x) {
 // std::stod on a plain token. value_needed = false: only decide that stod would accept it.
 __device__ bool parse_weight(const char* t, uint32_t len, bool value_needed, double& x) {
     uint64_t sig = 0;
-    int nsig = 0, dropped_exp = 0, frac = 0;
+    int nsig = 0, frac = 0;
     uint32_t i = 0;
     bool any = false, seen_dot = false;
     for (; i < len; ++i) {
@@ -106,7 +106,6 @@ __device__ bool parse_weight(const char* t, uint32_t len, bool value_needed, dou
         sig = sig * 10 + (uint64_t)(c - '0');
         ++nsig;
     }
-    (void)dropped_exp;
     if (!any) return false;
     int e10 = 0;
     if (i < len) {
@@ -412,6 +411,15 @@ int hsaw_gpu_edge_text_fetch(hsaw_gpu_edge_text* el, uint32_t* edge_u, uint32_t*
         if (edge_w) jobs.push_back({edge_w, el->w.p, el->ne * 8});
         if (raw_ids) jobs.push_back({raw_ids, el->sorted.p, el->nids * 8});
         if (!jobs.empty()) copy_to_host(el->ctx, jobs);
+    });
+}
+
+int hsaw_gpu_edge_text_install(hsaw_gpu_edge_text* el, int weight_mode, const double* p_of) {
+    if (!el) return HSAW_EINVAL;
+    return guarded(el->ctx, [&] {
+        if (el->nids > 0xFFFFFFFEull) fail(HSAW_EINVAL, "edge_text_install: node ids are 32-bit");
+        build_and_install(el->ctx, (uint32_t)el->nids, el->ne, el->dense.p, el->dense.p + el->ne,
+                          weight_mode == 0 ? el->w.p : nullptr, weight_mode, p_of, true);
     });
 }
 

@@ -285,6 +285,15 @@ int hsawh_device_from_cache(const char* path, int device, void* cuda_stream, voi
     return guarded([&] { *out = DeviceGraph::from_cache(path, device, cuda_stream).release(); });
 }
 
+int hsawh_device_from_edge_list(const char* path, int weight_mode, int device, void* cuda_stream,
+                                void** out) {
+    return guarded([&] {
+        *out = DeviceGraph::from_edge_list(path, static_cast<WeightMode>(weight_mode), device,
+                                           cuda_stream)
+                   .release();
+    });
+}
+
 int hsawh_device_set_suspects(void* dg, const void* g, const double* p_of) {
     return guarded([&] {
         SuspectSet vi = dense_suspects(G(g), p_of);

@@ -264,6 +264,56 @@ std::unique_ptr<DeviceGraph> DeviceGraph::from_cache(const std::string& path, in
     return dg;
 }
 
+std::unique_ptr<DeviceGraph> DeviceGraph::from_edge_list(const std::string& path, WeightMode mode,
+                                                         int device, void* cuda_stream) {
+    if (mode == WeightMode::RandomNormalized) return nullptr;  // host draw stream
+    int fd = ::open(path.c_str(), O_RDONLY);
+    if (fd < 0) throw DataError("cannot open edge list: " + path);
+    struct stat st {};
+    if (::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode) || st.st_size == 0) {
+        ::close(fd);
+        return nullptr;
+    }
+    const std::size_t bytes = static_cast<std::size_t>(st.st_size);
+    void* base = ::mmap(nullptr, bytes, PROT_READ, MAP_PRIVATE, fd, 0);
+    ::close(fd);
+    if (base == MAP_FAILED) return nullptr;
+    struct Unmap {
+        void* p;
+        std::size_t n;
+        ~Unmap() { ::munmap(p, n); }
+    } unmap{base, bytes};
+    ::madvise(base, bytes, MADV_SEQUENTIAL);
+
+    std::unique_ptr<DeviceGraph> dg(new DeviceGraph());
+    if (hsaw_gpu_ctx_create(device, cuda_stream, &dg->ctx_) != HSAW_OK) {
+        dg->ctx_ = nullptr;
+        throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");
+    }
+    hsaw_gpu_edge_text* el = nullptr;
+    std::uint64_t ne = 0, nids = 0, host_line = 0;
+    int identity = 0;
+    const int given = mode == WeightMode::Given ? 1 : 0;
+    int rc = hsaw_gpu_edge_text_parse(dg->ctx_, static_cast<const char*>(base), bytes, given, given,
+                                      &el, &ne, &nids, &identity, &host_line);
+    if (rc != HSAW_OK) raise(rc, dg->ctx_, "from_edge_list");
+    if (host_line != 0 || el == nullptr) return nullptr;  // host loader's business (incl. "no edges")
+    struct ElGuard {
+        hsaw_gpu_edge_text* e;
+        ~ElGuard() { hsaw_gpu_edge_text_free(e); }
+    } el_guard{el};
+    rc = hsaw_gpu_edge_text_install(el, given ? 0 : 1, nullptr);
+    if (rc != HSAW_OK) {
+        std::string msg = hsaw_gpu_last_error(dg->ctx_);
+        if (rc == HSAW_EDATA) throw DataError(msg);  // build_graph's / validate()'s own messages
+        if (rc == HSAW_EINVAL) throw std::invalid_argument(msg);
+        throw DeviceError(msg);
+    }
+    dg->n_ = static_cast<NodeId>(nids);
+    dg->m_ = static_cast<EdgeId>(ne);
+    return dg;
+}
+
 // ---- DeviceGraph --------------------------------------------------------------------------------
 DeviceGraph::DeviceGraph(const ProbGraph& g, const SuspectSet& vi, int device, void* cuda_stream)
     : n_(g.n), m_(g.m) {

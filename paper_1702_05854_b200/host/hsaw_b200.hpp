@@ -175,6 +175,12 @@ public:
     // No suspects yet: call set_suspects() before sampling.
     static std::unique_ptr<DeviceGraph> from_cache(const std::string& path, int device = 0,
                                                    void* cuda_stream = nullptr);
+    // Edge-list text file -> graph resident on the device (parse, re-rank, sort, sum and layout
+    // all on the GPU; hsaw_gpu_edge_text_parse + hsaw_gpu_edge_text_install), for
+    // WeightMode::Given / ::InDegree files within the device parser's plain grammar. Returns null
+    // when the file needs the host loader (load_edge_list_device + the constructor above).
+    static std::unique_ptr<DeviceGraph> from_edge_list(const std::string& path, WeightMode mode,
+                                                       int device = 0, void* cuda_stream = nullptr);
     ~DeviceGraph();
     DeviceGraph(const DeviceGraph&) = delete;
     DeviceGraph& operator=(const DeviceGraph&) = delete;

@@ -72,6 +72,7 @@ def lib() -> C.CDLL:
                                                     C.c_char_p, C.c_int, vpp]
     L.hsawh_graph_load_cache_device.argtypes = [C.c_char_p, C.c_int, vpp]
     L.hsawh_device_from_cache.argtypes = [C.c_char_p, C.c_int, vp, vpp]
+    L.hsawh_device_from_edge_list.argtypes = [C.c_char_p, C.c_int, C.c_int, vp, vpp]
     L.hsawh_device_set_suspects.argtypes = [vp, vp, f64p]
     L.hsawh_lt_forward_simulate.argtypes = [vp, vp, f64p, u64p, u32p]
     L.hsawh_estimate_suspension.argtypes = [vp, vp, f64p, C.c_int, u32p, C.c_uint64, C.c_double,
@@ -233,6 +234,16 @@ class DeviceGraph:
                                            C.c_void_p(cuda_stream) if cuda_stream else None,
                                            C.byref(self.h)))
         return self
+
+    @classmethod
+    def from_edge_list(cls, path, mode=1, device=0, cuda_stream: int | None = None):
+        """hsaw::DeviceGraph::from_edge_list: text file -> resident graph (None: host loader needed)."""
+        self = cls.__new__(cls)
+        self.graph, self.p_of, self.h = None, None, C.c_void_p()
+        _chk(lib().hsawh_device_from_edge_list(str(path).encode(), mode, device,
+                                               C.c_void_p(cuda_stream) if cuda_stream else None,
+                                               C.byref(self.h)))
+        return self if self.h else None
 
     def set_suspects(self, graph: "Graph", p_of):
         self.graph = graph

@@ -217,3 +217,40 @@ def test_full_size_text_round_trip(tmp_path):
     assert np.array_equal(bdst, np.searchsorted(present, dst).astype(np.uint32))
     assert boff[0] == 0 and np.array_equal(boff[1:], off[present.astype(np.int64) + 1])
     assert np.array_equal(cum.view(np.uint64), bcum.view(np.uint64))
+
+
+def test_text_to_resident_graph_without_host_csr(tmp_path, gpu_lib):
+    """DeviceGraph::from_edge_list / hsaw_gpu_edge_text_install: the parsed edges are sorted,
+    summed and laid out where they lie on the device; sampling equals the host-loaded graph's."""
+    from paper_1702_05854_b200 import hostapi
+    s = hostapi.Graph.synth(3000, 6, 11)
+    p = tmp_path / "s.edges"
+    s.save_edge_list(p)
+    for mode in (0, 1):
+        g = hostapi.Graph.load_edge_list(p, mode=mode)
+        p_of = g.random_suspects(30, seed=4)
+        with hostapi.DeviceGraph(g, p_of) as dg:
+            want = dg.sample(2000, seed=5)
+            est = hostapi.estimate_suspension(g, p_of, 0, [3, 4, 5], 0.3, 0.2, 9, dg=dg)
+        dg = hostapi.DeviceGraph.from_edge_list(p, mode=mode)
+        assert dg is not None
+        with dg:
+            dg.set_suspects(g, p_of)
+            assert dg.sample(2000, seed=5) == want
+            assert hostapi.estimate_suspension(g, p_of, 0, [3, 4, 5], 0.3, 0.2, 9, dg=dg) == est
+    # outside the plain grammar / host-only modes: no device graph, the host loader decides
+    odd = tmp_path / "odd.edges"
+    odd.write_text("0 1 0.5\n1 2 +0.25\n")
+    assert hostapi.DeviceGraph.from_edge_list(odd, mode=0) is None
+    assert hostapi.DeviceGraph.from_edge_list(p, mode=2) is None
+    # data errors surface with build_graph's messages
+    dup = tmp_path / "dup.edges"
+    dup.write_text("0 1 0.5\n0 1 0.25\n")
+    with pytest.raises(hostapi.HsawError) as ei:
+        hostapi.DeviceGraph.from_edge_list(dup, mode=0)
+    assert ei.value.status == 2 and "duplicate edge 0 -> 1" in str(ei.value)
+    with gpu_lib.Context(0) as ctx:
+        assert ctx.upload_edge_text(b"5 7\n7 9\n9 5\n", weight_mode=1,
+                                    p_of=np.array([1.0, 0.0, 0.0])) == (3, 3)
+        seeds, lens, counts, _ = ctx.encode_batches(0, 4)
+        assert counts.sum() > 0

@@ -23,6 +23,13 @@ def main():
         path = os.path.join(tmp, "g.edges")
         g.save_edge_list(path)
         out = {"n": g.n, "m": g.m, "file_bytes": os.path.getsize(path), "graph": kind}
+        t0 = time.perf_counter()
+        for _ in range(2):
+            t0 = time.perf_counter()
+            dg = hostapi.DeviceGraph.from_edge_list(path, mode=1)
+            out["device_text_to_resident_graph_s"] = time.perf_counter() - t0
+            if dg is not None:
+                dg.close()
         for name, fn in (("device_load_edge_list_s", hostapi.Graph.load_edge_list_device),
                          ("device_load_edge_list_2nd_s", hostapi.Graph.load_edge_list_device),
                          ("host_load_edge_list_s", hostapi.Graph.load_edge_list)):
