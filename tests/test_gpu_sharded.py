@@ -104,7 +104,13 @@ def _worker(rank, world, port_no, kind, k, out_q):
             ctx.upload_graph(n, m, z["in_offsets"], z["in_src"], z["in_cum"], z["p_of"])
             eng = GpuEngine(ctx, seed=3)
             try:
-                res = ShardedSolver(eng, Comm()).interdict(n, kind, k, 0.2, 0.1)
+                if isinstance(kind, dict):  # a forward-simulation case (estimate_suspension)
+                    c = kind
+                    res = ShardedSolver(eng, Comm()).estimate_suspension(
+                        n, int(np.count_nonzero(z["p_of"])), c["kind"], c["ids"], c["epsilon"],
+                        c["delta"], c["state0"], batch_runs=513)
+                else:
+                    res = ShardedSolver(eng, Comm()).interdict(n, kind, k, 0.2, 0.1)
             finally:
                 eng.close()
         out_q.put((rank, res))
@@ -125,3 +131,24 @@ def test_two_ranks_on_one_gpu(golden, kind, key):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert results[0] == results[1] == golden["synth3000"][key]
+
+
+def test_two_ranks_on_one_gpu_estimate_suspension():
+    """Runs of the paired forward simulation split over two processes (device kernels on cuda:0,
+    gloo for the per-batch all-gather of the counts): the reference's value / runs / state."""
+    import json
+    with open(os.path.join(GOLDEN_DIR, "evaluation_vectors.json")) as f:
+        c = json.load(f)["synth3000"]["estimate_suspension"][2]
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port_no = _free_port()
+    procs = [mpc.Process(target=_worker, args=(r, 2, port_no, c, 0, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = dict(value=float.fromhex(c["value"]), capped=c["capped"], runs=c["runs"],
+                state=c["state_after"])
+    assert results[0] == results[1] == want
