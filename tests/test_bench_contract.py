@@ -54,3 +54,8 @@ def test_b200_arm_line():
     assert d["gpu_launches"] > 0 and {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert "workload" in d["config"] and "model" not in d["config"]
     assert d["esia"]["passed_check"] in (True, False) and d["esia"]["same_result_e2e"] is True
+    # the legs either side of the path: forward simulation of the solution, the k = 1000 solve
+    s = d["suspension"]
+    assert "error" not in s and s["paired_runs_per_sec"] > 0 and s["mean_residual"] <= s["mean_full"]
+    assert s["estimate"]["runs"] >= 1 and s["cpu_baseline"]["runs_per_sec"] > 0
+    assert d["esia_k1000"]["k"] == 1000 and d["esia_k1000"]["seconds_to_solution"] > 0
