@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(1024) greedy_tail_kernel(
     const uint32_t* __restrict__ inv, uint32_t* cnt, uint32_t* covered, uint64_t* blkmax,
     uint32_t nblk, uint32_t first, uint32_t k, uint32_t* __restrict__ solution,
     uint64_t* __restrict__ gains, uint32_t min_indexed, uint32_t max_list,
-    uint32_t* __restrict__ done_out) {
+    uint32_t* __restrict__ done_out, int bounds_exact) {
     // s_max[b]: upper bound of block b's maximum key; s_exact bit b: the bound IS the maximum.
     // A bound is made exact by recomputing the block and stays exact until the item that attains
     // it is decremented (decrements of other items cannot change a maximum), which the cover
@@ -351,7 +351,10 @@ __global__ void __launch_bounds__(1024) greedy_tail_kernel(
     const uint32_t limit = v.limit;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     for (uint32_t b = threadIdx.x; b < nblk; b += blockDim.x) s_max[b] = blkmax[b];
-    for (uint32_t b = threadIdx.x; b < (nblk + 31) / 32; b += blockDim.x) s_exact[b] = 0;
+    // bounds_exact: blkmax comes straight from block_maxima (no grid-wide round has decremented
+    // anything since), so every bound already is its block's maximum
+    for (uint32_t b = threadIdx.x; b < (nblk + 31) / 32; b += blockDim.x)
+        s_exact[b] = bounds_exact ? 0xFFFFFFFFu : 0u;
     __syncthreads();
     uint32_t r = first;
     for (; r < k; ++r) {
@@ -415,26 +418,74 @@ __global__ void __launch_bounds__(1024) greedy_tail_kernel(
         // ---- cover: the block's warps share the winner's inverted list, one walk per warp at a
         // time (lane-parallel claiming and a shared-memory queue of claimed walks were both
         // measured slower: the round is a chain of ~7 dependent memory round trips either way)
-        for (uint64_t i = lb + warp; i < le; i += nwarps) {
-            uint32_t lw = inv[i];
+        // two walks per warp and iteration: their list entries, claims (lanes 0 and 1), extents
+        // and items are fetched side by side, so each trip of the dependent chain
+        // inv -> {claim, extent} -> items serves two walks. A walk listed twice (an item that
+        // occurs twice in it) is claimed by exactly one of the two atomics, as before.
+        for (uint64_t i = lb + warp; i < le; i += 2 * nwarps) {
+            const uint64_t i2 = i + nwarps;
+            const bool has2 = i2 < le;
+            const uint32_t lw1 = inv[i];
+            const uint32_t lw2 = has2 ? inv[i2] : 0u;
             uint32_t old = 0;
-            if (lane == 0) old = atomicOr(&covered[lw >> 5], 1u << (lw & 31));
-            old = __shfl_sync(kFullMask, old, 0);
-            if (old & (1u << (lw & 31))) continue;  // already covered
-            uint64_t w = v.w0 + lw;
-            uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
-            for (uint64_t q = b + lane; q < e; q += 32) {
-                uint32_t it = v.items[q];
-                if (it < limit && is_cand(cand_bits, it)) {
-                    atomicSub(&cnt[it], 1u);
-                    const uint32_t blk = it / kMaxBlockItems;
-                    if ((uint32_t)s_max[blk] == 0xFFFFFFFFu - it)  // the item attaining the bound
-                        atomicAnd(&s_exact[blk >> 5], ~(1u << (blk & 31)));
+            if (lane == 0) old = atomicOr(&covered[lw1 >> 5], 1u << (lw1 & 31));
+            if (lane == 1 && has2) old = atomicOr(&covered[lw2 >> 5], 1u << (lw2 & 31));
+            // the extents are fetched while the claims are in flight: one round trip less on the
+            // round's dependent chain (a claim that fails wastes two loads)
+            const uint64_t w1 = v.w0 + lw1, w2 = v.w0 + lw2;
+            const uint64_t b1 = v.off[w1] + v.add * w1, e1 = v.off[w1 + 1] + v.add * (w1 + 1);
+            uint64_t b2 = 0, e2 = 0;
+            if (has2) {
+                b2 = v.off[w2] + v.add * w2;
+                e2 = v.off[w2 + 1] + v.add * (w2 + 1);
+            }
+            const uint32_t old1 = __shfl_sync(kFullMask, old, 0);
+            const uint32_t old2 = __shfl_sync(kFullMask, old, 1);
+            const uint64_t len1 = (old1 & (1u << (lw1 & 31))) ? 0 : e1 - b1;  // 0: already covered
+            const uint64_t len2 = (!has2 || (old2 & (1u << (lw2 & 31)))) ? 0 : e2 - b2;
+            const uint64_t longest = len1 > len2 ? len1 : len2;
+            for (uint64_t q = lane; q < longest; q += 32) {
+                uint32_t it1 = 0xFFFFFFFFu, it2 = 0xFFFFFFFFu;
+                if (q < len1) it1 = v.items[b1 + q];
+                if (q < len2) it2 = v.items[b2 + q];
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    const uint32_t it = s2 ? it2 : it1;
+                    if (it < limit && is_cand(cand_bits, it)) {
+                        atomicSub(&cnt[it], 1u);
+                        const uint32_t blk = it / kMaxBlockItems;
+                        if ((uint32_t)s_max[blk] == 0xFFFFFFFFu - it)  // the item attaining the bound
+                            atomicAnd(&s_exact[blk >> 5], ~(1u << (blk & 31)));
+                    }
                 }
             }
         }
-        __threadfence();
+        // One CTA owns the counts for the whole launch: the barrier alone orders this round's
+        // count atomics before the next round's ld.global.cg reads (CTA-scope visibility is all
+        // that is needed; a device-scope fence here cost a full round trip and an L1 flush per
+        // round). The kernel boundary publishes everything to the grid-wide kernels.
         __syncthreads();
+        // The winner's count just dropped, so its block's bound is stale by construction and - being
+        // the largest key of the last round - would surface first in the next selection only to
+        // be recomputed there and make that selection start over. Tighten it now instead.
+        {
+            const uint32_t wb = item / kMaxBlockItems;
+            const uint64_t base = (uint64_t)wb * kMaxBlockItems;
+            uint64_t exact = 0;
+            for (uint32_t i = threadIdx.x; i < kMaxBlockItems; i += blockDim.x) {
+                uint64_t id = base + i;
+                if (id < limit) {
+                    uint64_t key = gain_key(__ldcg(cnt + id), (uint32_t)id);
+                    exact = key > exact ? key : exact;
+                }
+            }
+            exact = block_max_u64(exact, smem);
+            if (threadIdx.x == 0) {
+                s_max[wb] = exact;
+                s_exact[wb >> 5] |= 1u << (wb & 31);
+            }
+            __syncthreads();
+        }
     }
     // hand the bounds back to the grid-wide kernels and report progress
     for (uint32_t b = threadIdx.x; b < nblk; b += blockDim.x) blkmax[b] = s_max[b];
@@ -793,6 +844,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             }
             done = 0;
             bool exhausted = p1 == p0;
+            bool blkmax_fresh = p1 > p0;  // block_maxima just ran: the bounds are exact maxima
             // Rounds with long lists go to the grid-wide kernel pair, a few at a time; as soon as
             // the lists are short the single-CTA tail kernel takes all remaining rounds in one
             // launch (it hands a round back if its list is too long after all).
@@ -820,7 +872,9 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                         StageScope timer(ctx, HSAW_STAGE_ROUNDS);
                         greedy_tail_kernel<<<1, 1024, tail_smem, st>>>(
                             v, d_cand, d_pos.p, d_inv.p, d_cnt.p, d_cov.p, d_blkmax.p, nblk, done,
-                            k, d_sol.p, d_gain.p, min_count, kMaxTailList, d_done);
+                            k, d_sol.p, d_gain.p, min_count, kMaxTailList, d_done,
+                            blkmax_fresh ? 1 : 0);
+                        blkmax_fresh = false;  // the tail's own rounds decrement counts
                         check_launch(ctx, "greedy_tail_kernel");
                     }
                     uint32_t h_done = 0;
@@ -830,6 +884,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                     upto = h_done;
                     try_tail = false;  // if rounds are left, the next one has a long list
                 } else {
+                    blkmax_fresh = false;
                     uint32_t group = std::min<uint32_t>(k - done, tail_ok ? 4 : 64);
                     StageScope timer(ctx, HSAW_STAGE_ROUNDS);
                     for (uint32_t r = done; r < done + group; ++r) {
