@@ -393,6 +393,11 @@ __global__ void __launch_bounds__(1024) greedy_tail_kernel(
             __syncthreads();
             if (exact == top) break;
         }
+        // Every thread must have taken its exit from the selection loop (which reads s_exact)
+        // before any warp starts covering (which clears s_exact bits): without this barrier a slow
+        // warp could see the top block's bit already cleared by a fast one and go on recomputing
+        // alone - found by compute-sanitizer racecheck as barrier-mismatch hazards.
+        __syncthreads();
         const uint32_t gain = (uint32_t)(top >> 32);
         const uint32_t item = 0xFFFFFFFFu - (uint32_t)top;
         const bool unindexed = gain != 0 && gain < min_indexed;
