@@ -123,6 +123,10 @@ InterdictionResult run_on_device(const DeviceGraph& dg, const ProbGraph& g,
         // greedy run and coverage counts. Only the final iteration's solution is ever reported
         // (interdiction.cpp:49-61), so the result is unchanged. HSAW_SKIP_BOUND=0 disables.
         if (skip_by_bound && static_cast<double>(size) < sched.n_max) {
+            // Cov_R'(S) <= |R'_t| = size for every S: while size < Lambda_1 (always the case at
+            // t = 1, where size = ceil(Lambda) and Lambda_1 = 1 + (1 + eps) Lambda) no histogram
+            // is needed to know the answer
+            if (static_cast<double>(size) < sched.lambda1) continue;
             ts = Clock::now();
             const auto bound = static_cast<double>(out_of_sample.coverage_upper_bound(k));
             res.check_s += seconds_since(ts);

@@ -426,8 +426,9 @@ class ShardedSolver:
             self.ensure(2 * size)
             # an iteration whose R'_t cannot reach Lambda_1 with any k candidates cannot pass the
             # check (coverage.cpp:216-217): skip its greedy run unless N_max ends the loop here
-            if float(size) < sched["n_max"] and \
-                    self.coverage_upper_bound(k, kind, size, size, cand) < sched["lambda1"]:
+            if float(size) < sched["n_max"] and (
+                    float(size) < sched["lambda1"]  # Cov_R'(S) <= |R'_t| = size
+                    or self.coverage_upper_bound(k, kind, size, size, cand) < sched["lambda1"]):
                 continue
             solution, coverage = self.greedy(k, kind, size, cand)
             cov_r = self.coverage_of(solution, kind, 0, size, cand)
