@@ -14,6 +14,7 @@
 // also words the errors. Results are therefore identical by construction on the plain grammar and
 // by delegation elsewhere.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <vector>
@@ -294,7 +295,7 @@ int hsaw_gpu_edge_text_parse(hsaw_gpu_ctx* ctx, const char* text, uint64_t bytes
             HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
             start.ensure_scratch(newlines + 1);
         }
-        cub::CountingInputIterator<uint64_t> positions(0);
+        thrust::counting_iterator<uint64_t> positions(0);
         LineStart pred{d_text.p};
         size_t tmp = 0;
         HSAW_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tmp, positions, start.p, d_n, (int64_t)bytes,
