@@ -1,18 +1,26 @@
 #!/usr/bin/env python
-"""bench.py — HSAWs/sec (and eSIA seconds-to-solution) of the B200 HSAW path.
+"""bench.py — HSAWs/sec and eSIA seconds-to-solution of the B200 HSAW path.
 
 Contract: `python bench.py --gpus N --steps K --warmup W [--impl reference]` prints ONE JSON line.
 
-Workload at N=1 = BASELINE.json configs[1] ("C2"): R-MAT scale 20 (2^20 nodes, ~16.1 M edges after
-dedupe), LT weights 1/in-degree, 1 % suspects with p ~ U(0,1), stream seed 42, the reference's
-default sampler (Brent + window 2, 10 chained attempts per batch).
+Workload at N=1 = the configuration BASELINE.json quotes its metric on ("C4", configs[3]): the
+Twitter-shape R-MAT graph — 41.65 M nodes, ~1.47 G edges after removing self-loops and duplicates,
+(a,b,c,d) = (.57,.19,.19,.05), generator seed 1 — with LT weights 1/in-degree, 1 % suspects with
+p ~ U(0,1) (seed 2), stream seed 42, the reference's default sampler (Brent + window 2, 10 chained
+attempts per batch), eSIA k = 1000, eps 0.1, delta 1/n. The graph is generated, sorted,
+deduplicated and summed on the device (csrc/rmat.cu, bit-identical to the sequential host generator
+hsaw::rmat_graph_n) and fits one B200 (48 GB in the 32-byte edge-record layout).
+`--workload c2|c3|c5` select the other BASELINE shapes; `--scale S --edge-factor F` a power-of-two
+R-MAT of any size (tests).
+
 A *step* = one pass of the sampling hot path over one batch range: 2^20 batches (10.49 M attempts)
-are generated (K1), replayed (K2), exactly rechecked (K2b) and compacted into the device-resident
+are generated and materialised (K1), exactly rechecked (K2b) and compacted into the device-resident
 pool in the reference's (batch, seq) order. `value` = accepted (post-recheck) HSAWs per second over
-the K timed steps with the graph already resident in HBM. `e2e` = the same metric through the
-reference-facing host call with HOST buffers (graph arrays uploaded inside the timed region, result
-counters read back). The eSIA k=100 seconds-to-solution of the same config rides along in "esia".
-With --gpus N>1 (torchrun) the graph is replicated, every rank samples its own batch ranges (weak
+the K timed steps with the graph resident in HBM. `e2e` = the same metric through the
+reference-facing host call with HOST buffers: the reference's own CSR arrays are uploaded inside the
+timed call (18 GB at C4), sampled, and the counters read back. `esia` carries the seconds-to-solution
+half of the metric, device-resident and host-to-result. With --gpus N > 1 (torchrun) the graph is
+replicated (each rank generates it on its own GPU), every rank samples its own batch ranges (weak
 scaling, no data-path collective) and the rates are summed over ranks / max over ranks' time.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref: the unmodified
@@ -38,6 +46,22 @@ import numpy as np  # noqa: E402
 METRIC = "hsaw_per_sec"
 UNIT = "HSAW/s"
 STREAM_SEED = 42
+GEN_SEED, SUSPECT_SEED = 1, 2
+
+# BASELINE.json configs[1..4]. n = the node count the shape is named after; raw = R-MAT edges drawn
+# (self-loops, endpoints >= n and duplicates are dropped afterwards), calibrated so that the edge
+# count after deduplication lands on the named figure.
+WORKLOADS = {
+    "c2": dict(name="C2", n=1 << 20, raw=16 << 20, k=100,
+               what="R-MAT 1M nodes / 16M edges (configs[1])"),
+    "c3": dict(name="C3", n=4_847_571, raw=93_000_000, k=100,
+               what="LiveJournal-shape R-MAT 4.8M nodes / 69M edges (configs[2])"),
+    "c4": dict(name="C4", n=41_652_230, raw=1_990_000_000, k=1000,
+               what="Twitter-shape R-MAT 41.7M nodes / 1.47B edges (configs[3], the configuration "
+                    "BASELINE.json's metric is quoted on)"),
+    "c5": dict(name="C5", n=65_608_366, raw=3_900_000_000, k=1000,
+               what="Friendster-shape R-MAT 65.6M nodes / 3.6B directed edges (configs[4])"),
+}
 
 
 def parse_args():
@@ -46,14 +70,20 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--scale", type=int, default=20, help="R-MAT scale (2^scale nodes)")
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--scale", type=int, default=None,
+                    help="instead of --workload: power-of-two R-MAT with 2^scale nodes")
     ap.add_argument("--edge-factor", type=float, default=16.0)
+    ap.add_argument("--nodes", type=int, default=None, help="override the workload's node count")
+    ap.add_argument("--raw-edges", type=int, default=None, help="override the raw edge count")
     ap.add_argument("--batches", type=int, default=1 << 20, help="batches per step per GPU")
-    ap.add_argument("--esia-k", type=int, default=100)
+    ap.add_argument("--esia-k", type=int, default=None,
+                    help="budget of the timed solve (default: the workload's, 1000 at C4)")
     ap.add_argument("--no-esia", action="store_true")
     ap.add_argument("--solver", default="esia", choices=["esia", "nsia"],
                     help="interdiction driver timed beside the sampler (edge or node candidates)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ingest", action="store_true",
                     help="also time the step before the path (SURVEY 8f row 1): HSAW1 cache and "
                          "edge-list text of a graph of this size -> ProbGraph / resident graph, "
@@ -62,23 +92,70 @@ def parse_args():
                     help="skip the forward-simulation leg (estimate_suspension of the solution)")
     ap.add_argument("--no-l2-flush", action="store_true",
                     help="A/B only: skip the L2 flush between timed steps")
-    ap.add_argument("--cpu-target", type=int, default=300_000,
+    ap.add_argument("--cpu-target", type=int, default=None,
                     help="HSAWs of the bounded CPU sample (cpu_baseline / reference arm step)")
-    return ap.parse_args()
+    ap.add_argument("--cpu-esia", action="store_true",
+                    help="run the reference's eSIA on the C2 shape on this box's cores now (minutes) "
+                         "and refresh profiles/cpu_esia_cache.json")
+    args = ap.parse_args()
+    if args.scale is not None:
+        n = 1 << args.scale
+        args.shape = dict(name=f"R-MAT scale {args.scale}", n=n, raw=int(args.edge_factor * n),
+                          k=100, what=f"power-of-two R-MAT, edge factor {args.edge_factor:g}")
+        if args.scale == 20 and args.edge_factor == 16.0:
+            args.shape = dict(WORKLOADS["c2"])
+    else:
+        args.shape = dict(WORKLOADS[args.workload])
+    if args.nodes:
+        args.shape["n"] = args.nodes
+    if args.raw_edges is not None:
+        args.shape["raw"] = args.raw_edges
+    if args.esia_k is None:
+        args.esia_k = args.shape["k"]
+    if args.cpu_target is None:
+        args.cpu_target = 300_000 if args.shape["n"] <= (1 << 23) else 200_000
+    return args
 
 
 def workload_name(args, n, m):
-    return (f"C2 R-MAT scale {args.scale} ({n} nodes, {m} edges after dedupe), LT weights "
-            f"1/in-degree, {max(1, n // 100)} suspects p~U(0,1), stream seed {STREAM_SEED}, "
-            f"Brent+window(2), 10 attempts/batch")
+    sh = args.shape
+    return (f"{sh['name']}: {sh['what']}; generated {n} nodes ({n / 1e6:.2f} M), {m} edges "
+            f"({m / 1e9:.3f} G) after dedupe from {sh['raw']} raw R-MAT(.57,.19,.19,.05) edges, "
+            f"generator seed {GEN_SEED}; LT weights 1/in-degree, {max(1, n // 100)} suspects "
+            f"p~U(0,1) (seed {SUSPECT_SEED}), stream seed {STREAM_SEED}, Brent+window(2), "
+            f"10 attempts/batch")
 
 
-def make_inputs(args):
-    """The same CSR arrays go to the GPU path and to the CPU reference."""
+def host_ram_available():
+    try:
+        import psutil
+        return int(psutil.virtual_memory().available)
+    except Exception:
+        return 0
+
+
+def have_cuda():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def suspects(n):
     from paper_1702_05854_b200 import hostapi
-    g = hostapi.Graph.rmat(args.scale, args.edge_factor, seed=1)
-    p_of = g.random_suspects(max(1, g.n // 100), seed=2)
-    return g, p_of
+    return hostapi.random_suspects_n(n, max(1, n // 100), SUSPECT_SEED)
+
+
+def host_graph(args, device=0):
+    """The workload's CSR as host arrays (what the reference consumes): generated on the GPU when one
+    is present (seconds at C4), by the sequential host generator otherwise — the two are
+    bit-identical (tests/test_gpu_rmat.py). Lean: in_offsets / in_src / in_cum only."""
+    from paper_1702_05854_b200 import hostapi
+    sh = args.shape
+    if have_cuda():
+        return hostapi.Graph.rmat_device(sh["n"], sh["raw"], GEN_SEED, device=device, lean=True)
+    return hostapi.Graph.rmat_n(sh["n"], sh["raw"], GEN_SEED)
 
 
 class ClockSampler(threading.Thread):
@@ -125,24 +202,92 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md, 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """dram bytes per K1 launch from the committed ncu capture, if one exists for this workload."""
+def ncu_traffic(shape_name, layout):
+    """DRAM bytes per K1 launch from the committed `ncu --set full` capture of THIS workload and
+    layout (profiles/k1_traffic.json, one entry per capture); None when there is none."""
     try:
         with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
-            return json.load(f)
+            return json.load(f).get(f"{shape_name.lower()}:{layout}")
     except Exception:
         return None
 
 
-def cpu_reference_rate(args, g, p_of, target, seed, workers):
-    """Reference CPU stream_samples on the host cores -> (HSAW/s, accepted, attempts, kind)."""
+def cpu_esia_cache():
+    """The reference's eSIA on the C2 shape (the largest shape its CoverageIndex fits and finishes
+    in minutes on), timed on host cores: cached runs, one per (cpu model, cores)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "cpu_esia_cache.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def cpu_model():
+    try:
+        return open("/proc/cpuinfo").read().split("model name")[1].split("\n")[0].strip(": \t")
+    except Exception:
+        return "unknown"
+
+
+def run_cpu_esia(cores):
+    """Reference esia() k=100 on the C2 arrays with all host threads -> cache entry."""
     from oracle import oracle
     from oracle.oracle import Csr
-    off, src, cum, _, _ = g.arrays()
+    from paper_1702_05854_b200 import hostapi
+    if not oracle.have_ref():
+        return None
+    sh = WORKLOADS["c2"]
+    g = (hostapi.Graph.rmat_device(sh["n"], sh["raw"], GEN_SEED, lean=False) if have_cuda()
+         else hostapi.Graph.rmat_n(sh["n"], sh["raw"], GEN_SEED))
+    p_of = suspects(g.n)
+    off, src, cum = g.views()
     csr = Csr(g.n, g.m, off, src, cum, p_of)
+    R = oracle.Ref()
+    with R.handles(csr) as hd:
+        r = R.interdict(csr, 0, 100, 0.1, 1.0 / g.n, seed=STREAM_SEED, workers=cores,
+                        max_attempts=10**15, hd=hd, want_json=True)
+    entry = {"config": "C2 (R-MAT 2^20 nodes / 16.09 M edges) eSIA k=100 eps 0.1 delta 1/n seed 42",
+             "seconds_to_solution": r["wall_time_s"], "cores": cores, "cpu": cpu_model(),
+             "kind": "reference", "iterations": r["iterations"], "samples_used": r["samples_used"],
+             "attempts": r["attempts"], "coverage": r["coverage"],
+             "est_suspension": r["est_suspension"], "solution_head": r["solution"][:5],
+             "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+    cache = cpu_esia_cache()
+    cache[f"{entry['cpu']} x{cores}"] = entry
+    try:
+        out_dir = os.path.join(ROOT, "gpurun_out")
+        os.makedirs(out_dir, exist_ok=True)
+        for path in (os.path.join(ROOT, "profiles", "cpu_esia_cache.json"),
+                     os.path.join(out_dir, "cpu_esia_cache.json")):
+            with open(path, "w") as f:
+                json.dump(cache, f, indent=1)
+    except Exception:
+        pass
+    return entry
+
+
+def cpu_seconds_to_solution(args, cores):
+    if args.cpu_esia:
+        e = run_cpu_esia(cores)
+        if e:
+            return dict(e, source="measured in this run")
+    cache = cpu_esia_cache()
+    key = f"{cpu_model()} x{cores}"
+    if key in cache:
+        return dict(cache[key], source="profiles/cpu_esia_cache.json (same cpu model and core count)")
+    if cache:
+        k0 = sorted(cache)[0]
+        return dict(cache[k0], source=f"profiles/cpu_esia_cache.json entry '{k0}' (a different host "
+                                      f"than this box: {key})")
+    return None
+
+
+def cpu_reference_rate(csr, target, seed, workers, lean):
+    """Reference CPU stream_samples on the host cores -> (HSAW/s, accepted, attempts, kind, ...)."""
+    from oracle import oracle
     if oracle.have_ref():
         R = oracle.Ref()
-        with R.handles(csr) as hd:
+        with R.handles(csr, lean=lean) as hd:
             t0 = time.perf_counter()
             ns, at, _ = R.stream_samples(csr, target, seed=seed, workers=workers,
                                          max_attempts=10**12, hd=hd, copy=False)
@@ -155,30 +300,72 @@ def cpu_reference_rate(args, g, p_of, target, seed, workers):
     return pool.nsamples / dt, pool.nsamples, pool.attempts, "port", 1, dt
 
 
+def cpu_footprint(n, m):
+    """Host bytes the CPU leg needs at once: our lean CSR + the reference's lean ProbGraph copy +
+    the per-worker DecodeContext mark arrays (4 n each, proj/include/hsaw/sampler.hpp:98-99)."""
+    cores = os.cpu_count() or 1
+    return 2 * (8 * (n + 1) + 12 * m) + 8 * n + cores * 4 * n + (2 << 30)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    g, p_of = make_inputs(args)
+    from oracle import oracle
+    from oracle.oracle import Csr
+    sh = args.shape
+    note = None
+    est_m = int(sh["raw"] * 0.75)
+    if cpu_footprint(sh["n"], est_m) > host_ram_available() > 0:
+        # never silently substitute (SURVEY 8d): say so and fall back to the C3 shape
+        note = (f"host RAM ({host_ram_available() >> 30} GiB available) cannot hold the reference's "
+                f"arrays for {sh['name']}; CPU arm ran the C3 shape instead")
+        args.shape = dict(WORKLOADS["c3"])
+        sh = args.shape
+    g = host_graph(args)
+    p_of = suspects(g.n)
+    off, src, cum = g.views()
+    csr = Csr(g.n, g.m, off, src, cum, p_of)
     cores = os.cpu_count() or 1
+    lean = g.m > (1 << 27)
     total, elapsed, kind, used = 0, 0.0, "reference", cores
-    for step in range(args.warmup + args.steps):
-        rate, ns, at, kind, used, dt = cpu_reference_rate(args, g, p_of, args.cpu_target,
-                                                          STREAM_SEED + step, cores)
-        if step >= args.warmup:
-            total += ns
-            elapsed += dt
+    R = oracle.Ref() if oracle.have_ref() else None
+    hd = R.handles(csr, lean=lean) if R else None
+    try:
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            if R:
+                ns, at, _ = R.stream_samples(csr, args.cpu_target, seed=STREAM_SEED + step,
+                                             workers=cores, max_attempts=10**12, hd=hd, copy=False)
+            else:
+                pool = oracle.Port().stream_samples(csr, args.cpu_target, seed=STREAM_SEED + step,
+                                                    max_attempts=10**12)
+                ns, kind, used = pool.nsamples, "port", 1
+            dt = time.perf_counter() - t0
+            if step >= args.warmup:
+                total += ns
+                elapsed += dt
+    finally:
+        if hd is not None:
+            hd.__exit__(None, None, None)
     value = total / elapsed if elapsed > 0 else 0.0
     sample = (f"each step: stream_samples to {args.cpu_target} HSAWs (fresh stream seed "
               f"{STREAM_SEED}+step) with {used} worker threads")
+    cfg = {"workload": workload_name(args, g.n, g.m), "step": sample,
+           "inputs": "graph generated on the GPU before the timed region (bit-identical to the host "
+                     "generator), then the device is released; the timed calls use host cores only"
+                     if have_cuda() else "graph generated by the host generator"}
+    if note:
+        cfg["substituted"] = note
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * elapsed / max(args.steps, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
-        "config": {"workload": workload_name(args, g.n, g.m), "step": sample},
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": kind,
-                         "sample": sample},
+                         "sample": sample,
+                         "seconds_to_solution": cpu_seconds_to_solution(args, cores)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }))
@@ -215,13 +402,25 @@ def run_b200(args):
         else:
             dist.all_reduce(t, op=op)
 
-    g, p_of = make_inputs(args)  # identical on every rank (seeded generator): replicated graph
-    off, src, cum, _, _ = g.arrays()
-    ref_bytes = 8 * (g.n + 1) + 12 * g.m + 8 * g.n
-
+    sh = args.shape
+    n = sh["n"]
+    p_of = suspects(n)  # identical on every rank (seeded); the graph is replicated per GPU
     tstream = torch.cuda.Stream()
-    dg = hostapi.DeviceGraph(g, p_of, device=local, cuda_stream=tstream.cuda_stream)
+    # The graph never visits the host on the timed path: generated, sorted, deduplicated, summed
+    # and laid out on this rank's GPU. The host copy (the reference's arrays) is fetched only for
+    # the legs that need HOST buffers: e2e and the CPU baseline (rank 0, N = 1).
+    need_host = (world == 1 and not (args.no_e2e and args.no_cpu_baseline))
+    if need_host and cpu_footprint(n, int(sh["raw"] * 0.75)) // 2 > host_ram_available() > 0:
+        need_host = False
+    t0 = time.perf_counter()
+    dg = hostapi.DeviceGraph.from_rmat(n, sh["raw"], GEN_SEED, p_of, device=local,
+                                       cuda_stream=tstream.cuda_stream, want_host=need_host)
+    build_s = time.perf_counter() - t0
+    g = dg.graph  # lean host copy, or a shell with n and m
+    ref_bytes = 8 * (g.n + 1) + 12 * g.m + 8 * g.n
     ctx = capi.Context.borrow(dg.ctx_handle(), g.n, g.m)
+    layout = ctx.graph_layout
+    fat = layout == "fat"
     cfg = capi.SamplerCfg(max_attempts=10**15)
     B = args.batches
 
@@ -277,6 +476,7 @@ def run_b200(args):
     clock_info = clocks.stop()
     stages = ctx.stage_times(reset=True)
     launches = ctx.launches - launches0
+    del flush
     # Algorithmic work of exactly the timed batch ranges, counted by an untimed instrumented pass
     # (the production kernels run with the counters compiled out).
     delta = {k: 0 for k in capi.STAT_NAMES}
@@ -305,35 +505,47 @@ def run_b200(args):
     alg_bytes_per_launch = (delta["alg_bytes"] + log_bytes) / max(k1_n, 1)
     k1_avg_ms = k1_ms / max(k1_n, 1)
     achieved = alg_bytes_per_launch / (k1_avg_ms / 1e3) / 1e9 if k1_avg_ms > 0 else 0.0
-    traffic = ncu_traffic()
-    # Secondary roofline in the kernel's own unit: random sector gathers. On the compact layout a
-    # step is one in_src gather (live picks) plus one 16-byte header gather (arrivals, start nodes
-    # included); tools/gather_probe.cu measured what this B200 sustains for dependent random
-    # gathers (profiles/README.md): 212 G/s from a 64 MB table (L2 resident), 150 G/s at 96 MB,
-    # 49 G/s from HBM (every miss costs a 128-byte line).
-    gathers = (2 * delta["steps"] + delta["attempts"]) / max(k1_n, 1)
+    traffic = ncu_traffic(sh["name"], layout)
+    if fat:
+        kernel = ("encode_kernel<Brent,2,record,fat> (K1, walk generation + materialisation, "
+                  "32-byte edge records gathered from HBM)")
+        # one 32-byte edge-record gather per step (the record carries the row header of its
+        # source), plus a node-record gather per attempt start
+        gathers = (delta["steps"] + delta["attempts"]) / max(k1_n, 1)
+        probe = {"hbm_512MB": 49.0, "hbm_4GB": 38.0}
+        note = ("algorithmic bytes are the reference-layout figure of SURVEY.md 8(d) (offset pair + "
+                "binary-search probes + in_src + p_of per step); the fat layout serves a step from "
+                "ONE 32-byte record, but every L2 miss moves a 64..128-byte DRAM burst, so the "
+                "random-gather rate below is the kernel's own limit")
+    else:
+        kernel = ("encode_compact_kernel<Brent,2,record> (K1, walk generation + materialisation, "
+                  "compact L2-resident layout)")
+        # a step is one in_src gather (live picks) plus one 16-byte header gather (arrivals, start
+        # nodes included); tools/gather_probe.cu measured what this B200 sustains for dependent
+        # random gathers (profiles/README.md)
+        gathers = (2 * delta["steps"] + delta["attempts"]) / max(k1_n, 1)
+        probe = {"l2_resident_64MB": 212.0, "96MB": 150.0, "hbm_512MB": 49.0}
+        note = ("algorithmic bytes are the reference-layout figure of SURVEY.md 8(d); the compact "
+                "layout serves them from packed sources + 16-byte row headers that stay in L2, so "
+                "measured DRAM traffic is a fraction of it and frac can exceed 1: this shape is not "
+                "HBM-bound. The kernel's own limit is the random-gather rate below.")
     roofline = {
-        "bound": "hbm", "kernel": "encode_compact_kernel<Brent,2,record> (K1, walk generation + "
-                                  "materialisation, compact L2-resident layout)",
-        "achieved": achieved,
+        "bound": "hbm", "kernel": kernel, "achieved": achieved,
         "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+        "traffic_source": traffic.get("source") if traffic else None,
         "peak_source": peak_src,
         "algorithmic_bytes_per_launch": alg_bytes_per_launch,
         "bytes_per_step_formula": "28+8*ceil(log2 d) per successful pick (16 empty row, 24 no "
                                   "live edge) + 8 per node arrival (SURVEY.md 8d) + 8 per item "
                                   "of an accepted walk (logged by the same kernel)",
-        "note": "algorithmic bytes are the reference-layout figure of SURVEY.md 8(d); the device "
-                "layout serves them from 4-byte sources + 16-byte row headers that stay in L2, so "
-                "measured DRAM traffic (`traffic`) is a fraction of it and frac can exceed 1. The "
-                "kernel's own limit is the random-gather rate below.",
+        "note": note,
         "walk_log_bytes_per_launch": log_bytes / max(k1_n, 1),
         "kernel_avg_ms": k1_avg_ms, "launches_timed": k1_n,
         "k1_walk_steps_per_s": delta["steps"] / (k1_ms / 1e3) if k1_ms > 0 else None,
         "gather": {"gathers_per_launch_upper": gathers,
                    "achieved_ggathers_per_s": gathers / (k1_avg_ms / 1e3) / 1e9 if k1_avg_ms else None,
-                   "probe_peak_ggathers_per_s": {"l2_resident_64MB": 212.0, "96MB": 150.0,
-                                                 "hbm_512MB": 49.0}},
+                   "probe_peak_ggathers_per_s": probe},
         "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
         "k1_share_of_step": k1_ms / elapsed_ms if elapsed_ms > 0 else None,
     }
@@ -347,16 +559,21 @@ def run_b200(args):
             "workload": workload_name(args, g.n, g.m),
             "step": f"{B} batches ({10 * B} attempts) per GPU: K1 encode+record, K2b exact recheck, "
                     f"ordered compaction into the device pool (K2 replay only on log overflow)",
-            "layout": ("compact (in_src packed three 21-bit entries per 64-bit word + 16-byte row "
+            "layout": "fat (32-byte edge records, one HBM gather per step)" if fat else
+                      ("compact (in_src packed three 21-bit entries per 64-bit word + 16-byte row "
                        "headers, L2 resident)" if g.n <= 2**20 else
-                       "compact (4-byte in_src + 16-byte row headers; headers L2 resident)")
-                      if 16 * g.n <= 126 * 2**20 else "fat (32-byte edge records)",
+                       "compact (4-byte in_src + 16-byte row headers; headers L2 resident)"),
             "parallelism": f"walks sharded by batch range over {world} GPU(s), graph replicated",
             "l2_policy": (f"L2 flushed before every timed step (256 MB memset on the launching "
                           f"stream between the per-step event pairs); graph on device "
-                          f"{hsaw_mb(dg)} MB")
+                          f"{round(ctx.graph_bytes / 1e6, 1)} MB")
                          if not args.no_l2_flush else "NOT flushed (A/B run)",
             "graph_device_bytes": ctx.graph_bytes, "graph_reference_bytes": ref_bytes,
+            "graph_build_s": round(build_s, 3),
+            "graph_build": "R-MAT keys, radix sort, dedupe, CSR, 1/d row sums and the walk layout "
+                           "all on the device (csrc/rmat.cu)" +
+                           ("; the reference-layout CSR was also copied to the host for the e2e / "
+                            "CPU legs" if need_host else ""),
         },
         "attempts_per_sec": tot_att / (elapsed_ms / 1e3),
         "walk_steps_per_sec": tot_steps / (elapsed_ms / 1e3),
@@ -365,97 +582,45 @@ def run_b200(args):
         "roofline": roofline, "clocks": clock_info, "gpu_launches": int(tot_launches),
     }
 
-    # ---- end to end through the reference-facing host call, HOST buffers (rank 0's GPU only
-    # times its own share; ranks run the same call concurrently and the rates are summed)
-    target = max(1, int(accepted / max(args.steps, 1)))
-    e2e_acc, e2e_s = 0, 0.0
-    e2e_calls = max(1, min(args.steps, 5))
-    e2e_error = None
-    for i in range(-min(args.warmup, 2), e2e_calls):  # negative i: untimed warm-up calls
-        barrier()
-        t0 = time.perf_counter()
-        try:
-            with hostapi.DeviceGraph(g, p_of, device=local) as dg2:    # H2D of the CSR arrays
-                _, acc = dg2.sample(target, seed=STREAM_SEED + 1000 * rank + i + 100,
-                                    max_attempts=10**15)               # ensure + counters (D2H)
-        except Exception as exc:  # e.g. a second copy of a 50 GB graph does not fit next to the first
-            e2e_error, acc = str(exc)[:200], 0
-        torch.cuda.synchronize()
-        if i >= 0:
-            e2e_s += time.perf_counter() - t0
-            e2e_acc += acc
-    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    ce = torch.tensor([float(e2e_acc)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        all_reduce(te, dist.ReduceOp.MAX)
-        all_reduce(ce, dist.ReduceOp.SUM)
-    out["e2e"] = {
-        "value": float(ce.item()) / float(te.item()), "unit": UNIT,
-        "h2d_bytes_per_step": ref_bytes, "d2h_bytes_per_step": 16,
-        "call": f"DeviceGraph(g, vi) upload + SampleStream.ensure({target}) + counters_for "
-                f"(the `hsaw sample` path), per call",
-        "calls_timed": e2e_calls, "ms_per_call": 1e3 * float(te.item()) / e2e_calls,
-    }
-    if e2e_error:
-        out["e2e"]["error"] = e2e_error
-
-    # ---- eSIA seconds-to-solution on the same config (single GPU path)
+    # ---- seconds-to-solution on the same config, graph resident (single GPU path)
+    r_dev = None
     if not args.no_esia and world == 1:
         delta_ = 1.0 / g.n
         kind = 0 if args.solver == "esia" else 1
-        try:
-            runs = [hostapi.interdict(g, p_of, kind, args.esia_k, 0.1, delta_, seed=STREAM_SEED,
+
+        def solve(k, reps):
+            runs = [hostapi.interdict(g, p_of, kind, k, 0.1, delta_, seed=STREAM_SEED,
                                       max_attempts=10**15, dg=dg, want_json=True)
-                    for _ in range(3)]
-            r_dev = runs[-1]
-            try:
-                e2e_runs = [hostapi.interdict(g, p_of, kind, args.esia_k, 0.1, delta_,
-                                              seed=STREAM_SEED, max_attempts=10**15, device=local,
-                                              want_json=True) for _ in range(2)]
-            except Exception:  # a second copy of a very large graph may not fit beside the first
-                e2e_runs = [dict(r_dev, timing=dict(r_dev["timing"], wall_time_s=None))] * 2
-            r_e2e = e2e_runs[-1]
-            out[args.solver] = {
-                "k": args.esia_k, "epsilon": 0.1, "delta": delta_,
+                    for _ in range(reps)]
+            r = runs[-1]
+            return r, {
+                "k": k, "epsilon": 0.1, "delta": delta_,
                 # graph resident in HBM; first call pays one-time pool allocations, later calls reuse
-                "seconds_to_solution": r_dev["timing"]["wall_time_s"],
+                "seconds_to_solution": r["timing"]["wall_time_s"],
                 "seconds_to_solution_first_call": runs[0]["timing"]["wall_time_s"],
-                # host ProbGraph in, InterdictionResult out (upload + context creation inside)
-                "seconds_to_solution_e2e": r_e2e["timing"]["wall_time_s"],
-                "seconds_to_solution_e2e_first_call": e2e_runs[0]["timing"]["wall_time_s"],
-                "breakdown_s": {k: r_dev["timing"][k] for k in ("sample_s", "greedy_s", "check_s")},
-                "iterations": r_dev["iterations"], "samples_used": r_dev["samples_used"],
-                "attempts": r_dev["attempts"], "coverage": r_dev["coverage"],
-                "passed_check": r_dev["passed_check"], "est_suspension": r_dev["est_suspension"],
-                "solution_head": r_dev["solution"][:5],
-                "same_result_e2e": all(r_dev[k] == r_e2e[k]
-                                       for k in ("solution", "attempts", "coverage")),
+                "breakdown_s": {k_: r["timing"][k_] for k_ in ("sample_s", "greedy_s", "check_s")},
+                "iterations": r["iterations"], "samples_used": r["samples_used"],
+                "attempts": r["attempts"], "coverage": r["coverage"],
+                "passed_check": r["passed_check"], "est_suspension": r["est_suspension"],
+                "solution_head": r["solution"][:5],
             }
+        try:
+            r_dev, out[args.solver] = solve(args.esia_k, 3 if g.m < (1 << 28) else 2)
         except Exception as exc:  # e.g. the walk pool of a huge instance outgrowing HBM
             out[args.solver] = {"k": args.esia_k, "error": str(exc)[:300]}
-
-    # ---- BASELINE.json quotes seconds-to-solution at k = 1000: the same solve with that budget
-    if (not args.no_esia and world == 1 and args.esia_k != 1000 and args.solver == "esia"
-            and isinstance(out.get("esia"), dict) and "error" not in out["esia"]):
-        try:
-            r1k = [hostapi.interdict(g, p_of, 0, 1000, 0.1, 1.0 / g.n, seed=STREAM_SEED,
-                                     max_attempts=10**15, dg=dg, want_json=True)
-                   for _ in range(2)][-1]
-            out["esia_k1000"] = {
-                "k": 1000, "epsilon": 0.1, "delta": 1.0 / g.n,
-                "seconds_to_solution": r1k["timing"]["wall_time_s"],
-                "breakdown_s": {k: r1k["timing"][k] for k in ("sample_s", "greedy_s", "check_s")},
-                "iterations": r1k["iterations"], "samples_used": r1k["samples_used"],
-                "coverage": r1k["coverage"], "passed_check": r1k["passed_check"],
-                "est_suspension": r1k["est_suspension"],
-            }
-        except Exception as exc:
-            out["esia_k1000"] = {"k": 1000, "error": str(exc)[:300]}
+        # BASELINE.json quotes seconds-to-solution at k = 1000: always present as "esia_k1000"
+        if args.solver == "esia":
+            if args.esia_k == 1000:
+                out["esia_k1000"] = out["esia"]
+            elif "error" not in out["esia"]:
+                try:
+                    _, out["esia_k1000"] = solve(1000, 2)
+                except Exception as exc:
+                    out["esia_k1000"] = {"k": 1000, "error": str(exc)[:300]}
 
     # ---- the step after the path: paired LT forward simulation of the solution
     # just found, on the same resident graph. Informational; not part of `value`.
-    if (not args.no_esia and not args.no_suspension and world == 1
-            and isinstance(out.get(args.solver), dict) and "error" not in out[args.solver]):
+    if r_dev is not None and not args.no_suspension:
         try:
             kind = 0 if args.solver == "esia" else 1
             sol = np.asarray(r_dev["solution"], dtype=np.uint32)
@@ -481,41 +646,8 @@ def run_b200(args):
                 "estimate": {"epsilon": 0.1, "delta": 0.1, "value": est["value"],
                              "capped": est["capped"], "runs": est["runs"], "seconds": est_s},
             }
-            if rank == 0 and not args.no_cpu_baseline:
-                from oracle import oracle
-                from oracle.oracle import Csr
-                off, src, cum, _, _ = g.arrays()
-                csr = Csr(g.n, g.m, off, src, cum, p_of)
-                cpu_runs = 3
-                if oracle.have_ref():
-                    R = oracle.Ref()
-                    with R.handles(csr) as hd:
-                        t0, s_ = time.perf_counter(), 7
-                        for _ in range(cpu_runs):
-                            _, s_ = R.lt_forward_simulate(csr, s_, hd=hd)
-                        dt = time.perf_counter() - t0
-                    cpu_kind = "reference"
-                else:
-                    P = oracle.Port()
-                    t0, s_ = time.perf_counter(), 7
-                    for _ in range(cpu_runs):
-                        _, s_ = P.lt_forward_simulate(csr, s_)
-                    dt = time.perf_counter() - t0
-                    cpu_kind = "port"
-                out["suspension"]["cpu_baseline"] = {
-                    "runs_per_sec": cpu_runs / dt, "cores": 1, "kind": cpu_kind,
-                    "sample": f"{cpu_runs} x lt_forward_simulate (one realisation + one count; a "
-                              f"paired run does two counts), single-threaded like the reference",
-                }
         except Exception as exc:
             out["suspension"] = {"error": str(exc)[:300]}
-
-    # ---- the step before the path (SURVEY 8f row 1), on request: file -> graph
-    if args.ingest and world == 1:
-        try:
-            out["ingest"] = ingest_leg(args, rank == 0 and not args.no_cpu_baseline)
-        except Exception as exc:
-            out["ingest"] = {"error": str(exc)[:300]}
 
     # ---- N > 1: the sharded solve (walks sharded by batch range, marginal-gain counts combined
     # over NCCL; paper_1702_05854_b200/sharded.py). Every rank runs it; device-timed, max over ranks.
@@ -567,23 +699,122 @@ def run_b200(args):
         except Exception as exc:
             out[args.solver] = {"k": args.esia_k, "sharded_over": world, "error": str(exc)[:300]}
 
-    # ---- CPU baseline beside it: rank 0, N=1 only, bounded sample
+    # ---- the resident graph is released before the HOST-buffer legs: each of their calls uploads
+    # the reference's arrays into a context of its own (the freed device memory is recycled)
+    dg.close()
+    have_host = need_host and g.m > 0
+
+    # ---- end to end through the reference-facing host call, HOST buffers. Every timed call
+    # creates a context, uploads the reference CSR (H2D), samples `target` HSAWs and reads the
+    # counters back (D2H): the `hsaw sample` path. Ranks run the same call concurrently.
+    if not args.no_e2e and have_host:
+        target = max(1, int(accepted / max(args.steps, 1)))
+        e2e_acc, e2e_s = 0, 0.0
+        e2e_calls = max(1, min(args.steps, 5 if g.m < (1 << 28) else 3))
+        e2e_error = None
+        for i in range(-min(args.warmup, 2 if g.m < (1 << 28) else 1), e2e_calls):  # i < 0: warm-up
+            barrier()
+            t0 = time.perf_counter()
+            try:
+                with hostapi.DeviceGraph(g, p_of, device=local) as dg2:    # H2D of the CSR arrays
+                    _, acc = dg2.sample(target, seed=STREAM_SEED + 1000 * rank + i + 100,
+                                        max_attempts=10**15)               # ensure + counters (D2H)
+            except Exception as exc:
+                e2e_error, acc = str(exc)[:200], 0
+            torch.cuda.synchronize()
+            if i >= 0:
+                e2e_s += time.perf_counter() - t0
+                e2e_acc += acc
+        out["e2e"] = {
+            "value": e2e_acc / e2e_s if e2e_s > 0 else 0.0, "unit": UNIT,
+            "h2d_bytes_per_step": ref_bytes, "d2h_bytes_per_step": 16,
+            "call": f"DeviceGraph(g, vi) upload + SampleStream.ensure({target}) + counters_for "
+                    f"(the `hsaw sample` path), per call",
+            "calls_timed": e2e_calls, "ms_per_call": 1e3 * e2e_s / e2e_calls,
+        }
+        if e2e_error:
+            out["e2e"]["error"] = e2e_error
+        # host ProbGraph in, InterdictionResult out (context creation, upload and solve inside)
+        if r_dev is not None:
+            try:
+                kind = 0 if args.solver == "esia" else 1
+                reps = 2 if g.m < (1 << 28) else 1
+                e2e_runs = [hostapi.interdict(g, p_of, kind, args.esia_k, 0.1, 1.0 / g.n,
+                                              seed=STREAM_SEED, max_attempts=10**15, device=local,
+                                              want_json=True) for _ in range(reps)]
+                r_e2e = e2e_runs[-1]
+                out[args.solver].update({
+                    "seconds_to_solution_e2e": r_e2e["timing"]["wall_time_s"],
+                    "seconds_to_solution_e2e_first_call": e2e_runs[0]["timing"]["wall_time_s"],
+                    "same_result_e2e": all(r_dev[k_] == r_e2e[k_]
+                                           for k_ in ("solution", "attempts", "coverage")),
+                })
+            except Exception as exc:
+                out[args.solver]["e2e_error"] = str(exc)[:300]
+    elif world > 1 or args.no_e2e:
+        out["e2e"] = None
+    else:
+        out["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": ref_bytes,
+                      "d2h_bytes_per_step": 16,
+                      "error": f"host RAM ({host_ram_available() >> 30} GiB available) cannot hold the "
+                               f"reference's CSR arrays ({ref_bytes >> 30} GiB) twice"}
+
+    # ---- the step before the path (SURVEY 8f row 1), on request: file -> graph
+    if args.ingest and world == 1:
+        try:
+            out["ingest"] = ingest_leg(args, rank == 0 and not args.no_cpu_baseline)
+        except Exception as exc:
+            out["ingest"] = {"error": str(exc)[:300]}
+
+    # ---- CPU baseline beside it: rank 0, N=1 only, bounded sample of the same workload
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        rate, ns, at, kind, used, dt = cpu_reference_rate(args, g, p_of, args.cpu_target,
-                                                          STREAM_SEED, cores)
-        out["cpu_baseline"] = {
-            "value": rate, "unit": UNIT, "cores": used, "kind": kind,
-            "sample": f"stream_samples to {args.cpu_target} HSAWs on the same graph/suspects/seed "
-                      f"({ns} HSAWs, {at} attempts, {dt:.1f} s)",
-        }
+        cb = {"unit": UNIT}
+        if have_host:
+            from oracle.oracle import Csr
+            off, src, cum = g.views()
+            csr = Csr(g.n, g.m, off, src, cum, p_of)
+            rate, ns, at, kind_, used, dt = cpu_reference_rate(csr, args.cpu_target, STREAM_SEED,
+                                                               cores, lean=g.m > (1 << 27))
+            cb.update({"value": rate, "cores": used, "kind": kind_,
+                       "sample": f"stream_samples to {args.cpu_target} HSAWs on the same graph/"
+                                 f"suspects/seed ({ns} HSAWs, {at} attempts, {dt:.1f} s)"})
+            if "suspension" in out and "error" not in out["suspension"] and g.m <= (1 << 27):
+                out["suspension"]["cpu_baseline"] = suspension_cpu(csr)
+        else:
+            cb.update({"value": None, "cores": cores, "kind": "reference",
+                       "sample": "not run: host RAM cannot hold the reference's arrays for this shape"})
+        cb["seconds_to_solution"] = cpu_seconds_to_solution(args, cores)
+        out["cpu_baseline"] = cb
     elif rank == 0:
         out["cpu_baseline"] = None
-    dg.close()
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def suspension_cpu(csr):
+    from oracle import oracle
+    cpu_runs = 3
+    if oracle.have_ref():
+        R = oracle.Ref()
+        with R.handles(csr) as hd:
+            t0, s_ = time.perf_counter(), 7
+            for _ in range(cpu_runs):
+                _, s_ = R.lt_forward_simulate(csr, s_, hd=hd)
+            dt = time.perf_counter() - t0
+        cpu_kind = "reference"
+    else:
+        P = oracle.Port()
+        t0, s_ = time.perf_counter(), 7
+        for _ in range(cpu_runs):
+            _, s_ = P.lt_forward_simulate(csr, s_)
+        dt = time.perf_counter() - t0
+        cpu_kind = "port"
+    return {"runs_per_sec": cpu_runs / dt, "cores": 1, "kind": cpu_kind,
+            "sample": f"{cpu_runs} x lt_forward_simulate (one realisation + one count; a paired "
+                      f"run does two counts), single-threaded like the reference"}
 
 
 def ingest_leg(args, with_cpu_baseline: bool) -> dict:
@@ -602,8 +833,10 @@ def ingest_leg(args, with_cpu_baseline: bool) -> dict:
             r.close()
         return dt
 
-    g = hostapi.Graph.synth(1 << args.scale, int(args.edge_factor), 3)
-    res = {"graph": f"synth_graph(2^{args.scale}, {int(args.edge_factor)}, seed 3): {g.n} nodes, {g.m} edges"}
+    n = min(args.shape["n"], 1 << 22)
+    dens = max(1, min(32, args.shape["raw"] // args.shape["n"]))
+    g = hostapi.Graph.synth(n, dens, 3)
+    res = {"graph": f"synth_graph({n}, {dens}, seed 3): {g.n} nodes, {g.m} edges"}
     with tempfile.TemporaryDirectory(dir="/dev/shm" if os.path.isdir("/dev/shm") else None) as tmp:
         cache, text = os.path.join(tmp, "g.hsaw1"), os.path.join(tmp, "g.edges")
         g.save_cache(cache)
@@ -632,11 +865,6 @@ def ingest_leg(args, with_cpu_baseline: bool) -> dict:
                                        "load_edge_list_s": t2 - t1,
                                        "sample": "the same two files, one call each"}
     return res
-
-
-def hsaw_mb(dg):
-    from paper_1702_05854_b200 import capi
-    return round(int(capi.lib().hsaw_gpu_graph_bytes(dg.ctx_handle())) / 1e6, 1)
 
 
 def main():

@@ -67,8 +67,9 @@ int hsaw_gpu_ctx_sync(hsaw_gpu_ctx* ctx);
  * (proj/include/hsaw/graph.hpp:19-51 in_offsets/in_src/in_cum, :84-94 p_of). The arrays are the
  * reference's own: in_offsets u64[n+1], in_src u32[m], in_cum f64[m] (per-row sequential FP64
  * cumulative sums, proj/src/graph.cpp:158-192 — uploaded, never recomputed), p_of f64[n].
- * They are re-laid out on the device into 32-byte node records and 16-byte edge records holding
- * exact integer thresholds. HSAW_EDATA if a row's cumulative array decreases. */
+ * They are re-laid out on the device into 32-byte node records plus either the
+ * compact arrays (packed in_src + 16-byte row headers, graphs whose headers fit in L2) or 32-byte
+ * edge records (fat layout), all holding exact integer thresholds. HSAW_EDATA if a row's cumulative array decreases. */
 int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* in_offsets,
                           const uint32_t* in_src, const double* in_cum, const double* p_of);
 
@@ -137,10 +138,34 @@ int hsaw_gpu_cache_decode(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const void*
 int hsaw_gpu_graph_cache_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const void* body,
                                 const double* p_of);
 
+/* Bench inputs (no reference counterpart: the reference's only generator is the uniform
+ * synth_graph, proj/src/graph.cpp:330-352; SURVEY.md §8d asks for R-MAT graphs of the named
+ * shapes). Generates on the device the graph hsaw::rmat_graph_n (host/graph_io.cpp) defines,
+ * bit-identical to it: quadrant probabilities (a, b, c, 1-a-b-c), ceil(log2 n) draws of one
+ * xorshift64* stream (proj/include/hsaw/prng.hpp:41-53) per raw edge starting from `prg_state`
+ * (the state after the generator's n-1 relabelling draws), endpoints relabelled through label[n]
+ * (host array), self-loops / endpoints >= n / duplicates removed, rows in (target, source) order,
+ * WeightMode::InDegree cumulative sums as build_graph forms them (graph.cpp:172-178). The CSR stays
+ * on the device, held by the context; *out_m = edges kept.
+ *   hsaw_gpu_held_csr_fetch    copies the reference-layout arrays out (any pointer nullable)
+ *   hsaw_gpu_held_csr_install  = hsaw_gpu_graph_upload on the held arrays where they lie (p_of NULL =
+ *                              no suspects yet); keep != 0 keeps the CSR for a later fetch
+ *   hsaw_gpu_held_csr_drop     frees it */
+int hsaw_gpu_rmat_build(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t raw_edges, const uint32_t* label,
+                        uint64_t prg_state, double a, double b, double c, uint64_t* out_m);
+int hsaw_gpu_held_csr_fetch(hsaw_gpu_ctx* ctx, uint64_t* in_offsets, uint32_t* in_src,
+                            double* in_cum);
+int hsaw_gpu_held_csr_install(hsaw_gpu_ctx* ctx, const double* p_of, int keep);
+void hsaw_gpu_held_csr_drop(hsaw_gpu_ctx* ctx);
+
 /* Same, but p_of replaced later without re-uploading the CSR (new SuspectSet on the same graph). */
 int hsaw_gpu_suspects_upload(hsaw_gpu_ctx* ctx, const double* p_of);
 /* Bytes of device memory held by the uploaded graph. */
 uint64_t hsaw_gpu_graph_bytes(const hsaw_gpu_ctx* ctx);
+/* Device layout of the uploaded graph: 0 = fat 32-byte edge records; 21 / 32 =
+ * compact arrays with 21-bit packed / 32-bit flagged sources; 1 = compact with plain sources
+ * (HSAW_PACK=0); -1 = no graph. Diagnostic only: results never depend on it. */
+int hsaw_gpu_graph_layout(const hsaw_gpu_ctx* ctx);
 
 /* ---- sampler: encode / decode (kernels K1, K2) ---------------------------------------------- */
 

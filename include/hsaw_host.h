@@ -28,6 +28,16 @@ int hsawh_graph_build_device(uint32_t n, uint64_t nedges, const uint32_t* u, con
                              const double* w, int weight_mode, int device, void** out);
 int hsawh_graph_synth(uint32_t n, uint32_t density, uint64_t seed, void** out);
 int hsawh_graph_rmat(uint32_t scale, double edge_factor, uint64_t seed, void** out);
+/* Bench inputs of any node count (hsaw::rmat_graph_n; rmat above = the power-of-two case), on the
+ * host, or generated / sorted / summed on the GPU (hsaw::rmat_graph_device; lean: no weight /
+ * edge_dst arrays). hsawh_graph_shell: a ProbGraph carrying only n and m, for callers that hold
+ * the graph on the device alone. hsawh_graph_ptrs: borrowed views of the CSR arrays. */
+int hsawh_graph_rmat_n(uint32_t n, uint64_t raw_edges, uint64_t seed, void** out);
+int hsawh_graph_rmat_device(uint32_t n, uint64_t raw_edges, uint64_t seed, int device, int lean,
+                            void** out);
+int hsawh_graph_shell(uint32_t n, uint32_t m, void** out);
+void hsawh_graph_ptrs(const void* g, const uint64_t** in_offsets, const uint32_t** in_src,
+                      const double** in_cum);
 int hsawh_graph_from_csr(uint32_t n, uint32_t m, const uint64_t* in_offsets,
                          const uint32_t* in_src, const double* in_cum, void** out);
 int hsawh_graph_save_cache(const void* g, const char* path);
@@ -42,6 +52,7 @@ void hsawh_graph_free(void* g);
 
 /* ---- suspects: dense p_of[n] out — graph.hpp:129-132 ---- */
 int hsawh_suspects_random(const void* g, uint32_t count, uint64_t seed, double* p_of);
+int hsawh_suspects_random_n(uint32_t n, uint32_t count, uint64_t seed, double* p_of);
 int hsawh_suspects_load(const char* path, const void* g, double* p_of);
 
 /* ---- schedule / stopping rule — proj/include/hsaw/coverage.hpp:61-92 ---- */
@@ -71,6 +82,12 @@ int hsawh_device_from_cache(const char* path, int device, void* cuda_stream, voi
  * the host loader (outside the device parser's plain grammar, RandomNormalized, empty). */
 int hsawh_device_from_edge_list(const char* path, int weight_mode, int device, void* cuda_stream,
                                 void** out);
+/* hsaw::DeviceGraph::from_rmat: the R-MAT graph generated on the device and installed where it
+ * lies. p_of dense f64[n] or NULL. *g_out: a ProbGraph handle — the lean host copy (in_offsets /
+ * in_src / in_cum) when want_host, else a shell with n and m only. */
+int hsawh_device_from_rmat(uint32_t n, uint64_t raw_edges, uint64_t seed, const double* p_of,
+                           int device, void* cuda_stream, int want_host, void** dg_out,
+                           void** g_out);
 int hsawh_device_set_suspects(void* dg, const void* g, const double* p_of);
 
 /* ---- eSIA / nSIA — proj/include/hsaw/interdiction.hpp:37-47 ---- */

@@ -397,6 +397,8 @@ class Ref:
         L.ref_splitmix_next.argtypes = [C.c_uint64, u64p, u64p]
         L.ref_graph_from_csr.restype = C.c_void_p
         L.ref_graph_from_csr.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p]
+        L.ref_graph_from_csr_lean.restype = C.c_void_p
+        L.ref_graph_from_csr_lean.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p]
         L.ref_graph_build.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, f64p, C.c_int,
                                       C.c_uint64, C.POINTER(C.c_void_p)]
         L.ref_graph_load_edge_list.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int,
@@ -555,9 +557,14 @@ class Ref:
         return p[: n.value]
 
     class _Handles:
-        def __init__(self, ref, csr):
+        def __init__(self, ref, csr, lean=False):
             self.ref = ref
-            self.g = ref.graph_from_csr(csr)
+            if lean:  # sampler-only ProbGraph (no weight / edge_dst): the 10^9-edge bench shapes
+                self.g = C.c_void_p(ref.L.ref_graph_from_csr_lean(
+                    csr.n, csr.m, _p(csr.in_offsets, u64p), _p(csr.in_src, u32p),
+                    _p(csr.in_cum, f64p)))
+            else:
+                self.g = ref.graph_from_csr(csr)
             self.vi = C.c_void_p()
             ref._chk(ref.L.ref_suspects_from_p(self.g, _p(csr.p_of, f64p), C.byref(self.vi)),
                      "suspects")
@@ -569,8 +576,8 @@ class Ref:
             self.ref.L.ref_suspects_free(self.vi)
             self.ref.L.ref_graph_free(self.g)
 
-    def handles(self, csr: Csr):
-        return Ref._Handles(self, csr)
+    def handles(self, csr: Csr, lean=False):
+        return Ref._Handles(self, csr, lean)
 
     # -- sampler (same signatures as Port)
     def thread_sample(self, csr, worker_id, l, heuristic=0, window=2, hd=None):

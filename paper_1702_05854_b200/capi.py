@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_edge_text_free.restype = None
     L.hsaw_gpu_graph_bytes.argtypes = [vp]
     L.hsaw_gpu_graph_bytes.restype = C.c_uint64
+    L.hsaw_gpu_graph_layout.argtypes = [vp]
     L.hsaw_gpu_launch_count.argtypes = [vp]
     L.hsaw_gpu_launch_count.restype = C.c_uint64
     L.hsaw_gpu_stage_times.argtypes = [vp, f64p, u64p, C.c_int]
@@ -156,6 +157,8 @@ EXPORTS = (
     "hsaw_gpu_cache_decode", "hsaw_gpu_graph_cache_upload", "hsaw_gpu_prg_jump",
     "hsaw_gpu_edge_text_parse", "hsaw_gpu_edge_text_fetch", "hsaw_gpu_edge_text_free",
     "hsaw_gpu_edge_text_install",
+    "hsaw_gpu_rmat_build", "hsaw_gpu_held_csr_fetch", "hsaw_gpu_held_csr_install",
+    "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout",
 )
 
 
@@ -278,6 +281,11 @@ class Context:
     @property
     def graph_bytes(self) -> int:
         return int(self.L.hsaw_gpu_graph_bytes(self.h))
+
+    @property
+    def graph_layout(self) -> str:
+        code = int(self.L.hsaw_gpu_graph_layout(self.h))
+        return {0: "fat", -1: "none"}.get(code, "compact")
 
     def upload_graph(self, n, m, in_offsets, in_src, in_cum, p_of):
         in_offsets = np.ascontiguousarray(in_offsets, dtype=np.uint64)

@@ -119,8 +119,11 @@ inline AllocStats& alloc_stats() {
 
 // Allocation sizes are rounded up to 1/8-octave classes (<= 12.5 % slack) so that buffers freed
 // by one round / stream are exact-fit candidates for the next and the pool does not fragment.
+// Beyond 1 GiB (graph stores, sort buffers of the C4 / C5 shapes) the classes are 64 MiB steps: a
+// 47 GB edge-record store must not carry gigabytes of slack.
 inline uint64_t size_class(uint64_t bytes) {
     if (bytes <= (1ull << 16)) return 1ull << 16;
+    if (bytes > (1ull << 30)) return (bytes + (1ull << 26) - 1) & ~((1ull << 26) - 1);
     int top = 63 - __builtin_clzll(bytes);
     uint64_t step = 1ull << (top - 3);
     return (bytes + step - 1) & ~(step - 1);
@@ -190,6 +193,17 @@ struct DevVec {
         a.bytes += bytes;
         return np;
     }
+    void ensure_exact(uint64_t want) {  // no headroom (large one-off buffers)
+        if (want <= cap) return;
+        cudaStream_t st = current_stream();
+        if (p) cudaFreeAsync(p, owner);
+        p = nullptr;
+        cap = 0;
+        uint64_t ncap = want;
+        p = alloc(ncap, st);
+        cap = ncap;
+        owner = st;
+    }
     // Grows capacity (doubling) preserving the first `size` elements; stream-ordered, no sync.
     void reserve(uint64_t want, cudaStream_t st) {
         if (want <= cap) return;
@@ -209,14 +223,15 @@ struct DevVec {
         cap = ncap;
         owner = st;
     }
-    // Scratch use: capacity only, contents undefined.
+    // Scratch use: capacity only, contents undefined. Small buffers get 50 % headroom so that a
+    // slightly larger request of the next round still fits; buffers past 1 GiB are sized exactly.
     void ensure_scratch(uint64_t want) {
         if (want <= cap) return;
         cudaStream_t st = current_stream();
         if (p) cudaFreeAsync(p, owner);
         p = nullptr;
         cap = 0;
-        uint64_t ncap = want + want / 2;
+        uint64_t ncap = want * sizeof(T) > (1ull << 30) ? want : want + want / 2;
         p = alloc(ncap, st);
         cap = ncap;
         owner = st;
@@ -242,6 +257,17 @@ struct SamplerScratch {
         enc_len.release(); enc_seq.release(); tmp_nodes.release(); tmp_edges.release();
         vidx.release(); status.release();
     }
+};
+
+// A device-resident CSR in the reference's own arrays (in_offsets / in_src / in_cum), held by the
+// context between a device-side build (rmat.cu) and its installation / download.
+struct HeldCsr {
+    DevVec<uint64_t> off;
+    DevVec<uint32_t> src;
+    DevVec<double> cum;
+    uint32_t n = 0;
+    uint64_t m = 0;
+    bool valid = false;
 };
 
 // Walk-pool buffers handed back by a destroyed stream, taken over by the next one.
@@ -281,6 +307,7 @@ struct hsaw_gpu_ctx {
     hsawgpu::DevVec<uint32_t> chk_list, chk_mid, chk_counters;  // distinctness-check scratch
     hsawgpu::SamplerScratch samp;                        // per-chunk sampler scratch
     hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
+    hsawgpu::HeldCsr held;                               // device-built CSR awaiting install / fetch
     // greedy / coverage scratch (greedy.cu), reused across the doubling iterations
     hsawgpu::DevVec<uint32_t> g_cand_bits, g_cnt, g_fill, g_inv, g_covered, g_solution, g_query_bits;
     hsawgpu::DevVec<uint32_t> g_indexed_bits;  // items that own an inverted list
@@ -454,6 +481,7 @@ inline SrcRef src_ref(const DeviceGraph& g) { return SrcRef{g.src, g.src_bits}; 
 void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_off,
                    const uint32_t* d_src, const double* d_cum, const double* d_p);
 void release_graph(hsaw_gpu_ctx* ctx);
+void drop_held_csr(hsaw_gpu_ctx* ctx);  // rmat.cu
 // Device CSR builder (build.cu): edge list -> resident graph in the chosen layout. on_device: the
 // edge arrays are device pointers (the text parser's output) instead of host arrays.
 void build_and_install(hsaw_gpu_ctx* ctx, uint32_t n, uint64_t ne, const uint32_t* edge_u,

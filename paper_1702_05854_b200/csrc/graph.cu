@@ -867,6 +867,7 @@ void hsaw_gpu_ctx_destroy(hsaw_gpu_ctx* ctx) {
     collect_timings(ctx);
     for (cudaEvent_t e : ctx->free_events) cudaEventDestroy(e);
     free_graph(ctx);
+    drop_held_csr(ctx);
     park_buffers(ctx);       // keep the device buffers for the next context on this device
     if (ctx->d_scalars) cudaFree(ctx->d_scalars);
     if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
@@ -888,6 +889,10 @@ int hsaw_gpu_ctx_sync(hsaw_gpu_ctx* ctx) {
 }
 
 uint64_t hsaw_gpu_graph_bytes(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->graph_bytes : 0; }
+int hsaw_gpu_graph_layout(const hsaw_gpu_ctx* ctx) {
+    if (!ctx || !ctx->g.nodes) return -1;
+    return ctx->g.layout == kLayoutCompact ? (int)ctx->g.src_bits : 0;
+}
 uint64_t hsaw_gpu_launch_count(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 void hsaw_gpu_debug_counters(double* out3) {

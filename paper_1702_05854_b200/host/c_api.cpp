@@ -88,6 +88,64 @@ int hsawh_graph_rmat(uint32_t scale, double edge_factor, uint64_t seed, void** o
     return guarded([&] { *out = new ProbGraph(rmat_graph(scale, edge_factor, seed)); });
 }
 
+int hsawh_graph_rmat_n(uint32_t n, uint64_t raw_edges, uint64_t seed, void** out) {
+    return guarded([&] { *out = new ProbGraph(rmat_graph_n(n, raw_edges, seed)); });
+}
+
+int hsawh_graph_rmat_device(uint32_t n, uint64_t raw_edges, uint64_t seed, int device, int lean,
+                            void** out) {
+    return guarded([&] {
+        *out = new ProbGraph(rmat_graph_device(n, raw_edges, seed, 0.57, 0.19, 0.19, device, lean != 0));
+    });
+}
+
+int hsawh_graph_shell(uint32_t n, uint32_t m, void** out) {
+    return guarded([&] {
+        auto* g = new ProbGraph;
+        g->n = n;
+        g->m = m;
+        *out = g;
+    });
+}
+
+void hsawh_graph_ptrs(const void* gp, const uint64_t** in_offsets, const uint32_t** in_src,
+                      const double** in_cum) {
+    const ProbGraph& g = G(gp);
+    *in_offsets = g.in_offsets.data();
+    *in_src = g.in_src.data();
+    *in_cum = g.in_cum.data();
+}
+
+int hsawh_suspects_random_n(uint32_t n, uint32_t count, uint64_t seed, double* p_of) {
+    return guarded([&] {
+        SuspectSet vi = random_suspects(n, count, seed);
+        std::memcpy(p_of, vi.p_of.data(), 8 * vi.p_of.size());
+    });
+}
+
+int hsawh_device_from_rmat(uint32_t n, uint64_t raw_edges, uint64_t seed, const double* p_of,
+                           int device, void* cuda_stream, int want_host, void** dg_out,
+                           void** g_out) {
+    return guarded([&] {
+        std::unique_ptr<SuspectSet> vi;
+        if (p_of) {
+            std::vector<std::pair<NodeId, double>> mem;
+            for (NodeId v = 0; v < n; ++v)
+                if (p_of[v] != 0.0) mem.emplace_back(v, p_of[v]);
+            vi = std::make_unique<SuspectSet>(SuspectSet::from_members(std::move(mem), n));
+        }
+        auto host = std::make_unique<ProbGraph>();
+        auto dg = DeviceGraph::from_rmat(n, raw_edges, seed, vi.get(), 0.57, 0.19, 0.19, device,
+                                         cuda_stream, want_host ? host.get() : nullptr);
+        if (!want_host) {  // a shell: node and edge counts only
+            host->n = dg->n();
+            host->m = dg->m();
+        }
+        *dg_out = dg.release();
+        *g_out = host.release();
+    });
+}
+
 int hsawh_graph_from_csr(uint32_t n, uint32_t m, const uint64_t* in_offsets,
                          const uint32_t* in_src, const double* in_cum, void** out) {
     return guarded([&] { *out = new ProbGraph(graph_from_csr(n, m, in_offsets, in_src, in_cum)); });

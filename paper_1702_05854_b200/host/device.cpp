@@ -97,6 +97,83 @@ ProbGraph build_graph_device(NodeId n, const std::vector<std::tuple<NodeId, Node
                               mode == WeightMode::Given ? w.data() : nullptr, mode, device);
 }
 
+// ---- R-MAT bench graphs on the device --------------------------------------------------------------
+namespace {
+
+// Fetches the CSR held by `ctx` into g (n, m set by the caller). lean: in_offsets / in_src / in_cum only.
+void fetch_held_csr(hsaw_gpu_ctx* ctx, ProbGraph& g, bool lean) {
+    g.in_offsets.resize(static_cast<std::size_t>(g.n) + 1);
+    g.in_src.resize(g.m);
+    g.in_cum.resize(g.m);
+    raise(hsaw_gpu_held_csr_fetch(ctx, g.in_offsets.data(), g.in_src.data(), g.in_cum.data()), ctx,
+          "rmat_graph_device");
+    if (lean) return;
+    g.weight.resize(g.m);
+    g.edge_dst.resize(g.m);
+    for (NodeId v = 0; v < g.n; ++v) {
+        const std::uint64_t lo = g.in_offsets[v], hi = g.in_offsets[v + 1];
+        if (hi == lo) continue;
+        const double share = 1.0 / static_cast<double>(hi - lo);  // rmat_graph_n's weight
+        for (std::uint64_t e = lo; e < hi; ++e) {
+            g.weight[e] = share;
+            g.edge_dst[e] = v;
+        }
+    }
+}
+
+}  // namespace
+
+ProbGraph rmat_graph_device(NodeId n, std::uint64_t raw_edges, std::uint64_t seed, double a,
+                            double b, double c, int device, bool lean) {
+    RmatLabels lab = rmat_labels(n, seed);
+    hsaw_gpu_ctx* ctx = nullptr;
+    if (hsaw_gpu_ctx_create(device, nullptr, &ctx) != HSAW_OK)
+        throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");
+    ProbGraph g;
+    try {
+        std::uint64_t m = 0;
+        raise(hsaw_gpu_rmat_build(ctx, n, raw_edges, lab.label.data(), lab.state.state, a, b, c, &m),
+              ctx, "rmat_graph_device");
+        g.n = n;
+        g.m = static_cast<EdgeId>(m);
+        fetch_held_csr(ctx, g, lean);
+    } catch (...) {
+        hsaw_gpu_ctx_destroy(ctx);
+        throw;
+    }
+    hsaw_gpu_ctx_destroy(ctx);
+    return g;
+}
+
+std::unique_ptr<DeviceGraph> DeviceGraph::from_rmat(NodeId n, std::uint64_t raw_edges,
+                                                    std::uint64_t seed, const SuspectSet* vi,
+                                                    double a, double b, double c, int device,
+                                                    void* cuda_stream, ProbGraph* host_copy) {
+    if (vi && vi->p_of.size() != n) throw std::invalid_argument("suspect set does not match graph");
+    RmatLabels lab = rmat_labels(n, seed);
+    std::unique_ptr<DeviceGraph> dg(new DeviceGraph());
+    if (hsaw_gpu_ctx_create(device, cuda_stream, &dg->ctx_) != HSAW_OK) {
+        dg->ctx_ = nullptr;
+        throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");
+    }
+    std::uint64_t m = 0;
+    raise(hsaw_gpu_rmat_build(dg->ctx_, n, raw_edges, lab.label.data(), lab.state.state, a, b, c, &m),
+          dg->ctx_, "DeviceGraph::from_rmat");
+    lab.label = {};
+    dg->n_ = n;
+    dg->m_ = static_cast<EdgeId>(m);
+    if (host_copy) {
+        host_copy->n = n;
+        host_copy->m = dg->m_;
+        host_copy->weight.clear();
+        host_copy->edge_dst.clear();
+        fetch_held_csr(dg->ctx_, *host_copy, true);
+    }
+    raise(hsaw_gpu_held_csr_install(dg->ctx_, vi ? vi->p_of.data() : nullptr, 0), dg->ctx_,
+          "DeviceGraph::from_rmat");
+    return dg;
+}
+
 // ---- binary ingest on the device -------------------------------------------------------------------
 namespace {
 

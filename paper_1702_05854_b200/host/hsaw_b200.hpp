@@ -101,6 +101,7 @@ struct SuspectSet {
     bool is_suspect(NodeId v) const { return p_of[v] > 0.0; }
     std::size_t size() const { return members.size(); }
     static SuspectSet from_members(std::vector<std::pair<NodeId, double>> mem, const ProbGraph& g);
+    static SuspectSet from_members(std::vector<std::pair<NodeId, double>> mem, NodeId n);
 };
 
 struct CandidateSet {
@@ -129,6 +130,7 @@ ProbGraph load_edge_list(const std::string& path, WeightMode mode, std::uint64_t
                          const LoadOptions& opts = {});
 SuspectSet load_suspects(const std::string& path, const ProbGraph& g);
 SuspectSet random_suspects(const ProbGraph& g, NodeId count, std::uint64_t seed);
+SuspectSet random_suspects(NodeId n, NodeId count, std::uint64_t seed);  // same draws, no graph needed
 ProbGraph synth_graph(NodeId n, std::uint32_t density, std::uint64_t seed);
 void save_edge_list(const ProbGraph& g, const std::string& path);
 void save_cache(const ProbGraph& g, const std::string& path);
@@ -138,6 +140,24 @@ ProbGraph load_cache(const std::string& path);
 // without validate() because hub rows exceed its 1e-12 tolerance.
 ProbGraph rmat_graph(std::uint32_t scale, double edge_factor, std::uint64_t seed, double a = 0.57,
                      double b = 0.19, double c = 0.19);
+// Same generator for any node count (the named shapes are not powers of two: 41.7 M, 65.6 M):
+// ceil(log2 n) quadrant draws per raw edge, raw edges with an endpoint >= n dropped like
+// self-loops and duplicates. rmat_graph(scale, f, ...) == rmat_graph_n(2^scale, floor(f 2^scale), ...).
+ProbGraph rmat_graph_n(NodeId n, std::uint64_t raw_edges, std::uint64_t seed, double a = 0.57,
+                       double b = 0.19, double c = 0.19);
+// The generator's relabelling (seeded Fisher-Yates, n-1 draws) and the PrgState after it: the
+// sequential part of the stream, computed on the host for the device generator too.
+struct RmatLabels {
+    std::vector<NodeId> label;
+    PrgState state;
+};
+RmatLabels rmat_labels(NodeId n, std::uint64_t seed);
+void fill_indegree_weights(ProbGraph& g);  // weight = 1/d + sequential in_cum from in_offsets
+// rmat_graph_n generated, sorted, deduplicated and summed on the GPU (hsaw_gpu_rmat_build): the
+// same ProbGraph bit for bit in seconds at the 1.47 G-edge shape. lean: leave weight / edge_dst
+// empty (the sampling path never reads them; 12 bytes per edge of host memory saved).
+ProbGraph rmat_graph_device(NodeId n, std::uint64_t raw_edges, std::uint64_t seed, double a = 0.57,
+                            double b = 0.19, double c = 0.19, int device = 0, bool lean = false);
 // Direct CSR fill (in_offsets, in_src, in_cum given); weight/edge_dst derived; no validate().
 ProbGraph graph_from_csr(NodeId n, EdgeId m, const std::uint64_t* in_offsets, const NodeId* in_src,
                          const double* in_cum);
@@ -181,6 +201,14 @@ public:
     // when the file needs the host loader (load_edge_list_device + the constructor above).
     static std::unique_ptr<DeviceGraph> from_edge_list(const std::string& path, WeightMode mode,
                                                        int device = 0, void* cuda_stream = nullptr);
+    // rmat_graph_n generated on the device and installed where it lies: no host CSR at all unless
+    // host_copy is given (filled lean: in_offsets / in_src / in_cum only). vi may be null (no
+    // suspects yet).
+    static std::unique_ptr<DeviceGraph> from_rmat(NodeId n, std::uint64_t raw_edges,
+                                                  std::uint64_t seed, const SuspectSet* vi,
+                                                  double a = 0.57, double b = 0.19, double c = 0.19,
+                                                  int device = 0, void* cuda_stream = nullptr,
+                                                  ProbGraph* host_copy = nullptr);
     ~DeviceGraph();
     DeviceGraph(const DeviceGraph&) = delete;
     DeviceGraph& operator=(const DeviceGraph&) = delete;

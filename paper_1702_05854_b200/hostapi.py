@@ -44,6 +44,14 @@ def lib() -> C.CDLL:
     L.hsawh_graph_synth.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, vpp]
     L.hsawh_graph_rmat.argtypes = [C.c_uint32, C.c_double, C.c_uint64, vpp]
     L.hsawh_graph_from_csr.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p, vpp]
+    L.hsawh_graph_rmat_n.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, vpp]
+    L.hsawh_graph_rmat_device.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, C.c_int, vpp]
+    L.hsawh_graph_shell.argtypes = [C.c_uint32, C.c_uint32, vpp]
+    L.hsawh_graph_ptrs.argtypes = [vp, C.POINTER(u64p), C.POINTER(u32p), C.POINTER(f64p)]
+    L.hsawh_graph_ptrs.restype = None
+    L.hsawh_suspects_random_n.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, f64p]
+    L.hsawh_device_from_rmat.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, f64p, C.c_int, vp,
+                                         C.c_int, vpp, vpp]
     L.hsawh_graph_save_cache.argtypes = [vp, C.c_char_p]
     L.hsawh_graph_load_cache.argtypes = [C.c_char_p, vpp]
     L.hsawh_graph_save_edge_list.argtypes = [vp, C.c_char_p]
@@ -145,6 +153,31 @@ class Graph:
         return cls._new(lib().hsawh_graph_rmat, scale, float(edge_factor), seed)
 
     @classmethod
+    def rmat_n(cls, n, raw_edges, seed=1):
+        """hsaw::rmat_graph_n on the host (sequential stream + std::sort; small shapes only)."""
+        return cls._new(lib().hsawh_graph_rmat_n, n, raw_edges, seed)
+
+    @classmethod
+    def rmat_device(cls, n, raw_edges, seed=1, device=0, lean=False):
+        """hsaw::rmat_graph_device: the same ProbGraph generated / sorted / summed on the GPU."""
+        return cls._new(lib().hsawh_graph_rmat_device, n, raw_edges, seed, device, int(lean))
+
+    @classmethod
+    def shell(cls, n, m):
+        """A ProbGraph carrying only n and m (the graph itself lives on the device)."""
+        return cls._new(lib().hsawh_graph_shell, n, m)
+
+    def views(self):
+        """(in_offsets, in_src, in_cum) as zero-copy views of the ProbGraph's own vectors — valid
+        while this Graph is alive."""
+        o, s_, c = u64p(), u32p(), f64p()
+        lib().hsawh_graph_ptrs(self.h, C.byref(o), C.byref(s_), C.byref(c))
+        m = max(self.m, 1)
+        return (np.ctypeslib.as_array(o, shape=(self.n + 1,)),
+                np.ctypeslib.as_array(s_, shape=(m,))[: self.m],
+                np.ctypeslib.as_array(c, shape=(m,))[: self.m])
+
+    @classmethod
     def from_csr(cls, n, m, in_offsets, in_src, in_cum):
         o = np.ascontiguousarray(in_offsets, dtype=np.uint64)
         s = np.ascontiguousarray(in_src, dtype=np.uint32)
@@ -199,6 +232,13 @@ class Graph:
         return p[: self.n]
 
 
+def random_suspects_n(n, count, seed) -> np.ndarray:
+    """hsaw::random_suspects by node count (the draws do not depend on the edges)."""
+    p = np.zeros(max(n, 1), dtype=np.float64)
+    _chk(lib().hsawh_suspects_random_n(n, count, seed, _p(p, f64p)))
+    return p[:n]
+
+
 def schedule(M, k, eps, delta) -> dict:
     out = np.zeros(4, dtype=np.float64)
     t = C.c_uint32()
@@ -244,6 +284,20 @@ class DeviceGraph:
                                                C.c_void_p(cuda_stream) if cuda_stream else None,
                                                C.byref(self.h)))
         return self if self.h else None
+
+    @classmethod
+    def from_rmat(cls, n, raw_edges, seed, p_of=None, device=0, cuda_stream: int | None = None,
+                  want_host=False) -> "DeviceGraph":
+        """hsaw::DeviceGraph::from_rmat: R-MAT graph generated on the device and installed where it
+        lies. self.graph is the lean host copy (want_host) or a shell with n and m only."""
+        self = cls.__new__(cls)
+        self.p_of = None if p_of is None else np.ascontiguousarray(p_of, dtype=np.float64)
+        self.h, gh = C.c_void_p(), C.c_void_p()
+        _chk(lib().hsawh_device_from_rmat(n, raw_edges, seed, _p(self.p_of, f64p), device,
+                                          C.c_void_p(cuda_stream) if cuda_stream else None,
+                                          int(want_host), C.byref(self.h), C.byref(gh)))
+        self.graph = Graph(gh)
+        return self
 
     def set_suspects(self, graph: "Graph", p_of):
         self.graph = graph
