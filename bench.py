@@ -54,9 +54,9 @@ GEN_SEED, SUSPECT_SEED = 1, 2
 WORKLOADS = {
     "c2": dict(name="C2", n=1 << 20, raw=16 << 20, k=100,
                what="R-MAT 1M nodes / 16M edges (configs[1])"),
-    "c3": dict(name="C3", n=4_847_571, raw=93_000_000, k=100,
+    "c3": dict(name="C3", n=4_847_571, raw=90_300_000, k=100,
                what="LiveJournal-shape R-MAT 4.8M nodes / 69M edges (configs[2])"),
-    "c4": dict(name="C4", n=41_652_230, raw=1_990_000_000, k=1000,
+    "c4": dict(name="C4", n=41_652_230, raw=1_862_000_000, k=1000,
                what="Twitter-shape R-MAT 41.7M nodes / 1.47B edges (configs[3], the configuration "
                     "BASELINE.json's metric is quoted on)"),
     "c5": dict(name="C5", n=65_608_366, raw=3_900_000_000, k=1000,

@@ -198,6 +198,13 @@ int hsaw_gpu_decode_walks(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* se
 /* SampleStream ctor. Batch b of the stream uses worker id seed + b (sampler.cpp:430). */
 int hsaw_gpu_stream_create(hsaw_gpu_ctx* ctx, uint64_t seed, const hsaw_sampler_cfg* cfg,
                            hsaw_gpu_stream** out);
+/* Which item arrays the stream's pool keeps. A SampleStream holds nodes and edge_ids of every
+ * walk (HsawSample, proj/include/hsaw/sampler.hpp:27-33); a solve over edge candidates only ever
+ * indexes the edge ids and one over node candidates only the nodes (CoverageIndex,
+ * proj/src/coverage.cpp:49-53), and at the Twitter shape each array is tens of gigabytes. Call
+ * before sampling. Order, counters and every result are unaffected; greedy / coverage / export
+ * calls that ask for a dropped array fail with HSAW_EINVAL. */
+int hsaw_gpu_stream_keep(hsaw_gpu_stream* stream, int keep_nodes, int keep_edges);
 void hsaw_gpu_stream_destroy(hsaw_gpu_stream* s);
 
 /* SampleStream::ensure (sampler.cpp:388-463): grow until >= min_accepted decoded samples exist.

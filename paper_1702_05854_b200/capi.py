@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_encode_stats.argtypes = [vp, C.POINTER(SamplerCfg), C.c_uint64, C.c_uint64, u64p]
     L.hsaw_gpu_decode_walks.argtypes = [vp, C.c_uint64, u64p, u32p, u64p, u32p, u32p, u8p]
     L.hsaw_gpu_stream_create.argtypes = [vp, C.c_uint64, C.POINTER(SamplerCfg), C.POINTER(vp)]
+    L.hsaw_gpu_stream_keep.argtypes = [vp, C.c_int, C.c_int]
     L.hsaw_gpu_stream_destroy.argtypes = [vp]
     L.hsaw_gpu_stream_destroy.restype = None
     L.hsaw_gpu_stream_ensure.argtypes = [vp, C.c_uint64]
@@ -158,7 +159,7 @@ EXPORTS = (
     "hsaw_gpu_edge_text_parse", "hsaw_gpu_edge_text_fetch", "hsaw_gpu_edge_text_free",
     "hsaw_gpu_edge_text_install",
     "hsaw_gpu_rmat_build", "hsaw_gpu_held_csr_fetch", "hsaw_gpu_held_csr_install",
-    "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout",
+    "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout", "hsaw_gpu_stream_keep",
 )
 
 
@@ -520,6 +521,11 @@ class Stream:
     def __exit__(self, *a):
         self.close()
 
+    def keep(self, nodes=True, edges=True):
+        """hsaw_gpu_stream_keep: which item arrays the pool holds (before sampling)."""
+        self.ctx._chk(self.L.hsaw_gpu_stream_keep(self.h, int(nodes), int(edges)))
+        return self
+
     def ensure(self, min_accepted):
         self.ctx._chk(self.L.hsaw_gpu_stream_ensure(self.h, min_accepted))
 
@@ -558,7 +564,10 @@ class Stream:
         self.ctx._chk(self.L.hsaw_gpu_stream_stats(self.h, _p(st, u64p)))
         return dict(zip(STAT_NAMES, (int(x) for x in st)))
 
-    def export(self, off=0, cnt=None, attempts=0) -> Pool:
+    def export(self, off=0, cnt=None, attempts=0, nodes=True, edges=True) -> Pool:
+        """Host copy of walks [off, off + cnt). nodes / edges False: skip that array (a stream
+        that keeps only one kind, see keep())."""
+        want_nodes, want_edges = nodes, edges
         cnt = self.count - off if cnt is None else cnt
         te = C.c_uint64()
         self.ctx._chk(self.L.hsaw_gpu_stream_slice_edges(self.h, off, cnt, C.byref(te)))
@@ -569,7 +578,8 @@ class Stream:
         tw = np.zeros(max(cnt, 1), dtype=np.uint64)
         ts = np.zeros(max(cnt, 1), dtype=np.uint32)
         self.ctx._chk(self.L.hsaw_gpu_stream_export(self.h, off, cnt, _p(eo, u64p),
-                                                    _p(nodes, u32p), _p(edges, u32p),
+                                                    _p(nodes, u32p) if want_nodes else None,
+                                                    _p(edges, u32p) if want_edges else None,
                                                     _p(tw, u64p), _p(ts, u32p)))
         return Pool(attempts, eo, nodes[: te + cnt], edges[:te], tw[:cnt], ts[:cnt])
 

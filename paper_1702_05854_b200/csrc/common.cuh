@@ -2,9 +2,13 @@
 // and the device-side graph layout. Product code — never includes anything from oracle/.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
+#include <type_traits>
 #include <utility>
 #include <cstdint>
 #include <cstdio>
@@ -238,6 +242,202 @@ struct DevVec {
     }
 };
 
+
+// ---- growable device arrays on CUDA virtual memory ------------------------------------------------
+// The walk pool of a stream is the one structure whose final size is not known in advance (the
+// doubling loop decides) and that reaches tens of gigabytes at the Twitter shape. A DevVec grows by
+// allocate-copy-free, which needs old + new at once (3x the payload while doubling); a GrowVec
+// reserves virtual address space for the whole device once and maps physical chunks behind the
+// data as it grows: the array never moves, nothing is copied and the peak is the payload itself.
+// The driver entry points are resolved through the runtime (no link-time libcuda dependency, so
+// the library still loads on a machine without a driver); without them a GrowVec behaves like a
+// DevVec.
+struct VmmApi {
+    CUresult (*address_reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+    CUresult (*address_free)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*,
+                       unsigned long long) = nullptr;
+    CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
+    CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+    CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+    CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+    bool ok = false;
+
+    static const VmmApi& get() {
+        static const VmmApi api = [] {
+            VmmApi a;
+            auto load = [](const char* name, auto& fn) {
+                void* ptr = nullptr;
+                cudaDriverEntryPointQueryResult q{};
+                if (cudaGetDriverEntryPoint(name, &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+                    q != cudaDriverEntryPointSuccess || !ptr) {
+                    cudaGetLastError();
+                    return false;
+                }
+                fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(ptr);
+                return true;
+            };
+            const char* off = std::getenv("HSAW_VMM");  // A/B knob: HSAW_VMM=0 -> plain DevVec growth
+            a.ok = !(off && std::atoi(off) == 0) &&
+                   load("cuMemAddressReserve", a.address_reserve) &&
+                   load("cuMemAddressFree", a.address_free) && load("cuMemCreate", a.create) &&
+                   load("cuMemRelease", a.release) && load("cuMemMap", a.map) &&
+                   load("cuMemUnmap", a.unmap) && load("cuMemSetAccess", a.set_access) &&
+                   load("cuMemGetAllocationGranularity", a.granularity);
+            return a;
+        }();
+        return api;
+    }
+};
+
+template <class T>
+struct GrowVec {
+    T* p = nullptr;
+    uint64_t size = 0, cap = 0;  // elements; cap = mapped capacity
+    cudaStream_t owner = nullptr;
+
+    GrowVec() = default;
+    GrowVec(const GrowVec&) = delete;
+    GrowVec& operator=(const GrowVec&) = delete;
+    GrowVec(GrowVec&& o) noexcept { swap(o); }
+    GrowVec& operator=(GrowVec&& o) noexcept {
+        if (this != &o) {
+            release();
+            swap(o);
+        }
+        return *this;
+    }
+    ~GrowVec() { release(); }
+
+    void swap(GrowVec& o) {
+        std::swap(p, o.p);
+        std::swap(size, o.size);
+        std::swap(cap, o.cap);
+        std::swap(owner, o.owner);
+        std::swap(base_, o.base_);
+        std::swap(va_bytes_, o.va_bytes_);
+        std::swap(mapped_, o.mapped_);
+        std::swap(device_, o.device_);
+        chunks_.swap(o.chunks_);
+        plain_.swap(o.plain_);
+    }
+
+    // Grows in place (contents preserved, pointer stable once mapped) to hold `want` elements.
+    void reserve(uint64_t want, cudaStream_t st) {
+        if (want <= cap) return;
+        const VmmApi& api = VmmApi::get();
+        if (!api.ok) {  // no virtual memory management: allocate-copy-free
+            plain_.size = size;
+            plain_.reserve(want, st);
+            p = plain_.p;
+            cap = plain_.cap;
+            owner = st;
+            return;
+        }
+        owner = st;
+        CUmemAllocationProp prop{};
+        prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        if (!base_) {
+            HSAW_CUDA_CHECK(cudaGetDevice(&device_));
+            prop.location.id = device_;
+            size_t gran = 0;
+            if (api.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !gran)
+                gran = 2u << 20;
+            gran_ = gran;
+            size_t free_b = 0, total_b = 0;
+            HSAW_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+            va_bytes_ = round_up(total_b, gran_);
+            if (api.address_reserve(&base_, va_bytes_, 0, 0, 0) != CUDA_SUCCESS)
+                throw ::hsawgpu::Error{HSAW_ECUDA, "cuMemAddressReserve failed"};
+        }
+        prop.location.id = device_;
+        const uint64_t need = round_up(want * sizeof(T), gran_);
+        if (need > va_bytes_)
+            throw ::hsawgpu::Error{HSAW_ECUDA, "device allocation of " + std::to_string(need) +
+                                                   " bytes: out of memory"};
+        // map at least a quarter more than is already there (bounded), so a pool that grows chunk
+        // by chunk needs a few dozen driver calls over its life, not one per chunk
+        uint64_t grow = need - mapped_;
+        const uint64_t floor_b = std::min<uint64_t>(std::max<uint64_t>(mapped_ / 4, 32ull << 20), 2ull << 30);
+        if (grow < floor_b) grow = std::min<uint64_t>(round_up(floor_b, gran_), va_bytes_ - mapped_);
+        CUmemGenericAllocationHandle h{};
+        CUresult rc = api.create(&h, grow, &prop, 0);
+        if (rc == CUDA_ERROR_OUT_OF_MEMORY) {
+            // physical memory may sit in the stream-ordered pool's cache: hand it back and retry
+            // with the exact need
+            cudaStreamSynchronize(st);
+            cudaMemPool_t pool = nullptr;
+            if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+            grow = need - mapped_;
+            rc = api.create(&h, grow, &prop, 0);
+        }
+        if (rc != CUDA_SUCCESS)
+            throw ::hsawgpu::Error{HSAW_ECUDA, "device allocation of " + std::to_string(grow) +
+                                                   " bytes: out of memory"};
+        CUmemAccessDesc acc{};
+        acc.location = prop.location;
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        if (api.map(base_ + mapped_, grow, 0, h, 0) != CUDA_SUCCESS ||
+            api.set_access(base_ + mapped_, grow, &acc, 1) != CUDA_SUCCESS) {
+            api.release(h);
+            throw ::hsawgpu::Error{HSAW_ECUDA, "cuMemMap failed"};
+        }
+        chunks_.push_back({h, grow});
+        mapped_ += grow;
+        p = reinterpret_cast<T*>(base_);
+        cap = mapped_ / sizeof(T);
+        AllocStats& a = alloc_stats();
+        a.calls += 1;
+        a.bytes += grow;
+    }
+
+    // Unmaps and frees everything. Work that touches the array must have finished: the owning
+    // stream is synchronised first.
+    void release() {
+        if (base_) {
+            const VmmApi& api = VmmApi::get();
+            if (owner) cudaStreamSynchronize(owner);
+            uint64_t at = 0;
+            for (auto& c : chunks_) {
+                api.unmap(base_ + at, c.second);
+                api.release(c.first);
+                at += c.second;
+            }
+            api.address_free(base_, va_bytes_);
+        }
+        chunks_.clear();
+        plain_.release();
+        base_ = 0;
+        va_bytes_ = mapped_ = 0;
+        p = nullptr;
+        size = cap = 0;
+    }
+    // process teardown after the CUDA context is gone: forget without calling the driver
+    void abandon() {
+        chunks_.clear();
+        plain_.p = nullptr;
+        plain_.cap = plain_.size = 0;
+        base_ = 0;
+        va_bytes_ = mapped_ = 0;
+        p = nullptr;
+        size = cap = 0;
+    }
+    void rebind(cudaStream_t st) {
+        owner = st;
+        plain_.owner = st;
+    }
+
+private:
+    static uint64_t round_up(uint64_t x, uint64_t g) { return (x + g - 1) / g * g; }
+    CUdeviceptr base_ = 0;
+    uint64_t va_bytes_ = 0, mapped_ = 0, gran_ = 2u << 20;
+    int device_ = 0;
+    std::vector<std::pair<CUmemGenericAllocationHandle, uint64_t>> chunks_;
+    DevVec<T> plain_;  // fallback storage when the driver entry points are unavailable
+};
+
 // Per-chunk scratch of the sample stream (stream.cu). Lives in the context so that consecutive
 // streams on one graph (the doubling loop is re-run per esia() call) reuse it without allocating.
 struct SamplerScratch {
@@ -273,7 +473,8 @@ struct HeldCsr {
 // Walk-pool buffers handed back by a destroyed stream, taken over by the next one.
 struct PoolCache {
     DevVec<uint64_t> edge_off, tag_batch, accepted_after_batch;
-    DevVec<uint32_t> nodes, edges, tag_seq;
+    DevVec<uint32_t> tag_seq;
+    GrowVec<uint32_t> nodes, edges;  // the two big ones: grown in place (virtual memory)
     void release() {
         edge_off.release(); tag_batch.release(); accepted_after_batch.release();
         nodes.release(); edges.release(); tag_seq.release();
@@ -361,7 +562,7 @@ struct hsaw_gpu_ctx {
         f(samp.tmp_nodes); f(samp.tmp_edges); f(samp.vidx); f(samp.status); f(samp.arena);
         f(samp.replay); f(samp.slot_log); f(samp.ovf_pairs); f(samp.sel); f(samp.enc_src);
         f(pool_cache.edge_off); f(pool_cache.tag_batch); f(pool_cache.accepted_after_batch);
-        f(pool_cache.nodes); f(pool_cache.edges); f(pool_cache.tag_seq);
+        f(pool_cache.tag_seq);  // pool_cache.nodes / .edges are GrowVecs: handled by the callers
         f(g_cand_bits); f(g_cnt); f(g_fill); f(g_inv); f(g_covered); f(g_solution);
         f(g_query_bits); f(g_pos); f(g_partial); f(g_gains); f(g_blkmax); f(g_sorted);
         f(g_indexed_bits);

@@ -603,11 +603,14 @@ struct Parked {
     std::map<int, hsaw_gpu_ctx*> by_device;
     ~Parked() {
         // process teardown: the CUDA context may already be gone, so the buffers are abandoned
-        for (auto& kv : by_device)
+        for (auto& kv : by_device) {
             kv.second->for_each_buffer([](auto& v) {
                 v.p = nullptr;
                 v.cap = v.size = 0;
             });
+            kv.second->pool_cache.nodes.abandon();
+            kv.second->pool_cache.edges.abandon();
+        }
     }
 };
 Parked& parked() {
@@ -622,6 +625,8 @@ void adopt_parked_buffers(hsaw_gpu_ctx* ctx) {
     if (it == pk.by_device.end()) return;
     ctx->swap_buffers(*it->second);
     ctx->for_each_buffer([&](auto& v) { v.owner = ctx->stream; });
+    ctx->pool_cache.nodes.rebind(ctx->stream);
+    ctx->pool_cache.edges.rebind(ctx->stream);
     std::swap(ctx->d_scalars, it->second->d_scalars);  // scalar scratch (device + pinned mirror)
     std::swap(ctx->h_scalars, it->second->h_scalars);
 }
@@ -636,8 +641,12 @@ void park_buffers(hsaw_gpu_ctx* ctx) {
         v.p = nullptr;
         v.cap = v.size = 0;
     });
+    slot->pool_cache.nodes.release();
+    slot->pool_cache.edges.release();
     slot->swap_buffers(*ctx);
     slot->for_each_buffer([](auto& v) { v.owner = nullptr; });
+    slot->pool_cache.nodes.rebind(nullptr);
+    slot->pool_cache.edges.rebind(nullptr);
     if (!slot->d_scalars) std::swap(slot->d_scalars, ctx->d_scalars);
     if (!slot->h_scalars) std::swap(slot->h_scalars, ctx->h_scalars);
 }

@@ -589,6 +589,8 @@ WalkView make_view(const hsaw_gpu_stream* s, const hsaw_gpu_walkset* ws, int kin
         if (kind != HSAW_KIND_EDGE && kind != HSAW_KIND_NODE) fail(HSAW_EINVAL, "unknown item kind");
         if (off + cnt > s->accepted)
             fail(HSAW_ERANGE, "sample stream prefix not materialized");
+        if (kind == HSAW_KIND_EDGE ? !s->keep_edges : !s->keep_nodes)
+            fail(HSAW_EINVAL, "this stream does not keep the item array of that kind (stream_keep)");
         v.off = s->edge_off.p;
         v.items = kind == HSAW_KIND_EDGE ? s->edges.p : s->nodes.p;
         v.add = kind == HSAW_KIND_EDGE ? 0u : 1u;
@@ -661,24 +663,29 @@ static void histogram_counts(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t p0, 
         StageScope timer(ctx, HSAW_STAGE_INDEX);
         const uint64_t nitems = p1 - p0;
         int hb = (int)std::min<uint64_t>((nitems + 255) / 256, (uint64_t)wide);
-        const bool partition = (uint64_t)limit * 4 > (48ull << 20) && nitems > (1ull << 22) &&
-                               nitems < (1ull << 33);
+        const bool partition = (uint64_t)limit * 4 > (48ull << 20) && nitems > (1ull << 22);
         if (partition) {
+            // in slices of 2^29 items: the partitioned copy and the sort's scratch stay at 2 GB
+            // each however large the pool is (5 G items per half at the Twitter shape)
+            constexpr uint64_t kSlice = 1ull << 29;
             DevVec<uint32_t>& d_sorted = ctx->g_sorted;
-            d_sorted.ensure_scratch(nitems);
+            d_sorted.ensure_scratch(std::min(nitems, kSlice));
             int top = 32 - __builtin_clz(limit - 1);
             int begin_bit = std::max(0, top - 8);
-            size_t bytes = 0;
-            HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
-                nullptr, bytes, v.items + p0, d_sorted.p, (int64_t)nitems, begin_bit, top,
-                st));
-            ctx->cub_tmp.ensure_scratch(bytes ? bytes : 1);
-            HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
-                ctx->cub_tmp.p, bytes, v.items + p0, d_sorted.p, (int64_t)nitems,
-                begin_bit, top, st));
-            ++ctx->launches;
-            key_histogram<<<hb, 256, 0, st>>>(d_sorted.p, nitems, limit, d_cand, d_cnt);
-            check_launch(ctx, "key_histogram");
+            for (uint64_t at = 0; at < nitems; at += kSlice) {
+                const uint64_t len = std::min(kSlice, nitems - at);
+                size_t bytes = 0;
+                HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
+                    nullptr, bytes, v.items + p0 + at, d_sorted.p, (int64_t)len, begin_bit, top, st));
+                ctx->cub_tmp.ensure_scratch(bytes ? bytes : 1);
+                HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(
+                    ctx->cub_tmp.p, bytes, v.items + p0 + at, d_sorted.p, (int64_t)len, begin_bit,
+                    top, st));
+                ++ctx->launches;
+                int sb = (int)std::min<uint64_t>((len + 255) / 256, (uint64_t)wide);
+                key_histogram<<<sb, 256, 0, st>>>(d_sorted.p, len, limit, d_cand, d_cnt);
+                check_launch(ctx, "key_histogram");
+            }
         } else {
             item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt);
             check_launch(ctx, "item_histogram");
@@ -860,13 +867,12 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             const uint32_t kMaxTailList = 4096;
             const size_t tail_smem = (size_t)nblk * 8 + ((size_t)nblk + 31) / 32 * 4;
             const bool tail_ok = !tail_off && tail_smem <= (200u << 10);
-            static size_t tail_smem_set = 0;
-            if (tail_ok && tail_smem > tail_smem_set) {
+            // the opt-in is a per-device function attribute: set before every use (it is a
+            // host-side table write, nothing next to a launch)
+            if (tail_ok && tail_smem > (48u << 10))
                 HSAW_CUDA_CHECK(cudaFuncSetAttribute(greedy_tail_kernel,
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     (int)std::max<size_t>(tail_smem, 48u << 10)));
-                tail_smem_set = std::max<size_t>(tail_smem, 48u << 10);
-            }
+                                                     (int)tail_smem));
             uint32_t* d_done = reinterpret_cast<uint32_t*>(d_partial.p + 2);
             bool try_tail = tail_ok;
             while (done < k && !exhausted) {

@@ -14,6 +14,7 @@ using namespace hsawgpu;
 namespace {
 
 constexpr uint64_t kMaxChunkBatches = 1ull << 22;  // bounds per-chunk scratch (slots = 10x this)
+constexpr uint64_t kArenaTargetBytes = 6ull << 30;  // soft bound of the K1 pair-log arena per chunk
 
 // (batch, seq) slots -> dense encoded list in batch-major order. One thread per slot.
 __global__ void gather_encoded(uint64_t nbatches, uint32_t l, uint64_t first_global_batch,
@@ -78,8 +79,10 @@ __global__ void compact_walks(uint64_t nwalks, const uint32_t* __restrict__ vfla
             tag_batch[dw] = enc_batch[w];
             tag_seq[dw] = enc_seq[w];
         }
-        for (uint32_t i = lane; i <= len; i += 32) nodes[de + dw + i] = tmp_nodes[se + w + i];
-        for (uint32_t i = lane; i < len; i += 32) edges[de + i] = tmp_edges[se + i];
+        if (nodes)
+            for (uint32_t i = lane; i <= len; i += 32) nodes[de + dw + i] = tmp_nodes[se + w + i];
+        if (edges)
+            for (uint32_t i = lane; i < len; i += 32) edges[de + i] = tmp_edges[se + i];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0)
         edge_off[base_walk + vidx[nwalks]] = base_edge + voff[nwalks];
@@ -125,34 +128,82 @@ __global__ void place_overflow(uint64_t nwalks, const uint32_t* __restrict__ ovf
     sel[atomicAdd(nsel, 1u)] = (uint32_t)w;  // order is irrelevant: each entry is independent work
 }
 
-// One warp per decoded walk: pair log -> final node / edge arrays of the pool.
-__global__ void compact_pairs(uint64_t nwalks, const uint32_t* __restrict__ vflag,
-                              const uint32_t* __restrict__ vidx, const uint64_t* __restrict__ voff,
-                              const uint2* const* __restrict__ enc_src,
-                              const uint32_t* __restrict__ enc_len,
-                              const uint64_t* __restrict__ enc_batch,
-                              const uint32_t* __restrict__ enc_seq, uint64_t base_walk,
-                              uint64_t base_edge, uint64_t* __restrict__ edge_off,
-                              uint32_t* __restrict__ nodes, uint32_t* __restrict__ edges,
-                              uint64_t* __restrict__ tag_batch, uint32_t* __restrict__ tag_seq) {
-    uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    uint32_t lane = threadIdx.x & 31;
-    uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t w = warp; w < nwalks; w += nwarps) {
-        if (!vflag[w]) continue;
-        uint64_t dw = base_walk + vidx[w];
-        uint64_t de = base_edge + voff[w];
-        uint32_t len = enc_len[w];
-        const uint2* src = enc_src[w];
-        if (lane == 0) {
+// Pair logs -> final node / edge arrays of the pool. One warp per group of 32 encoded walks: each
+// lane reads the metadata of one walk (coalesced), then the group's nodes are copied ITEM-parallel:
+// the kept walks of a group are contiguous in the pool, so flat node index q of the group maps to
+// pool position G + q, and its (walk, position) comes from a 5-step shuffle search over the group's
+// node-count prefix. Every lane moves one item per step whatever the walk lengths are and the
+// stores of a step are 32 consecutive words. nodes / edges may be null (array not kept).
+__global__ void __launch_bounds__(256) compact_pairs(
+    uint64_t nwalks, const uint32_t* __restrict__ vflag, const uint32_t* __restrict__ vidx,
+    const uint64_t* __restrict__ voff, const uint2* const* __restrict__ enc_src,
+    const uint32_t* __restrict__ enc_len, const uint64_t* __restrict__ enc_batch,
+    const uint32_t* __restrict__ enc_seq, uint64_t base_walk, uint64_t base_edge,
+    uint64_t* __restrict__ edge_off, uint32_t* __restrict__ nodes, uint32_t* __restrict__ edges,
+    uint64_t* __restrict__ tag_batch, uint32_t* __restrict__ tag_seq) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t groups = (nwalks + 31) / 32;
+    for (uint64_t grp = warp; grp < groups; grp += nwarps) {
+        const uint64_t w = grp * 32 + lane;
+        const bool valid = w < nwalks && vflag[w];
+        uint32_t len = 0;
+        const uint2* src = nullptr;
+        uint64_t dw = 0, de = 0;
+        if (valid) {
+            len = enc_len[w];
+            src = enc_src[w];
+            dw = base_walk + vidx[w];
+            de = base_edge + voff[w];
             edge_off[dw] = de;
             tag_batch[dw] = enc_batch[w];
             tag_seq[dw] = enc_seq[w];
         }
-        for (uint32_t i = lane; i <= len; i += 32) {
-            uint2 pr = src[i];
-            nodes[de + dw + i] = pr.x;
-            if (i) edges[de + i - 1] = pr.y;
+        const unsigned vmask = __ballot_sync(kFullMask, valid);
+        if (!vmask) continue;
+        const uint32_t cnt = valid ? len + 1 : 0;
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFullMask, incl, d);
+            if (lane >= (uint32_t)d) incl += t;
+        }
+        const uint32_t start = incl - cnt;  // first flat node index of this lane's walk
+        const uint32_t total = __shfl_sync(kFullMask, incl, 31);
+        const int first = __ffs(vmask) - 1;
+        const uint64_t G = __shfl_sync(kFullMask, (unsigned long long)(de + dw), first);   // pool node position of q = 0
+        const uint64_t dw0 = __shfl_sync(kFullMask, (unsigned long long)dw, first);
+        for (uint32_t q0 = 0; q0 < total; q0 += 64) {
+            uint2 pr[2];
+            uint32_t ii[2], jj[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t q = q0 + 32 * u + lane;
+                uint32_t j = 0;  // largest lane whose walk starts at or before q
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const uint32_t s_at = __shfl_sync(kFullMask, start, (j + step) & 31);
+                    if (s_at <= q) j += step;
+                }
+                const uint32_t sj = __shfl_sync(kFullMask, start, j);
+                const uint2* sp = reinterpret_cast<const uint2*>(
+                    __shfl_sync(kFullMask, (unsigned long long)src, j));
+                ii[u] = q - sj;
+                jj[u] = j;
+                if (q < total) pr[u] = __ldcs(sp + ii[u]);  // the log is read exactly once
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t q = q0 + 32 * u + lane;
+                if (q >= total) continue;
+                if (nodes) nodes[G + q] = pr[u].x;
+                if (edges && ii[u]) {
+                    // walk j is the (rank of j among the kept lanes)-th kept walk of the group
+                    const uint64_t dwj = dw0 + __popc(vmask & ((1u << jj[u]) - 1u));
+                    edges[G + q - dwj - 1] = pr[u].y;
+                }
+            }
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -275,17 +326,19 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
 
         // ---- append to the pool
         s->edge_off.reserve(s->accepted + A + 1, st);
-        s->nodes.reserve(s->total_edges + VT + s->accepted + A, st);
-        s->edges.reserve(s->total_edges + VT + 1, st);
+        if (s->keep_nodes) s->nodes.reserve(s->total_edges + VT + s->accepted + A, st);
+        if (s->keep_edges) s->edges.reserve(s->total_edges + VT + 1, st);
         s->tag_batch.reserve(s->accepted + A + 1, st);
         s->tag_seq.reserve(s->accepted + A + 1, st);
-        int cblocks = (int)std::min<uint64_t>((E + 7) / 8, (uint64_t)ctx->sm_count * 16);
+        // one warp per group of 32 encoded walks, 8 warps per block
+        int cblocks = (int)std::min<uint64_t>((E + 255) / 256, (uint64_t)ctx->sm_count * 16);
         {
             StageScope timer(ctx, HSAW_STAGE_COMPACT);
             compact_walks<<<cblocks, 256, 0, st>>>(
                 E, vflag, x.vidx.p, x.voff.p, x.tmp_off.p, x.tmp_nodes.p, x.tmp_edges.p,
                 x.enc_len.p, x.enc_batch.p, x.enc_seq.p, s->accepted, s->total_edges,
-                s->edge_off.p, s->nodes.p, s->edges.p, s->tag_batch.p, s->tag_seq.p);
+                s->edge_off.p, s->keep_nodes ? s->nodes.p : nullptr,
+                s->keep_edges ? s->edges.p : nullptr, s->tag_batch.p, s->tag_seq.p);
             check_launch(ctx, "compact_walks");
         }
     } else {
@@ -316,8 +369,8 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->total_edges += VT;
     s->local_batches += nb;
     s->edge_off.size = s->accepted + 1;
-    s->nodes.size = s->total_edges + s->accepted;
-    s->edges.size = s->total_edges;
+    s->nodes.size = s->keep_nodes ? s->total_edges + s->accepted : 0;
+    s->edges.size = s->keep_edges ? s->total_edges : 0;
     s->tag_batch.size = s->accepted;
     s->tag_seq.size = s->accepted;
     s->accepted_after_batch.size = s->local_batches;
@@ -433,17 +486,19 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
             fail(HSAW_EDATA, "decode: replay disagreed with generation (internal error)");
 
         s->edge_off.reserve(s->accepted + A + 1, st);
-        s->nodes.reserve(s->total_edges + VT + s->accepted + A, st);
-        s->edges.reserve(s->total_edges + VT + 1, st);
+        if (s->keep_nodes) s->nodes.reserve(s->total_edges + VT + s->accepted + A, st);
+        if (s->keep_edges) s->edges.reserve(s->total_edges + VT + 1, st);
         s->tag_batch.reserve(s->accepted + A + 1, st);
         s->tag_seq.reserve(s->accepted + A + 1, st);
-        int cblocks = (int)std::min<uint64_t>((E + 7) / 8, (uint64_t)ctx->sm_count * 16);
+        // one warp per group of 32 encoded walks, 8 warps per block
+        int cblocks = (int)std::min<uint64_t>((E + 255) / 256, (uint64_t)ctx->sm_count * 16);
         {
             StageScope timer(ctx, HSAW_STAGE_COMPACT);
             compact_pairs<<<cblocks, 256, 0, st>>>(
                 E, vflag, x.vidx.p, x.voff.p, reinterpret_cast<const uint2* const*>(x.enc_src.p),
                 x.enc_len.p, x.enc_batch.p, x.enc_seq.p, s->accepted, s->total_edges,
-                s->edge_off.p, s->nodes.p, s->edges.p, s->tag_batch.p, s->tag_seq.p);
+                s->edge_off.p, s->keep_nodes ? s->nodes.p : nullptr,
+                s->keep_edges ? s->edges.p : nullptr, s->tag_batch.p, s->tag_seq.p);
             check_launch(ctx, "compact_pairs");
         }
     } else {
@@ -479,8 +534,8 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->total_edges += VT;
     s->local_batches += nb;
     s->edge_off.size = s->accepted + 1;
-    s->nodes.size = s->total_edges + s->accepted;
-    s->edges.size = s->total_edges;
+    s->nodes.size = s->keep_nodes ? s->total_edges + s->accepted : 0;
+    s->edges.size = s->keep_edges ? s->total_edges : 0;
     s->tag_batch.size = s->accepted;
     s->tag_seq.size = s->accepted;
     s->accepted_after_batch.size = s->local_batches;
@@ -502,6 +557,14 @@ void sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches) {
     uint64_t done = 0;
     while (done < nbatches) {
         uint64_t nb = std::min(nbatches - done, kMaxChunkBatches);
+        // a chunk's slots carry 32-bit walk ids, and its pair-log arena (about 1.5x the expected
+        // log volume) is kept to a few gigabytes: long walks (Twitter shape: 130 pairs per accepted
+        // walk) get smaller chunks instead of a 25 GB arena
+        const uint64_t bs = std::max<uint64_t>(s->cfg.batch_size, 1);
+        nb = std::min(nb, std::max<uint64_t>(0xFFFFFFF0ull / bs, 1));
+        const double per_attempt = s->pairs_per_attempt > 0 ? s->pairs_per_attempt : 24.0;
+        const uint64_t arena_batches = (uint64_t)((double)(kArenaTargetBytes / 8) / (per_attempt * 1.5 * (double)bs));
+        nb = std::min(nb, std::max<uint64_t>(arena_batches, 1ull << 14));
         if (fused_enabled() && record_supported(s->cfg))
             sample_chunk_fused(s, first_batch + done, nb);
         else
@@ -576,7 +639,7 @@ void hsaw_gpu_stream_destroy(hsaw_gpu_stream* s) {
     current_stream() = s->ctx->stream;
     // hand the walk-pool buffers to the context for the next stream (keep the larger set)
     PoolCache& pc = s->ctx->pool_cache;
-    if (s->nodes.cap >= pc.nodes.cap) {
+    if (s->nodes.cap + s->edges.cap >= pc.nodes.cap + pc.edges.cap) {
         pc.edge_off.swap(s->edge_off);
         pc.nodes.swap(s->nodes);
         pc.edges.swap(s->edges);
@@ -711,6 +774,8 @@ int hsaw_gpu_stream_export(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
                                         cudaMemcpyDeviceToHost, st));
         HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
         uint64_t e0 = edge_off[0], e1 = edge_off[cnt];
+        if ((nodes && !s->keep_nodes) || (edges && !s->keep_edges))
+            fail(HSAW_EINVAL, "stream_export: this stream does not keep that item array");
         if (nodes && (e1 - e0 + cnt))
             HSAW_CUDA_CHECK(cudaMemcpyAsync(nodes, s->nodes.p + e0 + off, (e1 - e0 + cnt) * 4,
                                             cudaMemcpyDeviceToHost, st));
@@ -727,6 +792,16 @@ int hsaw_gpu_stream_export(const hsaw_gpu_stream* s, uint64_t off, uint64_t cnt,
         for (uint64_t i = 0; i <= cnt; ++i) edge_off[i] -= e0;
         if (tag_worker)
             for (uint64_t i = 0; i < cnt; ++i) tag_worker[i] += s->seed;  // worker id = seed + batch
+    });
+}
+
+int hsaw_gpu_stream_keep(hsaw_gpu_stream* s, int keep_nodes, int keep_edges) {
+    if (!s) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        if (s->local_batches) fail(HSAW_EINVAL, "stream_keep: must be called before sampling");
+        if (!keep_nodes && !keep_edges) fail(HSAW_EINVAL, "stream_keep: nothing to keep");
+        s->keep_nodes = keep_nodes != 0;
+        s->keep_edges = keep_edges != 0;
     });
 }
 

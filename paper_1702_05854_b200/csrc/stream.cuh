@@ -13,8 +13,11 @@ struct hsaw_gpu_stream {
     // pool: walk w has edges [edge_off[w], edge_off[w+1]) and nodes
     // [edge_off[w] + w, edge_off[w+1] + w + 1)  (len + 1 nodes per walk, no padding)
     hsawgpu::DevVec<uint64_t> edge_off;  // accepted + 1
-    hsawgpu::DevVec<uint32_t> nodes;     // total_edges + accepted
-    hsawgpu::DevVec<uint32_t> edges;     // total_edges
+    hsawgpu::GrowVec<uint32_t> nodes;    // total_edges + accepted   (grown in place, see GrowVec)
+    hsawgpu::GrowVec<uint32_t> edges;    // total_edges
+    // Which item arrays the pool keeps (hsaw_gpu_stream_keep): a solve over edge candidates never
+    // reads the node lists and vice versa; at the Twitter shape each array is tens of gigabytes.
+    bool keep_nodes = true, keep_edges = true;
     hsawgpu::DevVec<uint64_t> tag_batch; // global batch index of each walk (worker id = seed + it)
     hsawgpu::DevVec<uint32_t> tag_seq;   // seq within the batch, assigned before decode drops
     uint64_t accepted = 0, total_edges = 0;

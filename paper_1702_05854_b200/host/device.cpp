@@ -486,10 +486,19 @@ std::optional<HsawSample> DecodeContext::decode(const EncodedWalk& ew) {
 }
 
 // ---- SampleStream -------------------------------------------------------------------------------
-SampleStream::SampleStream(const DeviceGraph& dg, std::uint64_t seed, SamplerConfig cfg)
+SampleStream::SampleStream(const DeviceGraph& dg, std::uint64_t seed, SamplerConfig cfg,
+                           Items items)
     : dg_(dg) {
     hsaw_sampler_cfg c = to_c(cfg);
     raise(hsaw_gpu_stream_create(dg.ctx(), seed, &c, &s_), dg.ctx(), "SampleStream");
+    if (items != Items::Both) {
+        const int rc = hsaw_gpu_stream_keep(s_, items == Items::NodesOnly, items == Items::EdgesOnly);
+        if (rc != HSAW_OK) {
+            hsaw_gpu_stream_destroy(s_);
+            s_ = nullptr;
+            raise(rc, dg.ctx(), "SampleStream");
+        }
+    }
 }
 
 SampleStream::~SampleStream() { hsaw_gpu_stream_destroy(s_); }

@@ -284,7 +284,11 @@ private:
 // SampleStream (proj/include/hsaw/sampler.hpp:133-163): decoded walks stay on the device.
 class SampleStream {
 public:
-    SampleStream(const DeviceGraph& dg, std::uint64_t seed, SamplerConfig cfg = {});
+    // Which item lists of each walk the device pool keeps (hsaw_gpu_stream_keep). The drivers
+    // ask for the one their candidate kind indexes; prefix() / to_pool() need Both.
+    enum class Items { Both, EdgesOnly, NodesOnly };
+    SampleStream(const DeviceGraph& dg, std::uint64_t seed, SamplerConfig cfg = {},
+                 Items items = Items::Both);
     ~SampleStream();
     SampleStream(const SampleStream&) = delete;
     SampleStream& operator=(const SampleStream&) = delete;

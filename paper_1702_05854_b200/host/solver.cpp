@@ -95,7 +95,10 @@ InterdictionResult run_on_device(const DeviceGraph& dg, const ProbGraph& g,
     const Schedule sched = compute_schedule(g, cand.kind, k, epsilon, delta);
     const std::uint64_t base = sched.lambda_samples();
 
-    SampleStream stream(dg, opts.seed, opts.sampler);
+    // the pool keeps only the item lists this candidate kind indexes (coverage.cpp:49-53)
+    SampleStream stream(dg, opts.seed, opts.sampler,
+                        cand.kind == ItemKind::Edge ? SampleStream::Items::EdgesOnly
+                                                    : SampleStream::Items::NodesOnly);
     InterdictionResult res;
     res.kind = cand.kind;
     res.k = k;

@@ -172,10 +172,12 @@ class Graph:
         while this Graph is alive."""
         o, s_, c = u64p(), u32p(), f64p()
         lib().hsawh_graph_ptrs(self.h, C.byref(o), C.byref(s_), C.byref(c))
-        m = max(self.m, 1)
+        if self.m == 0:
+            return (np.ctypeslib.as_array(o, shape=(self.n + 1,)), np.zeros(0, dtype=np.uint32),
+                    np.zeros(0, dtype=np.float64))
         return (np.ctypeslib.as_array(o, shape=(self.n + 1,)),
-                np.ctypeslib.as_array(s_, shape=(m,))[: self.m],
-                np.ctypeslib.as_array(c, shape=(m,))[: self.m])
+                np.ctypeslib.as_array(s_, shape=(self.m,)),
+                np.ctypeslib.as_array(c, shape=(self.m,)))
 
     @classmethod
     def from_csr(cls, n, m, in_offsets, in_src, in_cum):

@@ -428,3 +428,32 @@ def test_large_upload_staged_and_plain(ctx, port, monkeypatch, threads):
     exp = port.stream_samples(csr, 3000, seed=5)
     assert got.attempts == exp.attempts and got.nsamples == exp.nsamples
     assert np.array_equal(got.nodes, exp.nodes) and np.array_equal(got.edges, exp.edges)
+
+
+def test_stream_keeping_one_item_array(ctx, gpu_lib, synth3000, port):
+    """hsaw_gpu_stream_keep: a pool that keeps only the edge ids (or only the nodes) has the same
+    order and counters, serves greedy / coverage of its own kind bit-exactly, and refuses the other."""
+    upload(ctx, synth3000)
+    with ctx.stream(seed=11) as both, ctx.stream(seed=11) as eo, ctx.stream(seed=11) as no:
+        eo.keep(nodes=False, edges=True)
+        no.keep(nodes=True, edges=False)
+        for st in (both, eo, no):
+            st.ensure(3000)
+        assert both.size() == eo.size() == no.size()
+        assert both.counters_for(3000) == eo.counters_for(3000) == no.counters_for(3000)
+        ref_pool = both.export(0, 3000)
+        e_pool = eo.export(0, 3000, nodes=False)
+        n_pool = no.export(0, 3000, edges=False)
+        assert np.array_equal(e_pool.edges, ref_pool.edges) and np.array_equal(n_pool.nodes, ref_pool.nodes)
+        assert np.array_equal(e_pool.edge_off, ref_pool.edge_off)
+        for kind, st, other in ((0, eo, no), (1, no, eo)):
+            a_sol, a_cov = ctx.greedy(7, stream=st, kind=kind, off=0, cnt=1500)
+            b_sol, b_cov = ctx.greedy(7, stream=both, kind=kind, off=0, cnt=1500)
+            assert a_sol.tolist() == b_sol.tolist() and a_cov == b_cov
+            with pytest.raises(gpu_lib.HsawError) as e:
+                ctx.greedy(7, stream=other, kind=kind, off=0, cnt=1500)
+            assert e.value.status == gpu_lib.HSAW_EINVAL
+        with pytest.raises(gpu_lib.HsawError):
+            eo.export(0, 10)
+        with pytest.raises(gpu_lib.HsawError):
+            eo.keep(nodes=True, edges=True)  # too late: sampling has started
