@@ -112,3 +112,61 @@ def test_solver_result_is_layout_independent(monkeypatch, c2, kind, k):
         assert r["samples_used"] == 2 * (r["samples_used"] // 2)
         out[layout] = r
     assert out["compact"] == out["fat"]
+
+
+# ---- the reference's own full-size results (tests/golden/make_c2_golden.py: the unmodified
+# reference compiled into oracle/_ref solved these on the same C2 arrays, 11 + 5 minutes of CPU)
+@pytest.fixture(scope="module")
+def c2_golden():
+    import json
+    import os
+
+    from conftest import GOLDEN_DIR
+    with open(os.path.join(GOLDEN_DIR, "c2_reference.json")) as f:
+        return json.load(f)
+
+
+RESULT_KEYS = ("solution", "coverage", "attempts", "samples_used", "iterations", "est_suspension",
+               "passed_check")
+
+
+@pytest.mark.parametrize("layout", ["compact", "fat"])
+@pytest.mark.parametrize("name,kind,k", [("esia_k100", 0, 100), ("nsia_k100", 1, 100),
+                                         ("esia_k1000", 0, 1000)])
+def test_solver_equals_the_reference_at_full_size(monkeypatch, c2, c2_golden, layout, name, kind, k):
+    """interdiction.cpp:12-67 end to end at BASELINE configs[1]: every InterdictionResult field the
+    reference produced, bit for bit (est_suspension included: same FP64 expression on the host)."""
+    from paper_1702_05854_b200 import hostapi
+    g, csr, _ = c2
+    gold = c2_golden[name]
+    assert (c2_golden["graph"]["n"], c2_golden["graph"]["m"]) == (g.n, g.m)
+    monkeypatch.setenv("HSAW_LAYOUT", layout)
+    r = hostapi.interdict(g, csr.p_of, kind, k, 0.1, 1.0 / g.n, seed=42, max_attempts=10**15)
+    for key in RESULT_KEYS:
+        assert r[key] == gold[key], key
+
+
+def test_fixed_walk_set_greedy_at_full_size(gpu_lib, monkeypatch, c2, c2_golden):
+    """north_star's mode 1 at real size: the device pool IS the reference's walk set of the last
+    eSIA iteration (sha256 over lengths, nodes and edge ids of 7.7 M walks / 360 M items), and the
+    device greedy on R_t (its first half) selects the reference's k edges with the same coverage."""
+    import hashlib
+    g, csr, _ = c2
+    gold = c2_golden["esia_k100"]
+    su = gold["samples_used"]
+    for k_ in ("HSAW_LAYOUT", "HSAW_FORCE_EXACT", "HSAW_PACK"):
+        monkeypatch.delenv(k_, raising=False)
+    with gpu_lib.Context(0) as ctx:
+        ctx.upload_graph(csr.n, csr.m, csr.in_offsets, csr.in_src, csr.in_cum, csr.p_of)
+        with ctx.stream(seed=42, cfg=gpu_lib.SamplerCfg(max_attempts=10**15)) as st:
+            st.ensure(su)
+            pool = st.export(0, su)
+            h = hashlib.sha256()
+            h.update(np.ascontiguousarray(pool.edge_off.astype(np.uint64)).tobytes())
+            h.update(np.ascontiguousarray(pool.nodes).tobytes())
+            h.update(np.ascontiguousarray(pool.edges).tobytes())
+            assert int(pool.edge_off[-1]) == gold["walkset_items"]
+            assert h.hexdigest() == gold["walkset_sha256"]
+            sol, cov = ctx.greedy(100, stream=st, kind=0, off=0, cnt=su // 2)
+            assert sol.tolist() == gold["greedy_on_rt"]["solution"] == gold["solution"]
+            assert cov == gold["greedy_on_rt"]["coverage"] == gold["coverage"]
