@@ -127,6 +127,9 @@ int hsawh_estimate_suspension(const void* dg, const void* g, const double* p_of,
                               uint64_t* state, double* value, int* capped, uint64_t* runs);
 
 /* ---- CLI (proj/include/hsaw/cli.hpp) ---- */
+/* A double as the result JSON prints it (nlohmann::json::dump's number layout,
+ * proj/src/interdiction.cpp:89-104). */
+void hsawh_json_number(double x, char* out, uint64_t cap);
 int hsawh_run_cli(int argc, const char** argv);
 
 #ifdef __cplusplus

@@ -395,6 +395,12 @@ int hsawh_estimate_suspension(const void* dg, const void* g, const double* p_of,
     });
 }
 
+void hsawh_json_number(double x, char* out, uint64_t cap) {
+    const std::string s = json_number(x);
+    std::strncpy(out, s.c_str(), cap - 1);
+    out[cap - 1] = 0;
+}
+
 int hsawh_run_cli(int argc, const char** argv) {
     return run_cli(std::vector<std::string>(argv, argv + argc));
 }

@@ -110,7 +110,10 @@ ProbGraph load_graph(const Flags& f, std::uint64_t seed) {
     opts.symmetrize = f.switches.count("symmetrize") != 0;
     // text edge lists are parsed, re-ranked, sorted and summed on the device; anything outside the
     // device parser's plain grammar goes through the host parser inside this call
-    return load_edge_list_device(path, weight_mode(f.str("weights", "indegree")), seed, opts,
+    // the reference's GraphArgs::seed is never bound to --seed (proj/src/cli.cpp:28,47,410): the
+    // graph is always loaded with seed 0, --seed drives suspects and sampling only
+    (void)seed;
+    return load_edge_list_device(path, weight_mode(f.str("weights", "indegree")), 0, opts,
                                  static_cast<int>(f.u64("device", 0)));
 }
 
@@ -168,14 +171,8 @@ std::string json_real(double x) {
     return s.str();
 }
 
-// nlohmann's number form: shortest round-trip, ".0" when integral (as to_json in solver.cpp)
-std::string json_shortest(double x) {
-    char buf[64];
-    auto res = std::to_chars(buf, buf + sizeof buf, x);
-    std::string s(buf, res.ptr);
-    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
-    return s;
-}
+// nlohmann's number form (json_number, solver.cpp)
+std::string json_shortest(double x) { return json_number(x); }
 
 const std::set<std::string> kGraphFlags = {"graph", "weights", "suspects", "random-suspects"};
 

@@ -417,6 +417,8 @@ InterdictionResult nsia(const DeviceGraph& dg, const ProbGraph& g, const Candida
                         std::uint32_t k, double epsilon, double delta,
                         const InterdictionOptions& opts = {});
 
+// A double as nlohmann::json::dump prints it (fixed notation for decimal exponents in (-4, 15]).
+std::string json_number(double x);
 std::string to_json(const InterdictionResult& r, bool include_timing = true);
 
 // ---- evaluation (proj/include/hsaw/evaluation.hpp:16-39) ----------------------------------------

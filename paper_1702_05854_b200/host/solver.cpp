@@ -6,6 +6,7 @@
 // come out bit-identical with the same libm.
 #include <charconv>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <limits>
@@ -205,17 +206,45 @@ InterdictionResult nsia(const ProbGraph& g, const SuspectSet& vi, const Candidat
 // Same document as nlohmann::json::dump(2) produces for the reference (interdiction.cpp:89-104):
 // keys in alphabetical order, two-space indent, one array element per line, doubles in shortest
 // round-trip form with a ".0" suffix when integral. tests/golden/interdict12.json is byte-stable.
-namespace {
-
+// nlohmann::json::dump formats doubles with its Grisu2 "to_chars": shortest round-trip digits laid
+// out in FIXED notation while the decimal exponent n satisfies -4 < n <= 15 ("0.0001",
+// "100000.0", "1000000.0"; integral values get ".0"), otherwise d[.ddd]e[+-]XX with at least two
+// exponent digits. std::to_chars alone would pick whichever form is shorter ("1e-04", "1e+05").
 std::string json_number(double x) {
+    if (x == 0.0) return std::signbit(x) ? "-0.0" : "0.0";
+    if (!std::isfinite(x)) return "null";  // nlohmann dumps non-finite numbers as null
     char buf[64];
-    auto res = std::to_chars(buf, buf + sizeof buf, x);
-    std::string s(buf, res.ptr);
-    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
-    return s;
+    auto res = std::to_chars(buf, buf + sizeof buf, x, std::chars_format::scientific);
+    std::string sci(buf, res.ptr);  // [-]d[.ddd]e[+-]XX, shortest round-trip digits
+    std::string out;
+    std::size_t pos = 0;
+    if (sci[0] == '-') {
+        out = "-";
+        pos = 1;
+    }
+    const std::size_t epos = sci.find('e');
+    std::string digits;
+    for (std::size_t i = pos; i < epos; ++i)
+        if (sci[i] != '.') digits += sci[i];
+    const int exp10 = std::stoi(sci.substr(epos + 1));
+    const int k = static_cast<int>(digits.size());
+    const int n = exp10 + 1;  // position of the decimal point relative to the digit string
+    if (k <= n && n <= 15) {  // integral: digits, zero padding, ".0"
+        out += digits + std::string(static_cast<std::size_t>(n - k), '0') + ".0";
+    } else if (0 < n && n <= 15) {  // dig.its
+        out += digits.substr(0, static_cast<std::size_t>(n)) + "." + digits.substr(static_cast<std::size_t>(n));
+    } else if (-4 < n && n <= 0) {  // 0.[000]digits
+        out += "0." + std::string(static_cast<std::size_t>(-n), '0') + digits;
+    } else {  // d[.igits]e+-XX
+        out += digits.substr(0, 1);
+        if (k > 1) out += "." + digits.substr(1);
+        const int e = n - 1;
+        char eb[16];
+        std::snprintf(eb, sizeof eb, "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
+        out += eb;
+    }
+    return out;
 }
-
-}  // namespace
 
 std::string to_json(const InterdictionResult& r, bool include_timing) {
     std::ostringstream out;

@@ -93,6 +93,8 @@ def lib() -> C.CDLL:
     L.hsawh_pool_free.argtypes = [vp]
     L.hsawh_pool_free.restype = None
     L.hsawh_run_cli.argtypes = [C.c_int, C.POINTER(C.c_char_p)]
+    L.hsawh_json_number.argtypes = [C.c_double, C.c_char_p, C.c_uint64]
+    L.hsawh_json_number.restype = None
     _LIB = L
     return L
 
@@ -411,6 +413,12 @@ def stream_samples(graph: Graph, p_of, target, seed=0, batch_size=10, max_attemp
         return Pool(at, eo, nodes[: te + ns], edges[:te], tw[:ns], ts[:ns])
     finally:
         lib().hsawh_pool_free(h)
+
+
+def json_number(x: float) -> str:
+    buf = C.create_string_buffer(64)
+    lib().hsawh_json_number(float(x), buf, len(buf))
+    return buf.value.decode()
 
 
 def run_cli(args: list[str]) -> int:

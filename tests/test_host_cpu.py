@@ -266,3 +266,34 @@ def test_file_formats_match_reference(host, ref, tmp_path):
         assert (tmp_path / "r.map").read_text() == (tmp_path / "m.map").read_text()
         ref.graph_free(rh)
     ref.graph_free(gh)
+
+
+def test_json_numbers_follow_nlohmann_layout(host):
+    """to_json (proj/src/interdiction.cpp:89-104) prints doubles as nlohmann::json::dump does:
+    fixed notation while the decimal exponent is in (-4, 15], else d.ddde+-XX. Expected strings
+    were produced by nlohmann 3.11.3 itself."""
+    cases = {1e-4: "0.0001", 1e5: "100000.0", 1e6: "1000000.0", 0.1: "0.1", 3.0: "3.0",
+             2.0664354087995083: "2.0664354087995083", 1e15: "1e+15", 123456789012345.0: "123456789012345.0",
+             1e16: "1e+16", 1.5e-5: "1.5e-05", 9.5367431640625e-07: "9.5367431640625e-07",
+             1.2345678901234568e+17: "1.2345678901234568e+17", 0.00012345: "0.00012345",
+             12345.678: "12345.678", -2.5: "-2.5", -1e-7: "-1e-07", 1e22: "1e+22",
+             5e-324: "5e-324", 804.4299041134876: "804.4299041134876", 0.0: "0.0"}
+    for x, want in cases.items():
+        assert host.json_number(x) == want, x
+
+
+def test_rmat_n_generalises_rmat(host):
+    """rmat_graph(scale, f) is rmat_graph_n(2^scale, floor(f 2^scale)); other node counts drop raw
+    edges with an endpoint >= n; suspects depend on the node count only."""
+    a, b = host.Graph.rmat(12, 8.0, seed=3), host.Graph.rmat_n(1 << 12, 8 << 12, seed=3)
+    assert all(np.array_equal(x, y) for x, y in zip(a.arrays(), b.arrays()))
+    g = host.Graph.rmat_n(3000, 40000, seed=3)
+    off, src, cum, w, dst = g.arrays()
+    assert g.n == 3000 and 0 < g.m < 40000 and src.max() < 3000 and off[-1] == g.m
+    key = dst.astype(np.int64) * g.n + src
+    assert np.all(np.diff(key) > 0) and not np.any(src == dst)
+    v = g.views()
+    assert np.array_equal(v[0], off) and np.array_equal(v[1], src) and v[2].tobytes() == cum.tobytes()
+    assert np.array_equal(host.random_suspects_n(3000, 30, 2), g.random_suspects(30, 2))
+    shell = host.Graph.shell(5, 7)
+    assert (shell.n, shell.m) == (5, 7)
