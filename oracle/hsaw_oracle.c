@@ -106,9 +106,16 @@ typedef struct { /* WalkCursor, sampler.cpp:16-62 */
     uint32_t edges;
 } cursor;
 
-/* WalkCursor::start with an empty domain, sampler.cpp:21-37 */
+/* WalkCursor::start, sampler.cpp:21-37: uniform over all nodes, or over the start domain */
 static int cursor_start(cursor* c, const orc_graph* g, uint64_t* draws) {
-    c->node = orc_pick_uniform_node(&c->s, g->n);
+    if (g->domain && g->ndomain) { /* sampler.cpp:26-31 */
+        double r = orc_u01(orc_prg_next(&c->s));
+        uint64_t idx = (uint64_t)(r * (double)g->ndomain);
+        if (idx >= g->ndomain) idx = g->ndomain - 1;
+        c->node = g->domain[idx];
+    } else {
+        c->node = orc_pick_uniform_node(&c->s, g->n);
+    }
     ++*draws;
     if (g->p_of[c->node] > 0.0) {
         double r = orc_u01(orc_prg_next(&c->s));
@@ -225,15 +232,28 @@ orc_attempt_result orc_attempt(const orc_graph* g, uint64_t* state, int heuristi
             res.len = hare.edges;
             break;
         }
+        if (g->allowed && !g->allowed[u]) { /* sampler.cpp:196-199: continuing needs u's adjacency */
+            res.crossed = 1;
+            break;
+        }
         win_push(&win, u);
     }
     *state = hare.s; /* sampler.cpp:202 */
     return res;
 }
 
-/* thread_sample, sampler.cpp:267-290 */
+/* thread_sample, sampler.cpp:267-290; with a restriction in g also sample_batch_restricted's
+ * attempt loop (sampler.cpp:520-536): *crossings counts the attempts that left the allowed set */
+static uint32_t thread_sample_x(const orc_graph* g, uint64_t worker_id, uint32_t l,
+                                const orc_cfg* cfg, uint64_t* seeds, uint32_t* lens,
+                                uint64_t* stats4, uint64_t* crossings);
 uint32_t orc_thread_sample(const orc_graph* g, uint64_t worker_id, uint32_t l, const orc_cfg* cfg,
                            uint64_t* seeds, uint32_t* lens, uint64_t* stats4) {
+    return thread_sample_x(g, worker_id, l, cfg, seeds, lens, stats4, NULL);
+}
+static uint32_t thread_sample_x(const orc_graph* g, uint64_t worker_id, uint32_t l,
+                                const orc_cfg* cfg, uint64_t* seeds, uint32_t* lens,
+                                uint64_t* stats4, uint64_t* crossings) {
     uint64_t s = orc_seed_from_worker(worker_id);
     for (int i = 0; i < 8; ++i) (void)orc_prg_next(&s); /* burn-in */
     uint32_t count = 0;
@@ -246,6 +266,7 @@ uint32_t orc_thread_sample(const orc_graph* g, uint64_t worker_id, uint32_t l, c
             stats4[2] += r.steps;
             stats4[3] += r.alg_bytes;
         }
+        if (crossings && r.crossed) ++*crossings;
         if (r.accepted) {
             seeds[count] = snapshot;
             lens[count] = r.len;
@@ -298,6 +319,7 @@ struct orc_pool {
     /* full stream bookkeeping for orc_interdict */
     uint64_t nbatches, cap_batches;
     uint64_t* accepted_after_batch;
+    uint64_t* crossed_after_batch; /* restricted sampling: cumulative crossings per batch */
 };
 
 static void pool_reserve(orc_pool* p, uint64_t more_samples, uint64_t more_items) {
@@ -358,8 +380,9 @@ static void stream_free(stream_t* st, int keep_pool) {
 static int stream_one_batch(stream_t* st) {
     orc_pool* p = st->pool;
     uint64_t wid = st->seed + p->nbatches;
-    uint32_t cnt = orc_thread_sample(st->g, wid, st->cfg.batch_size, &st->cfg, st->enc_seed,
-                                     st->enc_len, NULL);
+    uint64_t crossings = 0;
+    uint32_t cnt = thread_sample_x(st->g, wid, st->cfg.batch_size, &st->cfg, st->enc_seed,
+                                   st->enc_len, NULL, &crossings);
     for (uint32_t i = 0; i < cnt; ++i) {
         uint64_t need = (uint64_t)st->enc_len[i] + 1;
         if (need > st->tmp_cap) {
@@ -390,7 +413,10 @@ static int stream_one_batch(stream_t* st) {
     if (p->nbatches + 1 > p->cap_batches) {
         p->cap_batches = p->cap_batches ? p->cap_batches * 2 : 1024;
         p->accepted_after_batch = realloc(p->accepted_after_batch, p->cap_batches * 8);
+        p->crossed_after_batch = realloc(p->crossed_after_batch, p->cap_batches * 8);
     }
+    p->crossed_after_batch[p->nbatches] =
+        (p->nbatches ? p->crossed_after_batch[p->nbatches - 1] : 0) + crossings;
     p->accepted_after_batch[p->nbatches++] = p->nsamples;
     return 0;
 }
@@ -449,6 +475,32 @@ int orc_stream_samples(const orc_graph* g, uint64_t target, uint64_t seed, const
     p->attempts = attempts;
     p->nsamples = accepted;
     p->total_edges = p->edge_off[accepted];
+    stream_free(&st, 1);
+    *out = p;
+    return 0;
+}
+
+/* one part of distributed_sample, partition.cpp:183-268 */
+int orc_part_sample(const orc_graph* g, uint64_t target, uint64_t first_worker, const orc_cfg* cfg,
+                    orc_pool** out, uint64_t* crossings, uint64_t* attempts) {
+    stream_t st;
+    stream_init(&st, g, first_worker, cfg);
+    int rc = stream_ensure(&st, target);
+    if (rc) {
+        stream_free(&st, 0);
+        return rc;
+    }
+    orc_pool* p = st.pool;
+    uint64_t att = 0, acc = 0;
+    *crossings = 0;
+    if (target > 0) { /* cut at the minimal batch prefix reaching the quota, :245-262 */
+        stream_counters(&st, target, &att, &acc);
+        *crossings = p->crossed_after_batch[att / cfg->batch_size - 1];
+    }
+    p->attempts = att;
+    p->nsamples = acc;
+    p->total_edges = acc ? p->edge_off[acc] : 0;
+    *attempts = att;
     stream_free(&st, 1);
     *out = p;
     return 0;

@@ -101,7 +101,140 @@ class PoolData:
 
 class _OrcGraph(C.Structure):
     _fields_ = [("n", C.c_uint32), ("m", C.c_uint32), ("in_offsets", u64p), ("in_src", u32p),
-                ("in_cum", f64p), ("p_of", f64p)]
+                ("in_cum", f64p), ("p_of", f64p),
+                ("domain", u32p), ("ndomain", C.c_uint64), ("allowed", C.POINTER(C.c_uint8))]
+
+
+@dataclass
+class Partitioning:
+    """proj/include/hsaw/partition.hpp:16-25: node -> part, part -> owned nodes (ascending), part ->
+    byte mask of the h-hop in-neighbourhood closure."""
+
+    p: int
+    hops: int
+    assign: np.ndarray      # u32[n]
+    base: list              # p arrays of u32 node ids
+    extended: list          # p arrays of u8[n]
+
+
+@dataclass
+class DistributedData:
+    """DistributedResult, partition.hpp:38-44."""
+
+    pool: "PoolData"
+    crossings: int
+    attempts: int
+    crossing_fraction: float
+    targets: list
+
+
+def splitmix_output(x: int) -> int:
+    """splitmix_next(x).output, proj/include/hsaw/prng.hpp:29-38."""
+    M = (1 << 64) - 1
+    z = (x + 0x9E3779B97F4A7C15) & M
+    o = z
+    o = ((o ^ (o >> 30)) * 0xBF58476D1CE4E5B9) & M
+    o = ((o ^ (o >> 27)) * 0x94D049BB133111EB) & M
+    return o ^ (o >> 31)
+
+
+def partition_graph_np(csr: "Csr", p: int, method: str = "hash", seed: int = 0, assign=None):
+    """partition_graph, proj/src/partition.cpp:29-121 (restated; small graphs only — the label
+    propagation is a per-node Python loop). method: 'hash' (v mod p), 'labelprop', 'external'
+    (assign given)."""
+    n = csr.n
+    if p < 1 or p > n:
+        raise BuildError("part count must be in [1, n]")
+    if method == "hash":
+        a = (np.arange(n, dtype=np.uint64) % p).astype(np.uint32)
+    elif method == "external":
+        a = np.ascontiguousarray(assign, dtype=np.uint32)
+        if a.size != n or (a.size and a.max() >= p):
+            raise BuildError("part file does not match the graph")
+    elif method == "labelprop":
+        M = (1 << 64) - 1
+        label = np.array([splitmix_output((seed * 0x9E3779B97F4A7C15 + v) & M) % p
+                          for v in range(n)], dtype=np.int64)
+        dst = np.repeat(np.arange(n, dtype=np.int64), np.diff(csr.in_offsets).astype(np.int64))
+        src = csr.in_src.astype(np.int64)
+        neigh = [set() for _ in range(n)]
+        for u, v in zip(src.tolist(), dst.tolist()):  # undirected view, antiparallel edges once
+            neigh[u].add(v)
+            neigh[v].add(u)
+        cap = max((n * 115 + 100 * p - 1) // (100 * p), 1)
+        for _ in range(10):
+            size = [0] * p
+            nxt = label.copy()
+            for v in range(n):
+                freq = [0] * p
+                freq[label[v]] = 1
+                for u in neigh[v]:
+                    freq[label[u]] += 1
+                best = p
+                for c in range(p):
+                    if size[c] >= cap:
+                        continue
+                    if best == p or freq[c] > freq[best]:
+                        best = c
+                nxt[v] = best
+                size[best] += 1
+            label = nxt
+        size = np.bincount(label, minlength=p).tolist()
+        for c in range(p):  # a starved label gets one node from the largest part (:95-110)
+            if size[c] > 0:
+                continue
+            donor = int(np.argmax(size))
+            for v in range(n - 1, -1, -1):
+                if label[v] == donor:
+                    label[v] = c
+                    size[donor] -= 1
+                    size[c] += 1
+                    break
+        a = label.astype(np.uint32)
+    else:
+        raise ValueError(method)
+    base = [np.nonzero(a == i)[0].astype(np.uint32) for i in range(p)]
+    return extend_partition_np(csr, Partitioning(p, 0, a, base, []), 0)
+
+
+def extend_partition_np(csr: "Csr", part: Partitioning, h: int) -> Partitioning:
+    """extend_partition, proj/src/partition.cpp:123-145: h-step in-neighbourhood closure."""
+    ext = []
+    off = csr.in_offsets.astype(np.int64)
+    for i in range(part.p):
+        mask = np.zeros(csr.n, dtype=np.uint8)
+        frontier = part.base[i].astype(np.int64)
+        mask[frontier] = 1
+        for _ in range(h):
+            if frontier.size == 0:
+                break
+            lens = off[frontier + 1] - off[frontier]
+            idx = np.repeat(off[frontier], lens) + (np.arange(lens.sum()) -
+                                                    np.repeat(np.cumsum(lens) - lens, lens))
+            u = np.unique(csr.in_src[idx].astype(np.int64))
+            u = u[mask[u] == 0]
+            mask[u] = 1
+            frontier = u
+        ext.append(mask)
+    return Partitioning(part.p, h, part.assign, part.base, ext)
+
+
+def part_quotas(total_target: int, sizes: list, n: int) -> list:
+    """Largest-remainder quotas proportional to |part|, proj/src/partition.cpp:163-181."""
+    targets, rema, assigned = [], [], 0
+    for i, sz in enumerate(sizes):
+        share = float(total_target) * float(sz) / float(n)
+        t = int(share)
+        targets.append(t)
+        assigned += t
+        rema.append((share - float(t), i))
+    rema.sort(key=lambda a: (-a[0], a[1]))
+    for r in range(total_target - assigned):
+        targets[rema[r % len(sizes)][1]] += 1
+    return targets
+
+
+PART_STRIDE = 1 << 40  # worker-id window per part, proj/src/partition.cpp:14
 
 
 class _OrcCfg(C.Structure):
@@ -225,9 +358,41 @@ class Port:
 
     # -- helpers
     @staticmethod
-    def _g(csr: Csr):
+    def _g(csr: Csr, domain=None, allowed=None):
+        if domain is None:
+            return _OrcGraph(csr.n, csr.m, _p(csr.in_offsets, u64p), _p(csr.in_src, u32p),
+                             _p(csr.in_cum, f64p), _p(csr.p_of, f64p), None, 0, None)
         return _OrcGraph(csr.n, csr.m, _p(csr.in_offsets, u64p), _p(csr.in_src, u32p),
-                         _p(csr.in_cum, f64p), _p(csr.p_of, f64p))
+                         _p(csr.in_cum, f64p), _p(csr.p_of, f64p), _p(domain, u32p), domain.size,
+                         allowed.ctypes.data_as(C.POINTER(C.c_uint8)))
+
+    # -- partitioned sampling (proj/src/partition.cpp:153-279)
+    def distributed_sample(self, csr, part: "Partitioning", total_target, seed=0, heuristic=0,
+                           window=2, batch_size=10, max_attempts=100_000_000) -> "DistributedData":
+        for i in range(part.p):
+            if part.base[i].size == 0:
+                raise BuildError(f"part {i} is empty")
+        targets = part_quotas(total_target, [b.size for b in part.base], csr.n)
+        cfg = self._cfg(heuristic, window, batch_size, max_attempts)
+        pools, crossings, attempts = [], 0, 0
+        M = (1 << 64) - 1
+        for i in range(part.p):
+            dom = np.ascontiguousarray(part.base[i], dtype=np.uint32)
+            mask = np.ascontiguousarray(part.extended[i], dtype=np.uint8)
+            g = self._g(csr, dom, mask)
+            h, cr, at = C.c_void_p(), C.c_uint64(), C.c_uint64()
+            rc = self.L.orc_part_sample(C.byref(g), targets[i], (seed + i * PART_STRIDE) & M,
+                                        C.byref(cfg), C.byref(h), C.byref(cr), C.byref(at))
+            if rc:
+                raise OracleError(rc, "distributed_sample")
+            try:
+                pools.append(_copy_pool(self.L.orc_pool_stats, self.L.orc_pool_copy, h))
+            finally:
+                self.L.orc_pool_free(h)
+            crossings += cr.value
+            attempts += at.value
+        return DistributedData(concat_pools(pools, attempts), crossings, attempts,
+                               crossings / attempts if attempts else 0.0, targets)
 
     @staticmethod
     def _cfg(heuristic=0, window=2, batch_size=10, max_attempts=100_000_000):
@@ -362,6 +527,19 @@ class Port:
         if rc:
             raise OracleError(rc, "estimate_suspension")
         return dict(value=out.value, capped=bool(out.capped), runs=int(out.runs), state=s.value)
+
+
+def concat_pools(pools, attempts) -> "PoolData":
+    """Pools of the parts appended in part order (partition.cpp:263-266)."""
+    eo, base = [np.zeros(1, dtype=np.uint64)], 0
+    for q in pools:
+        eo.append(q.edge_off[1:].astype(np.uint64) + np.uint64(base))
+        base += int(q.edge_off[-1])
+    cat = lambda xs, dt: np.concatenate(xs) if xs else np.zeros(0, dtype=dt)
+    return PoolData(attempts, np.concatenate(eo), cat([q.nodes for q in pools], np.uint32),
+                    cat([q.edges for q in pools], np.uint32),
+                    cat([q.tag_worker for q in pools], np.uint64),
+                    cat([q.tag_seq for q in pools], np.uint32))
 
 
 def _copy_pool(stats_fn, copy_fn, h) -> PoolData:

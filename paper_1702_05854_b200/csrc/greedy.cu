@@ -185,7 +185,20 @@ __device__ __forceinline__ uint64_t block_max_u64(uint64_t v, uint64_t* smem) {
 // bound until that bound is exact — then it is the global argmax — instead of scanning all
 // `limit` counters (16 M for C2 edges, 1.47 G at the Twitter shape) every round. Keys are
 // count << 32 | ~id, unique per item, so the (largest gain, smallest id) order is preserved.
-constexpr uint32_t kMaxBlockItems = 2048;
+// Block size: 2^bshift items, at least 2048, and large enough for the bounds of all blocks to fit
+// the tail kernel's shared memory (1.47 G edge ids at the Twitter shape -> 65536-item blocks,
+// 22 k bounds; a grid-wide round over 717 k 2048-item blocks cost 0.33 ms there).
+constexpr uint32_t kMinBlockShift = 11;
+constexpr uint32_t kTailMaxBlocks = 24000;  // x 8 bytes + exact bits <= 200 KB of shared memory
+inline uint32_t block_shift_for(uint64_t limit) {
+    uint32_t sh = kMinBlockShift;
+    if (const char* env = std::getenv("HSAW_GREEDY_BLOCK_SHIFT")) {  // test hook: force large blocks
+        const int v = std::atoi(env);
+        if (v >= (int)kMinBlockShift && v <= 20) sh = (uint32_t)v;
+    }
+    while (((limit + (1ull << sh) - 1) >> sh) > kTailMaxBlocks && sh < 31) ++sh;
+    return sh;
+}
 constexpr uint32_t kUnindexed = 0xFFFFFFFEu;  // round marker: winner below the index threshold
 
 __device__ __forceinline__ uint64_t gain_key(uint32_t count, uint32_t id) {
@@ -194,8 +207,10 @@ __device__ __forceinline__ uint64_t gain_key(uint32_t count, uint32_t id) {
 
 // blkmax[b] = exact max key of items [b * 2048, (b + 1) * 2048)
 __global__ void __launch_bounds__(256) block_maxima(const uint32_t* __restrict__ cnt,
-                                                    uint32_t limit, uint64_t* __restrict__ blkmax) {
+                                                    uint32_t limit, uint64_t* __restrict__ blkmax,
+                                                    uint32_t bshift) {
     __shared__ uint64_t smem[32];
+    const uint32_t kMaxBlockItems = 1u << bshift;
     const uint64_t base = (uint64_t)blockIdx.x * kMaxBlockItems;
     uint64_t best = 0;
     for (uint32_t i = threadIdx.x; i < kMaxBlockItems; i += blockDim.x) {
@@ -213,9 +228,11 @@ __global__ void __launch_bounds__(256) block_maxima(const uint32_t* __restrict__
 // largest bound is exact. Writes the winner key to out[0] (0 = no positive gain left).
 __global__ void __launch_bounds__(1024) select_lazy(const uint32_t* __restrict__ cnt,
                                                     uint32_t limit, uint64_t* __restrict__ blkmax,
-                                                    uint32_t nblk, uint64_t* __restrict__ out) {
+                                                    uint32_t nblk, uint64_t* __restrict__ out,
+                                                    uint32_t bshift) {
     __shared__ uint64_t smem[32];
     __shared__ uint32_t s_blk;
+    const uint32_t kMaxBlockItems = 1u << bshift;
     // The block of the previous round's winner holds the stalest bound there is (the winner's own
     // key, now covered): tighten it up front instead of spending a whole scan to find that out.
     // (Whatever out[0] holds, recomputing a valid block's maximum exactly is always sound.)
@@ -338,7 +355,8 @@ __global__ void __launch_bounds__(1024) greedy_tail_kernel(
     const uint32_t* __restrict__ inv, uint32_t* cnt, uint32_t* covered, uint64_t* blkmax,
     uint32_t nblk, uint32_t first, uint32_t k, uint32_t* __restrict__ solution,
     uint64_t* __restrict__ gains, uint32_t min_indexed, uint32_t max_list,
-    uint32_t* __restrict__ done_out, int bounds_exact) {
+    uint32_t* __restrict__ done_out, int bounds_exact, uint32_t bshift) {
+    const uint32_t kMaxBlockItems = 1u << bshift;
     // s_max[b]: upper bound of block b's maximum key; s_exact bit b: the bound IS the maximum.
     // A bound is made exact by recomputing the block and stays exact until the item that attains
     // it is decremented (decrements of other items cannot change a maximum), which the cover
@@ -771,7 +789,8 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         d_cnt.ensure_scratch((uint64_t)limit + 4);
         d_fill.ensure_scratch((uint64_t)limit + 4);
         d_pos.ensure_scratch((uint64_t)limit + 2);
-        const uint32_t nblk = (uint32_t)(((uint64_t)limit + kMaxBlockItems - 1) / kMaxBlockItems);
+        const uint32_t bshift = block_shift_for(limit);
+        const uint32_t nblk = (uint32_t)(((uint64_t)limit + (1ull << bshift) - 1) >> bshift);
         d_partial.ensure_scratch(kCountBins + 4);
         d_blkmax.ensure_scratch(nblk + 1);
         d_sol.ensure_scratch(k);
@@ -851,7 +870,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             // ---- rounds
             if (p1 > p0) {
                 StageScope timer(ctx, HSAW_STAGE_ROUNDS);
-                block_maxima<<<nblk, 256, 0, st>>>(d_cnt.p, limit, d_blkmax.p);
+                block_maxima<<<nblk, 256, 0, st>>>(d_cnt.p, limit, d_blkmax.p, bshift);
                 check_launch(ctx, "block_maxima");
             }
             done = 0;
@@ -884,7 +903,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                         greedy_tail_kernel<<<1, 1024, tail_smem, st>>>(
                             v, d_cand, d_pos.p, d_inv.p, d_cnt.p, d_cov.p, d_blkmax.p, nblk, done,
                             k, d_sol.p, d_gain.p, min_count, kMaxTailList, d_done,
-                            blkmax_fresh ? 1 : 0);
+                            blkmax_fresh ? 1 : 0, bshift);
                         blkmax_fresh = false;  // the tail's own rounds decrement counts
                         check_launch(ctx, "greedy_tail_kernel");
                     }
@@ -900,7 +919,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                     StageScope timer(ctx, HSAW_STAGE_ROUNDS);
                     for (uint32_t r = done; r < done + group; ++r) {
                         select_lazy<<<1, 1024, 0, st>>>(d_cnt.p, limit, d_blkmax.p, nblk,
-                                                        d_partial.p);
+                                                        d_partial.p, bshift);
                         check_launch(ctx, "select_lazy");
                         cover_winner<<<cover_blocks, 256, 0, st>>>(
                             v, d_partial.p, 1, d_cand, d_pos.p, d_inv.p, d_cnt.p, d_cov.p, r,
@@ -977,6 +996,7 @@ struct hsaw_gpu_rounds {
     DevVec<uint64_t> pos, partial, scalars;
     uint64_t occurrences = 0;
     uint32_t npartial = 0;
+    uint32_t bshift = 11;
     bool maxima_ready = false;
 };
 
@@ -1039,7 +1059,8 @@ int hsaw_gpu_rounds_begin(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             uint64_t cov_words = (cnt + 31) / 32 + 1;
             g->covered.ensure_scratch(cov_words);
             HSAW_CUDA_CHECK(cudaMemsetAsync(g->covered.p, 0, cov_words * 4, st));
-            g->npartial = (uint32_t)((limit + kMaxBlockItems - 1) / kMaxBlockItems);  // blocks
+            g->bshift = block_shift_for(limit);
+            g->npartial = (uint32_t)(((uint64_t)limit + (1ull << g->bshift) - 1) >> g->bshift);  // blocks
             g->partial.ensure_scratch(g->npartial + 1);  // block maxima, built at the first select
             HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
             collect_timings(ctx);
@@ -1061,12 +1082,12 @@ int hsaw_gpu_rounds_select(hsaw_gpu_rounds* g, uint32_t* item, uint64_t* gain) {
         {
             StageScope timer(ctx, HSAW_STAGE_ROUNDS);
             if (!g->maxima_ready) {  // after the caller's all-reduce of the counts
-                block_maxima<<<g->npartial, 256, 0, st>>>(g->d_counts, g->limit, g->partial.p);
+                block_maxima<<<g->npartial, 256, 0, st>>>(g->d_counts, g->limit, g->partial.p, g->bshift);
                 check_launch(ctx, "block_maxima");
                 g->maxima_ready = true;
             }
             select_lazy<<<1, 1024, 0, st>>>(g->d_counts, g->limit, g->partial.p, g->npartial,
-                                            g->scalars.p + 3);
+                                            g->scalars.p + 3, g->bshift);
             check_launch(ctx, "select_lazy");
             select_final<<<1, 256, 0, st>>>(g->scalars.p + 3, 1, g->scalars.p);
             check_launch(ctx, "select_final");

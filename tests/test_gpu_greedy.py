@@ -190,3 +190,21 @@ def test_coverage_upper_bound(ctx, port, synth3000, kind):
         ub = ctx.coverage_upper_bound(3, stream=st, kind=kind, off=0, cnt=nw, cand=cand)
         assert ub == min(int(np.sort(counts[cand])[::-1][:3].sum()), nw)
         assert pool.nsamples >= nw
+
+
+@pytest.mark.parametrize("shift", [13, 16])
+def test_large_maxima_blocks(gpu_lib, monkeypatch, port, shift):
+    """Id spaces past ~50 M items (1.47 G edge ids at the Twitter shape) use 2^shift-item maxima
+    blocks so that the single-CTA tail kernel still holds every bound in shared memory; forced here
+    on instances small enough for the oracle: same selections, gains and padding."""
+    monkeypatch.setenv("HSAW_GREEDY_BLOCK_SHIFT", str(shift))
+    rng = np.random.Generator(np.random.PCG64(21))
+    with gpu_lib.Context(0) as ctx:
+        for limit, nsets, k in ((300_000, 200_000, 300), (70_000, 400_000, 2_000), (5, 40, 5)):
+            z = ((np.minimum(rng.zipf(1.25, size=nsets * 3), 10**6) * 2654435761) % limit)
+            z = z.astype(np.uint32)
+            off = np.arange(0, 3 * nsets + 1, 3, dtype=np.uint64)
+            exp_sol, exp_cov = port.greedy(limit, off, z, k)
+            with ctx.walkset(limit, off, z) as ws:
+                sol, cov = ctx.greedy(k, walkset=ws)
+                assert cov == exp_cov and sol.tolist() == exp_sol.tolist()
