@@ -512,6 +512,8 @@ struct hsaw_gpu_ctx {
     // greedy / coverage scratch (greedy.cu), reused across the doubling iterations
     hsawgpu::DevVec<uint32_t> g_cand_bits, g_cnt, g_fill, g_inv, g_covered, g_solution, g_query_bits;
     hsawgpu::DevVec<uint32_t> g_indexed_bits;  // items that own an inverted list
+    hsawgpu::DevVec<uint32_t> g_filter;        // hashed membership pre-filter (greedy.cu BitFilter)
+    hsawgpu::DevVec<uint32_t> g_hist_prefix, g_hist_seg;  // histogram cache (greedy.cu HistCache)
     hsawgpu::DevVec<uint32_t> g_sorted;  // radix-partitioned copy of the items (large id spaces)
     hsawgpu::DevVec<uint64_t> g_pos, g_partial, g_gains, g_blkmax;
     uint64_t* d_scalars = nullptr;  // 64 u64 of device scratch for counters / cursors
@@ -553,6 +555,9 @@ struct hsaw_gpu_ctx {
         g_blkmax.swap(o.g_blkmax);
         g_sorted.swap(o.g_sorted);
         g_indexed_bits.swap(o.g_indexed_bits);
+        g_filter.swap(o.g_filter);
+        g_hist_prefix.swap(o.g_hist_prefix);
+        g_hist_seg.swap(o.g_hist_seg);
     }
     template <class F>
     void for_each_buffer(F&& f) {
@@ -565,7 +570,7 @@ struct hsaw_gpu_ctx {
         f(pool_cache.tag_seq);  // pool_cache.nodes / .edges are GrowVecs: handled by the callers
         f(g_cand_bits); f(g_cnt); f(g_fill); f(g_inv); f(g_covered); f(g_solution);
         f(g_query_bits); f(g_pos); f(g_partial); f(g_gains); f(g_blkmax); f(g_sorted);
-        f(g_indexed_bits);
+        f(g_indexed_bits); f(g_filter); f(g_hist_prefix); f(g_hist_seg);
     }
 
     void release_scratch() {
@@ -592,6 +597,9 @@ struct hsaw_gpu_ctx {
         g_blkmax.release();
         g_sorted.release();
         g_indexed_bits.release();
+        g_filter.release();
+        g_hist_prefix.release();
+        g_hist_seg.release();
     }
 };
 

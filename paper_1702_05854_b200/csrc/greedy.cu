@@ -9,6 +9,8 @@
 // number of still-uncovered walks containing it, ties to the smallest id; rounds whose best gain
 // is zero are padded with the smallest unselected candidate ids (host side).
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -43,6 +45,30 @@ struct WalkView {
 
 __device__ __forceinline__ bool is_cand(const uint32_t* __restrict__ cand_bits, uint32_t item) {
     return cand_bits == nullptr || ((cand_bits[item >> 5] >> (item & 31)) & 1u);
+}
+
+// Membership pre-filter for bitmaps that do not fit L2 (m / 8 bytes = 183 MB at the Twitter shape):
+// one hashed bit per member in a table small enough to stay cached (64 KB..16 MB). A clear bit
+// proves non-membership, so the random DRAM read of the real bitmap is only paid for members and
+// the few false positives; answers are unchanged. log2 == 0 disables the filter.
+struct BitFilter {
+    const uint32_t* bits;
+    uint32_t log2;  // table size in bits = 2^log2
+};
+__device__ __forceinline__ uint32_t filter_slot(uint32_t item, uint32_t log2) {
+    return (item * 0x9E3779B1u) >> (32 - log2);
+}
+__device__ __forceinline__ bool filter_pass(const BitFilter& f, uint32_t item) {
+    if (f.log2 == 0) return true;
+    const uint32_t h = filter_slot(item, f.log2);
+    return (__ldg(f.bits + (h >> 5)) >> (h & 31)) & 1u;
+}
+__global__ void set_filter_bits(const uint32_t* __restrict__ ids, uint64_t n, uint32_t log2,
+                                uint32_t* __restrict__ filter) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t h = filter_slot(ids[i], log2);
+    atomicOr(&filter[h >> 5], 1u << (h & 31));
 }
 
 __global__ void set_bits(const uint32_t* __restrict__ ids, uint64_t n, uint32_t* __restrict__ bits) {
@@ -80,7 +106,8 @@ __global__ void key_histogram(const uint32_t* __restrict__ keys, uint64_t n, uin
 // One bit per item: is it indexed (candidate with count >= min_count)? The bitmap (limit / 8
 // bytes) stays in L2, so the scatter pass needs no random HBM read per item to find that out.
 __global__ void mark_indexed(const uint32_t* __restrict__ cnt, uint32_t limit, uint32_t min_count,
-                             uint32_t* __restrict__ bits) {
+                             uint32_t* __restrict__ bits, uint32_t* __restrict__ filter,
+                             uint32_t filter_log2) {
     uint64_t word = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint64_t base = word * 32;
     if (base >= limit) return;
@@ -89,14 +116,20 @@ __global__ void mark_indexed(const uint32_t* __restrict__ cnt, uint32_t limit, u
     for (uint32_t j = 0; j < 32; ++j) {
         uint64_t id = base + j;
         // count > 0 already implies "candidate": the histogram only counts candidates
-        if (id < limit && cnt[id] >= min_count && cnt[id] != 0) w |= 1u << j;
+        if (id < limit && cnt[id] >= min_count && cnt[id] != 0) {
+            w |= 1u << j;
+            if (filter_log2) {
+                const uint32_t h = filter_slot((uint32_t)id, filter_log2);
+                atomicOr(&filter[h >> 5], 1u << (h & 31));
+            }
+        }
     }
     bits[word] = w;
 }
 
 __global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ indexed_bits,
-                                 const uint64_t* __restrict__ pos, uint32_t* __restrict__ fill,
-                                 uint32_t* __restrict__ inv) {
+                                 BitFilter filter, const uint64_t* __restrict__ pos,
+                                 uint32_t* __restrict__ fill, uint32_t* __restrict__ inv) {
     uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t lane = threadIdx.x & 31;
     uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -106,7 +139,8 @@ __global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ indexe
         for (uint64_t p = b + lane; p < e; p += 32) {
             uint32_t item = v.items[p];
             // only items that can still win a round are indexed (min_count, see hsaw_gpu_greedy)
-            if (item < v.limit && ((indexed_bits[item >> 5] >> (item & 31)) & 1u)) {
+            if (item < v.limit && filter_pass(filter, item) &&
+                ((indexed_bits[item >> 5] >> (item & 31)) & 1u)) {
                 uint32_t slot = atomicAdd(&fill[item], 1u);
                 inv[pos[item] + slot] = (uint32_t)i;
             }
@@ -518,6 +552,7 @@ __global__ void __launch_bounds__(1024) greedy_tail_kernel(
 // K6: one warp per walk; a walk counts once if any of its items is in the query bitmap.
 __global__ void __launch_bounds__(256) count_covered(WalkView v,
                                                      const uint32_t* __restrict__ query_bits,
+                                                     BitFilter filter,
                                                      unsigned long long* __restrict__ out) {
     uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t lane = threadIdx.x & 31;
@@ -529,7 +564,8 @@ __global__ void __launch_bounds__(256) count_covered(WalkView v,
         bool hit = false;
         for (uint64_t p = b + lane; p < e && !hit; p += 32) {
             uint32_t it = v.items[p];
-            hit = it < v.limit && ((query_bits[it >> 5] >> (it & 31)) & 1u);
+            hit = it < v.limit && filter_pass(filter, it) &&
+                  ((query_bits[it >> 5] >> (it & 31)) & 1u);
         }
         if (__any_sync(kFullMask, hit) && lane == 0) ++mine;
     }
@@ -668,6 +704,19 @@ uint64_t prepare_candidates(hsaw_gpu_ctx* ctx, uint32_t limit, const uint32_t* c
 
 }  // namespace
 
+// A zeroed filter table for `members` entries of an id space of `limit` items, or {nullptr, 0} when
+// the exact bitmap (limit / 8 bytes) is small enough to stay in L2 by itself. Sized for <= ~0.4 %
+// false positives, between 64 KB and 32 MB.
+static BitFilter prepare_filter(hsaw_gpu_ctx* ctx, uint64_t limit, uint64_t members) {
+    if (limit / 8 <= (24ull << 20)) return BitFilter{nullptr, 0};
+    uint32_t log2 = 19;
+    while ((1ull << log2) < members * 256 && log2 < 28) ++log2;
+    const uint64_t words = (1ull << log2) / 32;
+    ctx->g_filter.ensure_scratch(words);
+    HSAW_CUDA_CHECK(cudaMemsetAsync(ctx->g_filter.p, 0, words * 4, ctx->stream));
+    return BitFilter{ctx->g_filter.p, log2};
+}
+
 // K3: occurrences of every candidate item in the walks' item range [p0, p1) -> cnt[item] (cnt is
 // zeroed by the caller). When the counters do not fit L2, random atomics go to
 // HBM one 32-byte sector at a time; one 8-bit radix pass on the items' top bits first
@@ -683,9 +732,15 @@ static void histogram_counts(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t p0, 
         int hb = (int)std::min<uint64_t>((nitems + 255) / 256, (uint64_t)wide);
         const bool partition = (uint64_t)limit * 4 > (48ull << 20) && nitems > (1ull << 22);
         if (partition) {
-            // in slices of 2^29 items: the partitioned copy and the sort's scratch stay at 2 GB
-            // each however large the pool is (5 G items per half at the Twitter shape)
-            constexpr uint64_t kSlice = 1ull << 29;
+            // in slices: the partitioned copy and the sort's scratch stay bounded however large
+            // the pool is (5 G items per half at the Twitter shape). Every slice sweeps the whole
+            // counter array once (read + write back through L2), so slices are as large as free
+            // memory allows: an eighth of it per buffer, between 2^27 and 2^31 items.
+            size_t free_b = 0, total_b = 0;
+            HSAW_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+            uint64_t slice = 1ull << 27;
+            while (slice < (1ull << 31) && slice * 2 * 4 <= (free_b + ctx->g_sorted.cap * 4) / 8) slice *= 2;
+            const uint64_t kSlice = slice;
             DevVec<uint32_t>& d_sorted = ctx->g_sorted;
             d_sorted.ensure_scratch(std::min(nitems, kSlice));
             int top = 32 - __builtin_clz(limit - 1);
@@ -709,6 +764,115 @@ static void histogram_counts(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t p0, 
             check_launch(ctx, "item_histogram");
         }
     }
+}
+
+// ---- per-context histogram cache of a stream's walks -------------------------------------------------
+// The doubling loop (proj/src/interdiction.cpp:36-47) asks, iteration after iteration, for the
+// counts of R'_t = walks [s, 2s) (the upper bound) and of R_t = walks [0, s) (greedy). R_{t+1} is
+// R_t u R'_t, so with the counts of the prefix kept and each new segment folded into it, every
+// walk item is histogrammed exactly ONCE per solve instead of once per iteration that contains it
+// (at the Twitter shape: 20 G instead of 37 G random counter updates). Only for "all candidates".
+struct HistCache {
+    uint64_t stream_uid = 0;
+    int kind = -1;
+    uint64_t prefix_end = 0;              // prefix[] = counts of walks [0, prefix_end)
+    uint64_t seg_begin = 0, seg_end = 0;  // seg[] = counts of walks [seg_begin, seg_end), if seg_ok
+    bool seg_ok = false;
+};
+static HistCache& hist_cache(hsaw_gpu_ctx* ctx) {
+    static std::mutex mu;
+    static std::map<hsaw_gpu_ctx*, HistCache> caches;  // contexts are few and long-lived
+    std::lock_guard<std::mutex> lock(mu);
+    return caches[ctx];
+}
+
+__global__ void add_counts(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint64_t n) {
+    uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] += src[i];
+}
+
+static bool hist_cache_usable(const hsaw_gpu_stream* stream, const uint32_t* cand_ids) {
+    static const bool off = [] {
+        const char* env = std::getenv("HSAW_HIST_CACHE");  // A/B knob
+        return env && std::atoi(env) == 0;
+    }();
+    return stream != nullptr && cand_ids == nullptr && !off;
+}
+
+// accumulates the counts of the stream's walks [a, b) into cnt (not zeroed here)
+static void hist_accumulate(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind, uint64_t a,
+                            uint64_t b, uint32_t* cnt) {
+    if (b <= a) return;
+    WalkView v = make_view(stream, nullptr, kind, a, b - a);
+    uint64_t p0 = 0, p1 = 0;
+    view_span(ctx, v, &p0, &p1);
+    histogram_counts(ctx, v, p0, p1, nullptr, cnt);
+}
+
+static HistCache& hist_bind(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind,
+                            uint64_t limit) {
+    HistCache& hc = hist_cache(ctx);
+    ctx->g_hist_prefix.ensure_scratch(limit + 4);
+    ctx->g_hist_seg.ensure_scratch(limit + 4);
+    if (hc.stream_uid != stream->uid || hc.kind != kind) {
+        hc = HistCache{};
+        hc.stream_uid = stream->uid;
+        hc.kind = kind;
+    }
+    if (hc.prefix_end == 0)
+        HSAW_CUDA_CHECK(cudaMemsetAsync(ctx->g_hist_prefix.p, 0, (limit + 4) * 4, ctx->stream));
+    return hc;
+}
+
+// folds the cached segment into the prefix when it starts at or after the prefix's end (the gap,
+// if any, is histogrammed now): afterwards prefix = [0, seg_end)
+static void hist_fold(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind, uint64_t limit,
+                      HistCache& hc) {
+    if (!hc.seg_ok || hc.seg_begin < hc.prefix_end) return;
+    hist_accumulate(ctx, stream, kind, hc.prefix_end, hc.seg_begin, ctx->g_hist_prefix.p);
+    {
+        StageScope timer(ctx, HSAW_STAGE_INDEX);
+        add_counts<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(ctx->g_hist_prefix.p,
+                                                               ctx->g_hist_seg.p, limit);
+        check_launch(ctx, "add_counts");
+    }
+    hc.prefix_end = hc.seg_end;
+    hc.seg_ok = false;
+}
+
+// counts of the stream's walks [a, b), device resident, valid until the next cache call
+static const uint32_t* hist_segment(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind,
+                                    uint64_t limit, uint64_t a, uint64_t b) {
+    HistCache& hc = hist_bind(ctx, stream, kind, limit);
+    if (hc.seg_ok && hc.seg_begin == a && hc.seg_end == b) return ctx->g_hist_seg.p;
+    if (a == 0) {  // a prefix request in disguise
+        hist_fold(ctx, stream, kind, limit, hc);
+        hc.seg_ok = false;
+    } else {
+        hist_fold(ctx, stream, kind, limit, hc);
+    }
+    HSAW_CUDA_CHECK(cudaMemsetAsync(ctx->g_hist_seg.p, 0, (limit + 4) * 4, ctx->stream));
+    hist_accumulate(ctx, stream, kind, a, b, ctx->g_hist_seg.p);
+    hc.seg_begin = a;
+    hc.seg_end = b;
+    hc.seg_ok = true;
+    return ctx->g_hist_seg.p;
+}
+
+// counts of the stream's walks [0, x)
+static const uint32_t* hist_prefix(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind,
+                                   uint64_t limit, uint64_t x) {
+    HistCache& hc = hist_bind(ctx, stream, kind, limit);
+    if (hc.seg_ok && hc.seg_begin >= hc.prefix_end && hc.seg_end <= x)
+        hist_fold(ctx, stream, kind, limit, hc);
+    if (hc.prefix_end > x) {  // cannot shrink: start over
+        HSAW_CUDA_CHECK(cudaMemsetAsync(ctx->g_hist_prefix.p, 0, (limit + 4) * 4, ctx->stream));
+        hc.prefix_end = 0;
+    }
+    hist_accumulate(ctx, stream, kind, hc.prefix_end, x, ctx->g_hist_prefix.p);
+    hc.prefix_end = x;
+    return ctx->g_hist_prefix.p;
 }
 
 extern "C" {
@@ -810,8 +974,14 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_partial.p, 0, 8, st));  // no previous winner yet
-            // ---- K3: marginal-gain counts
-            histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
+            // ---- K3: marginal-gain counts (a stream prefix comes from the histogram cache)
+            if (hist_cache_usable(stream, cand_ids) && off == 0) {
+                const uint32_t* cached = hist_prefix(ctx, stream, kind, limit, cnt);
+                HSAW_CUDA_CHECK(cudaMemcpyAsync(d_cnt.p, cached, (uint64_t)limit * 4,
+                                                cudaMemcpyDeviceToDevice, st));
+            } else {
+                histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
+            }
             if (min_count == 0) {
                 // Index only what can win: the smallest count whose items (and everything above)
                 // make up at most 1/8 of all occurrences. Small inputs index everything.
@@ -861,10 +1031,11 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                 DevVec<uint32_t>& d_ibits = ctx->g_indexed_bits;
                 uint64_t words = ((uint64_t)limit + 31) / 32;
                 d_ibits.ensure_scratch(words + 1);
-                mark_indexed<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(d_cnt.p, limit,
-                                                                             min_count, d_ibits.p);
+                const BitFilter filt = prepare_filter(ctx, limit, indexed);
+                mark_indexed<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(
+                    d_cnt.p, limit, min_count, d_ibits.p, const_cast<uint32_t*>(filt.bits), filt.log2);
                 check_launch(ctx, "mark_indexed");
-                scatter_inverted<<<sb, 256, 0, st>>>(v, d_ibits.p, d_pos.p, d_fill.p, d_inv.p);
+                scatter_inverted<<<sb, 256, 0, st>>>(v, d_ibits.p, filt, d_pos.p, d_fill.p, d_inv.p);
                 check_launch(ctx, "scatter_inverted");
             }
             // ---- rounds
@@ -1050,10 +1221,10 @@ int hsaw_gpu_rounds_begin(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                 uint64_t words = (limit + 31) / 32;
                 g->indexed_bits.ensure_scratch(words + 1);
                 mark_indexed<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(
-                    d_counts, (uint32_t)limit, 1u, g->indexed_bits.p);
+                    d_counts, (uint32_t)limit, 1u, g->indexed_bits.p, nullptr, 0);
                 check_launch(ctx, "mark_indexed");
-                scatter_inverted<<<sb, 256, 0, st>>>(v, g->indexed_bits.p, g->pos.p, g->fill.p,
-                                                     g->inv.p);
+                scatter_inverted<<<sb, 256, 0, st>>>(v, g->indexed_bits.p, BitFilter{nullptr, 0},
+                                                     g->pos.p, g->fill.p, g->inv.p);
                 check_launch(ctx, "scatter_inverted");
             }
             uint64_t cov_words = (cnt + 31) / 32 + 1;
@@ -1171,13 +1342,18 @@ int hsaw_gpu_coverage_upper_bound(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stre
         uint64_t p0 = 0, p1 = 0;
         view_span(ctx, v, &p0, &p1);
         if (p1 == p0) return;
-        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
-        histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
+        const uint32_t* counts = d_cnt.p;
+        if (hist_cache_usable(stream, cand_ids)) {
+            counts = hist_segment(ctx, stream, kind, limit, off, off + cnt);
+        } else {
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
+            histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
+        }
         auto* d_bins = reinterpret_cast<unsigned long long*>(d_partial.p + 4);
         HSAW_CUDA_CHECK(cudaMemsetAsync(d_bins, 0, kCountBins * 8, st));
         {
             StageScope timer(ctx, HSAW_STAGE_INDEX);
-            count_of_counts<<<ctx->sm_count * 8, 256, 0, st>>>(d_cnt.p, limit, d_bins);
+            count_of_counts<<<ctx->sm_count * 8, 256, 0, st>>>(counts, limit, d_bins);
             check_launch(ctx, "count_of_counts");
         }
         std::vector<uint64_t> bins(kCountBins);
@@ -1242,7 +1418,13 @@ int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         {
             StageScope timer(ctx, HSAW_STAGE_COVERAGE);
             int blocks = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)ctx->sm_count * 8);
-            count_covered<<<blocks, 256, 0, st>>>(v, bits.p, d_out);
+            BitFilter filt = prepare_filter(ctx, v.limit, q.size());
+            if (filt.log2) {
+                set_filter_bits<<<qb, 256, 0, st>>>(d_q.p, q.size(), filt.log2,
+                                                    const_cast<uint32_t*>(filt.bits));
+                check_launch(ctx, "set_filter_bits");
+            }
+            count_covered<<<blocks, 256, 0, st>>>(v, bits.p, filt, d_out);
             check_launch(ctx, "count_covered");
             clear_bits<<<qb, 256, 0, st>>>(d_q.p, q.size(), bits.p);
             check_launch(ctx, "clear_bits");

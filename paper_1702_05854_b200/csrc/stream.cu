@@ -4,6 +4,7 @@
 // so prefixes of the pool are pure functions of (graph, suspects, seed) exactly as in the reference.
 #include "stream.cuh"
 
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 
@@ -604,6 +605,8 @@ int hsaw_gpu_stream_create(hsaw_gpu_ctx* ctx, uint64_t seed, const hsaw_sampler_
         if (!ctx->g.nodes) fail(HSAW_EINVAL, "stream_create: no graph uploaded");
         validate_cfg(*cfg);
         auto* s = new hsaw_gpu_stream;
+        static std::atomic<uint64_t> next_uid{1};
+        s->uid = next_uid.fetch_add(1);
         s->ctx = ctx;
         s->seed = seed;
         s->cfg = *cfg;

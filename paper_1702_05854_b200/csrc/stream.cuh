@@ -7,6 +7,7 @@
 
 struct hsaw_gpu_stream {
     hsaw_gpu_ctx* ctx = nullptr;
+    uint64_t uid = 0;  // process-unique id (caches keyed by stream must survive address reuse)
     uint64_t seed = 0;
     hsaw_sampler_cfg cfg{};
 
