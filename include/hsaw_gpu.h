@@ -205,6 +205,20 @@ int hsaw_gpu_stream_create(hsaw_gpu_ctx* ctx, uint64_t seed, const hsaw_sampler_
  * before sampling. Order, counters and every result are unaffected; greedy / coverage / export
  * calls that ask for a dropped array fail with HSAW_EINVAL. */
 int hsaw_gpu_stream_keep(hsaw_gpu_stream* stream, int keep_nodes, int keep_edges);
+
+/* Partitioned sampling: the per-part restricted stream of distributed_sample
+ * (proj/src/partition.cpp:183-268; detail::sample_batch_restricted, proj/src/sampler.cpp:510-539;
+ * WalkCursor::start with a domain, sampler.cpp:24-31; the crossing abort, sampler.cpp:196-199).
+ * domain: the part's base nodes, ascending (start nodes are drawn from it); allowed: byte mask over
+ * all n nodes (the part's h-hop extension). A walk that moves onto a node outside the mask without
+ * hitting is aborted and counted as a crossing. Call before sampling; the caller creates the
+ * stream with seed + part * 2^40 (partition.cpp:14,218). hsaw_gpu_stream_crossings gives the
+ * crossings of the minimal whole-batch prefix reaching min_accepted (the reference's
+ * crossed_after[cut_batches - 1]); hsaw_gpu_stream_counters gives its attempts and samples. */
+int hsaw_gpu_stream_restrict(hsaw_gpu_stream* stream, const uint32_t* domain, uint64_t ndomain,
+                             const uint8_t* allowed);
+int hsaw_gpu_stream_crossings(const hsaw_gpu_stream* stream, uint64_t min_accepted,
+                              uint64_t* crossings);
 void hsaw_gpu_stream_destroy(hsaw_gpu_stream* s);
 
 /* SampleStream::ensure (sampler.cpp:388-463): grow until >= min_accepted decoded samples exist.

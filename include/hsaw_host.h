@@ -127,6 +127,18 @@ int hsawh_estimate_suspension(const void* dg, const void* g, const double* p_of,
                               uint64_t* state, double* value, int* capped, uint64_t* runs);
 
 /* ---- CLI (proj/include/hsaw/cli.hpp) ---- */
+/* ---- partitioned sampling — proj/include/hsaw/partition.hpp:27-54 ---- */
+/* partition_graph (method 0 Hash, 1 LabelProp, 2 ExternalFile with part_file) followed by
+ * extend_partition(hops): assign_out u32[n], extended_out u8[p * n] part-major (nullable). */
+int hsawh_partition(const void* g, uint32_t p, int method, uint64_t seed, const char* part_file,
+                    uint32_t hops, uint32_t* assign_out, uint8_t* extended_out);
+/* distributed_sample on a DeviceGraph: pool handle for hsawh_pool_*, targets u64[p]. */
+int hsawh_distributed_sample(const void* dg, uint32_t n, uint32_t p, uint32_t hops,
+                             const uint32_t* assign, const uint8_t* extended,
+                             uint64_t total_target, uint64_t seed, uint32_t batch_size,
+                             uint64_t max_attempts, void** pool_out, uint64_t* crossings,
+                             uint64_t* attempts, double* crossing_fraction, uint64_t* targets);
+
 /* A double as the result JSON prints it (nlohmann::json::dump's number layout,
  * proj/src/interdiction.cpp:89-104). */
 void hsawh_json_number(double x, char* out, uint64_t cap);

@@ -310,6 +310,8 @@ class Port:
                                  u32p, u32p]
         L.orc_stream_samples.argtypes = [C.POINTER(_OrcGraph), C.c_uint64, C.c_uint64,
                                          C.POINTER(_OrcCfg), C.POINTER(C.c_void_p)]
+        L.orc_part_sample.argtypes = [C.POINTER(_OrcGraph), C.c_uint64, C.c_uint64,
+                                      C.POINTER(_OrcCfg), C.POINTER(C.c_void_p), u64p, u64p]
         L.orc_pool_stats.argtypes = [C.c_void_p, u64p, u64p, u64p]
         L.orc_pool_copy.argtypes = [C.c_void_p, u64p, u32p, u32p, u64p, u32p]
         L.orc_pool_free.argtypes = [C.c_void_p]
@@ -575,6 +577,18 @@ class Ref:
         L.ref_splitmix_next.argtypes = [C.c_uint64, u64p, u64p]
         L.ref_graph_from_csr.restype = C.c_void_p
         L.ref_graph_from_csr.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p]
+        L.ref_partition_graph.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_uint64, u32p,
+                                          C.POINTER(C.c_void_p)]
+        L.ref_extend_partition.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32,
+                                           C.POINTER(C.c_void_p)]
+        L.ref_partition_copy.argtypes = [C.c_void_p, u32p, C.POINTER(C.c_uint8)]
+        L.ref_partition_copy.restype = None
+        L.ref_partition_free.argtypes = [C.c_void_p]
+        L.ref_partition_free.restype = None
+        L.ref_distributed_sample.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                             C.c_uint64, C.c_uint32, C.c_int, C.c_uint32,
+                                             C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), u64p,
+                                             u64p, f64p, u64p]
         L.ref_graph_from_csr_lean.restype = C.c_void_p
         L.ref_graph_from_csr_lean.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p]
         L.ref_graph_build.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, f64p, C.c_int,
@@ -756,6 +770,69 @@ class Ref:
 
     def handles(self, csr: Csr, lean=False):
         return Ref._Handles(self, csr, lean)
+
+    # -- partitioned sampling (proj/include/hsaw/partition.hpp)
+    def partition(self, csr, p, method="hash", seed=0, assign=None, hops=0, hd=None) -> "Partitioning":
+        """partition_graph + extend_partition(h) by the reference -> Partitioning (numpy copy)."""
+        code = {"hash": 0, "labelprop": 1, "external": 2}[method]
+        a = None if assign is None else np.ascontiguousarray(assign, dtype=np.uint32)
+
+        def run(h):
+            ph, eh = C.c_void_p(), C.c_void_p()
+            self._chk(self.L.ref_partition_graph(h.g, p, code, seed, _p(a, u32p), C.byref(ph)),
+                      "partition_graph")
+            try:
+                self._chk(self.L.ref_extend_partition(h.g, ph, hops, C.byref(eh)), "extend_partition")
+                try:
+                    asg = np.zeros(csr.n, dtype=np.uint32)
+                    ext = np.zeros((p, csr.n), dtype=np.uint8)
+                    self.L.ref_partition_copy(eh, _p(asg, u32p),
+                                              ext.ctypes.data_as(C.POINTER(C.c_uint8)))
+                finally:
+                    self.L.ref_partition_free(eh)
+            finally:
+                self.L.ref_partition_free(ph)
+            base = [np.nonzero(asg == i)[0].astype(np.uint32) for i in range(p)]
+            return Partitioning(p, hops, asg, base, [ext[i].copy() for i in range(p)])
+
+        if hd is not None:
+            return run(hd)
+        with self.handles(csr) as h:
+            return run(h)
+
+    def distributed_sample(self, csr, part: "Partitioning", total_target, seed=0, workers=1,
+                           heuristic=0, window=2, batch_size=10, max_attempts=100_000_000,
+                           hd=None) -> "DistributedData":
+        def run(h):
+            ph, eh, pool = C.c_void_p(), C.c_void_p(), C.c_void_p()
+            a = np.ascontiguousarray(part.assign, dtype=np.uint32)
+            self._chk(self.L.ref_partition_graph(h.g, part.p, 2, 0, _p(a, u32p), C.byref(ph)),
+                      "partition_graph")
+            try:
+                self._chk(self.L.ref_extend_partition(h.g, ph, part.hops, C.byref(eh)),
+                          "extend_partition")
+                try:
+                    cr, at, fr = C.c_uint64(), C.c_uint64(), C.c_double()
+                    tg = np.zeros(part.p, dtype=np.uint64)
+                    self._chk(self.L.ref_distributed_sample(
+                        h.g, h.vi, eh, total_target, seed, workers, heuristic, window, batch_size,
+                        max_attempts, C.byref(pool), C.byref(cr), C.byref(at), C.byref(fr),
+                        _p(tg, u64p)), "distributed_sample")
+                    try:
+                        pd = _copy_pool(self.L.ref_pool_stats, self.L.ref_pool_copy, pool)
+                    finally:
+                        self.L.ref_pool_free(pool)
+                    return DistributedData(pd, cr.value, at.value, fr.value,
+                                           [int(x) for x in tg])
+                finally:
+                    self.L.ref_partition_free(eh)
+            finally:
+                self.L.ref_partition_free(ph)
+
+        if hd is not None:
+            return run(hd)
+        with self.handles(csr) as h:
+            return run(h)
 
     # -- sampler (same signatures as Port)
     def thread_sample(self, csr, worker_id, l, heuristic=0, window=2, hd=None):

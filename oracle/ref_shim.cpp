@@ -25,6 +25,7 @@
 #include "hsaw/evaluation.hpp"
 #include "hsaw/graph.hpp"
 #include "hsaw/interdiction.hpp"
+#include "hsaw/partition.hpp"
 #include "hsaw/prng.hpp"
 #include "hsaw/sampler.hpp"
 
@@ -353,6 +354,70 @@ void ref_pool_copy(void* pp, std::uint64_t* edge_off, std::uint32_t* nodes,
 }
 
 void ref_pool_free(void* p) { delete static_cast<Pool*>(p); }
+
+// ---- partitioned sampling (proj/include/hsaw/partition.hpp) -------------------
+// method: 0 Hash, 1 LabelProp, 2 = the given assignment (what ExternalFile reads,
+// built without the file: assign + rebuild_base + extend_partition(.., 0)).
+int ref_partition_graph(void* gp, std::uint32_t p, int method, std::uint64_t seed,
+                        const std::uint32_t* assign, void** out) {
+    return guarded([&] {
+        auto& g = *static_cast<ProbGraph*>(gp);
+        if (method == 2) {
+            if (p < 1 || p > g.n) throw DataError("part count must be in [1, n]");
+            Partitioning part;
+            part.p = p;
+            part.assign.assign(assign, assign + g.n);
+            part.base.assign(p, {});
+            for (NodeId v = 0; v < g.n; ++v) {
+                if (part.assign[v] >= p) throw DataError("part id out of range");
+                part.base[part.assign[v]].push_back(v);
+            }
+            *out = new Partitioning(extend_partition(g, std::move(part), 0));
+        } else {
+            *out = new Partitioning(partition_graph(
+                g, p, method == 0 ? PartitionMethod::Hash : PartitionMethod::LabelProp, seed));
+        }
+    });
+}
+int ref_extend_partition(void* gp, void* partp, std::uint32_t h, void** out) {
+    return guarded([&] {
+        *out = new Partitioning(extend_partition(*static_cast<ProbGraph*>(gp),
+                                                 *static_cast<Partitioning*>(partp), h));
+    });
+}
+// assign u32[n]; extended u8[p * n] (part-major); either may be null
+void ref_partition_copy(void* partp, std::uint32_t* assign, std::uint8_t* extended) {
+    auto& part = *static_cast<Partitioning*>(partp);
+    if (assign) std::memcpy(assign, part.assign.data(), 4 * part.assign.size());
+    if (extended)
+        for (std::uint32_t i = 0; i < part.p; ++i)
+            std::memcpy(extended + static_cast<std::size_t>(i) * part.assign.size(),
+                        part.extended[i].data(), part.extended[i].size());
+}
+void ref_partition_free(void* partp) { delete static_cast<Partitioning*>(partp); }
+
+// distributed_sample: pool handle (ref_pool_*), crossings, attempts, targets u64[p]
+int ref_distributed_sample(void* gp, void* vip, void* partp, std::uint64_t total_target,
+                           std::uint64_t seed, std::uint32_t workers, int heuristic,
+                           std::uint32_t window, std::uint32_t batch_size,
+                           std::uint64_t max_attempts, void** pool_out,
+                           std::uint64_t* crossings, std::uint64_t* attempts,
+                           double* crossing_fraction, std::uint64_t* targets) {
+    return guarded([&] {
+        SamplerConfig cfg = make_cfg(heuristic, window, batch_size, max_attempts);
+        auto& part = *static_cast<Partitioning*>(partp);
+        DistributedResult r = distributed_sample(*static_cast<ProbGraph*>(gp),
+                                                 *static_cast<SuspectSet*>(vip), part,
+                                                 total_target, seed, workers, cfg);
+        auto* p = new Pool;
+        p->pool = std::move(r.pool);
+        *pool_out = p;
+        *crossings = r.crossings;
+        *attempts = r.attempts;
+        *crossing_fraction = r.crossing_fraction;
+        for (std::uint32_t i = 0; i < part.p; ++i) targets[i] = r.targets[i];
+    });
+}
 
 // ---- coverage / greedy on raw item sets (fixed-walk-set mode) ---------------
 int ref_greedy(int kind, std::uint32_t limit, std::uint64_t nsets,

@@ -100,6 +100,8 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_decode_walks.argtypes = [vp, C.c_uint64, u64p, u32p, u64p, u32p, u32p, u8p]
     L.hsaw_gpu_stream_create.argtypes = [vp, C.c_uint64, C.POINTER(SamplerCfg), C.POINTER(vp)]
     L.hsaw_gpu_stream_keep.argtypes = [vp, C.c_int, C.c_int]
+    L.hsaw_gpu_stream_restrict.argtypes = [vp, u32p, C.c_uint64, C.POINTER(C.c_uint8)]
+    L.hsaw_gpu_stream_crossings.argtypes = [vp, C.c_uint64, u64p]
     L.hsaw_gpu_stream_destroy.argtypes = [vp]
     L.hsaw_gpu_stream_destroy.restype = None
     L.hsaw_gpu_stream_ensure.argtypes = [vp, C.c_uint64]
@@ -160,6 +162,7 @@ EXPORTS = (
     "hsaw_gpu_edge_text_install",
     "hsaw_gpu_rmat_build", "hsaw_gpu_held_csr_fetch", "hsaw_gpu_held_csr_install",
     "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout", "hsaw_gpu_stream_keep",
+    "hsaw_gpu_stream_restrict", "hsaw_gpu_stream_crossings",
 )
 
 
@@ -525,6 +528,19 @@ class Stream:
         """hsaw_gpu_stream_keep: which item arrays the pool holds (before sampling)."""
         self.ctx._chk(self.L.hsaw_gpu_stream_keep(self.h, int(nodes), int(edges)))
         return self
+
+    def restrict(self, domain, allowed):
+        """hsaw_gpu_stream_restrict: start domain + allowed byte mask (partitioned sampling)."""
+        d = np.ascontiguousarray(domain, dtype=np.uint32)
+        a = np.ascontiguousarray(allowed, dtype=np.uint8)
+        self.ctx._chk(self.L.hsaw_gpu_stream_restrict(self.h, _p(d, u32p), d.size,
+                                                      a.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return self
+
+    def crossings(self, min_accepted) -> int:
+        c = C.c_uint64()
+        self.ctx._chk(self.L.hsaw_gpu_stream_crossings(self.h, min_accepted, C.byref(c)))
+        return c.value
 
     def ensure(self, min_accepted):
         self.ctx._chk(self.L.hsaw_gpu_stream_ensure(self.h, min_accepted))

@@ -470,6 +470,15 @@ struct HeldCsr {
     bool valid = false;
 };
 
+// Partitioned sampling (proj/src/partition.cpp:153-279, sampler.cpp:510-539): while a restricted
+// stream samples a chunk, the sampler launches read the restriction from the context.
+struct Restriction {
+    const uint32_t* domain = nullptr;  // device: start nodes (a part's base list)
+    uint32_t ndomain = 0;
+    const uint8_t* allowed = nullptr;  // device: byte mask over nodes (the part's h-hop extension)
+    uint32_t* out_cross = nullptr;     // device: crossings per batch of the launch
+};
+
 // Walk-pool buffers handed back by a destroyed stream, taken over by the next one.
 struct PoolCache {
     DevVec<uint64_t> edge_off, tag_batch, accepted_after_batch;
@@ -509,6 +518,7 @@ struct hsaw_gpu_ctx {
     hsawgpu::SamplerScratch samp;                        // per-chunk sampler scratch
     hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
     hsawgpu::HeldCsr held;                               // device-built CSR awaiting install / fetch
+    hsawgpu::Restriction restr;                          // set only while a restricted chunk runs
     // greedy / coverage scratch (greedy.cu), reused across the doubling iterations
     hsawgpu::DevVec<uint32_t> g_cand_bits, g_cnt, g_fill, g_inv, g_covered, g_solution, g_query_bits;
     hsawgpu::DevVec<uint32_t> g_indexed_bits;  // items that own an inverted list

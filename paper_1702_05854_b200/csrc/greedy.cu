@@ -736,10 +736,13 @@ static void histogram_counts(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t p0, 
             // the pool is (5 G items per half at the Twitter shape). Every slice sweeps the whole
             // counter array once (read + write back through L2), so slices are as large as free
             // memory allows: an eighth of it per buffer, between 2^27 and 2^31 items.
-            size_t free_b = 0, total_b = 0;
-            HSAW_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-            uint64_t slice = 1ull << 27;
-            while (slice < (1ull << 31) && slice * 2 * 4 <= (free_b + ctx->g_sorted.cap * 4) / 8) slice *= 2;
+            uint64_t slice = 1ull << 28;
+            if (nitems > slice) {  // (cudaMemGetInfo is a slow call: only asked when it matters)
+                size_t free_b = 0, total_b = 0;
+                HSAW_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+                while (slice < (1ull << 31) && slice * 2 * 4 <= (free_b + ctx->g_sorted.cap * 4) / 8)
+                    slice *= 2;
+            }
             const uint64_t kSlice = slice;
             DevVec<uint32_t>& d_sorted = ctx->g_sorted;
             d_sorted.ensure_scratch(std::min(nitems, kSlice));

@@ -44,6 +44,12 @@ struct EncodeParams {
     uint32_t arena_cap;      // pairs
     uint32_t* arena_cursor;  // next free chunk (pairs)
     uint32_t* out_log;       // per (batch, seq) slot: first pair of the walk, or kLogOverflow
+    // restricted variant (RESTR): start nodes drawn from `domain`, walks that move onto a node
+    // outside `allowed` are aborted and counted per batch (sampler.cpp:24-31,196-199,528)
+    const uint32_t* domain;
+    uint32_t ndomain;
+    const uint8_t* allowed;
+    uint32_t* out_cross;
 };
 
 constexpr uint32_t kLogChunk = 4096;    // pairs per chunk (32 KB)
@@ -144,7 +150,7 @@ __device__ __forceinline__ bool claim(uint64_t* cursor, uint64_t total, bool wan
 // REC: 0 plain encode, 1 record walks (default stores), 2 record with streaming (.cs) stores.
 // STATS: per-lane work counters (draws, picks, algorithmic bytes) for instrumentation runs.
 // LAYOUT: kLayoutFat (32-byte edge records) or kLayoutCompact (in_src + 8-byte row headers).
-template <int HEUR, int WIN, int MINB, int REC, bool STATS, int LAYOUT>
+template <int HEUR, int WIN, int MINB, int REC, bool STATS, int LAYOUT, bool RESTR = false>
 __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) {
     // REC: every thread stages kStage pairs (128 bytes) in shared memory, slot-major so the
     // 8-byte accesses are conflict-free, and flushes whole 128-byte lines: short failed attempts
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
     uint32_t lo = 0, deg = 0;
     uint64_t tot = 0, scale = 0;  // fat layout: total-weight threshold and guess scale of the row
     uint32_t hw = 0, cur = 0;     // compact layout: header word and id of the current node
-    uint32_t nedges = 0, att = 0, cnt = 0;
+    uint32_t nedges = 0, att = 0, cnt = 0, ncross = 0;
     bool have = false, fresh = true, drained = false;
     Window<WIN> win;
     uint32_t b_anchor = kInvalidNode, b_power = 1, b_lam = 0;
@@ -198,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                 for (int i = 0; i < 8; ++i) (void)prg_next(s);  // burn-in, sampler.cpp:273
                 att = 0;
                 cnt = 0;
+                ncross = 0;
                 fresh = true;
                 have = true;
             }
@@ -212,7 +219,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
         if (fresh) {
             snapshot = s;  // Seed_h, sampler.cpp:155,277
             uint64_t k = draw53(s);
-            u = start_node(k, p.n);  // sampler.cpp:24
+            u = RESTR ? __ldg(p.domain + start_node(k, p.ndomain))  // sampler.cpp:26-31
+                      : start_node(k, p.n);                         // sampler.cpp:24
             nedges = 0;
             walking = true;
             if (STATS) st_draws += 1;
@@ -329,6 +337,10 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                 ++cnt;
                 if (STATS) st_acc += 1;
                 if (STATS) st_pairs += nedges + 1;  // items of the accepted walk (8 B each logged)
+            } else if (RESTR && !fresh && __ldg(p.allowed + u) == 0) {
+                // continuing would need u's adjacency, which this part does not hold: the attempt
+                // is aborted without another draw and counted as a crossing (sampler.cpp:196-199)
+                ++ncross;
             } else {
                 lo = rec.lo;
                 deg = rec.deg;
@@ -366,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             if (REC) lpos = astart;  // failed attempt: reuse its log space (no-op after accept)
             if (++att == p.l) {
                 p.out_count[bidx] = cnt;
+                if (RESTR) p.out_cross[bidx] = ncross;
                 have = false;
             }
         } else {
@@ -623,6 +636,9 @@ struct DecodeParams {
     // (node, edge id) pairs go to pair_dst[sel[i]]
     const uint32_t* sel;
     uint2* const* pair_dst;
+    // restricted replay (decode_restricted, sampler.cpp:299-338): the start node comes from the domain
+    const uint32_t* domain;
+    uint32_t ndomain;
 };
 
 template <bool PAIRS, int LAYOUT>
@@ -668,7 +684,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
                 if (p.nnodes) p.nnodes[w] = 0;
             } else {
                 uint64_t k = draw53(s);
-                u = start_node(k, p.n);
+                u = p.domain ? __ldg(p.domain + start_node(k, p.ndomain)) : start_node(k, p.n);
                 nedges = 0;
                 if (PAIRS)
                     pairs[0] = make_uint2(u, kInvalidNode);
@@ -978,8 +994,36 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
     if (nbatches > 0xFFFFFFFFull) fail(HSAW_EINVAL, "encode: more than 2^32 batches per launch");
     EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, src_ref(ctx->g), ctx->g.thr,
                    ctx->g.n, cfg.batch_size, cfg.window, first_worker, nbatches, d_seed, d_len, d_count,
-                   d_stats, d_cursor, nullptr, 0, nullptr, nullptr};
+                   d_stats, d_cursor, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr};
     const bool compact = ctx->g.layout == kLayoutCompact;
+    if (ctx->restr.domain) {  // partitioned sampling: the restricted instantiations, never recording
+        if (rec) fail(HSAW_EINVAL, "encode: restricted sampling does not record");
+        if (!ctx->restr.allowed || !ctx->restr.out_cross || ctx->restr.ndomain == 0)
+            fail(HSAW_EINVAL, "encode: incomplete restriction");
+        p.domain = ctx->restr.domain;
+        p.ndomain = ctx->restr.ndomain;
+        p.allowed = ctx->restr.allowed;
+        p.out_cross = ctx->restr.out_cross;
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
+        auto go_r = [&](auto kernel) {
+            int blocks = persistent_blocks(ctx, kernel, nbatches);
+            StageScope timer(ctx, HSAW_STAGE_ENCODE);
+            kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+            check_launch(ctx, "encode_kernel(restricted)");
+        };
+#define HSAW_GO_R(H, W)                                                              \
+    (compact ? go_r(encode_kernel<H, W, 4, 0, true, kLayoutCompact, true>)           \
+             : go_r(encode_kernel<H, W, 4, 0, true, kLayoutFat, true>))
+        const bool br = cfg.heuristic == 0;
+        if (cfg.window == 2)
+            br ? HSAW_GO_R(0, 2) : HSAW_GO_R(2, 2);
+        else if (cfg.window == 0)
+            br ? HSAW_GO_R(0, 0) : HSAW_GO_R(2, 0);
+        else
+            br ? HSAW_GO_R(0, -1) : HSAW_GO_R(2, -1);
+#undef HSAW_GO_R
+        return;
+    }
 // one instantiation per graph layout
 #define HSAW_GO(H, W, B, R, S)                                                   \
     (compact ? go(encode_kernel<H, W, B, R, S, kLayoutCompact>)                  \
@@ -1118,7 +1162,8 @@ static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_
     if (nwalks == 0) return;
     DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, src_ref(ctx->g), ctx->g.thr, ctx->g.n,
                    nwalks,       d_seed,       d_len,      d_edge_off, d_nodes,    d_edges,
-                   d_status,     d_nnodes,     d_stats,    d_cursor,   nullptr,    nullptr};
+                   d_status,     d_nnodes,     d_stats,    d_cursor,   nullptr,    nullptr,
+                   ctx->restr.domain, ctx->restr.ndomain};
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
     auto go = [&](auto kernel) {
         int blocks = persistent_blocks(ctx, kernel, nwalks);

@@ -262,6 +262,17 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     if (slots > 0xFFFFFFF0ull) fail(HSAW_EINVAL, "stream: chunk too large for 32-bit walk ids");
     SamplerScratch& x = ctx->samp;  // chunk scratch is shared by all streams of the context
 
+    // a restricted stream (partitioned sampling) hands its start domain / allowed mask to the
+    // sampler launches of this chunk through the context
+    struct RestrictGuard {
+        hsaw_gpu_ctx* c;
+        ~RestrictGuard() { c->restr = Restriction{}; }
+    } guard{ctx};
+    if (s->r_ndomain) {
+        s->r_cross.ensure_scratch(nb);
+        ctx->restr = Restriction{s->r_domain.p, s->r_ndomain, s->r_allowed.p, s->r_cross.p};
+    }
+
     // ---- K1
     x.slot_seed.ensure_scratch(slots + 1);
     x.slot_len.ensure_scratch(slots + 1);
@@ -270,6 +281,14 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     HSAW_CUDA_CHECK(cudaMemsetAsync(x.count.p + nb, 0, 4, st));
     launch_encode(ctx, s->cfg, s->seed + first_batch, nb, x.slot_seed.p, x.slot_len.p,
                   x.count.p, s->stats.p, s->stats.p + 8, nullptr, s->collect_stats);
+    if (s->r_ndomain) {  // crossings per batch -> cumulative, like crossed_after (partition.cpp:239-243)
+        std::vector<uint32_t> cross(nb);
+        HSAW_CUDA_CHECK(
+            cudaMemcpyAsync(cross.data(), s->r_cross.p, nb * 4, cudaMemcpyDeviceToHost, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        uint64_t run = s->crossed_after_batch.empty() ? 0 : s->crossed_after_batch.back();
+        for (uint64_t b = 0; b < nb; ++b) s->crossed_after_batch.push_back(run += cross[b]);
+    }
     exclusive_sum_u32(ctx, x.count.p, x.first.p, nb + 1);
     const uint64_t E = read_u32(ctx, x.first.p + nb);  // encoded (heuristically accepted) walks
 
@@ -566,7 +585,7 @@ void sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches) {
         const double per_attempt = s->pairs_per_attempt > 0 ? s->pairs_per_attempt : 24.0;
         const uint64_t arena_batches = (uint64_t)((double)(kArenaTargetBytes / 8) / (per_attempt * 1.5 * (double)bs));
         nb = std::min(nb, std::max<uint64_t>(arena_batches, 1ull << 14));
-        if (fused_enabled() && record_supported(s->cfg))
+        if (fused_enabled() && record_supported(s->cfg) && s->r_ndomain == 0)
             sample_chunk_fused(s, first_batch + done, nb);
         else
             sample_chunk(s, first_batch + done, nb);
@@ -805,6 +824,38 @@ int hsaw_gpu_stream_keep(hsaw_gpu_stream* s, int keep_nodes, int keep_edges) {
         if (!keep_nodes && !keep_edges) fail(HSAW_EINVAL, "stream_keep: nothing to keep");
         s->keep_nodes = keep_nodes != 0;
         s->keep_edges = keep_edges != 0;
+    });
+}
+
+int hsaw_gpu_stream_restrict(hsaw_gpu_stream* s, const uint32_t* domain, uint64_t ndomain,
+                             const uint8_t* allowed) {
+    if (!s) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        if (s->local_batches) fail(HSAW_EINVAL, "stream_restrict: must be called before sampling");
+        if (!domain || !allowed || ndomain == 0 || ndomain > 0xFFFFFFFFull)
+            fail(HSAW_EINVAL, "stream_restrict: empty start domain or null mask");
+        const uint32_t n = s->ctx->g.n;
+        for (uint64_t i = 0; i < ndomain; ++i)
+            if (domain[i] >= n) fail(HSAW_EDATA, "stream_restrict: start node out of range");
+        s->r_domain.ensure_scratch(ndomain);
+        s->r_allowed.ensure_scratch(n);
+        cudaStream_t st = s->ctx->stream;
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(s->r_domain.p, domain, ndomain * 4, cudaMemcpyHostToDevice, st));
+        HSAW_CUDA_CHECK(cudaMemcpyAsync(s->r_allowed.p, allowed, n, cudaMemcpyHostToDevice, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        s->r_ndomain = (uint32_t)ndomain;
+    });
+}
+
+int hsaw_gpu_stream_crossings(const hsaw_gpu_stream* s, uint64_t min_accepted, uint64_t* crossings) {
+    if (!s || !crossings) return HSAW_EINVAL;
+    return guarded(s->ctx, [&] {
+        *crossings = 0;
+        if (min_accepted == 0 || s->r_ndomain == 0) return;
+        uint64_t idx = 0, val = 0;
+        local_cut(s, min_accepted, &idx, &val);
+        if (idx >= s->local_batches) fail(HSAW_ERANGE, "sample stream target not materialized");
+        *crossings = s->crossed_after_batch[idx];
     });
 }
 

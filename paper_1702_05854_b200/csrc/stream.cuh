@@ -3,6 +3,8 @@
 // counters_for needs.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 struct hsaw_gpu_stream {
@@ -29,6 +31,14 @@ struct hsaw_gpu_stream {
     uint64_t next_batch = 0;   // next global batch for ensure()
     uint64_t last_batch_end = 0;  // ranges must be increasing
     uint64_t grow = 4096;      // first-round size while nothing has been accepted yet
+
+    // Partitioned sampling (hsaw_gpu_stream_restrict; proj/src/partition.cpp:183-268): start domain,
+    // allowed mask, and the cumulative crossing count after each batch (host side, like the
+    // reference's crossed_after vector)
+    hsawgpu::DevVec<uint32_t> r_domain, r_cross;
+    hsawgpu::DevVec<uint8_t> r_allowed;
+    uint32_t r_ndomain = 0;
+    std::vector<uint64_t> crossed_after_batch;
 
     hsawgpu::DevVec<uint64_t> stats;  // u64[8] + cursor scratch
     uint64_t dropped = 0;             // walks removed by the exact recheck

@@ -395,6 +395,53 @@ int hsawh_estimate_suspension(const void* dg, const void* g, const double* p_of,
     });
 }
 
+int hsawh_partition(const void* g, uint32_t p, int method, uint64_t seed, const char* part_file,
+                    uint32_t hops, uint32_t* assign_out, uint8_t* extended_out) {
+    return guarded([&] {
+        const ProbGraph& gr = G(g);
+        Partitioning part = extend_partition(
+            gr, partition_graph(gr, p, static_cast<PartitionMethod>(method), seed,
+                                part_file ? part_file : ""), hops);
+        if (assign_out) std::memcpy(assign_out, part.assign.data(), 4 * part.assign.size());
+        if (extended_out)
+            for (std::uint32_t i = 0; i < part.p; ++i)
+                std::memcpy(extended_out + static_cast<std::size_t>(i) * gr.n,
+                            part.extended[i].data(), gr.n);
+    });
+}
+
+int hsawh_distributed_sample(const void* dg, uint32_t n, uint32_t p, uint32_t hops,
+                             const uint32_t* assign, const uint8_t* extended,
+                             uint64_t total_target, uint64_t seed, uint32_t batch_size,
+                             uint64_t max_attempts, void** pool_out, uint64_t* crossings,
+                             uint64_t* attempts, double* crossing_fraction, uint64_t* targets) {
+    return guarded([&] {
+        Partitioning part;
+        part.p = p;
+        part.hops = hops;
+        part.assign.assign(assign, assign + n);
+        part.base.assign(p, {});
+        for (NodeId v = 0; v < n; ++v) {
+            if (assign[v] >= p) throw DataError("part id out of range");
+            part.base[assign[v]].push_back(v);
+        }
+        part.extended.resize(p);
+        for (std::uint32_t i = 0; i < p; ++i)
+            part.extended[i].assign(extended + static_cast<std::size_t>(i) * n,
+                                    extended + static_cast<std::size_t>(i + 1) * n);
+        SamplerConfig cfg;
+        cfg.batch_size = batch_size;
+        cfg.max_attempts = max_attempts;
+        DistributedResult r = distributed_sample(*static_cast<const DeviceGraph*>(dg), part,
+                                                 total_target, seed, cfg);
+        *pool_out = new SamplePool(std::move(r.pool));
+        *crossings = r.crossings;
+        *attempts = r.attempts;
+        *crossing_fraction = r.crossing_fraction;
+        for (std::uint32_t i = 0; i < p; ++i) targets[i] = r.targets[i];
+    });
+}
+
 void hsawh_json_number(double x, char* out, uint64_t cap) {
     const std::string s = json_number(x);
     std::strncpy(out, s.c_str(), cap - 1);

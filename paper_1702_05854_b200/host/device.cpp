@@ -507,6 +507,17 @@ void SampleStream::ensure(std::uint64_t min_accepted) {
     raise(hsaw_gpu_stream_ensure(s_, min_accepted), dg_.ctx(), "ensure");
 }
 
+void SampleStream::restrict(std::span<const NodeId> start_domain, const std::uint8_t* allowed) {
+    raise(hsaw_gpu_stream_restrict(s_, start_domain.data(), start_domain.size(), allowed), dg_.ctx(),
+          "restrict");
+}
+
+std::uint64_t SampleStream::crossings_for(std::uint64_t min_accepted) const {
+    std::uint64_t c = 0;
+    raise(hsaw_gpu_stream_crossings(s_, min_accepted, &c), dg_.ctx(), "crossings_for");
+    return c;
+}
+
 std::uint64_t SampleStream::materialized() const {
     std::uint64_t acc = 0;
     raise(hsaw_gpu_stream_size(s_, &acc, nullptr, nullptr), dg_.ctx(), "stream_size");

@@ -302,6 +302,10 @@ public:
     Counters counters_for(std::uint64_t min_accepted) const;
     SamplePool to_pool(std::uint64_t min_accepted) const;
 
+    // Partitioned sampling: start domain + allowed mask (before sampling), and the crossings of
+    // the minimal batch prefix reaching min_accepted.
+    void restrict(std::span<const NodeId> start_domain, const std::uint8_t* allowed);
+    std::uint64_t crossings_for(std::uint64_t min_accepted) const;
     std::uint64_t materialized() const;
     hsaw_gpu_stream* handle() const { return s_; }
     const DeviceGraph& device() const { return dg_; }
@@ -320,6 +324,42 @@ SamplePool stream_samples(const ProbGraph& g, const SuspectSet& vi, std::uint32_
                           const SamplerConfig& cfg = {});
 double estimate_influence(const SamplePool& pool, NodeId n);
 void dump_walks(const SamplePool& pool, std::ostream& out);
+
+// ---- partitioned sampling (proj/include/hsaw/partition.hpp) ---------------------------------------
+// Node partition plus, per part, the h-hop in-neighbourhood closure walks may enter; a walk that
+// steps outside it is aborted and counted as a crossing.
+struct Partitioning {
+    std::uint32_t p = 1;
+    std::uint32_t hops = 0;
+    std::vector<std::uint32_t> assign;                 // node -> part
+    std::vector<std::vector<NodeId>> base;             // part -> owned nodes, ascending
+    std::vector<std::vector<std::uint8_t>> extended;   // part -> byte mask over nodes
+    std::size_t extended_size(std::uint32_t part) const;
+};
+enum class PartitionMethod { Hash, LabelProp, ExternalFile };
+Partitioning partition_graph(const ProbGraph& g, std::uint32_t p, PartitionMethod method,
+                             std::uint64_t seed, const std::string& part_file = "");
+Partitioning extend_partition(const ProbGraph& g, Partitioning part, std::uint32_t h);
+void save_partition(const Partitioning& part, const std::string& path);
+
+struct DistributedResult {
+    SamplePool pool;
+    std::uint64_t crossings = 0;
+    std::uint64_t attempts = 0;
+    double crossing_fraction = 0;
+    std::vector<std::uint64_t> targets;  // per-part quotas
+};
+// distributed_sample (proj/src/partition.cpp:153-279) with every part's restricted batches run on
+// the device: quotas by largest remainder, part i samples worker ids seed + i * 2^40 + b with
+// starts in base[i] and the extended[i] mask, cut at the minimal batch prefix reaching its quota.
+// `workers` is accepted and ignored. Results equal the reference's for every worker count.
+DistributedResult distributed_sample(const DeviceGraph& dg, const Partitioning& part,
+                                     std::uint64_t total_target, std::uint64_t seed = 0,
+                                     const SamplerConfig& cfg = {});
+DistributedResult distributed_sample(const ProbGraph& g, const SuspectSet& vi,
+                                     const Partitioning& part, std::uint64_t total_target,
+                                     std::uint64_t seed = 0, std::uint32_t workers = 1,
+                                     const SamplerConfig& cfg = {});
 
 // ---- coverage (proj/include/hsaw/coverage.hpp) --------------------------------------------------
 // Device-resident coverage index: a range of a SampleStream (edge ids or nodes of each walk) or a

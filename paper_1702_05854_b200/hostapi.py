@@ -93,6 +93,12 @@ def lib() -> C.CDLL:
     L.hsawh_pool_free.argtypes = [vp]
     L.hsawh_pool_free.restype = None
     L.hsawh_run_cli.argtypes = [C.c_int, C.POINTER(C.c_char_p)]
+    u8p = C.POINTER(C.c_uint8)
+    L.hsawh_partition.argtypes = [vp, C.c_uint32, C.c_int, C.c_uint64, C.c_char_p, C.c_uint32, u32p,
+                                  u8p]
+    L.hsawh_distributed_sample.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint32, u32p, u8p,
+                                           C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, vpp,
+                                           u64p, u64p, f64p, u64p]
     L.hsawh_json_number.argtypes = [C.c_double, C.c_char_p, C.c_uint64]
     L.hsawh_json_number.restype = None
     _LIB = L
@@ -390,6 +396,55 @@ def estimate_suspension(graph: Graph, p_of, kind, ids, eps, delta, state,
                                          kind, _p(buf, u32p), a.size, eps, delta, C.byref(s),
                                          C.byref(v), C.byref(cp), C.byref(runs)))
     return dict(value=v.value, capped=bool(cp.value), runs=int(runs.value), state=s.value)
+
+
+PART_METHODS = {"hash": 0, "labelprop": 1, "external": 2}
+
+
+def partition(graph: Graph, p, method="hash", seed=0, part_file=None, hops=0):
+    """hsaw::partition_graph + extend_partition(hops) -> (assign u32[n], extended u8[p, n])."""
+    assign = np.zeros(max(graph.n, 1), dtype=np.uint32)
+    ext = np.zeros((p, graph.n), dtype=np.uint8)
+    _chk(lib().hsawh_partition(graph.h, p, PART_METHODS[method], seed,
+                               str(part_file).encode() if part_file else None, hops,
+                               _p(assign, u32p), ext.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return assign[: graph.n], ext
+
+
+def distributed_sample(dg: "DeviceGraph", assign, extended, total_target, seed=0, hops=0,
+                       batch_size=10, max_attempts=100_000_000) -> dict:
+    """hsaw::distributed_sample(dg, part, total_target, seed, cfg) -> dict(pool, crossings,
+    attempts, crossing_fraction, targets)."""
+    a = np.ascontiguousarray(assign, dtype=np.uint32)
+    e = np.ascontiguousarray(extended, dtype=np.uint8)
+    p = e.shape[0]
+    h, cr, at, fr = C.c_void_p(), C.c_uint64(), C.c_uint64(), C.c_double()
+    tg = np.zeros(p, dtype=np.uint64)
+    _chk(lib().hsawh_distributed_sample(dg.h, a.size, p, hops, _p(a, u32p),
+                                        e.ctypes.data_as(C.POINTER(C.c_uint8)), total_target, seed,
+                                        batch_size, max_attempts, C.byref(h), C.byref(cr),
+                                        C.byref(at), C.byref(fr), _p(tg, u64p)))
+    try:
+        pool = _pool_from_handle(h)
+    finally:
+        lib().hsawh_pool_free(h)
+    return dict(pool=pool, crossings=cr.value, attempts=at.value, crossing_fraction=fr.value,
+                targets=[int(x) for x in tg])
+
+
+def _pool_from_handle(h):
+    from .capi import Pool
+    ns, at, te = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    lib().hsawh_pool_stats(h, C.byref(ns), C.byref(at), C.byref(te))
+    ns, at, te = ns.value, at.value, te.value
+    eo = np.zeros(ns + 1, dtype=np.uint64)
+    nodes = np.zeros(max(te + ns, 1), dtype=np.uint32)
+    edges = np.zeros(max(te, 1), dtype=np.uint32)
+    tw = np.zeros(max(ns, 1), dtype=np.uint64)
+    ts = np.zeros(max(ns, 1), dtype=np.uint32)
+    lib().hsawh_pool_copy(h, _p(eo, u64p), _p(nodes, u32p), _p(edges, u32p), _p(tw, u64p),
+                          _p(ts, u32p))
+    return Pool(at, eo, nodes[: te + ns], edges[:te], tw[:ns], ts[:ns])
 
 
 def stream_samples(graph: Graph, p_of, target, seed=0, batch_size=10, max_attempts=100_000_000):

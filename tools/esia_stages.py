@@ -18,7 +18,9 @@ p_of = hostapi.random_suspects_n(sh["n"], max(1, sh["n"] // 100), bench.SUSPECT_
 dg = hostapi.DeviceGraph.from_rmat(sh["n"], sh["raw"], bench.GEN_SEED, p_of)
 g = dg.graph
 ctx = capi.Context.borrow(dg.ctx_handle(), g.n, g.m)
-for rep in range(2):
+import os
+REPS = int(os.environ.get("REPS", "2"))
+for rep in range(REPS):
     ctx.stage_times(reset=True)
     t0 = time.perf_counter()
     r = hostapi.interdict(g, p_of, 0, k, 0.1, 1.0 / g.n, seed=42, max_attempts=10**15, dg=dg,
@@ -32,6 +34,9 @@ for rep in range(2):
                       "stage_launches": {n_: v[1] for n_, v in st.items() if v[1]}}), flush=True)
 
 # touch concentration of the 32-byte edge records (one record is read per walk step)
+if os.environ.get("NO_TOUCH"):
+    dg.close()
+    sys.exit(0)
 with ctx.stream(seed=42, cfg=capi.SamplerCfg(max_attempts=10**15)) as s:
     s.keep(nodes=False, edges=True)
     s.ensure(1_000_000)
