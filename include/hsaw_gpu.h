@@ -361,6 +361,19 @@ int hsaw_gpu_estimate_suspension(hsaw_gpu_ctx* ctx, int kind, const uint32_t* re
                                  uint64_t nids, double epsilon, double delta, uint64_t* prg_state,
                                  double* value, int* capped, uint64_t* runs);
 
+/* Reverse-reachable node sets of the InfMax baselines (rr_node_sets, proj/src/evaluation.cpp:169-191,
+ * used by baseline(), :356-376): `count` sets drawn from the caller's sequential xorshift64* stream
+ * — a uniform start node, then live in-edge picks until "no edge" or a pick lands on a node already
+ * in the set; 1 + |set| draws each. Bit-exact with the reference's stream: the device evaluates the
+ * set that would start at every stream position of a window and the chain of real starts is
+ * followed through it. *prg_state is advanced past the last set. The sets come
+ * back as a device walk set over node ids (limit = n), ready for hsaw_gpu_greedy /
+ * hsaw_gpu_coverage_of; hsaw_gpu_walkset_export copies any walk set out (set_off u64[nsets + 1],
+ * items; both nullable). */
+int hsaw_gpu_rr_node_sets(hsaw_gpu_ctx* ctx, uint64_t* prg_state, uint32_t count,
+                          hsaw_gpu_walkset** out, uint64_t* total_nodes);
+int hsaw_gpu_walkset_export(const hsaw_gpu_walkset* walkset, uint64_t* set_off, uint32_t* items);
+
 /* ---- instrumentation ------------------------------------------------------------------------ */
 
 /* Number of kernel launches this context has issued since creation (bench.py "gpu_launches"). */

@@ -139,6 +139,17 @@ int hsawh_distributed_sample(const void* dg, uint32_t n, uint32_t p, uint32_t ho
                              uint64_t max_attempts, void** pool_out, uint64_t* crossings,
                              uint64_t* attempts, double* crossing_fraction, uint64_t* targets);
 
+/* ---- ranking baselines — proj/include/hsaw/evaluation.hpp:45-50 ---- */
+/* baseline(): kind 0 Pagerank, 1 MaxDegree, 2 Randomized, 3 InfMaxV, 4 InfMaxVI; mode 0 edge,
+ * 1 node; ids_out holds k ids; *state is the caller's PrgState, advanced as the reference does.
+ * dg may be NULL (a DeviceGraph is then created for the InfMax kinds). */
+int hsawh_baseline(const void* dg, const void* g, const double* p_of, int kind, int mode,
+                   uint32_t k, uint64_t* state, uint32_t infmax_samples, uint32_t* ids_out);
+/* rr_node_sets on the device: set_off u64[count + 1]; *total = nodes of all sets (items are only
+ * written while they fit items_cap: call again with a larger buffer if *total > items_cap). */
+int hsawh_rr_node_sets(const void* dg, uint64_t* state, uint32_t count, uint64_t* set_off,
+                       uint32_t* items, uint64_t items_cap, uint64_t* total);
+
 /* A double as the result JSON prints it (nlohmann::json::dump's number layout,
  * proj/src/interdiction.cpp:89-104). */
 void hsawh_json_number(double x, char* out, uint64_t cap);

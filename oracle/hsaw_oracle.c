@@ -530,6 +530,7 @@ void orc_pool_free(orc_pool* p) {
     free(p->tag_worker);
     free(p->tag_seq);
     free(p->accepted_after_batch);
+    free(p->crossed_after_batch);
     free(p);
 }
 
@@ -993,6 +994,33 @@ uint32_t orc_lt_forward_simulate(const orc_graph* g, uint64_t* state) {
     uint32_t r = sim_count(g, &c, 0);
     sim_free(&c);
     return r;
+}
+
+/* rr_node_sets, evaluation.cpp:169-191 */
+int orc_rr_node_sets(const orc_graph* g, uint64_t* state, uint32_t count, uint64_t* set_off,
+                     uint32_t* items, uint64_t items_cap) {
+    uint32_t* mark = calloc(g->n ? g->n : 1, 4);
+    uint64_t at = 0;
+    int rc = 0;
+    set_off[0] = 0;
+    for (uint32_t i = 1; i <= count && !rc; ++i) {
+        uint32_t v = orc_pick_uniform_node(state, g->n);
+        if (at >= items_cap) { rc = 5; break; }
+        items[at++] = v;
+        mark[v] = i;
+        for (;;) {
+            uint32_t u = 0, e = 0;
+            if (!orc_pick_live_in_edge(state, g, v, &u, &e)) break;
+            if (mark[u] == i) break;
+            v = u;
+            if (at >= items_cap) { rc = 5; break; }
+            items[at++] = v;
+            mark[v] = i;
+        }
+        set_off[i] = at;
+    }
+    free(mark);
+    return rc;
 }
 
 static int removal_valid(const orc_graph* g, int kind, const uint32_t* ids, uint64_t nids) {

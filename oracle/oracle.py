@@ -219,6 +219,35 @@ def extend_partition_np(csr: "Csr", part: Partitioning, h: int) -> Partitioning:
     return Partitioning(part.p, h, part.assign, part.base, ext)
 
 
+def ranked_by_score(score) -> list:
+    """ranked_by_score, evaluation.cpp:110-119: score descending, ties by ascending id."""
+    score = np.asarray(score, dtype=np.float64)
+    return [int(x) for x in np.lexsort((np.arange(score.size), -score))]
+
+
+def edges_into_nodes(off, weight, nodes, k) -> list:
+    """edges_into_nodes, evaluation.cpp:121-151: the k heaviest in-edges of the ranked nodes,
+    taken round-robin (per node: weight descending, ties by edge id)."""
+    per_node = []
+    for v in nodes:
+        lo, hi = int(off[v]), int(off[v + 1])
+        ids = np.arange(lo, hi)
+        per_node.append([int(e) for e in ids[np.lexsort((ids, -np.asarray(weight[lo:hi])))]])
+    out, nxt = [], [0] * len(nodes)
+    while len(out) < k:
+        advanced = False
+        for i in range(len(nodes)):
+            if len(out) >= k:
+                break
+            if nxt[i] < len(per_node[i]):
+                out.append(per_node[i][nxt[i]])
+                nxt[i] += 1
+                advanced = True
+        if not advanced:
+            raise BuildError("not enough incoming edges among ranked nodes")
+    return out
+
+
 def part_quotas(total_target: int, sizes: list, n: int) -> list:
     """Largest-remainder quotas proportional to |part|, proj/src/partition.cpp:163-181."""
     targets, rema, assigned = [], [], 0
@@ -312,6 +341,8 @@ class Port:
                                          C.POINTER(_OrcCfg), C.POINTER(C.c_void_p)]
         L.orc_part_sample.argtypes = [C.POINTER(_OrcGraph), C.c_uint64, C.c_uint64,
                                       C.POINTER(_OrcCfg), C.POINTER(C.c_void_p), u64p, u64p]
+        L.orc_rr_node_sets.argtypes = [C.POINTER(_OrcGraph), u64p, C.c_uint32, u64p, u32p,
+                                       C.c_uint64]
         L.orc_pool_stats.argtypes = [C.c_void_p, u64p, u64p, u64p]
         L.orc_pool_copy.argtypes = [C.c_void_p, u64p, u32p, u32p, u64p, u32p]
         L.orc_pool_free.argtypes = [C.c_void_p]
@@ -367,6 +398,86 @@ class Port:
         return _OrcGraph(csr.n, csr.m, _p(csr.in_offsets, u64p), _p(csr.in_src, u32p),
                          _p(csr.in_cum, f64p), _p(csr.p_of, f64p), _p(domain, u32p), domain.size,
                          allowed.ctypes.data_as(C.POINTER(C.c_uint8)))
+
+    # -- ranking baselines (proj/src/evaluation.cpp:110-191,310-395)
+    def rr_node_sets(self, csr, state, count):
+        """-> (set_off u64[count + 1], items, state_after)"""
+        g = self._g(csr)
+        s = C.c_uint64(state)
+        off = np.zeros(count + 1, dtype=np.uint64)
+        cap = max(4096, count * 64)
+        while True:
+            items = np.zeros(cap, dtype=np.uint32)
+            s = C.c_uint64(state)
+            rc = self.L.orc_rr_node_sets(C.byref(g), C.byref(s), count, _p(off, u64p),
+                                         _p(items, u32p), cap)
+            if rc == 0:
+                return off, items[: int(off[-1])].copy(), s.value
+            cap *= 4
+
+    def baseline(self, csr, weight, kind, mode, k, state, infmax_samples=100000):
+        """baseline(), evaluation.cpp:330-395 -> (ids, state_after). kind: 'pagerank', 'maxdegree',
+        'randomized', 'infmax-v', 'infmax-vi'; mode 0 edge / 1 node; weight = ProbGraph::weight."""
+        n, m = csr.n, csr.m
+        off = csr.in_offsets.astype(np.int64)
+        if kind == "randomized":  # distinct_uniform, :153-165
+            limit, seen, out, s = (m if mode == 0 else n), set(), [], state
+            if k > limit:
+                raise BuildError("k exceeds candidate count")
+            while len(out) < k:
+                s, o = self.prg_next(s)
+                x = int(self.u01(o) * limit)
+                x = min(x, limit - 1)
+                if x not in seen:
+                    seen.add(x)
+                    out.append(x)
+            return out, s
+        in_deg = np.diff(off)
+        out_deg = np.bincount(csr.in_src, minlength=n).astype(np.int64)
+        dst = np.repeat(np.arange(n, dtype=np.int64), in_deg)
+        if kind == "pagerank":  # pagerank_scores, :310-328 (sequential accumulation order)
+            pr = np.full(n, 1.0 / n)
+            for _ in range(200):
+                dangling = 0.0
+                for v in np.nonzero(out_deg == 0)[0]:
+                    dangling += pr[v]
+                base = (1.0 - 0.85) / n + 0.85 * dangling / n
+                nxt = np.full(n, base)
+                contrib = 0.85 * pr[csr.in_src] / out_deg[csr.in_src]
+                for e in range(m):
+                    nxt[dst[e]] += contrib[e]
+                diff = 0.0
+                for v in range(n):
+                    diff += abs(nxt[v] - pr[v])
+                pr = nxt
+                if diff < 1e-10:
+                    break
+            ranked = ranked_by_score(pr)
+        elif kind == "maxdegree":
+            ranked = ranked_by_score((out_deg + in_deg).astype(np.float64))
+        else:
+            so, items, state = self.rr_node_sets(csr, state, infmax_samples)
+            if kind == "infmax-vi":
+                cand = np.nonzero(csr.p_of > 0)[0].astype(np.uint32)
+                if cand.size == 0:
+                    raise BuildError("suspect set is empty")
+                ncand = cand.size
+            else:
+                cand, ncand = None, n
+            budget = min(ncand, max(k, 64) if mode == 0 else k)
+            sol, _ = self.greedy(n, so, items, budget, cand=cand, kind=1)
+            ranked = [int(x) for x in sol]
+        ranked = [int(x) for x in ranked]
+        if mode == 1:
+            if k > len(ranked):
+                raise BuildError("k exceeds candidate count")
+            return ranked[:k], state
+        if k > m:
+            raise BuildError("k exceeds edge count")
+        listed = np.zeros(n, dtype=bool)
+        listed[ranked] = True
+        ranked += [int(v) for v in np.nonzero(~listed)[0]]
+        return edges_into_nodes(off, weight, ranked, k), state
 
     # -- partitioned sampling (proj/src/partition.cpp:153-279)
     def distributed_sample(self, csr, part: "Partitioning", total_target, seed=0, heuristic=0,
@@ -577,6 +688,8 @@ class Ref:
         L.ref_splitmix_next.argtypes = [C.c_uint64, u64p, u64p]
         L.ref_graph_from_csr.restype = C.c_void_p
         L.ref_graph_from_csr.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p]
+        L.ref_baseline.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_uint32, u64p,
+                                   C.c_uint32, u32p]
         L.ref_partition_graph.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_uint64, u32p,
                                           C.POINTER(C.c_void_p)]
         L.ref_extend_partition.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32,
@@ -770,6 +883,23 @@ class Ref:
 
     def handles(self, csr: Csr, lean=False):
         return Ref._Handles(self, csr, lean)
+
+    BASELINES = {"pagerank": 0, "maxdegree": 1, "randomized": 2, "infmax-v": 3, "infmax-vi": 4}
+
+    def baseline(self, csr, kind, mode, k, state, infmax_samples=100000, hd=None):
+        """baseline() by the reference -> (ids, state_after)."""
+        ids = np.zeros(max(k, 1), dtype=np.uint32)
+
+        def run(h):
+            s = C.c_uint64(state)
+            self._chk(self.L.ref_baseline(h.g, h.vi, self.BASELINES[kind], mode, k, C.byref(s),
+                                          infmax_samples, _p(ids, u32p)), "baseline")
+            return [int(x) for x in ids[:k]], s.value
+
+        if hd is not None:
+            return run(hd)
+        with self.handles(csr) as h:
+            return run(h)
 
     # -- partitioned sampling (proj/include/hsaw/partition.hpp)
     def partition(self, csr, p, method="hash", seed=0, assign=None, hops=0, hd=None) -> "Partitioning":

@@ -355,6 +355,22 @@ void ref_pool_copy(void* pp, std::uint64_t* edge_off, std::uint32_t* nodes,
 
 void ref_pool_free(void* p) { delete static_cast<Pool*>(p); }
 
+// ---- ranking baselines (proj/include/hsaw/evaluation.hpp:45-50) ---------------
+// kind: 0 Pagerank, 1 MaxDegree, 2 Randomized, 3 InfMaxV, 4 InfMaxVI; ids_out holds k ids
+int ref_baseline(void* gp, void* vip, int kind, int mode, std::uint32_t k,
+                 std::uint64_t* state, std::uint32_t infmax_samples,
+                 std::uint32_t* ids_out) {
+    return guarded([&] {
+        PrgState s{*state};
+        RemovalSet r = baseline(*static_cast<ProbGraph*>(gp), *static_cast<SuspectSet*>(vip),
+                                static_cast<BaselineKind>(kind),
+                                mode == 0 ? ItemKind::Edge : ItemKind::Node, k, s,
+                                infmax_samples);
+        *state = s.state;
+        std::memcpy(ids_out, r.ids.data(), 4 * r.ids.size());
+    });
+}
+
 // ---- partitioned sampling (proj/include/hsaw/partition.hpp) -------------------
 // method: 0 Hash, 1 LabelProp, 2 = the given assignment (what ExternalFile reads,
 // built without the file: assign + rebuild_base + extend_partition(.., 0)).

@@ -132,6 +132,8 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_rounds_end.argtypes = [vp]
     L.hsaw_gpu_rounds_end.restype = None
     L.hsaw_gpu_paired_runs.argtypes = [vp, C.c_int, u32p, C.c_uint64, u64p, C.c_uint64, u32p, u32p]
+    L.hsaw_gpu_rr_node_sets.argtypes = [vp, u64p, C.c_uint32, C.POINTER(vp), u64p]
+    L.hsaw_gpu_walkset_export.argtypes = [vp, u64p, u32p]
     L.hsaw_gpu_prg_jump.argtypes = [C.c_uint64, C.c_uint64]
     L.hsaw_gpu_prg_jump.restype = C.c_uint64
     L.hsaw_gpu_estimate_suspension.argtypes = [vp, C.c_int, u32p, C.c_uint64, C.c_double,
@@ -163,6 +165,7 @@ EXPORTS = (
     "hsaw_gpu_rmat_build", "hsaw_gpu_held_csr_fetch", "hsaw_gpu_held_csr_install",
     "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout", "hsaw_gpu_stream_keep",
     "hsaw_gpu_stream_restrict", "hsaw_gpu_stream_crossings",
+    "hsaw_gpu_rr_node_sets", "hsaw_gpu_walkset_export",
 )
 
 
@@ -459,6 +462,13 @@ class Context:
     def walkset(self, limit, set_off, items) -> "WalkSet":
         return WalkSet(self, limit, set_off, items)
 
+    def rr_node_sets(self, state: int, count: int):
+        """hsaw_gpu_rr_node_sets -> (WalkSet over node ids, state_after)."""
+        s, h, total = C.c_uint64(state), C.c_void_p(), C.c_uint64()
+        self._chk(self.L.hsaw_gpu_rr_node_sets(self.h, C.byref(s), count, C.byref(h),
+                                               C.byref(total)))
+        return WalkSet.adopt(self, h, count, total.value), s.value
+
     # ---- greedy / coverage
     def greedy(self, k, *, stream=None, walkset=None, kind=KIND_EDGE, off=0, cnt=None, cand=None):
         src = stream if stream is not None else walkset
@@ -617,6 +627,20 @@ class WalkSet:
         ctx._chk(self.L.hsaw_gpu_walkset_import(ctx.h, limit, self.count, _p(set_off, u64p),
                                                 _p(items, u32p) if items.size else None,
                                                 C.byref(self.h)))
+
+    @classmethod
+    def adopt(cls, ctx, handle, count, nitems) -> "WalkSet":
+        self = cls.__new__(cls)
+        self.ctx, self.L, self.h, self.count, self.nitems = ctx, ctx.L, handle, count, nitems
+        return self
+
+    def export(self):
+        """(set_off u64[count + 1], items) host copies."""
+        off = np.zeros(self.count + 1, dtype=np.uint64)
+        self.ctx._chk(self.L.hsaw_gpu_walkset_export(self.h, _p(off, u64p), None))
+        items = np.zeros(max(int(off[-1]), 1), dtype=np.uint32)
+        self.ctx._chk(self.L.hsaw_gpu_walkset_export(self.h, None, _p(items, u32p)))
+        return off, items[: int(off[-1])]
 
     def close(self):
         if self.h:

@@ -20,13 +20,6 @@
 
 using namespace hsawgpu;
 
-struct hsaw_gpu_walkset {
-    hsaw_gpu_ctx* ctx = nullptr;
-    uint32_t limit = 0;
-    uint64_t nsets = 0, nitems = 0;
-    DevVec<uint64_t> off;
-    DevVec<uint32_t> items;
-};
 
 namespace {
 struct WalkView;

@@ -47,3 +47,13 @@ struct hsaw_gpu_stream {
     double pairs_per_attempt = 0;     // fused path: running arena-volume estimate
 
 };
+
+// A fixed collection of item sets on the device (CoverageIndex input): the fixed-walk-set parity
+// mode (hsaw_gpu_walkset_import) and the reverse-reachable node sets of the InfMax baselines.
+struct hsaw_gpu_walkset {
+    hsaw_gpu_ctx* ctx = nullptr;
+    uint32_t limit = 0;
+    uint64_t nsets = 0, nitems = 0;
+    hsawgpu::DevVec<uint64_t> off;
+    hsawgpu::DevVec<uint32_t> items;
+};

@@ -442,6 +442,39 @@ int hsawh_distributed_sample(const void* dg, uint32_t n, uint32_t p, uint32_t ho
     });
 }
 
+int hsawh_baseline(const void* dg, const void* g, const double* p_of, int kind, int mode,
+                   uint32_t k, uint64_t* state, uint32_t infmax_samples, uint32_t* ids_out) {
+    return guarded([&] {
+        SuspectSet vi = dense_suspects(G(g), p_of);
+        PrgState s{*state};
+        const auto bk = static_cast<BaselineKind>(kind);
+        const ItemKind ik = mode == 0 ? ItemKind::Edge : ItemKind::Node;
+        RemovalSet r = dg ? baseline(*static_cast<const DeviceGraph*>(dg), G(g), vi, bk, ik, k, s,
+                                     infmax_samples)
+                          : baseline(G(g), vi, bk, ik, k, s, infmax_samples);
+        *state = s.state;
+        std::memcpy(ids_out, r.ids.data(), 4 * r.ids.size());
+    });
+}
+
+int hsawh_rr_node_sets(const void* dg, uint64_t* state, uint32_t count, uint64_t* set_off,
+                       uint32_t* items, uint64_t items_cap, uint64_t* total) {
+    return guarded([&] {
+        PrgState s{*state};
+        auto sets = rr_node_sets(*static_cast<const DeviceGraph*>(dg), s, count);
+        uint64_t at = 0;
+        set_off[0] = 0;
+        for (uint32_t i = 0; i < count; ++i) {
+            if (at + sets[i].size() <= items_cap)
+                std::memcpy(items + at, sets[i].data(), 4 * sets[i].size());
+            at += sets[i].size();
+            set_off[i + 1] = at;
+        }
+        *total = at;
+        *state = s.state;
+    });
+}
+
 void hsawh_json_number(double x, char* out, uint64_t cap) {
     const std::string s = json_number(x);
     std::strncpy(out, s.c_str(), cap - 1);

@@ -636,6 +636,12 @@ CoverageIndex::CoverageIndex(const DeviceGraph& dg,
           ctx_, "CoverageIndex");
 }
 
+CoverageIndex::CoverageIndex(const DeviceGraph& dg, hsaw_gpu_walkset* adopted, std::uint64_t nsets,
+                             const CandidateSet& cand, const ProbGraph& g)
+    : kind_(cand.kind), ctx_(dg.ctx()), walkset_(adopted), count_(nsets), cand_(cand.ids) {
+    ncand_ = count_candidates(cand, kind_ == ItemKind::Edge ? g.m : g.n);
+}
+
 CoverageIndex::~CoverageIndex() { hsaw_gpu_walkset_destroy(walkset_); }
 
 std::uint64_t CoverageIndex::coverage_upper_bound(std::uint32_t k) const {

@@ -370,6 +370,9 @@ public:
                   std::uint64_t count, const CandidateSet& cand, const ProbGraph& g);
     CoverageIndex(const DeviceGraph& dg, std::span<const std::vector<std::uint32_t>> item_sets,
                   const CandidateSet& cand, const ProbGraph& g);
+    // Takes over a device-resident walk set (e.g. the reverse-reachable sets of rr_node_sets).
+    CoverageIndex(const DeviceGraph& dg, hsaw_gpu_walkset* adopted, std::uint64_t nsets,
+                  const CandidateSet& cand, const ProbGraph& g);
     ~CoverageIndex();
     CoverageIndex(const CoverageIndex&) = delete;
     CoverageIndex& operator=(const CoverageIndex&) = delete;
@@ -490,6 +493,23 @@ struct PairedRuns {
 };
 PairedRuns paired_runs(const DeviceGraph& dg, const RemovalSet& removal, std::uint64_t runs,
                        PrgState& s);
+
+// ---- ranking baselines (proj/include/hsaw/evaluation.hpp:45-50) -----------------------------------
+enum class BaselineKind { Pagerank, MaxDegree, Randomized, InfMaxV, InfMaxVI };
+// Reverse-reachable node sets (rr_node_sets, proj/src/evaluation.cpp:169-191) drawn on the device
+// from the caller's sequential stream, bit-exact (hsaw_gpu_rr_node_sets); s is advanced.
+std::vector<std::vector<std::uint32_t>> rr_node_sets(const DeviceGraph& dg, PrgState& s,
+                                                     std::uint32_t count);
+std::vector<double> pagerank_scores(const ProbGraph& g, double damping = 0.85, double tol = 1e-10,
+                                    int max_iters = 200);
+// baseline() (evaluation.cpp:330-395). The InfMax kinds draw their sets and run greedy on the
+// device (the sets never visit the host); Pagerank / MaxDegree / Randomized are host rankings as
+// in the reference. Edge mode maps the ranked nodes to their heaviest in-edges round-robin.
+RemovalSet baseline(const DeviceGraph& dg, const ProbGraph& g, const SuspectSet& vi,
+                    BaselineKind kind, ItemKind mode, std::uint32_t k, PrgState& s,
+                    std::uint32_t infmax_samples = 100000);
+RemovalSet baseline(const ProbGraph& g, const SuspectSet& vi, BaselineKind kind, ItemKind mode,
+                    std::uint32_t k, PrgState& s, std::uint32_t infmax_samples = 100000);
 
 // ---- cli (proj/include/hsaw/cli.hpp) ------------------------------------------------------------
 int run_cli(std::vector<std::string> args);

@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
     L.hsawh_distributed_sample.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint32, u32p, u8p,
                                            C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, vpp,
                                            u64p, u64p, f64p, u64p]
+    L.hsawh_baseline.argtypes = [vp, vp, f64p, C.c_int, C.c_int, C.c_uint32, u64p, C.c_uint32, u32p]
+    L.hsawh_rr_node_sets.argtypes = [vp, u64p, C.c_uint32, u64p, u32p, C.c_uint64, u64p]
     L.hsawh_json_number.argtypes = [C.c_double, C.c_char_p, C.c_uint64]
     L.hsawh_json_number.restype = None
     _LIB = L
@@ -396,6 +398,34 @@ def estimate_suspension(graph: Graph, p_of, kind, ids, eps, delta, state,
                                          kind, _p(buf, u32p), a.size, eps, delta, C.byref(s),
                                          C.byref(v), C.byref(cp), C.byref(runs)))
     return dict(value=v.value, capped=bool(cp.value), runs=int(runs.value), state=s.value)
+
+
+BASELINES = {"pagerank": 0, "maxdegree": 1, "randomized": 2, "infmax-v": 3, "infmax-vi": 4}
+
+
+def baseline(graph: Graph, p_of, kind, mode, k, state, infmax_samples=100000,
+             dg: "DeviceGraph | None" = None):
+    """hsaw::baseline(...) -> (ids, state_after). mode 0 edge / 1 node."""
+    p = np.ascontiguousarray(p_of, dtype=np.float64)
+    ids = np.zeros(max(k, 1), dtype=np.uint32)
+    s = C.c_uint64(state)
+    _chk(lib().hsawh_baseline(dg.h if dg is not None else None, graph.h, _p(p, f64p),
+                              BASELINES[kind], mode, k, C.byref(s), infmax_samples, _p(ids, u32p)))
+    return [int(x) for x in ids[:k]], s.value
+
+
+def rr_node_sets(dg: "DeviceGraph", state, count):
+    """hsaw::rr_node_sets(dg, s, count) -> (set_off, items, state_after)."""
+    off = np.zeros(count + 1, dtype=np.uint64)
+    cap = max(4096, count * 64)
+    while True:
+        items = np.zeros(cap, dtype=np.uint32)
+        s, total = C.c_uint64(state), C.c_uint64()
+        _chk(lib().hsawh_rr_node_sets(dg.h, C.byref(s), count, _p(off, u64p), _p(items, u32p), cap,
+                                      C.byref(total)))
+        if total.value <= cap:
+            return off, items[: total.value].copy(), s.value
+        cap = total.value
 
 
 PART_METHODS = {"hash": 0, "labelprop": 1, "external": 2}
