@@ -192,4 +192,20 @@ RemovalSet baseline(const ProbGraph& g, const SuspectSet& vi, BaselineKind kind,
     return r;
 }
 
+SolutionAnalysis analyze_solution(const ProbGraph& g, const SuspectSet& vi,
+                                  const RemovalSet& removal) {
+    if (removal.kind != ItemKind::Node)
+        throw std::invalid_argument("analysis requires a node removal set");
+    if (removal.ids.empty()) throw std::invalid_argument("removal set is empty");
+    removal.validate(g);
+    SolutionAnalysis a;
+    std::size_t in_vi = 0;
+    for (std::uint32_t v : removal.ids) {
+        if (vi.is_suspect(v)) ++in_vi;
+        a.cost += (1.0 - vi.p_of[v]) * std::log(g.in_degree(v) + 1.0);
+    }
+    a.ssr = static_cast<double>(in_vi) / static_cast<double>(removal.ids.size());
+    return a;
+}
+
 }  // namespace hsaw

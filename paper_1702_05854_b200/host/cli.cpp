@@ -314,14 +314,147 @@ int cmd_bench(const Flags& f) {  // cli.cpp:350-379, one device run instead of 1
     return 0;
 }
 
+// nlohmann dump(2) of an integer array value at nesting depth 1
+template <class T>
+std::string json_int_array(const std::vector<T>& xs) {
+    if (xs.empty()) return "[]";
+    std::ostringstream o;
+    o << "[";
+    for (std::size_t i = 0; i < xs.size(); ++i) o << (i ? ",\n    " : "\n    ") << xs[i];
+    o << "\n  ]";
+    return o.str();
+}
+
+ItemKind parse_item_mode(const std::string& mode) {
+    if (mode == "edge") return ItemKind::Edge;
+    if (mode == "node") return ItemKind::Node;
+    throw UsageError("--mode: expected edge|node");
+}
+
+BaselineKind parse_baseline_kind(const std::string& name) {  // cli.cpp:187-195
+    if (name == "pagerank") return BaselineKind::Pagerank;
+    if (name == "maxdegree") return BaselineKind::MaxDegree;
+    if (name == "randomized") return BaselineKind::Randomized;
+    if (name == "infmax-v") return BaselineKind::InfMaxV;
+    if (name == "infmax-vi") return BaselineKind::InfMaxVI;
+    throw UsageError("--method: expected pagerank|maxdegree|randomized|infmax-v|infmax-vi");
+}
+
+int cmd_baseline(const Flags& f) {  // cli.cpp:197-265
+    f.require("graph");
+    const std::uint64_t seed = f.u64("seed", 0);
+    ProbGraph g = load_graph(f, seed);
+    SuspectSet vi = load_suspect_args(f, g, seed);
+    const ItemKind kind = parse_item_mode(f.str("mode", "edge"));
+    const double eps = f.real("epsilon", 0.1), delta = f.real("delta", 0.1);
+    DeviceGraph dg(g, vi, static_cast<int>(f.u64("device", 0)));
+    if (f.has("sweep")) {  // suspension curves: every baseline plus the interdiction algorithm
+        std::vector<std::uint32_t> ks;
+        std::stringstream ss(f.str("sweep"));
+        std::string tok;
+        while (std::getline(ss, tok, ',')) ks.push_back(static_cast<std::uint32_t>(std::stoul(tok)));
+        const std::pair<const char*, BaselineKind> methods[] = {
+            {"pagerank", BaselineKind::Pagerank},     {"maxdegree", BaselineKind::MaxDegree},
+            {"randomized", BaselineKind::Randomized}, {"infmax-v", BaselineKind::InfMaxV},
+            {"infmax-vi", BaselineKind::InfMaxVI}};
+        const std::string csv = f.str("csv").empty() ? "sweep.csv" : f.str("csv");
+        std::ofstream out(csv);
+        if (!out) throw DataError("cannot write csv");
+        out << "method,k,suspension\n";
+        for (std::uint32_t kk : ks) {
+            for (const auto& [name, bk] : methods) {
+                PrgState s = seed_from_worker(seed);
+                RemovalSet r = baseline(dg, g, vi, bk, kind, kk, s);
+                out << name << ',' << kk << ',' << estimate_suspension(dg, r, eps, delta, s).value
+                    << '\n';
+            }
+            InterdictionOptions opts;
+            opts.seed = seed;
+            const CandidateSet cand = CandidateSet::all(kind);
+            const InterdictionResult res = kind == ItemKind::Edge
+                                               ? esia(dg, g, cand, kk, eps, delta, opts)
+                                               : nsia(dg, g, cand, kk, eps, delta, opts);
+            RemovalSet r{kind, res.solution};
+            PrgState s = seed_from_worker(seed);
+            out << (kind == ItemKind::Edge ? "esia" : "nsia") << ',' << kk << ','
+                << estimate_suspension(dg, r, eps, delta, s).value << '\n';
+        }
+        return 0;
+    }
+    const std::string method = f.str("method", "pagerank");
+    const auto k = static_cast<std::uint32_t>(f.u64("k", 1));
+    PrgState s = seed_from_worker(seed);
+    RemovalSet r = baseline(dg, g, vi, parse_baseline_kind(method), kind, k, s);
+    const SuspensionEstimate est = estimate_suspension(dg, r, eps, delta, s);
+    std::ostringstream j;  // nlohmann object: keys sorted, dump(2)
+    j << "{\n";
+    if (kind == ItemKind::Node) {
+        const SolutionAnalysis a = analyze_solution(g, vi, r);
+        j << "  \"cost\": " << json_shortest(a.cost) << ",\n";
+    }
+    j << "  \"ids\": " << json_int_array(r.ids) << ",\n  \"k\": " << k << ",\n  \"kind\": \""
+      << to_string(kind) << "\",\n  \"method\": \"" << method << "\"";
+    if (kind == ItemKind::Node) j << ",\n  \"ssr\": " << json_shortest(analyze_solution(g, vi, r).ssr);
+    j << ",\n  \"suspension\": " << json_shortest(est.value) << "\n}";
+    emit(j.str(), f.str("output"));
+    return 0;
+}
+
+int cmd_partition(const Flags& f) {  // cli.cpp:292-335
+    f.require("graph");
+    f.require("parts");
+    const std::uint64_t seed = f.u64("seed", 0);
+    ProbGraph g = load_graph(f, seed);
+    const std::string method = f.str("method", "hash");
+    PartitionMethod pm;
+    if (method == "hash")
+        pm = PartitionMethod::Hash;
+    else if (method == "labelprop")
+        pm = PartitionMethod::LabelProp;
+    else if (method == "external")
+        pm = PartitionMethod::ExternalFile;
+    else
+        throw UsageError("--method: expected hash|labelprop|external");
+    const auto p = static_cast<std::uint32_t>(f.u64("parts", 1));
+    const auto hops = static_cast<std::uint32_t>(f.u64("hops", 0));
+    Partitioning part = extend_partition(g, partition_graph(g, p, pm, seed, f.str("part-file")), hops);
+    if (f.has("save")) save_partition(part, f.str("save"));
+    std::vector<std::uint64_t> sizes, ext_sizes;
+    for (std::uint32_t i = 0; i < part.p; ++i) {
+        sizes.push_back(part.base[i].size());
+        ext_sizes.push_back(part.extended_size(i));
+    }
+    const std::uint64_t target = f.u64("target", 0);
+    std::ostringstream j;
+    j << "{\n";
+    DistributedResult res;
+    if (target > 0) {
+        SuspectSet vi = load_suspect_args(f, g, seed);
+        DeviceGraph dg(g, vi, static_cast<int>(f.u64("device", 0)));
+        res = distributed_sample(dg, part, target, seed);
+        j << "  \"accepted\": " << res.pool.accepted() << ",\n  \"attempts\": " << res.attempts
+          << ",\n  \"crossing_fraction\": " << json_shortest(res.crossing_fraction)
+          << ",\n  \"crossings\": " << res.crossings << ",\n";
+    }
+    j << "  \"extended_sizes\": " << json_int_array(ext_sizes) << ",\n  \"hops\": " << hops
+      << ",\n  \"method\": \"" << method << "\",\n  \"part_sizes\": " << json_int_array(sizes)
+      << ",\n  \"parts\": " << p;
+    if (target > 0)
+        j << ",\n  \"per_part_targets\": " << json_int_array(res.targets) << ",\n  \"target\": "
+          << target;
+    j << "\n}";
+    emit(j.str(), f.str("output"));
+    return 0;
+}
+
 }  // namespace
 
 int run_cli(std::vector<std::string> args) {
     try {
-        if (args.empty()) throw UsageError("a subcommand is required: interdict|sample|estimate|synth|bench");
+        if (args.empty()) throw UsageError("a subcommand is required: interdict|sample|estimate|baseline|partition|synth|bench");
         const std::string& cmd = args[0];
         if (cmd == "--help" || cmd == "-h") {
-            std::cout << "usage: hsaw interdict|sample|estimate|synth|bench [--flags]\n";
+            std::cout << "usage: hsaw interdict|sample|estimate|baseline|partition|synth|bench [--flags]\n";
             return 0;
         }
         if (cmd == "interdict")
@@ -350,9 +483,18 @@ int run_cli(std::vector<std::string> args) {
                 args, 1,
                 with(kGraphFlags, {"mode", "removal", "epsilon", "delta", "seed", "output", "device"}),
                 {"symmetrize"}));
-        if (cmd == "baseline" || cmd == "partition")
-            throw UsageError("subcommand '" + cmd +
-                             "' is outside the device hot path (use the reference build)");
+        if (cmd == "baseline")
+            return cmd_baseline(parse_flags(
+                args, 1,
+                with(kGraphFlags, {"method", "mode", "k", "epsilon", "delta", "seed", "workers",
+                                   "sweep", "csv", "output", "device"}),
+                {"symmetrize"}));
+        if (cmd == "partition")
+            return cmd_partition(parse_flags(
+                args, 1,
+                with(kGraphFlags, {"parts", "method", "hops", "part-file", "target", "workers", "seed",
+                                   "save", "output", "device"}),
+                {"symmetrize"}));
         throw UsageError("unknown subcommand '" + cmd + "'");
     } catch (const UsageError& e) {
         std::cerr << "usage error: " << e.what() << '\n';

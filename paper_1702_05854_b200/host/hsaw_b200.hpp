@@ -510,6 +510,12 @@ RemovalSet baseline(const DeviceGraph& dg, const ProbGraph& g, const SuspectSet&
                     std::uint32_t infmax_samples = 100000);
 RemovalSet baseline(const ProbGraph& g, const SuspectSet& vi, BaselineKind kind, ItemKind mode,
                     std::uint32_t k, PrgState& s, std::uint32_t infmax_samples = 100000);
+struct SolutionAnalysis {
+    double ssr = 0;   // fraction of the solution drawn from the suspect set
+    double cost = 0;  // sum (1 - p(v)) ln(d_in(v) + 1)
+};
+SolutionAnalysis analyze_solution(const ProbGraph& g, const SuspectSet& vi,
+                                  const RemovalSet& removal);  // evaluation.cpp:397-412
 
 // ---- cli (proj/include/hsaw/cli.hpp) ------------------------------------------------------------
 int run_cli(std::vector<std::string> args);

@@ -70,3 +70,35 @@ def test_restricted_stream_other_configs(gpu_lib, port, pv, pcsr, window, heuris
                 assert np.array_equal(getattr(pool, f), getattr(exp.pool, f)), f
             with pytest.raises(gpu_lib.HsawError):
                 st.restrict(part.base[2], part.extended[2])  # too late
+
+
+def test_cli_partition_and_baseline(pdg, pv, pcsr, tmp_path):  # noqa: F811
+    """`hsaw partition --target` and `hsaw baseline` (proj/src/cli.cpp:197-265,292-335) through the
+    drop-in CLI: the numbers the library calls give, nlohmann key order."""
+    import json
+    hostapi, dg = pdg
+    g = hostapi.Graph.from_csr(pcsr.n, pcsr.m, pcsr.in_offsets, pcsr.in_src, pcsr.in_cum)
+    cache, sus, out = tmp_path / "g.hsaw1", tmp_path / "s.txt", tmp_path / "o.json"
+    g.save_cache(cache)
+    sus.write_text("".join(f"{v} {float(pcsr.p_of[v])!r}\n" for v in np.nonzero(pcsr.p_of)[0]))
+    rc = hostapi.run_cli(["partition", "--graph", str(cache), "--suspects", str(sus), "--parts", "4",
+                          "--hops", "1", "--target", "700", "--seed", "7", "--output", str(out)])
+    assert rc == 0
+    rep = json.loads(out.read_text())
+    key = "hash_h1"
+    assert [rep["crossings"], rep["attempts"]] == pv[f"{key}_scalars"].tolist()
+    assert rep["per_part_targets"] == pv[f"{key}_targets"].tolist() and rep["target"] == 700
+    assert rep["accepted"] == pv[f"{key}_pool_edge_off"].size - 1
+    assert rep["crossing_fraction"] == float(pv[f"{key}_fraction"][0])
+    assert list(rep) == sorted(rep)
+    rc = hostapi.run_cli(["baseline", "--graph", str(cache), "--suspects", str(sus), "--method",
+                          "infmax-vi", "--mode", "node", "--k", "5", "--seed", "3", "--output",
+                          str(out)])
+    assert rc == 0
+    rep = json.loads(out.read_text())
+    s = __import__("oracle.oracle", fromlist=["Port"]).Port().seed_from_worker(3)
+    ids, s_after = hostapi.baseline(g, pcsr.p_of, "infmax-vi", 1, 5, s, dg=dg)
+    assert rep["ids"] == ids and rep["k"] == 5 and rep["kind"] == "node" and rep["method"] == "infmax-vi"
+    est = hostapi.estimate_suspension(g, pcsr.p_of, 1, ids, 0.1, 0.1, s_after, dg=dg)
+    assert rep["suspension"] == est["value"] and 0.0 <= rep["ssr"] <= 1.0 and rep["cost"] >= 0.0
+    assert list(rep) == sorted(rep)

@@ -109,3 +109,24 @@ def test_host_partition_errors(host, pcsr, tmp_path):
     with pytest.raises(host.HsawError) as e:
         host.partition(g, 2, "external", part_file=bad)
     assert "part id 5 out of range" in str(e.value)
+
+
+def test_cli_partition_report(host, pv, pcsr, tmp_path):
+    """`hsaw partition` without --target needs no device (proj/src/cli.cpp:292-335): part sizes,
+    extended sizes and the saved part vector."""
+    import json
+    g = host.Graph.from_csr(pcsr.n, pcsr.m, pcsr.in_offsets, pcsr.in_src, pcsr.in_cum)
+    cache, out, saved = tmp_path / "g.hsaw1", tmp_path / "p.json", tmp_path / "parts.txt"
+    g.save_cache(cache)
+    rc = host.run_cli(["partition", "--graph", str(cache), "--parts", "4", "--method", "labelprop",
+                       "--hops", "1", "--seed", "5", "--save", str(saved), "--output", str(out)])
+    assert rc == 0
+    rep = json.loads(out.read_text())
+    gold = golden_part(pv, "labelprop_h1", pcsr.n)
+    assert rep["parts"] == 4 and rep["hops"] == 1 and rep["method"] == "labelprop"
+    assert rep["part_sizes"] == [int(b.size) for b in gold.base]
+    assert rep["extended_sizes"] == [int(m.sum()) for m in gold.extended]
+    assert list(rep) == sorted(rep)  # nlohmann object order
+    assert [int(x) for x in saved.read_text().split()] == gold.assign.tolist()
+    assert host.run_cli(["partition", "--graph", str(cache), "--parts", "0"]) == 2
+    assert host.run_cli(["partition", "--graph", str(cache), "--parts", "2", "--method", "x"]) == 1
