@@ -97,17 +97,21 @@ WeightMode weight_mode(const std::string& w) {
 }
 
 // GraphArgs::load, cli.cpp:38-48: binary caches load directly, else the edge list.
-ProbGraph load_graph(const Flags& f, std::uint64_t seed) {
+// on_host: the command itself never touches the device (`partition` without --target), so the
+// host loaders are used (same ProbGraph, same errors).
+ProbGraph load_graph(const Flags& f, std::uint64_t seed, bool on_host = false) {
     const std::string path = f.str("graph");
     {
         std::ifstream probe(path, std::ios::binary);
         char magic[5] = {};
         // binary caches are decoded, summed and validated on the device (same ProbGraph, same errors)
         if (probe.read(magic, 5) && std::string(magic, 5) == "HSAW1")
-            return load_cache_device(path, static_cast<int>(f.u64("device", 0)));
+            return on_host ? load_cache(path)
+                           : load_cache_device(path, static_cast<int>(f.u64("device", 0)));
     }
     LoadOptions opts;
     opts.symmetrize = f.switches.count("symmetrize") != 0;
+    if (on_host) return load_edge_list(path, weight_mode(f.str("weights", "indegree")), 0, opts);
     // text edge lists are parsed, re-ranked, sorted and summed on the device; anything outside the
     // device parser's plain grammar goes through the host parser inside this call
     // the reference's GraphArgs::seed is never bound to --seed (proj/src/cli.cpp:28,47,410): the
@@ -404,7 +408,7 @@ int cmd_partition(const Flags& f) {  // cli.cpp:292-335
     f.require("graph");
     f.require("parts");
     const std::uint64_t seed = f.u64("seed", 0);
-    ProbGraph g = load_graph(f, seed);
+    ProbGraph g = load_graph(f, seed, /*on_host=*/f.u64("target", 0) == 0);
     const std::string method = f.str("method", "hash");
     PartitionMethod pm;
     if (method == "hash")
