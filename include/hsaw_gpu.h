@@ -47,6 +47,15 @@ typedef struct hsaw_sampler_cfg {
     uint32_t window;       /* exact short-cycle window, 0..8 (default 2) */
     uint32_t batch_size;   /* attempts chained per batch / worker id (default 10) */
     uint64_t max_attempts; /* stream budget (default 100000000) */
+    /* 0 (default): the reference's stream — xorshift64* chained through each batch
+     * (proj/src/sampler.cpp:267-290); every output is bit-exact with the reference.
+     * 1: throughput mode, NOT the reference's walks: a counter-based Philox4x32-10 substream per
+     * walk index, one independent attempt per lane with immediate refill. Same walk law (start,
+     * live-edge pick, Brent + window 2, acceptance), same (batch, seq) bookkeeping with
+     * batch = walk index / batch_size; parity is statistical only (hit rate, length distribution,
+     * per-edge frequency, est_suspension; tests/test_gpu_philox.py states the tolerances).
+     * Requires heuristic 0 and window 2. */
+    uint32_t rng_mode;
 } hsaw_sampler_cfg;
 
 /* ItemKind, proj/include/hsaw/types.hpp:14. */

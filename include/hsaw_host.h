@@ -103,6 +103,12 @@ int hsawh_interdict(const void* dg, const void* g, const double* p_of, int kind,
                     const uint32_t* cand, uint64_t ncand, uint32_t k, double eps, double delta,
                     uint64_t seed, uint32_t batch_size, uint64_t max_attempts, int device,
                     hsawh_result* out, uint32_t* solution, char* json, uint64_t json_cap);
+/* Same with SamplerConfig::rng: 0 the reference's stream (bit-exact), 1 the device's Philox
+ * per-walk throughput mode (statistical parity only; never implied). */
+int hsawh_interdict_rng(const void* dg, const void* g, const double* p_of, int kind,
+                    const uint32_t* cand, uint64_t ncand, uint32_t k, double eps, double delta,
+                    uint64_t seed, uint32_t batch_size, uint64_t max_attempts, int device, int rng_mode,
+                    hsawh_result* out, uint32_t* solution, char* json, uint64_t json_cap);
 
 /* ---- `hsaw sample` equivalent: stream to `target`, return the counters — cli.cpp:267-290 ---- */
 int hsawh_sample(const void* dg, uint64_t target, uint64_t seed, uint64_t max_attempts,

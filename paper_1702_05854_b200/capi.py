@@ -40,10 +40,11 @@ class SamplerCfg(C.Structure):
     """hsaw_sampler_cfg == SamplerConfig (proj/include/hsaw/sampler.hpp:48-55)."""
 
     _fields_ = [("heuristic", C.c_int32), ("window", C.c_uint32), ("batch_size", C.c_uint32),
-                ("max_attempts", C.c_uint64)]
+                ("max_attempts", C.c_uint64), ("rng_mode", C.c_uint32)]
 
-    def __init__(self, heuristic=0, window=2, batch_size=10, max_attempts=100_000_000):
-        super().__init__(heuristic, window, batch_size, max_attempts)
+    def __init__(self, heuristic=0, window=2, batch_size=10, max_attempts=100_000_000, rng_mode=0):
+        """rng_mode 0: the reference's stream (bit-exact); 1: Philox per-walk throughput mode."""
+        super().__init__(heuristic, window, batch_size, max_attempts, rng_mode)
 
 
 def _p(a, t):

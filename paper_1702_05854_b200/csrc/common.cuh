@@ -519,6 +519,7 @@ struct hsaw_gpu_ctx {
     hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
     hsawgpu::HeldCsr held;                               // device-built CSR awaiting install / fetch
     hsawgpu::Restriction restr;                          // set only while a restricted chunk runs
+    uint32_t rng_mode = 0;  // draw source of the sampler launches of the running chunk (cfg.rng_mode)
     // greedy / coverage scratch (greedy.cu), reused across the doubling iterations
     hsawgpu::DevVec<uint32_t> g_cand_bits, g_cnt, g_fill, g_inv, g_covered, g_solution, g_query_bits;
     hsawgpu::DevVec<uint32_t> g_indexed_bits;  // items that own an inverted list

@@ -150,7 +150,8 @@ __device__ __forceinline__ bool claim(uint64_t* cursor, uint64_t total, bool wan
 // REC: 0 plain encode, 1 record walks (default stores), 2 record with streaming (.cs) stores.
 // STATS: per-lane work counters (draws, picks, algorithmic bytes) for instrumentation runs.
 // LAYOUT: kLayoutFat (32-byte edge records) or kLayoutCompact (in_src + 8-byte row headers).
-template <int HEUR, int WIN, int MINB, int REC, bool STATS, int LAYOUT, bool RESTR = false>
+template <int HEUR, int WIN, int MINB, int REC, bool STATS, int LAYOUT, bool RESTR = false,
+          class RNG = XorRng>
 __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) {
     // REC: every thread stages kStage pairs (128 bytes) in shared memory, slot-major so the
     // 8-byte accesses are conflict-free, and flushes whole 128-byte lines: short failed attempts
@@ -181,7 +182,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
     const NodeRec* __restrict__ nodes = p.nodes;
     const EdgeRec* __restrict__ edges = p.edges;
 
-    uint64_t s = 0, snapshot = 0;
+    RNG rng{};
+    uint64_t snapshot = 0;
     uint32_t bidx = 0;  // batch index within the launch (launches hold < 2^32 batches)
     uint32_t lo = 0, deg = 0;
     uint64_t tot = 0, scale = 0;  // fat layout: total-weight threshold and guess scale of the row
@@ -199,9 +201,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             uint64_t mine = 0;
             if (claim(p.cursor, p.nbatches, !have, lane, mine, drained)) {
                 bidx = (uint32_t)mine;
-                s = seed_from_worker(p.first_worker + mine);  // sampler.cpp:272
-#pragma unroll
-                for (int i = 0; i < 8; ++i) (void)prg_next(s);  // burn-in, sampler.cpp:273
+                rng.start(p.first_worker + mine);  // seed + burn-in, sampler.cpp:272-273
                 att = 0;
                 cnt = 0;
                 ncross = 0;
@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
         bool walking, from_edge = false;
         EdgeRec erec;
         if (fresh) {
-            snapshot = s;  // Seed_h, sampler.cpp:155,277
-            uint64_t k = draw53(s);
+            snapshot = rng.snapshot();  // Seed_h, sampler.cpp:155,277
+            uint64_t k = rng.draw();
             u = RESTR ? __ldg(p.domain + start_node(k, p.ndomain))  // sampler.cpp:26-31
                       : start_node(k, p.n);                         // sampler.cpp:24
             nedges = 0;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
         } else {
             walking = false;
             if (nedges < p.n) {  // len_cap = g.n, sampler.cpp:43,281
-                uint64_t k = draw53(s);
+                uint64_t k = rng.draw();
                 if (STATS) st_draws += 1;
                 if (STATS) st_steps += 1;
                 bool live;
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                 new_hw = h.y;
                 if (hdr_suspect(h.y)) {  // is_suspect, sampler.cpp:32,55
                     const NodeRec full = load_node(nodes, u);
-                    uint64_t k2 = draw53(s);
+                    uint64_t k2 = rng.draw();
                     if (STATS) st_draws += 1;
                     accepted = k2 < full.acc_thr;  // r <= p_of[u], sampler.cpp:34,57
                 }
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
             } else {
                 rec = load_node(nodes, u);
                 if (rec.acc_thr != 0) {  // is_suspect, sampler.cpp:32,55
-                    uint64_t k2 = draw53(s);
+                    uint64_t k2 = rng.draw();
                     if (STATS) st_draws += 1;
                     accepted = k2 < rec.acc_thr;  // r <= p_of[u], sampler.cpp:34,57
                 }
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                     // The next pick is certain to fail after exactly one draw (empty row), unless
                     // the length cap stops it before drawing: settle it now, saving an iteration.
                     if (nedges < p.n) {
-                        (void)prg_next(s);
+                        rng.skip();
                         if (STATS) st_draws += 1;
                         if (STATS) st_steps += 1;
                         if (STATS) st_bytes += 16;
@@ -641,13 +641,14 @@ struct DecodeParams {
     uint32_t ndomain;
 };
 
-template <bool PAIRS, int LAYOUT>
+template <bool PAIRS, int LAYOUT, class RNG = XorRng>
 __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
     const uint32_t lane = threadIdx.x & 31;
     const NodeRec* __restrict__ nodes = p.nodes;
     const EdgeRec* __restrict__ edges = p.edges;
 
-    uint64_t s = 0, w = 0, base = 0;
+    RNG rng{};
+    uint64_t w = 0, base = 0;
     uint2* pairs = nullptr;
     uint32_t lo = 0, deg = 0, len = 0, nedges = 0;
     uint64_t tot = 0, scale = 0;
@@ -660,7 +661,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
             uint64_t mine = 0;
             if (claim(p.cursor, p.nwalks, !have, lane, mine, drained)) {
                 w = PAIRS ? p.sel[mine] : mine;
-                s = p.seed[w];
+                rng.restore(p.seed[w]);
                 len = p.len[w];
                 if (PAIRS)
                     pairs = p.pair_dst[w];
@@ -678,12 +679,12 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
         bool arrived = false, from_edge = false;
         EdgeRec erec;
         if (fresh) {
-            if (s == 0) {
+            if (!rng.valid()) {
                 verdict = 2;  // "decode: zero seed state", sampler.cpp:306
                 nedges = 0;
                 if (p.nnodes) p.nnodes[w] = 0;
             } else {
-                uint64_t k = draw53(s);
+                uint64_t k = rng.draw();
                 u = p.domain ? __ldg(p.domain + start_node(k, p.ndomain)) : start_node(k, p.n);
                 nedges = 0;
                 if (PAIRS)
@@ -697,7 +698,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
             if (nedges >= p.n) {
                 verdict = 2;
             } else {
-                uint64_t k = draw53(s);
+                uint64_t k = rng.draw();
                 st_steps += 1;
                 bool live;
                 uint32_t slot = 0;
@@ -743,13 +744,13 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
                 rec.lo = h.x;
                 rec.deg = hdr_deg(h.y);
                 new_hw = h.y;
-                if (hdr_suspect(h.y)) hit = draw53(s) < load_node(nodes, u).acc_thr;
+                if (hdr_suspect(h.y)) hit = rng.draw() < load_node(nodes, u).acc_thr;
             } else if (from_edge &&
                        header_from_edge(erec, rec.lo, rec.deg, rec.tot_thr, rec.scale)) {
                 rec.acc_thr = 0;
             } else {
                 rec = load_node(nodes, u);
-                if (rec.acc_thr != 0) hit = draw53(s) < rec.acc_thr;
+                if (rec.acc_thr != 0) hit = rng.draw() < rec.acc_thr;
             }
             if (hit) {
                 verdict = nedges == len ? 1 : 2;  // sampler.cpp:311-314, 329-332
@@ -770,7 +771,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
         }
         if (verdict != 0) {
             p.status[w] = (uint8_t)verdict;
-            if (p.nnodes && !(fresh && s == 0)) p.nnodes[w] = nedges + 1;
+            if (p.nnodes && !(fresh && !rng.valid())) p.nnodes[w] = nedges + 1;
             have = false;
         }
     }
@@ -983,6 +984,9 @@ void validate_cfg(const hsaw_sampler_cfg& cfg) {
              "sampler: the Floyd heuristic is not available on the device path (use Brent or None)");
     if (cfg.heuristic != 0 && cfg.heuristic != 2) fail(HSAW_EINVAL, "sampler: unknown heuristic");
     if (cfg.batch_size == 0) fail(HSAW_EINVAL, "sampler: batch_size must be positive");
+    if (cfg.rng_mode > 1) fail(HSAW_EINVAL, "sampler: unknown rng_mode");
+    if (cfg.rng_mode == 1 && (cfg.heuristic != 0 || cfg.window != 2))
+        fail(HSAW_EINVAL, "sampler: the Philox per-walk mode is built for Brent + window 2 only");
 }
 
 // rec == nullptr: plain encode. Otherwise accepted walks are logged into rec->arena.
@@ -996,6 +1000,34 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
                    ctx->g.n, cfg.batch_size, cfg.window, first_worker, nbatches, d_seed, d_len, d_count,
                    d_stats, d_cursor, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr};
     const bool compact = ctx->g.layout == kLayoutCompact;
+    if (cfg.rng_mode == 1) {
+        // Philox per-walk mode: the caller passes one work item per ATTEMPT (batch_size 1), so a
+        // lane that finishes its attempt refills at once; recording as in the default path
+        if (ctx->restr.domain) fail(HSAW_EINVAL, "encode: the Philox mode does not combine with a restriction");
+        if (cfg.batch_size != 1) fail(HSAW_EINVAL, "encode: Philox launches carry one attempt per item");
+        if (rec) {
+            if (rec->arena_cap < kLogChunk) fail(HSAW_EINVAL, "encode: record arena too small");
+            p.arena = rec->arena;
+            p.arena_cap = rec->arena_cap;
+            p.arena_cursor = rec->arena_cursor;
+            p.out_log = rec->out_log;
+            HSAW_CUDA_CHECK(cudaMemsetAsync(rec->arena_cursor, 0, 4, ctx->stream));
+        }
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
+        auto go_p = [&](auto kernel) {
+            int blocks = persistent_blocks(ctx, kernel, nbatches);
+            StageScope timer(ctx, HSAW_STAGE_ENCODE);
+            kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+            check_launch(ctx, "encode_kernel(philox)");
+        };
+        if (rec)
+            compact ? go_p(encode_kernel<0, 2, 4, 2, false, kLayoutCompact, false, PhiloxRng>)
+                    : go_p(encode_kernel<0, 2, 4, 2, false, kLayoutFat, false, PhiloxRng>);
+        else
+            compact ? go_p(encode_kernel<0, 2, 4, 0, true, kLayoutCompact, false, PhiloxRng>)
+                    : go_p(encode_kernel<0, 2, 4, 0, true, kLayoutFat, false, PhiloxRng>);
+        return;
+    }
     if (ctx->restr.domain) {  // partitioned sampling: the restricted instantiations, never recording
         if (rec) fail(HSAW_EINVAL, "encode: restricted sampling does not record");
         if (!ctx->restr.allowed || !ctx->restr.out_cross || ctx->restr.ndomain == 0)
@@ -1171,7 +1203,10 @@ static void launch_decode_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_
         kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
         check_launch(ctx, "decode_kernel");
     };
-    if (ctx->g.layout == kLayoutCompact)
+    if (ctx->rng_mode == 1)
+        ctx->g.layout == kLayoutCompact ? go(decode_kernel<false, kLayoutCompact, PhiloxRng>)
+                                        : go(decode_kernel<false, kLayoutFat, PhiloxRng>);
+    else if (ctx->g.layout == kLayoutCompact)
         go(decode_kernel<false, kLayoutCompact>);
     else
         go(decode_kernel<false, kLayoutFat>);
@@ -1199,7 +1234,10 @@ void launch_decode_pairs(hsaw_gpu_ctx* ctx, uint64_t nsel, const uint32_t* d_sel
         kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
         check_launch(ctx, "decode_kernel<pairs>");
     };
-    if (ctx->g.layout == kLayoutCompact)
+    if (ctx->rng_mode == 1)
+        ctx->g.layout == kLayoutCompact ? go(decode_kernel<true, kLayoutCompact, PhiloxRng>)
+                                        : go(decode_kernel<true, kLayoutFat, PhiloxRng>);
+    else if (ctx->g.layout == kLayoutCompact)
         go(decode_kernel<true, kLayoutCompact>);
     else
         go(decode_kernel<true, kLayoutFat>);

@@ -212,12 +212,27 @@ __global__ void __launch_bounds__(256) compact_pairs(
 }
 
 // accepted_after_batch (sampler.cpp:459) for the batches of this chunk.
+// `first` is indexed by launch item: batches, or single attempts in the Philox mode, where a batch
+// is `stride` consecutive items.
 __global__ void batch_cumulative(uint64_t nbatches, const uint32_t* __restrict__ first,
                                  const uint32_t* __restrict__ vidx, uint64_t base_walk,
-                                 uint64_t* __restrict__ out) {
+                                 uint64_t* __restrict__ out, uint32_t stride) {
     uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nbatches) return;
-    out[b] = base_walk + vidx[first[b + 1]];
+    out[b] = base_walk + vidx[first[(b + 1) * stride]];
+}
+
+// Philox mode: the launch items were single attempts; turn (global attempt index, 0) into the
+// stream's (batch, seq) tags: batch = attempt / l, seq = rank among the batch's accepted attempts.
+__global__ void philox_tags(uint64_t nwalks, uint32_t l, uint64_t first_attempt, uint64_t first_batch,
+                            const uint32_t* __restrict__ first, uint64_t* __restrict__ enc_batch,
+                            uint32_t* __restrict__ enc_seq) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nwalks) return;
+    const uint64_t item = enc_batch[i] - first_attempt;  // launch item of this walk
+    const uint64_t b = item / l;
+    enc_seq[i] = first[item] - first[b * l];
+    enc_batch[i] = first_batch + b;
 }
 
 // first index with a[i] >= key, or n
@@ -375,7 +390,7 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->accepted_after_batch.reserve(s->local_batches + nb, st);
     if (E > 0) {
         batch_cumulative<<<blocks_for(nb, 256), 256, 0, st>>>(
-            nb, x.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches);
+            nb, x.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches, 1);
         check_launch(ctx, "batch_cumulative");
     } else {
         std::vector<uint64_t> flat(nb, s->accepted);
@@ -405,6 +420,19 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     const uint64_t slots = nb * l;
     if (slots > 0xFFFFFFF0ull) fail(HSAW_EINVAL, "stream: chunk too large for 32-bit walk ids");
     SamplerScratch& x = ctx->samp;
+    // Philox per-walk mode: the launch items are single attempts (ni items of ml = 1 attempt);
+    // a batch is l consecutive items. Reference mode: items are batches.
+    const bool philox = s->cfg.rng_mode == 1;
+    const uint64_t ni = philox ? slots : nb;
+    const uint32_t ml = philox ? 1u : l;
+    hsaw_sampler_cfg kcfg = s->cfg;
+    kcfg.batch_size = ml;
+    const uint64_t first_item = philox ? (s->seed + first_batch) * l : s->seed + first_batch;
+    struct RngGuard {
+        hsaw_gpu_ctx* c;
+        ~RngGuard() { c->rng_mode = 0; }
+    } rng_guard{ctx};
+    ctx->rng_mode = s->cfg.rng_mode;
 
     // ---- arena sizing: one open chunk per resident lane + the expected volume of accepted walks
     // (observed pairs per attempt so far, with slack). Too small is safe: overflow -> replay.
@@ -425,17 +453,17 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     x.slot_seed.ensure_scratch(slots + 1);
     x.slot_len.ensure_scratch(slots + 1);
     x.slot_log.ensure_scratch(slots + 1);
-    x.count.ensure_scratch(nb + 1);
-    x.first.ensure_scratch(nb + 1);
-    HSAW_CUDA_CHECK(cudaMemsetAsync(x.count.p + nb, 0, 4, st));
+    x.count.ensure_scratch(ni + 1);
+    x.first.ensure_scratch(ni + 1);
+    HSAW_CUDA_CHECK(cudaMemsetAsync(x.count.p + ni, 0, 4, st));
     uint32_t* arena_cursor = reinterpret_cast<uint32_t*>(s->stats.p + 10);
     EncodeRecord rec{x.arena.p, arena_cap, arena_cursor, x.slot_log.p};
-    launch_encode(ctx, s->cfg, s->seed + first_batch, nb, x.slot_seed.p, x.slot_len.p, x.count.p,
+    launch_encode(ctx, kcfg, first_item, ni, x.slot_seed.p, x.slot_len.p, x.count.p,
                   s->stats.p, s->stats.p + 8, &rec, s->collect_stats);
-    exclusive_sum_u32(ctx, x.count.p, x.first.p, nb + 1);
+    exclusive_sum_u32(ctx, x.count.p, x.first.p, ni + 1);
     HSAW_CUDA_CHECK(
         cudaMemcpyAsync(ctx->h_scalars + 1, arena_cursor, 4, cudaMemcpyDeviceToHost, st));
-    const uint64_t E = read_u32(ctx, x.first.p + nb);
+    const uint64_t E = read_u32(ctx, x.first.p + ni);
     const uint64_t arena_used = *reinterpret_cast<uint32_t*>(ctx->h_scalars + 1);
     (void)arena_used;
 
@@ -454,11 +482,16 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
         {
             StageScope timer(ctx, HSAW_STAGE_COMPACT);
             gather_recorded<<<blocks_for(slots, 256), 256, 0, st>>>(
-                nb, l, first_batch, x.count.p, x.first.p, x.slot_seed.p, x.slot_len.p,
-                x.slot_log.p, x.arena.p, record_overflow_marker(), x.enc_seed.p, x.enc_len.p,
-                x.enc_batch.p, x.enc_seq.p, reinterpret_cast<const uint2**>(x.enc_src.p),
-                x.ovf_pairs.p);
+                ni, ml, philox ? first_batch * l : first_batch, x.count.p, x.first.p, x.slot_seed.p,
+                x.slot_len.p, x.slot_log.p, x.arena.p, record_overflow_marker(), x.enc_seed.p,
+                x.enc_len.p, x.enc_batch.p, x.enc_seq.p,
+                reinterpret_cast<const uint2**>(x.enc_src.p), x.ovf_pairs.p);
             check_launch(ctx, "gather_recorded");
+            if (philox) {
+                philox_tags<<<blocks_for(E, 256), 256, 0, st>>>(E, l, first_batch * l, first_batch,
+                                                               x.first.p, x.enc_batch.p, x.enc_seq.p);
+                check_launch(ctx, "philox_tags");
+            }
             HSAW_CUDA_CHECK(cudaMemsetAsync(x.ovf_pairs.p + E, 0, 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(nsel, 0, 4, st));
             exclusive_sum_u32_to_u64(ctx, x.ovf_pairs.p, x.tmp_off.p, E + 1);
@@ -534,7 +567,7 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->accepted_after_batch.reserve(s->local_batches + nb, st);
     if (E > 0) {
         batch_cumulative<<<blocks_for(nb, 256), 256, 0, st>>>(
-            nb, x.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches);
+            nb, x.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches, ml);
         check_launch(ctx, "batch_cumulative");
     } else {
         std::vector<uint64_t> flat(nb, s->accepted);
@@ -585,7 +618,9 @@ void sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches) {
         const double per_attempt = s->pairs_per_attempt > 0 ? s->pairs_per_attempt : 24.0;
         const uint64_t arena_batches = (uint64_t)((double)(kArenaTargetBytes / 8) / (per_attempt * 1.5 * (double)bs));
         nb = std::min(nb, std::max<uint64_t>(arena_batches, 1ull << 14));
-        if (fused_enabled() && record_supported(s->cfg) && s->r_ndomain == 0)
+        if (s->cfg.rng_mode == 1 && s->r_ndomain != 0)
+            fail(HSAW_EINVAL, "stream: the Philox mode does not combine with a restriction");
+        if ((fused_enabled() || s->cfg.rng_mode == 1) && record_supported(s->cfg) && s->r_ndomain == 0)
             sample_chunk_fused(s, first_batch + done, nb);
         else
             sample_chunk(s, first_batch + done, nb);

@@ -36,6 +36,69 @@ __device__ __forceinline__ uint64_t seed_from_worker(uint64_t worker_id) {
     }
 }
 
+// ---- draw sources of the walk kernels ------------------------------------------------------------
+// XorRng is the reference's stream (xorshift64* chained through a batch): the bit-exact mode.
+// PhiloxRng is the throughput mode of north_star item 2: a counter-based Philox4x32-10 substream
+// per WALK INDEX (counter = walk id | draw-pair index, fixed key), so every attempt is an
+// independent work item and a finished lane refills at once instead of carrying a 10-attempt
+// chain. Its walks follow the same law but are not the reference's walks: statistical parity only.
+struct XorRng {
+    uint64_t s;
+    __device__ __forceinline__ void start(uint64_t worker_id) {
+        s = seed_from_worker(worker_id);  // sampler.cpp:272
+#pragma unroll
+        for (int i = 0; i < 8; ++i) (void)prg_next(s);  // burn-in, sampler.cpp:273
+    }
+    __device__ __forceinline__ uint64_t snapshot() const { return s; }
+    __device__ __forceinline__ void restore(uint64_t snap) { s = snap; }
+    __device__ __forceinline__ bool valid() const { return s != 0; }
+    __device__ __forceinline__ uint64_t draw() { return draw53(s); }
+    __device__ __forceinline__ void skip() { (void)prg_next(s); }
+};
+
+__device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                             uint32_t k0, uint32_t k1) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+}
+
+struct PhiloxRng {
+    uint64_t id;     // walk index: the encoded "seed" of the walk
+    uint64_t spare;  // second 64-bit half of the last block
+    uint32_t ctr;    // next draw-pair index
+    uint32_t have;
+    __device__ __forceinline__ void start(uint64_t walk_id) { restore(walk_id); }
+    __device__ __forceinline__ uint64_t snapshot() const { return id; }
+    __device__ __forceinline__ void restore(uint64_t snap) {
+        id = snap;
+        ctr = 0;
+        have = 0;
+    }
+    __device__ __forceinline__ bool valid() const { return true; }
+    __device__ __forceinline__ uint64_t draw() {
+        if (have) {
+            have = 0;
+            return spare >> 11;
+        }
+        uint32_t c0 = (uint32_t)id, c1 = (uint32_t)(id >> 32), c2 = ctr++, c3 = 0x48534157u;  // "HSAW"
+        uint32_t k0 = 0xA4093822u, k1 = 0x299F31D0u;
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            philox_round(c0, c1, c2, c3, k0, k1);
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        spare = (uint64_t)c2 | ((uint64_t)c3 << 32);
+        have = 1;
+        return ((uint64_t)c0 | ((uint64_t)c1 << 32)) >> 11;
+    }
+    __device__ __forceinline__ void skip() { (void)draw(); }
+};
+
 // pick_uniform_node, prng.hpp:57-61: floor(fl(u01 * (double)n)) clamped to n-1. The product is a
 // single IEEE round-to-nearest FP64 multiply on both sides (no FMA contraction possible).
 __device__ __forceinline__ uint32_t start_node(uint64_t k, uint32_t n) {

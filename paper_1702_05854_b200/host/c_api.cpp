@@ -232,6 +232,15 @@ int hsawh_interdict(const void* dg, const void* g, const double* p_of, int kind,
                     const uint32_t* cand, uint64_t ncand, uint32_t k, double eps, double delta,
                     uint64_t seed, uint32_t batch_size, uint64_t max_attempts, int device,
                     hsawh_result* out, uint32_t* solution, char* json, uint64_t json_cap) {
+    return hsawh_interdict_rng(dg, g, p_of, kind, cand, ncand, k, eps, delta, seed, batch_size,
+                               max_attempts, device, 0, out, solution, json, json_cap);
+}
+
+int hsawh_interdict_rng(const void* dg, const void* g, const double* p_of, int kind,
+                        const uint32_t* cand, uint64_t ncand, uint32_t k, double eps, double delta,
+                        uint64_t seed, uint32_t batch_size, uint64_t max_attempts, int device,
+                        int rng_mode, hsawh_result* out, uint32_t* solution, char* json,
+                        uint64_t json_cap) {
     return guarded([&] {
         const ItemKind ik = kind == 0 ? ItemKind::Edge : ItemKind::Node;
         CandidateSet cs = cand ? CandidateSet::of(ik, std::vector<std::uint32_t>(cand, cand + ncand))
@@ -240,6 +249,7 @@ int hsawh_interdict(const void* dg, const void* g, const double* p_of, int kind,
         opts.seed = seed;
         opts.sampler.batch_size = batch_size;
         opts.sampler.max_attempts = max_attempts;
+        opts.sampler.rng = rng_mode == 1 ? WalkRng::PhiloxPerWalk : WalkRng::Reference;
         opts.device = device;
         InterdictionResult r;
         if (dg) {

@@ -38,6 +38,7 @@ hsaw_sampler_cfg to_c(const SamplerConfig& cfg) {
     c.window = cfg.window;
     c.batch_size = cfg.batch_size;
     c.max_attempts = cfg.max_attempts;
+    c.rng_mode = cfg.rng == WalkRng::PhiloxPerWalk ? 1u : 0u;
     return c;
 }
 

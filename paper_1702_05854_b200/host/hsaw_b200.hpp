@@ -255,11 +255,17 @@ struct SamplePool {
 
 enum class CycleHeuristic { Brent, Floyd, None };  // Floyd is not offered on the device path
 
+// Reference: the reference's xorshift64* stream, every result bit-exact (the default, always).
+// PhiloxPerWalk: the device's throughput mode — an independent counter-based substream per walk
+// index; same walk law, different walks (statistical parity only). Never chosen implicitly.
+enum class WalkRng { Reference, PhiloxPerWalk };
+
 struct SamplerConfig {
     CycleHeuristic heuristic = CycleHeuristic::Brent;
     std::uint32_t window = 2;
     std::uint32_t batch_size = 10;
     std::uint64_t max_attempts = 100'000'000;
+    WalkRng rng = WalkRng::Reference;  // not in the reference's SamplerConfig (sampler.hpp:48-55)
 };
 
 // thread_sample (proj/src/sampler.cpp:267-290) on the device.

@@ -75,6 +75,9 @@ def lib() -> C.CDLL:
     L.hsawh_interdict.argtypes = [vp, vp, f64p, C.c_int, u32p, C.c_uint64, C.c_uint32, C.c_double,
                                   C.c_double, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int,
                                   C.POINTER(Result), u32p, C.c_char_p, C.c_uint64]
+    L.hsawh_interdict_rng.argtypes = [vp, vp, f64p, C.c_int, u32p, C.c_uint64, C.c_uint32, C.c_double,
+                                      C.c_double, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int,
+                                      C.c_int, C.POINTER(Result), u32p, C.c_char_p, C.c_uint64]
     L.hsawh_sample.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p]
     L.hsawh_graph_load_edge_list_device.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int,
                                                     C.c_char_p, C.c_int, vpp]
@@ -353,8 +356,9 @@ class DeviceGraph:
 
 def interdict(graph: Graph, p_of, kind, k, eps, delta, seed=0, cand=None, batch_size=10,
               max_attempts=100_000_000, device=0, dg: DeviceGraph | None = None,
-              want_json=False) -> dict:
-    """esia (kind 0) / nsia (kind 1). With dg the graph is already on the device."""
+              want_json=False, rng_mode=0) -> dict:
+    """esia (kind 0) / nsia (kind 1). With dg the graph is already on the device. rng_mode 1: the
+    Philox per-walk throughput mode (statistical parity only)."""
     p = np.ascontiguousarray(p_of, dtype=np.float64)
     ca = None if cand is None else np.ascontiguousarray(cand, dtype=np.uint32)
     if ca is not None and ca.size == 0:
@@ -364,9 +368,9 @@ def interdict(graph: Graph, p_of, kind, k, eps, delta, seed=0, cand=None, batch_
     res = Result()
     sol = np.zeros(max(k, 1), dtype=np.uint32)
     buf = C.create_string_buffer(1 << 16)
-    _chk(lib().hsawh_interdict(dg.h if dg is not None else None, graph.h, _p(p, f64p), kind,
-                               ca_ptr, nc, k, eps, delta, seed, batch_size, max_attempts, device,
-                               C.byref(res), _p(sol, u32p), buf, len(buf)))
+    _chk(lib().hsawh_interdict_rng(dg.h if dg is not None else None, graph.h, _p(p, f64p), kind,
+                                   ca_ptr, nc, k, eps, delta, seed, batch_size, max_attempts,
+                                   device, rng_mode, C.byref(res), _p(sol, u32p), buf, len(buf)))
     out = dict(kind="edge" if kind == 0 else "node", k=res.k, epsilon=eps, delta=delta,
                solution=[int(x) for x in sol[:k]], est_suspension=res.est_suspension,
                coverage=res.coverage, samples_used=res.samples_used, attempts=res.attempts,
