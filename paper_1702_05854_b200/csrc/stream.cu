@@ -567,7 +567,8 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->accepted_after_batch.reserve(s->local_batches + nb, st);
     if (E > 0) {
         batch_cumulative<<<blocks_for(nb, 256), 256, 0, st>>>(
-            nb, x.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches, ml);
+            nb, x.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches,
+            philox ? l : 1u);  // launch items per batch
         check_launch(ctx, "batch_cumulative");
     } else {
         std::vector<uint64_t> flat(nb, s->accepted);
