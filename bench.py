@@ -84,6 +84,8 @@ def parse_args():
                     help="interdiction driver timed beside the sampler (edge or node candidates)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-philox", action="store_true",
+                    help="skip the Philox per-walk throughput leg")
     ap.add_argument("--ingest", action="store_true",
                     help="also time the step before the path (SURVEY 8f row 1): HSAW1 cache and "
                          "edge-list text of a graph of this size -> ProbGraph / resident graph, "
@@ -581,6 +583,45 @@ def run_b200(args):
         "walks_replayed_after_log_overflow": int(sum(replay_counts[-args.steps:])),
         "roofline": roofline, "clocks": clock_info, "gpu_launches": int(tot_launches),
     }
+
+    # ---- the Philox per-walk throughput mode on the same batch ranges (north_star item 2): NOT the
+    # reference's stream (statistical parity only, tests/test_gpu_philox.py), reported beside the
+    # bit-exact headline, never instead of it
+    if world == 1 and not args.no_philox:
+        try:
+            pcfg = capi.SamplerCfg(max_attempts=10**15, rng_mode=1)
+
+            def philox_step(i):
+                with ctx.stream(seed=STREAM_SEED, cfg=pcfg) as st:
+                    return st.sample_range(i * B, B)
+            for i in range(2):
+                philox_step(i)
+            torch.cuda.synchronize()
+            ctx.stage_times(reset=True)
+            flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+            pp, pacc = [], 0
+            with torch.cuda.stream(tstream):
+                for i in range(min(args.steps, 5)):
+                    flush.zero_()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(tstream)
+                    pacc += philox_step(2 + i)
+                    b.record(tstream)
+                    pp.append((a, b))
+            torch.cuda.synchronize()
+            del flush
+            pms = sum(a.elapsed_time(b) for a, b in pp)
+            pst = ctx.stage_times(reset=True)
+            out["philox_mode"] = {
+                "value": pacc / (pms / 1e3), "unit": UNIT, "steps": len(pp),
+                "ms_per_step": pms / len(pp), "accept_rate": pacc / (len(pp) * B * 10),
+                "k1_ms_per_step": pst["encode"][0] / max(pst["encode"][1], 1),
+                "note": "rng_mode 1: counter-based Philox4x32-10 substream per walk index, one "
+                        "attempt per lane with immediate refill; same walk law, not the "
+                        "reference's walks",
+            }
+        except Exception as exc:
+            out["philox_mode"] = {"error": str(exc)[:300]}
 
     # ---- seconds-to-solution on the same config, graph resident (single GPU path)
     r_dev = None
