@@ -315,6 +315,38 @@ int hsaw_gpu_coverage_upper_bound(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stre
                                   uint64_t cnt, const uint32_t* cand_ids, uint64_t ncand,
                                   uint32_t k, uint64_t* bound);
 
+/* Building blocks of the sharded (multi-GPU) solve: walks are sharded over ranks by
+ * batch range, so CoverageIndex / greedy_max_cover (proj/src/coverage.cpp:37-138) become: local
+ * counts -> all-reduce (the caller's NCCL) -> every rank extracts from its LOCAL walks the items
+ * that can still win -> all-gather of those reduced walks -> the single-GPU greedy run redundantly.
+ * d_counts arguments are DEVICE pointers to `limit` u32 counters (limit = m for edges, n for nodes).
+ *   hsaw_gpu_stream_histogram   occurrences of every candidate item in walks [off, off+cnt)
+ *   hsaw_gpu_counts_bound       hsaw_gpu_coverage_upper_bound's answer from (all-reduced) counts
+ *   hsaw_gpu_counts_threshold   the indexing threshold hsaw_gpu_greedy would choose for them
+ *   hsaw_gpu_reduced_walks      walks [off, off+cnt) restricted to items with count >= min_count
+ *                               (walks left empty are dropped), as a device walk set
+ *   hsaw_gpu_walkset_copy_device / _from_device   lengths + items out of / into a walk set,
+ *                               device to device (the all-gather buffers)
+ *   hsaw_gpu_last_greedy_min_gain  smallest per-round gain of the last hsaw_gpu_greedy on this
+ *                               context (0 if it ran out of positive gains): below min_count means
+ *                               the reduced instance was not enough and the caller gathers all */
+int hsaw_gpu_stream_histogram(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind,
+                              uint64_t off, uint64_t cnt, const uint32_t* cand_ids, uint64_t ncand,
+                              uint32_t* d_counts);
+int hsaw_gpu_counts_bound(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint32_t limit, uint32_t k,
+                          uint64_t cap, uint64_t* bound);
+int hsaw_gpu_counts_threshold(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint32_t limit,
+                              uint32_t* min_count);
+int hsaw_gpu_reduced_walks(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind, uint64_t off,
+                           uint64_t cnt, const uint32_t* d_counts, uint32_t min_count,
+                           hsaw_gpu_walkset** out, uint64_t* nsets, uint64_t* nitems);
+int hsaw_gpu_walkset_copy_device(const hsaw_gpu_walkset* walkset, uint32_t* d_lens,
+                                 uint32_t* d_items);
+int hsaw_gpu_walkset_from_device(hsaw_gpu_ctx* ctx, uint32_t limit, uint64_t nsets,
+                                 const uint32_t* d_lens, const uint32_t* d_items, uint64_t nitems,
+                                 hsaw_gpu_walkset** out);
+uint64_t hsaw_gpu_last_greedy_min_gain(const hsaw_gpu_ctx* ctx);
+
 /* ---- stepwise greedy for sharded (multi-GPU) solves ---------------------------------------- */
 
 /* The rounds of greedy_max_cover split into steps so that ranks holding disjoint shards of R_t can

@@ -135,6 +135,16 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_paired_runs.argtypes = [vp, C.c_int, u32p, C.c_uint64, u64p, C.c_uint64, u32p, u32p]
     L.hsaw_gpu_rr_node_sets.argtypes = [vp, u64p, C.c_uint32, C.POINTER(vp), u64p]
     L.hsaw_gpu_walkset_export.argtypes = [vp, u64p, u32p]
+    L.hsaw_gpu_stream_histogram.argtypes = [vp, vp, C.c_int, C.c_uint64, C.c_uint64, u32p, C.c_uint64, vp]
+    L.hsaw_gpu_counts_bound.argtypes = [vp, vp, C.c_uint32, C.c_uint32, C.c_uint64, u64p]
+    L.hsaw_gpu_counts_threshold.argtypes = [vp, vp, C.c_uint32, u32p]
+    L.hsaw_gpu_reduced_walks.argtypes = [vp, vp, C.c_int, C.c_uint64, C.c_uint64, vp, C.c_uint32,
+                                         C.POINTER(vp), u64p, u64p]
+    L.hsaw_gpu_walkset_copy_device.argtypes = [vp, vp, vp]
+    L.hsaw_gpu_walkset_from_device.argtypes = [vp, C.c_uint32, C.c_uint64, vp, vp, C.c_uint64,
+                                               C.POINTER(vp)]
+    L.hsaw_gpu_last_greedy_min_gain.argtypes = [vp]
+    L.hsaw_gpu_last_greedy_min_gain.restype = C.c_uint64
     L.hsaw_gpu_prg_jump.argtypes = [C.c_uint64, C.c_uint64]
     L.hsaw_gpu_prg_jump.restype = C.c_uint64
     L.hsaw_gpu_estimate_suspension.argtypes = [vp, C.c_int, u32p, C.c_uint64, C.c_double,
@@ -167,6 +177,9 @@ EXPORTS = (
     "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout", "hsaw_gpu_stream_keep",
     "hsaw_gpu_stream_restrict", "hsaw_gpu_stream_crossings",
     "hsaw_gpu_rr_node_sets", "hsaw_gpu_walkset_export",
+    "hsaw_gpu_stream_histogram", "hsaw_gpu_counts_bound", "hsaw_gpu_counts_threshold",
+    "hsaw_gpu_reduced_walks", "hsaw_gpu_walkset_copy_device", "hsaw_gpu_walkset_from_device",
+    "hsaw_gpu_last_greedy_min_gain",
 )
 
 

@@ -507,6 +507,7 @@ struct hsaw_gpu_ctx {
     bool k1_window_on = false;
     uint64_t launches = 0;
     uint64_t greedy_full_index_reruns = 0;  // thresholded index was too optimistic (diagnostic)
+    uint64_t last_greedy_min_gain = 0;      // smallest per-round gain of the last hsaw_gpu_greedy
     std::string last_error;
     // reusable scratch
     hsawgpu::DevVec<unsigned char> cub_tmp;

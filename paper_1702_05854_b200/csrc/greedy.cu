@@ -788,6 +788,11 @@ __global__ void add_counts(uint32_t* __restrict__ dst, const uint32_t* __restric
         dst[i] += src[i];
 }
 
+__global__ void offsets_to_lens(const uint64_t* __restrict__ off, uint64_t n, uint32_t* __restrict__ lens) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) lens[i] = (uint32_t)(off[i + 1] - off[i]);
+}
+
 static bool hist_cache_usable(const hsaw_gpu_stream* stream, const uint32_t* cand_ids) {
     static const bool off = [] {
         const char* env = std::getenv("HSAW_HIST_CACHE");  // A/B knob
@@ -1125,9 +1130,13 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         // ---- zero-gain padding: smallest unselected candidates in ascending order
         // (proj/src/coverage.cpp:101-106,155; pinned by tests/test_coverage.cpp:58-64)
         uint64_t cov = 0;
+        // smallest gain of this run's rounds (0 when fewer than k rounds had a positive gain):
+        // what a caller that fed a thresholded instance needs to know (sharded solve)
+        ctx->last_greedy_min_gain = done < k ? 0 : ~0ull;
         for (uint32_t r = 0; r < done; ++r) {
             solution[r] = h_sol[r];
             cov += h_gain[r];
+            ctx->last_greedy_min_gain = std::min<uint64_t>(ctx->last_greedy_min_gain, h_gain[r]);
         }
         if (done < k) {
             std::vector<uint32_t> chosen(solution, solution + done);
@@ -1432,5 +1441,281 @@ int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         *coverage = ctx->h_scalars[0];
     });
 }
+
+}  // extern "C"
+
+// ---- building blocks of the sharded solve (paper_1702_05854_b200/sharded.py) -------------------------
+// Walks are sharded over ranks; counts are combined with an all-reduce by the caller (NCCL over
+// NVLink through torch.distributed, or libnccl directly). After the all-reduce every rank knows the
+// global marginal-gain vector, extracts from its LOCAL walks only the items that can still win
+// (global count >= the indexing threshold — the same rule the single-GPU greedy uses), the ranks
+// all-gather those reduced walks, and each runs the single-GPU greedy (tail kernel included) on
+// the gathered set redundantly: identical selections everywhere, rounds stay ~8 us, and what
+// crosses NVLink is at most an eighth of the items once per greedy call instead of two collectives
+// per round.
+
+// one warp per walk: how many of its items are indexed
+__global__ void reduced_count(WalkView v, const uint32_t* __restrict__ indexed_bits, BitFilter filter,
+                              uint32_t* __restrict__ wcount) {
+    uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = warp; i < v.cnt; i += nwarps) {
+        uint64_t w = v.w0 + i;
+        uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
+        uint32_t c = 0;
+        for (uint64_t p = b + lane; p < e; p += 32) {
+            uint32_t it = v.items[p];
+            c += it < v.limit && filter_pass(filter, it) &&
+                 ((indexed_bits[it >> 5] >> (it & 31)) & 1u);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFullMask, c, o);
+        if (lane == 0) wcount[i] = c;
+    }
+}
+
+__global__ void reduced_flags(const uint32_t* __restrict__ wcount, uint64_t n,
+                              uint32_t* __restrict__ flag) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= n) flag[i] = i < n && wcount[i] ? 1u : 0u;
+}
+
+// kept walks (>= 1 indexed item) in order; item order inside a walk is irrelevant (set semantics
+// with multiplicity), so lanes place their items by ballot ranks
+__global__ void reduced_write(WalkView v, const uint32_t* __restrict__ indexed_bits, BitFilter filter,
+                              const uint32_t* __restrict__ wcount, const uint32_t* __restrict__ widx,
+                              const uint64_t* __restrict__ ioff, uint32_t* __restrict__ out_lens,
+                              uint32_t* __restrict__ out_items) {
+    uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t lane = threadIdx.x & 31;
+    uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = warp; i < v.cnt; i += nwarps) {
+        if (!wcount[i]) continue;
+        uint64_t w = v.w0 + i;
+        uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
+        if (lane == 0) out_lens[widx[i]] = wcount[i];
+        uint64_t at = ioff[i];
+        for (uint64_t p0 = b; p0 < e; p0 += 32) {
+            uint64_t p = p0 + lane;
+            uint32_t it = p < e ? v.items[p] : 0xFFFFFFFFu;
+            bool keep = p < e && it < v.limit && filter_pass(filter, it) &&
+                        ((indexed_bits[it >> 5] >> (it & 31)) & 1u);
+            unsigned m = __ballot_sync(kFullMask, keep);
+            if (keep) out_items[at + __popc(m & ((1u << lane) - 1))] = it;
+            at += __popc(m);
+        }
+    }
+}
+
+static uint64_t scan_total_u32(hsaw_gpu_ctx* ctx, const uint32_t* d_in, uint64_t* d_out, uint64_t n) {
+    exclusive_sum_u32_to_u64(ctx, d_in, d_out, n + 1);
+    uint64_t total = 0;
+    HSAW_CUDA_CHECK(cudaMemcpyAsync(&total, d_out + n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    return total;
+}
+
+extern "C" {
+
+int hsaw_gpu_stream_histogram(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind,
+                              uint64_t off, uint64_t cnt, const uint32_t* cand_ids, uint64_t ncand,
+                              uint32_t* d_counts) {
+    if (!ctx || !stream || !d_counts) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        WalkView v = make_view(stream, nullptr, kind, off, cnt);
+        std::vector<uint32_t> cand_sorted;
+        (void)prepare_candidates(ctx, v.limit, cand_ids, ncand, cand_sorted, ctx->g_cand_bits);
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, (uint64_t)v.limit * 4, ctx->stream));
+        if (cnt) {
+            uint64_t p0 = 0, p1 = 0;
+            view_span(ctx, v, &p0, &p1);
+            histogram_counts(ctx, v, p0, p1, cand_ids ? ctx->g_cand_bits.p : nullptr, d_counts);
+        }
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        collect_timings(ctx);
+    });
+}
+
+// bins[c] = c * (#items with count c), counts >= kCountBins - 1 pooled in the last bin
+static std::vector<uint64_t> count_bins(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint32_t limit) {
+    ctx->g_partial.ensure_scratch(kCountBins + 4);
+    auto* d_bins = reinterpret_cast<unsigned long long*>(ctx->g_partial.p + 4);
+    HSAW_CUDA_CHECK(cudaMemsetAsync(d_bins, 0, kCountBins * 8, ctx->stream));
+    {
+        StageScope timer(ctx, HSAW_STAGE_INDEX);
+        count_of_counts<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(d_counts, limit, d_bins);
+        check_launch(ctx, "count_of_counts");
+    }
+    std::vector<uint64_t> bins(kCountBins);
+    HSAW_CUDA_CHECK(cudaMemcpyAsync(bins.data(), d_bins, kCountBins * 8, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    collect_timings(ctx);
+    return bins;
+}
+
+int hsaw_gpu_counts_bound(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint32_t limit, uint32_t k,
+                          uint64_t cap, uint64_t* bound) {
+    if (!ctx || !d_counts || !bound) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        const std::vector<uint64_t> bins = count_bins(ctx, d_counts, limit);
+        uint64_t total = bins[kCountBins - 1], left = k;  // as hsaw_gpu_coverage_upper_bound
+        for (uint32_t c = kCountBins - 2; c >= 1 && left > 0; --c) {
+            uint64_t items = bins[c] / c;
+            uint64_t take = std::min(items, left);
+            total += take * c;
+            left -= take;
+        }
+        *bound = std::min<uint64_t>(total, cap);
+    });
+}
+
+int hsaw_gpu_counts_threshold(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint32_t limit,
+                              uint32_t* min_count) {
+    if (!ctx || !d_counts || !min_count) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        const std::vector<uint64_t> bins = count_bins(ctx, d_counts, limit);
+        uint64_t total = 0;
+        for (uint64_t b : bins) total += b;
+        uint32_t mc = 1;  // the rule of hsaw_gpu_greedy: index at most 1/8 of all occurrences
+        if (total > (1ull << 20)) {
+            uint64_t above = 0;
+            mc = kCountBins - 1;
+            for (uint32_t c = kCountBins - 1; c >= 1; --c) {
+                if (above + bins[c] > total / 8) break;
+                above += bins[c];
+                mc = c;
+            }
+        }
+        *min_count = mc;
+    });
+}
+
+int hsaw_gpu_reduced_walks(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind, uint64_t off,
+                           uint64_t cnt, const uint32_t* d_counts, uint32_t min_count,
+                           hsaw_gpu_walkset** out, uint64_t* nsets, uint64_t* nitems) {
+    if (!ctx || !stream || !d_counts || !out) return HSAW_EINVAL;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        WalkView v = make_view(stream, nullptr, kind, off, cnt);
+        cudaStream_t st = ctx->stream;
+        const uint32_t limit = v.limit;
+        auto w = std::make_unique<hsaw_gpu_walkset>();
+        w->ctx = ctx;
+        w->limit = limit;
+        DevVec<uint32_t> wcount, flag, widx32;
+        DevVec<uint64_t> ioff, widx;
+        wcount.ensure_scratch(cnt + 1);
+        flag.ensure_scratch(cnt + 1);
+        ioff.ensure_scratch(cnt + 2);
+        widx.ensure_scratch(cnt + 2);
+        widx32.ensure_scratch(cnt + 1);
+        uint64_t kept = 0, total = 0;
+        if (cnt) {
+            DevVec<uint32_t>& d_ibits = ctx->g_indexed_bits;
+            const uint64_t words = ((uint64_t)limit + 31) / 32;
+            d_ibits.ensure_scratch(words + 1);
+            const BitFilter filt = prepare_filter(ctx, limit, (uint64_t)1 << 24);
+            const int wide = ctx->sm_count * 8;
+            const int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
+            {
+                StageScope timer(ctx, HSAW_STAGE_INDEX);
+                mark_indexed<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(
+                    d_counts, limit, min_count ? min_count : 1u, d_ibits.p,
+                    const_cast<uint32_t*>(filt.bits), filt.log2);
+                check_launch(ctx, "mark_indexed");
+                HSAW_CUDA_CHECK(cudaMemsetAsync(wcount.p + cnt, 0, 4, st));
+                reduced_count<<<sb, 256, 0, st>>>(v, d_ibits.p, filt, wcount.p);
+                check_launch(ctx, "reduced_count");
+                reduced_flags<<<(unsigned)((cnt + 256) / 256), 256, 0, st>>>(wcount.p, cnt, flag.p);
+                check_launch(ctx, "reduced_flags");
+            }
+            total = scan_total_u32(ctx, wcount.p, ioff.p, cnt);
+            kept = scan_total_u32(ctx, flag.p, widx.p, cnt);
+            // 32-bit copy of the walk ranks for the write kernel (kept < 2^32: walk ids are u32)
+            w->off.ensure_scratch(kept + 1);
+            w->items.ensure_scratch(total + 1);
+            DevVec<uint32_t> lens;
+            lens.ensure_scratch(kept + 1);
+            exclusive_sum_u32(ctx, flag.p, widx32.p, cnt + 1);
+            {
+                StageScope timer(ctx, HSAW_STAGE_INDEX);
+                reduced_write<<<sb, 256, 0, st>>>(v, d_ibits.p, filt, wcount.p, widx32.p, ioff.p,
+                                                  lens.p, w->items.p);
+                check_launch(ctx, "reduced_write");
+            }
+            HSAW_CUDA_CHECK(cudaMemsetAsync(lens.p + kept, 0, 4, st));
+            exclusive_sum_u32_to_u64(ctx, lens.p, w->off.p, kept + 1);
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        } else {
+            w->off.ensure_scratch(1);
+            HSAW_CUDA_CHECK(cudaMemsetAsync(w->off.p, 0, 8, st));
+            w->items.ensure_scratch(1);
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+        collect_timings(ctx);
+        w->nsets = kept;
+        w->nitems = total;
+        if (nsets) *nsets = kept;
+        if (nitems) *nitems = total;
+        *out = w.release();
+    });
+}
+
+// device-to-device: per-set lengths (u32[nsets]) and the items of a walk set into caller buffers
+int hsaw_gpu_walkset_copy_device(const hsaw_gpu_walkset* w, uint32_t* d_lens, uint32_t* d_items) {
+    if (!w) return HSAW_EINVAL;
+    return guarded(w->ctx, [&] {
+        cudaStream_t st = w->ctx->stream;
+        if (d_lens && w->nsets) {
+            offsets_to_lens<<<(unsigned)((w->nsets + 255) / 256), 256, 0, st>>>(w->off.p, w->nsets, d_lens);
+            check_launch(w->ctx, "offsets_to_lens");
+        }
+        if (d_items && w->nitems)
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(d_items, w->items.p, w->nitems * 4,
+                                            cudaMemcpyDeviceToDevice, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+// a walk set from device-resident per-set lengths and concatenated items (the all-gathered pieces)
+int hsaw_gpu_walkset_from_device(hsaw_gpu_ctx* ctx, uint32_t limit, uint64_t nsets,
+                                 const uint32_t* d_lens, const uint32_t* d_items, uint64_t nitems,
+                                 hsaw_gpu_walkset** out) {
+    if (!ctx || !out) return HSAW_EINVAL;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        if (nsets > 0xFFFFFFFFull) fail(HSAW_EINVAL, "walkset_from_device: more than 2^32 sets");
+        if ((nsets && !d_lens) || (nitems && !d_items)) fail(HSAW_EINVAL, "walkset_from_device: null array");
+        auto w = std::make_unique<hsaw_gpu_walkset>();
+        w->ctx = ctx;
+        w->limit = limit;
+        w->nsets = nsets;
+        w->nitems = nitems;
+        w->off.ensure_scratch(nsets + 1);
+        w->items.ensure_scratch(nitems + 1);
+        cudaStream_t st = ctx->stream;
+        if (nsets) {
+            DevVec<uint32_t> lens;
+            lens.ensure_scratch(nsets + 1);
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(lens.p, d_lens, nsets * 4, cudaMemcpyDeviceToDevice, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(lens.p + nsets, 0, 4, st));
+            exclusive_sum_u32_to_u64(ctx, lens.p, w->off.p, nsets + 1);
+            uint64_t total = 0;
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(&total, w->off.p + nsets, 8, cudaMemcpyDeviceToHost, st));
+            HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+            if (total != nitems) fail(HSAW_EINVAL, "walkset_from_device: lengths do not add up to nitems");
+        } else {
+            HSAW_CUDA_CHECK(cudaMemsetAsync(w->off.p, 0, 8, st));
+        }
+        if (nitems)
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(w->items.p, d_items, nitems * 4, cudaMemcpyDeviceToDevice, st));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+        *out = w.release();
+    });
+}
+
+uint64_t hsaw_gpu_last_greedy_min_gain(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->last_greedy_min_gain : 0; }
 
 }  // extern "C"

@@ -184,6 +184,70 @@ class GpuEngine:
         return self.ctx.coverage_upper_bound(k, stream=self.stream, kind=kind, off=off, cnt=cnt,
                                              cand=cand)
 
+    # -- building blocks of the gather-and-replicate greedy (hsaw_gpu.h, "sharded solve")
+    def local_counts(self, kind, off, cnt, cand) -> torch.Tensor:
+        """Occurrences of every candidate item in local walks [off, off+cnt): int32[limit], device."""
+        counts = torch.zeros(self.limit(kind), dtype=torch.int32, device=self.device)
+        torch.cuda.current_stream().synchronize()
+        ca = None if cand is None else np.ascontiguousarray(cand, dtype=np.uint32)
+        self.ctx._chk(self.capi.lib().hsaw_gpu_stream_histogram(
+            self.ctx.h, self.stream.h, kind, off, cnt, self.capi._p(ca, self.capi.u32p),
+            0 if ca is None else ca.size, counts.data_ptr()))
+        return counts
+
+    def bound_from_counts(self, counts: torch.Tensor, k: int, cap: int) -> int:
+        out = self.capi.C.c_uint64()
+        torch.cuda.current_stream().synchronize()
+        self.ctx._chk(self.capi.lib().hsaw_gpu_counts_bound(self.ctx.h, counts.data_ptr(),
+                                                            counts.numel(), k, cap,
+                                                            self.capi.C.byref(out)))
+        return out.value
+
+    def threshold_from_counts(self, counts: torch.Tensor) -> int:
+        out = self.capi.C.c_uint32()
+        torch.cuda.current_stream().synchronize()
+        self.ctx._chk(self.capi.lib().hsaw_gpu_counts_threshold(self.ctx.h, counts.data_ptr(),
+                                                                counts.numel(),
+                                                                self.capi.C.byref(out)))
+        return out.value
+
+    def reduced_walks(self, kind, off, cnt, counts: torch.Tensor, min_count: int):
+        """Local walks restricted to items with global count >= min_count -> (lens int32[w'],
+        items int32[...]) device tensors; walks left empty are dropped."""
+        C = self.capi.C
+        h, ns, ni = C.c_void_p(), C.c_uint64(), C.c_uint64()
+        torch.cuda.current_stream().synchronize()
+        self.ctx._chk(self.capi.lib().hsaw_gpu_reduced_walks(
+            self.ctx.h, self.stream.h, kind, off, cnt, counts.data_ptr(), min_count, C.byref(h),
+            C.byref(ns), C.byref(ni)))
+        try:
+            lens = torch.empty(ns.value, dtype=torch.int32, device=self.device)
+            items = torch.empty(ni.value, dtype=torch.int32, device=self.device)
+            torch.cuda.current_stream().synchronize()
+            self.ctx._chk(self.capi.lib().hsaw_gpu_walkset_copy_device(
+                h, lens.data_ptr() if ns.value else None, items.data_ptr() if ni.value else None))
+        finally:
+            self.capi.lib().hsaw_gpu_walkset_destroy(h)
+        return lens, items
+
+    def greedy_on_sets(self, kind, lens: torch.Tensor, items: torch.Tensor, k: int, cand):
+        """The single-GPU greedy (tail kernel and all) on gathered sets -> (solution, coverage,
+        smallest per-round gain; 0 if the gains ran out)."""
+        C = self.capi.C
+        h = C.c_void_p()
+        lens, items = lens.contiguous(), items.contiguous()
+        torch.cuda.current_stream().synchronize()
+        self.ctx._chk(self.capi.lib().hsaw_gpu_walkset_from_device(
+            self.ctx.h, self.limit(kind), lens.numel(), lens.data_ptr() if lens.numel() else None,
+            items.data_ptr() if items.numel() else None, items.numel(), C.byref(h)))
+        ws = self.capi.WalkSet.adopt(self.ctx, h, lens.numel(), items.numel())
+        try:
+            sol, cov = self.ctx.greedy(k, walkset=ws, kind=kind, cand=cand)
+            min_gain = int(self.capi.lib().hsaw_gpu_last_greedy_min_gain(self.ctx.h))
+        finally:
+            ws.close()
+        return [int(x) for x in sol], int(cov), min_gain
+
     def paired_runs(self, kind, ids, state0, first_run, nruns, draws_per_run):
         """Runs [first_run, first_run + nruns) of the simulation stream that starts at state0."""
         if nruns == 0:
@@ -294,10 +358,15 @@ class ShardedSolver:
 
     def coverage_upper_bound(self, k, kind, off, cnt, cand=None) -> int:
         """Upper bound of coverage_of over every k candidates on global walks [off, off+cnt): the
-        sum over ranks of the local bounds (each rank's k most frequent items bound its share of
-        any k-set). Engines without the primitive report 'no bound' (cnt)."""
-        fn = getattr(self.eng, "coverage_upper_bound", None)
+        counts of all ranks are all-reduced first, so the bound is exactly the single-GPU one (the
+        sum of the k largest global counts) and the same iterations are skipped for every world
+        size. Engines without the primitives fall back to the (looser) sum of local bounds."""
         lo, n = self.layout.local_range(self.comm.rank, off, cnt)
+        if hasattr(self.eng, "local_counts"):
+            counts = self.eng.local_counts(kind, lo, n, cand)
+            self.comm.allreduce_sum_(counts)
+            return self.eng.bound_from_counts(counts, k, cnt)
+        fn = getattr(self.eng, "coverage_upper_bound", None)
         local = n if fn is None else fn(k, kind, lo, n, cand)
         t = torch.tensor([local], dtype=torch.int64)
         if self.comm.backend == "nccl":
@@ -317,6 +386,8 @@ class ShardedSolver:
         if k > ncand:
             raise HsawError(HSAW_EINVAL, "budget k exceeds candidate count")
         lo, n = self.layout.local_range(self.comm.rank, 0, size)
+        if hasattr(self.eng, "reduced_walks"):
+            return self._greedy_gathered(k, kind, lo, n, cand)
         rounds = self.eng.begin_rounds(kind, lo, n, cand)
         try:
             self.comm.allreduce_sum_(rounds.counts)  # local histograms -> global marginal gains
@@ -343,6 +414,25 @@ class ShardedSolver:
                 solution.append(cid)
                 chosen.add(cid)
         return solution, coverage
+
+    def _greedy_gathered(self, k, kind, lo, n, cand):
+        """One all-reduce of the local count vectors, one all-gather of the local walks restricted
+        to the items that can still win (global count >= the indexing threshold of the single-GPU
+        greedy), then the single-GPU greedy on the gathered sets, redundantly on every rank: same
+        selections everywhere, no per-round exchange. If the k-th gain falls below the threshold
+        the reduced instance was not enough: repeat with everything (threshold 1)."""
+        counts = self.eng.local_counts(kind, lo, n, cand)
+        self.comm.allreduce_sum_(counts)
+        min_count = self.eng.threshold_from_counts(counts)
+        while True:
+            lens, items = self.eng.reduced_walks(kind, lo, n, counts, min_count)
+            all_lens = self.comm.allgather_var(lens)
+            all_items = self.comm.allgather_var(items)
+            solution, coverage, min_gain = self.eng.greedy_on_sets(
+                kind, torch.cat(all_lens), torch.cat(all_items), k, cand)
+            if min_count <= 1 or min_gain >= min_count:
+                return solution, coverage
+            min_count = 1
 
     # -- run_interdiction (proj/src/interdiction.cpp:12-67), sharded
     # ---- estimate_suspension (proj/src/evaluation.cpp:209-242), runs sharded over the ranks -------

@@ -57,6 +57,82 @@ class CpuEngine:
             q &= set(int(c) for c in cand)
         return sum(1 for w in range(off, off + cnt) if q.intersection(self._items(kind, w).tolist()))
 
+    # -- building blocks of the gather-and-replicate greedy (mirrors sharded.GpuEngine)
+    K_BINS = 1024
+
+    def local_counts(self, kind, off, cnt, cand):
+        limit = self.limit(kind)
+        counts = np.zeros(limit, dtype=np.int64)
+        ok = np.ones(limit, dtype=bool)
+        if cand is not None:
+            ok[:] = False
+            ok[np.asarray(cand, dtype=np.int64)] = True
+        for w in range(off, off + cnt):
+            it = self._items(kind, w).astype(np.int64)
+            np.add.at(counts, it[ok[it]], 1)
+        return torch.from_numpy(counts.astype(np.int32))
+
+    def _bins(self, counts):
+        c = counts.numpy().astype(np.int64)
+        c = c[c > 0]
+        bins = np.zeros(self.K_BINS, dtype=np.int64)
+        np.add.at(bins, np.minimum(c, self.K_BINS - 1), c)
+        return bins
+
+    def bound_from_counts(self, counts, k, cap):
+        bins = self._bins(counts)
+        total, left = int(bins[self.K_BINS - 1]), k
+        for c in range(self.K_BINS - 2, 0, -1):
+            if left <= 0:
+                break
+            take = min(int(bins[c]) // c, left)
+            total += take * c
+            left -= take
+        return min(total, cap)
+
+    def threshold_from_counts(self, counts):
+        bins = self._bins(counts)
+        total = int(bins.sum())
+        if total <= (1 << 20):
+            return 1
+        above, mc = 0, self.K_BINS - 1
+        for c in range(self.K_BINS - 1, 0, -1):
+            if above + int(bins[c]) > total // 8:
+                break
+            above += int(bins[c])
+            mc = c
+        return mc
+
+    def reduced_walks(self, kind, off, cnt, counts, min_count):
+        c = counts.numpy()
+        lens, items = [], []
+        for w in range(off, off + cnt):
+            it = self._items(kind, w)
+            keep = it[(c[it] >= max(min_count, 1)) & (c[it] > 0)]
+            if keep.size:
+                lens.append(keep.size)
+                items.append(keep.astype(np.int32))
+        cat = np.concatenate(items) if items else np.zeros(0, dtype=np.int32)
+        return torch.tensor(lens, dtype=torch.int32), torch.from_numpy(cat)
+
+    def greedy_on_sets(self, kind, lens, items, k, cand):
+        limit = self.limit(kind)
+        off = np.zeros(lens.numel() + 1, dtype=np.uint64)
+        np.cumsum(lens.numpy().astype(np.uint64), out=off[1:])
+        it = items.numpy().astype(np.uint32)
+        sol, cov = self.port.greedy(limit, off, it, k, cand=cand)
+        # per-round gains by replay (the oracle only returns their sum)
+        sets = [set(it[int(off[i]):int(off[i + 1])].tolist()) for i in range(lens.numel())]
+        covered, gains = np.zeros(len(sets), dtype=bool), []
+        for x in sol.tolist():
+            g = 0
+            for i, st in enumerate(sets):
+                if not covered[i] and x in st:
+                    covered[i] = True
+                    g += 1
+            gains.append(g)
+        return [int(x) for x in sol], int(cov), (min(gains) if gains else 0)
+
     class _Rounds:
         def __init__(self, eng, kind, off, cnt, cand):
             limit = eng.limit(kind)

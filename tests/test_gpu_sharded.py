@@ -152,3 +152,46 @@ def test_two_ranks_on_one_gpu_estimate_suspension():
     want = dict(value=float.fromhex(c["value"]), capped=c["capped"], runs=c["runs"],
                 state=c["state_after"])
     assert results[0] == results[1] == want
+
+
+def test_gathered_greedy_with_threshold_and_fallback(gpu_lib):
+    """The gather-and-replicate greedy of the sharded solve on an instance large enough for a
+    threshold above 1 (R-MAT 2^16, ~4e5 walks, > 2^20 items): the reduced walk set selects what the
+    single-GPU greedy selects, the sharded upper bound equals the single-GPU one, and a budget deep
+    into the low counts (k-th gain below the threshold) takes the full-gather fallback."""
+    import torch
+    from paper_1702_05854_b200 import hostapi
+    from paper_1702_05854_b200.sharded import GpuEngine, ShardedSolver
+    g = hostapi.Graph.rmat(16, 16.0, seed=1)
+    p_of = g.random_suspects(g.n // 100, seed=2)
+    with hostapi.DeviceGraph(g, p_of) as dg:
+        ctx = gpu_lib.Context.borrow(dg.ctx_handle(), g.n, g.m)
+        eng = GpuEngine(ctx, seed=42, cfg=gpu_lib.SamplerCfg(max_attempts=10**12))
+        try:
+            solver = ShardedSolver(eng)
+            solver.ensure(400_000)
+            for kind in (0, 1):
+                counts = eng.local_counts(kind, 0, 200_000, None)
+                mc = eng.threshold_from_counts(counts)
+                assert mc > 1
+                lens, items = eng.reduced_walks(kind, 0, 200_000, counts, mc)
+                c = counts.cpu().numpy()
+                it = items.cpu().numpy()
+                assert lens.sum().item() == items.numel() and np.all(c[it] >= mc)
+                assert items.numel() == int(c[c >= mc].sum())  # every occurrence of an indexed item
+                for k in (30, 3000):
+                    exp_sol, exp_cov = ctx.greedy(k, stream=eng.stream, kind=kind, off=0, cnt=200_000)
+                    sol, cov = solver.greedy(k, kind, 200_000)
+                    assert sol == exp_sol.tolist() and cov == exp_cov
+                exp_b = ctx.coverage_upper_bound(100, stream=eng.stream, kind=kind, off=200_000,
+                                                 cnt=200_000)
+                assert solver.coverage_upper_bound(100, kind, 200_000, 200_000) == exp_b
+        finally:
+            eng.close()
+        res = hostapi.interdict(g, p_of, 0, 50, 0.1, 1.0 / g.n, seed=42, max_attempts=10**12, dg=dg)
+        eng = GpuEngine(ctx, seed=42, cfg=gpu_lib.SamplerCfg(max_attempts=10**12))
+        try:
+            got = ShardedSolver(eng).interdict(g.n, 0, 50, 0.1, 1.0 / g.n)
+        finally:
+            eng.close()
+        assert got == res
