@@ -346,6 +346,13 @@ int hsaw_gpu_walkset_from_device(hsaw_gpu_ctx* ctx, uint32_t limit, uint64_t nse
                                  const uint32_t* d_lens, const uint32_t* d_items, uint64_t nitems,
                                  hsaw_gpu_walkset** out);
 uint64_t hsaw_gpu_last_greedy_min_gain(const hsaw_gpu_ctx* ctx);
+/* Device-buffer plumbing for a host that drives several contexts from one process (the C++
+ * multi-device solve, host/multi.cpp): allocation on the context's device, copies between any two
+ * device pointers (also across devices), and dst[i] += src[i] over u32 counters. */
+int hsaw_gpu_device_alloc(hsaw_gpu_ctx* ctx, uint64_t bytes, void** out);
+void hsaw_gpu_device_free(hsaw_gpu_ctx* ctx, void* p);
+int hsaw_gpu_device_copy(hsaw_gpu_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int hsaw_gpu_counts_add(hsaw_gpu_ctx* ctx, uint32_t* d_dst, const uint32_t* d_src, uint64_t n);
 
 /* ---- stepwise greedy for sharded (multi-GPU) solves ---------------------------------------- */
 

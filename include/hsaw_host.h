@@ -133,6 +133,18 @@ int hsawh_estimate_suspension(const void* dg, const void* g, const double* p_of,
                               uint64_t* state, double* value, int* capped, uint64_t* runs);
 
 /* ---- CLI (proj/include/hsaw/cli.hpp) ---- */
+/* esia / nsia with InterdictionOptions::devices: the multi-device solve of the C++ host layer
+ * (graph replicated per device, walks sharded by batch range, NCCL all-reduce of the marginal-gain
+ * counts; a repeated device id selects the in-process exchange). Same result for every list. */
+int hsawh_interdict_devices(const void* g, const double* p_of, int kind, const uint32_t* cand,
+                            uint64_t ncand, uint32_t k, double eps, double delta, uint64_t seed,
+                            uint64_t max_attempts, const int* devices, uint32_t ndevices,
+                            hsawh_result* out, uint32_t* solution);
+
+/* Transport the multi-device solve would use for a device list: "nccl" (distinct devices,
+ * libnccl.so.2 resolvable), "in-process exchange" (a repeated id) or "single device". */
+void hsawh_multi_transport(const int* devices, uint32_t ndevices, char* out, uint64_t cap);
+
 /* ---- partitioned sampling — proj/include/hsaw/partition.hpp:27-54 ---- */
 /* partition_graph (method 0 Hash, 1 LabelProp, 2 ExternalFile with part_file) followed by
  * extend_partition(hops): assign_out u32[n], extended_out u8[p * n] part-major (nullable). */

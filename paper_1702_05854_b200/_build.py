@@ -82,11 +82,11 @@ def build_host(force: bool = False) -> str | None:
     if not cpps:
         return None
     headers = _sources(HOST, (".hpp", ".h")) + [os.path.join(ROOT, "include", "hsaw_gpu.h")]
-    flags = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
-             "-I", HOST]
+    flags = ["-std=c++20", "-O2", "-fPIC", "-pthread", "-Wall", "-Wextra", "-I",
+             os.path.join(ROOT, "include"), "-I", HOST]
     if force or not _newer(HOST_SO, cpps + headers + [GPU_SO]):
         subprocess.check_call([CXX, *flags, "-shared", "-o", HOST_SO, *cpps, "-L", LIB,
-                               "-lhsaw_gpu", "-Wl,-rpath,$ORIGIN"])
+                               "-lhsaw_gpu", "-ldl", "-pthread", "-Wl,-rpath,$ORIGIN"])
     mains = [c for c in _sources(HOST, (".cpp",)) if c.endswith("_main.cpp")]
     if mains and (force or not _newer(CLI, mains + headers + [HOST_SO])):
         os.makedirs(BIN, exist_ok=True)

@@ -179,7 +179,8 @@ EXPORTS = (
     "hsaw_gpu_rr_node_sets", "hsaw_gpu_walkset_export",
     "hsaw_gpu_stream_histogram", "hsaw_gpu_counts_bound", "hsaw_gpu_counts_threshold",
     "hsaw_gpu_reduced_walks", "hsaw_gpu_walkset_copy_device", "hsaw_gpu_walkset_from_device",
-    "hsaw_gpu_last_greedy_min_gain",
+    "hsaw_gpu_last_greedy_min_gain", "hsaw_gpu_device_alloc", "hsaw_gpu_device_free",
+    "hsaw_gpu_device_copy", "hsaw_gpu_counts_add",
 )
 
 

@@ -1718,4 +1718,38 @@ int hsaw_gpu_walkset_from_device(hsaw_gpu_ctx* ctx, uint32_t limit, uint64_t nse
 
 uint64_t hsaw_gpu_last_greedy_min_gain(const hsaw_gpu_ctx* ctx) { return ctx ? ctx->last_greedy_min_gain : 0; }
 
+// Plumbing for a host that drives several contexts from one process without its own CUDA code
+// (host/multi.cpp): device buffers, copies between any two device pointers (unified addressing;
+// across devices the driver goes peer-to-peer or through the host) and the element-wise sum the
+// in-process all-reduce is made of. With distinct devices the host layer uses NCCL instead.
+int hsaw_gpu_device_alloc(hsaw_gpu_ctx* ctx, uint64_t bytes, void** out) {
+    if (!ctx || !out) return HSAW_EINVAL;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        *out = pool_alloc(bytes ? bytes : 1, ctx->stream);
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+void hsaw_gpu_device_free(hsaw_gpu_ctx* ctx, void* p) {
+    if (!ctx || !p) return;
+    guarded(ctx, [&] { cudaFreeAsync(p, ctx->stream); });
+}
+int hsaw_gpu_device_copy(hsaw_gpu_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (bytes) HSAW_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int hsaw_gpu_counts_add(hsaw_gpu_ctx* ctx, uint32_t* d_dst, const uint32_t* d_src, uint64_t n) {
+    if (!ctx) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        if (n) {
+            add_counts<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(d_dst, d_src, n);
+            check_launch(ctx, "add_counts");
+        }
+        HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 }  // extern "C"

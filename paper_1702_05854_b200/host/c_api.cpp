@@ -485,6 +485,42 @@ int hsawh_rr_node_sets(const void* dg, uint64_t* state, uint32_t count, uint64_t
     });
 }
 
+int hsawh_interdict_devices(const void* g, const double* p_of, int kind, const uint32_t* cand,
+                            uint64_t ncand, uint32_t k, double eps, double delta, uint64_t seed,
+                            uint64_t max_attempts, const int* devices, uint32_t ndevices,
+                            hsawh_result* out, uint32_t* solution) {
+    return guarded([&] {
+        const ItemKind ik = kind == 0 ? ItemKind::Edge : ItemKind::Node;
+        CandidateSet cs = cand ? CandidateSet::of(ik, std::vector<std::uint32_t>(cand, cand + ncand))
+                               : CandidateSet::all(ik);
+        InterdictionOptions opts;
+        opts.seed = seed;
+        opts.sampler.max_attempts = max_attempts;
+        opts.devices.assign(devices, devices + ndevices);
+        SuspectSet vi = dense_suspects(G(g), p_of);
+        InterdictionResult r = kind == 0 ? esia(G(g), vi, cs, k, eps, delta, opts)
+                                         : nsia(G(g), vi, cs, k, eps, delta, opts);
+        out->k = r.k;
+        out->iterations = r.iterations;
+        out->coverage = r.coverage;
+        out->samples_used = r.samples_used;
+        out->attempts = r.attempts;
+        out->est_suspension = r.est_suspension;
+        out->wall_time_s = r.wall_time_s;
+        out->sample_s = r.sample_s;
+        out->greedy_s = r.greedy_s;
+        out->check_s = r.check_s;
+        out->passed_check = r.passed_check ? 1 : 0;
+        std::memcpy(solution, r.solution.data(), 4 * r.solution.size());
+    });
+}
+
+void hsawh_multi_transport(const int* devices, uint32_t ndevices, char* out, uint64_t cap) {
+    const std::string s = multi_device_transport(std::vector<int>(devices, devices + ndevices));
+    std::strncpy(out, s.c_str(), cap - 1);
+    out[cap - 1] = 0;
+}
+
 void hsawh_json_number(double x, char* out, uint64_t cap) {
     const std::string s = json_number(x);
     std::strncpy(out, s.c_str(), cap - 1);

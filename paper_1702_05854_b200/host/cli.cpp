@@ -208,6 +208,18 @@ int cmd_interdict(const Flags& f) {  // cli.cpp:138-160
     opts.seed = seed;
     opts.sampler.max_attempts = f.u64("max-attempts", 100'000'000);
     opts.device = static_cast<int>(f.u64("device", 0));
+    // --gpus N: devices 0..N-1 (graph replicated, walks sharded, NCCL); --devices a,b,c: an explicit
+    // list (a repeated id runs the same path over the in-process exchange: one-GPU boxes)
+    if (f.has("devices")) {
+        std::stringstream ss(f.str("devices"));
+        std::string tok;
+        while (std::getline(ss, tok, ',')) opts.devices.push_back(std::stoi(tok));
+    } else if (f.u64("gpus", 1) > 1) {
+        for (std::uint64_t d = 0; d < f.u64("gpus", 1); ++d) opts.devices.push_back(static_cast<int>(d));
+    }
+    if (opts.devices.size() > 1)
+        std::cerr << "hsaw: multi-device solve over " << opts.devices.size() << " devices, transport: "
+                  << multi_device_transport(opts.devices) << '\n';
     const double eps = f.real("epsilon", 0.1), delta = f.real("delta", 0.1);
     InterdictionResult res = kind == ItemKind::Edge
                                  ? esia(g, vi, cand, static_cast<std::uint32_t>(k), eps, delta, opts)
@@ -465,7 +477,7 @@ int run_cli(std::vector<std::string> args) {
             return cmd_interdict(parse_flags(
                 args, 1,
                 with(kGraphFlags, {"mode", "k", "epsilon", "delta", "candidates", "workers", "seed",
-                                   "max-attempts", "output", "device"}),
+                                   "max-attempts", "output", "device", "gpus", "devices"}),
                 {"symmetrize", "omit-timing"}));
         if (cmd == "sample")
             return cmd_sample(parse_flags(

@@ -450,7 +450,21 @@ struct InterdictionOptions {
     std::uint64_t seed = 0;
     SamplerConfig sampler;
     int device = 0;
+    // More than one entry: the multi-device solve (host/multi.cpp) — the graph is replicated on
+    // every listed device, each round's batch range is split into contiguous blocks (one per
+    // device), marginal-gain counts are combined with an all-reduce (NCCL over NVLink when the
+    // devices are distinct; an in-process exchange when a device id repeats, which is how the
+    // path is tested on a single GPU). Same InterdictionResult for every device list.
+    std::vector<int> devices;
 };
+
+// The multi-device doubling loop behind esia / nsia when opts.devices lists more than one device
+// (host/multi.cpp), and the transport it would use for a device list ("nccl", "in-process
+// exchange", "single device").
+InterdictionResult run_interdiction_multi(const ProbGraph& g, const SuspectSet& vi,
+                                          const CandidateSet& cand, std::uint32_t k, double epsilon,
+                                          double delta, const InterdictionOptions& opts);
+std::string multi_device_transport(const std::vector<int>& devices);
 
 InterdictionResult esia(const ProbGraph& g, const SuspectSet& vi, const CandidateSet& cand,
                         std::uint32_t k, double epsilon, double delta,

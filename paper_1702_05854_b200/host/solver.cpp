@@ -184,8 +184,9 @@ InterdictionResult esia(const ProbGraph& g, const SuspectSet& vi, const Candidat
                         std::uint32_t k, double epsilon, double delta,
                         const InterdictionOptions& opts) {
     require_kind(cand, ItemKind::Edge, "esia requires an edge candidate set");
+    if (opts.devices.size() > 1) return run_interdiction_multi(g, vi, cand, k, epsilon, delta, opts);
     const auto t0 = Clock::now();
-    DeviceGraph dg(g, vi, opts.device);
+    DeviceGraph dg(g, vi, opts.devices.size() == 1 ? opts.devices[0] : opts.device);
     InterdictionResult res = run_on_device(dg, g, cand, k, epsilon, delta, opts);
     res.wall_time_s = seconds_since(t0);  // upload included, like a host-to-result call
     return res;
@@ -195,8 +196,9 @@ InterdictionResult nsia(const ProbGraph& g, const SuspectSet& vi, const Candidat
                         std::uint32_t k, double epsilon, double delta,
                         const InterdictionOptions& opts) {
     require_kind(cand, ItemKind::Node, "nsia requires a node candidate set");
+    if (opts.devices.size() > 1) return run_interdiction_multi(g, vi, cand, k, epsilon, delta, opts);
     const auto t0 = Clock::now();
-    DeviceGraph dg(g, vi, opts.device);
+    DeviceGraph dg(g, vi, opts.devices.size() == 1 ? opts.devices[0] : opts.device);
     InterdictionResult res = run_on_device(dg, g, cand, k, epsilon, delta, opts);
     res.wall_time_s = seconds_since(t0);
     return res;

@@ -78,6 +78,11 @@ def lib() -> C.CDLL:
     L.hsawh_interdict_rng.argtypes = [vp, vp, f64p, C.c_int, u32p, C.c_uint64, C.c_uint32, C.c_double,
                                       C.c_double, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int,
                                       C.c_int, C.POINTER(Result), u32p, C.c_char_p, C.c_uint64]
+    L.hsawh_interdict_devices.argtypes = [vp, f64p, C.c_int, u32p, C.c_uint64, C.c_uint32, C.c_double,
+                                          C.c_double, C.c_uint64, C.c_uint64, C.POINTER(C.c_int),
+                                          C.c_uint32, C.POINTER(Result), u32p]
+    L.hsawh_multi_transport.argtypes = [C.POINTER(C.c_int), C.c_uint32, C.c_char_p, C.c_uint64]
+    L.hsawh_multi_transport.restype = None
     L.hsawh_sample.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p]
     L.hsawh_graph_load_edge_list_device.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int,
                                                     C.c_char_p, C.c_int, vpp]
@@ -380,6 +385,30 @@ def interdict(graph: Graph, p_of, kind, k, eps, delta, seed=0, cand=None, batch_
         out["timing"] = dict(wall_time_s=res.wall_time_s, sample_s=res.sample_s,
                              greedy_s=res.greedy_s, check_s=res.check_s)
     return out
+
+
+def multi_transport(devices) -> str:
+    dev = (C.c_int * len(devices))(*devices)
+    buf = C.create_string_buffer(128)
+    lib().hsawh_multi_transport(dev, len(devices), buf, len(buf))
+    return buf.value.decode()
+
+
+def interdict_devices(graph: Graph, p_of, kind, k, eps, delta, devices, seed=0, cand=None,
+                      max_attempts=100_000_000) -> dict:
+    """esia / nsia with InterdictionOptions::devices (the C++ multi-device solve, host/multi.cpp)."""
+    p = np.ascontiguousarray(p_of, dtype=np.float64)
+    ca = None if cand is None else np.ascontiguousarray(cand, dtype=np.uint32)
+    dev = (C.c_int * len(devices))(*devices)
+    res = Result()
+    sol = np.zeros(max(k, 1), dtype=np.uint32)
+    _chk(lib().hsawh_interdict_devices(graph.h, _p(p, f64p), kind, _p(ca, u32p),
+                                       0 if ca is None else ca.size, k, eps, delta, seed,
+                                       max_attempts, dev, len(devices), C.byref(res), _p(sol, u32p)))
+    return dict(kind="edge" if kind == 0 else "node", k=res.k, epsilon=eps, delta=delta,
+                solution=[int(x) for x in sol[:k]], est_suspension=res.est_suspension,
+                coverage=res.coverage, samples_used=res.samples_used, attempts=res.attempts,
+                iterations=res.iterations, passed_check=bool(res.passed_check))
 
 
 def lt_forward_simulate(graph: Graph, p_of, state, dg: DeviceGraph | None = None):

@@ -195,3 +195,46 @@ def test_gathered_greedy_with_threshold_and_fallback(gpu_lib):
         finally:
             eng.close()
         assert got == res
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
+def test_cpp_multi_device_solve_equals_single_device(golden, synth3000, devices):
+    """The C++ multi-device solve (host/multi.cpp, InterdictionOptions::devices) with 2 and 3 ranks
+    sharing cuda:0: rank threads, sharded ensure / counters / coverage / bound, gather-and-replicate
+    greedy over the in-process exchange — the reference's golden results, bit for bit."""
+    from paper_1702_05854_b200 import hostapi
+    g = hostapi.Graph.from_csr(synth3000.n, synth3000.m, synth3000.in_offsets, synth3000.in_src,
+                               synth3000.in_cum)
+    for kind, key in ((0, "esia_k5"), (1, "nsia_k5")):
+        res = hostapi.interdict_devices(g, synth3000.p_of, kind, 5, 0.2, 0.1, devices, seed=3)
+        assert res == golden["synth3000"][key]
+
+
+def test_cpp_multi_device_solve_at_scale_16(tmp_path):
+    """A larger instance (threshold > 1 in the gathered greedy, several sampling rounds) and the
+    CLI flag: `hsaw interdict --devices 0,0` prints the single-device document."""
+    import json
+    from paper_1702_05854_b200 import hostapi
+    g = hostapi.Graph.rmat(16, 16.0, seed=1)
+    p_of = g.random_suspects(g.n // 100, seed=2)
+    one = hostapi.interdict(g, p_of, 0, 50, 0.1, 1.0 / g.n, seed=42, max_attempts=10**12)
+    two = hostapi.interdict_devices(g, p_of, 0, 50, 0.1, 1.0 / g.n, [0, 0], seed=42,
+                                    max_attempts=10**12)
+    assert two == one
+    n1 = hostapi.interdict(g, p_of, 1, 20, 0.1, 1.0 / g.n, seed=7, max_attempts=10**12)
+    n3 = hostapi.interdict_devices(g, p_of, 1, 20, 0.1, 1.0 / g.n, [0, 0, 0], seed=7,
+                                   max_attempts=10**12)
+    assert n3 == n1
+    cache, sus = tmp_path / "g.hsaw1", tmp_path / "s.txt"
+    small = hostapi.Graph.synth(2000, 6, 3)
+    small.save_cache(cache)
+    sp = small.random_suspects(40, 2)
+    sus.write_text("".join(f"{v} {float(sp[v])!r}\n" for v in np.nonzero(sp)[0]))
+    outs = []
+    for extra in ([], ["--devices", "0,0"]):
+        out = tmp_path / f"o{len(outs)}.json"
+        rc = hostapi.run_cli(["interdict", "--graph", str(cache), "--suspects", str(sus), "--k", "4",
+                              "--seed", "5", "--omit-timing", "--output", str(out)] + extra)
+        assert rc == 0
+        outs.append(json.loads(out.read_text()))
+    assert outs[0] == outs[1]

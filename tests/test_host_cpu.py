@@ -297,3 +297,13 @@ def test_rmat_n_generalises_rmat(host):
     assert np.array_equal(host.random_suspects_n(3000, 30, 2), g.random_suspects(30, 2))
     shell = host.Graph.shell(5, 7)
     assert (shell.n, shell.m) == (5, 7)
+
+
+def test_multi_device_transport_selection(host):
+    """host/multi.cpp: distinct devices go over NCCL (libnccl.so.2 is resolved at run time, all the
+    entry points the solve calls are present), a repeated device id selects the in-process
+    exchange (NCCL refuses duplicate devices), one device is the single-device path."""
+    assert host.multi_transport([0, 1]) == "nccl"
+    assert host.multi_transport([0, 1, 2, 3, 4, 5, 6, 7]) == "nccl"
+    assert host.multi_transport([0, 0]) == "in-process exchange"
+    assert host.multi_transport([3]) == "single device"
