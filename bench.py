@@ -391,6 +391,9 @@ def run_b200(args):
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
+        # the communicator set-up lines (NCCL INFO ... Init COMPLETE) go to stderr, beside the JSON
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if one_gpu:
             dist.init_process_group("gloo")
         else:
