@@ -43,7 +43,7 @@ typedef struct hsaw_gpu_walkset hsaw_gpu_walkset; /* fixed item sets (CoverageIn
 
 /* SamplerConfig, proj/include/hsaw/sampler.hpp:48-55. */
 typedef struct hsaw_sampler_cfg {
-    int32_t heuristic;     /* 0 Brent (default), 1 Floyd (not on device: HSAW_EINVAL), 2 None */
+    int32_t heuristic;     /* 0 Brent (default), 1 Floyd, 2 None (CycleHeuristic, sampler.hpp:46) */
     uint32_t window;       /* exact short-cycle window, 0..8 (default 2) */
     uint32_t batch_size;   /* attempts chained per batch / worker id (default 10) */
     uint64_t max_attempts; /* stream budget (default 100000000) */

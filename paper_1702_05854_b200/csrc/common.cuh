@@ -133,14 +133,32 @@ inline uint64_t size_class(uint64_t bytes) {
     return (bytes + step - 1) & ~(step - 1);
 }
 
-// cudaMallocAsync with one retry after handing the pool's cached blocks back to the driver (the
-// pool never releases memory on its own: release threshold "never").
+// The context whose C-ABI call this thread is serving (set by guarded()), and the last resort of a
+// failing allocation: a hook that drops that context's IDLE caches (the recycled walk-pool buffers
+// of finished streams: tens of gigabytes of mapped virtual memory at the Twitter shape, which no
+// pool trim can reach). Registered by graph.cu.
+inline hsaw_gpu_ctx*& current_ctx() {
+    static thread_local hsaw_gpu_ctx* c = nullptr;
+    return c;
+}
+using OomHook = void (*)(hsaw_gpu_ctx*);
+inline OomHook& oom_hook() {
+    static OomHook h = nullptr;
+    return h;
+}
+inline void run_oom_hook() {
+    if (oom_hook() && current_ctx()) oom_hook()(current_ctx());
+}
+
+// cudaMallocAsync with one retry after dropping idle caches and handing the pool's cached blocks
+// back to the driver (the pool never releases memory on its own: release threshold "never").
 inline void* pool_alloc(uint64_t bytes, cudaStream_t st) {
     void* np = nullptr;
     cudaError_t e = cudaMallocAsync(&np, bytes, st);
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
         cudaStreamSynchronize(st);
+        run_oom_hook();
         int dev = 0;
         cudaMemPool_t pool = nullptr;
         if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -365,9 +383,10 @@ struct GrowVec {
         CUmemGenericAllocationHandle h{};
         CUresult rc = api.create(&h, grow, &prop, 0);
         if (rc == CUDA_ERROR_OUT_OF_MEMORY) {
-            // physical memory may sit in the stream-ordered pool's cache: hand it back and retry
-            // with the exact need
+            // physical memory may sit in the stream-ordered pool's cache or in the idle walk-pool
+            // buffers of finished streams: hand it back and retry with the exact need
             cudaStreamSynchronize(st);
+            run_oom_hook();
             cudaMemPool_t pool = nullptr;
             if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
             grow = need - mapped_;
@@ -585,6 +604,15 @@ struct hsaw_gpu_ctx {
         f(g_indexed_bits); f(g_filter); f(g_hist_prefix); f(g_hist_seg);
     }
 
+    // The buffers a solve leaves behind (greedy index, histogram cache, partition copy): tens of
+    // gigabytes at the Twitter shape, worthless once another graph is installed. Back to the pool.
+    void release_solve_scratch() {
+        g_cand_bits.release(); g_cnt.release(); g_fill.release(); g_inv.release();
+        g_covered.release(); g_solution.release(); g_query_bits.release(); g_pos.release();
+        g_partial.release(); g_gains.release(); g_blkmax.release(); g_sorted.release();
+        g_indexed_bits.release(); g_filter.release(); g_hist_prefix.release(); g_hist_seg.release();
+    }
+
     void release_scratch() {
         g_nodes_store.release();
         g_edges_store.release();
@@ -624,6 +652,7 @@ int guarded(hsaw_gpu_ctx* ctx, F&& f) {
         if (ctx) {
             HSAW_CUDA_CHECK(cudaSetDevice(ctx->device));
             current_stream() = ctx->stream;
+            current_ctx() = ctx;
         }
         f();
         return HSAW_OK;

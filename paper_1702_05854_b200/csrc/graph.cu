@@ -618,6 +618,14 @@ Parked& parked() {
     return p;
 }
 
+// Allocation failure (common.cuh, run_oom_hook): the walk-pool buffers of finished streams are idle
+// by construction (a live stream owns its arrays; they come back here when it is destroyed).
+void release_idle_caches(hsaw_gpu_ctx* ctx) { ctx->pool_cache.release(); }
+const bool oom_hook_registered = [] {
+    oom_hook() = &release_idle_caches;
+    return true;
+}();
+
 void adopt_parked_buffers(hsaw_gpu_ctx* ctx) {
     Parked& pk = parked();
     std::lock_guard<std::mutex> lock(pk.mu);
@@ -729,6 +737,9 @@ void copy_to_host(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs) {
 // Chooses the layout for an (n, m) graph and points ctx->g at (re)allocated stores. Returns true
 // for the compact layout.
 bool prepare_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
+    // what an earlier solve left behind (adopted from a parked context, or this context's own) is
+    // sized for another graph: it goes back to the pool before the new stores are allocated
+    ctx->release_solve_scratch();
     const int layout = choose_layout(ctx, n, m);
     const bool compact = layout == kLayoutCompact;
     ctx->g_nodes_store.ensure_scratch(n);

@@ -774,6 +774,7 @@ struct HistCache {
     uint64_t prefix_end = 0;              // prefix[] = counts of walks [0, prefix_end)
     uint64_t seg_begin = 0, seg_end = 0;  // seg[] = counts of walks [seg_begin, seg_end), if seg_ok
     bool seg_ok = false;
+    const uint32_t *prefix_buf = nullptr, *seg_buf = nullptr;  // the buffers the state describes
 };
 static HistCache& hist_cache(hsaw_gpu_ctx* ctx) {
     static std::mutex mu;
@@ -816,10 +817,15 @@ static HistCache& hist_bind(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, in
     HistCache& hc = hist_cache(ctx);
     ctx->g_hist_prefix.ensure_scratch(limit + 4);
     ctx->g_hist_seg.ensure_scratch(limit + 4);
-    if (hc.stream_uid != stream->uid || hc.kind != kind) {
+    // (the buffers are scratch of the context: a graph install or an allocation failure may have
+    // released them since the state was recorded)
+    if (hc.stream_uid != stream->uid || hc.kind != kind || hc.prefix_buf != ctx->g_hist_prefix.p ||
+        hc.seg_buf != ctx->g_hist_seg.p) {
         hc = HistCache{};
         hc.stream_uid = stream->uid;
         hc.kind = kind;
+        hc.prefix_buf = ctx->g_hist_prefix.p;
+        hc.seg_buf = ctx->g_hist_seg.p;
     }
     if (hc.prefix_end == 0)
         HSAW_CUDA_CHECK(cudaMemsetAsync(ctx->g_hist_prefix.p, 0, (limit + 4) * 4, ctx->stream));

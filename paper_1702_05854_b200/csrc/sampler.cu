@@ -144,9 +144,36 @@ __device__ __forceinline__ bool claim(uint64_t* cursor, uint64_t total, bool wan
     return mine < total;
 }
 
+// FloydState::check's tortoise move (proj/src/sampler.cpp:121-137): the second cursor replays the
+// attempt's own draw stream, so its pick is the one the hare made at that position (always live)
+// and its resolve is never a hit; only the draws have to be consumed again. The cursor is kept as
+// (generator state, node): the row comes from the node record and the exact pick of the layout,
+// a non-default correctness path that costs three dependent reads per move. Returns the node the
+// tortoise arrives at.
+template <int LAYOUT, class RNG>
+static __device__ __noinline__ uint32_t tortoise_step(const NodeRec* __restrict__ nodes,
+                                                      const EdgeRec* __restrict__ edges,
+                                                      const uint64_t* __restrict__ thr, SrcRef src,
+                                                      RNG& t_rng, uint32_t t_node) {
+    const NodeRec r = load_node(nodes, t_node);
+    const uint64_t k = t_rng.draw();  // advance_edge, sampler.cpp:45
+    uint32_t u;
+    if (LAYOUT == kLayoutCompact) {
+        const int64_t slot = pick_exact_slot(nodes, thr, t_node, k);
+        bool dead;
+        u = load_src(src, (uint64_t)r.lo + (uint32_t)(slot < 0 ? 0 : slot), dead);
+    } else {
+        EdgeRec e;
+        (void)pick_slot(edges, r.lo, r.deg, r.scale, k, e);
+        u = e.src;
+    }
+    if (load_node(nodes, u).acc_thr != 0) t_rng.skip();  // resolve(): a suspect costs one draw
+    return u;
+}
+
 // ---- K1 ----------------------------------------------------------------------------------------
-// HEUR: 0 Brent, 2 None (CycleHeuristic, proj/include/hsaw/sampler.hpp:46). WIN: window width or
-// -1 for the runtime-width variant.
+// HEUR: 0 Brent, 1 Floyd, 2 None (CycleHeuristic, proj/include/hsaw/sampler.hpp:46). WIN: window
+// width or -1 for the runtime-width variant.
 // REC: 0 plain encode, 1 record walks (default stores), 2 record with streaming (.cs) stores.
 // STATS: per-lane work counters (draws, picks, algorithmic bytes) for instrumentation runs.
 // LAYOUT: kLayoutFat (32-byte edge records) or kLayoutCompact (in_src + 8-byte row headers).
@@ -192,6 +219,8 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
     bool have = false, fresh = true, drained = false;
     Window<WIN> win;
     uint32_t b_anchor = kInvalidNode, b_power = 1, b_lam = 0;
+    RNG t_rng{};                     // Floyd: the tortoise cursor (generator state, node)
+    uint32_t t_node = kInvalidNode;
     // per-lane work counters; 32 bits suffice for one launch's share of one lane, except bytes
     uint32_t st_draws = 0, st_steps = 0, st_att = 0, st_acc = 0;
     uint64_t st_bytes = 0, st_pairs = 0;
@@ -280,6 +309,12 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                             b_lam = 0;
                         }
                     }
+                    // FloydState::check, sampler.cpp:121-137: hare_pos counts the hare's steps that
+                    // reached the check (= nedges + 1 here); every second one moves the tortoise
+                    if (HEUR == 1 && !cyc && ((nedges + 1) & 1u) == 0) {
+                        t_node = tortoise_step<LAYOUT>(nodes, edges, p.thr, p.src, t_rng, t_node);
+                        cyc = t_node == u;
+                    }
                     if (!cyc) {
                         ++nedges;  // resolve(), sampler.cpp:54
                         walking = true;
@@ -356,6 +391,10 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
                     b_anchor = u;
                     b_power = 1;
                     b_lam = 0;
+                    if (HEUR == 1) {  // FloydState::reset, sampler.cpp:116-122: the tortoise has
+                        t_rng = rng;  // replayed the start draw and its resolve, like the hare
+                        t_node = u;
+                    }
                 } else {
                     win.push(u);  // sampler.cpp:200
                 }
@@ -979,10 +1018,7 @@ int persistent_blocks(hsaw_gpu_ctx* ctx, K kernel, uint64_t items) {
 }  // namespace
 
 void validate_cfg(const hsaw_sampler_cfg& cfg) {
-    if (cfg.heuristic == 1)
-        fail(HSAW_EINVAL,
-             "sampler: the Floyd heuristic is not available on the device path (use Brent or None)");
-    if (cfg.heuristic != 0 && cfg.heuristic != 2) fail(HSAW_EINVAL, "sampler: unknown heuristic");
+    if (cfg.heuristic < 0 || cfg.heuristic > 2) fail(HSAW_EINVAL, "sampler: unknown heuristic");
     if (cfg.batch_size == 0) fail(HSAW_EINVAL, "sampler: batch_size must be positive");
     if (cfg.rng_mode > 1) fail(HSAW_EINVAL, "sampler: unknown rng_mode");
     if (cfg.rng_mode == 1 && (cfg.heuristic != 0 || cfg.window != 2))
@@ -1047,7 +1083,9 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
     (compact ? go_r(encode_kernel<H, W, 4, 0, true, kLayoutCompact, true>)           \
              : go_r(encode_kernel<H, W, 4, 0, true, kLayoutFat, true>))
         const bool br = cfg.heuristic == 0;
-        if (cfg.window == 2)
+        if (cfg.heuristic == 1)  // Floyd: one runtime-window instantiation
+            HSAW_GO_R(1, -1);
+        else if (cfg.window == 2)
             br ? HSAW_GO_R(0, 2) : HSAW_GO_R(2, 2);
         else if (cfg.window == 0)
             br ? HSAW_GO_R(0, 0) : HSAW_GO_R(2, 0);
@@ -1165,7 +1203,9 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
     } else {
         // other SamplerConfig values: correctness paths, instrumented, never recording
         if (rec) fail(HSAW_EINVAL, "encode: recording is only built for the default sampler config");
-        if (cfg.window == 2)
+        if (cfg.heuristic == 1)  // Floyd: one runtime-window instantiation
+            HSAW_GO(1, -1, 4, 0, true);
+        else if (cfg.window == 2)
             HSAW_GO(2, 2, 4, 0, true);
         else if (cfg.window == 0)
             brent ? HSAW_GO(0, 0, 4, 0, true) : HSAW_GO(2, 0, 4, 0, true);

@@ -253,7 +253,7 @@ struct SamplePool {
     std::uint64_t accepted() const { return samples.size(); }
 };
 
-enum class CycleHeuristic { Brent, Floyd, None };  // Floyd is not offered on the device path
+enum class CycleHeuristic { Brent, Floyd, None };  // proj/include/hsaw/sampler.hpp:46
 
 // Reference: the reference's xorshift64* stream, every result bit-exact (the default, always).
 // PhiloxPerWalk: the device's throughput mode — an independent counter-based substream per walk

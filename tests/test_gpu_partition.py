@@ -48,10 +48,10 @@ def test_uneven_parts_and_zero_quota(pdg, pv, pcsr):  # noqa: F811
         assert np.array_equal(getattr(r["pool"], f), pv[f"ext_pool_{f}"]), f
 
 
-@pytest.mark.parametrize("window,heuristic", [(0, 0), (3, 0), (2, 2)])
+@pytest.mark.parametrize("window,heuristic", [(0, 0), (3, 0), (2, 2), (2, 1), (0, 1)])
 def test_restricted_stream_other_configs(gpu_lib, port, pv, pcsr, window, heuristic):  # noqa: F811
     """The restricted kernels exist for every SamplerConfig the device supports: one part's
-    stream against the oracle's orc_part_sample (windows 0 and 3, heuristic None)."""
+    stream against the oracle's orc_part_sample (windows 0 and 3, heuristics None and Floyd)."""
     part = golden_part(pv, "hash_h1", pcsr.n)
     from oracle.oracle import PART_STRIDE, Partitioning
     one = Partitioning(1, 1, np.zeros(pcsr.n, dtype=np.uint32), [part.base[2]], [part.extended[2]])

@@ -63,19 +63,36 @@ def test_encode_golden_kats(ctx, gpu_lib, golden, fixture12):
         assert seeds[0, :c].tolist() == [w["seed"] for w in kat["walks"]]
         assert lens[0, :c].tolist() == [w["len"] for w in kat["walks"]]
     for v in golden["fixture12_given"]["window_variants"]:
-        if v["heuristic"] == 1:
-            continue  # Floyd is not offered on the device path
         cfg = gpu_lib.SamplerCfg(heuristic=v["heuristic"], window=v["window"], batch_size=50)
         seeds, lens, counts, _ = ctx.encode_batches(42, 1, cfg)
         c = int(counts[0])
         assert seeds[0, :c].tolist() == v["seeds"] and lens[0, :c].tolist() == v["lens"]
 
 
-def test_floyd_is_rejected(ctx, gpu_lib, fixture12):
+def test_unknown_heuristic_is_rejected(ctx, gpu_lib, fixture12):
     upload(ctx, fixture12)
     with pytest.raises(gpu_lib.HsawError) as e:
-        ctx.encode_batches(0, 1, gpu_lib.SamplerCfg(heuristic=1))
+        ctx.encode_batches(0, 1, gpu_lib.SamplerCfg(heuristic=3))
     assert e.value.status == gpu_lib.HSAW_EINVAL
+
+
+@pytest.mark.parametrize("name,window", [("uniform2000", 2), ("uniform2000", 0), ("rmat12", 2),
+                                         ("rmat14_dense", 3), ("ring", 0)])
+def test_encode_floyd_matches_oracle(ctx, gpu_lib, port, name, window):
+    """CycleHeuristic::Floyd (proj/src/sampler.cpp:113-138): the tortoise cursor replays the
+    attempt's draw stream on the device; batches equal the oracle's, work counters included (the
+    tortoise's draws are not the attempt's: sampler.cpp:128-133 uses the second cursor's state)."""
+    if name == "ring":  # cycles only: every walk that misses the single suspect is flagged
+        from oracle.oracle import Csr
+        n = 64
+        p = np.zeros(n)
+        p[0] = 0.02
+        csr = Csr(n, n, np.arange(n + 1, dtype=np.uint64),
+                  ((np.arange(n) + 1) % n).astype(np.uint32), np.ones(n), p)
+    else:
+        csr = make_csr(small_graphs()[name])
+    upload(ctx, csr)
+    check_encode(ctx, gpu_lib, port, csr, 77, 600, l=10, heuristic=1, window=window)
 
 
 def test_encode_matches_oracle_fixture12(ctx, gpu_lib, port, fixture12, fixture12_indegree):
@@ -275,6 +292,18 @@ def test_stream_pool_golden(ctx, golden, fixture12, synth3000):
         got = st.to_pool(4000)
     assert (got.nsamples, got.attempts) == (exp["nsamples"], exp["attempts"])
     assert digest(got.edge_off, got.nodes, got.edges, got.tag_worker, got.tag_seq) == exp["sha256"]
+
+
+def test_stream_floyd_matches_oracle(ctx, gpu_lib, port):
+    """The whole stream under CycleHeuristic::Floyd: pool, tags and attempts equal the oracle's
+    (the unfused K1 -> K2 -> K2b path serves every non-default SamplerConfig)."""
+    csr = make_csr(small_graphs()["uniform2000"])
+    upload(ctx, csr)
+    for window in (2, 0):
+        with ctx.stream(seed=8, cfg=gpu_lib.SamplerCfg(heuristic=1, window=window)) as st:
+            st.ensure(2500)
+            pools_equal(st.to_pool(2500),
+                        port.stream_samples(csr, 2500, seed=8, heuristic=1, window=window))
 
 
 @pytest.mark.parametrize("name", ["uniform2000", "rmat12"])

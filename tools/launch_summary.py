@@ -1,30 +1,41 @@
-"""Per-kernel totals of an ncu launch list (--metrics gpu__time_duration.sum[,dram__bytes_*] --csv).
-python tools/launch_summary.py launches.csv [top]"""
+"""Summarise an ncu --csv launch list (one row per launch and metric) by kernel:
+total time, launches, DRAM bytes. usage: python tools/launch_summary.py file.csv [top]"""
 import collections
 import csv
+import re
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
-hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
-hdr = rows[hi]
-ki, mi, vi, ui = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
-t, c = collections.defaultdict(float), collections.Counter()
-rd, wr = collections.defaultdict(float), collections.defaultdict(float)
-TS = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1, "msecond": 1, "second": 1e3, "s": 1e3}
-BS = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1, "Tbyte": 1e3}
-for r in rows[hi + 1:]:
-    if len(r) <= vi:
-        continue
-    name = r[ki].split("(")[0][-64:]
-    v = float(r[vi].replace(",", ""))
-    if r[mi] == "gpu__time_duration.sum":
-        t[name] += v * TS[r[ui]]
-        c[name] += 1
-    elif r[mi] == "dram__bytes_read.sum":
-        rd[name] += v * BS[r[ui]]
-    elif r[mi] == "dram__bytes_write.sum":
-        wr[name] += v * BS[r[ui]]
-tot = sum(t.values())
-print(f"total {tot:.2f} ms over {sum(c.values())} launches")
-for k, v in sorted(t.items(), key=lambda x: -x[1])[: int(sys.argv[2]) if len(sys.argv) > 2 else 30]:
-    print(f"{v:10.2f} ms {100 * v / tot:5.1f}% n={c[k]:5d} rd={rd[k]:8.1f}GB wr={wr[k]:8.1f}GB  {k}")
+
+def main():
+    fn = sys.argv[1]
+    top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+    rows = list(csv.reader(open(fn)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr = rows[hi]
+    ki, mi, vi, ui = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
+    scale = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        name = re.sub(r"\(.*", "", r[ki])
+        name = re.sub(r"hsawgpu::|<unnamed>::|void ", "", name)[:80]
+        a = agg[name]
+        if r[mi] == "gpu__time_duration.sum":
+            a[0] += 1
+            a[1] += v
+        elif r[mi] == "dram__bytes_read.sum":
+            a[2] += v
+        elif r[mi] == "dram__bytes_write.sum":
+            a[3] += v
+    tot = sum(a[1] for a in agg.values())
+    print(f"{fn}: {sum(a[0] for a in agg.values())} launches, {tot:.1f} ms of kernel time")
+    print(f"{'ms':>10} {'share':>6} {'n':>6} {'GB rd':>8} {'GB wr':>8} {'TB/s':>6}  kernel")
+    for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+        bw = (a[2] + a[3]) / (a[1] * 1e-3) / 1e12 if a[1] else 0
+        print(f"{a[1]:10.2f} {100 * a[1] / tot:5.1f}% {a[0]:6d} {a[2] / 1e9:8.2f} {a[3] / 1e9:8.2f} {bw:6.2f}  {k}")
+
+
+if __name__ == "__main__":
+    main()
