@@ -3,6 +3,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -383,7 +384,7 @@ const DeviceInfo& device_info(int device) {
 class StagedCopier {
 public:
     using Job = hsawgpu::CopyJob;
-    static constexpr int kMaxThreads = 8, kMaxSlots = 4;
+    static constexpr int kMaxThreads = 16, kMaxSlots = 4;
     static size_t chunk_bytes() {  // HSAW_UPLOAD_CHUNK_MB: A/B knob
         static const size_t v = [] {
             const char* env = std::getenv("HSAW_UPLOAD_CHUNK_MB");
@@ -949,6 +950,21 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             fail(HSAW_EDATA, "graph: offsets do not cover edge range");
         for (uint32_t v = 0; v < n; ++v)
             if (in_offsets[v + 1] < in_offsets[v]) fail(HSAW_EDATA, "graph: offsets not monotone");
+        // HSAW_UPLOAD_TIMING=1: phase times of this call on stderr (host clock, stream synchronised)
+        static const bool timing = [] {
+            const char* env = std::getenv("HSAW_UPLOAD_TIMING");
+            return env && std::atoi(env) != 0;
+        }();
+        auto t_last = std::chrono::steady_clock::now();
+        auto lap = [&](const char* what) {
+            if (!timing) return;
+            cudaStreamSynchronize(ctx->stream);
+            auto t = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[hsaw upload] %-10s %8.2f ms\n", what,
+                         std::chrono::duration<double, std::milli>(t - t_last).count());
+            t_last = t;
+        };
+        lap("checks");
         free_graph(ctx);
         cudaStream_t st = ctx->stream;
         uint64_t* d_off = nullptr;
@@ -973,8 +989,11 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
                 jobs.push_back({d_cum, in_cum, (uint64_t)m * 8});
             }
             jobs.push_back({d_p, p_of, (uint64_t)n * 8});
+            lap("alloc");
             copy_to_device(ctx, jobs);
+            lap("copy");
             install_graph(ctx, n, m, d_off, d_src, d_cum, d_p);
+            lap("install");
         } catch (...) {
             cleanup();
             free_graph(ctx);

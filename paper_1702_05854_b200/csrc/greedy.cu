@@ -27,14 +27,22 @@ struct WalkView;
 
 namespace {
 
-// Walks [w0, w0 + cnt) of either source. Walk w occupies items[off[w] + add*w, off[w+1] + add*(w+1)).
+// Walks [w0, w0 + cnt) of either source. Walk w occupies items[off[w] + add*w, off[w+1] + add*(w+1)),
+// or, when `len` is set (the dense reduced instance of a large id space, see build_dense),
+// items[off[w], off[w] + len[w]).
 struct WalkView {
     const uint64_t* off;
     const uint32_t* items;
     uint64_t w0, cnt;
     uint32_t add;  // 1 for the node arrays of a stream (len + 1 nodes per walk), else 0
     uint32_t limit;
+    const uint32_t* len;  // per-walk item counts of a (start, length) view, else nullptr
 };
+
+__device__ __forceinline__ void walk_extent(const WalkView& v, uint64_t w, uint64_t& b, uint64_t& e) {
+    b = v.off[w] + v.add * w;
+    e = v.len ? b + v.len[w] : v.off[w + 1] + v.add * (w + 1);
+}
 
 __device__ __forceinline__ bool is_cand(const uint32_t* __restrict__ cand_bits, uint32_t item) {
     return cand_bits == nullptr || ((cand_bits[item >> 5] >> (item & 31)) & 1u);
@@ -90,7 +98,7 @@ __global__ void key_histogram(const uint32_t* __restrict__ keys, uint64_t n, uin
                               const uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ cnt) {
     uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
-        uint32_t item = keys[p];
+        uint32_t item = __ldcs(keys + p);  // read once: must not push the counters out of L2
         if (item < limit && is_cand(cand_bits, item)) atomicAdd(&cnt[item], 1u);
     }
 }
@@ -128,12 +136,15 @@ __global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ indexe
     uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i = warp; i < v.cnt; i += nwarps) {
         uint64_t w = v.w0 + i;
-        uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
+        uint64_t b, e;
+        walk_extent(v, w, b, e);
         for (uint64_t p = b + lane; p < e; p += 32) {
             uint32_t item = v.items[p];
-            // only items that can still win a round are indexed (min_count, see hsaw_gpu_greedy)
-            if (item < v.limit && filter_pass(filter, item) &&
-                ((indexed_bits[item >> 5] >> (item & 31)) & 1u)) {
+            // only items that can still win a round are indexed (min_count, see hsaw_gpu_greedy);
+            // a dense reduced instance holds nothing else (indexed_bits == nullptr)
+            if (item < v.limit && (indexed_bits == nullptr ||
+                                   (filter_pass(filter, item) &&
+                                    ((indexed_bits[item >> 5] >> (item & 31)) & 1u)))) {
                 uint32_t slot = atomicAdd(&fill[item], 1u);
                 inv[pos[item] + slot] = (uint32_t)i;
             }
@@ -142,36 +153,48 @@ __global__ void scatter_inverted(WalkView v, const uint32_t* __restrict__ indexe
 }
 
 // Occurrences per count value (counts >= kCountBins - 1 share the last bin): lets the host pick the
-// smallest count worth indexing.
+// smallest count worth indexing. occ_bins[c] += c * (#items with count c).
+// A streaming pass over the counters (5.9 GB at the Twitter shape, where the mean count is ~7): the
+// bins are per-warp 32-bit ITEM counters in shared memory (native atomics whose conflicts stay
+// inside one warp), multiplied out once per block; 128-bit loads. The first version hammered one
+// 64-bit shared-memory bin per count with CAS loops: 1.2 TB/s.
 constexpr uint32_t kCountBins = 1024;
-__global__ void __launch_bounds__(256) count_of_counts(const uint32_t* __restrict__ cnt,
-                                                       uint32_t limit,
-                                                       unsigned long long* __restrict__ occ_bins) {
-    __shared__ unsigned long long bins[kCountBins];
-    for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x) bins[i] = 0;
+constexpr uint32_t kCocWarps = 8;
+__global__ void __launch_bounds__(kCocWarps * 32) count_of_counts(const uint32_t* __restrict__ cnt,
+                                                                   uint32_t limit,
+                                                                   unsigned long long* __restrict__ occ_bins) {
+    __shared__ uint32_t bins[kCocWarps][kCountBins];
+    __shared__ unsigned long long big;  // sum of the counts >= kCountBins - 1 (rare)
+    for (uint32_t i = threadIdx.x; i < kCocWarps * kCountBins; i += blockDim.x) (&bins[0][0])[i] = 0;
+    if (threadIdx.x == 0) big = 0;
     __syncthreads();
-    // almost every non-zero count is tiny: keep those in registers instead of hammering one
-    // shared-memory address with atomics
-    unsigned long long small[5] = {0, 0, 0, 0, 0};
-    uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < limit; i += stride) {
-        uint32_t c = cnt[i];
-        if (c == 0) continue;
-        if (c <= 4)
-            small[c] += c;
+    uint32_t* mine = bins[threadIdx.x >> 5];
+    auto add = [&](uint32_t c) {
+        if (c == 0) return;
+        if (c < kCountBins - 1)
+            atomicAdd(&mine[c], 1u);
         else
-            atomicAdd(&bins[c < kCountBins ? c : kCountBins - 1], (unsigned long long)c);
+            atomicAdd(&big, (unsigned long long)c);
+    };
+    const uint64_t quads = limit / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint4* cnt4 = reinterpret_cast<const uint4*>(cnt);  // pool allocations are 256-byte aligned
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < quads; i += stride) {
+        const uint4 c = __ldcs(cnt4 + i);
+        add(c.x);
+        add(c.y);
+        add(c.z);
+        add(c.w);
     }
-#pragma unroll
-    for (int c = 1; c <= 4; ++c) {
-        unsigned long long v = small[c];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
-        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&bins[c], v);
-    }
+    if (blockIdx.x == 0 && threadIdx.x < (limit & 3u)) add(cnt[quads * 4 + threadIdx.x]);
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x)
-        if (bins[i]) atomicAdd(&occ_bins[i], bins[i]);
+    for (uint32_t c = threadIdx.x; c < kCountBins - 1; c += blockDim.x) {
+        unsigned long long n = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < kCocWarps; ++w) n += bins[w][c];
+        if (n) atomicAdd(&occ_bins[c], n * c);
+    }
+    if (threadIdx.x == 0 && big) atomicAdd(&occ_bins[kCountBins - 1], big);
 }
 
 // pos input: counts below the threshold take no inverted-list space
@@ -179,6 +202,174 @@ __global__ void threshold_counts(const uint32_t* __restrict__ cnt, uint64_t n, u
                                  uint32_t* __restrict__ out) {
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = cnt[i] >= min_count ? cnt[i] : 0;
+}
+
+// ---- dense reduced instance of a large id space ---------------------------------------------------
+// With 1.47 G edge ids (Twitter shape) every per-item array of the greedy run is 6..12 GB and every
+// access to it a DRAM round trip: the histogram, the inverted-list scatter (one bitmap line, one
+// fill counter and one list slot per indexed occurrence), and each of the ~130 count decrements per
+// covered walk in the rounds. Only the items at or above the indexing threshold can be selected
+// (see hsaw_gpu_greedy), a few per cent of the ids. build_dense renames them 0..D-1 in id order
+// (so the smallest-id tie-break is unchanged) and copies the walks restricted to them, in one
+// streaming pass, into a (start, length) view whose items are the new names: everything after it
+// (pos / fill / counts / block maxima / the rounds) works on D-sized arrays that live in L2 and on
+// walks an eighth as long. Gains, selections and the "winner below the threshold" protocol are
+// those of the full instance: the reduced walks hold every occurrence of every indexed item.
+
+// Word-blocked two-bit Bloom filter in front of the rank map (367 MB at the Twitter shape: one DRAM
+// line per lookup): a clear bit proves "not indexed" from a table that stays cached.
+struct Bloom2 {
+    const uint32_t* words;
+    uint32_t log2w;  // table size in 32-bit words = 2^log2w
+};
+__device__ __forceinline__ void bloom2_slot(uint32_t item, uint32_t log2w, uint32_t& word, uint32_t& mask) {
+    word = (item * 0x9E3779B1u) >> (32 - log2w);
+    const uint32_t h2 = item * 0x85EBCA6Bu;
+    mask = (1u << (h2 >> 27)) | (1u << ((h2 >> 22) & 31u));
+}
+__device__ __forceinline__ bool bloom2_pass(const Bloom2& f, uint32_t item) {
+    uint32_t word, mask;
+    bloom2_slot(item, f.log2w, word, mask);
+    return (__ldg(f.words + word) & mask) == mask;
+}
+
+// One warp per 32 words (1024 ids): coalesced count reads, the ballot of "indexed" IS the word.
+__global__ void __launch_bounds__(256) dense_mark(const uint32_t* __restrict__ cnt, uint32_t limit,
+                                                  uint32_t min_count, uint32_t* __restrict__ bits,
+                                                  uint32_t* __restrict__ pc, uint32_t* __restrict__ bloom,
+                                                  uint32_t log2w) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t words = ((uint64_t)limit + 31) / 32;
+    const uint64_t w0 = warp * 32;
+    if (w0 >= words) return;
+    uint32_t my = 0;
+#pragma unroll 4
+    for (uint32_t j = 0; j < 32; ++j) {
+        const uint64_t id = (w0 + j) * 32 + lane;
+        const uint32_t c = id < limit ? cnt[id] : 0u;
+        const bool in = c != 0 && c >= min_count;
+        const uint32_t m = __ballot_sync(kFullMask, in);
+        if (lane == j) my = m;
+        if (in) {
+            uint32_t word, mask;
+            bloom2_slot((uint32_t)id, log2w, word, mask);
+            atomicOr(&bloom[word], mask);
+        }
+    }
+    if (w0 + lane < words) {
+        bits[w0 + lane] = my;
+        pc[w0 + lane] = __popc(my);
+    }
+}
+
+// rmap[word] = (indexed bits of the word, rank of its first indexed id); ids / counts by rank.
+__global__ void __launch_bounds__(256) dense_emit(const uint32_t* __restrict__ cnt, uint32_t limit,
+                                                  const uint32_t* __restrict__ bits,
+                                                  const uint32_t* __restrict__ base,
+                                                  uint2* __restrict__ rmap, uint32_t* __restrict__ rids,
+                                                  uint32_t* __restrict__ rcnt) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t words = ((uint64_t)limit + 31) / 32;
+    const uint64_t w0 = warp * 32;
+    if (w0 >= words) return;
+    uint32_t my_bits = 0, my_base = 0;
+    if (w0 + lane < words) {
+        my_bits = bits[w0 + lane];
+        my_base = base[w0 + lane];
+        rmap[w0 + lane] = make_uint2(my_bits, my_base);
+    }
+    uint32_t any = __ballot_sync(kFullMask, my_bits != 0);
+    while (any) {
+        const int j = __ffs(any) - 1;
+        any &= any - 1;
+        const uint32_t b = __shfl_sync(kFullMask, my_bits, j);
+        const uint32_t r0 = __shfl_sync(kFullMask, my_base, j);
+        if ((b >> lane) & 1u) {
+            const uint32_t id = (uint32_t)((w0 + j) * 32 + lane);
+            const uint32_t r = r0 + __popc(b & ((1u << lane) - 1u));
+            rids[r] = id;
+            rcnt[r] = cnt[id];
+        }
+    }
+}
+
+// Walks -> (start, length) view of their indexed items, renamed. One warp per walk; a block's eight
+// walks share one atomicAdd on the output cursor. Up to kDenseStage renamed items are staged per
+// warp in shared memory between the counting and the writing half; longer ones are looked up twice.
+constexpr uint32_t kDenseStage = 256;
+__global__ void __launch_bounds__(256) dense_extract(WalkView v, Bloom2 bloom,
+                                                     const uint2* __restrict__ rmap,
+                                                     unsigned long long* __restrict__ cursor,
+                                                     uint64_t* __restrict__ rstart,
+                                                     uint32_t* __restrict__ rlen,
+                                                     uint32_t* __restrict__ ritems) {
+    __shared__ uint32_t stage[8][kDenseStage];
+    __shared__ uint32_t s_cnt[8];
+    __shared__ unsigned long long s_base;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto lookup = [&](uint32_t it, uint32_t& rank) -> bool {
+        if (it >= v.limit || !bloom2_pass(bloom, it)) return false;
+        const uint2 m = __ldg(rmap + (it >> 5));
+        if (!((m.x >> (it & 31)) & 1u)) return false;
+        rank = m.y + __popc(m.x & ((1u << (it & 31)) - 1u));
+        return true;
+    };
+    for (uint64_t i0 = (uint64_t)blockIdx.x * 8; i0 < v.cnt; i0 += (uint64_t)gridDim.x * 8) {
+        const uint64_t i = i0 + warp;
+        uint32_t c = 0;
+        uint64_t b = 0, e = 0;
+        if (i < v.cnt) {
+            walk_extent(v, v.w0 + i, b, e);
+            for (uint64_t p0 = b; p0 < e; p0 += 32) {
+                const uint64_t p = p0 + lane;
+                uint32_t rank = 0;
+                const bool keep = p < e && lookup(v.items[p], rank);
+                const uint32_t m = __ballot_sync(kFullMask, keep);
+                const uint32_t at = c + __popc(m & ((1u << lane) - 1u));
+                if (keep && at < kDenseStage) stage[warp][at] = rank;
+                c += __popc(m);
+            }
+        }
+        if (lane == 0) s_cnt[warp] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < 8; ++w) t += s_cnt[w];
+            s_base = t ? atomicAdd(cursor, (unsigned long long)t) : 0ull;
+        }
+        __syncthreads();
+        if (i < v.cnt) {
+            uint64_t start = s_base;
+            for (uint32_t w = 0; w < warp; ++w) start += s_cnt[w];
+            if (lane == 0) {
+                rstart[i] = start;
+                rlen[i] = c;
+            }
+            if (c <= kDenseStage) {
+                for (uint32_t q = lane; q < c; q += 32) ritems[start + q] = stage[warp][q];
+            } else {  // a walk with more indexed items than the stage holds: second look-up pass
+                uint32_t at0 = 0;
+                for (uint64_t p0 = b; p0 < e; p0 += 32) {
+                    const uint64_t p = p0 + lane;
+                    uint32_t rank = 0;
+                    const bool keep = p < e && lookup(v.items[p], rank);
+                    const uint32_t m = __ballot_sync(kFullMask, keep);
+                    if (keep) ritems[start + at0 + __popc(m & ((1u << lane) - 1u))] = rank;
+                    at0 += __popc(m);
+                }
+            }
+        }
+        __syncthreads();  // stage / s_cnt are reused by the next iteration
+    }
+}
+
+// solution slots hold ranks of the dense instance: back to ids (markers pass through)
+__global__ void dense_solution_ids(uint32_t* __restrict__ sol, uint32_t n, uint32_t limit,
+                                   const uint32_t* __restrict__ rids) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && sol[i] < limit) sol[i] = rids[sol[i]];
 }
 
 __device__ __forceinline__ uint64_t block_max_u64(uint64_t v, uint64_t* smem) {
@@ -359,7 +550,8 @@ __global__ void __launch_bounds__(256) cover_winner(WalkView v, const uint64_t* 
         old = __shfl_sync(kFullMask, old, 0);
         if (old & (1u << (lw & 31))) continue;  // already covered (earlier round or duplicate item)
         uint64_t w = v.w0 + lw;
-        uint64_t b = v.off[w] + v.add * w, e = v.off[w + 1] + v.add * (w + 1);
+        uint64_t b, e;
+        walk_extent(v, w, b, e);
         for (uint64_t p = b + lane; p < e; p += 32) {
             uint32_t it = v.items[p];
             if (it < v.limit && is_cand(cand_bits, it)) atomicSub(&cnt[it], 1u);
@@ -483,12 +675,9 @@ __global__ void __launch_bounds__(1024) greedy_tail_kernel(
             // the extents are fetched while the claims are in flight: one round trip less on the
             // round's dependent chain (a claim that fails wastes two loads)
             const uint64_t w1 = v.w0 + lw1, w2 = v.w0 + lw2;
-            const uint64_t b1 = v.off[w1] + v.add * w1, e1 = v.off[w1 + 1] + v.add * (w1 + 1);
-            uint64_t b2 = 0, e2 = 0;
-            if (has2) {
-                b2 = v.off[w2] + v.add * w2;
-                e2 = v.off[w2 + 1] + v.add * (w2 + 1);
-            }
+            uint64_t b1, e1, b2 = 0, e2 = 0;
+            walk_extent(v, w1, b1, e1);
+            if (has2) walk_extent(v, w2, b2, e2);
             const uint32_t old1 = __shfl_sync(kFullMask, old, 0);
             const uint32_t old2 = __shfl_sync(kFullMask, old, 1);
             const uint64_t len1 = (old1 & (1u << (lw1 & 31))) ? 0 : e1 - b1;  // 0: already covered
@@ -654,6 +843,17 @@ WalkView make_view(const hsaw_gpu_stream* s, const hsaw_gpu_walkset* ws, int kin
     return v;
 }
 
+uint64_t read_u64(hsaw_gpu_ctx* ctx, const uint64_t* d) {
+    HSAW_CUDA_CHECK(cudaMemcpyAsync(ctx->h_scalars, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    return ctx->h_scalars[0];
+}
+uint32_t read_u32(hsaw_gpu_ctx* ctx, const uint32_t* d) {
+    HSAW_CUDA_CHECK(cudaMemcpyAsync(ctx->h_scalars, d, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    return *reinterpret_cast<uint32_t*>(ctx->h_scalars);
+}
+
 // first/last item position of the view (two 8-byte reads)
 void view_span(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t* p0, uint64_t* p1) {
     uint64_t a = 0, b = 0;
@@ -740,7 +940,12 @@ static void histogram_counts(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t p0, 
             DevVec<uint32_t>& d_sorted = ctx->g_sorted;
             d_sorted.ensure_scratch(std::min(nitems, kSlice));
             int top = 32 - __builtin_clz(limit - 1);
-            int begin_bit = std::max(0, top - 8);
+            static const int part_bits = [] {  // A/B knob: radix bits of the partition (8 per pass)
+                const char* env = std::getenv("HSAW_HIST_BITS");
+                const int v = env ? std::atoi(env) : 8;
+                return v < 1 ? 8 : (v > 32 ? 32 : v);
+            }();
+            int begin_bit = std::max(0, top - part_bits);
             for (uint64_t at = 0; at < nitems; at += kSlice) {
                 const uint64_t len = std::min(kSlice, nitems - at);
                 size_t bytes = 0;
@@ -783,10 +988,27 @@ static HistCache& hist_cache(hsaw_gpu_ctx* ctx) {
     return caches[ctx];
 }
 
+// (128-bit accesses when both arrays are 16-byte aligned: 17.6 GB per fold at the Twitter shape)
 __global__ void add_counts(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint64_t n) {
-    uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        dst[i] += src[i];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t done = 0;
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u) == 0) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        const uint64_t quads = n / 4;
+        for (uint64_t i = tid; i < quads; i += stride) {
+            uint4 a = d4[i];
+            const uint4 b = __ldcs(s4 + i);
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+            d4[i] = a;
+        }
+        done = quads * 4;
+    }
+    for (uint64_t i = done + tid; i < n; i += stride) dst[i] += src[i];
 }
 
 __global__ void offsets_to_lens(const uint64_t* __restrict__ off, uint64_t n, uint32_t* __restrict__ lens) {
@@ -957,13 +1179,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         DevVec<uint64_t>& d_blkmax = ctx->g_blkmax;
         DevVec<uint32_t>& d_sol = ctx->g_solution;
         DevVec<uint64_t>& d_gain = ctx->g_gains;
-        d_cnt.ensure_scratch((uint64_t)limit + 4);
-        d_fill.ensure_scratch((uint64_t)limit + 4);
-        d_pos.ensure_scratch((uint64_t)limit + 2);
-        const uint32_t bshift = block_shift_for(limit);
-        const uint32_t nblk = (uint32_t)(((uint64_t)limit + (1ull << bshift) - 1) >> bshift);
         d_partial.ensure_scratch(kCountBins + 4);
-        d_blkmax.ensure_scratch(nblk + 1);
         d_sol.ensure_scratch(k);
         d_gain.ensure_scratch(k);
         uint64_t cov_words = (cnt + 31) / 32 + 1;
@@ -975,34 +1191,54 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         const int wide = ctx->sm_count * 8;
         const int cover_blocks = ctx->sm_count * 2;
         uint32_t done = 0;
+        // Large id spaces run on a dense reduced instance (build_dense above). HSAW_DENSE_MIN_BYTES:
+        // size of the per-item counter array from which it applies (0 forces it everywhere: tests);
+        // HSAW_INDEX_MASS_DIV: the indexed items hold at most 1/div of all occurrences.
+        const uint64_t dense_min_bytes = [] {  // (read per call: the tests flip it)
+            const char* env = std::getenv("HSAW_DENSE_MIN_BYTES");
+            return env ? std::strtoull(env, nullptr, 10) : (256ull << 20);
+        }();
+        const uint64_t mass_div = [] {
+            const char* env = std::getenv("HSAW_INDEX_MASS_DIV");
+            const uint64_t d = env ? std::strtoull(env, nullptr, 10) : 8;
+            return d ? d : 8;
+        }();
+        const bool dense_forced = dense_min_bytes == 0;
+        const bool dense_possible = cand_ids == nullptr && p1 > p0 &&
+                                    (dense_forced || ((uint64_t)limit * 4 > dense_min_bytes &&
+                                                      p1 - p0 > (1ull << 24)));
 
         auto run = [&](uint32_t min_count) -> bool {
-            HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
-            HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_partial.p, 0, 8, st));  // no previous winner yet
             // ---- K3: marginal-gain counts (a stream prefix comes from the histogram cache)
-            if (hist_cache_usable(stream, cand_ids) && off == 0) {
-                const uint32_t* cached = hist_prefix(ctx, stream, kind, limit, cnt);
-                HSAW_CUDA_CHECK(cudaMemcpyAsync(d_cnt.p, cached, (uint64_t)limit * 4,
-                                                cudaMemcpyDeviceToDevice, st));
+            const uint32_t* full_cnt = nullptr;  // counts of the view's items, limit (+ zero pad) entries
+            const bool from_cache = hist_cache_usable(stream, cand_ids) && off == 0;
+            if (from_cache) {
+                full_cnt = hist_prefix(ctx, stream, kind, limit, cnt);
             } else {
+                d_cnt.ensure_scratch((uint64_t)limit + 4);
+                HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
                 histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
+                full_cnt = d_cnt.p;
             }
-            if (min_count == 0) {
-                // Index only what can win: the smallest count whose items (and everything above)
-                // make up at most 1/8 of all occurrences. Small inputs index everything.
+            std::vector<uint64_t> bins;
+            if (min_count == 0 || dense_possible) {
                 auto* d_bins = reinterpret_cast<unsigned long long*>(d_partial.p + 4);
                 HSAW_CUDA_CHECK(cudaMemsetAsync(d_bins, 0, kCountBins * 8, st));
                 {
                     StageScope timer(ctx, HSAW_STAGE_INDEX);
-                    count_of_counts<<<wide, 256, 0, st>>>(d_cnt.p, limit, d_bins);
+                    count_of_counts<<<wide, kCocWarps * 32, 0, st>>>(full_cnt, limit, d_bins);
                     check_launch(ctx, "count_of_counts");
                 }
-                std::vector<uint64_t> bins(kCountBins);
+                bins.resize(kCountBins);
                 HSAW_CUDA_CHECK(cudaMemcpyAsync(bins.data(), d_bins, kCountBins * 8,
                                                 cudaMemcpyDeviceToHost, st));
                 HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
+            }
+            if (min_count == 0) {
+                // Index only what can win: the smallest count whose items (and everything above)
+                // make up at most 1/8 of all occurrences. Small inputs index everything.
                 uint64_t total = 0;
                 for (uint64_t b : bins) total += b;
                 min_count = 1;
@@ -1010,24 +1246,95 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                     uint64_t above = 0;
                     min_count = kCountBins - 1;
                     for (uint32_t c = kCountBins - 1; c >= 1; --c) {
-                        if (above + bins[c] > total / 8) break;
+                        if (above + bins[c] > total / mass_div) break;
                         above += bins[c];
                         min_count = c;
                     }
                 }
             }
+            // ---- the instance the rounds run on: the view itself, or its dense reduction
+            const bool dense = dense_possible && (dense_forced || min_count > 1);
+            WalkView rv = v;
+            uint32_t rlimit = limit;
+            uint32_t* rcnt = nullptr;
+            DevVec<uint32_t> x_bits, x_pc, x_base, x_bloom, x_ids, x_cnt, x_len, x_items;
+            DevVec<uint64_t> x_map, x_start;
+            if (dense) {
+                uint64_t occ = 0, d_est = 0;  // occurrences / distinct ids at or above min_count
+                for (uint32_t c = std::max(min_count, 1u); c < kCountBins; ++c) {
+                    occ += bins[c];
+                    d_est += c < kCountBins - 1 ? bins[c] / c : (bins[c] + kCountBins - 2) / (kCountBins - 1);
+                }
+                const uint64_t words = ((uint64_t)limit + 31) / 32;
+                uint32_t log2w = 14;  // 32 filter bits per indexed id where a cached table allows it
+                while ((1ull << log2w) < d_est && log2w < 23) ++log2w;
+                x_bits.ensure_scratch(words + 1);
+                x_pc.ensure_scratch(words + 1);
+                x_base.ensure_scratch(words + 1);
+                x_bloom.ensure_scratch(1ull << log2w);
+                HSAW_CUDA_CHECK(cudaMemsetAsync(x_bloom.p, 0, (1ull << log2w) * 4, st));
+                HSAW_CUDA_CHECK(cudaMemsetAsync(x_pc.p + words, 0, 4, st));
+                const unsigned mark_blocks = (unsigned)((words + 255) / 256);  // 8 warps x 32 words
+                {
+                    StageScope timer(ctx, HSAW_STAGE_INDEX);
+                    dense_mark<<<mark_blocks, 256, 0, st>>>(full_cnt, limit, std::max(min_count, 1u),
+                                                            x_bits.p, x_pc.p, x_bloom.p, log2w);
+                    check_launch(ctx, "dense_mark");
+                    exclusive_sum_u32(ctx, x_pc.p, x_base.p, words + 1);
+                }
+                const uint64_t D = read_u32(ctx, x_base.p + words);
+                x_map.ensure_scratch(words + 1);
+                x_ids.ensure_scratch(D + 1);
+                x_cnt.ensure_scratch(D + 4);
+                x_start.ensure_scratch(cnt + 1);
+                x_len.ensure_scratch(cnt + 1);
+                x_items.ensure_scratch(occ + 1);
+                auto* d_cursor = reinterpret_cast<unsigned long long*>(ctx->d_scalars + 12);
+                HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, st));
+                HSAW_CUDA_CHECK(cudaMemsetAsync(x_cnt.p, 0, (D + 4) * 4, st));
+                {
+                    StageScope timer(ctx, HSAW_STAGE_INDEX);
+                    dense_emit<<<mark_blocks, 256, 0, st>>>(full_cnt, limit, x_bits.p, x_base.p,
+                                                            reinterpret_cast<uint2*>(x_map.p), x_ids.p,
+                                                            x_cnt.p);
+                    check_launch(ctx, "dense_emit");
+                    const int eb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
+                    dense_extract<<<eb, 256, 0, st>>>(v, Bloom2{x_bloom.p, log2w},
+                                                      reinterpret_cast<const uint2*>(x_map.p), d_cursor,
+                                                      x_start.p, x_len.p, x_items.p);
+                    check_launch(ctx, "dense_extract");
+                }
+                if (read_u64(ctx, reinterpret_cast<uint64_t*>(d_cursor)) != occ)
+                    fail(HSAW_ECUDA, "greedy: dense instance does not match the counts (internal error)");
+                rv = WalkView{x_start.p, x_items.p, 0, cnt, 0, (uint32_t)D, x_len.p};
+                rlimit = (uint32_t)D;
+                rcnt = x_cnt.p;
+            } else {
+                d_cnt.ensure_scratch((uint64_t)limit + 4);
+                if (from_cache) {
+                    HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p + limit, 0, 16, st));
+                    HSAW_CUDA_CHECK(cudaMemcpyAsync(d_cnt.p, full_cnt, (uint64_t)limit * 4,
+                                                    cudaMemcpyDeviceToDevice, st));
+                }
+                rcnt = d_cnt.p;
+            }
+            const uint32_t index_min = dense ? 1u : min_count;  // a dense instance holds indexed items only
+            const uint32_t bshift = block_shift_for(rlimit);
+            const uint32_t nblk = (uint32_t)(((uint64_t)rlimit + (1ull << bshift) - 1) >> bshift);
+            d_blkmax.ensure_scratch(nblk + 1);
+            d_fill.ensure_scratch((uint64_t)rlimit + 4);
+            d_pos.ensure_scratch((uint64_t)rlimit + 2);
             // ---- K3b: inverted lists (counting sort) of the items at or above min_count
             uint32_t* d_thr = d_fill.p;  // reused as the scan input, re-zeroed below
             {
                 StageScope timer(ctx, HSAW_STAGE_INDEX);
-                uint64_t n1 = (uint64_t)limit + 1;
-                threshold_counts<<<(unsigned)((n1 + 255) / 256), 256, 0, st>>>(d_cnt.p, n1,
-                                                                                 min_count, d_thr);
+                uint64_t n1 = (uint64_t)rlimit + 1;
+                threshold_counts<<<(unsigned)((n1 + 255) / 256), 256, 0, st>>>(rcnt, n1, index_min, d_thr);
                 check_launch(ctx, "threshold_counts");
                 exclusive_sum_u32_to_u64(ctx, d_thr, d_pos.p, n1);
-                HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)limit + 4) * 4, st));
+                HSAW_CUDA_CHECK(cudaMemsetAsync(d_fill.p, 0, ((uint64_t)rlimit + 4) * 4, st));
             }
-            HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], d_pos.p + limit, 8,
+            HSAW_CUDA_CHECK(cudaMemcpyAsync(&ctx->h_scalars[0], d_pos.p + rlimit, 8,
                                             cudaMemcpyDeviceToHost, st));
             HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
             const uint64_t indexed = ctx->h_scalars[0];
@@ -1035,20 +1342,25 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             if (indexed) {
                 StageScope timer(ctx, HSAW_STAGE_INDEX);
                 int sb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
-                DevVec<uint32_t>& d_ibits = ctx->g_indexed_bits;
-                uint64_t words = ((uint64_t)limit + 31) / 32;
-                d_ibits.ensure_scratch(words + 1);
-                const BitFilter filt = prepare_filter(ctx, limit, indexed);
-                mark_indexed<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(
-                    d_cnt.p, limit, min_count, d_ibits.p, const_cast<uint32_t*>(filt.bits), filt.log2);
-                check_launch(ctx, "mark_indexed");
-                scatter_inverted<<<sb, 256, 0, st>>>(v, d_ibits.p, filt, d_pos.p, d_fill.p, d_inv.p);
+                if (dense) {
+                    scatter_inverted<<<sb, 256, 0, st>>>(rv, nullptr, BitFilter{nullptr, 0}, d_pos.p,
+                                                         d_fill.p, d_inv.p);
+                } else {
+                    DevVec<uint32_t>& d_ibits = ctx->g_indexed_bits;
+                    uint64_t words = ((uint64_t)limit + 31) / 32;
+                    d_ibits.ensure_scratch(words + 1);
+                    const BitFilter filt = prepare_filter(ctx, limit, indexed);
+                    mark_indexed<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(
+                        rcnt, limit, min_count, d_ibits.p, const_cast<uint32_t*>(filt.bits), filt.log2);
+                    check_launch(ctx, "mark_indexed");
+                    scatter_inverted<<<sb, 256, 0, st>>>(rv, d_ibits.p, filt, d_pos.p, d_fill.p, d_inv.p);
+                }
                 check_launch(ctx, "scatter_inverted");
             }
             // ---- rounds
             if (p1 > p0) {
                 StageScope timer(ctx, HSAW_STAGE_ROUNDS);
-                block_maxima<<<nblk, 256, 0, st>>>(d_cnt.p, limit, d_blkmax.p, bshift);
+                block_maxima<<<nblk, 256, 0, st>>>(rcnt, rlimit, d_blkmax.p, bshift);
                 check_launch(ctx, "block_maxima");
             }
             done = 0;
@@ -1079,7 +1391,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                     {
                         StageScope timer(ctx, HSAW_STAGE_ROUNDS);
                         greedy_tail_kernel<<<1, 1024, tail_smem, st>>>(
-                            v, d_cand, d_pos.p, d_inv.p, d_cnt.p, d_cov.p, d_blkmax.p, nblk, done,
+                            rv, d_cand, d_pos.p, d_inv.p, rcnt, d_cov.p, d_blkmax.p, nblk, done,
                             k, d_sol.p, d_gain.p, min_count, kMaxTailList, d_done,
                             blkmax_fresh ? 1 : 0, bshift);
                         blkmax_fresh = false;  // the tail's own rounds decrement counts
@@ -1096,11 +1408,11 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                     uint32_t group = std::min<uint32_t>(k - done, tail_ok ? 4 : 64);
                     StageScope timer(ctx, HSAW_STAGE_ROUNDS);
                     for (uint32_t r = done; r < done + group; ++r) {
-                        select_lazy<<<1, 1024, 0, st>>>(d_cnt.p, limit, d_blkmax.p, nblk,
+                        select_lazy<<<1, 1024, 0, st>>>(rcnt, rlimit, d_blkmax.p, nblk,
                                                         d_partial.p, bshift);
                         check_launch(ctx, "select_lazy");
                         cover_winner<<<cover_blocks, 256, 0, st>>>(
-                            v, d_partial.p, 1, d_cand, d_pos.p, d_inv.p, d_cnt.p, d_cov.p, r,
+                            rv, d_partial.p, 1, d_cand, d_pos.p, d_inv.p, rcnt, d_cov.p, r,
                             d_sol.p, d_gain.p, min_count);
                         check_launch(ctx, "cover_winner");
                     }
@@ -1125,6 +1437,13 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                     }
                 }
                 done = r;
+            }
+            if (dense && done) {  // the rounds selected ranks of the dense instance: back to ids
+                dense_solution_ids<<<(done + 255) / 256, 256, 0, st>>>(d_sol.p, done, rlimit, x_ids.p);
+                check_launch(ctx, "dense_solution_ids");
+                HSAW_CUDA_CHECK(cudaMemcpyAsync(h_sol.data(), d_sol.p, done * 4ull,
+                                                cudaMemcpyDeviceToHost, st));
+                HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
             }
             return true;
         };
@@ -1348,15 +1667,16 @@ int hsaw_gpu_coverage_upper_bound(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stre
         const uint32_t* d_cand = cand_ids ? cand_bits.p : nullptr;
         DevVec<uint32_t>& d_cnt = ctx->g_cnt;
         DevVec<uint64_t>& d_partial = ctx->g_partial;
-        d_cnt.ensure_scratch((uint64_t)limit + 4);
         d_partial.ensure_scratch(kCountBins + 4);
         uint64_t p0 = 0, p1 = 0;
         view_span(ctx, v, &p0, &p1);
         if (p1 == p0) return;
-        const uint32_t* counts = d_cnt.p;
+        const uint32_t* counts = nullptr;
         if (hist_cache_usable(stream, cand_ids)) {
             counts = hist_segment(ctx, stream, kind, limit, off, off + cnt);
         } else {
+            d_cnt.ensure_scratch((uint64_t)limit + 4);
+            counts = d_cnt.p;
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
             histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
         }
@@ -1364,7 +1684,7 @@ int hsaw_gpu_coverage_upper_bound(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stre
         HSAW_CUDA_CHECK(cudaMemsetAsync(d_bins, 0, kCountBins * 8, st));
         {
             StageScope timer(ctx, HSAW_STAGE_INDEX);
-            count_of_counts<<<ctx->sm_count * 8, 256, 0, st>>>(counts, limit, d_bins);
+            count_of_counts<<<ctx->sm_count * 8, kCocWarps * 32, 0, st>>>(counts, limit, d_bins);
             check_launch(ctx, "count_of_counts");
         }
         std::vector<uint64_t> bins(kCountBins);
@@ -1550,7 +1870,7 @@ static std::vector<uint64_t> count_bins(hsaw_gpu_ctx* ctx, const uint32_t* d_cou
     HSAW_CUDA_CHECK(cudaMemsetAsync(d_bins, 0, kCountBins * 8, ctx->stream));
     {
         StageScope timer(ctx, HSAW_STAGE_INDEX);
-        count_of_counts<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(d_counts, limit, d_bins);
+        count_of_counts<<<ctx->sm_count * 8, kCocWarps * 32, 0, ctx->stream>>>(d_counts, limit, d_bins);
         check_launch(ctx, "count_of_counts");
     }
     std::vector<uint64_t> bins(kCountBins);

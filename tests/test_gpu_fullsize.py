@@ -146,6 +146,21 @@ def test_solver_equals_the_reference_at_full_size(monkeypatch, c2, c2_golden, la
         assert r[key] == gold[key], key
 
 
+@pytest.mark.parametrize("name,kind,k", [("esia_k100", 0, 100), ("nsia_k100", 1, 100),
+                                         ("esia_k1000", 0, 1000)])
+def test_solver_on_dense_instances_equals_the_reference(monkeypatch, c2, c2_golden, name, kind, k):
+    """The same full-size goldens with every greedy run forced onto the dense reduced instance
+    (greedy.cu build_dense; production switches to it from 256 MB of counters, i.e. above C2):
+    thresholded index, renamed items, (start, length) walks, rank -> id mapping of the solution."""
+    from paper_1702_05854_b200 import hostapi
+    g, csr, _ = c2
+    gold = c2_golden[name]
+    monkeypatch.setenv("HSAW_DENSE_MIN_BYTES", "0")
+    r = hostapi.interdict(g, csr.p_of, kind, k, 0.1, 1.0 / g.n, seed=42, max_attempts=10**15)
+    for key in RESULT_KEYS:
+        assert r[key] == gold[key], key
+
+
 def test_fixed_walk_set_greedy_at_full_size(gpu_lib, monkeypatch, c2, c2_golden):
     """north_star's mode 1 at real size: the device pool IS the reference's walk set of the last
     eSIA iteration (sha256 over lengths, nodes and edge ids of 7.7 M walks / 360 M items), and the

@@ -9,6 +9,18 @@ from conftest import make_csr, upload
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["full-ids", "dense"])
+def instance_form(request, monkeypatch):
+    """Every test of this module runs twice: on the id space as given, and with the dense reduced
+    instance forced (greedy.cu build_dense: indexed items renamed 0..D-1, walks restricted to them;
+    production uses it from 256 MB of counters upwards, i.e. the LiveJournal shape and beyond)."""
+    if request.param == "dense":
+        monkeypatch.setenv("HSAW_DENSE_MIN_BYTES", "0")
+    else:
+        monkeypatch.setenv("HSAW_DENSE_MIN_BYTES", str(1 << 60))
+    return request.param
+
+
 def to_csr_sets(sets):
     off = np.zeros(len(sets) + 1, dtype=np.uint64)
     np.cumsum([len(s) for s in sets], out=off[1:])
