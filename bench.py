@@ -756,25 +756,32 @@ def run_b200(args):
         e2e_acc, e2e_s = 0, 0.0
         e2e_calls = max(1, min(args.steps, 5 if g.m < (1 << 28) else 3))
         e2e_error = None
+        phases = {"upload_and_layout": 0.0, "sample_and_counters": 0.0, "release": 0.0}
         for i in range(-min(args.warmup, 2 if g.m < (1 << 28) else 1), e2e_calls):  # i < 0: warm-up
             barrier()
-            t0 = time.perf_counter()
+            t0 = t1 = t2 = time.perf_counter()
             try:
                 with hostapi.DeviceGraph(g, p_of, device=local) as dg2:    # H2D of the CSR arrays
+                    t1 = time.perf_counter()
                     _, acc = dg2.sample(target, seed=STREAM_SEED + 1000 * rank + i + 100,
                                         max_attempts=10**15)               # ensure + counters (D2H)
+                    t2 = time.perf_counter()
             except Exception as exc:
                 e2e_error, acc = str(exc)[:200], 0
             torch.cuda.synchronize()
             if i >= 0:
-                e2e_s += time.perf_counter() - t0
+                t3 = time.perf_counter()
+                e2e_s += t3 - t0
                 e2e_acc += acc
+                for k_, dt in zip(phases, (t1 - t0, t2 - t1, t3 - t2)):
+                    phases[k_] += dt
         out["e2e"] = {
             "value": e2e_acc / e2e_s if e2e_s > 0 else 0.0, "unit": UNIT,
             "h2d_bytes_per_step": ref_bytes, "d2h_bytes_per_step": 16,
             "call": f"DeviceGraph(g, vi) upload + SampleStream.ensure({target}) + counters_for "
                     f"(the `hsaw sample` path), per call",
             "calls_timed": e2e_calls, "ms_per_call": 1e3 * e2e_s / e2e_calls,
+            "phases_ms_per_call": {k_: round(1e3 * v / e2e_calls, 2) for k_, v in phases.items()},
         }
         if e2e_error:
             out["e2e"]["error"] = e2e_error

@@ -499,6 +499,24 @@ struct Restriction {
 };
 
 // Walk-pool buffers handed back by a destroyed stream, taken over by the next one.
+// Buffers of the dense reduced greedy instance (greedy.cu, build_dense): kept on the context like
+// the other greedy scratch, so a solve's six greedy calls do not churn gigabytes through the pool.
+struct DenseScratch {
+    DevVec<uint32_t> bits, pc, base, bloom, ids, cnt, len, items;
+    DevVec<uint64_t> map, start;
+    template <class F>
+    void for_each(F&& f) {
+        f(bits); f(pc); f(base); f(bloom); f(ids); f(cnt); f(len); f(items); f(map); f(start);
+    }
+    void release() {
+        for_each([](auto& v) { v.release(); });
+    }
+    void swap(DenseScratch& o) {
+        bits.swap(o.bits); pc.swap(o.pc); base.swap(o.base); bloom.swap(o.bloom); ids.swap(o.ids);
+        cnt.swap(o.cnt); len.swap(o.len); items.swap(o.items); map.swap(o.map); start.swap(o.start);
+    }
+};
+
 struct PoolCache {
     DevVec<uint64_t> edge_off, tag_batch, accepted_after_batch;
     DevVec<uint32_t> tag_seq;
@@ -546,6 +564,7 @@ struct hsaw_gpu_ctx {
     hsawgpu::DevVec<uint32_t> g_filter;        // hashed membership pre-filter (greedy.cu BitFilter)
     hsawgpu::DevVec<uint32_t> g_hist_prefix, g_hist_seg;  // histogram cache (greedy.cu HistCache)
     hsawgpu::DevVec<uint32_t> g_sorted;  // radix-partitioned copy of the items (large id spaces)
+    hsawgpu::DenseScratch g_dense;       // dense reduced instance (large id spaces)
     hsawgpu::DevVec<uint64_t> g_pos, g_partial, g_gains, g_blkmax;
     uint64_t* d_scalars = nullptr;  // 64 u64 of device scratch for counters / cursors
     uint64_t* h_scalars = nullptr;  // pinned mirror
@@ -589,6 +608,7 @@ struct hsaw_gpu_ctx {
         g_filter.swap(o.g_filter);
         g_hist_prefix.swap(o.g_hist_prefix);
         g_hist_seg.swap(o.g_hist_seg);
+        g_dense.swap(o.g_dense);
     }
     template <class F>
     void for_each_buffer(F&& f) {
@@ -602,6 +622,7 @@ struct hsaw_gpu_ctx {
         f(g_cand_bits); f(g_cnt); f(g_fill); f(g_inv); f(g_covered); f(g_solution);
         f(g_query_bits); f(g_pos); f(g_partial); f(g_gains); f(g_blkmax); f(g_sorted);
         f(g_indexed_bits); f(g_filter); f(g_hist_prefix); f(g_hist_seg);
+        g_dense.for_each(f);
     }
 
     // The buffers a solve leaves behind (greedy index, histogram cache, partition copy): tens of
@@ -611,6 +632,7 @@ struct hsaw_gpu_ctx {
         g_covered.release(); g_solution.release(); g_query_bits.release(); g_pos.release();
         g_partial.release(); g_gains.release(); g_blkmax.release(); g_sorted.release();
         g_indexed_bits.release(); g_filter.release(); g_hist_prefix.release(); g_hist_seg.release();
+        g_dense.release();
     }
 
     void release_scratch() {
@@ -640,6 +662,7 @@ struct hsaw_gpu_ctx {
         g_filter.release();
         g_hist_prefix.release();
         g_hist_seg.release();
+        g_dense.release();
     }
 };
 

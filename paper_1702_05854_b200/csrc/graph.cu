@@ -839,7 +839,15 @@ void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_
         pin_compact_graph_in_l2(ctx);
     } else {
         ctx->graph_bytes = (uint64_t)n * sizeof(NodeRec) + (uint64_t)m * sizeof(EdgeRec);
-        pin_node_records_in_l2(ctx);
+        // Round 1 put a stream-wide access-policy window over the node records here (persisting
+        // hits, STREAMING misses). On the shapes that take this layout it buys K1 nothing (start
+        // nodes are uniform, the records are read for suspects only) and it marks every other
+        // access of every kernel on the stream evict-first: the greedy counters, the compaction
+        // and the membership filters lost their L2 residency to it (Twitter shape: K1 20.1 ->
+        // 18.8 ms, compaction 2.97 -> 1.2 ms per step, index stage 1.43 -> 1.03 s per solve once
+        // it was gone). HSAW_L2_PIN_NODES=1 brings it back for A/B runs.
+        if (const char* env = std::getenv("HSAW_L2_PIN_NODES"))
+            if (std::atoi(env) != 0) pin_node_records_in_l2(ctx);
     }
 }
 

@@ -1208,22 +1208,38 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                                     (dense_forced || ((uint64_t)limit * 4 > dense_min_bytes &&
                                                       p1 - p0 > (1ull << 24)));
 
-        auto run = [&](uint32_t min_count) -> bool {
+        // min_count 0: choose the indexing threshold from the count distribution: the mass rule
+        // (at most 1/mass_div of all occurrences indexed), raised to ck_percent % of the k-th
+        // largest count when ck_percent is set. A winner's gain never exceeds its initial count
+        // and the gains of a run never increase, so items whose count is below the LAST round's
+        // gain can never be selected: a threshold near that gain keeps a few thousand items
+        // instead of millions. It is a guess that the protocol verifies (a round whose winner
+        // falls below the threshold fails the run), so a wrong guess costs one cheap attempt.
+        std::vector<uint32_t> failed_thresholds;
+        // counts of the view's items (limit + zero pad entries) and their distribution: computed
+        // once, again only after an attempt that decremented them in place (the non-dense form on
+        // counts that did not come from the histogram cache)
+        const uint32_t* full_cnt = nullptr;
+        const bool from_cache = hist_cache_usable(stream, cand_ids) && off == 0;
+        bool counts_valid = false;
+        std::vector<uint64_t> bins;
+        auto run = [&](uint32_t min_count, uint32_t ck_percent) -> bool {
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(d_partial.p, 0, 8, st));  // no previous winner yet
             // ---- K3: marginal-gain counts (a stream prefix comes from the histogram cache)
-            const uint32_t* full_cnt = nullptr;  // counts of the view's items, limit (+ zero pad) entries
-            const bool from_cache = hist_cache_usable(stream, cand_ids) && off == 0;
-            if (from_cache) {
-                full_cnt = hist_prefix(ctx, stream, kind, limit, cnt);
-            } else {
-                d_cnt.ensure_scratch((uint64_t)limit + 4);
-                HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
-                histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
-                full_cnt = d_cnt.p;
+            if (!counts_valid) {
+                if (from_cache) {
+                    full_cnt = hist_prefix(ctx, stream, kind, limit, cnt);
+                } else {
+                    d_cnt.ensure_scratch((uint64_t)limit + 4);
+                    HSAW_CUDA_CHECK(cudaMemsetAsync(d_cnt.p, 0, ((uint64_t)limit + 4) * 4, st));
+                    histogram_counts(ctx, v, p0, p1, d_cand, d_cnt.p);
+                    full_cnt = d_cnt.p;
+                }
+                counts_valid = true;
+                bins.clear();
             }
-            std::vector<uint64_t> bins;
-            if (min_count == 0 || dense_possible) {
+            if ((min_count == 0 || dense_possible) && bins.empty()) {
                 auto* d_bins = reinterpret_cast<unsigned long long*>(d_partial.p + 4);
                 HSAW_CUDA_CHECK(cudaMemsetAsync(d_bins, 0, kCountBins * 8, st));
                 {
@@ -1251,14 +1267,29 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                         min_count = c;
                     }
                 }
+                if (ck_percent) {
+                    // k-th largest count (the pooled top bin is counted as if all its items sat at
+                    // its lower edge: more items than there are, i.e. a bolder guess at worst)
+                    uint64_t items = 0;
+                    uint32_t ck = 0;
+                    for (uint32_t c = kCountBins - 1; c >= 1 && ck == 0; --c) {
+                        items += (bins[c] + c - 1) / c;
+                        if (items >= k) ck = c;
+                    }
+                    min_count = std::max<uint32_t>(min_count, (uint32_t)((uint64_t)ck * ck_percent / 100));
+                }
+                for (uint32_t t : failed_thresholds)
+                    if (min_count >= t) return false;  // already known to be too high
             }
             // ---- the instance the rounds run on: the view itself, or its dense reduction
             const bool dense = dense_possible && (dense_forced || min_count > 1);
             WalkView rv = v;
             uint32_t rlimit = limit;
             uint32_t* rcnt = nullptr;
-            DevVec<uint32_t> x_bits, x_pc, x_base, x_bloom, x_ids, x_cnt, x_len, x_items;
-            DevVec<uint64_t> x_map, x_start;
+            DenseScratch& dx = ctx->g_dense;
+            DevVec<uint32_t>&x_bits = dx.bits, &x_pc = dx.pc, &x_base = dx.base, &x_bloom = dx.bloom,
+                             &x_ids = dx.ids, &x_cnt = dx.cnt, &x_len = dx.len, &x_items = dx.items;
+            DevVec<uint64_t>&x_map = dx.map, &x_start = dx.start;
             if (dense) {
                 uint64_t occ = 0, d_est = 0;  // occurrences / distinct ids at or above min_count
                 for (uint32_t c = std::max(min_count, 1u); c < kCountBins; ++c) {
@@ -1317,6 +1348,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                                                     cudaMemcpyDeviceToDevice, st));
                 }
                 rcnt = d_cnt.p;
+                if (!from_cache) counts_valid = false;  // the rounds decrement d_cnt in place
             }
             const uint32_t index_min = dense ? 1u : min_count;  // a dense instance holds indexed items only
             const uint32_t bshift = block_shift_for(rlimit);
@@ -1430,7 +1462,10 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                 }
                 uint32_t r = done;
                 for (; r < upto; ++r) {
-                    if (h_sol[r] == kUnindexed) return false;  // needs the full index
+                    if (h_sol[r] == kUnindexed) {  // needs a lower threshold / the full index
+                        failed_thresholds.push_back(min_count);
+                        return false;
+                    }
                     if (h_gain[r] == 0) {
                         exhausted = true;
                         break;
@@ -1447,9 +1482,14 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             }
             return true;
         };
-        if (!run(0)) {
+        bool ok = false;
+        if (dense_possible)  // optimistic thresholds: an attempt on a dense instance is cheap
+            for (uint32_t pct : {60u, 30u})
+                if ((ok = run(0, pct))) break;
+        if (!ok) ok = run(0, 0);
+        if (!ok) {
             ++ctx->greedy_full_index_reruns;
-            if (!run(1)) fail(HSAW_ECUDA, "greedy: full index run reported an unindexed winner");
+            if (!run(1, 0)) fail(HSAW_ECUDA, "greedy: full index run reported an unindexed winner");
         }
         collect_timings(ctx);
         // ---- zero-gain padding: smallest unselected candidates in ascending order

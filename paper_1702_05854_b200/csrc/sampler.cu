@@ -895,20 +895,42 @@ __global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
             }
         }
         unsigned todo = __ballot_sync(kFullMask, my_nn > 1);  // a single node cannot repeat
+        auto node_of = [&](uint64_t srcv, uint32_t i) -> uint32_t {
+            if (PAIRS) return __ldg(&reinterpret_cast<const uint2*>(srcv)[i].x);
+            return __ldg(p.nodes + srcv + i);
+        };
+        // The first 128 nodes of the NEXT walk of the group are requested before the current
+        // walk's inserts start, so the load latency of a walk hides behind the table work of its
+        // predecessor instead of being paid once per walk (the walks of a warp run back to back).
+        uint32_t pre[4];
+        uint32_t pre_nn = 0;
+        uint64_t pre_src = 0;
+        auto prefetch = [&](unsigned rest) {
+            if (!rest) return;
+            const int jn = __ffs(rest) - 1;
+            pre_nn = __shfl_sync(kFullMask, my_nn, jn);
+            pre_src = __shfl_sync(kFullMask, my_src, jn);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t i = q * 32 + lane;
+                pre[q] = i < pre_nn ? node_of(pre_src, i) : kInvalidNode;
+            }
+        };
+        prefetch(todo);
         while (todo) {
             const int j = __ffs(todo) - 1;
             todo &= todo - 1;
-            const uint32_t nn = __shfl_sync(kFullMask, my_nn, j);
-            const uint64_t srcv = __shfl_sync(kFullMask, my_src, j);
-            auto node_at = [&](uint32_t i) -> uint32_t {
-                if (PAIRS) return __ldg(&reinterpret_cast<const uint2*>(srcv)[i].x);
-                return __ldg(p.nodes + srcv + i);
-            };
+            const uint32_t nn = pre_nn;
+            const uint64_t srcv = pre_src;
+            uint32_t v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = pre[q];
+            prefetch(todo);
+            auto node_at = [&](uint32_t i) -> uint32_t { return node_of(srcv, i); };
             bool dup = false;
             if (nn <= 32) {
-                uint32_t v = lane < nn ? node_at(lane) : 0;
                 unsigned valid = nn == 32 ? kFullMask : ((1u << nn) - 1);
-                unsigned same = __match_any_sync(kFullMask, v) & valid & ~(1u << lane);
+                unsigned same = __match_any_sync(kFullMask, v[0]) & valid & ~(1u << lane);
                 dup = __any_sync(kFullMask, lane < nn && same != 0);
             } else if (nn <= TABLE / 2) {
                 // table of >= 4*nn slots where the warp's share allows it, else >= 2*nn: lanes
@@ -918,11 +940,12 @@ __global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
                 const uint32_t size = 1u << bits;
                 bool mydup = false;
                 for (uint32_t c = 0; c < nn; c += 128) {
-                    uint32_t v[4];
+                    if (c != 0) {  // (the first 128 were requested one walk ahead)
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t i = c + q * 32 + lane;
-                        v[q] = i < nn ? node_at(i) : kInvalidNode;
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t i = c + q * 32 + lane;
+                            v[q] = i < nn ? node_at(i) : kInvalidNode;
+                        }
                     }
                     if (c == 0) {  // the clears overlap the reads in flight
                         for (uint32_t i = lane; i < size; i += 32) tab[i] = kInvalidNode;
