@@ -756,12 +756,16 @@ def run_b200(args):
         e2e_acc, e2e_s = 0, 0.0
         e2e_calls = max(1, min(args.steps, 5 if g.m < (1 << 28) else 3))
         e2e_error = None
+        # the caller's own objects, built once: ProbGraph (g) and SuspectSet (vi), the two arguments
+        # of hsaw::DeviceGraph(g, vi) / stream_samples(g, vi, ...) in the reference's API
+        vi = hostapi.Suspects(g, p_of)
         phases = {"upload_and_layout": 0.0, "sample_and_counters": 0.0, "release": 0.0}
-        for i in range(-min(args.warmup, 2 if g.m < (1 << 28) else 1), e2e_calls):  # i < 0: warm-up
+        # (two warm-up calls: the first allocates the stores, the second still grows the pool)
+        for i in range(-min(args.warmup, 2), e2e_calls):  # i < 0: warm-up
             barrier()
             t0 = t1 = t2 = time.perf_counter()
             try:
-                with hostapi.DeviceGraph(g, p_of, device=local) as dg2:    # H2D of the CSR arrays
+                with hostapi.DeviceGraph(g, vi, device=local) as dg2:      # H2D of the CSR arrays
                     t1 = time.perf_counter()
                     _, acc = dg2.sample(target, seed=STREAM_SEED + 1000 * rank + i + 100,
                                         max_attempts=10**15)               # ensure + counters (D2H)
@@ -769,6 +773,9 @@ def run_b200(args):
             except Exception as exc:
                 e2e_error, acc = str(exc)[:200], 0
             torch.cuda.synchronize()
+            if os.environ.get("HSAW_UPLOAD_TIMING"):
+                print(f"[bench e2e] call {i}: DeviceGraph {1e3 * (t1 - t0):.1f} ms, sample "
+                      f"{1e3 * (t2 - t1):.1f} ms", file=sys.stderr)
             if i >= 0:
                 t3 = time.perf_counter()
                 e2e_s += t3 - t0

@@ -65,6 +65,12 @@ int hsawh_check(double cov_r, double cov_rp, double n_rp, uint64_t M, uint32_t k
 /* ---- device graph (hsaw::DeviceGraph) ---- */
 int hsawh_device_create(const void* g, const double* p_of, int device, void* cuda_stream,
                         void** out);
+/* the same with a prebuilt hsaw::SuspectSet handle (hsawh_suspects_create), i.e. exactly the
+ * arguments of hsaw::DeviceGraph(const ProbGraph&, const SuspectSet&, int device) */
+int hsawh_suspects_create(const void* g, const double* p_of, void** out);
+void hsawh_suspects_free(void* vi);
+int hsawh_device_create_vi(const void* g, const void* vi, int device, void* cuda_stream,
+                           void** out);
 void hsawh_device_free(void* dg);
 void* hsawh_device_ctx(const void* dg); /* the hsaw_gpu_ctx* underneath */
 

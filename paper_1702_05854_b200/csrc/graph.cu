@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "walk.cuh"
 
 using namespace hsawgpu;
 
@@ -62,20 +63,21 @@ __global__ void update_accept_thresholds(uint32_t n, const double* __restrict__ 
 }
 
 // Row header of node u as the edge records carry it: simple iff the total-weight threshold is
-// within 2^32 draw units of 2^53 (always the case for 1/d rows) or the row is empty.
-__device__ __forceinline__ void source_header(const uint64_t* __restrict__ off,
-                                              const double* __restrict__ cum,
-                                              const double* __restrict__ p_of, uint32_t u,
+// within 2^32 draw units of 2^53 (always the case for 1/d rows) or the row is empty. Read from
+// u's node record (built first): ONE 32-byte gather per edge. The first version went back to the
+// CSR (offset pair -> last cumulative weight of the row, plus p_of): three dependent DRAM lines
+// per edge, 76 ms for the 1.47 G edges of the Twitter shape.
+__device__ __forceinline__ void source_header(const NodeRec* __restrict__ nodes, uint32_t u,
                                               EdgeRec& r) {
-    uint64_t lo = off[u], hi = off[u + 1];
-    r.src_lo = (uint32_t)lo;
-    r.src_deg = (uint32_t)(hi - lo);
+    const NodeRec s = load_node(nodes, u);
+    r.src_lo = s.lo;
+    r.src_deg = s.deg;
     r.src_deficit = 0;
-    r.flags = p_of[u] > 0.0 ? kEdgeSuspect : 0u;
-    if (hi == lo) {
+    r.flags = s.acc_thr != 0 ? kEdgeSuspect : 0u;  // acc_thr != 0 <=> p_of[u] > 0
+    if (s.deg == 0) {
         r.flags |= kEdgeSimple;
     } else {
-        uint64_t deficit = (1ull << 53) - ge_threshold(cum[hi - 1]);
+        uint64_t deficit = (1ull << 53) - s.tot_thr;  // tot_thr = ge_threshold(cum[hi - 1]) <= 2^53
         if (deficit <= 0xFFFFFFFFull) {
             r.src_deficit = (uint32_t)deficit;
             r.flags |= kEdgeSimple;
@@ -89,7 +91,7 @@ __device__ __forceinline__ void edge_row_slice(uint32_t v, uint32_t n, uint64_t 
                                                const uint64_t* __restrict__ off,
                                                const uint32_t* __restrict__ src,
                                                const double* __restrict__ cum,
-                                               const double* __restrict__ p_of,
+                                               const NodeRec* __restrict__ nodes,
                                                EdgeRec* __restrict__ out,
                                                uint32_t* __restrict__ bad_row) {
     for (uint64_t e = lo + first; e < hi; e += stride) {
@@ -109,7 +111,7 @@ __device__ __forceinline__ void edge_row_slice(uint32_t v, uint32_t n, uint64_t 
             atomicMin(bad_row + 1, v);  // source id out of range
             r.src_lo = r.src_deg = r.src_deficit = r.flags = 0;
         } else {
-            source_header(off, cum, p_of, r.src, r);
+            source_header(nodes, r.src, r);
         }
         out[e] = r;
     }
@@ -119,7 +121,7 @@ __device__ __forceinline__ void edge_row_slice(uint32_t v, uint32_t n, uint64_t 
 // build_edge_records_big (one block per row) so that hub rows are not a single warp's tail.
 __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
                                    const uint32_t* __restrict__ src, const double* __restrict__ cum,
-                                   const double* __restrict__ p_of, EdgeRec* __restrict__ out,
+                                   const NodeRec* __restrict__ nodes, EdgeRec* __restrict__ out,
                                    uint32_t* __restrict__ bad_row, uint32_t* __restrict__ big_rows,
                                    uint32_t* __restrict__ big_count, uint32_t big_cap) {
     uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -136,19 +138,19 @@ __global__ void build_edge_records(uint32_t n, const uint64_t* __restrict__ off,
                 continue;
             }
         }
-        edge_row_slice(v, n, lo, hi, lane, 32, off, src, cum, p_of, out, bad_row);
+        edge_row_slice(v, n, lo, hi, lane, 32, off, src, cum, nodes, out, bad_row);
     }
 }
 
 __global__ void __launch_bounds__(256) build_edge_records_big(
     uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ src,
-    const double* __restrict__ cum, const double* __restrict__ p_of, EdgeRec* __restrict__ out,
+    const double* __restrict__ cum, const NodeRec* __restrict__ nodes, EdgeRec* __restrict__ out,
     uint32_t* __restrict__ bad_row, const uint32_t* __restrict__ big_rows,
     const uint32_t* __restrict__ big_count, uint32_t big_cap) {
     const uint32_t count = min(*big_count, big_cap);
     for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
         const uint32_t v = big_rows[i];
-        edge_row_slice(v, n, off[v], off[v + 1], threadIdx.x, blockDim.x, off, src, cum, p_of, out,
+        edge_row_slice(v, n, off[v], off[v + 1], threadIdx.x, blockDim.x, off, src, cum, nodes, out,
                        bad_row);
     }
 }
@@ -495,7 +497,9 @@ private:
         static std::map<int, State> per_device;
         State& st = per_device[device];
         if (st.nthreads) return st;
-        int want = 4;
+        // 8 copier threads reach the pinned-DMA rate of a Gen5 x16 link from pageable memory
+        // (tools/upload_probe.cu on the B200 box: 4 threads 47 GB/s, 8 threads 51, pinned 55.6)
+        int want = 8;
         if (const char* env = std::getenv("HSAW_UPLOAD_THREADS")) want = std::atoi(env);
         unsigned hw = std::thread::hardware_concurrency();
         if (hw && (unsigned)want > hw) want = (int)hw;
@@ -813,11 +817,11 @@ void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_
                                                 cudaMemcpyDeviceToDevice, st));
             }
         } else if (m) {
-            build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, d_p, ctx->g.edges,
+            build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, ctx->g.nodes, ctx->g.edges,
                                                        d_bad, big_rows, big_count, big_cap);
             check_launch(ctx, "build_edge_records");
             build_edge_records_big<<<ctx->sm_count * 2, 256, 0, st>>>(
-                n, d_off, d_src, d_cum, d_p, ctx->g.edges, d_bad, big_rows, big_count, big_cap);
+                n, d_off, d_src, d_cum, ctx->g.nodes, ctx->g.edges, d_bad, big_rows, big_count, big_cap);
             check_launch(ctx, "build_edge_records_big");
         }
     }
@@ -954,16 +958,30 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
         if (n == 0) fail(HSAW_EDATA, "graph: no nodes");
         if (!in_offsets || !p_of || (m && (!in_src || !in_cum)))
             fail(HSAW_EINVAL, "graph_upload: null array");
-        if (in_offsets[0] != 0 || in_offsets[n] != m)
-            fail(HSAW_EDATA, "graph: offsets do not cover edge range");
-        for (uint32_t v = 0; v < n; ++v)
-            if (in_offsets[v + 1] < in_offsets[v]) fail(HSAW_EDATA, "graph: offsets not monotone");
         // HSAW_UPLOAD_TIMING=1: phase times of this call on stderr (host clock, stream synchronised)
         static const bool timing = [] {
             const char* env = std::getenv("HSAW_UPLOAD_TIMING");
             return env && std::atoi(env) != 0;
         }();
         auto t_last = std::chrono::steady_clock::now();
+        if (in_offsets[0] != 0 || in_offsets[n] != m)
+            fail(HSAW_EDATA, "graph: offsets do not cover edge range");
+        {   // 41.6 M offsets at the Twitter shape: 40 ms on one core, shared out over eight
+            const unsigned parts = n > (1u << 22) ? 8u : 1u;
+            std::vector<uint8_t> bad(parts, 0);
+            auto scan = [&](unsigned t) {
+                const uint64_t a = (uint64_t)n * t / parts, b = (uint64_t)n * (t + 1) / parts;
+                uint8_t any = 0;
+                for (uint64_t v = a; v < b; ++v) any |= in_offsets[v + 1] < in_offsets[v];
+                bad[t] = any;
+            };
+            std::vector<std::thread> pool;
+            for (unsigned t = 1; t < parts; ++t) pool.emplace_back(scan, t);
+            scan(0);
+            for (auto& th : pool) th.join();
+            for (uint8_t x : bad)
+                if (x) fail(HSAW_EDATA, "graph: offsets not monotone");
+        }
         auto lap = [&](const char* what) {
             if (!timing) return;
             cudaStreamSynchronize(ctx->stream);

@@ -103,6 +103,45 @@ __global__ void key_histogram(const uint32_t* __restrict__ keys, uint64_t n, uin
     }
 }
 
+// K3 for large id spaces, shared-memory form. Random counter updates in global memory run at
+// ~40 G/s on this device whatever the window they fall into (L2 misses when the window is wide,
+// same-sector serialisation when it is narrow: measured with 8..20 partition bits). So the keys
+// are sorted on their top bits down to windows of 2^wbits ids (<= 128 KB of counters), one CTA
+// takes a window, counts its keys with shared-memory atomics and adds the window to the global
+// array with plain coalesced read-modify-writes (it is the only writer of that range).
+__global__ void bucket_starts(const uint32_t* __restrict__ keys, uint64_t n, uint32_t wbits,
+                              uint32_t nbuckets, uint64_t* __restrict__ starts) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t b = min(keys[i] >> wbits, nbuckets);  // ids >= limit: past the last window
+    const uint32_t prev = i ? min(keys[i - 1] >> wbits, nbuckets) : 0u;
+    for (uint32_t x = i ? prev + 1 : 0u; x <= b; ++x) starts[x] = i;
+    if (i == n - 1)
+        for (uint32_t x = b + 1; x <= nbuckets; ++x) starts[x] = n;
+}
+
+__global__ void __launch_bounds__(1024) window_histogram(const uint32_t* __restrict__ keys,
+                                                         const uint64_t* __restrict__ starts,
+                                                         uint32_t wbits, uint32_t limit,
+                                                         const uint32_t* __restrict__ cand_bits,
+                                                         uint32_t* __restrict__ cnt) {
+    extern __shared__ uint32_t win[];
+    const uint32_t W = 1u << wbits;
+    const uint64_t a = starts[blockIdx.x], b = starts[blockIdx.x + 1];
+    if (a == b) return;
+    for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) win[i] = 0;
+    __syncthreads();
+    for (uint64_t p = a + threadIdx.x; p < b; p += blockDim.x)
+        atomicAdd(&win[__ldcs(keys + p) & (W - 1)], 1u);
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x << wbits;
+    for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
+        const uint32_t c = win[i];
+        const uint64_t id = base + i;
+        if (c && id < limit && is_cand(cand_bits, (uint32_t)id)) cnt[id] += c;
+    }
+}
+
 // K3b: one warp per walk; slot order inside an item's list is irrelevant (set semantics).
 // One bit per item: is it indexed (candidate with count >= min_count)? The bitmap (limit / 8
 // bytes) stays in L2, so the scatter pass needs no random HBM read per item to find that out.
@@ -940,12 +979,25 @@ static void histogram_counts(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t p0, 
             DevVec<uint32_t>& d_sorted = ctx->g_sorted;
             d_sorted.ensure_scratch(std::min(nitems, kSlice));
             int top = 32 - __builtin_clz(limit - 1);
-            static const int part_bits = [] {  // A/B knob: radix bits of the partition (8 per pass)
+            // HSAW_HIST_BITS: radix bits of the partition (A/B knob). 0 = the shared-memory form:
+            // windows of at most 2^15 ids (128 KB of counters per CTA), two radix passes at the
+            // Twitter shape. Anything else: that many top bits, counted with global atomics.
+            static const int part_bits = [] {
                 const char* env = std::getenv("HSAW_HIST_BITS");
-                const int v = env ? std::atoi(env) : 8;
-                return v < 1 ? 8 : (v > 32 ? 32 : v);
+                const int v = env ? std::atoi(env) : 0;
+                return v < 0 ? 0 : (v > 32 ? 32 : v);
             }();
-            int begin_bit = std::max(0, top - part_bits);
+            const bool windows = part_bits == 0;
+            const int wbits = std::min(15, top);
+            int begin_bit = windows ? wbits : std::max(0, top - part_bits);
+            const uint32_t nbuckets = (uint32_t)(((uint64_t)limit + (1ull << wbits) - 1) >> wbits);
+            DevVec<uint64_t> starts;
+            if (windows) {
+                starts.ensure_scratch((uint64_t)nbuckets + 2);
+                HSAW_CUDA_CHECK(cudaFuncSetAttribute(window_histogram,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)(4u << wbits)));
+            }
             for (uint64_t at = 0; at < nitems; at += kSlice) {
                 const uint64_t len = std::min(kSlice, nitems - at);
                 size_t bytes = 0;
@@ -956,9 +1008,18 @@ static void histogram_counts(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t p0, 
                     ctx->cub_tmp.p, bytes, v.items + p0 + at, d_sorted.p, (int64_t)len, begin_bit,
                     top, st));
                 ++ctx->launches;
-                int sb = (int)std::min<uint64_t>((len + 255) / 256, (uint64_t)wide);
-                key_histogram<<<sb, 256, 0, st>>>(d_sorted.p, len, limit, d_cand, d_cnt);
-                check_launch(ctx, "key_histogram");
+                if (windows) {
+                    bucket_starts<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(
+                        d_sorted.p, len, (uint32_t)wbits, nbuckets, starts.p);
+                    check_launch(ctx, "bucket_starts");
+                    window_histogram<<<nbuckets, 1024, (size_t)4 << wbits, st>>>(
+                        d_sorted.p, starts.p, (uint32_t)wbits, limit, d_cand, d_cnt);
+                    check_launch(ctx, "window_histogram");
+                } else {
+                    int sb = (int)std::min<uint64_t>((len + 255) / 256, (uint64_t)wide);
+                    key_histogram<<<sb, 256, 0, st>>>(d_sorted.p, len, limit, d_cand, d_cnt);
+                    check_launch(ctx, "key_histogram");
+                }
             }
         } else {
             item_histogram<<<hb, 256, 0, st>>>(v, p0, p1, d_cand, d_cnt);
@@ -1467,6 +1528,19 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                         return false;
                     }
                     if (h_gain[r] == 0) {
+                        // A dense instance holds the indexed items only: running out of gain there
+                        // says nothing about the items below the threshold, which still have
+                        // their (smaller) counts - the full-id form would have reported one of
+                        // them as an unindexed winner.
+                        if (dense && min_count > 1) {
+                            bool below = false;
+                            for (uint32_t c = 1; c < min_count && c < kCountBins && !below; ++c)
+                                below = bins[c] != 0;
+                            if (below) {
+                                failed_thresholds.push_back(min_count);
+                                return false;
+                            }
+                        }
                         exhausted = true;
                         break;
                     }

@@ -224,6 +224,20 @@ int hsawh_device_create(const void* g, const double* p_of, int device, void* cud
     });
 }
 
+/* A prebuilt hsaw::SuspectSet (what a C++ caller of DeviceGraph(g, vi) holds already): built once
+ * from the dense p_of array, so repeated device_create calls do not rebuild it. */
+int hsawh_suspects_create(const void* g, const double* p_of, void** out) {
+    return guarded([&] { *out = new SuspectSet(dense_suspects(G(g), p_of)); });
+}
+void hsawh_suspects_free(void* vi) { delete static_cast<SuspectSet*>(vi); }
+
+int hsawh_device_create_vi(const void* g, const void* vi, int device, void* cuda_stream,
+                           void** out) {
+    return guarded([&] {
+        *out = new DeviceGraph(G(g), *static_cast<const SuspectSet*>(vi), device, cuda_stream);
+    });
+}
+
 void hsawh_device_free(void* dg) { delete static_cast<DeviceGraph*>(dg); }
 
 void* hsawh_device_ctx(const void* dg) { return static_cast<const DeviceGraph*>(dg)->ctx(); }

@@ -2,6 +2,8 @@
 // include/hsaw_gpu.h and rethrows its status codes as the exception types the reference uses
 // (std::invalid_argument / DataError / SamplingError / std::out_of_range), so callers and the CLI
 // keep the reference's error behaviour (proj/src/cli.cpp:520-538).
+#include <chrono>
+#include <cstdio>
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -396,11 +398,21 @@ std::unique_ptr<DeviceGraph> DeviceGraph::from_edge_list(const std::string& path
 DeviceGraph::DeviceGraph(const ProbGraph& g, const SuspectSet& vi, int device, void* cuda_stream)
     : n_(g.n), m_(g.m) {
     if (vi.p_of.size() != g.n) throw std::invalid_argument("suspect set does not match graph");
+    const char* tenv = std::getenv("HSAW_UPLOAD_TIMING");
+    const bool timing = tenv && std::atoi(tenv) != 0;
+    const auto t0 = std::chrono::steady_clock::now();
     int rc = hsaw_gpu_ctx_create(device, cuda_stream, &ctx_);
     if (rc != HSAW_OK)
         throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");
+    const auto t1 = std::chrono::steady_clock::now();
     rc = hsaw_gpu_graph_upload(ctx_, g.n, g.m, g.in_offsets.data(), g.in_src.data(),
                                g.in_cum.data(), vi.p_of.data());
+    if (timing) {
+        const auto t2 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[hsaw upload] ctx_create %.2f ms, graph_upload %.2f ms\n",
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                     std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
     if (rc != HSAW_OK) {
         std::string msg = hsaw_gpu_last_error(ctx_);
         hsaw_gpu_ctx_destroy(ctx_);

@@ -68,6 +68,10 @@ def lib() -> C.CDLL:
     L.hsawh_check.argtypes = [C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_uint32,
                               C.c_double, C.c_double, C.c_uint32, C.POINTER(C.c_int), f64p]
     L.hsawh_device_create.argtypes = [vp, f64p, C.c_int, vp, vpp]
+    L.hsawh_suspects_create.argtypes = [vp, f64p, vpp]
+    L.hsawh_suspects_free.argtypes = [vp]
+    L.hsawh_suspects_free.restype = None
+    L.hsawh_device_create_vi.argtypes = [vp, vp, C.c_int, vp, vpp]
     L.hsawh_device_free.argtypes = [vp]
     L.hsawh_device_free.restype = None
     L.hsawh_device_ctx.argtypes = [vp]
@@ -274,15 +278,40 @@ def check(cov_r, cov_rp, n_rp, M, k, eps, delta, t):
     return bool(ok.value), e.value
 
 
+class Suspects:
+    """hsaw::SuspectSet built once from a dense p_of array (0 = not a suspect): the object a C++
+    caller hands to DeviceGraph(g, vi), so per-call uploads do not rebuild it."""
+
+    def __init__(self, graph: Graph, p_of):
+        self.p_of = np.ascontiguousarray(p_of, dtype=np.float64)
+        self.h = C.c_void_p()
+        _chk(lib().hsawh_suspects_create(graph.h, _p(self.p_of, f64p), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().hsawh_suspects_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class DeviceGraph:
     """hsaw::DeviceGraph: the graph + suspects uploaded to one GPU."""
 
     def __init__(self, graph: Graph, p_of, device=0, cuda_stream: int | None = None):
         self.graph = graph
-        self.p_of = np.ascontiguousarray(p_of, dtype=np.float64)
         self.h = C.c_void_p()
-        _chk(lib().hsawh_device_create(graph.h, _p(self.p_of, f64p), device,
-                                       C.c_void_p(cuda_stream) if cuda_stream else None,
+        stream = C.c_void_p(cuda_stream) if cuda_stream else None
+        if isinstance(p_of, Suspects):
+            self.p_of = p_of.p_of
+            _chk(lib().hsawh_device_create_vi(graph.h, p_of.h, device, stream, C.byref(self.h)))
+            return
+        self.p_of = np.ascontiguousarray(p_of, dtype=np.float64)
+        _chk(lib().hsawh_device_create(graph.h, _p(self.p_of, f64p), device, stream,
                                        C.byref(self.h)))
 
     @classmethod
