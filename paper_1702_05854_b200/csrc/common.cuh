@@ -502,18 +502,20 @@ struct Restriction {
 // Buffers of the dense reduced greedy instance (greedy.cu, build_dense): kept on the context like
 // the other greedy scratch, so a solve's six greedy calls do not churn gigabytes through the pool.
 struct DenseScratch {
-    DevVec<uint32_t> bits, pc, base, bloom, ids, cnt, len, items;
+    DevVec<uint32_t> bits, pc, base, bloom, ids, cnt, items, pw, pr, sw, flag;
     DevVec<uint64_t> map, start;
     template <class F>
     void for_each(F&& f) {
-        f(bits); f(pc); f(base); f(bloom); f(ids); f(cnt); f(len); f(items); f(map); f(start);
+        f(bits); f(pc); f(base); f(bloom); f(ids); f(cnt); f(items); f(pw); f(pr); f(sw); f(flag);
+        f(map); f(start);
     }
     void release() {
         for_each([](auto& v) { v.release(); });
     }
     void swap(DenseScratch& o) {
         bits.swap(o.bits); pc.swap(o.pc); base.swap(o.base); bloom.swap(o.bloom); ids.swap(o.ids);
-        cnt.swap(o.cnt); len.swap(o.len); items.swap(o.items); map.swap(o.map); start.swap(o.start);
+        cnt.swap(o.cnt); items.swap(o.items); pw.swap(o.pw); pr.swap(o.pr); sw.swap(o.sw);
+        flag.swap(o.flag); map.swap(o.map); start.swap(o.start);
     }
 };
 

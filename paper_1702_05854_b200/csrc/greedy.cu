@@ -27,21 +27,18 @@ struct WalkView;
 
 namespace {
 
-// Walks [w0, w0 + cnt) of either source. Walk w occupies items[off[w] + add*w, off[w+1] + add*(w+1)),
-// or, when `len` is set (the dense reduced instance of a large id space, see build_dense),
-// items[off[w], off[w] + len[w]).
+// Walks [w0, w0 + cnt) of either source. Walk w occupies items[off[w] + add*w, off[w+1] + add*(w+1)).
 struct WalkView {
     const uint64_t* off;
     const uint32_t* items;
     uint64_t w0, cnt;
     uint32_t add;  // 1 for the node arrays of a stream (len + 1 nodes per walk), else 0
     uint32_t limit;
-    const uint32_t* len;  // per-walk item counts of a (start, length) view, else nullptr
 };
 
 __device__ __forceinline__ void walk_extent(const WalkView& v, uint64_t w, uint64_t& b, uint64_t& e) {
     b = v.off[w] + v.add * w;
-    e = v.len ? b + v.len[w] : v.off[w + 1] + v.add * (w + 1);
+    e = v.off[w + 1] + v.add * (w + 1);
 }
 
 __device__ __forceinline__ bool is_cand(const uint32_t* __restrict__ cand_bits, uint32_t item) {
@@ -109,17 +106,40 @@ __global__ void key_histogram(const uint32_t* __restrict__ keys, uint64_t n, uin
 // are sorted on their top bits down to windows of 2^wbits ids (<= 128 KB of counters), one CTA
 // takes a window, counts its keys with shared-memory atomics and adds the window to the global
 // array with plain coalesced read-modify-writes (it is the only writer of that range).
-__global__ void bucket_starts(const uint32_t* __restrict__ keys, uint64_t n, uint32_t wbits,
-                              uint32_t nbuckets, uint64_t* __restrict__ starts) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t b = min(keys[i] >> wbits, nbuckets);  // ids >= limit: past the last window
-    const uint32_t prev = i ? min(keys[i - 1] >> wbits, nbuckets) : 0u;
-    for (uint32_t x = i ? prev + 1 : 0u; x <= b; ++x) starts[x] = i;
-    if (i == n - 1)
-        for (uint32_t x = b + 1; x <= nbuckets; ++x) starts[x] = n;
+// starts[b] = first position of window b's keys in the sorted slice (starts[nbuckets] = end of the
+// in-range keys). Four keys per thread (128-bit loads), the left neighbour comes by shuffle.
+__global__ void __launch_bounds__(256) bucket_starts(const uint32_t* __restrict__ keys, uint64_t n,
+                                                     uint32_t wbits, uint32_t nbuckets,
+                                                     uint64_t* __restrict__ starts) {
+    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;  // quad index
+    const uint64_t i0 = q * 4;
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t b[4] = {nbuckets, nbuckets, nbuckets, nbuckets};
+    if (i0 + 3 < n) {
+        const uint4 k4 = __ldcs(reinterpret_cast<const uint4*>(keys) + q);
+        b[0] = min(k4.x >> wbits, nbuckets);  // ids >= limit: past the last window
+        b[1] = min(k4.y >> wbits, nbuckets);
+        b[2] = min(k4.z >> wbits, nbuckets);
+        b[3] = min(k4.w >> wbits, nbuckets);
+    } else {
+        for (int j = 0; j < 4; ++j)
+            if (i0 + j < n) b[j] = min(keys[i0 + j] >> wbits, nbuckets);
+    }
+    uint32_t left = __shfl_up_sync(kFullMask, b[3], 1);
+    if (i0 >= n) return;
+    if (lane == 0 && i0 > 0) left = min(keys[i0 - 1] >> wbits, nbuckets);
+    for (int j = 0; j < 4 && i0 + j < n; ++j) {
+        const uint64_t i = i0 + j;
+        const uint32_t prev = j ? b[j - 1] : left;
+        for (uint32_t x = i ? prev + 1 : 0u; x <= b[j]; ++x) starts[x] = i;
+        if (i == n - 1)
+            for (uint32_t x = b[j] + 1; x <= nbuckets; ++x) starts[x] = n;
+    }
 }
 
+// One CTA per window: zero, count (eight key loads in flight per thread), then add the window to
+// the global counters with all of a thread's 32 read-modify-writes issued together (the loads of
+// the non-zero slots first, then the stores) instead of one dependent round trip per slot.
 __global__ void __launch_bounds__(1024) window_histogram(const uint32_t* __restrict__ keys,
                                                          const uint64_t* __restrict__ starts,
                                                          uint32_t wbits, uint32_t limit,
@@ -131,14 +151,30 @@ __global__ void __launch_bounds__(1024) window_histogram(const uint32_t* __restr
     if (a == b) return;
     for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) win[i] = 0;
     __syncthreads();
-    for (uint64_t p = a + threadIdx.x; p < b; p += blockDim.x)
-        atomicAdd(&win[__ldcs(keys + p) & (W - 1)], 1u);
+    uint64_t p = a + threadIdx.x;
+    for (; p + 7 * 1024ull < b; p += 8 * 1024ull) {
+        uint32_t k[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) k[j] = __ldcs(keys + p + j * 1024ull);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) atomicAdd(&win[k[j] & (W - 1)], 1u);
+    }
+    for (; p < b; p += 1024) atomicAdd(&win[__ldcs(keys + p) & (W - 1)], 1u);
     __syncthreads();
     const uint64_t base = (uint64_t)blockIdx.x << wbits;
-    for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
-        const uint32_t c = win[i];
-        const uint64_t id = base + i;
-        if (c && id < limit && is_cand(cand_bits, (uint32_t)id)) cnt[id] += c;
+    for (uint32_t i0 = threadIdx.x; i0 < W; i0 += 8 * 1024) {
+        uint32_t c[8], g[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t i = i0 + j * 1024;
+            const uint64_t id = base + i;
+            c[j] = i < W ? win[i] : 0u;
+            if (c[j] && (id >= limit || !is_cand(cand_bits, (uint32_t)id))) c[j] = 0;
+            g[j] = c[j] ? cnt[id] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (c[j]) cnt[base + i0 + j * 1024] = g[j] + c[j];
     }
 }
 
@@ -334,74 +370,76 @@ __global__ void __launch_bounds__(256) dense_emit(const uint32_t* __restrict__ c
     }
 }
 
-// Walks -> (start, length) view of their indexed items, renamed. One warp per walk; a block's eight
-// walks share one atomicAdd on the output cursor. Up to kDenseStage renamed items are staged per
-// warp in shared memory between the counting and the writing half; longer ones are looked up twice.
-constexpr uint32_t kDenseStage = 256;
-__global__ void __launch_bounds__(256) dense_extract(WalkView v, Bloom2 bloom,
-                                                     const uint2* __restrict__ rmap,
-                                                     unsigned long long* __restrict__ cursor,
-                                                     uint64_t* __restrict__ rstart,
-                                                     uint32_t* __restrict__ rlen,
-                                                     uint32_t* __restrict__ ritems) {
-    __shared__ uint32_t stage[8][kDenseStage];
-    __shared__ uint32_t s_cnt[8];
-    __shared__ unsigned long long s_base;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    auto lookup = [&](uint32_t it, uint32_t& rank) -> bool {
-        if (it >= v.limit || !bloom2_pass(bloom, it)) return false;
-        const uint2 m = __ldg(rmap + (it >> 5));
-        if (!((m.x >> (it & 31)) & 1u)) return false;
-        rank = m.y + __popc(m.x & ((1u << (it & 31)) - 1u));
-        return true;
-    };
-    for (uint64_t i0 = (uint64_t)blockIdx.x * 8; i0 < v.cnt; i0 += (uint64_t)gridDim.x * 8) {
-        const uint64_t i = i0 + warp;
-        uint32_t c = 0;
-        uint64_t b = 0, e = 0;
-        if (i < v.cnt) {
-            walk_extent(v, v.w0 + i, b, e);
-            for (uint64_t p0 = b; p0 < e; p0 += 32) {
-                const uint64_t p = p0 + lane;
-                uint32_t rank = 0;
-                const bool keep = p < e && lookup(v.items[p], rank);
-                const uint32_t m = __ballot_sync(kFullMask, keep);
-                const uint32_t at = c + __popc(m & ((1u << lane) - 1u));
-                if (keep && at < kDenseStage) stage[warp][at] = rank;
-                c += __popc(m);
-            }
+// The walks' indexed items as (walk, new name) pairs: a flat, coalesced pass over the item range
+// (the walk structure does not matter to a membership test); only for the few items that pass the
+// filter and the map is the owning walk looked up (binary search over the extents) and the pair
+// appended through a warp-aggregated cursor. The first version went walk by walk (one warp per
+// walk, block-wide allocation): 0.6 TB/s on the 39 GB of the largest R_t.
+__global__ void __launch_bounds__(256) dense_pairs(WalkView v, uint64_t p0, uint64_t p1, Bloom2 bloom,
+                                                   const uint2* __restrict__ rmap,
+                                                   unsigned long long* __restrict__ cursor,
+                                                   uint32_t* __restrict__ pair_walk,
+                                                   uint32_t* __restrict__ pair_rank) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    constexpr int kInFlight = 4;
+    // (the loop bound is warp-uniform: the ballots below need all 32 lanes)
+    for (uint64_t wbase = p0 + (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wbase < p1;
+         wbase += kInFlight * stride) {
+        const uint64_t base = wbase + lane;
+        uint32_t it[kInFlight];
+#pragma unroll
+        for (int j = 0; j < kInFlight; ++j) {
+            const uint64_t p = base + j * stride;
+            it[j] = p < p1 ? __ldcs(v.items + p) : 0xFFFFFFFFu;
         }
-        if (lane == 0) s_cnt[warp] = c;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t t = 0;
-            for (int w = 0; w < 8; ++w) t += s_cnt[w];
-            s_base = t ? atomicAdd(cursor, (unsigned long long)t) : 0ull;
-        }
-        __syncthreads();
-        if (i < v.cnt) {
-            uint64_t start = s_base;
-            for (uint32_t w = 0; w < warp; ++w) start += s_cnt[w];
-            if (lane == 0) {
-                rstart[i] = start;
-                rlen[i] = c;
+#pragma unroll
+        for (int j = 0; j < kInFlight; ++j) {
+            const uint64_t p = base + j * stride;
+            uint32_t rank = 0;
+            bool keep = it[j] < v.limit && bloom2_pass(bloom, it[j]);
+            if (keep) {
+                const uint2 m = __ldg(rmap + (it[j] >> 5));
+                keep = (m.x >> (it[j] & 31)) & 1u;
+                rank = m.y + __popc(m.x & ((1u << (it[j] & 31)) - 1u));
             }
-            if (c <= kDenseStage) {
-                for (uint32_t q = lane; q < c; q += 32) ritems[start + q] = stage[warp][q];
-            } else {  // a walk with more indexed items than the stage holds: second look-up pass
-                uint32_t at0 = 0;
-                for (uint64_t p0 = b; p0 < e; p0 += 32) {
-                    const uint64_t p = p0 + lane;
-                    uint32_t rank = 0;
-                    const bool keep = p < e && lookup(v.items[p], rank);
-                    const uint32_t m = __ballot_sync(kFullMask, keep);
-                    if (keep) ritems[start + at0 + __popc(m & ((1u << lane) - 1u))] = rank;
-                    at0 += __popc(m);
+            const uint32_t mask = __ballot_sync(kFullMask, keep);
+            if (!mask) continue;
+            uint64_t wi = 0;
+            if (keep) {  // largest walk index whose first item position is <= p
+                uint64_t lo = 0, hi = v.cnt - 1;
+                while (lo < hi) {
+                    const uint64_t mid = lo + (hi - lo + 1) / 2;
+                    const uint64_t w = v.w0 + mid;
+                    if (v.off[w] + v.add * w <= p)
+                        lo = mid;
+                    else
+                        hi = mid - 1;
                 }
+                wi = lo;
+            }
+            unsigned long long at = 0;
+            const int leader = __ffs(mask) - 1;
+            if ((int)lane == leader) at = atomicAdd(cursor, (unsigned long long)__popc(mask));
+            at = __shfl_sync(kFullMask, at, leader) + __popc(mask & ((1u << lane) - 1u));
+            if (keep) {
+                pair_walk[at] = (uint32_t)wi;
+                pair_rank[at] = rank;
             }
         }
-        __syncthreads();  // stage / s_cnt are reused by the next iteration
     }
+}
+
+// pairs sorted by walk -> heads of the runs (flag[n] = 0 closes the scan) and the run starts
+__global__ void pair_heads(const uint32_t* __restrict__ sw, uint64_t n, uint32_t* __restrict__ flag) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= n) flag[i] = i < n && (i == 0 || sw[i] != sw[i - 1]) ? 1u : 0u;
+}
+__global__ void pair_starts(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ widx,
+                            uint64_t n, uint64_t* __restrict__ start) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) start[widx[i]] = i;
+    if (i == n) start[widx[n]] = n;
 }
 
 // solution slots hold ranks of the dense instance: back to ids (markers pass through)
@@ -793,6 +831,49 @@ __global__ void __launch_bounds__(256) count_covered(WalkView v,
     if (lane == 0 && mine) atomicAdd(out, (unsigned long long)mine);
 }
 
+// K6, flat form: a coalesced pass over the item range; the walk of an item only matters for the
+// few items that are in the query set (binary search over the extents, then one bit per walk so
+// that a walk counts once). The walk-by-walk form above streams at ~1.9 TB/s on 130-item walks.
+__global__ void __launch_bounds__(256) count_covered_flat(WalkView v, uint64_t p0, uint64_t p1,
+                                                          const uint32_t* __restrict__ query_bits,
+                                                          BitFilter filter,
+                                                          uint32_t* __restrict__ walk_bits,
+                                                          unsigned long long* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    constexpr int kInFlight = 4;
+    uint32_t mine = 0;
+    for (uint64_t base = p0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; base < p1;
+         base += kInFlight * stride) {
+        uint32_t it[kInFlight];
+#pragma unroll
+        for (int j = 0; j < kInFlight; ++j) {
+            const uint64_t p = base + j * stride;
+            it[j] = p < p1 ? __ldcs(v.items + p) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int j = 0; j < kInFlight; ++j) {
+            if (!(it[j] < v.limit && filter_pass(filter, it[j]) &&
+                  ((query_bits[it[j] >> 5] >> (it[j] & 31)) & 1u)))
+                continue;
+            const uint64_t p = base + j * stride;
+            uint64_t lo = 0, hi = v.cnt - 1;  // largest walk index whose first item is at or before p
+            while (lo < hi) {
+                const uint64_t mid = lo + (hi - lo + 1) / 2;
+                const uint64_t w = v.w0 + mid;
+                if (v.off[w] + v.add * w <= p)
+                    lo = mid;
+                else
+                    hi = mid - 1;
+            }
+            const uint32_t bit = 1u << (lo & 31);
+            if (!(atomicOr(&walk_bits[lo >> 5], bit) & bit)) ++mine;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFullMask, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(out, (unsigned long long)mine);
+}
+
 // ---- stepwise session (sharded solves): the same round split into host-visible steps -----------
 // select_final: reduce the partial maxima to the winner (item, gain) for the host.
 __global__ void __launch_bounds__(256) select_final(const uint64_t* __restrict__ partial,
@@ -1009,7 +1090,7 @@ static void histogram_counts(hsaw_gpu_ctx* ctx, const WalkView& v, uint64_t p0, 
                     top, st));
                 ++ctx->launches;
                 if (windows) {
-                    bucket_starts<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(
+                    bucket_starts<<<(unsigned)((len + 1023) / 1024), 256, 0, st>>>(
                         d_sorted.p, len, (uint32_t)wbits, nbuckets, starts.p);
                     check_launch(ctx, "bucket_starts");
                     window_histogram<<<nbuckets, 1024, (size_t)4 << wbits, st>>>(
@@ -1349,7 +1430,8 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             uint32_t* rcnt = nullptr;
             DenseScratch& dx = ctx->g_dense;
             DevVec<uint32_t>&x_bits = dx.bits, &x_pc = dx.pc, &x_base = dx.base, &x_bloom = dx.bloom,
-                             &x_ids = dx.ids, &x_cnt = dx.cnt, &x_len = dx.len, &x_items = dx.items;
+                             &x_ids = dx.ids, &x_cnt = dx.cnt, &x_items = dx.items, &x_pw = dx.pw,
+                             &x_pr = dx.pr, &x_sw = dx.sw, &x_flag = dx.flag;
             DevVec<uint64_t>&x_map = dx.map, &x_start = dx.start;
             if (dense) {
                 uint64_t occ = 0, d_est = 0;  // occurrences / distinct ids at or above min_count
@@ -1378,9 +1460,12 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                 x_map.ensure_scratch(words + 1);
                 x_ids.ensure_scratch(D + 1);
                 x_cnt.ensure_scratch(D + 4);
-                x_start.ensure_scratch(cnt + 1);
-                x_len.ensure_scratch(cnt + 1);
-                x_items.ensure_scratch(occ + 1);
+                const uint64_t P = occ;  // every occurrence of an indexed item becomes one pair
+                x_pw.ensure_scratch(P + 2);
+                x_pr.ensure_scratch(P + 2);
+                x_sw.ensure_scratch(P + 2);
+                x_items.ensure_scratch(P + 2);
+                x_flag.ensure_scratch(P + 2);
                 auto* d_cursor = reinterpret_cast<unsigned long long*>(ctx->d_scalars + 12);
                 HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, st));
                 HSAW_CUDA_CHECK(cudaMemsetAsync(x_cnt.p, 0, (D + 4) * 4, st));
@@ -1390,15 +1475,42 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                                                             reinterpret_cast<uint2*>(x_map.p), x_ids.p,
                                                             x_cnt.p);
                     check_launch(ctx, "dense_emit");
-                    const int eb = (int)std::min<uint64_t>((cnt + 7) / 8, (uint64_t)wide);
-                    dense_extract<<<eb, 256, 0, st>>>(v, Bloom2{x_bloom.p, log2w},
-                                                      reinterpret_cast<const uint2*>(x_map.p), d_cursor,
-                                                      x_start.p, x_len.p, x_items.p);
-                    check_launch(ctx, "dense_extract");
+                    const int eb = (int)std::min<uint64_t>((p1 - p0 + 1023) / 1024, (uint64_t)wide * 2);
+                    dense_pairs<<<eb, 256, 0, st>>>(v, p0, p1, Bloom2{x_bloom.p, log2w},
+                                                    reinterpret_cast<const uint2*>(x_map.p), d_cursor,
+                                                    x_pw.p, x_pr.p);
+                    check_launch(ctx, "dense_pairs");
                 }
-                if (read_u64(ctx, reinterpret_cast<uint64_t*>(d_cursor)) != occ)
+                if (read_u64(ctx, reinterpret_cast<uint64_t*>(d_cursor)) != P)
                     fail(HSAW_ECUDA, "greedy: dense instance does not match the counts (internal error)");
-                rv = WalkView{x_start.p, x_items.p, 0, cnt, 0, (uint32_t)D, x_len.p};
+                uint64_t nw = 0;
+                if (P) {
+                    StageScope timer(ctx, HSAW_STAGE_INDEX);
+                    int wbits = 1;
+                    while (wbits < 32 && (1ull << wbits) < cnt) ++wbits;
+                    size_t bytes = 0;
+                    HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(
+                        nullptr, bytes, x_pw.p, x_sw.p, x_pr.p, x_items.p, (int64_t)P, 0, wbits, st));
+                    ctx->cub_tmp.ensure_scratch(bytes ? bytes : 1);
+                    HSAW_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(
+                        ctx->cub_tmp.p, bytes, x_pw.p, x_sw.p, x_pr.p, x_items.p, (int64_t)P, 0, wbits,
+                        st));
+                    ++ctx->launches;
+                    pair_heads<<<(unsigned)((P + 256) / 256), 256, 0, st>>>(x_sw.p, P, x_flag.p);
+                    check_launch(ctx, "pair_heads");
+                    exclusive_sum_u32(ctx, x_flag.p, x_pw.p, P + 1);  // x_pw: walk rank of each pair
+                }
+                if (P) nw = read_u32(ctx, x_pw.p + P);
+                x_start.ensure_scratch(nw + 2);
+                if (P) {
+                    StageScope timer(ctx, HSAW_STAGE_INDEX);
+                    pair_starts<<<(unsigned)((P + 256) / 256), 256, 0, st>>>(x_flag.p, x_pw.p, P,
+                                                                             x_start.p);
+                    check_launch(ctx, "pair_starts");
+                } else {
+                    HSAW_CUDA_CHECK(cudaMemsetAsync(x_start.p, 0, 8, st));
+                }
+                rv = WalkView{x_start.p, x_items.p, 0, nw, 0, (uint32_t)D};
                 rlimit = (uint32_t)D;
                 rcnt = x_cnt.p;
             } else {
@@ -1869,8 +1981,25 @@ int hsaw_gpu_coverage_of(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                                                     const_cast<uint32_t*>(filt.bits));
                 check_launch(ctx, "set_filter_bits");
             }
-            count_covered<<<blocks, 256, 0, st>>>(v, bits.p, filt, d_out);
-            check_launch(ctx, "count_covered");
+            // HSAW_COVERAGE_FLAT: 0 keeps the walk-by-walk kernel, 2 forces the flat one (tests);
+            // default: flat from 2^20 items (read per call)
+            const char* fenv = std::getenv("HSAW_COVERAGE_FLAT");
+            const int fmode = fenv ? std::atoi(fenv) : 1;
+            uint64_t p0 = 0, p1 = 0;
+            view_span(ctx, v, &p0, &p1);
+            if (p1 > p0 && (fmode == 2 || (fmode == 1 && p1 - p0 > (1ull << 20)))) {
+                DevVec<uint32_t>& wb = ctx->g_covered;
+                const uint64_t wwords = (cnt + 31) / 32 + 1;
+                wb.ensure_scratch(wwords);
+                HSAW_CUDA_CHECK(cudaMemsetAsync(wb.p, 0, wwords * 4, st));
+                const int fb = (int)std::min<uint64_t>((p1 - p0 + 1023) / 1024,
+                                                       (uint64_t)ctx->sm_count * 16);
+                count_covered_flat<<<fb, 256, 0, st>>>(v, p0, p1, bits.p, filt, wb.p, d_out);
+                check_launch(ctx, "count_covered_flat");
+            } else {
+                count_covered<<<blocks, 256, 0, st>>>(v, bits.p, filt, d_out);
+                check_launch(ctx, "count_covered");
+            }
             clear_bits<<<qb, 256, 0, st>>>(d_q.p, q.size(), bits.p);
             check_launch(ctx, "clear_bits");
         }

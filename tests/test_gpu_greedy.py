@@ -16,8 +16,10 @@ def instance_form(request, monkeypatch):
     production uses it from 256 MB of counters upwards, i.e. the LiveJournal shape and beyond)."""
     if request.param == "dense":
         monkeypatch.setenv("HSAW_DENSE_MIN_BYTES", "0")
+        monkeypatch.setenv("HSAW_COVERAGE_FLAT", "2")  # and the flat coverage_of kernel
     else:
         monkeypatch.setenv("HSAW_DENSE_MIN_BYTES", str(1 << 60))
+        monkeypatch.setenv("HSAW_COVERAGE_FLAT", "0")
     return request.param
 
 
