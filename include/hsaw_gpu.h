@@ -175,6 +175,10 @@ uint64_t hsaw_gpu_graph_bytes(const hsaw_gpu_ctx* ctx);
  * compact arrays with 21-bit packed / 32-bit flagged sources; 1 = compact with plain sources
  * (HSAW_PACK=0); -1 = no graph. Diagnostic only: results never depend on it. */
 int hsaw_gpu_graph_layout(const hsaw_gpu_ctx* ctx);
+/* How the last hsaw_gpu_graph_upload moved in_cum: 0 copied from the host array, 1 regenerated on
+ * the device after host threads verified, bit for bit, that every row holds the sequential
+ * 1/in-degree sums of WeightMode::InDegree (proj/src/graph.cpp:172-178). Diagnostic. */
+int hsaw_gpu_graph_upload_mode(const hsaw_gpu_ctx* ctx);
 
 /* ---- sampler: encode / decode (kernels K1, K2) ---------------------------------------------- */
 

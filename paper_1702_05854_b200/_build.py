@@ -53,8 +53,9 @@ def _sources(directory: str, exts: tuple[str, ...]) -> list[str]:
 def build_gpu(force: bool = False, verbose: bool = False) -> str:
     """nvcc -gencode arch=compute_100a,code=sm_100a for every .cu under csrc/, linked into one .so."""
     cus = _sources(CSRC, (".cu",))
+    cpps = _sources(CSRC, (".cpp",))
     headers = _sources(CSRC, (".cuh", ".h")) + [os.path.join(ROOT, "include", "hsaw_gpu.h")]
-    if not force and _newer(GPU_SO, cus + headers):
+    if not force and _newer(GPU_SO, cus + cpps + headers):
         return GPU_SO
     if not os.path.exists(NVCC):
         raise RuntimeError(f"nvcc not found at {NVCC}")
@@ -70,8 +71,15 @@ def build_gpu(force: bool = False, verbose: bool = False) -> str:
         subprocess.check_call(cmd)
         return obj
 
+    def compile_cpp(cpp: str) -> str:  # host-only helpers of the same library (plain g++)
+        obj = os.path.join(OBJ, os.path.basename(cpp)[:-4] + ".o")
+        if force or not _newer(obj, [cpp] + headers):
+            subprocess.check_call([CXX, "-std=c++17", "-O3", "-fPIC", "-pthread", "-c", cpp, "-o", obj])
+        return obj
+
     with ThreadPoolExecutor(max_workers=4) as ex:
         objs = list(ex.map(compile_one, cus))
+    objs += [compile_cpp(c) for c in cpps]
     subprocess.check_call([NVCC, "-shared", "-ccbin", CXX, "-o", GPU_SO, *objs, "-lcudart"])
     return GPU_SO
 

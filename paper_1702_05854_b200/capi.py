@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_graph_bytes.argtypes = [vp]
     L.hsaw_gpu_graph_bytes.restype = C.c_uint64
     L.hsaw_gpu_graph_layout.argtypes = [vp]
+    L.hsaw_gpu_graph_upload_mode.argtypes = [vp]
     L.hsaw_gpu_launch_count.argtypes = [vp]
     L.hsaw_gpu_launch_count.restype = C.c_uint64
     L.hsaw_gpu_stage_times.argtypes = [vp, f64p, u64p, C.c_int]
@@ -174,7 +175,8 @@ EXPORTS = (
     "hsaw_gpu_edge_text_parse", "hsaw_gpu_edge_text_fetch", "hsaw_gpu_edge_text_free",
     "hsaw_gpu_edge_text_install",
     "hsaw_gpu_rmat_build", "hsaw_gpu_held_csr_fetch", "hsaw_gpu_held_csr_install",
-    "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout", "hsaw_gpu_stream_keep",
+    "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout", "hsaw_gpu_graph_upload_mode",
+    "hsaw_gpu_stream_keep",
     "hsaw_gpu_stream_restrict", "hsaw_gpu_stream_crossings",
     "hsaw_gpu_rr_node_sets", "hsaw_gpu_walkset_export",
     "hsaw_gpu_stream_histogram", "hsaw_gpu_counts_bound", "hsaw_gpu_counts_threshold",
@@ -308,6 +310,10 @@ class Context:
     def graph_layout(self) -> str:
         code = int(self.L.hsaw_gpu_graph_layout(self.h))
         return {0: "fat", -1: "none"}.get(code, "compact")
+
+    @property
+    def upload_mode(self) -> str:
+        return "regenerated" if int(self.L.hsaw_gpu_graph_upload_mode(self.h)) == 1 else "copied"
 
     def upload_graph(self, n, m, in_offsets, in_src, in_cum, p_of):
         in_offsets = np.ascontiguousarray(in_offsets, dtype=np.uint64)

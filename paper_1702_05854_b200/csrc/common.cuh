@@ -539,6 +539,7 @@ struct hsaw_gpu_ctx {
     bool own_stream = false;
     hsawgpu::DeviceGraph g;
     uint64_t graph_bytes = 0;
+    int upload_mode = 0;  // in_cum of the last graph_upload: 0 copied, 1 regenerated on the device
     // L2 access-policy window over the compact graph (headers + sources), attached to the K1
     // launches only: those lines are marked persisting, so the walk-log stream of the same kernel
     // cannot evict them, while every other kernel on the stream keeps normal caching.

@@ -1333,12 +1333,13 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         const int wide = ctx->sm_count * 8;
         const int cover_blocks = ctx->sm_count * 2;
         uint32_t done = 0;
-        // Large id spaces run on a dense reduced instance (build_dense above). HSAW_DENSE_MIN_BYTES:
+        // Id spaces from 4 M items run on a dense reduced instance (build_dense above; C2's 16 M
+        // edges: eSIA k=1000 0.083 -> 0.056 s, the Twitter shape: see DESIGN.md). HSAW_DENSE_MIN_BYTES:
         // size of the per-item counter array from which it applies (0 forces it everywhere: tests);
         // HSAW_INDEX_MASS_DIV: the indexed items hold at most 1/div of all occurrences.
         const uint64_t dense_min_bytes = [] {  // (read per call: the tests flip it)
             const char* env = std::getenv("HSAW_DENSE_MIN_BYTES");
-            return env ? std::strtoull(env, nullptr, 10) : (256ull << 20);
+            return env ? std::strtoull(env, nullptr, 10) : (16ull << 20);
         }();
         const uint64_t mass_div = [] {
             const char* env = std::getenv("HSAW_INDEX_MASS_DIV");
@@ -1348,7 +1349,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         const bool dense_forced = dense_min_bytes == 0;
         const bool dense_possible = cand_ids == nullptr && p1 > p0 &&
                                     (dense_forced || ((uint64_t)limit * 4 > dense_min_bytes &&
-                                                      p1 - p0 > (1ull << 24)));
+                                                      p1 - p0 > (1ull << 20)));
 
         // min_count 0: choose the indexing threshold from the count distribution: the mass rule
         // (at most 1/mass_div of all occurrences indexed), raised to ck_percent % of the k-th

@@ -1,0 +1,123 @@
+// Host-side check behind hsaw_gpu_graph_upload's "regenerate in_cum on the device" path
+// (graph.cu): do the caller's cumulative weights equal, bit for bit, the sequential 1/in-degree
+// sums of WeightMode::InDegree (proj/src/graph.cpp:172-178: w = 1.0 / d, cum += w, left to right)?
+// Each element is compared with its left neighbour plus w (cum[lo] with w itself), which states
+// the same thing by induction and has no dependent chain, so the scan runs at memory speed:
+// AVX2 where the CPU has it (4 doubles per compare), scalar otherwise. Plain g++ translation unit:
+// the intrinsics stay out of nvcc's front end.
+#include <atomic>
+#include <cstdint>
+#include <thread>
+#include <vector>
+
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
+
+namespace hsawgpu {
+
+namespace {
+
+// 1.0 / d for the short rows that make up most of a power-law graph (a division per row costs
+// as much as checking a dozen elements)
+constexpr uint64_t kRecipTable = 2048;
+const double* recip_table() {
+    static const std::vector<double> t = [] {
+        std::vector<double> r(kRecipTable, 0.0);
+        for (uint64_t d = 1; d < kRecipTable; ++d) r[d] = 1.0 / (double)d;
+        return r;
+    }();
+    return t.data();
+}
+
+// mismatches in one row (any non-zero value = "differs"); c = cum + lo, d = row length >= 1
+inline uint64_t row_scalar(const double* c, uint64_t d, double w) {
+    uint64_t bad = c[0] != w;  // 0.0 + w
+    for (uint64_t i = 1; i < d; ++i) bad += c[i] != c[i - 1] + w;
+    return bad;
+}
+
+#if defined(__x86_64__)
+__attribute__((target("avx2"))) uint64_t rows_avx2(const uint64_t* off, const double* cum,
+                                                   uint64_t va, uint64_t vb,
+                                                   const std::atomic<bool>& stop) {
+    uint64_t bad = 0;
+    const double* recip = recip_table();
+    for (uint64_t v = va; v < vb; ++v) {
+        if ((v & 1023) == 0 && (bad || stop.load(std::memory_order_relaxed))) break;
+        const uint64_t lo = off[v], hi = off[v + 1];
+        if (hi <= lo) continue;
+        const uint64_t d = hi - lo;
+        const double w = d < kRecipTable ? recip[d] : 1.0 / (double)d;
+        const double* c = cum + lo;
+        bad += c[0] != w;
+        const __m256d wv = _mm256_set1_pd(w);
+        __m256d acc = _mm256_setzero_pd();
+        uint64_t i = 1;
+        for (; i + 4 <= d; i += 4) {
+            const __m256d a = _mm256_loadu_pd(c + i);
+            const __m256d s = _mm256_add_pd(_mm256_loadu_pd(c + i - 1), wv);
+            acc = _mm256_or_pd(acc, _mm256_cmp_pd(a, s, _CMP_NEQ_UQ));  // NaN counts as different
+        }
+        bad += (uint64_t)_mm256_movemask_pd(acc);
+        for (; i < d; ++i) bad += c[i] != c[i - 1] + w;
+    }
+    return bad;
+}
+#endif
+
+uint64_t rows_plain(const uint64_t* off, const double* cum, uint64_t va, uint64_t vb,
+                    const std::atomic<bool>& stop) {
+    uint64_t bad = 0;
+    for (uint64_t v = va; v < vb; ++v) {
+        if ((v & 1023) == 0 && (bad || stop.load(std::memory_order_relaxed))) break;
+        const uint64_t lo = off[v], hi = off[v + 1];
+        if (hi > lo) bad += row_scalar(cum + lo, hi - lo, 1.0 / (double)(hi - lo));
+    }
+    return bad;
+}
+
+// first row whose first edge is at or after edge position e
+uint64_t row_at(const uint64_t* off, uint64_t n, uint64_t e) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (off[mid] < e)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+}  // namespace
+
+// off: n + 1 non-decreasing offsets (checked by the caller), cum: off[n] doubles.
+bool rows_are_indegree_sums(uint32_t n, const uint64_t* off, const double* cum, unsigned threads) {
+    if (threads == 0) threads = 1;
+    const uint64_t m = off[n];
+    std::atomic<bool> stop{false};
+#if defined(__x86_64__)
+    const bool avx2 = __builtin_cpu_supports("avx2");
+#else
+    const bool avx2 = false;
+#endif
+    auto scan = [&](unsigned t) {  // rows split by edge position: equal bytes per worker
+        const uint64_t va = row_at(off, n, m / threads * t);
+        const uint64_t vb = t + 1 == threads ? n : row_at(off, n, m / threads * (t + 1));
+        uint64_t bad;
+#if defined(__x86_64__)
+        bad = avx2 ? rows_avx2(off, cum, va, vb, stop) : rows_plain(off, cum, va, vb, stop);
+#else
+        bad = rows_plain(off, cum, va, vb, stop);
+#endif
+        if (bad) stop.store(true, std::memory_order_relaxed);
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < threads; ++t) pool.emplace_back(scan, t);
+    scan(0);
+    for (auto& th : pool) th.join();
+    return !stop.load();
+}
+
+}  // namespace hsawgpu

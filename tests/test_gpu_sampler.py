@@ -459,6 +459,36 @@ def test_large_upload_staged_and_plain(ctx, port, monkeypatch, threads):
     assert np.array_equal(got.nodes, exp.nodes) and np.array_equal(got.edges, exp.edges)
 
 
+@pytest.mark.parametrize("weights", ["indegree", "one-bit-off", "given"])
+def test_upload_regenerates_indegree_sums(ctx, port, monkeypatch, weights):
+    """Large uploads do not send in_cum when host threads have verified, bit for bit, that every
+    row holds build_graph's sequential 1/in-degree sums (proj/src/graph.cpp:172-178): the device
+    regenerates them. Forced here on a small graph: same pool as the oracle either way, and any
+    other weights - a single differing bit included - take the plain copy."""
+    from oracle.oracle import Csr
+    from paper_1702_05854_b200 import rmat
+    monkeypatch.setenv("HSAW_UPLOAD_REGEN", "2")
+    g = rmat.rmat_graph(13, 10, seed=4, suspect_frac=0.02)
+    cum = g.in_cum.copy()
+    if weights == "one-bit-off":  # last bit of one interior cumulative weight (still increasing)
+        e = int(np.argmax(np.diff(g.in_offsets.astype(np.int64)))) 
+        pos = int(g.in_offsets[e]) + 1
+        cum[pos] = np.nextafter(cum[pos], 2.0)
+    elif weights == "given":
+        deg = np.diff(g.in_offsets.astype(np.int64))
+        row = np.repeat(np.arange(g.n), deg)
+        cum = cum * (0.5 + 0.4 * ((row % 7) / 7.0))  # rows still increasing, totals below one
+    csr = Csr(g.n, g.m, g.in_offsets, g.in_src, cum, g.p_of)
+    upload(ctx, csr)
+    assert ctx.upload_mode == ("regenerated" if weights == "indegree" else "copied")
+    with ctx.stream(seed=6) as st:
+        st.ensure(2000)
+        got = st.to_pool(2000)
+    exp = port.stream_samples(csr, 2000, seed=6)
+    assert got.attempts == exp.attempts and got.nsamples == exp.nsamples
+    assert np.array_equal(got.nodes, exp.nodes) and np.array_equal(got.edges, exp.edges)
+
+
 def test_stream_keeping_one_item_array(ctx, gpu_lib, synth3000, port):
     """hsaw_gpu_stream_keep: a pool that keeps only the edge ids (or only the nodes) has the same
     order and counters, serves greedy / coverage of its own kind bit-exactly, and refuses the other."""
