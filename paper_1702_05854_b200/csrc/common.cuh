@@ -540,6 +540,11 @@ struct hsaw_gpu_ctx {
     hsawgpu::DeviceGraph g;
     uint64_t graph_bytes = 0;
     int upload_mode = 0;  // in_cum of the last graph_upload: 0 copied, 1 regenerated on the device
+    // side stream for work that may run beside the context stream (the replay of walks that
+    // outgrew their log chunk, sampler.cu launch_decode_pairs / join_side_stream)
+    cudaStream_t side = nullptr;
+    cudaEvent_t side_go = nullptr, side_done = nullptr;
+    bool side_pending = false;
     // L2 access-policy window over the compact graph (headers + sources), attached to the K1
     // launches only: those lines are marked persisting, so the walk-log stream of the same kernel
     // cannot evict them, while every other kernel on the stream keeps normal caching.
@@ -715,13 +720,15 @@ struct StageScope {
         HSAW_CUDA_CHECK(cudaEventCreate(&e));
         return e;
     }
-    StageScope(hsaw_gpu_ctx* c, int s) : ctx(c), stage(s) {
+    cudaStream_t on = nullptr;
+    StageScope(hsaw_gpu_ctx* c, int s, cudaStream_t stream = nullptr)
+        : ctx(c), stage(s), on(stream ? stream : c->stream) {
         a = get(c);
         b = get(c);
-        cudaEventRecord(a, c->stream);
+        cudaEventRecord(a, on);
     }
     ~StageScope() {
-        cudaEventRecord(b, ctx->stream);
+        cudaEventRecord(b, on);
         ctx->pending.push_back({stage, a, b});
         ++ctx->stage_launches[stage];
     }

@@ -928,6 +928,12 @@ void hsaw_gpu_ctx_destroy(hsaw_gpu_ctx* ctx) {
     if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
     ctx->release_scratch();  // (now empty) stream-ordered frees precede the stream's destruction
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+        cudaEventDestroy(ctx->side_go);
+        cudaEventDestroy(ctx->side_done);
+    }
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

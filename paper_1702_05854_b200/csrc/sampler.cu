@@ -1283,18 +1283,42 @@ void launch_decode(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_t* d_seed,
 }
 
 // Replay of the `nsel` walks listed in d_sel (indices into the encoded arrays) as pair logs.
+// walks with more nodes than this are only queued by K2b's main pass (the mid / long passes read
+// them): the edge count from which a replay may overlap that pass
+uint32_t distinct_check_defers_walks_longer_than() { return kTableSize / 2; }
+
+// Makes the context stream wait for a replay that was launched on the side stream.
+void join_side_stream(hsaw_gpu_ctx* ctx) {
+    if (!ctx->side_pending) return;
+    HSAW_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->side_done, 0));
+    ctx->side_pending = false;
+}
+
+// on_side: run on the context's side stream, after everything queued on the context stream so
+// far; join_side_stream orders the context stream behind it again.
 void launch_decode_pairs(hsaw_gpu_ctx* ctx, uint64_t nsel, const uint32_t* d_sel,
                          const uint64_t* d_seed, const uint32_t* d_len, uint2* const* d_pair_dst,
-                         uint8_t* d_status, uint64_t* d_stats, uint64_t* d_cursor) {
+                         uint8_t* d_status, uint64_t* d_stats, uint64_t* d_cursor, bool on_side) {
     if (nsel == 0) return;
     DecodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, src_ref(ctx->g), ctx->g.thr, ctx->g.n,
                    nsel,         d_seed,       d_len,      nullptr,    nullptr,    nullptr,
                    d_status,     nullptr,      d_stats,    d_cursor,   d_sel,      d_pair_dst};
-    HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
+    cudaStream_t run = ctx->stream;
+    if (on_side) {
+        if (!ctx->side) {
+            HSAW_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+            HSAW_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->side_go, cudaEventDisableTiming));
+            HSAW_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->side_done, cudaEventDisableTiming));
+        }
+        HSAW_CUDA_CHECK(cudaEventRecord(ctx->side_go, ctx->stream));
+        HSAW_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->side_go, 0));
+        run = ctx->side;
+    }
+    HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, run));
     auto go = [&](auto kernel) {
         int blocks = persistent_blocks(ctx, kernel, nsel);
-        StageScope timer(ctx, HSAW_STAGE_DECODE);
-        kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+        StageScope timer(ctx, HSAW_STAGE_DECODE, run);
+        kernel<<<blocks, kThreads, 0, run>>>(p);
         check_launch(ctx, "decode_kernel<pairs>");
     };
     if (ctx->rng_mode == 1)
@@ -1304,6 +1328,10 @@ void launch_decode_pairs(hsaw_gpu_ctx* ctx, uint64_t nsel, const uint32_t* d_sel
         go(decode_kernel<true, kLayoutCompact>);
     else
         go(decode_kernel<true, kLayoutFat>);
+    if (on_side) {
+        HSAW_CUDA_CHECK(cudaEventRecord(ctx->side_done, ctx->side));
+        ctx->side_pending = true;
+    }
 }
 
 // Exact recheck on either node source. Classic: d_edge_off/d_nodes(/d_nnodes). Pair logs:
@@ -1346,6 +1374,7 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 16, cudaMemcpyDeviceToHost, ctx->stream));
     HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     if (h[2] > mid_cap) fail(HSAW_ECUDA, "distinct check: mid-size walk queue overflow");
+    join_side_stream(ctx);  // a replay running beside the main pass: its walks are read from here on
     if (h[2]) {  // walks of 513..2048 nodes: second pass with 16 KB tables over the queued ids
         CheckParams q = p;
         q.nwalks = h[2];

@@ -49,7 +49,12 @@ uint32_t launch_distinct_check(hsaw_gpu_ctx* ctx, uint64_t nwalks, const uint64_
 // the recheck reading nodes from d_pair_src[w][0..d_lens[w]].x.
 void launch_decode_pairs(hsaw_gpu_ctx* ctx, uint64_t nsel, const uint32_t* d_sel,
                          const uint64_t* d_seed, const uint32_t* d_len, uint2* const* d_pair_dst,
-                         uint8_t* d_status, uint64_t* d_stats, uint64_t* d_cursor);
+                         uint8_t* d_status, uint64_t* d_stats, uint64_t* d_cursor,
+                         bool on_side = false);
+// on_side replays run beside the context stream until join_side_stream (called by the recheck
+// after its main pass); that is safe for walks of more than this many edges
+uint32_t distinct_check_defers_walks_longer_than();
+void join_side_stream(hsaw_gpu_ctx* ctx);
 uint32_t launch_distinct_check_pairs(hsaw_gpu_ctx* ctx, uint64_t nwalks,
                                      const uint2* const* d_pair_src, const uint32_t* d_lens,
                                      uint8_t* d_status);

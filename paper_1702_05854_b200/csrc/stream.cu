@@ -122,11 +122,12 @@ __global__ void gather_recorded(uint64_t nbatches, uint32_t l, uint64_t first_gl
 __global__ void place_overflow(uint64_t nwalks, const uint32_t* __restrict__ ovf_pairs,
                                const uint64_t* __restrict__ ovf_off, uint2* replay_base,
                                const uint2** __restrict__ enc_src, uint32_t* __restrict__ sel,
-                               uint32_t* __restrict__ nsel) {
+                               uint32_t* __restrict__ nsel, const uint32_t* __restrict__ enc_len) {
     uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= nwalks || ovf_pairs[w] == 0) return;
     enc_src[w] = replay_base + ovf_off[w];
     sel[atomicAdd(nsel, 1u)] = (uint32_t)w;  // order is irrelevant: each entry is independent work
+    atomicMin(nsel + 1, enc_len[w]);         // shortest replayed walk (decides the overlap below)
 }
 
 // Pair logs -> final node / edge arrays of the pool. One warp per group of 32 encoded walks: each
@@ -495,6 +496,7 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
             }
             HSAW_CUDA_CHECK(cudaMemsetAsync(x.ovf_pairs.p + E, 0, 4, st));
             HSAW_CUDA_CHECK(cudaMemsetAsync(nsel, 0, 4, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(nsel + 1, 0xFF, 4, st));
             exclusive_sum_u32_to_u64(ctx, x.ovf_pairs.p, x.tmp_off.p, E + 1);
             // recorded walks are complete by construction
             HSAW_CUDA_CHECK(cudaMemsetAsync(x.status.p, 1, E, st));
@@ -505,12 +507,21 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
             x.sel.ensure_scratch(E);
             place_overflow<<<blocks_for(E, 256), 256, 0, st>>>(
                 E, x.ovf_pairs.p, x.tmp_off.p, x.replay.p,
-                reinterpret_cast<const uint2**>(x.enc_src.p), x.sel.p, nsel);
+                reinterpret_cast<const uint2**>(x.enc_src.p), x.sel.p, nsel, x.enc_len.p);
             check_launch(ctx, "place_overflow");
-            const uint64_t nreplay = read_u32(ctx, nsel);
+            const uint64_t both = read_u64(ctx, s->stats.p + 11);
+            const uint64_t nreplay = (uint32_t)both;
+            const uint32_t shortest = (uint32_t)(both >> 32);
+            // The replay is a handful of single lanes chasing thousands of dependent steps each
+            // (1.3 ms per chunk at the Twitter shape with the GPU idle). Walks that outgrew a log
+            // chunk (> 1024 pairs) are beyond what K2b's main pass reads (it only queues them for
+            // the mid / long passes), so the replay runs on a side stream beside that pass and
+            // is joined right after it. Replays of SHORT walks (arena exhaustion) keep the
+            // serial order.
+            const bool overlap = distinct_check_defers_walks_longer_than() <= shortest;
             launch_decode_pairs(ctx, nreplay, x.sel.p, x.enc_seed.p, x.enc_len.p,
                                 reinterpret_cast<uint2* const*>(x.enc_src.p), x.status.p,
-                                s->stats.p, s->stats.p + 8);
+                                s->stats.p, s->stats.p + 8, overlap);
             s->replayed += nreplay;
         }
         // ---- K2b on the pair logs
