@@ -586,15 +586,21 @@ void pin_in_l2(hsaw_gpu_ctx* ctx, const void* base, size_t bytes) {
 // Layout choice: the compact arrays while the 16-byte row headers fit in L2 (the
 // header gather then stays an L2 hit even when the sources spill to HBM: measured 10.5 vs 11.0 ms
 // per 2^20 batches at R-MAT scale 22, 13.7 vs 11.0 ms at scale 24), else fat edge records (one HBM
-// line per step). HSAW_LAYOUT=compact|fat overrides.
+// line per step) while they fit the TLB's reach, else compact again. HSAW_LAYOUT=compact|fat
+// overrides.
 int choose_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
     if (const char* env = std::getenv("HSAW_LAYOUT")) {
         if (env[0] == 'c') return kLayoutCompact;
         if (env[0] == 'f') return kLayoutFat;
     }
     const uint64_t l2 = (uint64_t)device_info(ctx->device).l2_bytes;
-    (void)m;
-    return 16ull * n <= l2 ? kLayoutCompact : kLayoutFat;
+    if (16ull * n <= l2) return kLayoutCompact;
+    // One gather per step beats two only while the edge records stay inside the TLB's reach:
+    // dependent random 32-byte gathers run at 36 G/s from tables of up to 64 GB and at 14 / 10 / 9
+    // G/s from 96 / 120 / 150 GB, whatever the allocation API (tools/tlb_probe.cu,
+    // profiles/r02e_tlb_probe.txt: 2 MB pages everywhere). The Friendster shape (3.78 G edges,
+    // 121 GB of records) samples 1.6x faster from 15 GB of sources + 1 GB of headers.
+    return 32ull * m <= (64ull << 30) ? kLayoutFat : kLayoutCompact;
 }
 
 void free_graph(hsaw_gpu_ctx* ctx) {  // the backing stores keep their capacity for the next upload
