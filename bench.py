@@ -567,7 +567,10 @@ def run_b200(args):
             "layout": "fat (32-byte edge records, one HBM gather per step)" if fat else
                       ("compact (in_src packed three 21-bit entries per 64-bit word + 16-byte row "
                        "headers, L2 resident)" if g.n <= 2**20 else
-                       "compact (4-byte in_src + 16-byte row headers; headers L2 resident)"),
+                       "compact (4-byte in_src + 16-byte row headers; headers L2 resident)"
+                       if 16 * g.n <= (120 << 20) else
+                       "compact (4-byte in_src + 16-byte row headers, two HBM gathers per step: "
+                       "32-byte edge records would exceed the TLB's reach, tools/tlb_probe.cu)"),
             "parallelism": f"walks sharded by batch range over {world} GPU(s), graph replicated",
             "l2_policy": (f"L2 flushed before every timed step (256 MB memset on the launching "
                           f"stream between the per-step event pairs); graph on device "
