@@ -827,6 +827,10 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
 // Two table sizes: the main pass keeps 56 warps per SM resident with 4 KB tables (walks of up to
 // 512 nodes); the few longer walks are queued for a second pass with 16 KB tables, and walks beyond
 // that for the block-per-walk kernel.
+#ifndef HSAW_K2B_LOAD
+#define HSAW_K2B_LOAD 4
+#endif
+constexpr uint32_t kTableLoad = HSAW_K2B_LOAD;  // slots per node before rounding up to a power of two
 constexpr int kCheckWarps = 8, kMidWarps = 4;
 constexpr uint32_t kTableSize = 1024, kMidTableSize = 4096;  // u32 slots per warp
 constexpr uint32_t kSmemNodes = kMidTableSize / 2;           // largest walk handled in shared memory
@@ -935,7 +939,8 @@ __global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
             } else if (nn <= TABLE / 2) {
                 // table of >= 4*nn slots where the warp's share allows it, else >= 2*nn: lanes
                 // probe in lockstep, so the longest probe sequence of the 32 sets the pace
-                uint32_t bits = 32 - __clz(4 * nn - 1);
+                // HSAW_K2B_LOAD (compile-time A/B): table of >= 4*nn slots; 2*nn was measured slower (C4: K2b 2.7 -> 3.5 ms per step: the lanes probe in lockstep, the longest probe sets the pace)
+                uint32_t bits = 32 - __clz(kTableLoad * nn - 1);
                 if ((1u << bits) > TABLE) --bits;
                 const uint32_t size = 1u << bits;
                 bool mydup = false;
