@@ -341,6 +341,11 @@ int hsaw_gpu_counts_bound(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint32_t 
                           uint64_t cap, uint64_t* bound);
 int hsaw_gpu_counts_threshold(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint32_t limit,
                               uint32_t* min_count);
+/* hsaw_gpu_counts_threshold raised to ck_percent % of the k-th largest count (0: the plain rule):
+ * an optimistic threshold, valid iff the greedy run on the reduced walks ends with
+ * hsaw_gpu_last_greedy_min_gain >= it; callers step down 60 -> 30 -> 0 -> everything. */
+int hsaw_gpu_counts_threshold_for(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint32_t limit,
+                                  uint32_t k, uint32_t ck_percent, uint32_t* min_count);
 int hsaw_gpu_reduced_walks(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind, uint64_t off,
                            uint64_t cnt, const uint32_t* d_counts, uint32_t min_count,
                            hsaw_gpu_walkset** out, uint64_t* nsets, uint64_t* nitems);

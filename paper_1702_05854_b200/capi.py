@@ -139,6 +139,7 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_stream_histogram.argtypes = [vp, vp, C.c_int, C.c_uint64, C.c_uint64, u32p, C.c_uint64, vp]
     L.hsaw_gpu_counts_bound.argtypes = [vp, vp, C.c_uint32, C.c_uint32, C.c_uint64, u64p]
     L.hsaw_gpu_counts_threshold.argtypes = [vp, vp, C.c_uint32, u32p]
+    L.hsaw_gpu_counts_threshold_for.argtypes = [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, u32p]
     L.hsaw_gpu_reduced_walks.argtypes = [vp, vp, C.c_int, C.c_uint64, C.c_uint64, vp, C.c_uint32,
                                          C.POINTER(vp), u64p, u64p]
     L.hsaw_gpu_walkset_copy_device.argtypes = [vp, vp, vp]
@@ -180,6 +181,7 @@ EXPORTS = (
     "hsaw_gpu_stream_restrict", "hsaw_gpu_stream_crossings",
     "hsaw_gpu_rr_node_sets", "hsaw_gpu_walkset_export",
     "hsaw_gpu_stream_histogram", "hsaw_gpu_counts_bound", "hsaw_gpu_counts_threshold",
+    "hsaw_gpu_counts_threshold_for",
     "hsaw_gpu_reduced_walks", "hsaw_gpu_walkset_copy_device", "hsaw_gpu_walkset_from_device",
     "hsaw_gpu_last_greedy_min_gain", "hsaw_gpu_device_alloc", "hsaw_gpu_device_free",
     "hsaw_gpu_device_copy", "hsaw_gpu_counts_add",

@@ -2162,6 +2162,39 @@ int hsaw_gpu_counts_threshold(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint3
     });
 }
 
+// The mass rule of hsaw_gpu_counts_threshold raised to ck_percent % of the k-th largest count: the
+// optimistic rungs of hsaw_gpu_greedy's threshold ladder for callers that gather reduced walks
+// (a run whose smallest gain stays at or above the threshold proves it was enough).
+int hsaw_gpu_counts_threshold_for(hsaw_gpu_ctx* ctx, const uint32_t* d_counts, uint32_t limit,
+                                  uint32_t k, uint32_t ck_percent, uint32_t* min_count) {
+    if (!ctx || !d_counts || !min_count) return HSAW_EINVAL;
+    return guarded(ctx, [&] {
+        const std::vector<uint64_t> bins = count_bins(ctx, d_counts, limit);
+        uint64_t total = 0;
+        for (uint64_t b : bins) total += b;
+        uint32_t mc = 1;
+        if (total > (1ull << 20)) {
+            uint64_t above = 0;
+            mc = kCountBins - 1;
+            for (uint32_t c = kCountBins - 1; c >= 1; --c) {
+                if (above + bins[c] > total / 8) break;
+                above += bins[c];
+                mc = c;
+            }
+        }
+        if (ck_percent && k) {
+            uint64_t items = 0;
+            uint32_t ck = 0;
+            for (uint32_t c = kCountBins - 1; c >= 1 && ck == 0; --c) {
+                items += (bins[c] + c - 1) / c;
+                if (items >= k) ck = c;
+            }
+            mc = std::max<uint32_t>(mc, (uint32_t)((uint64_t)ck * ck_percent / 100));
+        }
+        *min_count = mc;
+    });
+}
+
 int hsaw_gpu_reduced_walks(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream, int kind, uint64_t off,
                            uint64_t cnt, const uint32_t* d_counts, uint32_t min_count,
                            hsaw_gpu_walkset** out, uint64_t* nsets, uint64_t* nitems) {

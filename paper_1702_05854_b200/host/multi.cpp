@@ -414,8 +414,18 @@ public:
         GreedyResult res;
         res.solution.resize(k);
         try {
-            std::uint32_t min_count = 1;
-            chk(hsaw_gpu_counts_threshold(ctx_, counts, limit, &min_count), ctx_, "counts_threshold");
+            // thresholds from bold to safe: 60 %, 30 % of the k-th largest count, the 1/8-mass rule,
+            // then everything; a run whose smallest gain stays at or above its threshold is exact
+            std::vector<std::uint32_t> ladder;
+            for (std::uint32_t pct : {60u, 30u, 0u}) {
+                std::uint32_t mc = 1;
+                chk(hsaw_gpu_counts_threshold_for(ctx_, counts, limit, k, pct, &mc), ctx_,
+                    "counts_threshold");
+                if (ladder.empty() || mc < ladder.back()) ladder.push_back(mc);
+            }
+            if (ladder.back() > 1) ladder.push_back(1);
+            std::size_t rung = 0;
+            std::uint32_t min_count = ladder[rung];
             for (;;) {
                 hsaw_gpu_walkset* mine = nullptr;
                 std::uint64_t nsets = 0, nitems = 0;
@@ -452,7 +462,7 @@ public:
                 hsaw_gpu_walkset_destroy(all);
                 chk(rc3, ctx_, "greedy");
                 if (min_count <= 1 || hsaw_gpu_last_greedy_min_gain(ctx_) >= min_count) break;
-                min_count = 1;  // the k-th gain fell below the threshold: gather everything
+                min_count = ladder[++rung];  // the k-th gain fell below the threshold: next rung
             }
         } catch (...) {
             hsaw_gpu_device_free(ctx_, counts);

@@ -203,12 +203,12 @@ class GpuEngine:
                                                             self.capi.C.byref(out)))
         return out.value
 
-    def threshold_from_counts(self, counts: torch.Tensor) -> int:
+    def threshold_from_counts(self, counts: torch.Tensor, k: int = 0, ck_percent: int = 0) -> int:
+        """The 1/8-mass indexing threshold, raised to ck_percent % of the k-th largest count."""
         out = self.capi.C.c_uint32()
         torch.cuda.current_stream().synchronize()
-        self.ctx._chk(self.capi.lib().hsaw_gpu_counts_threshold(self.ctx.h, counts.data_ptr(),
-                                                                counts.numel(),
-                                                                self.capi.C.byref(out)))
+        self.ctx._chk(self.capi.lib().hsaw_gpu_counts_threshold_for(
+            self.ctx.h, counts.data_ptr(), counts.numel(), k, ck_percent, self.capi.C.byref(out)))
         return out.value
 
     def reduced_walks(self, kind, off, cnt, counts: torch.Tensor, min_count: int):
@@ -420,11 +420,19 @@ class ShardedSolver:
         to the items that can still win (global count >= the indexing threshold of the single-GPU
         greedy), then the single-GPU greedy on the gathered sets, redundantly on every rank: same
         selections everywhere, no per-round exchange. If the k-th gain falls below the threshold
-        the reduced instance was not enough: repeat with everything (threshold 1)."""
+        the reduced instance was not enough: repeat with the next, lower threshold."""
         counts = self.eng.local_counts(kind, lo, n, cand)
         self.comm.allreduce_sum_(counts)
-        min_count = self.eng.threshold_from_counts(counts)
-        while True:
+        # thresholds from bold to safe (60 %, 30 % of the k-th largest count, the 1/8-mass rule,
+        # then everything): a run whose smallest gain stays at or above its threshold is exact
+        ladder = []
+        for pct in (60, 30, 0):
+            mc = self.eng.threshold_from_counts(counts, k, pct)
+            if not ladder or mc < ladder[-1]:
+                ladder.append(mc)
+        if ladder[-1] > 1:
+            ladder.append(1)
+        for min_count in ladder:
             lens, items = self.eng.reduced_walks(kind, lo, n, counts, min_count)
             all_lens = self.comm.allgather_var(lens)
             all_items = self.comm.allgather_var(items)
@@ -432,7 +440,7 @@ class ShardedSolver:
                 kind, torch.cat(all_lens), torch.cat(all_items), k, cand)
             if min_count <= 1 or min_gain >= min_count:
                 return solution, coverage
-            min_count = 1
+        raise AssertionError("unreachable: the last rung gathers everything")
 
     # -- run_interdiction (proj/src/interdiction.cpp:12-67), sharded
     # ---- estimate_suspension (proj/src/evaluation.cpp:209-242), runs sharded over the ranks -------

@@ -90,17 +90,25 @@ class CpuEngine:
             left -= take
         return min(total, cap)
 
-    def threshold_from_counts(self, counts):
+    def threshold_from_counts(self, counts, k=0, ck_percent=0):
         bins = self._bins(counts)
         total = int(bins.sum())
-        if total <= (1 << 20):
-            return 1
-        above, mc = 0, self.K_BINS - 1
-        for c in range(self.K_BINS - 1, 0, -1):
-            if above + int(bins[c]) > total // 8:
-                break
-            above += int(bins[c])
-            mc = c
+        mc = 1
+        if total > (1 << 20):
+            above, mc = 0, self.K_BINS - 1
+            for c in range(self.K_BINS - 1, 0, -1):
+                if above + int(bins[c]) > total // 8:
+                    break
+                above += int(bins[c])
+                mc = c
+        if ck_percent and k:  # hsaw_gpu_counts_threshold_for: a share of the k-th largest count
+            items, ck = 0, 0
+            for c in range(self.K_BINS - 1, 0, -1):
+                items += (int(bins[c]) + c - 1) // c
+                if items >= k:
+                    ck = c
+                    break
+            mc = max(mc, ck * ck_percent // 100)
         return mc
 
     def reduced_walks(self, kind, off, cnt, counts, min_count):
