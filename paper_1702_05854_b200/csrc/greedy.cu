@@ -1366,10 +1366,9 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
         const bool from_cache = hist_cache_usable(stream, cand_ids) && off == 0;
         bool counts_valid = false;
         std::vector<uint64_t> bins;
-        auto run = [&](uint32_t min_count, uint32_t ck_percent) -> bool {
-            HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
-            HSAW_CUDA_CHECK(cudaMemsetAsync(d_partial.p, 0, 8, st));  // no previous winner yet
-            // ---- K3: marginal-gain counts (a stream prefix comes from the histogram cache)
+        // ---- K3: marginal-gain counts (a stream prefix comes from the histogram cache) and their
+        // distribution; idempotent until an attempt invalidates the counts
+        auto prepare = [&](bool want_bins) {
             if (!counts_valid) {
                 if (from_cache) {
                     full_cnt = hist_prefix(ctx, stream, kind, limit, cnt);
@@ -1382,7 +1381,7 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                 counts_valid = true;
                 bins.clear();
             }
-            if ((min_count == 0 || dense_possible) && bins.empty()) {
+            if (want_bins && bins.empty()) {
                 auto* d_bins = reinterpret_cast<unsigned long long*>(d_partial.p + 4);
                 HSAW_CUDA_CHECK(cudaMemsetAsync(d_bins, 0, kCountBins * 8, st));
                 {
@@ -1395,11 +1394,16 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                                                 cudaMemcpyDeviceToHost, st));
                 HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
             }
+        };
+        auto run = [&](uint32_t min_count, uint32_t ck_percent) -> bool {
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_cov.p, 0, cov_words * 4, st));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(d_partial.p, 0, 8, st));  // no previous winner yet
+            prepare(min_count == 0 || dense_possible);
+            uint64_t total = 0;  // occurrences of all (candidate) items in the view
+            for (uint64_t b : bins) total += b;
             if (min_count == 0) {
                 // Index only what can win: the smallest count whose items (and everything above)
                 // make up at most 1/8 of all occurrences. Small inputs index everything.
-                uint64_t total = 0;
-                for (uint64_t b : bins) total += b;
                 min_count = 1;
                 if (total > (1ull << 20)) {
                     uint64_t above = 0;
@@ -1425,7 +1429,10 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                     if (min_count >= t) return false;  // already known to be too high
             }
             // ---- the instance the rounds run on: the view itself, or its dense reduction
-            const bool dense = dense_possible && (dense_forced || min_count > 1);
+            // (the full index too takes the dense form while the view holds fewer items than the
+            // id space has ids: every per-item array then has one entry per PRESENT item - nSIA at
+            // the Twitter shape: 4.7 M node occurrences against 41.6 M nodes)
+            const bool dense = dense_possible && (dense_forced || min_count > 1 || total < limit);
             WalkView rv = v;
             uint32_t rlimit = limit;
             uint32_t* rcnt = nullptr;
@@ -1670,10 +1677,26 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
             return true;
         };
         bool ok = false;
-        if (dense_possible)  // optimistic thresholds: an attempt on a dense instance is cheap
+        // Thresholds only pay while the rounds' gains stay near the initial counts. When the k
+        // largest counts alone add up to a good part of the walks (node candidates next to the
+        // suspects: a few hundred picks cover almost everything), coverage saturates, the late
+        // gains collapse towards 1 and every thresholded attempt is bound to fail: go straight to
+        // the full index then.
+        bool saturating = false;
+        if (dense_possible) {
+            prepare(true);
+            uint64_t top = bins[kCountBins - 1], left = k;
+            for (uint32_t c = kCountBins - 2; c >= 1 && left > 0; --c) {
+                const uint64_t take = std::min<uint64_t>(bins[c] / c, left);
+                top += take * c;
+                left -= take;
+            }
+            saturating = top >= cnt / 2;
+        }
+        if (dense_possible && !saturating)  // optimistic thresholds: a dense attempt is cheap
             for (uint32_t pct : {60u, 30u})
                 if ((ok = run(0, pct))) break;
-        if (!ok) ok = run(0, 0);
+        if (!ok && !saturating) ok = run(0, 0);
         if (!ok) {
             ++ctx->greedy_full_index_reruns;
             if (!run(1, 0)) fail(HSAW_ECUDA, "greedy: full index run reported an unindexed winner");
