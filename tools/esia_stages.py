@@ -27,7 +27,11 @@ for rep in range(REPS):
                           want_json=True)
     wall = time.perf_counter() - t0
     st = ctx.stage_times(reset=True)
-    print(json.dumps({"rep": rep, "wall_s": round(wall, 3), "timing": r["timing"],
+    try:
+        alloc = capi.alloc_counters()
+    except Exception:
+        alloc = None
+    print(json.dumps({"rep": rep, "wall_s": round(wall, 3), "alloc": alloc, "timing": r["timing"],
                       "iterations": r["iterations"], "samples_used": r["samples_used"],
                       "coverage": r["coverage"],
                       "stage_ms": {n_: round(v[0], 1) for n_, v in st.items() if v[1]},
