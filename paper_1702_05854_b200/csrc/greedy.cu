@@ -251,17 +251,24 @@ __global__ void __launch_bounds__(kCocWarps * 32) count_of_counts(const uint32_t
         else
             atomicAdd(&big, (unsigned long long)c);
     };
-    const uint64_t quads = limit / 4;
+    // 128-bit loads over the 16-byte aligned middle (pool allocations are aligned; a caller's
+    // device pointer need not be), scalar loads for the few counters before and after it
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint4* cnt4 = reinterpret_cast<const uint4*>(cnt);  // pool allocations are 256-byte aligned
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < quads; i += stride) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t head = min((uint64_t)((16u - (reinterpret_cast<uintptr_t>(cnt) & 15u)) & 15u) / 4,
+                              (uint64_t)limit);
+    const uint64_t quads = (limit - head) / 4;
+    const uint4* cnt4 = reinterpret_cast<const uint4*>(cnt + head);
+    for (uint64_t i = tid; i < quads; i += stride) {
         const uint4 c = __ldcs(cnt4 + i);
         add(c.x);
         add(c.y);
         add(c.z);
         add(c.w);
     }
-    if (blockIdx.x == 0 && threadIdx.x < (limit & 3u)) add(cnt[quads * 4 + threadIdx.x]);
+    if (tid < head) add(cnt[tid]);
+    const uint64_t tail0 = head + quads * 4;
+    if (tid < limit - tail0) add(cnt[tail0 + tid]);
     __syncthreads();
     for (uint32_t c = threadIdx.x; c < kCountBins - 1; c += blockDim.x) {
         unsigned long long n = 0;

@@ -179,6 +179,9 @@ def test_gathered_greedy_with_threshold_and_fallback(gpu_lib):
                 it = items.cpu().numpy()
                 assert lens.sum().item() == items.numel() and np.all(c[it] >= mc)
                 assert items.numel() == int(c[c >= mc].sum())  # every occurrence of an indexed item
+                # counts handed over at any alignment (a view that starts 4 bytes into the buffer)
+                assert eng.bound_from_counts(counts[1:], 100, 10**12) == \
+                    eng.bound_from_counts(counts[1:].clone(), 100, 10**12)
                 for k in (30, 3000):
                     exp_sol, exp_cov = ctx.greedy(k, stream=eng.stream, kind=kind, off=0, cnt=200_000)
                     sol, cov = solver.greedy(k, kind, 200_000)
