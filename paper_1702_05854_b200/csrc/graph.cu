@@ -848,7 +848,7 @@ void install_graph(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint64_t* d_
             build_edge_records<<<blocks, 256, 0, st>>>(n, d_off, d_src, d_cum, ctx->g.nodes, ctx->g.edges,
                                                        d_bad, big_rows, big_count, big_cap);
             check_launch(ctx, "build_edge_records");
-            build_edge_records_big<<<ctx->sm_count * 2, 256, 0, st>>>(
+            build_edge_records_big<<<ctx->sm_count * 8, 256, 0, st>>>(
                 n, d_off, d_src, d_cum, ctx->g.nodes, ctx->g.edges, d_bad, big_rows, big_count, big_cap);
             check_launch(ctx, "build_edge_records_big");
         }
