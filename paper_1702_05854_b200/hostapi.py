@@ -437,7 +437,9 @@ def interdict_devices(graph: Graph, p_of, kind, k, eps, delta, devices, seed=0, 
     return dict(kind="edge" if kind == 0 else "node", k=res.k, epsilon=eps, delta=delta,
                 solution=[int(x) for x in sol[:k]], est_suspension=res.est_suspension,
                 coverage=res.coverage, samples_used=res.samples_used, attempts=res.attempts,
-                iterations=res.iterations, passed_check=bool(res.passed_check))
+                iterations=res.iterations, passed_check=bool(res.passed_check),
+                timing=dict(wall_time_s=res.wall_time_s, sample_s=res.sample_s,
+                            greedy_s=res.greedy_s, check_s=res.check_s))
 
 
 def lt_forward_simulate(graph: Graph, p_of, state, dg: DeviceGraph | None = None):
