@@ -831,6 +831,10 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
 #define HSAW_K2B_LOAD 4
 #endif
 constexpr uint32_t kTableLoad = HSAW_K2B_LOAD;  // slots per node before rounding up to a power of two
+#ifndef HSAW_K2B_BITMAP
+#define HSAW_K2B_BITMAP 1
+#endif
+constexpr bool kBitmapProof = HSAW_K2B_BITMAP != 0;  // compile-time A/B of the bit-map fast path
 constexpr int kCheckWarps = 8, kMidWarps = 4;
 constexpr uint32_t kTableSize = 1024, kMidTableSize = 4096;  // u32 slots per warp
 constexpr uint32_t kSmemNodes = kMidTableSize / 2;           // largest walk handled in shared memory
@@ -871,7 +875,7 @@ __device__ __forceinline__ uint32_t walk_node(const CheckParams& p, uint64_t w, 
 // walks, where 32 serial long walks per warp would leave most of the GPU idle).
 template <bool PAIRS, uint32_t TABLE, int WARPS, uint32_t GROUP>
 __global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
-    extern __shared__ uint32_t tables[];  // WARPS x TABLE
+    extern __shared__ __align__(16) uint32_t tables[];  // WARPS x TABLE
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     uint32_t* tab = tables + wib * TABLE;
@@ -944,7 +948,40 @@ __global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
                 if ((1u << bits) > TABLE) --bits;
                 const uint32_t size = 1u << bits;
                 bool mydup = false;
-                for (uint32_t c = 0; c < nn; c += 128) {
+                // Fast proof of distinctness first: hash every node to one bit of a 32*TABLE-bit
+                // map (the same shared memory); if no two nodes meet in a bit they are pairwise
+                // distinct and the walk is done - one atomicOr per node, no probing, no lockstep
+                // tails. Only walks with a bit collision (a true repeat, or chance: 1 - exp(-nn^2
+                // / (64 TABLE)), 23 % at 131 nodes) go through the exact hash set below.
+                bool exact_needed = true;
+                if (kBitmapProof && (uint64_t)nn * nn <= 64ull * TABLE) {
+                    constexpr uint32_t kMapBits = 5 + (TABLE == 1024 ? 10 : TABLE == 4096 ? 12 : 0);
+                    static_assert(TABLE == 1024 || TABLE == 4096, "bit-map width follows the table size");
+                    for (uint32_t i = lane; i < TABLE / 4; i += 32)  // 128-bit stores
+                        reinterpret_cast<uint4*>(tab)[i] = make_uint4(0u, 0u, 0u, 0u);
+                    __syncwarp();
+                    uint32_t coll = 0;
+                    uint32_t first[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) first[q] = v[q];
+                    for (uint32_t c = 0; c < nn; c += 128) {
+                        uint32_t x[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t i = c + q * 32 + lane;
+                            x[q] = c == 0 ? first[q] : (i < nn ? node_at(i) : kInvalidNode);
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            if (c + q * 32 + lane >= nn) continue;
+                            const uint32_t r = (x[q] * 0x85EBCA6Bu) >> (32 - kMapBits);
+                            coll |= atomicOr(&tab[r >> 5], 1u << (r & 31)) >> (r & 31);
+                        }
+                    }
+                    exact_needed = __any_sync(kFullMask, coll & 1u);
+                    __syncwarp();
+                }
+                for (uint32_t c = 0; exact_needed && c < nn; c += 128) {
                     if (c != 0) {  // (the first 128 were requested one walk ahead)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
@@ -953,7 +990,10 @@ __global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
                         }
                     }
                     if (c == 0) {  // the clears overlap the reads in flight
-                        for (uint32_t i = lane; i < size; i += 32) tab[i] = kInvalidNode;
+                        // (nn > 32 here, so size >= 128 words: whole 128-bit stores per lane)
+                        for (uint32_t i = lane; i < size / 4; i += 32)
+                            reinterpret_cast<uint4*>(tab)[i] =
+                                make_uint4(kInvalidNode, kInvalidNode, kInvalidNode, kInvalidNode);
                         __syncwarp();
                     }
 #pragma unroll
