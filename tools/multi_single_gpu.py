@@ -24,7 +24,8 @@ only = sys.argv[4] if len(sys.argv) > 4 else ""  # "multi" / "single": run just 
 for label, fn in (
         ("single", lambda: hostapi.interdict(g, p_of, 0, k, 0.1, 1.0 / g.n, seed=42, max_attempts=10**15)),
         (f"multi_{ranks}x_cuda0", lambda: hostapi.interdict_devices(g, p_of, 0, k, 0.1, 1.0 / g.n, [0] * ranks,
-                                                                    seed=42, max_attempts=10**15))):
+                                                                    seed=42, max_attempts=10**15,
+                                                                    with_timing=True))):
     if only and not label.startswith(only):
         continue
     runs = []
