@@ -488,6 +488,7 @@ public:
         GreedyResult picked;
         CheckResult verdict;
         std::uint32_t t = 0;
+        bool bound_can_skip = true;
         auto since = [](Clock::time_point a) { return std::chrono::duration<double>(Clock::now() - a).count(); };
         for (;;) {
             ++t;
@@ -495,12 +496,13 @@ public:
             auto ts = Clock::now();
             ensure(2 * size);
             res.sample_s += since(ts);
-            if (static_cast<double>(size) < sched.n_max) {  // same skips as the single-device loop
+            if (bound_can_skip && static_cast<double>(size) < sched.n_max) {  // same skips as the single-device loop
                 if (static_cast<double>(size) < sched.lambda1) continue;
                 ts = Clock::now();
                 const auto bound = static_cast<double>(coverage_upper_bound(k, kind, size, size, cand, limit));
                 res.check_s += since(ts);
                 if (bound < sched.lambda1) continue;
+                bound_can_skip = false;  // reached once: later (larger) R' will reach it too
             }
             ts = Clock::now();
             picked = greedy(k, kind, size, cand, limit);

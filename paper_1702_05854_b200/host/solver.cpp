@@ -112,6 +112,7 @@ InterdictionResult run_on_device(const DeviceGraph& dg, const ProbGraph& g,
     std::uint32_t t = 0;
     const char* skip_env = std::getenv("HSAW_SKIP_BOUND");
     const bool skip_by_bound = !(skip_env && std::atoi(skip_env) == 0);
+    bool bound_can_skip = true;
     for (;;) {  // interdiction.cpp:36-47
         ++t;
         size = base << (t - 1);
@@ -126,7 +127,7 @@ InterdictionResult run_on_device(const DeviceGraph& dg, const ProbGraph& g,
         // last iteration N_max allows — the iteration cannot pass whatever greedy picks: skip its
         // greedy run and coverage counts. Only the final iteration's solution is ever reported
         // (interdiction.cpp:49-61), so the result is unchanged. HSAW_SKIP_BOUND=0 disables.
-        if (skip_by_bound && static_cast<double>(size) < sched.n_max) {
+        if (skip_by_bound && bound_can_skip && static_cast<double>(size) < sched.n_max) {
             // Cov_R'(S) <= |R'_t| = size for every S: while size < Lambda_1 (always the case at
             // t = 1, where size = ceil(Lambda) and Lambda_1 = 1 + (1 + eps) Lambda) no histogram
             // is needed to know the answer
@@ -135,6 +136,12 @@ InterdictionResult run_on_device(const DeviceGraph& dg, const ProbGraph& g,
             const auto bound = static_cast<double>(out_of_sample.coverage_upper_bound(k));
             res.check_s += seconds_since(ts);
             if (bound < sched.lambda1) continue;
+            // The k largest counts of R'_t grow with its size (each R' is a fresh sample twice as
+            // large) while Lambda_1 is fixed: once the bound has reached it, later iterations
+            // will not be skipped either, and computing their bound only costs a histogram of
+            // R'_t - half of all walk items in the final iteration, whose R' is never needed
+            // again if the check passes. (Purely a cost decision: a bound is never required.)
+            bound_can_skip = false;
         }
         ts = Clock::now();
         picked = greedy_max_cover(in_sample, k);

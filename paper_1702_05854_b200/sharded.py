@@ -518,16 +518,20 @@ class ShardedSolver:
         sched = hostapi.schedule(limit, k, eps, delta)
         lam = sched["lambda_samples"]
         t = 0
+        bound_can_skip = True
         while True:
             t += 1
             size = lam << (t - 1)
             self.ensure(2 * size)
             # an iteration whose R'_t cannot reach Lambda_1 with any k candidates cannot pass the
-            # check (coverage.cpp:216-217): skip its greedy run unless N_max ends the loop here
-            if float(size) < sched["n_max"] and (
-                    float(size) < sched["lambda1"]  # Cov_R'(S) <= |R'_t| = size
-                    or self.coverage_upper_bound(k, kind, size, size, cand) < sched["lambda1"]):
-                continue
+            # check (coverage.cpp:216-217): skip its greedy run unless N_max ends the loop here.
+            # Once a bound has reached Lambda_1 the later, larger R' will too: no more bounds.
+            if bound_can_skip and float(size) < sched["n_max"]:
+                if float(size) < sched["lambda1"]:  # Cov_R'(S) <= |R'_t| = size
+                    continue
+                if self.coverage_upper_bound(k, kind, size, size, cand) < sched["lambda1"]:
+                    continue
+                bound_can_skip = False
             solution, coverage = self.greedy(k, kind, size, cand)
             cov_r = self.coverage_of(solution, kind, 0, size, cand)
             cov_rp = self.coverage_of(solution, kind, size, size, cand)
