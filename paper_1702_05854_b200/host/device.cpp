@@ -303,6 +303,17 @@ ProbGraph load_edge_list_device(const std::string& path, WeightMode mode, std::u
 
 ProbGraph load_cache_device(const std::string& path, int device) {
     MappedCache file(path);
+    if (file.n == 0) {
+        // the reference accepts an empty cache (load_cache reads the single offset, sums no rows,
+        // validate() passes iff that offset is 0 and m is 0, proj/src/graph.cpp:76-77); nothing
+        // for a device to do
+        std::uint64_t first = 0;
+        std::memcpy(&first, file.body, 8);
+        if (first != 0 || file.m != 0) throw DataError("graph: offsets do not cover edge range");
+        ProbGraph empty;
+        empty.in_offsets.assign(1, 0);
+        return empty;
+    }
     hsaw_gpu_ctx* ctx = nullptr;
     if (hsaw_gpu_ctx_create(device, nullptr, &ctx) != HSAW_OK)
         throw DeviceError("no usable CUDA device: the HSAW path has no CPU fallback");

@@ -145,6 +145,22 @@ def test_cache_and_edge_list_round_trip(host, tmp_path):  # test_graph.cpp:211-2
     assert e.value.status == 2
 
 
+def test_empty_cache_is_accepted_like_the_reference(host, tmp_path):
+    """An HSAW1 cache with n = 0, m = 0 passes the reference's load_cache + validate()
+    (proj/src/graph.cpp:76-77, 398-430): both loaders return the empty graph; a non-zero single
+    offset or m > 0 is the reference's coverage error. Needs no device."""
+    import struct
+    (tmp_path / "empty.cache").write_bytes(b"HSAW1" + struct.pack("<QQQ", 0, 0, 0))
+    for loader in (host.Graph.load_cache, host.Graph.load_cache_device):
+        g = loader(tmp_path / "empty.cache")
+        assert (g.n, g.m) == (0, 0)
+    (tmp_path / "off.cache").write_bytes(b"HSAW1" + struct.pack("<QQQ", 0, 0, 7))
+    for loader in (host.Graph.load_cache, host.Graph.load_cache_device):
+        with pytest.raises(host.HsawError) as e:
+            loader(tmp_path / "off.cache")
+        assert e.value.status == 2 and "offsets do not cover edge range" in str(e.value)
+
+
 def test_schedule_and_check(host, golden):
     s = host.schedule(100, 2, 0.1, 0.1)  # proj/tests/test_coverage.cpp:162-175
     assert (s["t_max"], s["lambda_samples"]) == (10, 1179)
