@@ -80,7 +80,8 @@ def build_gpu(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=4) as ex:
         objs = list(ex.map(compile_one, cus))
     objs += [compile_cpp(c) for c in cpps]
-    subprocess.check_call([NVCC, "-shared", "-ccbin", CXX, "-o", GPU_SO, *objs, "-lcudart"])
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-ccbin", CXX,
+                           "-o", GPU_SO, *objs, "-lcudart"])
     return GPU_SO
 
 
