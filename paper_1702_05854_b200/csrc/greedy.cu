@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <cstdio>
 #include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -377,6 +378,10 @@ __global__ void __launch_bounds__(256) dense_emit(const uint32_t* __restrict__ c
     }
 }
 
+// (Measured and dropped: the filter copied to shared memory - 64 KB copies changed nothing, 128 KB
+// ones leave one block per SM: 42 -> 51 ms per C4 solve - and 128-bit item loads with one vote per
+// four items: 42 -> 55 ms. At the largest R_t the pass runs at 1.9 TB/s with 67 % of the issue
+// slots busy: per-item filter arithmetic, not memory.)
 // The walks' indexed items as (walk, new name) pairs: a flat, coalesced pass over the item range
 // (the walk structure does not matter to a membership test); only for the few items that pass the
 // filter and the map is the owning walk looked up (binary search over the extents) and the pair
@@ -1476,6 +1481,14 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                 x_ids.ensure_scratch(D + 1);
                 x_cnt.ensure_scratch(D + 4);
                 const uint64_t P = occ;  // every occurrence of an indexed item becomes one pair
+                if (const char* env = std::getenv("HSAW_GREEDY_DEBUG"))
+                    if (std::atoi(env))
+                        std::fprintf(stderr,
+                                     "[hsaw greedy] walks %llu items %llu k %u: threshold %u (%u %% of "
+                                     "c_k) -> D %llu ids, %llu pairs, filter 2^%u words\n",
+                                     (unsigned long long)cnt, (unsigned long long)(p1 - p0), k,
+                                     min_count, ck_percent, (unsigned long long)D,
+                                     (unsigned long long)P, log2w);
                 x_pw.ensure_scratch(P + 2);
                 x_pr.ensure_scratch(P + 2);
                 x_sw.ensure_scratch(P + 2);
