@@ -179,6 +179,9 @@ int hsaw_gpu_graph_layout(const hsaw_gpu_ctx* ctx);
  * the device after host threads verified, bit for bit, that every row holds the sequential
  * 1/in-degree sums of WeightMode::InDegree (proj/src/graph.cpp:172-178). Diagnostic. */
 int hsaw_gpu_graph_upload_mode(const hsaw_gpu_ctx* ctx);
+/* Bytes the last hsaw_gpu_graph_upload copied host -> device (the regenerated part of in_cum is
+ * the difference to 8 (n + 1) + 12 m + 8 n). */
+uint64_t hsaw_gpu_graph_upload_bytes(const hsaw_gpu_ctx* ctx);
 
 /* ---- sampler: encode / decode (kernels K1, K2) ---------------------------------------------- */
 

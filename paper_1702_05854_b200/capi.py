@@ -91,6 +91,8 @@ def lib() -> C.CDLL:
     L.hsaw_gpu_graph_bytes.restype = C.c_uint64
     L.hsaw_gpu_graph_layout.argtypes = [vp]
     L.hsaw_gpu_graph_upload_mode.argtypes = [vp]
+    L.hsaw_gpu_graph_upload_bytes.argtypes = [vp]
+    L.hsaw_gpu_graph_upload_bytes.restype = C.c_uint64
     L.hsaw_gpu_launch_count.argtypes = [vp]
     L.hsaw_gpu_launch_count.restype = C.c_uint64
     L.hsaw_gpu_stage_times.argtypes = [vp, f64p, u64p, C.c_int]
@@ -176,7 +178,7 @@ EXPORTS = (
     "hsaw_gpu_edge_text_parse", "hsaw_gpu_edge_text_fetch", "hsaw_gpu_edge_text_free",
     "hsaw_gpu_edge_text_install",
     "hsaw_gpu_rmat_build", "hsaw_gpu_held_csr_fetch", "hsaw_gpu_held_csr_install",
-    "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout", "hsaw_gpu_graph_upload_mode",
+    "hsaw_gpu_held_csr_drop", "hsaw_gpu_graph_layout", "hsaw_gpu_graph_upload_mode", "hsaw_gpu_graph_upload_bytes",
     "hsaw_gpu_stream_keep",
     "hsaw_gpu_stream_restrict", "hsaw_gpu_stream_crossings",
     "hsaw_gpu_rr_node_sets", "hsaw_gpu_walkset_export",
@@ -316,6 +318,10 @@ class Context:
     @property
     def upload_mode(self) -> str:
         return "regenerated" if int(self.L.hsaw_gpu_graph_upload_mode(self.h)) == 1 else "copied"
+
+    @property
+    def upload_bytes(self) -> int:
+        return int(self.L.hsaw_gpu_graph_upload_bytes(self.h))
 
     def upload_graph(self, n, m, in_offsets, in_src, in_cum, p_of):
         in_offsets = np.ascontiguousarray(in_offsets, dtype=np.uint64)

@@ -539,7 +539,8 @@ struct hsaw_gpu_ctx {
     bool own_stream = false;
     hsawgpu::DeviceGraph g;
     uint64_t graph_bytes = 0;
-    int upload_mode = 0;  // in_cum of the last graph_upload: 0 copied, 1 regenerated on the device
+    int upload_mode = 0;  // in_cum of the last graph_upload: 0 copied, 1 (partly) regenerated on the device
+    uint64_t upload_bytes = 0;  // bytes the last graph_upload copied host -> device
     // side stream for work that may run beside the context stream (the replay of walks that
     // outgrew their log chunk, sampler.cu launch_decode_pairs / join_side_stream)
     cudaStream_t side = nullptr;

@@ -481,6 +481,8 @@ def test_upload_regenerates_indegree_sums(ctx, port, monkeypatch, weights):
     csr = Csr(g.n, g.m, g.in_offsets, g.in_src, cum, g.p_of)
     upload(ctx, csr)
     assert ctx.upload_mode == ("regenerated" if weights == "indegree" else "copied")
+    full = 8 * (g.n + 1) + 12 * g.m + 8 * g.n
+    assert ctx.upload_bytes == (full - 8 * g.m if weights == "indegree" else full)
     with ctx.stream(seed=6) as st:
         st.ensure(2000)
         got = st.to_pool(2000)
