@@ -757,7 +757,7 @@ def run_b200(args):
     if not args.no_e2e and have_host:
         target = max(1, int(accepted / max(args.steps, 1)))
         e2e_acc, e2e_s = 0, 0.0
-        e2e_calls = max(1, min(args.steps, 5 if g.m < (1 << 28) else 3))
+        e2e_calls = max(1, min(args.steps, 5))
         e2e_error = None
         # the caller's own objects, built once: ProbGraph (g) and SuspectSet (vi), the two arguments
         # of hsaw::DeviceGraph(g, vi) / stream_samples(g, vi, ...) in the reference's API
