@@ -1477,6 +1477,17 @@ int hsaw_gpu_greedy(hsaw_gpu_ctx* ctx, const hsaw_gpu_stream* stream,
                     exclusive_sum_u32(ctx, x_pc.p, x_base.p, words + 1);
                 }
                 const uint64_t D = read_u32(ctx, x_base.p + words);
+                if (D == 0) {
+                    // nothing at or above the threshold (the mass rule can land one above a flat
+                    // distribution's only count): the full-id form would report an unindexed
+                    // winner at once; with threshold 1 there is simply nothing to select
+                    if (min_count > 1) {
+                        failed_thresholds.push_back(min_count);
+                        return false;
+                    }
+                    done = 0;
+                    return true;
+                }
                 x_map.ensure_scratch(words + 1);
                 x_ids.ensure_scratch(D + 1);
                 x_cnt.ensure_scratch(D + 4);

@@ -168,6 +168,21 @@ def test_thresholded_index_falls_back_to_full(ctx, port):
     assert cov == exp_cov and sol.tolist() == exp_sol.tolist()
 
 
+def test_flat_counts_above_the_mass_rule(ctx, port):
+    """Every item occurs equally often: the 1/8-mass rule lands one above the only count there is,
+    so nothing is indexed at the first threshold (an empty dense instance / an unindexed first
+    winner) and the run must step down to the full index."""
+    limit, reps = 300_000, 4
+    items = np.tile(np.arange(limit, dtype=np.uint32), reps)  # > 2^20 occurrences, all counts = 4
+    off = np.arange(0, items.size + 1, 3, dtype=np.uint64)
+    if off[-1] != items.size:
+        off = np.append(off, np.uint64(items.size))
+    exp_sol, exp_cov = port.greedy(limit, off, items, 50)
+    with ctx.walkset(limit, off, items) as ws:
+        sol, cov = ctx.greedy(50, walkset=ws)
+    assert cov == exp_cov and sol.tolist() == exp_sol.tolist()
+
+
 def test_partitioned_histogram_large_id_space(ctx, port):
     """Id spaces whose counters do not fit L2 take the radix-partitioned histogram path."""
     rng = np.random.Generator(np.random.PCG64(9))
