@@ -131,10 +131,13 @@ void decode_on_device(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const void* bod
     HSAW_CUDA_CHECK(cudaMemcpyAsync(&ends[0], c.off.p, 8, cudaMemcpyDeviceToHost, st));
     HSAW_CUDA_CHECK(cudaMemcpyAsync(&ends[1], c.off.p + n, 8, cudaMemcpyDeviceToHost, st));
     HSAW_CUDA_CHECK(cudaStreamSynchronize(st));
-    // the loader's own guard (host load_cache: rows must be usable before they are summed) ...
-    if (err[0] != kNoRow) fail(HSAW_EDATA, "graph: offsets not monotone");
-    // ... then validate(), graph.cpp:76-103
+    // validate()'s order (graph.cpp:76-103): coverage of the edge range first, then the rows in
+    // ascending order, where a row whose offsets run backwards (or past m: the reference's loader
+    // would have read out of bounds there) is "not monotone" and any other defect is replayed on
+    // the host to get the reference's wording - whichever row comes first
     if (ends[0] != 0 || ends[1] != m) fail(HSAW_EDATA, "graph: offsets do not cover edge range");
+    if (err[0] != kNoRow && (err[1] == kNoRow || err[0] <= err[1]))
+        fail(HSAW_EDATA, "graph: offsets not monotone");
     if (err[1] != kNoRow) {
         const uint32_t v = err[1];
         uint64_t lohi[2];
