@@ -955,7 +955,9 @@ __global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
                 // in which some node finds both bits set (a true repeat, or chance) go through
                 // the exact hash set below.
                 bool exact_needed = true;
-                if (kBitmapProof && (uint64_t)nn * nn <= 64ull * TABLE) {
+                // (worth it while false alarms stay rare: with two bits per node about
+                // nn^3 / (3 * (16 TABLE)^2) of the walks, 8 % at 400 nodes in the main pass)
+                if (kBitmapProof && (uint64_t)nn * nn * nn <= 24ull * TABLE * TABLE * 16 / 6) {
                     constexpr uint32_t kMapBits = 5 + (TABLE == 1024 ? 10 : TABLE == 4096 ? 12 : 0);
                     static_assert(TABLE == 1024 || TABLE == 4096, "bit-map width follows the table size");
                     for (uint32_t i = lane; i < TABLE / 4; i += 32)  // 128-bit stores
