@@ -583,10 +583,9 @@ void pin_in_l2(hsaw_gpu_ctx* ctx, const void* base, size_t bytes) {
         cudaGetLastError();
 }
 
-// Layout choice: the compact arrays while the 16-byte row headers fit in L2 (the
-// header gather then stays an L2 hit even when the sources spill to HBM: measured 10.5 vs 11.0 ms
-// per 2^20 batches at R-MAT scale 22, 13.7 vs 11.0 ms at scale 24), else fat edge records (one HBM
-// line per step) while they fit the TLB's reach, else compact again. HSAW_LAYOUT=compact|fat
+// Layout choice: the compact arrays while the 16-byte row headers fit well inside L2
+// (the header gather then stays an L2 hit even when the sources spill to HBM), else fat edge
+// records (one HBM line per step) while they fit the TLB's reach, else compact again. HSAW_LAYOUT=compact|fat
 // overrides.
 int choose_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
     if (const char* env = std::getenv("HSAW_LAYOUT")) {
@@ -594,7 +593,11 @@ int choose_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m) {
         if (env[0] == 'f') return kLayoutFat;
     }
     const uint64_t l2 = (uint64_t)device_info(ctx->device).l2_bytes;
-    if (16ull * n <= l2) return kLayoutCompact;
+    // (crossover measured at ~3 M nodes once the fat layout lost its stream-wide L2 window: R-MAT
+    // scale 21 compact 177 vs fat 159 M HSAW/s, 3 M nodes 137 vs 137, LiveJournal shape 4.85 M
+    // nodes 138 vs 148, scale 23 134 vs 159 - the headers must fit the share of L2 that one
+    // partition keeps, not all of it)
+    if (16ull * n <= l2 * 3 / 8) return kLayoutCompact;
     // One gather per step beats two only while the edge records stay inside the TLB's reach:
     // dependent random 32-byte gathers run at 36 G/s from tables of up to 64 GB and at 14 / 10 / 9
     // G/s from 96 / 120 / 150 GB, whatever the allocation API (tools/tlb_probe.cu,
