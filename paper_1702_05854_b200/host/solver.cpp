@@ -147,7 +147,19 @@ InterdictionResult run_on_device(const DeviceGraph& dg, const ProbGraph& g,
         picked = greedy_max_cover(in_sample, k);
         res.greedy_s += seconds_since(ts);
         ts = Clock::now();
-        verdict = check_solution(picked.solution, in_sample, out_of_sample, sched, t);
+        // check_solution (coverage.cpp:212-231) with Cov_R(S) taken from the greedy run instead of
+        // a second pass over R_t: the walks of a stream are self-avoiding (K2b), so no item occurs
+        // twice in a walk and the sum of the marginal gains IS the number of walks S covers (the
+        // zero-gain padding covers nothing new). HSAW_RECOUNT_COVERAGE=1 keeps the second pass.
+        const char* recount_env = std::getenv("HSAW_RECOUNT_COVERAGE");  // (read per call: tests)
+        const bool recount = recount_env && std::atoi(recount_env) != 0;
+        if (recount) {
+            verdict = check_solution(picked.solution, in_sample, out_of_sample, sched, t);
+        } else {
+            const auto cov_rp = static_cast<double>(out_of_sample.coverage_of(picked.solution));
+            verdict = check_counts(static_cast<double>(picked.coverage), cov_rp,
+                                   static_cast<double>(out_of_sample.num_samples()), sched, t);
+        }
         res.check_s += seconds_since(ts);
         if (verdict.pass || static_cast<double>(size) >= sched.n_max) break;
     }

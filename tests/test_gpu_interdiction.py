@@ -173,3 +173,18 @@ def test_bound_skip_does_not_change_results(host, synth3000, monkeypatch, kind, 
     monkeypatch.delenv("HSAW_SKIP_BOUND")
     fast = host.interdict(g, synth3000.p_of, kind, k, 0.1, 0.05, seed=5)
     assert full == fast and full["iterations"] >= 2
+
+
+@pytest.mark.parametrize("kind,k", [(0, 20), (1, 10)])
+def test_greedy_coverage_is_the_in_sample_coverage(host, synth3000, monkeypatch, kind, k):
+    """The doubling loop takes Cov_R(S) from the greedy run (the walks of a stream are
+    self-avoiding, so the sum of the marginal gains is the number of walks S covers) instead of a
+    second coverage_of pass over R_t; HSAW_RECOUNT_COVERAGE=1 runs that pass as the reference does
+    (coverage.cpp:212-231). Same InterdictionResult either way."""
+    g = host.Graph.from_csr(synth3000.n, synth3000.m, synth3000.in_offsets, synth3000.in_src,
+                            synth3000.in_cum)
+    monkeypatch.setenv("HSAW_RECOUNT_COVERAGE", "1")
+    recounted = host.interdict(g, synth3000.p_of, kind, k, 0.1, 0.05, seed=5)
+    monkeypatch.delenv("HSAW_RECOUNT_COVERAGE")
+    fast = host.interdict(g, synth3000.p_of, kind, k, 0.1, 0.05, seed=5)
+    assert recounted == fast and fast["iterations"] >= 2
