@@ -802,6 +802,25 @@ def run_b200(args):
         }
         if e2e_error:
             out["e2e"]["error"] = e2e_error
+        else:
+            # the same call at other request sizes (one call each): the upload is a fixed cost per
+            # call, so end-to-end HSAWs/s grows with the request (BASELINE.md plans a sweep over
+            # 10^6..10^8 samples; the largest size is bounded by what the pool may take beside a
+            # second copy of nothing: 8 B per walk item with both item arrays kept)
+            sweep = {}
+            for tgt in (10**6, 10**7, 3 * 10**7):
+                try:
+                    barrier()
+                    t0 = time.perf_counter()
+                    with hostapi.DeviceGraph(g, vi, device=local) as dg2:
+                        _, acc = dg2.sample(tgt, seed=STREAM_SEED + 7, max_attempts=10**15)
+                    torch.cuda.synchronize()
+                    dt = time.perf_counter() - t0
+                    sweep[str(tgt)] = {"hsaw_per_sec": acc / dt, "seconds": dt, "accepted": acc}
+                except Exception as exc:
+                    sweep[str(tgt)] = {"error": str(exc)[:120]}
+                    break
+            out["e2e"]["request_size_sweep"] = sweep
         # host ProbGraph in, InterdictionResult out (context creation, upload and solve inside)
         if r_dev is not None:
             try:
