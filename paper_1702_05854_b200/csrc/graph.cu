@@ -15,6 +15,9 @@
 #include "common.cuh"
 #include "walk.cuh"
 
+namespace hsawgpu {
+void staging_copy(void* dst, const void* src, size_t bytes);  // hostcheck.cpp (non-temporal stores)
+}
 using namespace hsawgpu;
 
 namespace {
@@ -440,7 +443,7 @@ public:
                 for (size_t i = t; i < pieces.size(); i += nthreads, ++turn) {
                     const int slot = t * kSlotsPerThread + (turn % kSlotsPerThread);
                     if (turn >= kSlotsPerThread) cudaEventSynchronize(st.slot_done[slot]);
-                    std::memcpy(st.pinned[slot], pieces[i].src, pieces[i].bytes);
+                    staging_copy(st.pinned[slot], pieces[i].src, pieces[i].bytes);  // hostcheck.cpp
                     cudaError_t e = cudaMemcpyAsync(pieces[i].dst, st.pinned[slot],
                                                     pieces[i].bytes, cudaMemcpyHostToDevice, s);
                     if (e != cudaSuccess) errs[t] = e;

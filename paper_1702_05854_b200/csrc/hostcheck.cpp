@@ -7,6 +7,7 @@
 // the intrinsics stay out of nvcc's front end.
 #include <atomic>
 #include <cstdint>
+#include <cstring>
 #include <thread>
 #include <vector>
 
@@ -91,6 +92,41 @@ uint64_t row_at(const uint64_t* off, uint64_t n, uint64_t e) {
 }
 
 }  // namespace
+
+#if defined(__x86_64__)
+namespace {
+__attribute__((target("avx2"))) void copy_nt_avx2(char* dst, const char* src, size_t bytes) {
+    size_t i = 0;
+    for (; i + 128 <= bytes; i += 128) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 32));
+        const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 64));
+        const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 96));
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), a);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 32), b);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 64), c);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 96), d);
+    }
+    _mm_sfence();
+    if (i < bytes) std::memcpy(dst + i, src + i, bytes - i);
+}
+}  // namespace
+#endif
+
+// Pageable -> pinned staging copy of the upload path. The destination (a pinned ring slot, 32-byte
+// aligned) is only read by the DMA engine afterwards, so it is written with non-temporal stores:
+// no read-for-ownership of the slot's lines, a quarter less host memory traffic per staged byte
+// while the in_cum check competes for the same bandwidth.
+void staging_copy(void* dst, const void* src, size_t bytes) {
+#if defined(__x86_64__)
+    static const bool avx2 = __builtin_cpu_supports("avx2");
+    if (avx2 && (reinterpret_cast<uintptr_t>(dst) & 31u) == 0 && bytes >= 4096) {
+        copy_nt_avx2(static_cast<char*>(dst), static_cast<const char*>(src), bytes);
+        return;
+    }
+#endif
+    std::memcpy(dst, src, bytes);
+}
 
 // off: n + 1 non-decreasing offsets (checked by the caller), cum: off[n] doubles.
 bool rows_are_indegree_sums(uint32_t n, const uint64_t* off, const double* cum, unsigned threads) {
