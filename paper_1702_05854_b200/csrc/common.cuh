@@ -753,7 +753,7 @@ struct CopyJob {
     const void* src;
     size_t bytes;
 };
-void copy_to_device(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs);
+void copy_to_device(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs, size_t piece_bytes = 0);
 void copy_to_host(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs);
 bool prepare_layout(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m);
 // Kernel-side view of DeviceGraph::src (passed by value in the kernel parameter structs).

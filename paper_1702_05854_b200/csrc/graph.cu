@@ -8,16 +8,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
 
 #include "common.cuh"
+#include "hostcheck.h"
 #include "walk.cuh"
 
-namespace hsawgpu {
-void staging_copy(void* dst, const void* src, size_t bytes);  // hostcheck.cpp (non-temporal stores)
-}
 using namespace hsawgpu;
 
 namespace {
@@ -411,8 +410,12 @@ public:
     // Copies all jobs; returns false (nothing copied) when the ring cannot be set up.
     // to_device: pageable host -> device; otherwise device -> pageable host (the call returns
     // once the host arrays are complete).
+    // piece_bytes (0 = a whole ring slot): smaller pieces keep the part of the ring in use inside
+    // the last-level cache, which pays when other host threads stream through memory at the same
+    // time (the in_cum check of graph_upload: 2 MB pieces 250 ms per call, 4 MB 295 ms; alone,
+    // 4 MB pieces copy faster: 51 vs 43 GB/s)
     static bool run(int device, cudaStream_t consumer, const std::vector<Job>& jobs,
-                    bool to_device = true) {
+                    bool to_device = true, size_t piece_bytes = 0) {
         static std::mutex mu;  // one staged copy at a time per process
         std::lock_guard<std::mutex> lock(mu);
         State& st = state(device);
@@ -422,7 +425,7 @@ public:
             const char* src;
             size_t bytes;
         };
-        const size_t kChunk = chunk_bytes();
+        const size_t kChunk = piece_bytes && piece_bytes < chunk_bytes() ? piece_bytes : chunk_bytes();
         const int kSlotsPerThread = slots_per_thread();
         std::vector<Piece> pieces;
         for (const Job& j : jobs)
@@ -732,10 +735,11 @@ namespace hsawgpu {
 
 // Large transfers: multi-threaded staging through pinned memory; small ones (and the fallback when
 // the ring cannot be set up) go through plain pageable copies on the context stream.
-void copy_to_device(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs) {
+void copy_to_device(hsaw_gpu_ctx* ctx, const std::vector<CopyJob>& jobs, size_t piece_bytes) {
     uint64_t total = 0;
     for (const auto& j : jobs) total += j.bytes;
-    if (total >= (16u << 20) && StagedCopier::run(ctx->device, ctx->stream, jobs, true)) return;
+    if (total >= (16u << 20) && StagedCopier::run(ctx->device, ctx->stream, jobs, true, piece_bytes))
+        return;
     for (const auto& j : jobs)
         HSAW_CUDA_CHECK(
             cudaMemcpyAsync(j.dst, j.src, j.bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -803,10 +807,6 @@ __global__ void indegree_row_cum(uint32_t n, const uint64_t* __restrict__ off,
         in_cum[i] = cum;
     }
 }
-
-// hostcheck.cpp: do the host's cumulative weights equal, bit for bit, what indegree_row_cum
-// produces? Runs on host threads beside the copier threads.
-bool rows_are_indegree_sums(uint32_t n, const uint64_t* off, const double* cum, unsigned threads);
 
 // Re-lays a device-resident CSR (the reference's arrays) out into the walk kernels' records.
 // Synchronises; throws HSAW_EDATA on bad rows.
@@ -1060,12 +1060,15 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             bool try_regen = m >= (1u << 23) && hw >= 12;  // (C2, 16 M edges: 16.3 -> 14.7 ms per call)
             if (const char* env = std::getenv("HSAW_UPLOAD_REGEN")) {
                 const int v = std::atoi(env);
-                try_regen = v == 2 ? m > 0 : (v != 0 && try_regen);  // 2 forces the attempt (tests)
+                try_regen = v >= 2 ? m > 0 : (v != 0 && try_regen);  // 2, 3 force the attempt (tests)
             }
-            // (Sharing in_cum between the check and the wire - the rows holding the first 78 % of
-            // the edges checked and regenerated, the rest copied meanwhile - was measured: 223 ms
-            // against 226 ms. Both sides draw on the same host memory bandwidth; the whole array
-            // goes through the check.)
+            // The check and the wire share in_cum through one work list (RowCheck, hostcheck.cpp):
+            // the check workers verify chunks from the front while the other arrays are copied;
+            // when those are through, this thread copies chunks from the back until the two meet.
+            // On an idle 16-core box the workers get through nearly all of it; when the host cores
+            // are busy the link takes the tail, so the call never falls behind the plain copy by
+            // more than the small part verified in vain. (A fixed split and a rate threshold were
+            // both tried: the first cannot know the box's state, the second misfires on start-up.)
             std::vector<CopyJob> first, rest;
             first.push_back({d_off, in_offsets, ((uint64_t)n + 1) * 8});
             if (m) rest.push_back({d_src, in_src, (uint64_t)m * 4});
@@ -1075,23 +1078,29 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
             for (const CopyJob& j : first) sent += j.bytes;
             for (const CopyJob& j : rest) sent += j.bytes;
             lap("alloc");
-            bool regen_ok = false;
+            uint64_t chunk_edges = 1u << 21;  // 16 MB of in_cum per chunk
+            if (const char* env = std::getenv("HSAW_UPLOAD_CHUNK_EDGES"))  // tests: many small chunks
+                chunk_edges = (uint64_t)std::max(1ll, std::atoll(env));
+            std::unique_ptr<RowCheck> check;
             std::thread checker;
-            if (try_regen)
+            if (try_regen) {
+                check.reset(new RowCheck(n, in_offsets, in_cum, chunk_edges));
                 checker = std::thread([&] {
                     // beside the 8 copier threads (B200 box, 16 cores: 8 / 12 / 16 workers ->
                     // 258 / 226 / 226 ms for 11.7 GB, against 230 ms more on the wire)
                     unsigned workers = hw >= 16 ? 12u : 4u;
                     if (const char* env = std::getenv("HSAW_UPLOAD_CHECK_THREADS"))
                         workers = (unsigned)std::max(1, std::atoi(env));
-                    regen_ok = rows_are_indegree_sums(n, in_offsets, in_cum, workers);
+                    check->run(workers);
                 });
+            }
+            uint64_t copied_edges = 0;
             try {
                 copy_to_device(ctx, first);
                 if (try_regen) {
-                    // the sums are regenerated speculatively on the side stream as soon as the
-                    // offsets are there, beside the remaining copies (13 ms at the Twitter
-                    // shape); if the check fails the plain copy below simply overwrites them
+                    // the sums are regenerated on the side stream as soon as the offsets are
+                    // there, beside the remaining copies (13 ms at the Twitter shape); chunks that
+                    // are copied instead, or everything if the check fails, overwrite them
                     if (!ctx->side) {
                         HSAW_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
                         HSAW_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->side_go, cudaEventDisableTiming));
@@ -1103,24 +1112,43 @@ int hsaw_gpu_graph_upload(hsaw_gpu_ctx* ctx, uint32_t n, uint32_t m, const uint6
                     check_launch(ctx, "indegree_row_cum");
                     HSAW_CUDA_CHECK(cudaEventRecord(ctx->side_done, ctx->side));
                 }
-                copy_to_device(ctx, rest);
+                const size_t piece = try_regen ? (size_t)(2u << 20) : 0;
+                copy_to_device(ctx, rest, piece);
+                if (try_regen) {
+                    HSAW_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->side_done, 0));  // join the side stream
+                    lap("copy");
+                    // HSAW_UPLOAD_REGEN=2 (tests): the whole array goes through the check (3: shared)
+                    const char* env = std::getenv("HSAW_UPLOAD_REGEN");
+                    const bool share = !(env && std::atoi(env) == 2);
+                    uint64_t e0 = 0, e1 = 0;
+                    while (share && !check->differs() && check->claim_back(16, &e0, &e1)) {
+                        if (e1 == e0) continue;
+                        copy_to_device(ctx, {CopyJob{d_cum + e0, in_cum + e0, (e1 - e0) * 8}}, piece);
+                        copied_edges += e1 - e0;
+                    }
+                }
             } catch (...) {
                 if (checker.joinable()) checker.join();
                 throw;
             }
             if (checker.joinable()) checker.join();
+            bool regen_ok = false;
             if (try_regen) {
-                HSAW_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->side_done, 0));  // join the side stream
+                lap("check+tail");
+                regen_ok = !check->differs();
                 if (!regen_ok && m) {
                     copy_to_device(ctx, {CopyJob{d_cum, in_cum, (uint64_t)m * 8}});
-                    sent += (uint64_t)m * 8;
+                    copied_edges = m;
+                    lap("cum");
                 }
+                sent += copied_edges * 8;
+            } else {
+                lap("copy");
             }
-            ctx->upload_mode = try_regen && regen_ok && m ? 1 : 0;
-            ctx->upload_bytes = sent;
-            lap(try_regen ? (regen_ok ? "copy+regen" : "copy+cum") : "copy");
             install_graph(ctx, n, m, d_off, d_src, d_cum, d_p);
             lap("install");
+            ctx->upload_mode = try_regen && regen_ok && copied_edges < m ? 1 : 0;
+            ctx->upload_bytes = sent;
         } catch (...) {
             cleanup();
             free_graph(ctx);

@@ -5,11 +5,16 @@
 // the same thing by induction and has no dependent chain, so the scan runs at memory speed:
 // AVX2 where the CPU has it (4 doubles per compare), scalar otherwise. Plain g++ translation unit:
 // the intrinsics stay out of nvcc's front end.
+#include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
+
+#include "hostcheck.h"
 
 #if defined(__x86_64__)
 #include <immintrin.h>
@@ -113,13 +118,19 @@ __attribute__((target("avx2"))) void copy_nt_avx2(char* dst, const char* src, si
 }  // namespace
 #endif
 
-// Pageable -> pinned staging copy of the upload path. The destination (a pinned ring slot, 32-byte
-// aligned) is only read by the DMA engine afterwards, so it is written with non-temporal stores:
-// no read-for-ownership of the slot's lines, a quarter less host memory traffic per staged byte
-// while the in_cum check competes for the same bandwidth.
+// Pageable -> pinned staging copy of the upload path: memcpy, or (A/B knob) non-temporal stores,
+// which save the read-for-ownership of the slot's lines but bypass the cache the DMA could read
+// the slot from.
 void staging_copy(void* dst, const void* src, size_t bytes) {
 #if defined(__x86_64__)
-    static const bool avx2 = __builtin_cpu_supports("avx2");
+    static const bool avx2 = [] {
+        // HSAW_UPLOAD_NT=1 turns the non-temporal form on. Measured beside the in_cum check at
+        // the Twitter shape (ms per upload call, 2 / 4 MB ring slots): plain memcpy 253 / 295,
+        // non-temporal 276 / 283 - with 2 MB slots the ring stays in the last-level cache and
+        // the DMA reads it from there, which the cache-bypassing stores defeat. Off by default.
+        const char* env = std::getenv("HSAW_UPLOAD_NT");
+        return env && std::atoi(env) != 0 && __builtin_cpu_supports("avx2");
+    }();
     if (avx2 && (reinterpret_cast<uintptr_t>(dst) & 31u) == 0 && bytes >= 4096) {
         copy_nt_avx2(static_cast<char*>(dst), static_cast<const char*>(src), bytes);
         return;
@@ -129,31 +140,81 @@ void staging_copy(void* dst, const void* src, size_t bytes) {
 }
 
 // off: n + 1 non-decreasing offsets (checked by the caller), cum: off[n] doubles.
-bool rows_are_indegree_sums(uint32_t n, const uint64_t* off, const double* cum, unsigned threads) {
-    if (threads == 0) threads = 1;
+//
+// The array is cut into row-aligned chunks of ~edges_per_chunk elements on one work list with two
+// ends: check workers claim chunks from the front, the uploader - once the other arrays are on
+// the wire - claims runs of chunks from the back and simply copies them. So the split between
+// "verified, regenerated on the device" and "copied" follows whatever the host cores and the link
+// manage at that moment (an idle 16-core box verifies everything beside the other copies; a busy
+// one leaves the tail to PCIe), and no rate has to be guessed in advance.
+RowCheck::RowCheck(uint32_t n, const uint64_t* off, const double* cum, uint64_t edges_per_chunk)
+    : n_(n), off_(off), cum_(cum) {
     const uint64_t m = off[n];
-    std::atomic<bool> stop{false};
+    const uint64_t per = std::max<uint64_t>(edges_per_chunk, 1);
+    const uint64_t chunks = std::max<uint64_t>(1, std::min<uint64_t>((m + per - 1) / per, 1u << 20));
+    rows_.resize(chunks + 1);
+    for (uint64_t c = 0; c < chunks; ++c) rows_[c] = c == 0 ? 0 : row_at(off, n, m / chunks * c);
+    rows_[chunks] = n;
+    ends_.store(chunks);  // front 0 (high half), back = chunks (low half)
 #if defined(__x86_64__)
-    const bool avx2 = __builtin_cpu_supports("avx2");
-#else
-    const bool avx2 = false;
+    avx2_ = __builtin_cpu_supports("avx2");
 #endif
-    auto scan = [&](unsigned t) {  // rows split by edge position: equal bytes per worker
-        const uint64_t va = row_at(off, n, m / threads * t);
-        const uint64_t vb = t + 1 == threads ? n : row_at(off, n, m / threads * (t + 1));
-        uint64_t bad;
+}
+
+bool RowCheck::claim_front(uint64_t* c) {
+    uint64_t e = ends_.load(std::memory_order_relaxed);
+    for (;;) {
+        const uint64_t front = e >> 32, back = e & 0xFFFFFFFFu;
+        if (front >= back) return false;
+        if (ends_.compare_exchange_weak(e, ((front + 1) << 32) | back, std::memory_order_acq_rel)) {
+            *c = front;
+            return true;
+        }
+    }
+}
+
+bool RowCheck::claim_back(uint32_t max_chunks, uint64_t* e0, uint64_t* e1) {
+    uint64_t e = ends_.load(std::memory_order_relaxed);
+    for (;;) {
+        const uint64_t front = e >> 32, back = e & 0xFFFFFFFFu;
+        if (front >= back || max_chunks == 0) return false;
+        // near the end leave the workers something to do: at most half of what is left
+        const uint64_t take = std::max<uint64_t>(1, std::min<uint64_t>(max_chunks, (back - front + 1) / 2));
+        if (ends_.compare_exchange_weak(e, (front << 32) | (back - take), std::memory_order_acq_rel)) {
+            *e0 = off_[rows_[back - take]];
+            *e1 = off_[rows_[back]];
+            return true;
+        }
+    }
+}
+
+void RowCheck::work() {
+    uint64_t c;
+    while (!differs_.load(std::memory_order_relaxed) && claim_front(&c)) {
+        const uint64_t va = rows_[c], vb = rows_[c + 1];
 #if defined(__x86_64__)
-        bad = avx2 ? rows_avx2(off, cum, va, vb, stop) : rows_plain(off, cum, va, vb, stop);
+        const uint64_t bad = avx2_ ? rows_avx2(off_, cum_, va, vb, differs_)
+                                   : rows_plain(off_, cum_, va, vb, differs_);
 #else
-        bad = rows_plain(off, cum, va, vb, stop);
+        const uint64_t bad = rows_plain(off_, cum_, va, vb, differs_);
 #endif
-        if (bad) stop.store(true, std::memory_order_relaxed);
-    };
+        if (bad) differs_.store(true, std::memory_order_relaxed);
+        checked_.fetch_add(off_[vb] - off_[va], std::memory_order_relaxed);
+    }
+}
+
+void RowCheck::run(unsigned threads) {
     std::vector<std::thread> pool;
-    for (unsigned t = 1; t < threads; ++t) pool.emplace_back(scan, t);
-    scan(0);
+    for (unsigned t = 1; t < threads; ++t) pool.emplace_back([this] { work(); });
+    work();
     for (auto& th : pool) th.join();
-    return !stop.load();
+}
+
+// The whole array through the check (tests, tools).
+bool rows_are_indegree_sums(uint32_t n, const uint64_t* off, const double* cum, unsigned threads) {
+    RowCheck check(n, off, cum, 1u << 21);
+    check.run(threads ? threads : 1);
+    return !check.differs();
 }
 
 }  // namespace hsawgpu

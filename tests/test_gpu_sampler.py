@@ -491,6 +491,41 @@ def test_upload_regenerates_indegree_sums(ctx, port, monkeypatch, weights):
     assert np.array_equal(got.nodes, exp.nodes) and np.array_equal(got.edges, exp.edges)
 
 
+@pytest.mark.parametrize("weights", ["indegree", "one-bit-off"])
+def test_upload_shares_indegree_sums_between_check_and_wire(ctx, port, monkeypatch, weights):
+    """The check and the link work through in_cum from both ends (RowCheck, csrc/hostcheck.cpp): with
+    many small chunks and one check thread some chunks are verified and regenerated, the others
+    copied, wherever the two meet. Whatever the split, the device holds the host's exact sums -
+    same pool as the oracle - and the bytes sent say how much went over the wire; a differing bit
+    anywhere sends everything."""
+    from oracle.oracle import Csr
+    from paper_1702_05854_b200 import rmat
+    monkeypatch.setenv("HSAW_UPLOAD_REGEN", "3")
+    monkeypatch.setenv("HSAW_UPLOAD_CHUNK_EDGES", "512")
+    monkeypatch.setenv("HSAW_UPLOAD_CHECK_THREADS", "1")
+    g = rmat.rmat_graph(14, 10, seed=9, suspect_frac=0.02)
+    cum = g.in_cum.copy()
+    if weights == "one-bit-off":
+        pos = int(g.m) - 2  # in the part the link would take
+        cum[pos] = np.nextafter(cum[pos], 0.0) if cum[pos] > cum[pos - 1] else cum[pos]
+        if cum[pos] == g.in_cum[pos]:
+            pos = int(g.in_offsets[int(np.argmax(np.diff(g.in_offsets.astype(np.int64))))]) + 1
+            cum[pos] = np.nextafter(cum[pos], 2.0)
+    csr = Csr(g.n, g.m, g.in_offsets, g.in_src, cum, g.p_of)
+    upload(ctx, csr)
+    base = 8 * (g.n + 1) + 4 * g.m + 8 * g.n
+    if weights == "indegree":
+        assert base <= ctx.upload_bytes <= base + 8 * g.m
+        assert (ctx.upload_bytes - base) % 8 == 0
+        assert ctx.upload_mode == ("regenerated" if ctx.upload_bytes < base + 8 * g.m else "copied")
+    with ctx.stream(seed=6) as st:
+        st.ensure(2000)
+        got = st.to_pool(2000)
+    exp = port.stream_samples(csr, 2000, seed=6)
+    assert got.attempts == exp.attempts and got.nsamples == exp.nsamples
+    assert np.array_equal(got.nodes, exp.nodes) and np.array_equal(got.edges, exp.edges)
+
+
 def test_stream_keeping_one_item_array(ctx, gpu_lib, synth3000, port):
     """hsaw_gpu_stream_keep: a pool that keeps only the edge ids (or only the nodes) has the same
     order and counters, serves greedy / coverage of its own kind bit-exactly, and refuses the other."""
