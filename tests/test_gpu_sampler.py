@@ -396,6 +396,25 @@ def test_upload_rejects_bad_graphs(ctx, gpu_lib):
     assert e.value.status == gpu_lib.HSAW_EDATA  # cumulative weights decrease
 
 
+def test_upload_beside_the_check_rejects_bad_sources(ctx, gpu_lib, monkeypatch):
+    """The layout built beside the in_cum check (segments of sources, csrc/graph.cu) reports a bad
+    source row like the plain path does, with the reference's wording."""
+    from paper_1702_05854_b200 import rmat
+    monkeypatch.setenv("HSAW_UPLOAD_REGEN", "3")
+    monkeypatch.setenv("HSAW_UPLOAD_CHUNK_EDGES", "512")
+    g = rmat.rmat_graph(12, 10, seed=3, suspect_frac=0.02)
+    src = g.in_src.copy()
+    row = int(np.argmax(np.diff(g.in_offsets.astype(np.int64))))
+    src[int(g.in_offsets[row]) + 1] = g.n + 5
+    with pytest.raises(gpu_lib.HsawError) as e:
+        ctx.upload_graph(g.n, g.m, g.in_offsets, src, g.in_cum, g.p_of)
+    assert e.value.status == gpu_lib.HSAW_EDATA
+    assert "source id out of range" in str(e.value) and str(row) in str(e.value)
+    ctx.upload_graph(g.n, g.m, g.in_offsets, g.in_src, g.in_cum, g.p_of)  # the context is still usable
+    with ctx.stream(seed=1) as st:
+        st.ensure(100)
+
+
 # ---- fused recording path (K1 logs walks while generating them) ---------------------------------
 def test_fused_overflow_and_arena_exhaustion(ctx, port, monkeypatch):
     """Walks that outgrow their log chunk, and walks generated after the arena ran out, must be
