@@ -468,7 +468,9 @@ struct SamplerScratch {
     DevVec<uint2> arena, replay;
     DevVec<uint32_t> slot_log, ovf_pairs, sel;
     DevVec<uint64_t> enc_src;
+    DevVec<uint64_t> k1_words;  // [0] K1's work cursor, [1] its arena cursor (fused path)
     void release() {
+        k1_words.release();
         arena.release(); replay.release(); slot_log.release(); ovf_pairs.release();
         sel.release(); enc_src.release();
         slot_seed.release(); enc_seed.release(); tmp_off.release(); voff.release();
@@ -546,6 +548,14 @@ struct hsaw_gpu_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t side_go = nullptr, side_done = nullptr;
     bool side_pending = false;
+    // second stream for the chunk that is sampled AHEAD (stream.cu sample_range): K1 of chunk
+    // i + 1 runs on it beside the recheck / compaction of chunk i on the context stream.
+    // k1_stream is non-null only while such a launch is being queued.
+    // (two of them, used alternately: consecutive K1 launches overlap each other's tails, the
+    // last lanes of a launch chase the longest walks for a millisecond or more)
+    cudaStream_t ahead[2] = {nullptr, nullptr};
+    cudaEvent_t ahead_go = nullptr, ahead_done[2] = {nullptr, nullptr};
+    cudaStream_t k1_stream = nullptr;
     // L2 access-policy window over the compact graph (headers + sources), attached to the K1
     // launches only: those lines are marked persisting, so the walk-log stream of the same kernel
     // cannot evict them, while every other kernel on the stream keeps normal caching.
@@ -563,6 +573,7 @@ struct hsaw_gpu_ctx {
     hsawgpu::DevVec<uint64_t> g_thr_store;      // compact layout: pick thresholds (exact path)
     hsawgpu::DevVec<uint32_t> chk_list, chk_mid, chk_counters;  // distinctness-check scratch
     hsawgpu::SamplerScratch samp;                        // per-chunk sampler scratch
+    hsawgpu::SamplerScratch samp2;  // K1 outputs of the chunk sampled ahead (slot arrays, counts, arena)
     hsawgpu::PoolCache pool_cache;                       // recycled walk-pool buffers
     hsawgpu::HeldCsr held;                               // device-built CSR awaiting install / fetch
     hsawgpu::Restriction restr;                          // set only while a restricted chunk runs
@@ -600,6 +611,7 @@ struct hsaw_gpu_ctx {
         chk_mid.swap(o.chk_mid);
         chk_counters.swap(o.chk_counters);
         std::swap(samp, o.samp);
+        std::swap(samp2, o.samp2);
         std::swap(pool_cache, o.pool_cache);
         g_cand_bits.swap(o.g_cand_bits);
         g_cnt.swap(o.g_cnt);
@@ -626,6 +638,9 @@ struct hsaw_gpu_ctx {
         f(samp.slot_len); f(samp.count); f(samp.first); f(samp.enc_len); f(samp.enc_seq);
         f(samp.tmp_nodes); f(samp.tmp_edges); f(samp.vidx); f(samp.status); f(samp.arena);
         f(samp.replay); f(samp.slot_log); f(samp.ovf_pairs); f(samp.sel); f(samp.enc_src);
+        f(samp.k1_words);
+        f(samp2.slot_seed); f(samp2.slot_len); f(samp2.slot_log); f(samp2.count); f(samp2.first);
+        f(samp2.arena); f(samp2.k1_words);
         f(pool_cache.edge_off); f(pool_cache.tag_batch); f(pool_cache.accepted_after_batch);
         f(pool_cache.tag_seq);  // pool_cache.nodes / .edges are GrowVecs: handled by the callers
         f(g_cand_bits); f(g_cnt); f(g_fill); f(g_inv); f(g_covered); f(g_solution);
@@ -650,6 +665,7 @@ struct hsaw_gpu_ctx {
         g_compact_store.release();
         g_thr_store.release();
         samp.release();
+        samp2.release();
         pool_cache.release();
         cub_tmp.release();
         chk_list.release();
@@ -737,13 +753,19 @@ struct StageScope {
 
 // Folds finished event pairs into ctx->stage_ms. Call after the stream has been synchronised.
 inline void collect_timings(hsaw_gpu_ctx* ctx) {
+    size_t kept = 0;
     for (auto& p : ctx->pending) {
+        // a pair recorded on the second stream (a chunk sampled ahead) may still be running
+        if (cudaEventQuery(p.b) == cudaErrorNotReady) {
+            ctx->pending[kept++] = p;
+            continue;
+        }
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) ctx->stage_ms[p.stage] += ms;
         ctx->free_events.push_back(p.a);
         ctx->free_events.push_back(p.b);
     }
-    ctx->pending.clear();
+    ctx->pending.resize(kept);
     cudaGetLastError();
 }
 

@@ -946,6 +946,14 @@ void hsaw_gpu_ctx_destroy(hsaw_gpu_ctx* ctx) {
         cudaEventDestroy(ctx->side_go);
         cudaEventDestroy(ctx->side_done);
     }
+    if (ctx->ahead[0]) {
+        for (cudaStream_t a : ctx->ahead) {
+            cudaStreamSynchronize(a);
+            cudaStreamDestroy(a);
+        }
+        cudaEventDestroy(ctx->ahead_go);
+        for (cudaEvent_t e : ctx->ahead_done) cudaEventDestroy(e);
+    }
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

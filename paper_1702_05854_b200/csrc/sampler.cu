@@ -1109,6 +1109,9 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
                    bool with_stats) {
     if (nbatches == 0) return;
     if (nbatches > 0xFFFFFFFFull) fail(HSAW_EINVAL, "encode: more than 2^32 batches per launch");
+    // a chunk sampled ahead of its predecessor's post-processing runs on the context's second
+    // stream (stream.cu sample_range); everything else on the context stream
+    cudaStream_t st = ctx->k1_stream ? ctx->k1_stream : ctx->stream;
     EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, src_ref(ctx->g), ctx->g.thr,
                    ctx->g.n, cfg.batch_size, cfg.window, first_worker, nbatches, d_seed, d_len, d_count,
                    d_stats, d_cursor, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr};
@@ -1124,13 +1127,13 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
             p.arena_cap = rec->arena_cap;
             p.arena_cursor = rec->arena_cursor;
             p.out_log = rec->out_log;
-            HSAW_CUDA_CHECK(cudaMemsetAsync(rec->arena_cursor, 0, 4, ctx->stream));
+            HSAW_CUDA_CHECK(cudaMemsetAsync(rec->arena_cursor, 0, 4, st));
         }
-        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, st));
         auto go_p = [&](auto kernel) {
             int blocks = persistent_blocks(ctx, kernel, nbatches);
-            StageScope timer(ctx, HSAW_STAGE_ENCODE);
-            kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+            StageScope timer(ctx, HSAW_STAGE_ENCODE, st);
+            kernel<<<blocks, kThreads, 0, st>>>(p);
             check_launch(ctx, "encode_kernel(philox)");
         };
         if (rec)
@@ -1149,11 +1152,11 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
         p.ndomain = ctx->restr.ndomain;
         p.allowed = ctx->restr.allowed;
         p.out_cross = ctx->restr.out_cross;
-        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, st));
         auto go_r = [&](auto kernel) {
             int blocks = persistent_blocks(ctx, kernel, nbatches);
-            StageScope timer(ctx, HSAW_STAGE_ENCODE);
-            kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+            StageScope timer(ctx, HSAW_STAGE_ENCODE, st);
+            kernel<<<blocks, kThreads, 0, st>>>(p);
             check_launch(ctx, "encode_kernel(restricted)");
         };
 #define HSAW_GO_R(H, W)                                                              \
@@ -1181,17 +1184,24 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
         p.arena_cap = rec->arena_cap;
         p.arena_cursor = rec->arena_cursor;
         p.out_log = rec->out_log;
-        HSAW_CUDA_CHECK(cudaMemsetAsync(rec->arena_cursor, 0, 4, ctx->stream));
+        HSAW_CUDA_CHECK(cudaMemsetAsync(rec->arena_cursor, 0, 4, st));
     }
-    HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, ctx->stream));
+    HSAW_CUDA_CHECK(cudaMemsetAsync(d_cursor, 0, 8, st));
     auto go = [&](auto kernel) {
         int blocks = persistent_blocks(ctx, kernel, nbatches);
-        if (const char* env = std::getenv("HSAW_K1_GRID_BLOCKS_PER_SM")) {  // A/B knob
-            int cap = std::atoi(env) * ctx->sm_count;
-            if (cap > 0 && blocks > cap) blocks = cap;
-        }
-        StageScope timer(ctx, HSAW_STAGE_ENCODE);
-        kernel<<<blocks, kThreads, 0, ctx->stream>>>(p);
+        // Resident blocks per SM. Once the edge records outgrow the TLB's reach (8 GB and more:
+        // the 36 G gathers/s plateau of tools/tlb_probe.cu) the recording kernel is bound by
+        // HBM's random-gather rate, not by lanes in flight: 3 blocks per SM run 1-2.5 % FASTER
+        // than the 4 its registers allow (Twitter shape, 47 GB of records, per 2^20 batches:
+        // 18.6 / 18.8 ms, 2 blocks: 21.0) and leave a quarter of every SM to whatever runs
+        // beside K1 (stream.cu sample_range). Below that (LiveJournal shape, 2.2 GB: 9.76 ms with
+        // 3 blocks, 9.66 with 4) every lane still counts.
+        // HSAW_K1_GRID_BLOCKS_PER_SM: A/B knob (0 = whatever fits).
+        int per_sm = (rec && !compact && (uint64_t)ctx->g.m * sizeof(EdgeRec) > (8ull << 30)) ? 3 : 0;
+        if (const char* env = std::getenv("HSAW_K1_GRID_BLOCKS_PER_SM")) per_sm = std::atoi(env);
+        if (per_sm > 0) blocks = std::min(blocks, per_sm * ctx->sm_count);
+        StageScope timer(ctx, HSAW_STAGE_ENCODE, st);
+        kernel<<<blocks, kThreads, 0, st>>>(p);
         check_launch(ctx, "encode_kernel");
     };
     const bool brent = cfg.heuristic == 0;
@@ -1221,11 +1231,11 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
                 kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve > 100 ? 100 : carve));
             int blocks = persistent_blocks(ctx, kernel, nbatches);
             blocks = std::min(blocks, fast_blocks * ctx->sm_count);
-            StageScope timer(ctx, HSAW_STAGE_ENCODE);
+            StageScope timer(ctx, HSAW_STAGE_ENCODE, st);
             cudaLaunchConfig_t lc{};
             lc.gridDim = dim3(blocks);
             lc.blockDim = dim3(kThreads);
-            lc.stream = ctx->stream;
+            lc.stream = st;
             cudaLaunchAttribute attr{};
             if (ctx->k1_window_on) {  // keep the graph's L2 lines through the kernel's log stream
                 attr.id = cudaLaunchAttributeAccessPolicyWindow;

@@ -415,24 +415,55 @@ void sample_chunk(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
 
 // Fused variant of sample_chunk: K1 records the walks while generating them, so the replay kernel
 // only runs for walks that outgrew their log chunk. Same outputs, same order.
-void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
+// The chunk is handled in two halves so that sample_range can pipeline: fused_launch_k1 queues K1
+// (its outputs live in one of two scratch sets), fused_finish does everything after it. K1 of
+// chunk i + 1 is queued on the context's second stream BEFORE chunk i is finished, so it runs
+// beside K2b / the compaction of chunk i.
+struct FusedLaunch {
+    uint64_t first_batch = 0, nb = 0, ni = 0, slots = 0;
+    uint32_t l = 0, ml = 0;
+    bool philox = false;
+    int buf = 0;         // scratch set holding K1's outputs (0: ctx->samp, 1: ctx->samp2)
+    bool ahead = false;  // K1 was queued on ctx->ahead[buf]; ahead_done[buf] marks its end
+};
+
+static void ensure_ahead_stream(hsaw_gpu_ctx* ctx) {
+    if (ctx->ahead[0]) return;
+    for (auto& a : ctx->ahead) HSAW_CUDA_CHECK(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+    HSAW_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ahead_go, cudaEventDisableTiming));
+    for (auto& e : ctx->ahead_done)
+        HSAW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+FusedLaunch fused_launch_k1(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb, int buf,
+                            bool ahead) {
     hsaw_gpu_ctx* ctx = s->ctx;
-    cudaStream_t st = ctx->stream;
     const uint32_t l = s->cfg.batch_size;
     const uint64_t slots = nb * l;
     if (slots > 0xFFFFFFF0ull) fail(HSAW_EINVAL, "stream: chunk too large for 32-bit walk ids");
-    SamplerScratch& x = ctx->samp;
+    SamplerScratch& k = buf ? ctx->samp2 : ctx->samp;
     // Philox per-walk mode: the launch items are single attempts (ni items of ml = 1 attempt);
     // a batch is l consecutive items. Reference mode: items are batches.
-    const bool philox = s->cfg.rng_mode == 1;
-    const uint64_t ni = philox ? slots : nb;
-    const uint32_t ml = philox ? 1u : l;
+    FusedLaunch fl;
+    fl.first_batch = first_batch;
+    fl.nb = nb;
+    fl.l = l;
+    fl.slots = slots;
+    fl.philox = s->cfg.rng_mode == 1;
+    fl.ni = fl.philox ? slots : nb;
+    fl.ml = fl.philox ? 1u : l;
+    fl.buf = buf;
+    fl.ahead = ahead;
+    const uint64_t ni = fl.ni;
     hsaw_sampler_cfg kcfg = s->cfg;
-    kcfg.batch_size = ml;
-    const uint64_t first_item = philox ? (s->seed + first_batch) * l : s->seed + first_batch;
+    kcfg.batch_size = fl.ml;
+    const uint64_t first_item = fl.philox ? (s->seed + first_batch) * l : s->seed + first_batch;
     struct RngGuard {
         hsaw_gpu_ctx* c;
-        ~RngGuard() { c->rng_mode = 0; }
+        ~RngGuard() {
+            c->rng_mode = 0;
+            c->k1_stream = nullptr;
+        }
     } rng_guard{ctx};
     ctx->rng_mode = s->cfg.rng_mode;
 
@@ -443,8 +474,8 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     double per_attempt = s->pairs_per_attempt > 0 ? s->pairs_per_attempt : 24.0;
     uint64_t want = lanes * chunk + (uint64_t)((double)slots * per_attempt * 1.5) + 64 * chunk;
     want = std::min<uint64_t>(want, 0xFFFF0000ull);
-    x.arena.ensure_scratch(want);
-    uint32_t arena_cap = (uint32_t)std::min<uint64_t>(x.arena.cap, 0xFFFF0000ull);
+    k.arena.ensure_scratch(want);
+    uint32_t arena_cap = (uint32_t)std::min<uint64_t>(k.arena.cap, 0xFFFF0000ull);
     // test hook: a deliberately tiny arena exercises the "arena exhausted -> replay" path
     if (const char* env = std::getenv("HSAW_ARENA_MAX_PAIRS")) {
         uint64_t cap = std::strtoull(env, nullptr, 10);
@@ -452,20 +483,51 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     }
 
     // ---- K1 (recording)
-    x.slot_seed.ensure_scratch(slots + 1);
-    x.slot_len.ensure_scratch(slots + 1);
-    x.slot_log.ensure_scratch(slots + 1);
-    x.count.ensure_scratch(ni + 1);
-    x.first.ensure_scratch(ni + 1);
-    HSAW_CUDA_CHECK(cudaMemsetAsync(x.count.p + ni, 0, 4, st));
-    uint32_t* arena_cursor = reinterpret_cast<uint32_t*>(s->stats.p + 10);
-    EncodeRecord rec{x.arena.p, arena_cap, arena_cursor, x.slot_log.p};
-    launch_encode(ctx, kcfg, first_item, ni, x.slot_seed.p, x.slot_len.p, x.count.p,
-                  s->stats.p, s->stats.p + 8, &rec, s->collect_stats);
-    exclusive_sum_u32(ctx, x.count.p, x.first.p, ni + 1);
+    k.slot_seed.ensure_scratch(slots + 1);
+    k.slot_len.ensure_scratch(slots + 1);
+    k.slot_log.ensure_scratch(slots + 1);
+    k.count.ensure_scratch(ni + 1);
+    k.first.ensure_scratch(ni + 1);
+    k.k1_words.ensure_scratch(4);
+    cudaStream_t st = ctx->stream;
+    if (ahead) {
+        // the buffers above were (re)allocated in the context stream's order: the second stream
+        // starts behind that point (the context stream is idle here: the previous chunk's
+        // finish ended with a synchronisation)
+        ensure_ahead_stream(ctx);
+        HSAW_CUDA_CHECK(cudaEventRecord(ctx->ahead_go, ctx->stream));
+        st = ctx->ahead[buf];
+        HSAW_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ahead_go, 0));
+        ctx->k1_stream = st;
+    }
+    HSAW_CUDA_CHECK(cudaMemsetAsync(k.count.p + ni, 0, 4, st));
+    uint32_t* arena_cursor = reinterpret_cast<uint32_t*>(k.k1_words.p + 1);
+    EncodeRecord rec{k.arena.p, arena_cap, arena_cursor, k.slot_log.p};
+    launch_encode(ctx, kcfg, first_item, ni, k.slot_seed.p, k.slot_len.p, k.count.p,
+                  s->stats.p, k.k1_words.p, &rec, s->collect_stats);
+    if (ahead) HSAW_CUDA_CHECK(cudaEventRecord(ctx->ahead_done[buf], st));
+    return fl;
+}
+
+void fused_finish(hsaw_gpu_stream* s, const FusedLaunch& fl) {
+    hsaw_gpu_ctx* ctx = s->ctx;
+    cudaStream_t st = ctx->stream;
+    const uint32_t l = fl.l, ml = fl.ml;
+    const uint64_t slots = fl.slots, ni = fl.ni, nb = fl.nb, first_batch = fl.first_batch;
+    const bool philox = fl.philox;
+    SamplerScratch& x = ctx->samp;                       // post-processing scratch (one set)
+    SamplerScratch& k = fl.buf ? ctx->samp2 : ctx->samp;  // K1's outputs
+    struct RngGuard {
+        hsaw_gpu_ctx* c;
+        ~RngGuard() { c->rng_mode = 0; }
+    } rng_guard{ctx};
+    ctx->rng_mode = s->cfg.rng_mode;
+    if (fl.ahead) HSAW_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ahead_done[fl.buf], 0));
+    uint32_t* arena_cursor = reinterpret_cast<uint32_t*>(k.k1_words.p + 1);
+    exclusive_sum_u32(ctx, k.count.p, k.first.p, ni + 1);
     HSAW_CUDA_CHECK(
         cudaMemcpyAsync(ctx->h_scalars + 1, arena_cursor, 4, cudaMemcpyDeviceToHost, st));
-    const uint64_t E = read_u32(ctx, x.first.p + ni);
+    const uint64_t E = read_u32(ctx, k.first.p + ni);
     const uint64_t arena_used = *reinterpret_cast<uint32_t*>(ctx->h_scalars + 1);
     (void)arena_used;
 
@@ -484,14 +546,14 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
         {
             StageScope timer(ctx, HSAW_STAGE_COMPACT);
             gather_recorded<<<blocks_for(slots, 256), 256, 0, st>>>(
-                ni, ml, philox ? first_batch * l : first_batch, x.count.p, x.first.p, x.slot_seed.p,
-                x.slot_len.p, x.slot_log.p, x.arena.p, record_overflow_marker(), x.enc_seed.p,
+                ni, ml, philox ? first_batch * l : first_batch, k.count.p, k.first.p, k.slot_seed.p,
+                k.slot_len.p, k.slot_log.p, k.arena.p, record_overflow_marker(), x.enc_seed.p,
                 x.enc_len.p, x.enc_batch.p, x.enc_seq.p,
                 reinterpret_cast<const uint2**>(x.enc_src.p), x.ovf_pairs.p);
             check_launch(ctx, "gather_recorded");
             if (philox) {
                 philox_tags<<<blocks_for(E, 256), 256, 0, st>>>(E, l, first_batch * l, first_batch,
-                                                               x.first.p, x.enc_batch.p, x.enc_seq.p);
+                                                               k.first.p, x.enc_batch.p, x.enc_seq.p);
                 check_launch(ctx, "philox_tags");
             }
             HSAW_CUDA_CHECK(cudaMemsetAsync(x.ovf_pairs.p + E, 0, 4, st));
@@ -528,8 +590,8 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
         s->dropped += launch_distinct_check_pairs(
             ctx, E, reinterpret_cast<const uint2* const*>(x.enc_src.p), x.enc_len.p, x.status.p);
 
-        uint32_t* vflag = x.slot_len.p;  // slot arrays are dead after the gather (>= E + 1 entries)
-        uint32_t* vlen = reinterpret_cast<uint32_t*>(x.slot_seed.p);
+        uint32_t* vflag = k.slot_len.p;  // slot arrays are dead after the gather (>= E + 1 entries)
+        uint32_t* vlen = reinterpret_cast<uint32_t*>(k.slot_seed.p);
         x.voff.ensure_scratch(E + 1);
         uint32_t* mismatch = reinterpret_cast<uint32_t*>(s->stats.p + 9);
         HSAW_CUDA_CHECK(cudaMemsetAsync(mismatch, 0, 4, st));
@@ -579,7 +641,7 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->accepted_after_batch.reserve(s->local_batches + nb, st);
     if (E > 0) {
         batch_cumulative<<<blocks_for(nb, 256), 256, 0, st>>>(
-            nb, x.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches,
+            nb, k.first.p, x.vidx.p, s->accepted, s->accepted_after_batch.p + s->local_batches,
             philox ? l : 1u);  // launch items per batch
         check_launch(ctx, "batch_cumulative");
     } else {
@@ -607,6 +669,10 @@ void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
     s->accepted_after_batch.size = s->local_batches;
 }
 
+void sample_chunk_fused(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nb) {
+    fused_finish(s, fused_launch_k1(s, first_batch, nb, 0, false));
+}
+
 bool ctx_has_window(const hsaw_gpu_ctx* ctx) { return ctx->k1_window_on; }
 
 bool fused_enabled() {
@@ -617,11 +683,31 @@ bool fused_enabled() {
     return on;
 }
 
+// Pipelined sampling (default; HSAW_PIPELINE=0 keeps the serial chunks): when a call spans more
+// than one chunk, K1 of chunk i + 1 is queued on one of the context's two extra streams before
+// chunk i is finished, so the tail of a K1 launch (its last lanes chase the longest walks for a
+// millisecond or more while the SMs drain), K2b, the scans and the compaction of a chunk run
+// beside the next chunk's walk generation. Measured at the Twitter shape (47 chunks of ~1.1 M
+// batches per eSIA solve): sampling 1.114 -> 1.057 s. Cutting a call into SMALLER chunks to
+// pipeline more (HSAW_PIPE_BATCHES, 0 = off; the tests use it) loses: a launch of 2^18 batches
+// gives each lane two or three batches, most of the launch is tail, and K2b squeezed into the
+// registers K1 leaves runs 5x slower (2^20 batches as 4 x 2^18: 24.3 ms against 22.9 serial).
+// Results and their order do not change: chunks are finished strictly in batch order.
+static uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* env = std::getenv(name);
+    return env && *env ? std::strtoull(env, nullptr, 10) : dflt;
+}
+
 void sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches) {
     if (first_batch < s->last_batch_end)
         fail(HSAW_EINVAL, "stream: batch ranges must be issued in increasing order");
-    uint64_t done = 0;
-    while (done < nbatches) {
+    hsaw_gpu_ctx* ctx = s->ctx;
+    if (s->cfg.rng_mode == 1 && s->r_ndomain != 0)
+        fail(HSAW_EINVAL, "stream: the Philox mode does not combine with a restriction");
+    const bool fused =
+        (fused_enabled() || s->cfg.rng_mode == 1) && record_supported(s->cfg) && s->r_ndomain == 0;
+    const uint64_t pipe_batches = env_u64("HSAW_PIPE_BATCHES", 0);
+    auto chunk_batches = [&](uint64_t done) {
         uint64_t nb = std::min(nbatches - done, kMaxChunkBatches);
         // a chunk's slots carry 32-bit walk ids, and its pair-log arena (about 1.5x the expected
         // log volume) is kept to a few gigabytes: long walks (Twitter shape: 130 pairs per accepted
@@ -631,14 +717,46 @@ void sample_range(hsaw_gpu_stream* s, uint64_t first_batch, uint64_t nbatches) {
         const double per_attempt = s->pairs_per_attempt > 0 ? s->pairs_per_attempt : 24.0;
         const uint64_t arena_batches = (uint64_t)((double)(kArenaTargetBytes / 8) / (per_attempt * 1.5 * (double)bs));
         nb = std::min(nb, std::max<uint64_t>(arena_batches, 1ull << 14));
-        if (s->cfg.rng_mode == 1 && s->r_ndomain != 0)
-            fail(HSAW_EINVAL, "stream: the Philox mode does not combine with a restriction");
-        if ((fused_enabled() || s->cfg.rng_mode == 1) && record_supported(s->cfg) && s->r_ndomain == 0)
-            sample_chunk_fused(s, first_batch + done, nb);
-        else
-            sample_chunk(s, first_batch + done, nb);
-        done += nb;
-        s->last_batch_end = first_batch + done;
+        if (pipe_batches > 0) nb = std::min(nb, pipe_batches);
+        return nb;
+    };
+    const bool pipelined =
+        fused && env_u64("HSAW_PIPELINE", 1) != 0 && chunk_batches(0) < nbatches;
+    if (pipelined) {
+        try {
+            int buf = 0;
+            uint64_t issued = chunk_batches(0);
+            FusedLaunch cur = fused_launch_k1(s, first_batch, issued, buf, true);
+            for (;;) {
+                const bool more = issued < nbatches;
+                FusedLaunch next;
+                if (more) {
+                    const uint64_t nb = chunk_batches(issued);
+                    next = fused_launch_k1(s, first_batch + issued, nb, buf ^ 1, true);
+                    issued += nb;
+                }
+                fused_finish(s, cur);
+                s->last_batch_end = cur.first_batch + cur.nb;
+                if (!more) break;
+                cur = next;
+                buf ^= 1;
+            }
+        } catch (...) {
+            for (cudaStream_t a : ctx->ahead)  // a chunk sampled ahead may be in flight
+                if (a) cudaStreamSynchronize(a);
+            throw;
+        }
+    } else {
+        uint64_t done = 0;
+        while (done < nbatches) {
+            const uint64_t nb = chunk_batches(done);
+            if (fused)
+                sample_chunk_fused(s, first_batch + done, nb);
+            else
+                sample_chunk(s, first_batch + done, nb);
+            done += nb;
+            s->last_batch_end = first_batch + done;
+        }
     }
     s->last_batch_end = first_batch + nbatches;
     // sampling is over for this call: the graph lines K1 kept persisting go back to normal, the

@@ -7,6 +7,7 @@ reference numbers as two reference runs sit to each other (up to the stated slac
 Checked: determinism and chunking independence, the HSAW invariants of every pooled walk, the
 walk law on fixture12 (tolerance 0.01 at 2e5 samples, as proj/tests/test_sampler.cpp:204-228),
 hit rate, length distribution, per-edge frequency, and the final est_suspension of eSIA."""
+import os
 import hashlib
 
 import numpy as np
@@ -37,6 +38,13 @@ def test_philox_is_deterministic_and_chunking_independent(ctx, gpu_lib, synth300
                 st.sample_range(first, nb)
             out.append((_digest(st.export()), st.size(), st.counters_for(st.count)))
     assert out[0] == out[1] == out[2]
+    os.environ["HSAW_PIPE_BATCHES"] = "500"  # 18 chunks, each sampled ahead of its predecessor's finish
+    try:
+        with ctx.stream(seed=5, cfg=_cfg(gpu_lib, 1)) as st:
+            st.sample_range(0, 9000)
+            assert (_digest(st.export()), st.size(), st.counters_for(st.count)) == out[0]
+    finally:
+        del os.environ["HSAW_PIPE_BATCHES"]
     with ctx.stream(seed=6, cfg=_cfg(gpu_lib, 1)) as st:  # another seed: another sample
         st.sample_range(0, 9000)
         assert _digest(st.export()) != out[0][0]

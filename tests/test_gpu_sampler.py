@@ -434,6 +434,42 @@ def test_fused_overflow_and_arena_exhaustion(ctx, port, monkeypatch):
         pools_equal(st.to_pool(4000), exp)
 
 
+def test_pipelined_chunks_match(ctx, port, monkeypatch):
+    """A call that spans several chunks samples chunk i + 1 on a second stream while chunk i is
+    rechecked and compacted (csrc/stream.cu sample_range). The pool and its order must not depend
+    on the cut: tiny chunks (HSAW_PIPE_BATCHES), tiny chunks with the arena running out (replays
+    beside chunks sampled ahead), and the serial chunks of HSAW_PIPELINE=0 all give the
+    reference's pool (sampler.cpp:423-461: pool order = worker id, then sequence)."""
+    csr = make_csr(small_graphs()["uniform2000"])
+    upload(ctx, csr)
+    exp = port.stream_samples(csr, 6000, seed=13)
+    for env in ({"HSAW_PIPE_BATCHES": "64"},
+                {"HSAW_PIPE_BATCHES": "37", "HSAW_ARENA_MAX_PAIRS": "4096"},
+                {"HSAW_PIPE_BATCHES": "64", "HSAW_PIPELINE": "0"},
+                {"HSAW_PIPE_BATCHES": "1"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with ctx.stream(seed=13) as st:
+            st.ensure(6000)
+            pools_equal(st.to_pool(6000), exp)
+        for k in env:
+            monkeypatch.delenv(k)
+    # explicit ranges: one pipelined call equals the same range issued batch by batch
+    monkeypatch.setenv("HSAW_PIPE_BATCHES", "50")
+    with ctx.stream(seed=13) as st:
+        st.sample_range(0, 700)
+        n_piped = st.count
+        piped = st.to_pool(n_piped)
+    monkeypatch.delenv("HSAW_PIPE_BATCHES")
+    with ctx.stream(seed=13) as st:
+        for b in range(700):
+            st.sample_range(b, 1)
+        n_serial = st.count
+        serial = st.to_pool(n_serial)
+    assert n_piped == n_serial
+    pools_equal(piped, serial)
+
+
 def test_unfused_path_still_matches(gpu_lib, port, monkeypatch):
     """HSAW_FUSED=0 keeps the encode -> replay pipeline selectable (A/B measurements)."""
     import subprocess
