@@ -824,7 +824,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeParams p) {
 // Verdict to reproduce (sampler.cpp:318-337): the walk is dropped iff its replayed nodes are not
 // pairwise distinct. One warp per walk; <= 32 nodes: one __match_any_sync; <= kSmemNodes: an
 // open-addressing hash set in shared memory; longer walks are queued for distinct_long_kernel.
-// Two table sizes: the main pass keeps 56 warps per SM resident with 4 KB tables (walks of up to
+// Two table sizes: the main pass keeps 48 warps per SM resident (six blocks: launch_distinct_check) with 4 KB tables (walks of up to
 // 512 nodes); the few longer walks are queued for a second pass with 16 KB tables, and walks beyond
 // that for the block-per-walk kernel.
 #ifndef HSAW_K2B_LOAD
@@ -836,6 +836,7 @@ constexpr uint32_t kTableLoad = HSAW_K2B_LOAD;  // slots per node before roundin
 #endif
 constexpr bool kBitmapProof = HSAW_K2B_BITMAP != 0;  // compile-time A/B of the bit-map fast path
 constexpr int kCheckWarps = 8, kMidWarps = 4;
+constexpr int kCheckMinBlocks = 6;  // register budget of the main pass (blocks per SM), see launch_distinct_check
 constexpr uint32_t kTableSize = 1024, kMidTableSize = 4096;  // u32 slots per warp
 constexpr uint32_t kSmemNodes = kMidTableSize / 2;           // largest walk handled in shared memory
 
@@ -873,8 +874,10 @@ __device__ __forceinline__ uint32_t walk_node(const CheckParams& p, uint64_t w, 
 // costs one exposed memory latency per 128 nodes instead of one per 32.
 // GROUP: walks dealt to a warp at a time (32 for the bulk pass; 1 for the short queues of long
 // walks, where 32 serial long walks per warp would leave most of the GPU idle).
-template <bool PAIRS, uint32_t TABLE, int WARPS, uint32_t GROUP>
-__global__ void __launch_bounds__(WARPS * 32) distinct_kernel(CheckParams p) {
+// MINB: resident blocks per SM the register budget is held to (the main pass: 6 x 32 KB of tables
+// fill the shared memory of an SM; without the bound the kernel takes 52 registers, four blocks).
+template <bool PAIRS, uint32_t TABLE, int WARPS, uint32_t GROUP, int MINB = 1>
+__global__ void __launch_bounds__(WARPS * 32, MINB) distinct_kernel(CheckParams p) {
     extern __shared__ __align__(16) uint32_t tables[];  // WARPS x TABLE
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
@@ -1417,7 +1420,6 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     CheckParams p{nwalks,   d_edge_off,      d_nodes,  d_nnodes, d_pair_src,      d_lens,
                   d_status, ctx->chk_list.p, counters, long_cap, ctx->chk_mid.p, mid_cap,
                   nullptr};
-    auto main_kernel = distinct_kernel<PAIRS, kTableSize, kCheckWarps, 32>;
     auto mid_kernel = distinct_kernel<PAIRS, kMidTableSize, kMidWarps, 1>;
     const int smem_main = kCheckWarps * kTableSize * 4, smem_mid = kMidWarps * kMidTableSize * 4;
     static bool attr_set = false;
@@ -1428,12 +1430,39 @@ static uint32_t distinct_check_impl(hsaw_gpu_ctx* ctx, uint64_t nwalks,
     }
     uint32_t* h = reinterpret_cast<uint32_t*>(ctx->h_scalars + 32);
     {
-        uint64_t want = ((nwalks + 31) / 32 + kCheckWarps - 1) / kCheckWarps;  // 32 walks per warp
-        uint64_t full = (uint64_t)ctx->sm_count * 7;  // 32 KB of tables per block: 7 blocks / SM
-        int blocks = (int)(want < full ? want : full);
-        StageScope timer(ctx, HSAW_STAGE_DISTINCT);
-        main_kernel<<<blocks, kCheckWarps * 32, smem_main, ctx->stream>>>(p);
-        check_launch(ctx, "distinct_kernel");
+        // Register budget and grid of the main pass (C4, ms per 2^20-batch step; until the end of
+        // round 2 it ran with 52 registers = 4 resident blocks and a grid of 7 per SM: 1.88). Six
+        // blocks per SM (40 registers, 40 bytes of spills; 6 x 32 KB of tables fill the shared
+        // memory) with a grid of eight waves: 1.63. The waves matter as much as the occupancy:
+        // walks differ in length by orders of magnitude, a single resident wave with a static
+        // stride leaves SMs idle behind the slowest warps (2.53 with 4 blocks, 2.15 with 6),
+        // later blocks fill the gaps. HSAW_K2B_MINB (1 / 5 / 6), HSAW_K2B_GRID_PER_SM: A/B knobs.
+        static const int minb = [] {
+            const char* env = std::getenv("HSAW_K2B_MINB");
+            return env ? std::atoi(env) : kCheckMinBlocks;
+        }();
+        auto go = [&](auto main_kernel) {
+            HSAW_CUDA_CHECK(cudaFuncSetAttribute(main_kernel,
+                                                 cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                 cudaSharedmemCarveoutMaxShared));
+            int per_sm = 0;
+            HSAW_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, main_kernel, kCheckWarps * 32, smem_main));
+            per_sm = std::max(per_sm, 1) * 8;
+            if (const char* env = std::getenv("HSAW_K2B_GRID_PER_SM")) per_sm = std::max(1, std::atoi(env));
+            uint64_t want = ((nwalks + 31) / 32 + kCheckWarps - 1) / kCheckWarps;  // 32 walks per warp
+            uint64_t full = (uint64_t)ctx->sm_count * per_sm;
+            int blocks = (int)(want < full ? want : full);
+            StageScope timer(ctx, HSAW_STAGE_DISTINCT);
+            main_kernel<<<blocks, kCheckWarps * 32, smem_main, ctx->stream>>>(p);
+            check_launch(ctx, "distinct_kernel");
+        };
+        if (minb >= 6)
+            go(distinct_kernel<PAIRS, kTableSize, kCheckWarps, 32, 6>);
+        else if (minb == 5)
+            go(distinct_kernel<PAIRS, kTableSize, kCheckWarps, 32, 5>);
+        else
+            go(distinct_kernel<PAIRS, kTableSize, kCheckWarps, 32, 1>);
     }
     HSAW_CUDA_CHECK(cudaMemcpyAsync(h, counters, 16, cudaMemcpyDeviceToHost, ctx->stream));
     HSAW_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
