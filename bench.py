@@ -802,25 +802,6 @@ def run_b200(args):
         }
         if e2e_error:
             out["e2e"]["error"] = e2e_error
-        else:
-            # the same call at other request sizes (one call each): the upload is a fixed cost per
-            # call, so end-to-end HSAWs/s grows with the request (BASELINE.md plans a sweep over
-            # 10^6..10^8 samples; the largest size is bounded by what the pool may take beside a
-            # second copy of nothing: 8 B per walk item with both item arrays kept)
-            sweep = {}
-            for tgt in (10**6, 10**7, 3 * 10**7):
-                try:
-                    barrier()
-                    t0 = time.perf_counter()
-                    with hostapi.DeviceGraph(g, vi, device=local) as dg2:
-                        _, acc = dg2.sample(tgt, seed=STREAM_SEED + 7, max_attempts=10**15)
-                    torch.cuda.synchronize()
-                    dt = time.perf_counter() - t0
-                    sweep[str(tgt)] = {"hsaw_per_sec": acc / dt, "seconds": dt, "accepted": acc}
-                except Exception as exc:
-                    sweep[str(tgt)] = {"error": str(exc)[:120]}
-                    break
-            out["e2e"]["request_size_sweep"] = sweep
         # host ProbGraph in, InterdictionResult out (context creation, upload and solve inside)
         if r_dev is not None:
             try:
@@ -838,6 +819,35 @@ def run_b200(args):
                 })
             except Exception as exc:
                 out[args.solver]["e2e_error"] = str(exc)[:300]
+        # (after the host-array solve: that one finds the walk pool of the device-resident solve
+        # parked on the device, as a second call of a long-lived service would)
+        if not e2e_error:
+            # the same call at other request sizes (two calls each, the second reported): the upload is a fixed cost per
+            # call, so end-to-end HSAWs/s grows with the request (BASELINE.md plans a sweep over
+            # 10^6..10^8 samples; the largest size is bounded by what the pool may take beside a
+            # second copy of nothing: 8 B per walk item with both item arrays kept)
+            sweep = {}
+            for tgt in (10**6, 10**7, 3 * 10**7):
+                try:
+                    # two calls per size, the second is reported: the first call at a new size
+                    # pays for device allocations (walk pool, pair-log arenas) that later calls
+                    # find parked on the device (0.1-0.3 s at these sizes, whichever call needs
+                    # them first)
+                    secs = []
+                    for _ in range(2):
+                        barrier()
+                        t0 = time.perf_counter()
+                        with hostapi.DeviceGraph(g, vi, device=local) as dg2:
+                            _, acc = dg2.sample(tgt, seed=STREAM_SEED + 7, max_attempts=10**15)
+                        torch.cuda.synchronize()
+                        secs.append(time.perf_counter() - t0)
+                    dt = secs[-1]
+                    sweep[str(tgt)] = {"hsaw_per_sec": acc / dt, "seconds": dt, "accepted": acc,
+                                       "first_call_seconds": secs[0]}
+                except Exception as exc:
+                    sweep[str(tgt)] = {"error": str(exc)[:120]}
+                    break
+            out["e2e"]["request_size_sweep"] = sweep
     elif world > 1 or args.no_e2e:
         out["e2e"] = None
     else:
