@@ -44,6 +44,7 @@ struct EncodeParams {
     uint32_t arena_cap;      // pairs
     uint32_t* arena_cursor;  // next free chunk (pairs)
     uint32_t* out_log;       // per (batch, seq) slot: first pair of the walk, or kLogOverflow
+    uint32_t grow_mode;      // experiment, see grow_log (0 = off)
     // restricted variant (RESTR): start nodes drawn from `domain`, walks that move onto a node
     // outside `allowed` are aborted and counted per batch (sampler.cpp:24-31,196-199,528)
     const uint32_t* domain;
@@ -177,6 +178,31 @@ static __device__ __noinline__ uint32_t tortoise_step(const NodeRec* __restrict_
 // REC: 0 plain encode, 1 record walks (default stores), 2 record with streaming (.cs) stores.
 // STATS: per-lane work counters (draws, picks, algorithmic bytes) for instrumentation runs.
 // LAYOUT: kLayoutFat (32-byte edge records) or kLayoutCompact (in_src + 8-byte row headers).
+// Opt-in (HSAW_LOG_GROW=1; off by default, measured at the very end of round 2): a walk that fills
+// its log chunk moves to a fresh run of chunks twice its length instead of being replayed by K2 -
+// the pairs logged so far ([from, from + have): whole staged lines, all flushed) are copied by the
+// lane itself with plain 8-byte volatile accesses and the walk goes on recording there; when the
+// arena has no room the walk is replayed as before. At C4 this removes the replay (~80 walks per
+// 2^20 batches, 1.5 ms of single-lane latency beside K2b's main pass): 22.07 -> 21.94 ms per step
+// with a first version whose vectorised copy (ld.global.cg.v4 + the st.global.cs.v4.u64 asm of
+// store_sector) turned out to lose the copied prefix when many lanes of a warp moved at once
+// (ring tests); this plain copy passes them (tests/test_gpu_sampler.py::test_log_growth_opt_in).
+__device__ __noinline__ uint32_t grow_log(uint2* arena, uint32_t* cursor, uint32_t cap,
+                                          uint32_t from, uint32_t have, uint32_t need) {
+    const uint32_t base = atomicAdd(cursor, need);
+    if ((uint64_t)base + need > cap) return kLogOverflow;
+    volatile unsigned long long* src = reinterpret_cast<volatile unsigned long long*>(arena + from);
+    volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(arena + base);
+    for (uint32_t i = 0; i < have; i += 8) {  // `have` is a multiple of kStage; 8 loads in flight
+        unsigned long long t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = src[i + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[i + q] = t[q];
+    }
+    return base;
+}
+
 template <int HEUR, int WIN, int MINB, int REC, bool STATS, int LAYOUT, bool RESTR = false,
           class RNG = XorRng>
 __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) {
@@ -198,8 +224,19 @@ __global__ void __launch_bounds__(kThreads, MINB) encode_kernel(EncodeParams p) 
     auto log_pair = [&](uint32_t node, uint32_t edge) {
         if (!REC || !rec_ok) return;
         if (lpos == lend) {  // the walk outgrew its chunk: it will be replayed instead
-            rec_ok = false;
-            return;
+            const uint32_t have = lpos - astart;
+            const uint32_t need = (2 * have + kLogChunk - 1) / kLogChunk * kLogChunk;
+            const uint32_t moved = (arena_dead || p.grow_mode == 0)
+                                       ? kLogOverflow
+                                       : grow_log(p.arena, p.arena_cursor, p.arena_cap, astart, have, need);
+            if (moved == kLogOverflow) {
+                rec_ok = false;
+                arena_dead = arena_dead || p.grow_mode != 0;
+                return;
+            }
+            astart = moved;
+            lpos = moved + have;
+            lend = moved + need;
         }
         stage[lpos & (kStage - 1)][threadIdx.x] = make_uint2(node, edge);
         if ((lpos & (kStage - 1)) == kStage - 1) flush(lpos & ~(kStage - 1), kStage / 4);
@@ -1117,7 +1154,8 @@ void launch_encode(hsaw_gpu_ctx* ctx, const hsaw_sampler_cfg& cfg, uint64_t firs
     cudaStream_t st = ctx->k1_stream ? ctx->k1_stream : ctx->stream;
     EncodeParams p{ctx->g.nodes, ctx->g.edges, ctx->g.hdr, src_ref(ctx->g), ctx->g.thr,
                    ctx->g.n, cfg.batch_size, cfg.window, first_worker, nbatches, d_seed, d_len, d_count,
-                   d_stats, d_cursor, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr};
+                   d_stats, d_cursor, nullptr, 0, nullptr, nullptr, 0, nullptr, 0, nullptr, nullptr};
+    if (const char* env = std::getenv("HSAW_LOG_GROW")) p.grow_mode = (uint32_t)std::atoi(env);
     const bool compact = ctx->g.layout == kLayoutCompact;
     if (cfg.rng_mode == 1) {
         // Philox per-walk mode: the caller passes one work item per ATTEMPT (batch_size 1), so a

@@ -3,6 +3,8 @@ Bar: bit-exact with the oracle — same (seed, len) per batch, same decoded node
 order, tags, attempts. Mirrors proj/tests/test_sampler.cpp."""
 import hashlib
 
+import os
+
 import numpy as np
 import pytest
 
@@ -263,6 +265,32 @@ def test_long_walk_distinct_check(ctx, port):
     assert got.attempts == exp.attempts and got.nsamples == exp.nsamples
     assert np.array_equal(got.nodes, exp.nodes) and np.array_equal(got.edges, exp.edges)
     assert int(np.diff(exp.edge_off.astype(np.int64)).max()) > 2048
+
+
+def test_log_growth_opt_in(ctx, port, monkeypatch):
+    """HSAW_LOG_GROW=1 (csrc/sampler.cu grow_log, the generic K1 = the fat layout's production
+    kernel): walks that outgrow their 4096-pair log chunk move to a larger run of chunks while
+    they are recorded - several times on a ring of 20000 nodes - instead of being replayed by K2.
+    Same pool as the oracle; on the fat layout nothing is replayed."""
+    from oracle.oracle import Csr
+    n = 20000
+    off = np.arange(n + 1, dtype=np.uint64)
+    src = ((np.arange(n) + 1) % n).astype(np.uint32)
+    p = np.zeros(n)
+    p[0] = 1.0
+    csr = Csr(n, n, off, src, np.ones(n), p)
+    upload(ctx, csr)
+    exp = port.stream_samples(csr, 60, seed=9)
+    assert int(np.diff(exp.edge_off.astype(np.int64)).max()) > 16384
+    monkeypatch.setenv("HSAW_LOG_GROW", "1")
+    monkeypatch.setenv("HSAW_PIPE_BATCHES", "8")  # small calls: the arena does not run out
+    with ctx.stream(seed=9, cfg=None) as st:
+        for b in range(0, 64, 8):
+            st.sample_range(b, 8)
+        pools_equal(st.to_pool(60), exp)
+        replayed = st.stats()["spare"]
+    if os.environ.get("HSAW_LAYOUT") == "fat":
+        assert replayed == 0
 
 
 # ---- stream -------------------------------------------------------------------------------------
